@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path; prints ONE JSON line on rank 0.
+
+Main line: least-model fixpoint of configuration C4 (10M atoms, 50M rules, ~150M
+nonzeros; BASELINE.json configs[3], the configuration the roofline target is quoted on)
+with the full fused θ-pass kernel (Algorithm 1), v0 = facts.  A step = one whole
+fixpoint (init + all θ-passes until no change + model extraction) through the C ABI,
+inputs resident in HBM.  value = nnz · iters / step time, summed over ranks.
+
+Also measured (extra keys): the frontier variant on C4, the batched stable-model search
+on C5 (guesses/s), the end-to-end call with host buffers (e2e), the per-launch roofline
+of the dominant kernel and the CPU oracle baseline (cpu_baseline).
+
+--impl reference times the CPU oracle (oracle/, as it stands) on the same workload and
+metric: each step is a bounded sample (one Jacobi T_P pass over all of C4's rules).
+
+Multi-GPU (torchrun, N > 1): "replicas only" -- every rank solves its own copy of the
+workload (the least-model fixpoint has no partition without a per-pass exchange; see
+DESIGN.md), timing is the max over ranks, value the sum of units over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("least-model fixpoint time & nnz·iter/s (HBM GB/s vs peak); "
+          "stable-model guesses/s")
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, util, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+                util.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm), "samples_under_load": len([u for u in util if u > 0])}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, bounded sample per step."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import lpgen
+    import oracle
+    oracle.build()
+    P = lpgen.config(args.workload)
+    nnz = int(P.nnz) + int((np.diff(P.body_ptr) == 0).sum())
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        _, it, _, _ = oracle.lm_jacobi(P, max_iters=1)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = float(np.mean(times))
+    v = nnz * 1 / t
+    sample = f"one Jacobi T_P pass over all {P.n_rules} rules of {args.workload} per step"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "nnz*iter/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": args.workload, "variant": "oracle O-LM Jacobi (oracle/lp_oracle.c)"},
+        "cpu_baseline": {"value": v, "unit": "nnz*iter/s", "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "nnz*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C4")
+    ap.add_argument("--stable-workload", default="C5")
+    ap.add_argument("--no-extras", action="store_true", help="main line only (for ncu)")
+    ap.add_argument("--cpu-sample-passes", type=int, default=1)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    import lpgen
+    from paper_2009_10247_b200 import lp
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.Stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+
+    def flush_l2():
+        with torch.cuda.stream(stream):
+            flush.fill_(rank + 1)
+
+    # ---- load the workload (not timed: lp_load is the one-time upload) --------------
+    t0 = time.perf_counter()
+    P = lpgen.config(args.workload)
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    prog = lp.Program(P, device=local)
+    torch.cuda.synchronize()
+    t_load = time.perf_counter() - t0
+    info = prog.info
+    n = P.n_atoms
+    Wm = lp.bits_words(n)
+    nfacts = int((np.diff(P.body_ptr) == 0).sum())
+    launches_per_call = 3 + (1 if nfacts else 0) + 1
+
+    model = torch.zeros(Wm, dtype=torch.int64, device="cuda")
+    iters_d = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+    def timed_least_model(frontier, steps, warmup):
+        tot, ker = [], []
+        for i in range(warmup + steps):
+            flush_l2()
+            e0, e1, k0, k1 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e0.record(stream)
+            lp.lp_least_model(prog, None, model, frontier=frontier, stream=stream, device_ptrs=True,
+                              iters_out=iters_d, ev_begin=k0, ev_end=k1)
+            e1.record(stream)
+            stream.synchronize()
+            if i >= warmup:
+                tot.append(e0.elapsed_time(e1))
+                ker.append(k0.elapsed_time(k1))
+        return float(np.mean(tot)), float(np.mean(ker)), int(iters_d.item())
+
+    # ---- main line: full θ-pass fixpoint ---------------------------------------------
+    clocks = ClockSampler(local)
+    timed_least_model(False, 0, args.warmup)            # warm-up
+    barrier()
+    clocks.start()
+    ms, kms, iters = timed_least_model(False, args.steps, 0)
+    barrier()
+    clk = clocks.stop()
+    ms_max = allmax(ms)
+    kms_max = allmax(kms)
+    nnz = int(info["nnz"])
+    value = ws * nnz * iters / (ms_max / 1e3)
+
+    hbm_peak, peak_src = _peaks()
+    pass_bytes = int(info["pass_bytes"])
+    achieved = pass_bytes * iters / (kms_max / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                "kernel": "lm_full_kernel<false> (persistent, all passes in one launch)",
+                "bytes_per_pass": pass_bytes, "passes_per_launch": iters,
+                "kernel_ms": kms_max}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "nnz*iter/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": args.workload, "n_atoms": n, "n_rules": int(info["n_rules"]),
+                   "nnz": nnz, "iters": iters, "variant": "full fused θ-pass (Algorithm 1)",
+                   "v0": "facts only", "l2": "flushed between steps (256 MiB write)",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "truth_mode": "summary-in-smem" if info["truth_mode"] else "exact-in-smem",
+                   "grid": [int(info["grid_blocks"]), int(info["block_threads"])]},
+        "fixpoint_ms": ms_max, "kernel_ms": kms_max,
+        "gpu_launches": launches_per_call * args.steps,
+        "roofline": roofline, "clocks": clk,
+        "load": {"generate_s": t_gen, "lp_load_s": t_load, "device_bytes": int(info["device_bytes"])},
+    }
+
+    # ---- e2e: the C-ABI call with host (pinned) buffers -------------------------------
+    v0_host = torch.zeros(Wm, dtype=torch.int64).pin_memory()
+    model_host = torch.zeros(Wm, dtype=torch.int64).pin_memory()
+    facts = P.head[np.diff(P.body_ptr) == 0]
+    v0_np = lp.pack_mask(np.isin(np.arange(n), facts))
+    v0_host.numpy().view(np.uint64)[:] = v0_np[:Wm]
+    e2e_t = []
+    for i in range(args.warmup + args.steps):
+        flush_l2()
+        stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        it = lp.lp_least_model(prog, v0_host, model_host, stream=stream)
+        e1.record(stream)
+        e1.synchronize()
+        if i >= args.warmup:
+            e2e_t.append(e0.elapsed_time(e1))
+        assert it == iters
+    e2e_ms = allmax(float(np.mean(e2e_t)))
+    out["e2e"] = {"value": ws * nnz * iters / (e2e_ms / 1e3), "unit": "nnz*iter/s",
+                  "h2d_bytes_per_step": Wm * 8, "d2h_bytes_per_step": Wm * 8 + 12,
+                  "ms_per_step": e2e_ms, "api": "lp_least_model (host pointers, synchronous)"}
+
+    if not args.no_extras:
+        # ---- frontier variant on the same workload --------------------------------------
+        fms, fkms, fit = timed_least_model(True, args.steps, args.warmup)
+        assert fit == iters
+        out["frontier"] = {"ms_per_step": allmax(fms), "kernel_ms": allmax(fkms), "iters": fit,
+                           "speedup_vs_full": ms_max / allmax(fms)}
+        # ---- stable models ---------------------------------------------------------------
+        S = lpgen.config(args.stable_workload)
+        sprog = lp.Program(S, device=local)
+        G = 1 << sprog.info["n_free_negated"]
+        W = (G + 63) // 64
+        acc = torch.zeros(W, dtype=torch.int64, device="cuda")
+        nacc = torch.zeros(1, dtype=torch.int64, device="cuda")
+        passes = torch.zeros(1, dtype=torch.int32, device="cuda")
+        st_t, st_k = [], []
+        for i in range(args.warmup + args.steps):
+            flush_l2()
+            e0, e1, k0, k1 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e0.record(stream)
+            lp.lp_stable_models(sprog, None, G, acc, stream=stream, device_ptrs=True,
+                                n_accepted_out=nacc, passes_out=passes, ev_begin=k0, ev_end=k1)
+            e1.record(stream)
+            stream.synchronize()
+            if i >= args.warmup:
+                st_t.append(e0.elapsed_time(e1))
+                st_k.append(k0.elapsed_time(k1))
+        sms = allmax(float(np.mean(st_t)))
+        out["stable"] = {"workload": args.stable_workload, "guesses": G,
+                         "guesses_per_s": ws * G / (sms / 1e3), "ms_per_step": sms,
+                         "kernel_ms": allmax(float(np.mean(st_k))), "passes": int(passes.item()),
+                         "accepted": int(nacc.item()), "n_negated": sprog.info["n_negated"],
+                         "l2": "flushed between steps"}
+        sprog.close()
+
+    # ---- CPU baseline: the oracle as it stands, rank 0, N = 1 only ----------------------
+    if rank == 0 and ws == 1:
+        import oracle
+        oracle.build()
+        t0 = time.perf_counter()
+        _, it_cpu, _, conv = oracle.lm_jacobi(P, max_iters=args.cpu_sample_passes)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": nnz * it_cpu / dt, "unit": "nnz*iter/s", "cores": 1,
+                               "kind": "oracle",
+                               "sample": f"{it_cpu} Jacobi T_P pass(es) of O-LM over all of "
+                                         f"{args.workload} ({dt:.1f} s, single thread)"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,186 @@
+/*
+ * lp.h -- C ABI of the B200 (sm_100a) least-model / stable-model engine
+ * (paper_2009_10247_b200/liblp_b200.so).
+ *
+ * The method (arXiv 2009.10247, PAPER.md = its LaTeX source):
+ *   - least model of a definite program = fixpoint of the immediate-consequence
+ *     operator T_P iterated from the initial vector, computed as the thresholded
+ *     sparse mat-vec v_{k+1} = θ(M_P v_k)   (Algorithm 1, PAPER.md:152-173;
+ *     T_P PAPER.md:70-72; θ Def. 5; M_P Def. 2);
+ *   - stable models of a normal program = the same iteration batched over an initial
+ *     matrix of guesses on the negated atoms, followed by a complementarity check
+ *     (Algorithms 2-3; positive form Eq. 4 PAPER.md:188-194;
+ *     initial matrix Def. 8).
+ *
+ * Plain C types only: host or device pointers and sizes.  Every call returns an
+ * lp_status; lp_last_error() gives a thread-local detail string for the last failure.
+ *
+ * Bit conventions (all bit vectors): LSB-first little-endian uint64 words; atom a is
+ * word a>>6, bit a&63; guess g is word g>>6, bit g&63.  Padding bits are written as 0
+ * and ignored on input.  Model outputs cover the original atoms 0..n_atoms-1 only.
+ *
+ * Ownership: inputs are borrowed for the duration of the call (lp_load copies what it
+ * keeps); outputs are caller-allocated.  Device memory is owned by the lp_program
+ * handle until lp_free() and comes from the lp_options alloc/free hooks (the Python
+ * binding passes PyTorch's caching allocator) or cudaMalloc by default.  A handle must
+ * not be used by two threads at once; distinct handles are independent.
+ *
+ * Synchronisation: without LP_PTR_DEVICE every pointer argument of a run call is a host
+ * pointer and the call returns after the results are in host memory.  With
+ * LP_PTR_DEVICE every pointer argument of that call (v0, outputs, guesses, counters)
+ * is a device pointer and the call is asynchronous on lp_run.stream.
+ */
+#ifndef LP_B200_H
+#define LP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lp_program lp_program; /* opaque */
+
+typedef enum {
+    LP_OK = 0,
+    LP_E_INVALID = 1,        /* bad argument: NULL required pointer, atom id out of
+                                range, non-monotone body_ptr, size overflow          */
+    LP_E_PARSE = 2,          /* reserved (no text loader in this library)            */
+    LP_E_SEMANTIC = 3,       /* lp_least_model on a program with negation            */
+    LP_E_CAP = 4,            /* guesses == NULL and free negated atoms > guess_cap   */
+    LP_E_NOMEM = 5,          /* host or device allocation failed                     */
+    LP_E_CUDA = 6,           /* CUDA runtime error (detail in lp_last_error)         */
+    LP_E_NOT_CONVERGED = 7,  /* pass guard exceeded (cannot happen for valid input)  */
+    LP_E_NODEVICE = 8        /* run call on a host-only handle (lp_options.device<0) */
+} lp_status;
+
+/* A ground normal program (Eq. 3; definite when body_neg is NULL
+ * or all zero, Eq. 1).  Rule r: head[r] <- the literals
+ * body_atom[body_ptr[r] .. body_ptr[r+1]-1], literal j negative ("not atom") iff
+ * body_neg[j] = 1.  An empty body is a fact.  Duplicate body literals
+ * are removed (footnote PAPER.md:54); duplicate rules are kept (harmless).  Several
+ * rules with one head are the paper's multi-rule heads, standardized into AND-rows +
+ * an OR-row by lp_load. */
+typedef struct {
+    int32_t n_atoms;          /* atoms 0..n_atoms-1 (>= 0)                      */
+    int64_t n_rules;          /* >= 0                                           */
+    const int32_t *head;      /* [n_rules]                                      */
+    const int64_t *body_ptr;  /* [n_rules+1], body_ptr[0] = 0, non-decreasing   */
+    const int32_t *body_atom; /* [body_ptr[n_rules]]                            */
+    const uint8_t *body_neg;  /* [body_ptr[n_rules]] or NULL (definite)         */
+} lp_rules;
+
+typedef void *(*lp_alloc_fn)(size_t bytes, void *ctx);
+typedef void (*lp_free_fn)(void *ptr, size_t bytes, void *ctx);
+
+#define LP_LOAD_NO_FRONTIER 0x1u /* do not build the transposed occurrence lists */
+
+typedef struct {
+    int device;             /* CUDA device ordinal; -1 = host-only handle: encode and
+                               validate only (lp_info works, run calls fail with
+                               LP_E_NODEVICE) -- used by CPU tests                 */
+    int guess_cap;          /* max free negated atoms when guesses == NULL (<=0: 20) */
+    uint32_t flags;         /* LP_LOAD_*                                           */
+    int32_t smem_bits_cap;  /* test hook: max truth/summary bits kept in shared
+                               memory per CTA (0 = automatic)                      */
+    int32_t grid_blocks;    /* test hook: CTAs of the persistent kernels (0 = all
+                               co-resident CTAs)                                   */
+    lp_alloc_fn alloc;      /* device allocator hook (NULL = cudaMalloc)           */
+    lp_free_fn free;
+    void *alloc_ctx;
+} lp_options;
+
+#define LP_PTR_DEVICE 0x1u /* pointer args of this call are device pointers; async */
+#define LP_FRONTIER 0x2u   /* least model: frontier (semi-naive) variant            */
+
+typedef struct {
+    void *stream;            /* cudaStream_t (NULL = legacy default stream)          */
+    uint32_t flags;          /* LP_PTR_DEVICE | LP_FRONTIER                          */
+    int32_t *popcounts_out;  /* optional [popcounts_cap]: |I_0|, |I_1|, ..., |I_k*|   */
+    int32_t popcounts_cap;
+    int32_t *stage_out;      /* optional [n_atoms]: k if the atom first appears in
+                                I_k, -1 if it is not in the least model             */
+    void *ev_begin;          /* optional cudaEvent_t recorded on stream immediately
+                                before the fixpoint kernel, ev_end right after it   */
+    void *ev_end;
+} lp_run;
+
+typedef struct {
+    int32_t n_atoms;
+    int64_t n_rules;
+    int64_t nnz;              /* body literals after de-duplication, + 1 per fact (⊤) */
+    int64_t n_heads;          /* distinct heads                                       */
+    int32_t n_negated;        /* k: distinct atoms under negation (abar atoms)         */
+    int32_t n_free_negated;   /* f: negated atoms that are not facts (Def. 8 item 3)   */
+    int32_t max_body;
+    int32_t n_segments;       /* body-length buckets of the device layout              */
+    int64_t n_prime_paper;    /* side of the paper's standardized matrix (n + k + aux) */
+    double sparsity_eq5;      /* Eq. 5, over the input rules         */
+    int64_t device_bytes;     /* device memory held by the handle                      */
+    int64_t pass_bytes;       /* algorithmic bytes one full θ-pass streams */
+    int32_t truth_mode;       /* 0: exact truth vector in shared memory; 1: summary    */
+    int32_t summary_shift;    /* atoms per summary bit = 1 << summary_shift            */
+    int32_t grid_blocks;      /* CTAs of the persistent kernels                        */
+    int32_t block_threads;
+} lp_info_t;
+
+/* Validate, standardize and encode a program, upload it (PAPER.md:62, 82-95,
+ * 188-192, 197-210).  opt may be NULL (device 0). */
+lp_status lp_load(const lp_rules *rules, const lp_options *opt, lp_program **out);
+
+/* Shapes and layout statistics of a loaded program. */
+lp_status lp_info(const lp_program *p, lp_info_t *out);
+
+/* The k negated atoms in ascending id: abar_j of the positive form (Eq. 4) and row j
+ * of the guess matrix.  out: int32[k] host array. */
+lp_status lp_negated_atoms(const lp_program *p, int32_t *out);
+
+/* Least model of a definite program (Algorithm 1).
+ *   v0        : optional start set, bits over the original atoms ([ceil(n/64)] words);
+ *               NULL = the paper's initial vector (facts only, Def. 4).  The computed
+ *               model is LM(P ∪ {a <- : a ∈ v0}); facts are always included.
+ *   model_out : [ceil(n/64)] words, required.
+ *   iters_out : required; the number of T_P evaluations (θ-passes) including the
+ *               final one that finds no change (reading R4).
+ * Identical results (model, iters, popcounts, stages) with and without LP_FRONTIER.
+ * LP_E_SEMANTIC if the program has a negative literal. */
+lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t *model_out,
+                         int32_t *iters_out, const lp_run *run);
+
+/* Stable models (Algorithms 2-3) over a batch of guesses.
+ *   guesses    : bit-sliced guess matrix, [k][W] words with W = ceil(n_guesses/64):
+ *                bit g of row j is the value of abar_j (1 = a_j assumed false) in
+ *                guess g.  NULL = all 2^f assignments of the free negated atoms in
+ *                binary counting order (bit i of g = abar of the i-th free negated
+ *                atom; abar of a negated fact fixed to 0, Def. 8 item 3); n_guesses is
+ *                then ignored and taken as 2^f (LP_E_CAP if f > guess_cap).
+ *   accepted_out : [W] words, bit g set iff guess g's fixpoint column satisfies
+ *                a_j + abar_j = 1 for every negated atom (Algorithm 3, reading R7).
+ *   n_accepted_out : number of accepted guesses (int64).
+ *   passes_out : whole-matrix θ-passes until the matrix stopped changing
+ *                (= max over guesses of the column's pass count).
+ * The fixpoint matrix stays on the device for lp_stable_matrix / lp_guess_model. */
+lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, int64_t n_guesses,
+                           uint64_t *accepted_out, int64_t *n_accepted_out,
+                           int32_t *passes_out, const lp_run *run);
+
+/* After lp_stable_models: the fixpoint rows of the original atoms, [n_atoms][W]
+ * words (row a, bit g = atom a true in guess g's fixpoint column). */
+lp_status lp_stable_matrix(lp_program *p, uint64_t *out, const lp_run *run);
+
+/* After lp_stable_models: column `guess` of the fixpoint as a model bit vector over
+ * the original atoms, [ceil(n/64)] words. */
+lp_status lp_guess_model(lp_program *p, int64_t guess, uint64_t *model_out,
+                         const lp_run *run);
+
+/* Release the handle and its device memory (NULL is a no-op). */
+void lp_free(lp_program *p);
+
+const char *lp_status_str(lp_status s);
+const char *lp_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LP_B200_H */

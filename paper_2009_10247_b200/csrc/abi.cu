@@ -1,0 +1,576 @@
+// C ABI (include/lp.h): device residency, launch configuration and the three calls of
+// the boundary: lp_load, lp_least_model, lp_stable_models.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "kernels.h"
+
+using namespace lpb;
+
+static thread_local std::string g_err;
+
+static lp_status set_err(lp_status s, const std::string &m) {
+    g_err = m;
+    return s;
+}
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess)                                                             \
+            return set_err(LP_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+
+struct lp_program {
+    HostLayout L;
+    int device = -1;
+    lp_alloc_fn af = nullptr;
+    lp_free_fn ff = nullptr;
+    void *actx = nullptr;
+    std::vector<std::pair<void *, size_t>> allocs;
+    int64_t dev_bytes = 0;
+    int guess_cap = 20;
+
+    Segment *d_segs = nullptr;
+    int32_t *d_col = nullptr, *d_head = nullptr;
+    int64_t *d_occ_ptr = nullptr;
+    int32_t *d_occ_slot = nullptr;
+    uint32_t *d_cnt = nullptr;
+    int cnt_bytes = 1;
+    uint32_t *d_buf0 = nullptr, *d_buf1 = nullptr;
+    int32_t nwords = 0;
+    uint32_t *d_summary = nullptr;
+    int32_t sm_words = 0, shift = 0;
+    bool exact = true;
+    int32_t *d_order = nullptr;
+    int32_t *d_scal = nullptr;  // [0] tail [1] iters [2] status [3] passes [4,5] n_accepted
+    int32_t *d_facts = nullptr;
+    int32_t nfacts = 0;
+    int32_t *d_negated = nullptr, *d_negated_ext = nullptr, *d_free_rank = nullptr;
+    unsigned long long *d_v0 = nullptr, *d_model = nullptr;
+    int32_t *d_stage = nullptr, *d_pops = nullptr;
+    int32_t pops_alloc = 0;
+
+    unsigned long long *d_T0 = nullptr, *d_T1 = nullptr;
+    size_t T_words_alloc = 0;
+    int32_t W = 0, Wp = 0;
+    int64_t G = 0;
+    bool stable_valid = false;
+    uint32_t *d_any = nullptr;
+    int32_t any_words = 0, any_shift = 0;
+    int32_t *d_mark = nullptr;
+    unsigned long long *d_acc = nullptr, *d_guess = nullptr;
+    size_t acc_words_alloc = 0, guess_words_alloc = 0;
+
+    int sms = 0, threads = kThreads;
+    int lm_blocks = 0, fr_blocks = 0, st_blocks = 0, grid_cap = 0;
+    size_t lm_smem = 0, st_smem = 0;
+};
+
+// ------------------------------------------------------------------------------------
+// device memory
+// ------------------------------------------------------------------------------------
+
+static lp_status dev_alloc(lp_program *p, size_t bytes, void **out) {
+    bytes = std::max<size_t>(bytes, 16);
+    bytes = (bytes + 255) / 256 * 256;
+    void *ptr = nullptr;
+    if (p->af) {
+        ptr = p->af(bytes, p->actx);
+        if (!ptr) return set_err(LP_E_NOMEM, "device allocation hook failed");
+    } else {
+        cudaError_t e = cudaMalloc(&ptr, bytes);
+        if (e != cudaSuccess)
+            return set_err(LP_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    p->allocs.emplace_back(ptr, bytes);
+    p->dev_bytes += (int64_t)bytes;
+    *out = ptr;
+    return LP_OK;
+}
+
+template <class T>
+static lp_status dalloc(lp_program *p, T **out, size_t count) {
+    void *v = nullptr;
+    lp_status s = dev_alloc(p, count * sizeof(T), &v);
+    *out = (T *)v;
+    return s;
+}
+
+static void dev_release(lp_program *p, void *ptr) {
+    for (size_t i = 0; i < p->allocs.size(); ++i) {
+        if (p->allocs[i].first != ptr) continue;
+        if (p->ff) p->ff(ptr, p->allocs[i].second, p->actx);
+        else cudaFree(ptr);
+        p->dev_bytes -= (int64_t)p->allocs[i].second;
+        p->allocs.erase(p->allocs.begin() + (long)i);
+        return;
+    }
+}
+
+template <class T>
+static lp_status upload(lp_program *p, T **out, const std::vector<T> &v) {
+    lp_status s = dalloc(p, out, std::max<size_t>(v.size(), 1));
+    if (s) return s;
+    if (!v.empty()) CK(cudaMemcpy(*out, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return LP_OK;
+}
+
+#define TRY(x)                          \
+    do {                                \
+        lp_status s_ = (x);             \
+        if (s_ != LP_OK) return s_;     \
+    } while (0)
+
+// ------------------------------------------------------------------------------------
+// lp_load
+// ------------------------------------------------------------------------------------
+
+static lp_status load_device(lp_program *p, const lp_options *opt) {
+    HostLayout &L = p->L;
+    CK(cudaSetDevice(p->device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+    p->sms = sms;
+
+    TRY(upload(p, &p->d_segs, L.segs));
+    TRY(upload(p, &p->d_col, L.col));
+    TRY(upload(p, &p->d_head, L.head));
+    TRY(upload(p, &p->d_facts, L.facts));
+    p->nfacts = (int32_t)L.facts.size();
+    TRY(upload(p, &p->d_negated, L.negated));
+    {
+        std::vector<int32_t> ext(L.k), rank(L.k, -1);
+        for (int32_t j = 0; j < L.k; ++j) ext[j] = L.n + j;
+        for (size_t i = 0; i < L.free_j.size(); ++i) rank[L.free_j[i]] = (int32_t)i;
+        TRY(upload(p, &p->d_negated_ext, ext));
+        TRY(upload(p, &p->d_free_rank, rank));
+    }
+    if (L.has_occ) {
+        TRY(upload(p, &p->d_occ_ptr, L.occ_ptr));
+        TRY(upload(p, &p->d_occ_slot, L.occ_slot));
+        p->cnt_bytes = L.max_body <= 255 ? 1 : 4;
+        const size_t cw = p->cnt_bytes == 1 ? ((size_t)L.n_slots + 3) / 4 : (size_t)L.n_slots;
+        TRY(dalloc(p, &p->d_cnt, std::max<size_t>(cw, 1)));
+    }
+    // truth vector: bit a of word a>>5, padded to a multiple of 4 words (int4 loads)
+    p->nwords = (int32_t)((((int64_t)L.n_ext + 31) / 32 + 3) / 4 * 4);
+    TRY(dalloc(p, &p->d_buf0, p->nwords));
+    TRY(dalloc(p, &p->d_buf1, p->nwords));
+    TRY(dalloc(p, &p->d_order, (size_t)L.n_ext + 1));
+    TRY(dalloc(p, &p->d_scal, 16));
+    const size_t mw = std::max<size_t>(((size_t)L.n + 63) / 64, 1);
+    TRY(dalloc(p, &p->d_v0, mw));
+    TRY(dalloc(p, &p->d_model, mw));
+
+    // shared-memory plan: exact truth vector if it fits, else a summary
+    int64_t cap = kMaxSmemBytes;
+    if (opt && opt->smem_bits_cap > 0) cap = std::min<int64_t>(cap, opt->smem_bits_cap / 8);
+    cap = std::max<int64_t>(cap, 16);
+    if ((int64_t)p->nwords * 4 <= cap) {
+        p->exact = true;
+        p->shift = 0;
+        p->sm_words = p->nwords;
+    } else {
+        p->exact = false;
+        int sh = 1;
+        for (;; ++sh) {
+            const int64_t groups = (((int64_t)L.n_ext - 1) >> sh) + 1;
+            const int64_t w = ((groups + 31) / 32 + 3) / 4 * 4;
+            if (w * 4 <= cap) { p->sm_words = (int32_t)w; break; }
+        }
+        p->shift = sh;
+        TRY(dalloc(p, &p->d_summary, p->sm_words));
+    }
+    p->lm_smem = (size_t)p->sm_words * 4;
+
+    // stable path filter: one bit per extended atom (or per 2^any_shift atoms)
+    {
+        int sh = 0;
+        for (;; ++sh) {
+            const int64_t groups = (((int64_t)L.n_ext - 1) >> sh) + 1;
+            const int64_t w = ((groups + 31) / 32 + 3) / 4 * 4;
+            if (w * 4 <= cap) { p->any_words = (int32_t)w; break; }
+        }
+        p->any_shift = sh;
+        p->st_smem = (size_t)p->any_words * 4;
+        TRY(dalloc(p, &p->d_any, p->any_words));
+        TRY(dalloc(p, &p->d_mark, (size_t)L.n_ext));
+    }
+
+    CK(prepare_kernels(p->lm_smem, p->st_smem));
+    const int bl = lm_full_blocks_per_sm(p->exact, p->lm_smem);
+    const int bf = lm_frontier_blocks_per_sm();
+    const int bs = st_blocks_per_sm(p->st_smem);
+    if (bl < 1 || bf < 1 || bs < 1) return set_err(LP_E_CUDA, "persistent kernels do not fit on an SM");
+    p->grid_cap = (opt && opt->grid_blocks > 0) ? opt->grid_blocks : 0;
+    auto cap_grid = [&](int b) { return p->grid_cap > 0 ? std::min(b, p->grid_cap) : b; };
+    p->lm_blocks = cap_grid(sms * bl);
+    p->fr_blocks = cap_grid(sms * bf);
+    p->st_blocks = cap_grid(sms * bs);
+    CK(cudaDeviceSynchronize());
+
+    // the host copies of the big arrays are no longer needed
+    std::vector<int32_t>().swap(L.col);
+    std::vector<int32_t>().swap(L.head);
+    std::vector<int64_t>().swap(L.occ_ptr);
+    std::vector<int32_t>().swap(L.occ_slot);
+    return LP_OK;
+}
+
+static void free_all(lp_program *p) {
+    if (p->device >= 0) {
+        cudaSetDevice(p->device);
+        cudaDeviceSynchronize();
+    }
+    for (auto &a : p->allocs) {
+        if (p->ff) p->ff(a.first, a.second, p->actx);
+        else cudaFree(a.first);
+    }
+    p->allocs.clear();
+}
+
+extern "C" lp_status lp_load(const lp_rules *rules, const lp_options *opt, lp_program **out) {
+    if (!out) return set_err(LP_E_INVALID, "out is NULL");
+    *out = nullptr;
+    lp_program *p = new (std::nothrow) lp_program();
+    if (!p) return set_err(LP_E_NOMEM, "host allocation failed");
+    p->device = opt ? opt->device : 0;
+    if (opt && opt->guess_cap > 0) p->guess_cap = opt->guess_cap;
+    if (opt) { p->af = opt->alloc; p->ff = opt->free; p->actx = opt->alloc_ctx; }
+    if ((p->af == nullptr) != (p->ff == nullptr)) {
+        delete p;
+        return set_err(LP_E_INVALID, "alloc and free hooks must be given together");
+    }
+    const bool occ = !(opt && (opt->flags & LP_LOAD_NO_FRONTIER));
+    std::string err;
+    lp_status s;
+    try {
+        s = encode(rules, occ && p->device >= 0, &p->L, &err);
+    } catch (const std::bad_alloc &) {
+        s = LP_E_NOMEM;
+        err = "host allocation failed while encoding";
+    }
+    if (s != LP_OK) {
+        delete p;
+        return set_err(s, err);
+    }
+    if (p->device >= 0) {
+        s = load_device(p, opt);
+        if (s != LP_OK) {
+            free_all(p);
+            delete p;
+            return s;
+        }
+    }
+    *out = p;
+    return LP_OK;
+}
+
+extern "C" void lp_free(lp_program *p) {
+    if (!p) return;
+    free_all(p);
+    delete p;
+}
+
+extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
+    if (!p || !o) return set_err(LP_E_INVALID, "NULL argument");
+    const HostLayout &L = p->L;
+    std::memset(o, 0, sizeof(*o));
+    o->n_atoms = L.n;
+    o->n_rules = L.n_rules;
+    o->nnz = L.nnz;
+    o->n_heads = L.n_heads;
+    o->n_negated = L.k;
+    o->n_free_negated = L.f;
+    o->max_body = L.max_body;
+    o->n_segments = (int32_t)L.segs.size();
+    o->n_prime_paper = L.n_prime_paper;
+    o->sparsity_eq5 = L.sparsity_eq5;
+    o->device_bytes = p->dev_bytes;
+    // one full θ-pass streams every body entry once (4 B, padding included) and reads +
+    // writes the truth vector; heads are read only for firing rows
+    int64_t col_entries = 0;
+    for (const Segment &sg : L.segs) col_entries += (int64_t)sg.L * sg.count_pad;
+    o->pass_bytes = 4 * col_entries + 2 * (int64_t)p->nwords * 4;
+    o->truth_mode = p->exact ? 0 : 1;
+    o->summary_shift = p->shift;
+    o->grid_blocks = p->lm_blocks;
+    o->block_threads = p->threads;
+    return LP_OK;
+}
+
+extern "C" lp_status lp_negated_atoms(const lp_program *p, int32_t *out) {
+    if (!p) return set_err(LP_E_INVALID, "NULL program");
+    if (p->L.k > 0 && !out) return set_err(LP_E_INVALID, "NULL out");
+    for (int32_t j = 0; j < p->L.k; ++j) out[j] = p->L.negated[j];
+    return LP_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// lp_least_model
+// ------------------------------------------------------------------------------------
+
+extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t *model_out,
+                                    int32_t *iters_out, const lp_run *run) {
+    if (!p || !model_out || !iters_out) return set_err(LP_E_INVALID, "NULL argument");
+    if (p->device < 0) return set_err(LP_E_NODEVICE, "host-only handle");
+    if (!p->L.definite) return set_err(LP_E_SEMANTIC, "program is not definite");
+    const HostLayout &L = p->L;
+    const uint32_t flags = run ? run->flags : 0u;
+    const bool dev = flags & LP_PTR_DEVICE;
+    const bool frontier = flags & LP_FRONTIER;
+    if (frontier && !L.has_occ)
+        return set_err(LP_E_INVALID, "LP_FRONTIER on a program loaded with LP_LOAD_NO_FRONTIER");
+    cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
+    CK(cudaSetDevice(p->device));
+    const size_t mw = ((size_t)L.n + 63) / 64;
+
+    const uint32_t *v0d = nullptr;
+    if (v0) {
+        if (dev) {
+            v0d = reinterpret_cast<const uint32_t *>(v0);
+        } else {
+            if (mw) CK(cudaMemcpyAsync(p->d_v0, v0, mw * 8, cudaMemcpyHostToDevice, st));
+            v0d = reinterpret_cast<const uint32_t *>(p->d_v0);
+        }
+    }
+    int32_t *stage = nullptr;
+    if (run && run->stage_out && L.n > 0) {
+        if (dev) stage = run->stage_out;
+        else {
+            if (!p->d_stage) TRY(dalloc(p, &p->d_stage, (size_t)L.n));
+            stage = p->d_stage;
+        }
+    }
+    int32_t *pops = nullptr;
+    int32_t pop_cap = 0;
+    if (run && run->popcounts_out && run->popcounts_cap > 0) {
+        pop_cap = run->popcounts_cap;
+        if (dev) pops = run->popcounts_out;
+        else {
+            if (p->pops_alloc < pop_cap) {
+                if (p->d_pops) dev_release(p, p->d_pops);
+                TRY(dalloc(p, &p->d_pops, (size_t)pop_cap));
+                p->pops_alloc = pop_cap;
+            }
+            pops = p->d_pops;
+        }
+    }
+
+    LMParams q{};
+    q.segs = p->d_segs;
+    q.nseg = (int32_t)L.segs.size();
+    q.n = L.n;
+    q.col = p->d_col;
+    q.head = p->d_head;
+    q.buf0 = p->d_buf0;
+    q.buf1 = p->d_buf1;
+    q.nwords = p->nwords;
+    q.summary = p->d_summary;
+    q.sm_words = p->sm_words;
+    q.shift = p->shift;
+    q.order = p->d_order;
+    q.tail = p->d_scal + 0;
+    q.stage = stage;
+    q.pops = pops;
+    q.pop_cap = pop_cap;
+    q.iters_out = dev ? iters_out : p->d_scal + 1;
+    q.status_out = p->d_scal + 2;
+    q.max_passes = L.n_ext + 2;
+    q.occ_ptr = p->d_occ_ptr;
+    q.occ_slot = p->d_occ_slot;
+    q.cnt = p->d_cnt;
+    q.cnt_bytes = p->cnt_bytes;
+
+    CK(launch_lm_init(q, v0d, (int32_t)(mw * 2), p->d_facts, p->nfacts, L.top,
+                      p->exact ? nullptr : p->d_summary, p->exact ? 0 : p->sm_words,
+                      p->sms, st));
+    if (frontier) CK(launch_fill_counters(L.segs.data(), (int)L.segs.size(), p->d_cnt, p->cnt_bytes, st));
+    if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
+    if (frontier) CK(launch_lm_frontier(q, p->fr_blocks, st));
+    else CK(launch_lm_full(q, p->exact, p->lm_blocks, p->lm_smem, st));
+    if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
+    unsigned long long *mout = dev ? reinterpret_cast<unsigned long long *>(model_out) : p->d_model;
+    CK(launch_extract_model(p->d_buf0, L.n, mout, st));
+    if (dev) return LP_OK;
+
+    int32_t scal[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(scal, p->d_scal, sizeof(scal), cudaMemcpyDeviceToHost, st));
+    if (mw) CK(cudaMemcpyAsync(model_out, p->d_model, mw * 8, cudaMemcpyDeviceToHost, st));
+    if (stage) CK(cudaMemcpyAsync(run->stage_out, stage, sizeof(int32_t) * (size_t)L.n,
+                                  cudaMemcpyDeviceToHost, st));
+    if (pops) CK(cudaMemcpyAsync(run->popcounts_out, pops, sizeof(int32_t) * (size_t)pop_cap,
+                                 cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *iters_out = scal[1];
+    if (scal[2] != 0) return set_err(LP_E_NOT_CONVERGED, "pass guard exceeded");
+    return LP_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// lp_stable_models
+// ------------------------------------------------------------------------------------
+
+static STParams st_params(lp_program *p) {
+    const HostLayout &L = p->L;
+    STParams s{};
+    s.segs = p->d_segs;
+    s.nseg = (int32_t)L.segs.size();
+    s.n_ext = L.n_ext;
+    s.col = p->d_col;
+    s.head = p->d_head;
+    s.T0 = p->d_T0;
+    s.T1 = p->d_T1;
+    s.Wp = p->Wp;
+    s.any_init = p->d_any;
+    s.any_words = p->any_words;
+    s.any_shift = p->any_shift;
+    s.order = p->d_order;
+    s.tail = p->d_scal + 0;
+    s.mark = p->d_mark;
+    s.passes_out = p->d_scal + 3;
+    s.status_out = p->d_scal + 2;
+    s.max_passes = L.n_ext + 2;
+    return s;
+}
+
+extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, int64_t n_guesses,
+                                      uint64_t *accepted_out, int64_t *n_accepted_out,
+                                      int32_t *passes_out, const lp_run *run) {
+    if (!p || !accepted_out || !n_accepted_out || !passes_out)
+        return set_err(LP_E_INVALID, "NULL argument");
+    if (p->device < 0) return set_err(LP_E_NODEVICE, "host-only handle");
+    const HostLayout &L = p->L;
+    const uint32_t flags = run ? run->flags : 0u;
+    const bool dev = flags & LP_PTR_DEVICE;
+    cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
+    int64_t G;
+    if (!guesses) {
+        if (L.f > p->guess_cap)
+            return set_err(LP_E_CAP, "guess explosion: " + std::to_string(L.f) +
+                                         " free negated atoms > guess_cap " + std::to_string(p->guess_cap));
+        G = (int64_t)1 << L.f;
+    } else {
+        if (n_guesses < 1) return set_err(LP_E_INVALID, "n_guesses < 1");
+        G = n_guesses;
+    }
+    const int64_t W64 = (G + 63) / 64;
+    if (W64 > (1 << 26)) return set_err(LP_E_INVALID, "too many guesses");
+    const int32_t W = (int32_t)W64, Wp = (W + 1) / 2 * 2;
+    CK(cudaSetDevice(p->device));
+    const size_t need = (size_t)L.n_ext * Wp;
+    if (need > p->T_words_alloc) {
+        if (p->d_T0) dev_release(p, p->d_T0);
+        if (p->d_T1) dev_release(p, p->d_T1);
+        p->d_T0 = p->d_T1 = nullptr;
+        TRY(dalloc(p, &p->d_T0, need));
+        TRY(dalloc(p, &p->d_T1, need));
+        p->T_words_alloc = need;
+    }
+    p->W = W;
+    p->Wp = Wp;
+    p->G = G;
+    p->stable_valid = false;
+    const unsigned long long *gd = nullptr;
+    if (guesses && L.k > 0) {
+        if (dev) gd = reinterpret_cast<const unsigned long long *>(guesses);
+        else {
+            const size_t gw = (size_t)L.k * W;
+            if (gw > p->guess_words_alloc) {
+                if (p->d_guess) dev_release(p, p->d_guess);
+                TRY(dalloc(p, &p->d_guess, gw));
+                p->guess_words_alloc = gw;
+            }
+            CK(cudaMemcpyAsync(p->d_guess, guesses, gw * 8, cudaMemcpyHostToDevice, st));
+            gd = p->d_guess;
+        }
+    }
+    unsigned long long *acc;
+    if (dev) acc = reinterpret_cast<unsigned long long *>(accepted_out);
+    else {
+        if ((size_t)W > p->acc_words_alloc) {
+            if (p->d_acc) dev_release(p, p->d_acc);
+            TRY(dalloc(p, &p->d_acc, (size_t)W));
+            p->acc_words_alloc = W;
+        }
+        acc = p->d_acc;
+    }
+    long long *nacc = dev ? reinterpret_cast<long long *>(n_accepted_out)
+                          : reinterpret_cast<long long *>(p->d_scal + 4);
+    STParams s = st_params(p);
+    if (dev) s.passes_out = passes_out;
+    CK(launch_st_init(s, L.n, L.k, p->d_negated_ext, p->d_free_rank, guesses ? gd : nullptr, W, G,
+                      p->d_facts, p->nfacts, L.top, p->d_any, st));
+    if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
+    CK(launch_st_fixpoint(s, p->st_blocks, p->st_smem, st));
+    if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
+    CK(launch_st_check(s, L.n, L.k, p->d_negated, W, G, acc, nacc, st));
+    p->stable_valid = true;
+    if (dev) return LP_OK;
+    int32_t scal[6] = {0, 0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(scal, p->d_scal, sizeof(scal), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(accepted_out, acc, (size_t)W * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *passes_out = scal[3];
+    int64_t na;
+    std::memcpy(&na, scal + 4, sizeof(na));
+    *n_accepted_out = na;
+    if (scal[2] != 0) return set_err(LP_E_NOT_CONVERGED, "pass guard exceeded");
+    return LP_OK;
+}
+
+extern "C" lp_status lp_stable_matrix(lp_program *p, uint64_t *out, const lp_run *run) {
+    if (!p || !out) return set_err(LP_E_INVALID, "NULL argument");
+    if (p->device < 0) return set_err(LP_E_NODEVICE, "host-only handle");
+    if (!p->stable_valid) return set_err(LP_E_INVALID, "no lp_stable_models result");
+    const bool dev = run && (run->flags & LP_PTR_DEVICE);
+    cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
+    CK(cudaSetDevice(p->device));
+    if (p->L.n == 0) return LP_OK;
+    CK(cudaMemcpy2DAsync(out, (size_t)p->W * 8, p->d_T0, (size_t)p->Wp * 8, (size_t)p->W * 8,
+                         (size_t)p->L.n, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (!dev) CK(cudaStreamSynchronize(st));
+    return LP_OK;
+}
+
+extern "C" lp_status lp_guess_model(lp_program *p, int64_t guess, uint64_t *model_out,
+                                    const lp_run *run) {
+    if (!p || !model_out) return set_err(LP_E_INVALID, "NULL argument");
+    if (p->device < 0) return set_err(LP_E_NODEVICE, "host-only handle");
+    if (!p->stable_valid) return set_err(LP_E_INVALID, "no lp_stable_models result");
+    if (guess < 0 || guess >= p->G) return set_err(LP_E_INVALID, "guess out of range");
+    const bool dev = run && (run->flags & LP_PTR_DEVICE);
+    cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
+    CK(cudaSetDevice(p->device));
+    STParams s = st_params(p);
+    unsigned long long *o = dev ? reinterpret_cast<unsigned long long *>(model_out) : p->d_model;
+    CK(launch_st_column(s, p->L.n, guess, o, st));
+    if (dev) return LP_OK;
+    const size_t mw = ((size_t)p->L.n + 63) / 64;
+    if (mw) CK(cudaMemcpyAsync(model_out, p->d_model, mw * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return LP_OK;
+}
+
+extern "C" const char *lp_status_str(lp_status s) {
+    switch (s) {
+        case LP_OK: return "ok";
+        case LP_E_INVALID: return "invalid argument";
+        case LP_E_PARSE: return "parse error";
+        case LP_E_SEMANTIC: return "semantic error";
+        case LP_E_CAP: return "guess cap exceeded";
+        case LP_E_NOMEM: return "out of memory";
+        case LP_E_CUDA: return "CUDA error";
+        case LP_E_NOT_CONVERGED: return "not converged";
+        case LP_E_NODEVICE: return "host-only handle";
+    }
+    return "unknown status";
+}
+
+extern "C" const char *lp_last_error(void) { return g_err.c_str(); }

@@ -1,0 +1,190 @@
+// Host-side standardiser / encoder.
+//
+// Turns the caller's rules into the device layout:
+//   * positive form (Eq. 4): a negative literal "not a" becomes the
+//     fresh atom abar_j = n + j, j = rank of a among the negated atoms (ascending);
+//   * facts point at the always-true atom ⊤ = n + k (one AND-row with
+//     body {⊤}), instead of the paper's diagonal a_ii = 1 (Def. 2 item 3; reading R2);
+//   * every rule is one AND-row whose threshold is its (de-duplicated) body length, so
+//     θ (Def. 5) is the exact integer test "all body atoms true" (reading R1);
+//   * the OR-row of a multi-rule head (standardisation) is not
+//     materialised: all AND-rows of a head scatter into the head's bit with an OR,
+//     which is the OR-rule's T_P clause fused into the same pass;
+//   * AND-rows are bucketed by body length L into position-major segments so a
+//     thread streams 4 rules per int4 load with no row-pointer array.
+#include <algorithm>
+#include <cstring>
+#include <limits>
+
+#include "lp_internal.h"
+
+namespace lpb {
+
+static lp_status fail(std::string *err, lp_status s, const std::string &msg) {
+    if (err) *err = msg;
+    return s;
+}
+
+lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *err) {
+    if (!r || !L) return fail(err, LP_E_INVALID, "NULL rules or output");
+    const int64_t R = r->n_rules;
+    const int32_t n = r->n_atoms;
+    if (n < 0 || R < 0) return fail(err, LP_E_INVALID, "negative n_atoms or n_rules");
+    if (R > 0 && (!r->head || !r->body_ptr))
+        return fail(err, LP_E_INVALID, "NULL head or body_ptr");
+    const int64_t nnz_in = R > 0 ? r->body_ptr[R] : 0;
+    if (R > 0 && r->body_ptr[0] != 0) return fail(err, LP_E_INVALID, "body_ptr[0] != 0");
+    for (int64_t i = 0; i < R; ++i) {
+        if (r->body_ptr[i + 1] < r->body_ptr[i])
+            return fail(err, LP_E_INVALID, "body_ptr not non-decreasing at rule " + std::to_string(i));
+        if (r->head[i] < 0 || r->head[i] >= n)
+            return fail(err, LP_E_INVALID, "head out of range at rule " + std::to_string(i));
+    }
+    if (nnz_in > 0 && !r->body_atom) return fail(err, LP_E_INVALID, "NULL body_atom");
+    for (int64_t j = 0; j < nnz_in; ++j)
+        if (r->body_atom[j] < 0 || r->body_atom[j] >= n)
+            return fail(err, LP_E_INVALID, "body atom out of range at literal " + std::to_string(j));
+
+    // ---- negated atoms, facts -----------------------------------------------------
+    std::vector<uint8_t> isneg((size_t)n + 1, 0), isfact((size_t)n + 1, 0);
+    if (r->body_neg)
+        for (int64_t j = 0; j < nnz_in; ++j)
+            if (r->body_neg[j]) isneg[r->body_atom[j]] = 1;
+    for (int64_t i = 0; i < R; ++i)
+        if (r->body_ptr[i] == r->body_ptr[i + 1]) isfact[r->head[i]] = 1;
+    std::vector<int32_t> jof((size_t)n + 1, -1);
+    int32_t k = 0;
+    for (int32_t a = 0; a < n; ++a)
+        if (isneg[a]) { jof[a] = k++; L->negated.push_back(a); }
+    if ((int64_t)n + k + 2 > std::numeric_limits<int32_t>::max())
+        return fail(err, LP_E_INVALID, "too many atoms for int32 ids");
+    for (int32_t j = 0; j < k; ++j)
+        if (!isfact[L->negated[j]]) L->free_j.push_back(j);
+    for (int32_t a = 0; a < n; ++a)
+        if (isfact[a]) L->facts.push_back(a);
+
+    L->n = n;
+    L->k = k;
+    L->f = (int32_t)L->free_j.size();
+    L->top = n + k;
+    L->bot = n + k + 1;
+    L->n_ext = n + k + 2;
+    L->n_rules = R;
+    L->definite = (k == 0);
+
+    // ---- per-rule de-duplicated extended bodies -----------------------------------
+    std::vector<int32_t> ext((size_t)std::max<int64_t>(nnz_in, 1));
+    std::vector<int32_t> len((size_t)std::max<int64_t>(R, 1));
+    std::vector<int32_t> tmp;
+    int64_t pos = 0;
+    int32_t maxL = 0;
+    for (int64_t i = 0; i < R; ++i) {
+        const int64_t s = r->body_ptr[i], e = r->body_ptr[i + 1];
+        const int64_t start = pos;
+        if (e - s <= 16) {
+            for (int64_t j = s; j < e; ++j) {
+                int32_t a = r->body_atom[j];
+                int32_t x = (r->body_neg && r->body_neg[j]) ? n + jof[a] : a;
+                bool dup = false;
+                for (int64_t q = start; q < pos; ++q)
+                    if (ext[q] == x) { dup = true; break; }
+                if (!dup) ext[pos++] = x;
+            }
+        } else {
+            tmp.clear();
+            for (int64_t j = s; j < e; ++j) {
+                int32_t a = r->body_atom[j];
+                tmp.push_back((r->body_neg && r->body_neg[j]) ? n + jof[a] : a);
+            }
+            std::sort(tmp.begin(), tmp.end());
+            tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+            for (int32_t x : tmp) ext[pos++] = x;
+        }
+        int64_t l = pos - start;
+        if (l > std::numeric_limits<int32_t>::max()) return fail(err, LP_E_INVALID, "body too long");
+        len[i] = (int32_t)l;
+        int32_t Le = l == 0 ? 1 : (int32_t)l;   // a fact is the AND-row {⊤}
+        if (Le > maxL) maxL = Le;
+    }
+    L->max_body = maxL;
+
+    // ---- statistics ----------------------------------------------------------------
+    {
+        std::vector<int32_t> per_head((size_t)n + 1, 0);
+        for (int64_t i = 0; i < R; ++i) per_head[r->head[i]]++;
+        int64_t heads = 0, aux = 0;
+        for (int32_t a = 0; a < n; ++a) {
+            if (per_head[a]) ++heads;
+            if (per_head[a] >= 2) aux += per_head[a];
+        }
+        L->n_heads = heads;
+        L->n_prime_paper = (int64_t)n + k + aux;
+        L->sparsity_eq5 = n == 0 ? 1.0 : 1.0 - (double)nnz_in / ((double)n * (double)n);
+    }
+
+    // ---- segments by body length ---------------------------------------------------
+    std::vector<int64_t> cnt((size_t)maxL + 1, 0);
+    for (int64_t i = 0; i < R; ++i) cnt[len[i] == 0 ? 1 : len[i]]++;
+    std::vector<int32_t> segof((size_t)maxL + 1, -1);
+    int64_t col_off = 0, slot_off = 0, nnz = 0;
+    for (int32_t l = 1; l <= maxL; ++l) {
+        if (!cnt[l]) continue;
+        Segment sg{};
+        sg.L = l;
+        sg.count = cnt[l];
+        sg.count_pad = (cnt[l] + 3) / 4 * 4;
+        sg.col_off = col_off;
+        sg.slot_off = slot_off;
+        col_off += (int64_t)l * sg.count_pad;
+        slot_off += sg.count_pad;
+        nnz += (int64_t)l * sg.count;
+        segof[l] = (int32_t)L->segs.size();
+        L->segs.push_back(sg);
+    }
+    if (slot_off > std::numeric_limits<int32_t>::max())
+        return fail(err, LP_E_INVALID, "too many rules for int32 slots");
+    L->nnz = nnz;
+    L->n_slots = slot_off;
+    L->col.assign((size_t)col_off, L->bot);
+    L->head.assign((size_t)slot_off, L->bot);
+    std::vector<int64_t> fillc(L->segs.size(), 0);
+    pos = 0;
+    for (int64_t i = 0; i < R; ++i) {
+        const int32_t l = len[i];
+        const int32_t le = l == 0 ? 1 : l;
+        const Segment &sg = L->segs[segof[le]];
+        const int64_t slot = fillc[segof[le]]++;
+        int32_t *c = L->col.data() + sg.col_off + slot;
+        if (l == 0) {
+            c[0] = L->top;
+        } else {
+            for (int32_t j = 0; j < l; ++j) c[(int64_t)j * sg.count_pad] = ext[pos + j];
+        }
+        pos += l;
+        L->head[sg.slot_off + slot] = r->head[i];
+    }
+
+    // ---- transposed occurrence lists (frontier variant) ----------
+    L->has_occ = build_occ;
+    if (build_occ) {
+        L->occ_ptr.assign((size_t)L->n_ext + 1, 0);
+        for (const Segment &sg : L->segs)
+            for (int32_t j = 0; j < sg.L; ++j) {
+                const int32_t *c = L->col.data() + sg.col_off + (int64_t)j * sg.count_pad;
+                for (int64_t i = 0; i < sg.count; ++i)
+                    if (c[i] != L->top) L->occ_ptr[c[i] + 1]++;
+            }
+        for (int32_t a = 0; a < L->n_ext; ++a) L->occ_ptr[a + 1] += L->occ_ptr[a];
+        L->occ_slot.assign((size_t)std::max<int64_t>(L->occ_ptr[L->n_ext], 1), 0);
+        std::vector<int64_t> fo(L->occ_ptr.begin(), L->occ_ptr.end() - 1);
+        for (const Segment &sg : L->segs)
+            for (int32_t j = 0; j < sg.L; ++j) {
+                const int32_t *c = L->col.data() + sg.col_off + (int64_t)j * sg.count_pad;
+                for (int64_t i = 0; i < sg.count; ++i)
+                    if (c[i] != L->top) L->occ_slot[fo[c[i]]++] = (int32_t)(sg.slot_off + i);
+            }
+    }
+    return LP_OK;
+}
+
+}  // namespace lpb

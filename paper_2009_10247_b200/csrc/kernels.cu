@@ -1,0 +1,689 @@
+// sm_100a kernels of the least-model / stable-model hot path.
+//
+//   lm_init_*          v_0 = v0 ∪ facts ∪ {⊤}                         (row a3; Def. 4)
+//   lm_full_kernel     persistent fused θ-pass loop: every AND-row's body is tested
+//                      against the bit-packed truth vector, firing rows OR their head
+//                      bit into v_{k+1}, the changed flag is the growth of the
+//                      derivation list; one cooperative launch runs all passes to the
+//                      fixpoint                               (rows a4, a5; Alg. 1)
+//   lm_frontier_kernel level-synchronous semi-naive variant: only the rows whose
+//                      bodies contain newly-true atoms are touched   (row a6)
+//   st_init_kernel     bit-sliced initial matrix, 64 guesses per word (row a7; Def. 8)
+//   st_fixpoint_kernel batched θ-pass loop over the guess matrix    (row a8; Alg. 2)
+//   st_check_kernel    complementarity test a_j + abar_j = 1 per guess (row a9; Alg. 3)
+//
+// See DESIGN.md for the layout, the roofline of each kernel and the readings of the
+// paper they implement.
+#include <cooperative_groups.h>
+
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace lpb {
+
+// ------------------------------------------------------------------------------------
+// memory helpers
+// ------------------------------------------------------------------------------------
+
+// Streaming 128-bit load of read-only program data: no L1 allocation (no reuse).
+__device__ __forceinline__ int4 ld_stream(const int4 *p) {
+    int4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ bool sm_bit(const uint32_t *sm, uint32_t x) {
+    return (sm[x >> 5] >> (x & 31)) & 1u;
+}
+
+// ------------------------------------------------------------------------------------
+// least model: initial vector
+// ------------------------------------------------------------------------------------
+
+__global__ void lm_init_words(uint32_t *buf0, uint32_t *buf1, int32_t nwords,
+                              const uint32_t *v0, int32_t v0_words, int32_t n, int32_t top) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t bits = 0;
+        const int64_t lo = w * 32;
+        if (v0 && w < v0_words && lo < n) {
+            bits = v0[w];
+            if (lo + 32 > n) bits &= (1u << (uint32_t)(n - lo)) - 1u;
+        }
+        if (w == (top >> 5)) bits |= 1u << (top & 31);
+        buf0[w] = bits;
+        buf1[w] = bits;
+    }
+}
+
+__global__ void lm_init_facts(uint32_t *buf0, uint32_t *buf1, const int32_t *facts,
+                              int32_t nfacts) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nfacts;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t a = facts[i];
+        atomicOr(buf0 + (a >> 5), 1u << (a & 31));
+        atomicOr(buf1 + (a >> 5), 1u << (a & 31));
+    }
+}
+
+// List the initial atoms (original atoms of v_0) into the derivation order list, set
+// their stage to 0 and build the initial summary (FILTER mode).
+__global__ void lm_init_list(const uint32_t *buf0, int32_t n, int32_t top, int32_t *order,
+                             int32_t *tail, int32_t *stage, uint32_t *summary, int32_t shift) {
+    const int64_t nw = ((int64_t)n + 31) >> 5;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (summary && tid == 0) {
+        const uint32_t g = (uint32_t)top >> shift;
+        atomicOr(summary + (g >> 5), 1u << (g & 31));
+    }
+    for (int64_t w = tid; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t bits = buf0[w];
+        const int64_t lo = w * 32;
+        if (lo + 32 > n) bits &= (1u << (uint32_t)(n - lo)) - 1u;
+        if (!bits) continue;
+        int32_t pos = atomicAdd(tail, __popc(bits));
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int32_t a = (int32_t)(lo + b);
+            order[pos++] = a;
+            if (stage) stage[a] = 0;
+            if (summary) {
+                const uint32_t g = (uint32_t)a >> shift;
+                atomicOr(summary + (g >> 5), 1u << (g & 31));
+            }
+        }
+    }
+}
+
+cudaError_t launch_lm_init(const LMParams &p, const uint32_t *v0_words32, int32_t v0_words,
+                           const int32_t *facts, int32_t nfacts, int32_t top, uint32_t *summary,
+                           int32_t sum_words, int blocks, cudaStream_t st) {
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(p.tail, 0, sizeof(int32_t), st))) return e;
+    if (p.stage && p.n > 0)
+        if ((e = cudaMemsetAsync(p.stage, 0xFF, sizeof(int32_t) * (size_t)p.n, st))) return e;
+    if (summary && sum_words > 0)
+        if ((e = cudaMemsetAsync(summary, 0, sizeof(uint32_t) * (size_t)sum_words, st))) return e;
+    const int tb = 256;
+    int gb = (int)std::min<int64_t>(((int64_t)p.nwords + tb - 1) / tb, (int64_t)blocks * 8);
+    lm_init_words<<<std::max(gb, 1), tb, 0, st>>>(p.buf0, p.buf1, p.nwords, v0_words32, v0_words,
+                                                  p.n, top);
+    if (nfacts > 0) {
+        int fb = (int)std::min<int64_t>(((int64_t)nfacts + tb - 1) / tb, (int64_t)blocks * 8);
+        lm_init_facts<<<std::max(fb, 1), tb, 0, st>>>(p.buf0, p.buf1, facts, nfacts);
+    }
+    int lb = (int)std::min<int64_t>((((int64_t)p.n + 31) / 32 + tb - 1) / tb, (int64_t)blocks * 8);
+    lm_init_list<<<std::max(lb, 1), tb, 0, st>>>(p.buf0, p.n, top, p.order, p.tail, p.stage,
+                                                 summary, p.shift);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// least model: fused θ-pass (full variant)
+// ------------------------------------------------------------------------------------
+
+struct PassCtx {
+    const uint32_t *rd;  // v_k (global)
+    uint32_t *wr;        // v_{k+1} (global)
+    const uint32_t *sm;  // shared copy of v_k (EXACT) or of its summary
+    int k;
+};
+
+// Smem test of 4 AND-rows at one body position; `fire` bit e = row e still alive.
+template <bool EXACT>
+__device__ __forceinline__ unsigned test4(int4 a, unsigned fire, const uint32_t *sm, int shift) {
+    const uint32_t s = EXACT ? 0u : (uint32_t)shift;
+    if ((fire & 1u) && !sm_bit(sm, (uint32_t)a.x >> s)) fire &= ~1u;
+    if ((fire & 2u) && !sm_bit(sm, (uint32_t)a.y >> s)) fire &= ~2u;
+    if ((fire & 4u) && !sm_bit(sm, (uint32_t)a.z >> s)) fire &= ~4u;
+    if ((fire & 8u) && !sm_bit(sm, (uint32_t)a.w >> s)) fire &= ~8u;
+    return fire;
+}
+
+// Rows (slots i0..i0+3 of segment sg) that passed the shared-memory test.  In FILTER
+// mode the test was on the summary, so the exact bits are checked in v_k (L2).  A row
+// that fires ORs its head into v_{k+1}; the thread that sets a new bit appends the
+// head to the derivation list (this is the pass's "changed" signal).
+template <bool EXACT>
+__device__ __noinline__ void on_fire(const LMParams &p, const Segment &sg, int64_t i0,
+                                     unsigned fire, const PassCtx &c) {
+    for (int e = 0; e < 4; ++e) {
+        if (!((fire >> e) & 1u)) continue;
+        const int64_t i = i0 + e;
+        if (!EXACT) {
+            bool ok = true;
+            for (int32_t j = 0; j < sg.L && ok; ++j) {
+                const uint32_t a = (uint32_t)__ldg(p.col + sg.col_off + (int64_t)j * sg.count_pad + i);
+                ok = (__ldcg(c.rd + (a >> 5)) >> (a & 31)) & 1u;
+            }
+            if (!ok) continue;
+        }
+        const int32_t h = __ldg(p.head + sg.slot_off + i);
+        const uint32_t bit = 1u << (h & 31);
+        const uint32_t cur = EXACT ? c.sm[h >> 5] : __ldcg(c.rd + (h >> 5));
+        if (cur & bit) continue;                       // already in v_k
+        const uint32_t old = atomicOr(c.wr + (h >> 5), bit);
+        if (old & bit) continue;                       // another row set it this pass
+        const int32_t pos = atomicAdd(p.tail, 1);
+        p.order[pos] = h;
+        if (p.stage) p.stage[h] = c.k + 1;
+    }
+}
+
+template <int L, int U, bool EXACT>
+__device__ __forceinline__ void seg_pass(const LMParams &p, const Segment &sg, const PassCtx &c,
+                                         int64_t gtid, int64_t gthreads) {
+    const int64_t nq = sg.count_pad >> 2;
+    const int4 *base = reinterpret_cast<const int4 *>(p.col + sg.col_off);
+    for (int64_t q0 = gtid; q0 < nq; q0 += gthreads * U) {
+        int4 v[U][L];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = q0 + u * gthreads;
+#pragma unroll
+            for (int j = 0; j < L; ++j)
+                v[u][j] = q < nq ? ld_stream(base + j * nq + q) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = q0 + u * gthreads;
+            if (q >= nq) break;
+            unsigned fire = 0xFu;
+#pragma unroll
+            for (int j = 0; j < L; ++j) fire = test4<EXACT>(v[u][j], fire, c.sm, p.shift);
+            if (fire) on_fire<EXACT>(p, sg, q * 4, fire, c);
+        }
+    }
+}
+
+template <bool EXACT>
+__device__ void seg_pass_generic(const LMParams &p, const Segment &sg, const PassCtx &c,
+                                 int64_t gtid, int64_t gthreads) {
+    const int64_t nq = sg.count_pad >> 2;
+    const int4 *base = reinterpret_cast<const int4 *>(p.col + sg.col_off);
+    for (int64_t q = gtid; q < nq; q += gthreads) {
+        unsigned fire = 0xFu;
+#pragma unroll 4
+        for (int32_t j = 0; j < sg.L; ++j) fire = test4<EXACT>(ld_stream(base + j * nq + q), fire, c.sm, p.shift);
+        if (fire) on_fire<EXACT>(p, sg, q * 4, fire, c);
+    }
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c, int64_t gtid,
+                                             int64_t gthreads) {
+    for (int32_t s = 0; s < p.nseg; ++s) {
+        const Segment sg = p.segs[s];
+        switch (sg.L) {
+            case 1: seg_pass<1, 4, EXACT>(p, sg, c, gtid, gthreads); break;
+            case 2: seg_pass<2, 4, EXACT>(p, sg, c, gtid, gthreads); break;
+            case 3: seg_pass<3, 2, EXACT>(p, sg, c, gtid, gthreads); break;
+            case 4: seg_pass<4, 2, EXACT>(p, sg, c, gtid, gthreads); break;
+            case 5: seg_pass<5, 1, EXACT>(p, sg, c, gtid, gthreads); break;
+            case 6: seg_pass<6, 1, EXACT>(p, sg, c, gtid, gthreads); break;
+            case 7: seg_pass<7, 1, EXACT>(p, sg, c, gtid, gthreads); break;
+            case 8: seg_pass<8, 1, EXACT>(p, sg, c, gtid, gthreads); break;
+            default: seg_pass_generic<EXACT>(p, sg, c, gtid, gthreads); break;
+        }
+    }
+}
+
+// One cooperative launch = the whole fixpoint loop of Algorithm 1:
+// pass k reads v_k (rd) and writes v_{k+1} (wr); the loop ends after the first pass
+// that derives nothing (u = v), and iters = k + 1 counts that pass too.
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads, 1) lm_full_kernel(LMParams p) {
+    extern __shared__ uint32_t sm[];
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+
+    const uint32_t *src0 = EXACT ? p.buf0 : p.summary;
+    for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(src0 + w);
+    const int32_t n0 = __ldcg(p.tail);
+    if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = n0;
+    __syncthreads();
+
+    int32_t ds = n0, de = n0;  // atoms that became true in the previous pass
+    for (int k = 0;; ++k) {
+        const uint32_t *rd = (k & 1) ? p.buf1 : p.buf0;
+        uint32_t *wr = (k & 1) ? p.buf0 : p.buf1;
+        if (k > 0) {
+            // wr holds v_{k-1}: add the atoms derived in pass k-1 to make it v_k
+            for (int64_t i = ds + gtid; i < de; i += gthreads) {
+                const int32_t a = __ldcg(p.order + i);
+                atomicOr(wr + (a >> 5), 1u << (a & 31));
+            }
+            // shared copy: v_{k-1} -> v_k
+            if (EXACT && (de - ds) > (p.sm_words >> 2)) {
+                for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(rd + w);
+            } else {
+                for (int64_t i = ds + tid; i < de; i += blockDim.x) {
+                    const uint32_t a = (uint32_t)__ldcg(p.order + i);
+                    const uint32_t g = EXACT ? a : (a >> p.shift);
+                    atomicOr(sm + (g >> 5), 1u << (g & 31));
+                }
+            }
+            __syncthreads();
+        }
+        const PassCtx c{rd, wr, sm, k};
+        all_segments<EXACT>(p, c, gtid, gthreads);
+        grid.sync();
+        const int32_t t = __ldcg(p.tail);
+        const bool lead = blockIdx.x == 0 && tid == 0;
+        if (t == de) {  // u = v: fixpoint
+            if (lead) { *p.iters_out = k + 1; *p.status_out = 0; }
+            return;
+        }
+        if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
+        if (k + 1 >= p.max_passes) {
+            if (lead) { *p.iters_out = k + 1; *p.status_out = 1; }
+            return;
+        }
+        ds = de;
+        de = t;
+    }
+}
+
+cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st) {
+    LMParams q = p;
+    void *args[] = {(void *)&q};
+    if (exact)
+        return cudaLaunchCooperativeKernel((const void *)lm_full_kernel<true>, dim3(blocks),
+                                           dim3(kThreads), args, smem, st);
+    return cudaLaunchCooperativeKernel((const void *)lm_full_kernel<false>, dim3(blocks),
+                                       dim3(kThreads), args, smem, st);
+}
+
+// ------------------------------------------------------------------------------------
+// least model: frontier (semi-naive) variant
+// ------------------------------------------------------------------------------------
+
+// Level-synchronous push: the atoms that became true at level k decrement the
+// remaining-body counter of every row whose body contains them; a counter reaching 0
+// means body(r) ⊆ I_k, so head(r) ∈ I_{k+1} -- the same stage as the full θ-pass, hence
+// the same model, pass count and popcount trace (reading R6).
+__global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(LMParams p) {
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
+    const int64_t gwarp = gtid >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int32_t qs = 0, qe = __ldcg(p.tail);
+    if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = qe;
+    for (int k = 0;; ++k) {
+        for (int64_t i = qs + gwarp; i < qe; i += nwarps) {
+            const int32_t a = __ldcg(p.order + i);
+            const int64_t o0 = __ldg(p.occ_ptr + a), o1 = __ldg(p.occ_ptr + a + 1);
+            for (int64_t o = o0 + lane; o < o1; o += 32) {
+                const int32_t slot = __ldg(p.occ_slot + o);
+                bool fired;
+                if (p.cnt_bytes == 1) {
+                    const uint32_t sh = (uint32_t)(slot & 3) << 3;
+                    const uint32_t old = atomicSub(p.cnt + (slot >> 2), 1u << sh);
+                    fired = ((old >> sh) & 0xFFu) == 1u;
+                } else {
+                    fired = atomicSub(p.cnt + slot, 1u) == 1u;
+                }
+                if (fired) {
+                    const int32_t h = __ldg(p.head + slot);
+                    const uint32_t bit = 1u << (h & 31);
+                    const uint32_t old = atomicOr(p.buf0 + (h >> 5), bit);
+                    if (!(old & bit)) {
+                        const int32_t pos = atomicAdd(p.tail, 1);
+                        p.order[pos] = h;
+                        if (p.stage) p.stage[h] = k + 1;
+                    }
+                }
+            }
+        }
+        grid.sync();
+        const int32_t t = __ldcg(p.tail);
+        const bool lead = blockIdx.x == 0 && tid == 0;
+        if (t == qe) {
+            if (lead) { *p.iters_out = k + 1; *p.status_out = 0; }
+            return;
+        }
+        if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
+        if (k + 1 >= p.max_passes) {
+            if (lead) { *p.iters_out = k + 1; *p.status_out = 1; }
+            return;
+        }
+        qs = qe;
+        qe = t;
+    }
+}
+
+cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st) {
+    LMParams q = p;
+    void *args[] = {(void *)&q};
+    return cudaLaunchCooperativeKernel((const void *)lm_frontier_kernel, dim3(blocks),
+                                       dim3(kThreads), args, 0, st);
+}
+
+__global__ void fill_u32(uint32_t *p, uint32_t v, int64_t count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+cudaError_t launch_fill_counters(const Segment *hsegs, int nseg, uint32_t *cnt, int cnt_bytes,
+                                 cudaStream_t st) {
+    for (int s = 0; s < nseg; ++s) {
+        const Segment &sg = hsegs[s];
+        cudaError_t e;
+        if (cnt_bytes == 1) {
+            e = cudaMemsetAsync(reinterpret_cast<uint8_t *>(cnt) + sg.slot_off, sg.L,
+                                (size_t)sg.count_pad, st);
+        } else {
+            int b = (int)std::min<int64_t>((sg.count_pad + 255) / 256, 4096);
+            fill_u32<<<std::max(b, 1), 256, 0, st>>>(cnt + sg.slot_off, (uint32_t)sg.L, sg.count_pad);
+            e = cudaGetLastError();
+        }
+        if (e) return e;
+    }
+    return cudaSuccess;
+}
+
+__global__ void extract_model(const uint32_t *truth, int32_t n, unsigned long long *out) {
+    const int64_t nw = ((int64_t)n + 63) >> 6;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long v = (unsigned long long)truth[2 * w] |
+                               ((unsigned long long)truth[2 * w + 1] << 32);
+        const int64_t lo = w * 64;
+        if (lo + 64 > n) v &= (1ull << (uint32_t)(n - lo)) - 1ull;
+        out[w] = v;
+    }
+}
+
+cudaError_t launch_extract_model(const uint32_t *truth, int32_t n, unsigned long long *out,
+                                 cudaStream_t st) {
+    const int64_t nw = ((int64_t)n + 63) >> 6;
+    if (nw == 0) return cudaSuccess;
+    int b = (int)std::min<int64_t>((nw + 255) / 256, 4096);
+    extract_model<<<b, 256, 0, st>>>(truth, n, out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// stable models: bit-sliced guess matrix, 64 guesses per uint64 word
+// ------------------------------------------------------------------------------------
+
+__device__ __forceinline__ unsigned long long valid_word(int64_t w, int32_t W, int64_t G) {
+    if (w >= W) return 0ull;
+    const int64_t rem = G - w * 64;
+    return rem >= 64 ? ~0ull : ((1ull << rem) - 1ull);
+}
+
+// bit b of the result = bit i of the guess id 64*w + b
+__device__ __forceinline__ unsigned long long count_pattern(int i, int64_t w) {
+    switch (i) {
+        case 0: return 0xAAAAAAAAAAAAAAAAull;
+        case 1: return 0xCCCCCCCCCCCCCCCCull;
+        case 2: return 0xF0F0F0F0F0F0F0F0ull;
+        case 3: return 0xFF00FF00FF00FF00ull;
+        case 4: return 0xFFFF0000FFFF0000ull;
+        case 5: return 0xFFFFFFFF00000000ull;
+        default: return ((w >> (i - 6)) & 1) ? ~0ull : 0ull;
+    }
+}
+
+// Initial matrix M_0 (Def. 8): ⊤ and fact rows all ones (over the
+// valid guesses), abar rows from the guesses, every other row zero (memset before).
+__global__ void st_init_kernel(STParams p, int32_t n, int32_t k, const int32_t *negated_ext,
+                               const int32_t *free_rank, const unsigned long long *guesses,
+                               int32_t W, int64_t G, const int32_t *facts, int32_t nfacts,
+                               int32_t top, uint32_t *any_bits) {
+    const int64_t rows = 1 + (int64_t)nfacts + k;
+    const int64_t total = rows * p.Wp;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = x / p.Wp, w = x % p.Wp;
+        const unsigned long long valid = valid_word(w, W, G);
+        int32_t row;
+        unsigned long long v;
+        if (r == 0) {
+            row = top;
+            v = valid;
+        } else if (r <= nfacts) {
+            row = facts[r - 1];
+            v = valid;
+        } else {
+            const int32_t j = (int32_t)(r - 1 - nfacts);
+            row = negated_ext[j];
+            if (guesses) {
+                v = (w < W ? guesses[(int64_t)j * W + w] : 0ull) & valid;
+            } else {
+                const int32_t rank = free_rank[j];
+                v = rank < 0 ? 0ull : (count_pattern(rank, w) & valid);
+            }
+        }
+        p.T0[(int64_t)row * p.Wp + w] = v;
+        p.T1[(int64_t)row * p.Wp + w] = v;
+        if (v) {
+            const uint32_t g = (uint32_t)row >> p.any_shift;
+            atomicOr(any_bits + (g >> 5), 1u << (g & 31));
+        }
+    }
+}
+
+cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_t *negated_ext,
+                           const int32_t *free_rank, const unsigned long long *guesses,
+                           int32_t W, int64_t G, const int32_t *facts, int32_t nfacts,
+                           int32_t top, uint32_t *any_bits, cudaStream_t st) {
+    cudaError_t e;
+    const size_t tbytes = (size_t)p.n_ext * p.Wp * sizeof(unsigned long long);
+    if ((e = cudaMemsetAsync(p.T0, 0, tbytes, st))) return e;
+    if ((e = cudaMemsetAsync(p.T1, 0, tbytes, st))) return e;
+    if ((e = cudaMemsetAsync(any_bits, 0, sizeof(uint32_t) * (size_t)p.any_words, st))) return e;
+    if ((e = cudaMemsetAsync(p.mark, 0, sizeof(int32_t) * (size_t)p.n_ext, st))) return e;
+    if ((e = cudaMemsetAsync(p.tail, 0, sizeof(int32_t), st))) return e;
+    const int64_t total = (1 + (int64_t)nfacts + k) * p.Wp;
+    int b = (int)std::min<int64_t>((total + 255) / 256, 8192);
+    st_init_kernel<<<std::max(b, 1), 256, 0, st>>>(p, n, k, negated_ext, free_rank, guesses, W, G,
+                                                   facts, nfacts, top, any_bits);
+    return cudaGetLastError();
+}
+
+// One candidate AND-row, all guess words: acc = AND of the body rows of T_k; the new
+// bits (acc & ~T_k[head]) are ORed into T_{k+1}[head].  A warp owns the row, each lane
+// two words (one 16-byte load per body atom).
+__device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int64_t i,
+                                       const unsigned long long *rd, unsigned long long *wr,
+                                       int k, int lane) {
+    const int32_t h = __ldg(p.head + sg.slot_off + i);
+    bool changed = false;
+    for (int32_t w = 2 * lane; w < p.Wp; w += 64) {
+        ulonglong2 acc = make_ulonglong2(~0ull, ~0ull);
+        for (int32_t j = 0; j < sg.L; ++j) {
+            const int32_t a = __ldg(p.col + sg.col_off + (int64_t)j * sg.count_pad + i);
+            const ulonglong2 r = __ldcg(reinterpret_cast<const ulonglong2 *>(rd + (int64_t)a * p.Wp + w));
+            acc.x &= r.x;
+            acc.y &= r.y;
+            if (!(acc.x | acc.y)) break;
+        }
+        if (!(acc.x | acc.y)) continue;
+        const ulonglong2 hv = __ldcg(reinterpret_cast<const ulonglong2 *>(rd + (int64_t)h * p.Wp + w));
+        const unsigned long long nx = acc.x & ~hv.x, ny = acc.y & ~hv.y;
+        if (nx) { atomicOr(wr + (int64_t)h * p.Wp + w, nx); changed = true; }
+        if (ny) { atomicOr(wr + (int64_t)h * p.Wp + w + 1, ny); changed = true; }
+    }
+    if (__any_sync(0xFFFFFFFFu, changed) && lane == 0) {
+        if (atomicExch(p.mark + h, k + 1) != k + 1) {
+            const int32_t pos = atomicAdd(p.tail, 1);
+            p.order[pos] = h;
+        }
+    }
+}
+
+// Algorithm 2: M_{k+1} = θ(M_P M_k) over all guess columns at
+// once, until no word changes.  Shared memory holds one "any guess" bit per extended
+// atom; a row whose body has an atom false in every guess is skipped after the bit
+// test, so only candidate rows gather the 8·Wp-byte guess rows.
+__global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(STParams p) {
+    extern __shared__ uint32_t sm[];
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
+    for (int32_t w = tid; w < p.any_words; w += blockDim.x) sm[w] = __ldcg(p.any_init + w);
+    __syncthreads();
+    int32_t ds = 0, de = 0;
+    for (int k = 0;; ++k) {
+        const unsigned long long *rd = (k & 1) ? p.T1 : p.T0;
+        unsigned long long *wr = (k & 1) ? p.T0 : p.T1;
+        if (k > 0) {
+            const int64_t tot = (int64_t)(de - ds) * p.Wp;
+            for (int64_t x = gtid; x < tot; x += gthreads) {
+                const int32_t h = __ldcg(p.order + ds + x / p.Wp);
+                const int64_t off = (int64_t)h * p.Wp + x % p.Wp;
+                const unsigned long long v = __ldcg(rd + off);
+                if (v != __ldcg(wr + off)) atomicOr(wr + off, v);
+            }
+            for (int64_t i = ds + tid; i < de; i += blockDim.x) {
+                const uint32_t g = (uint32_t)__ldcg(p.order + i) >> p.any_shift;
+                atomicOr(sm + (g >> 5), 1u << (g & 31));
+            }
+            __syncthreads();
+        }
+        for (int32_t s = 0; s < p.nseg; ++s) {
+            const Segment sg = p.segs[s];
+            for (int64_t base = gwarp * 32; base < sg.count_pad; base += nwarps * 32) {
+                const int64_t i = base + lane;
+                bool cand = i < sg.count_pad;
+                for (int32_t j = 0; j < sg.L && cand; ++j)
+                    cand = sm_bit(sm, (uint32_t)__ldg(p.col + sg.col_off + (int64_t)j * sg.count_pad + i) >> p.any_shift);
+                unsigned m = __ballot_sync(0xFFFFFFFFu, cand);
+                while (m) {
+                    const int e = __ffs(m) - 1;
+                    m &= m - 1;
+                    st_row(p, sg, base + e, rd, wr, k, lane);
+                }
+            }
+        }
+        grid.sync();
+        const int32_t t = __ldcg(p.tail);
+        const bool lead = blockIdx.x == 0 && tid == 0;
+        if (t == de) {
+            if (lead) { *p.passes_out = k + 1; *p.status_out = 0; }
+            return;
+        }
+        if (k + 1 >= p.max_passes) {
+            if (lead) { *p.passes_out = k + 1; *p.status_out = 1; }
+            return;
+        }
+        ds = de;
+        de = t;
+    }
+}
+
+cudaError_t launch_st_fixpoint(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
+    STParams q = p;
+    void *args[] = {(void *)&q};
+    return cudaLaunchCooperativeKernel((const void *)st_fixpoint_kernel, dim3(blocks),
+                                       dim3(kThreads), args, smem, st);
+}
+
+// Algorithm 3 (reading R7): guess g is accepted iff for every negated
+// atom a_j, T[a_j] + T[abar_j] = 1 in column g, i.e. the XOR of the two rows is 1.
+__global__ void st_check_kernel(const unsigned long long *T, int32_t Wp, int32_t n, int32_t k,
+                                const int32_t *negated, int32_t W, int64_t G,
+                                unsigned long long *accepted, long long *n_accepted) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long ok = valid_word(w, W, G);
+        for (int32_t j = 0; j < k; ++j)
+            ok &= T[(int64_t)negated[j] * Wp + w] ^ T[(int64_t)(n + j) * Wp + w];
+        accepted[w] = ok;
+        if (ok) atomicAdd((unsigned long long *)n_accepted, (unsigned long long)__popcll(ok));
+    }
+}
+
+cudaError_t launch_st_check(const STParams &p, int32_t n, int32_t k, const int32_t *negated,
+                            int32_t W, int64_t G, unsigned long long *accepted,
+                            long long *n_accepted, cudaStream_t st) {
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(n_accepted, 0, sizeof(long long), st))) return e;
+    int b = (int)std::min<int64_t>((W + 255) / 256, 1024);
+    st_check_kernel<<<std::max(b, 1), 256, 0, st>>>(p.T0, p.Wp, n, k, negated, W, G, accepted,
+                                                    n_accepted);
+    return cudaGetLastError();
+}
+
+__global__ void st_column_kernel(const unsigned long long *T, int32_t Wp, int32_t n, int64_t g,
+                                 unsigned long long *out) {
+    const int64_t nw = ((int64_t)n + 63) >> 6;
+    const int64_t gw = g >> 6;
+    const int gb = (int)(g & 63);
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long v = 0;
+        for (int b = 0; b < 64; ++b) {
+            const int64_t a = w * 64 + b;
+            if (a >= n) break;
+            v |= ((T[a * Wp + gw] >> gb) & 1ull) << b;
+        }
+        out[w] = v;
+    }
+}
+
+cudaError_t launch_st_column(const STParams &p, int32_t n, int64_t g, unsigned long long *out,
+                             cudaStream_t st) {
+    const int64_t nw = ((int64_t)n + 63) >> 6;
+    if (nw == 0) return cudaSuccess;
+    int b = (int)std::min<int64_t>((nw + 255) / 256, 4096);
+    st_column_kernel<<<b, 256, 0, st>>>(p.T0, p.Wp, n, g, out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// occupancy
+// ------------------------------------------------------------------------------------
+
+cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
+    cudaError_t e;
+    const int cap = kMaxSmemBytes + 1024;
+    (void)lm_smem;
+    (void)st_smem;
+    if ((e = cudaFuncSetAttribute((const void *)lm_full_kernel<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, cap)))
+        return e;
+    if ((e = cudaFuncSetAttribute((const void *)lm_full_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, cap)))
+        return e;
+    if ((e = cudaFuncSetAttribute((const void *)st_fixpoint_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, cap)))
+        return e;
+    return cudaSuccess;
+}
+
+int lm_full_blocks_per_sm(bool exact, size_t smem) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &nb, exact ? (const void *)lm_full_kernel<true> : (const void *)lm_full_kernel<false>,
+        kThreads, smem);
+    return nb;
+}
+
+int lm_frontier_blocks_per_sm() {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)lm_frontier_kernel, kThreads, 0);
+    return nb;
+}
+
+int st_blocks_per_sm(size_t smem) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)st_fixpoint_kernel, kThreads, smem);
+    return nb;
+}
+
+}  // namespace lpb

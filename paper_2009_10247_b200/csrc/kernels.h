@@ -1,0 +1,95 @@
+// Kernel parameter blocks and launchers (kernels.cu), used by abi.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lp_internal.h"
+
+namespace lpb {
+
+constexpr int kThreads = 1024;          // persistent kernels: 32 warps per CTA
+constexpr int kMaxSmemBytes = 200 * 1024;
+
+// Least-model fixpoint (full θ-pass and frontier variants).
+struct LMParams {
+    const Segment *segs;
+    int32_t nseg;
+    int32_t n;                 // original atoms (stage / popcount range)
+    const int32_t *col;
+    const int32_t *head;
+    uint32_t *buf0;            // truth vector v_k (bit a of word a>>5); double buffer
+    uint32_t *buf1;
+    int32_t nwords;            // 32-bit words per truth buffer
+    // shared-memory copy of the truth vector: exact (shift 0) or a summary whose bit g
+    // is the OR of atoms [g << shift, (g+1) << shift)
+    const uint32_t *summary;   // initial summary (global), FILTER mode only
+    int32_t sm_words;
+    int32_t shift;
+    // derivation order list: initial atoms at [0, n0), then every atom in the pass /
+    // level it became true; tail = next free slot (device counter)
+    int32_t *order;
+    int32_t *tail;
+    int32_t *stage;            // optional [n]
+    int32_t *pops;             // optional [pop_cap]
+    int32_t pop_cap;
+    int32_t *iters_out;
+    int32_t *status_out;       // 0 ok, 1 not converged
+    int32_t max_passes;
+    // frontier variant
+    const int64_t *occ_ptr;
+    const int32_t *occ_slot;
+    uint32_t *cnt;             // per-slot remaining-body counters
+    int32_t cnt_bytes;         // 1: uint8 packed 4 per word; 4: uint32
+};
+
+// Batched (bit-sliced) stable-model fixpoint.
+struct STParams {
+    const Segment *segs;
+    int32_t nseg;
+    int32_t n_ext;
+    const int32_t *col;
+    const int32_t *head;
+    unsigned long long *T0;    // [n_ext][Wp] words, double buffer
+    unsigned long long *T1;
+    int32_t Wp;                // words per row (even)
+    const uint32_t *any_init;  // bit g: some row of atoms [g<<any_shift, (g+1)<<any_shift)
+    int32_t any_words;         //        is nonzero in T_0 (a superset filter)
+    int32_t any_shift;
+    int32_t *order;            // rows changed per pass
+    int32_t *tail;
+    int32_t *mark;             // [n_ext] pass tag of the last push
+    int32_t *passes_out;
+    int32_t *status_out;
+    int32_t max_passes;
+};
+
+// ---- launchers (return cudaError_t of the launch) -----------------------------------
+cudaError_t launch_lm_init(const LMParams &p, const uint32_t *v0_words32, int32_t v0_words,
+                           const int32_t *facts, int32_t nfacts, int32_t top, uint32_t *summary,
+                           int32_t sum_words, int blocks, cudaStream_t st);
+cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st);
+cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st);
+cudaError_t launch_fill_counters(const Segment *hsegs, int nseg, uint32_t *cnt, int cnt_bytes,
+                                 cudaStream_t st);
+cudaError_t launch_extract_model(const uint32_t *truth, int32_t n, unsigned long long *out,
+                                 cudaStream_t st);
+
+cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_t *negated_ext,
+                           const int32_t *free_rank, const unsigned long long *guesses,
+                           int32_t W, int64_t G, const int32_t *facts, int32_t nfacts,
+                           int32_t top, uint32_t *any_bits, cudaStream_t st);
+cudaError_t launch_st_fixpoint(const STParams &p, int blocks, size_t smem, cudaStream_t st);
+cudaError_t launch_st_check(const STParams &p, int32_t n, int32_t k, const int32_t *negated,
+                            int32_t W, int64_t G, unsigned long long *accepted,
+                            long long *n_accepted, cudaStream_t st);
+cudaError_t launch_st_column(const STParams &p, int32_t n, int64_t g, unsigned long long *out,
+                             cudaStream_t st);
+
+// occupancy helpers
+int lm_full_blocks_per_sm(bool exact, size_t smem);
+int lm_frontier_blocks_per_sm();
+int st_blocks_per_sm(size_t smem);
+cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem);
+
+}  // namespace lpb

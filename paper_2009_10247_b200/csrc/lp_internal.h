@@ -1,0 +1,60 @@
+// Internal structures shared by the host encoder (encode.cpp), the kernels
+// (kernels.cu) and the ABI glue (abi.cu).  Not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/lp.h"
+
+namespace lpb {
+
+// One body-length bucket of AND-rows.
+// Rule slot i (0 <= i < count_pad) of the segment has body atoms
+//   col[col_off + j * count_pad + i]   for j = 0..L-1    (position-major, coalesced)
+// and head head[slot_off + i].  Slots count..count_pad-1 are padding rules whose body
+// is the always-false atom ⊥ and whose head is ⊥ (they never fire).
+struct Segment {
+    int32_t L;
+    int32_t pad_;
+    int64_t count;
+    int64_t count_pad;   // multiple of 4 (int4 loads of 4 rules per position)
+    int64_t col_off;     // in int32 elements, multiple of 4
+    int64_t slot_off;    // in rule slots, multiple of 4
+};
+
+// Host-side result of standardisation + encoding.
+struct HostLayout {
+    int32_t n = 0;        // original atoms
+    int32_t k = 0;        // negated atoms (abar_j = n + j)
+    int32_t f = 0;        // free negated atoms (not facts)
+    int32_t top = 0;      // ⊤ = n + k  (always true; body of every fact)
+    int32_t bot = 0;      // ⊥ = n + k + 1 (always false; padding)
+    int32_t n_ext = 0;    // n + k + 2
+    int64_t n_rules = 0;
+    int64_t nnz = 0;      // real body entries (after dedupe, facts count 1 for ⊤)
+    int64_t n_heads = 0;
+    int64_t n_prime_paper = 0;
+    int32_t max_body = 0;
+    double sparsity_eq5 = 1.0;
+    bool definite = true;
+
+    std::vector<Segment> segs;
+    std::vector<int32_t> col;       // all segments, position-major
+    std::vector<int32_t> head;      // per slot
+    int64_t n_slots = 0;
+
+    std::vector<int32_t> facts;     // distinct original atoms with a fact rule
+    std::vector<int32_t> negated;   // k ascending atom ids
+    std::vector<int32_t> free_j;    // indices j of the free negated atoms (ascending)
+
+    // transposed occurrence lists over extended atoms (frontier variant)
+    bool has_occ = false;
+    std::vector<int64_t> occ_ptr;   // [n_ext + 1]
+    std::vector<int32_t> occ_slot;  // [nnz]
+};
+
+// encode.cpp
+lp_status encode(const lp_rules *r, bool build_occ, HostLayout *out, std::string *err);
+
+}  // namespace lpb

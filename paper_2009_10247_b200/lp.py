@@ -1,0 +1,355 @@
+"""Thin ctypes binding of include/lp.h (argument marshalling only).
+
+Every step of the hot path runs in liblp_b200.so's CUDA kernels; this module only
+converts numpy / torch buffers to pointers.  There is no CPU fallback: if the shared
+library is missing or no GPU is present, the calls raise.
+
+Names follow the C ABI: lp_load, lp_info, lp_negated_atoms, lp_least_model,
+lp_stable_models, lp_stable_matrix, lp_guess_model, lp_free.  ``Program`` wraps a
+handle with the same operations.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblp_b200.so")
+
+LP_OK, LP_E_INVALID, LP_E_PARSE, LP_E_SEMANTIC, LP_E_CAP = 0, 1, 2, 3, 4
+LP_E_NOMEM, LP_E_CUDA, LP_E_NOT_CONVERGED, LP_E_NODEVICE = 5, 6, 7, 8
+LP_LOAD_NO_FRONTIER = 0x1
+LP_PTR_DEVICE = 0x1
+LP_FRONTIER = 0x2
+
+_P = ctypes.c_void_p
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+
+
+class lp_rules(ctypes.Structure):
+    _fields_ = [("n_atoms", ctypes.c_int32), ("n_rules", ctypes.c_int64), ("head", _P),
+                ("body_ptr", _P), ("body_atom", _P), ("body_neg", _P)]
+
+
+class lp_options(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("guess_cap", ctypes.c_int), ("flags", ctypes.c_uint32),
+                ("smem_bits_cap", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
+                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", _P)]
+
+
+class lp_run(ctypes.Structure):
+    _fields_ = [("stream", _P), ("flags", ctypes.c_uint32), ("popcounts_out", _P),
+                ("popcounts_cap", ctypes.c_int32), ("stage_out", _P), ("ev_begin", _P),
+                ("ev_end", _P)]
+
+
+class lp_info_t(ctypes.Structure):
+    _fields_ = [("n_atoms", ctypes.c_int32), ("n_rules", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("n_heads", ctypes.c_int64), ("n_negated", ctypes.c_int32),
+                ("n_free_negated", ctypes.c_int32), ("max_body", ctypes.c_int32),
+                ("n_segments", ctypes.c_int32), ("n_prime_paper", ctypes.c_int64),
+                ("sparsity_eq5", ctypes.c_double), ("device_bytes", ctypes.c_int64),
+                ("pass_bytes", ctypes.c_int64), ("truth_mode", ctypes.c_int32),
+                ("summary_shift", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
+                ("block_threads", ctypes.c_int32)]
+
+
+SYMBOLS = ("lp_load", "lp_info", "lp_negated_atoms", "lp_least_model", "lp_stable_models",
+           "lp_stable_matrix", "lp_guess_model", "lp_free", "lp_status_str", "lp_last_error")
+
+_lib = None
+
+
+def library():
+    """Load liblp_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (nvcc, sm_100a); there is no CPU fallback")
+        lib = ctypes.CDLL(LIB_PATH)
+        st = ctypes.c_int
+        lib.lp_load.argtypes = [ctypes.POINTER(lp_rules), ctypes.POINTER(lp_options), ctypes.POINTER(_P)]
+        lib.lp_load.restype = st
+        lib.lp_info.argtypes = [_P, ctypes.POINTER(lp_info_t)]
+        lib.lp_info.restype = st
+        lib.lp_negated_atoms.argtypes = [_P, _P]
+        lib.lp_negated_atoms.restype = st
+        lib.lp_least_model.argtypes = [_P, _P, _P, _P, ctypes.POINTER(lp_run)]
+        lib.lp_least_model.restype = st
+        lib.lp_stable_models.argtypes = [_P, _P, ctypes.c_int64, _P, _P, _P, ctypes.POINTER(lp_run)]
+        lib.lp_stable_models.restype = st
+        lib.lp_stable_matrix.argtypes = [_P, _P, ctypes.POINTER(lp_run)]
+        lib.lp_stable_matrix.restype = st
+        lib.lp_guess_model.argtypes = [_P, ctypes.c_int64, _P, ctypes.POINTER(lp_run)]
+        lib.lp_guess_model.restype = st
+        lib.lp_free.argtypes = [_P]
+        lib.lp_free.restype = None
+        lib.lp_status_str.argtypes = [st]
+        lib.lp_status_str.restype = ctypes.c_char_p
+        lib.lp_last_error.argtypes = []
+        lib.lp_last_error.restype = ctypes.c_char_p
+        _lib = lib
+    return _lib
+
+
+class LPError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        lib = library()
+        self.status = status
+        msg = lib.lp_status_str(status).decode()
+        detail = lib.lp_last_error().decode()
+        super().__init__(f"{where}: {msg} ({status}): {detail}")
+
+
+def _check(status: int, where: str):
+    if status != LP_OK:
+        raise LPError(status, where)
+
+
+def _ptr(a) -> Optional[int]:
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return int(a.data_ptr())  # torch tensor
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)
+
+
+def _event_ptr(ev) -> Optional[int]:
+    if ev is None:
+        return None
+    if isinstance(ev, int):
+        return ev
+    if int(ev.cuda_event) == 0:   # torch creates its cudaEvent_t lazily on first record
+        ev.record()
+    return int(ev.cuda_event)
+
+
+def _torch_allocator(device: int):
+    import torch
+
+    def _alloc(nbytes, ctx):
+        try:
+            return int(torch.cuda.caching_allocator_alloc(int(nbytes), device=device))
+        except Exception:  # noqa: BLE001 -- reported to C as NULL -> LP_E_NOMEM
+            return None
+
+    def _free(ptr, nbytes, ctx):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    return ALLOC_FN(_alloc), FREE_FN(_free)
+
+
+def bits_words(n: int) -> int:
+    return (n + 63) // 64
+
+
+class Program:
+    """A loaded program (lp_program handle)."""
+
+    def __init__(self, rules, device: int = 0, guess_cap: int = 20, frontier: bool = True,
+                 smem_bits_cap: int = 0, grid_blocks: int = 0, allocator: str = "torch"):
+        lib = library()
+        self._keep = []
+        head = np.ascontiguousarray(rules.head, dtype=np.int32)
+        ptr = np.ascontiguousarray(rules.body_ptr, dtype=np.int64)
+        atom = np.ascontiguousarray(rules.body_atom, dtype=np.int32)
+        neg = None if rules.body_neg is None else np.ascontiguousarray(rules.body_neg, dtype=np.uint8)
+        r = lp_rules(int(rules.n_atoms), int(head.shape[0]), _ptr(head), _ptr(ptr), _ptr(atom), _ptr(neg))
+        opt = lp_options()
+        opt.device = int(device)
+        opt.guess_cap = int(guess_cap)
+        opt.flags = 0 if frontier else LP_LOAD_NO_FRONTIER
+        opt.smem_bits_cap = int(smem_bits_cap)
+        opt.grid_blocks = int(grid_blocks)
+        if device >= 0 and allocator == "torch":
+            a, f = _torch_allocator(device)
+            opt.alloc, opt.free = a, f
+            self._keep += [a, f]
+        h = _P()
+        _check(lib.lp_load(ctypes.byref(r), ctypes.byref(opt), ctypes.byref(h)), "lp_load")
+        self._h = h
+        self.device = device
+        self.n_atoms = int(rules.n_atoms)
+        self.info = lp_info(self)
+
+    # -- lifetime --------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            library().lp_free(self._h)
+            self._h = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- calls -----------------------------------------------------------------------
+    def negated_atoms(self):
+        return lp_negated_atoms(self)
+
+    def least_model(self, v0=None, frontier: bool = False, popcounts: bool = False,
+                    stages: bool = False, stream=None):
+        """Host-buffer call.  v0: None, a bool mask [n], or an id list.  Returns
+        (model uint64[ceil(n/64)], iters, dict(popcounts=..., stage=...))."""
+        n = self.n_atoms
+        v0w = None
+        if v0 is not None:
+            a = np.asarray(v0)
+            mask = np.zeros(n, dtype=bool)
+            if a.dtype == bool:
+                mask[:] = a
+            elif a.size:
+                mask[a.astype(np.int64)] = True
+            v0w = pack_mask(mask)
+        model = np.zeros(max(bits_words(n), 1), dtype=np.uint64)
+        pops = np.zeros(n + 3, dtype=np.int32) if popcounts else None
+        stage = np.zeros(max(n, 1), dtype=np.int32) if stages else None
+        iters = lp_least_model(self, v0w, model, frontier=frontier, pops=pops, stage=stage,
+                               stream=stream)
+        extra = {}
+        if popcounts:
+            extra["popcounts"] = pops[:iters].tolist()
+        if stages:
+            extra["stage"] = stage[:n]
+        return model[:bits_words(n)], iters, extra
+
+    def stable_models(self, guesses=None, n_guesses: int = 0, stream=None):
+        """Host-buffer call.  guesses: None or uint64[k][W].  Returns
+        (accepted guess ids (np.int64), passes, accepted mask words)."""
+        if guesses is None:
+            G = 1 << self.info["n_free_negated"]
+        else:
+            G = int(n_guesses)
+        W = (G + 63) // 64
+        acc = np.zeros(max(W, 1), dtype=np.uint64)
+        nacc, passes = lp_stable_models(self, guesses, G, acc, stream=stream)
+        bits = np.unpackbits(acc[:W].view(np.uint8), bitorder="little")[:G]
+        ids = np.nonzero(bits)[0].astype(np.int64)
+        assert ids.size == nacc
+        return ids, passes, acc[:W]
+
+    def stable_matrix(self, stream=None):
+        G = self._last_G
+        W = (G + 63) // 64
+        out = np.zeros((self.n_atoms, W), dtype=np.uint64)
+        lp_stable_matrix(self, out, stream=stream)
+        return out
+
+    def guess_model(self, g: int, stream=None):
+        out = np.zeros(max(bits_words(self.n_atoms), 1), dtype=np.uint64)
+        lp_guess_model(self, g, out, stream=stream)
+        return out[:bits_words(self.n_atoms)]
+
+
+def pack_mask(mask) -> np.ndarray:
+    m = np.asarray(mask, dtype=np.uint8)
+    n = m.shape[0]
+    w = bits_words(n)
+    padded = np.zeros(max(w, 1) * 64, dtype=np.uint8)
+    padded[:n] = m
+    return np.packbits(padded, bitorder="little").view(np.uint64).copy()
+
+
+def unpack_bits(words, n: int) -> np.ndarray:
+    return np.unpackbits(np.asarray(words, dtype=np.uint64).view(np.uint8), bitorder="little")[:n]
+
+
+# ---- module-level functions with the C names ----------------------------------------
+
+def lp_load(rules, **kw) -> Program:
+    return Program(rules, **kw)
+
+
+def lp_info(p: Program) -> dict:
+    info = lp_info_t()
+    _check(library().lp_info(p.handle, ctypes.byref(info)), "lp_info")
+    return {name: getattr(info, name) for name, _ in lp_info_t._fields_}
+
+
+def lp_negated_atoms(p: Program):
+    k = p.info["n_negated"]
+    out = np.zeros(max(k, 1), dtype=np.int32)
+    _check(library().lp_negated_atoms(p.handle, _ptr(out)), "lp_negated_atoms")
+    return out[:k].tolist()
+
+
+def _run(stream=None, flags=0, pops=None, stage=None, ev_begin=None, ev_end=None):
+    r = lp_run()
+    r.stream = _stream_ptr(stream)
+    r.flags = flags
+    r.popcounts_out = _ptr(pops)
+    r.popcounts_cap = 0 if pops is None else int(pops.shape[0] if hasattr(pops, "shape") else len(pops))
+    r.stage_out = _ptr(stage)
+    r.ev_begin = _event_ptr(ev_begin)
+    r.ev_end = _event_ptr(ev_end)
+    return r
+
+
+def lp_least_model(p: Program, v0, model_out, frontier=False, pops=None, stage=None, stream=None,
+                   device_ptrs=False, iters_out=None, ev_begin=None, ev_end=None):
+    """Marshals lp_least_model.  Host mode (default): numpy buffers, returns iters.
+    device_ptrs=True: torch CUDA tensors (v0 int64 words or None, model_out int64
+    words, iters_out int32[1], optional pops/stage), asynchronous on ``stream``."""
+    flags = (LP_FRONTIER if frontier else 0) | (LP_PTR_DEVICE if device_ptrs else 0)
+    run = _run(stream, flags, pops, stage, ev_begin, ev_end)
+    if device_ptrs:
+        _check(library().lp_least_model(p.handle, _ptr(v0), _ptr(model_out), _ptr(iters_out),
+                                         ctypes.byref(run)), "lp_least_model")
+        return None
+    it = ctypes.c_int32(0)
+    _check(library().lp_least_model(p.handle, _ptr(v0), _ptr(model_out), ctypes.addressof(it),
+                                     ctypes.byref(run)), "lp_least_model")
+    return it.value
+
+
+def lp_stable_models(p: Program, guesses, n_guesses, accepted_out, stream=None, device_ptrs=False,
+                     n_accepted_out=None, passes_out=None, ev_begin=None, ev_end=None):
+    flags = LP_PTR_DEVICE if device_ptrs else 0
+    run = _run(stream, flags, ev_begin=ev_begin, ev_end=ev_end)
+    g = None
+    if guesses is not None:
+        g = guesses if device_ptrs else np.ascontiguousarray(guesses, dtype=np.uint64)
+    p._last_G = int(n_guesses) if guesses is not None else (1 << p.info["n_free_negated"])
+    if device_ptrs:
+        _check(library().lp_stable_models(p.handle, _ptr(g), int(n_guesses), _ptr(accepted_out),
+                                           _ptr(n_accepted_out), _ptr(passes_out), ctypes.byref(run)),
+               "lp_stable_models")
+        return None
+    na = ctypes.c_int64(0)
+    ps = ctypes.c_int32(0)
+    _check(library().lp_stable_models(p.handle, _ptr(g), int(n_guesses), _ptr(accepted_out),
+                                       ctypes.addressof(na), ctypes.addressof(ps), ctypes.byref(run)),
+           "lp_stable_models")
+    return na.value, ps.value
+
+
+def lp_stable_matrix(p: Program, out, stream=None, device_ptrs=False):
+    run = _run(stream, LP_PTR_DEVICE if device_ptrs else 0)
+    _check(library().lp_stable_matrix(p.handle, _ptr(out), ctypes.byref(run)), "lp_stable_matrix")
+
+
+def lp_guess_model(p: Program, g, out, stream=None, device_ptrs=False):
+    run = _run(stream, LP_PTR_DEVICE if device_ptrs else 0)
+    _check(library().lp_guess_model(p.handle, int(g), _ptr(out), ctypes.byref(run)), "lp_guess_model")
+
+
+def lp_free(p: Program):
+    p.close()

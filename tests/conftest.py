@@ -17,3 +17,9 @@ def pytest_configure(config):
 def _build_oracle():
     import oracle
     oracle.build()
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _build_library():
+    from paper_2009_10247_b200 import build
+    build.build()

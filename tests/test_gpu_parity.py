@@ -1,0 +1,257 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle -- bit-exact models,
+identical pass counts, popcount traces and stages, identical accepted guesses and
+whole fixpoint matrices.  Every GPU output is also checked by the oracle's
+certificate checker (O-CERT)."""
+import numpy as np
+import pytest
+
+import lpgen
+import oracle
+from paper_2009_10247_b200 import lp
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device (these tests run on the B200 box)")
+
+
+def _oracle_lm(P, v0=None):
+    model, stage, iters = oracle.lm_stage(P, v0=v0)
+    return oracle.pack_bits(model), stage, iters, oracle.popcounts_from_stage(stage, iters)
+
+
+def check_lm(P, v0=None, prog=None, variants=(False, True), jacobi=False, **kw):
+    om, ostage, oit, opops = _oracle_lm(P, v0)
+    if jacobi:
+        jm, jit, jpops, conv = oracle.lm_jacobi(P, v0=v0)
+        assert conv and jit == oit and jpops == opops and (oracle.pack_bits(jm) == om).all()
+    prog = prog or lp.Program(P, **kw)
+    for frontier in variants:
+        model, iters, ex = prog.least_model(v0, frontier=frontier, popcounts=True, stages=True)
+        tag = "frontier" if frontier else "full"
+        assert iters == oit, (tag, iters, oit)
+        assert (model == om).all(), tag
+        assert ex["popcounts"] == opops, tag
+        assert (ex["stage"] == ostage).all(), tag
+        m8 = lp.unpack_bits(model, P.n_atoms)
+        assert oracle.certify(P, v0, m8, ex["stage"], iters) == 0, tag
+    return prog
+
+
+# ---------------------------------------------------------------------------------
+# least model: small programs, edge cases
+# ---------------------------------------------------------------------------------
+
+def test_example1_and_degenerate():
+    P = lpgen.from_lists(5, [(0, [1, 2]), (0, [3, 4]), (2, [3]), (1, [4]), (3, []), (4, [])])
+    check_lm(P, jacobi=True)
+    for Q in [lpgen.from_lists(0, []), lpgen.from_lists(5, []),
+              lpgen.from_lists(4, [(1, []), (3, []), (3, [])]),
+              lpgen.from_lists(2, [(0, [0]), (1, [0])]),
+              lpgen.from_lists(2, [(0, []), (0, [1]), (1, [0, 0])]),
+              lpgen.from_lists(1, [(0, [])]), lpgen.from_lists(1, [(0, [0])])]:
+        check_lm(Q, jacobi=True)
+
+
+@pytest.mark.parametrize("L", [1, 2, 33, 64, 65, 1000, 4097])
+def test_chain_gpu(L):
+    check_lm(lpgen.chain(L), jacobi=True)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_programs(seed):
+    rng = np.random.default_rng([seed, 5150])
+    n = int(rng.integers(1, 400))
+    R = int(rng.integers(0, 5 * n))
+    P = lpgen.random_program(rng, n, R, max_len=int(rng.integers(1, 13)))
+    prog = check_lm(P, jacobi=True)
+    v0 = rng.choice(n, size=int(rng.integers(0, n // 4 + 1)), replace=False).tolist()
+    check_lm(P, v0=v0, prog=prog, jacobi=True)
+
+
+@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("cfg", [dict(smem_bits_cap=128), dict(smem_bits_cap=1024, grid_blocks=3),
+                                 dict(grid_blocks=1)])
+def test_forced_summary_mode_and_small_grids(seed, cfg):
+    """FILTER mode (summary in shared memory, exact test in L2) and tiny grids."""
+    rng = np.random.default_rng([seed, 99])
+    n = int(rng.integers(1200, 3000))
+    P = lpgen.random_program(rng, n, 4 * n, max_len=6, n_facts=n // 20)
+    prog = check_lm(P, **cfg)
+    if cfg.get("smem_bits_cap"):
+        assert prog.info["truth_mode"] == 1 and prog.info["summary_shift"] >= 1
+
+
+def test_long_bodies_generic_path_and_u32_counters():
+    rng = np.random.default_rng(7)
+    n = 3000
+    rules = [(int(rng.integers(0, n)), rng.choice(n, size=int(rng.integers(9, 40)), replace=False).tolist())
+             for _ in range(2000)]
+    rules += [(a, []) for a in rng.choice(n, size=1500, replace=False).tolist()]
+    rules += [(1, list(range(2, 602)))]            # a 600-atom body: 32-bit counters
+    rules += [(0, [1] + list(range(2, 300)))]
+    P = lpgen.from_lists(n, rules)
+    prog = check_lm(P, jacobi=True)
+    assert prog.info["max_body"] == 600
+    check_lm(P, jacobi=True, smem_bits_cap=256)
+
+
+def test_ragged_sizes():
+    """n and R that are not multiples of 4 / 32 / 64, bits at word edges."""
+    for n in (31, 32, 33, 63, 64, 65, 127, 129):
+        rules = [(i + 1, [i]) for i in range(n - 1)] + [(0, [])]
+        rules += [(n - 1, [0, n // 2])]
+        check_lm(lpgen.from_lists(n, rules), jacobi=True)
+        check_lm(lpgen.from_lists(n, rules), v0=[n - 1], jacobi=True)
+
+
+def test_layered_deep_recursion_small():
+    P = lpgen.layered(300, 16, 300 * 16 * 4, 3, seed=4)
+    prog = check_lm(P, jacobi=True)
+    check_lm(P, variants=(False,), smem_bits_cap=128)
+
+
+def test_transitive_closure_gpu():
+    rng = np.random.default_rng(3)
+    for V in (2, 17, 45):
+        edges = lpgen.random_digraph(rng, V, 3 * V, self_loops=True)
+        check_lm(lpgen.tc_program(V, edges), jacobi=True)
+
+
+def test_semantic_error_on_normal_program():
+    P = lpgen.from_lists(2, [(0, [], [1])])
+    prog = lp.Program(P)
+    with pytest.raises(lp.LPError) as e:
+        prog.least_model()
+    assert e.value.status == lp.LP_E_SEMANTIC
+
+
+def test_device_pointer_mode_matches_host_mode():
+    import torch
+    rng = np.random.default_rng(11)
+    P = lpgen.random_program(rng, 5000, 20000, max_len=5, n_facts=200)
+    prog = lp.Program(P)
+    om, ostage, oit, opops = _oracle_lm(P)
+    s = torch.cuda.Stream()
+    W = lp.bits_words(P.n_atoms)
+    for frontier in (False, True):
+        model = torch.zeros(W, dtype=torch.int64, device="cuda")
+        iters = torch.zeros(1, dtype=torch.int32, device="cuda")
+        pops = torch.zeros(P.n_atoms + 2, dtype=torch.int32, device="cuda")
+        stage = torch.zeros(P.n_atoms, dtype=torch.int32, device="cuda")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        lp.lp_least_model(prog, None, model, frontier=frontier, pops=pops, stage=stage, stream=s,
+                          device_ptrs=True, iters_out=iters, ev_begin=e0, ev_end=e1)
+        s.synchronize()
+        assert int(iters.item()) == oit
+        assert (model.cpu().numpy().view(np.uint64) == om).all()
+        assert pops.cpu().numpy()[:oit].tolist() == opops
+        assert (stage.cpu().numpy() == ostage).all()
+        assert e0.elapsed_time(e1) > 0
+
+
+# ---------------------------------------------------------------------------------
+# least model: BASELINE.json configurations C1-C4 at full size
+# ---------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_config_parity(cfg):
+    P = lpgen.config(cfg)
+    check_lm(P, jacobi=(cfg != "C3"))
+
+
+@pytest.mark.slow
+def test_config_c4_parity():
+    P = lpgen.config("C4")
+    prog = check_lm(P)
+    assert prog.info["truth_mode"] == 1     # the 10M-atom truth vector is L2-resident
+
+
+# ---------------------------------------------------------------------------------
+# stable models
+# ---------------------------------------------------------------------------------
+
+def _oracle_matrix_bits(models, n, G):
+    """oracle per-guess models [G][words] -> bool [G][n]"""
+    return np.unpackbits(np.ascontiguousarray(models).view(np.uint8), axis=1, bitorder="little")[:, :n]
+
+
+def check_stable(P, guesses_u8=None, prog=None, chunk=8192, **kw):
+    """guesses_u8: None (all 2^f) or uint8[G][k] abar values."""
+    o = oracle.stable(P, guesses=guesses_u8, want_models=True)
+    prog = prog or lp.Program(P, **kw)
+    k = o["k"]
+    if guesses_u8 is None:
+        ids, passes, acc = prog.stable_models()
+        G = 1 << o["f"]
+    else:
+        g = np.asarray(guesses_u8, dtype=np.uint8).reshape(-1, k)
+        G = g.shape[0]
+        W = (G + 63) // 64
+        sliced = np.zeros((max(k, 1), W), dtype=np.uint64)
+        for j in range(k):
+            sliced[j] = lp.pack_mask(g[:, j].astype(bool))[:W]
+        ids, passes, acc = prog.stable_models(sliced[:k] if k else np.zeros((0, W), np.uint64), n_guesses=G)
+    assert ids.tolist() == np.nonzero(o["accepted"])[0].tolist()
+    assert passes == o["passes"]
+    M = prog.stable_matrix()                       # [n][W], bit g = guess g
+    n = P.n_atoms
+    for a0 in range(0, n, chunk):
+        a1 = min(n, a0 + chunk)
+        dev = np.unpackbits(M[a0:a1].view(np.uint8), axis=1, bitorder="little")[:, :G]
+        ora = np.unpackbits(np.ascontiguousarray(o["models"]).view(np.uint8), axis=1,
+                            bitorder="little")[:, a0:a1]
+        assert (dev == ora.T).all()
+    for g in list(ids[:3]) + [0, G - 1]:
+        gm = prog.guess_model(int(g))
+        assert (gm == o["models"][g]).all()
+    return prog, o
+
+
+def test_stable_examples():
+    ex2 = lpgen.from_lists(6, [(0, [1, 2]), (1, [0, 3]), (2, [], [3]), (3, []), (4, [5])])
+    check_stable(ex2)
+    check_stable(ex2, guesses_u8=[[0], [1]])
+    two = lpgen.from_lists(2, [(0, [], [1]), (1, [], [0])])
+    _, o = check_stable(two)
+    assert np.nonzero(o["accepted"])[0].tolist() == [1, 2]
+    check_stable(lpgen.from_lists(1, [(0, [], [0])]))
+    check_stable(lpgen.from_lists(3, [(0, [1]), (1, []), (2, [0, 1])]))       # definite, k = 0
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_normal_programs(seed):
+    rng = np.random.default_rng([seed, 4242])
+    n = int(rng.integers(1, 200))
+    P = lpgen.random_normal_program(rng, n, 3 * n, max_len=4, k_max=9)
+    prog, o = check_stable(P)
+    k = o["k"]
+    if k:
+        G = int(rng.integers(1, 200))
+        g = rng.integers(0, 2, size=(G, k)).astype(np.uint8)
+        check_stable(P, guesses_u8=g, prog=prog)
+
+
+def test_stable_summary_filter_mode():
+    rng = np.random.default_rng(8)
+    P = lpgen.random_normal_program(rng, 3000, 9000, max_len=4, k_max=7, n_facts=100)
+    check_stable(P, smem_bits_cap=256, grid_blocks=5)
+
+
+def test_guess_cap():
+    rules = [(i, [], [i + 1]) for i in range(0, 44, 2)]
+    P = lpgen.from_lists(46, rules)
+    prog = lp.Program(P, guess_cap=20)
+    with pytest.raises(lp.LPError) as e:
+        prog.stable_models()
+    assert e.value.status == lp.LP_E_CAP
+
+
+def test_config_c5_parity():
+    P = lpgen.config("C5")
+    prog, o = check_stable(P)
+    assert prog.info["n_negated"] == 12
