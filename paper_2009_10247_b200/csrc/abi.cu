@@ -48,6 +48,8 @@ struct lp_program {
     int32_t sm_words = 0, shift = 0;
     bool exact = true;
     int32_t *d_order = nullptr;
+    int32_t *d_qbuf = nullptr;  // FILTER-mode candidate queues, [lm_blocks][qcap]
+    int32_t qcap = 0;
     int32_t *d_scal = nullptr;  // [0] tail [1] iters [2] status [3] passes [4,5] n_accepted
     int32_t *d_facts = nullptr;
     int32_t nfacts = 0;
@@ -211,6 +213,15 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     p->grid_cap = (opt && opt->grid_blocks > 0) ? opt->grid_blocks : 0;
     auto cap_grid = [&](int b) { return p->grid_cap > 0 ? std::min(b, p->grid_cap) : b; };
     p->lm_blocks = cap_grid(sms * bl);
+    if (!p->exact) {
+        // a CTA handles at most 4 * kThreads * ceil(nq / gthreads) slots per segment, so
+        // its queue never overflows (an overflow would still be verified inline)
+        const int64_t gthreads = (int64_t)p->lm_blocks * kThreads;
+        int64_t cap = 0;
+        for (const Segment &sg : L.segs) cap += 4 * (int64_t)kThreads * (((sg.count_pad >> 2) + gthreads - 1) / gthreads);
+        p->qcap = (int32_t)std::min<int64_t>(std::max<int64_t>(cap, 1024), 1 << 26);
+        TRY(dalloc(p, &p->d_qbuf, (size_t)p->lm_blocks * p->qcap));
+    }
     p->fr_blocks = cap_grid(sms * bf);
     p->st_blocks = cap_grid(sms * bs);
     CK(cudaDeviceSynchronize());
@@ -387,6 +398,9 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.occ_slot = p->d_occ_slot;
     q.cnt = p->d_cnt;
     q.cnt_bytes = p->cnt_bytes;
+    q.dbg = debug_timing();
+    q.qbuf = p->d_qbuf;
+    q.qcap = p->qcap;
 
     CK(launch_lm_init(q, v0d, (int32_t)(mw * 2), p->d_facts, p->nfacts, L.top,
                       p->exact ? nullptr : p->d_summary, p->exact ? 0 : p->sm_words,
@@ -574,3 +588,8 @@ extern "C" const char *lp_status_str(lp_status s) {
 }
 
 extern "C" const char *lp_last_error(void) { return g_err.c_str(); }
+
+// Profiling hook, not part of include/lp.h: a device buffer of 16 passes x grid x 4
+// uint64 %globaltimer stamps per CTA (pass start, last warp done, CTA done, barrier
+// exit) filled by the next full θ-pass launch; NULL disables.
+extern "C" void lpdbg_set_timing(void *buf) { set_debug_timing((unsigned long long *)buf); }

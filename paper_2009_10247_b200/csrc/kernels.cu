@@ -35,6 +35,16 @@ __device__ __forceinline__ int4 ld_stream(const int4 *p) {
     return r;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+static unsigned long long *g_dbg = nullptr;
+void set_debug_timing(unsigned long long *buf) { g_dbg = buf; }
+unsigned long long *debug_timing() { return g_dbg; }
+
 __device__ __forceinline__ bool sm_bit(const uint32_t *sm, uint32_t x) {
     return (sm[x >> 5] >> (x & 31)) & 1u;
 }
@@ -130,6 +140,8 @@ struct PassCtx {
     const uint32_t *rd;  // v_k (global)
     uint32_t *wr;        // v_{k+1} (global)
     const uint32_t *sm;  // shared copy of v_k (EXACT) or of its summary
+    int32_t *qbuf;       // this CTA's candidate queue (global, FILTER mode)
+    int32_t *qcount;     // its fill counter (shared memory)
     int k;
 };
 
@@ -144,33 +156,69 @@ __device__ __forceinline__ unsigned test4(int4 a, unsigned fire, const uint32_t 
     return fire;
 }
 
-// Rows (slots i0..i0+3 of segment sg) that passed the shared-memory test.  In FILTER
-// mode the test was on the summary, so the exact bits are checked in v_k (L2).  A row
-// that fires ORs its head into v_{k+1}; the thread that sets a new bit appends the
-// head to the derivation list (this is the pass's "changed" signal).
-template <bool EXACT>
-__device__ __noinline__ void on_fire(const LMParams &p, const Segment &sg, int64_t i0,
-                                     unsigned fire, const PassCtx &c) {
+// OR a firing row's head into v_{k+1}; the thread that sets a new bit appends the head
+// to the derivation list (the pass's "changed" signal) and records its stage.
+__device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, int32_t h,
+                                          uint32_t cur_word) {
+    const uint32_t bit = 1u << (h & 31);
+    if (cur_word & bit) return;                            // already in v_k
+    const uint32_t old = atomicOr(c.wr + (h >> 5), bit);
+    if (old & bit) return;                                 // another row set it this pass
+    const int32_t pos = atomicAdd(p.tail, 1);
+    p.order[pos] = h;
+    if (p.stage) p.stage[h] = c.k + 1;
+}
+
+// EXACT mode: the shared-memory test is exact, so a passing row fires.
+__device__ __forceinline__ void fire_exact(const LMParams &p, const PassCtx &c, const Segment &sg,
+                                           int64_t i0, unsigned fire) {
+    int32_t h[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        h[e] = ((fire >> e) & 1u) ? __ldg(p.head + sg.slot_off + i0 + e) : 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        if ((fire >> e) & 1u) emit_head(p, c, h[e], c.sm[h[e] >> 5]);
+}
+
+// FILTER mode: exact test of one candidate row (global slot) against v_k in L2.
+__device__ __noinline__ void check_candidate(const LMParams &p, const PassCtx &c, int32_t slot) {
+    int lo = 0, hi = p.nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(&p.segs[mid].slot_off) <= slot) lo = mid; else hi = mid - 1;
+    }
+    const int32_t L = __ldg(&p.segs[lo].L);
+    const int64_t cp = __ldg(&p.segs[lo].count_pad);
+    const int32_t *colp = p.col + __ldg(&p.segs[lo].col_off) + (slot - __ldg(&p.segs[lo].slot_off));
+    const int32_t h = __ldg(p.head + slot);
+    bool ok = true;
+    for (int32_t j0 = 0; j0 < L && ok; j0 += 4) {
+        uint32_t a[4], w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[j] = j0 + j < L ? (uint32_t)__ldg(colp + (int64_t)(j0 + j) * cp) : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = j0 + j < L ? __ldcg(c.rd + (a[j] >> 5)) : ~0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ok = ok && ((w[j] >> (a[j] & 31)) & 1u);
+    }
+    if (ok) emit_head(p, c, h, __ldcg(c.rd + (h >> 5)));
+}
+
+// FILTER mode: rows that passed the summary test are queued and verified in the
+// pass epilogue with many independent L2 requests in flight, so the streaming loop
+// never waits on a dependent L2 round trip.
+__device__ __forceinline__ void enqueue(const LMParams &p, const PassCtx &c, int64_t slot0,
+                                        unsigned fire) {
+    const int cnt = __popc(fire);
+    int32_t pos = atomicAdd(c.qcount, cnt);
+#pragma unroll
     for (int e = 0; e < 4; ++e) {
         if (!((fire >> e) & 1u)) continue;
-        const int64_t i = i0 + e;
-        if (!EXACT) {
-            bool ok = true;
-            for (int32_t j = 0; j < sg.L && ok; ++j) {
-                const uint32_t a = (uint32_t)__ldg(p.col + sg.col_off + (int64_t)j * sg.count_pad + i);
-                ok = (__ldcg(c.rd + (a >> 5)) >> (a & 31)) & 1u;
-            }
-            if (!ok) continue;
-        }
-        const int32_t h = __ldg(p.head + sg.slot_off + i);
-        const uint32_t bit = 1u << (h & 31);
-        const uint32_t cur = EXACT ? c.sm[h >> 5] : __ldcg(c.rd + (h >> 5));
-        if (cur & bit) continue;                       // already in v_k
-        const uint32_t old = atomicOr(c.wr + (h >> 5), bit);
-        if (old & bit) continue;                       // another row set it this pass
-        const int32_t pos = atomicAdd(p.tail, 1);
-        p.order[pos] = h;
-        if (p.stage) p.stage[h] = c.k + 1;
+        const int32_t slot = (int32_t)(slot0 + e);
+        if (pos < p.qcap) c.qbuf[pos] = slot;
+        else check_candidate(p, c, slot);                  // queue full: verify inline
+        ++pos;
     }
 }
 
@@ -195,7 +243,10 @@ __device__ __forceinline__ void seg_pass(const LMParams &p, const Segment &sg, c
             unsigned fire = 0xFu;
 #pragma unroll
             for (int j = 0; j < L; ++j) fire = test4<EXACT>(v[u][j], fire, c.sm, p.shift);
-            if (fire) on_fire<EXACT>(p, sg, q * 4, fire, c);
+            if (fire) {
+                if (EXACT) fire_exact(p, c, sg, q * 4, fire);
+                else enqueue(p, c, sg.slot_off + q * 4, fire);
+            }
         }
     }
 }
@@ -209,7 +260,10 @@ __device__ void seg_pass_generic(const LMParams &p, const Segment &sg, const Pas
         unsigned fire = 0xFu;
 #pragma unroll 4
         for (int32_t j = 0; j < sg.L; ++j) fire = test4<EXACT>(ld_stream(base + j * nq + q), fire, c.sm, p.shift);
-        if (fire) on_fire<EXACT>(p, sg, q * 4, fire, c);
+        if (fire) {
+            if (EXACT) fire_exact(p, c, sg, q * 4, fire);
+            else enqueue(p, c, sg.slot_off + q * 4, fire);
+        }
     }
 }
 
@@ -238,6 +292,7 @@ __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c
 template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, 1) lm_full_kernel(LMParams p) {
     extern __shared__ uint32_t sm[];
+    __shared__ int32_t qcount;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
@@ -247,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_full_kernel(LMParams p) {
     for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(src0 + w);
     const int32_t n0 = __ldcg(p.tail);
     if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = n0;
+    if (tid == 0) qcount = 0;
     __syncthreads();
 
     int32_t ds = n0, de = n0;  // atoms that became true in the previous pass
@@ -271,9 +327,23 @@ __global__ void __launch_bounds__(kThreads, 1) lm_full_kernel(LMParams p) {
             }
             __syncthreads();
         }
-        const PassCtx c{rd, wr, sm, k};
+        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k};
+        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 0] = globaltimer();
         all_segments<EXACT>(p, c, gtid, gthreads);
+        if (!EXACT) {  // epilogue: verify this CTA's queued candidates
+            __syncthreads();
+            const int32_t nc = min(qcount, p.qcap);
+            __syncthreads();
+            if (tid == 0) qcount = 0;
+            for (int32_t i = tid; i < nc; i += blockDim.x) check_candidate(p, c, __ldcg(c.qbuf + i));
+        }
+        if (p.dbg && k < 16) {
+            if ((tid & 31) == 0) atomicMax(p.dbg + (k * gridDim.x + blockIdx.x) * 4 + 1, globaltimer());
+            __syncthreads();
+            if (tid == 0) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 2] = globaltimer();
+        }
         grid.sync();
+        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 3] = globaltimer();
         const int32_t t = __ldcg(p.tail);
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (t == de) {  // u = v: fixpoint

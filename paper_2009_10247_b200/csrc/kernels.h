@@ -41,7 +41,15 @@ struct LMParams {
     const int32_t *occ_slot;
     uint32_t *cnt;             // per-slot remaining-body counters
     int32_t cnt_bytes;         // 1: uint8 packed 4 per word; 4: uint32
+    unsigned long long *dbg;   // optional profiling timestamps (lpdbg_set_timing)
+    // FILTER mode: per-CTA candidate queues (rows that passed the summary test)
+    int32_t *qbuf;             // [grid][qcap]
+    int32_t qcap;
 };
+
+// profiling hook (not part of the ABI): per-CTA %globaltimer stamps
+void set_debug_timing(unsigned long long *buf);
+unsigned long long *debug_timing();
 
 // Batched (bit-sliced) stable-model fixpoint.
 struct STParams {
