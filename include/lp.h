@@ -75,6 +75,9 @@ typedef void *(*lp_alloc_fn)(size_t bytes, void *ctx);
 typedef void (*lp_free_fn)(void *ptr, size_t bytes, void *ctx);
 
 #define LP_LOAD_NO_FRONTIER 0x1u /* do not build the transposed occurrence lists */
+#define LP_LOAD_TMA 0x2u         /* use the TMA-pipelined full θ-pass (cp.async.bulk ring)
+                                    instead of the register-streaming one; same results,
+                                    slower on B200 for HBM-streaming programs */
 
 typedef struct {
     int device;             /* CUDA device ordinal; -1 = host-only handle: encode and
@@ -123,6 +126,8 @@ typedef struct {
     int32_t summary_shift;    /* atoms per summary bit = 1 << summary_shift            */
     int32_t grid_blocks;      /* CTAs of the persistent kernels                        */
     int32_t block_threads;
+    int32_t full_kernel;      /* 1: TMA-pipelined full θ-pass, 0: register-streaming   */
+    int32_t tma_stages;       /* depth of the TMA shared-memory ring                   */
 } lp_info_t;
 
 /* Validate, standardize and encode a program, upload it (PAPER.md:62, 82-95,

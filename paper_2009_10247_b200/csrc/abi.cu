@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -50,6 +51,11 @@ struct lp_program {
     int32_t *d_order = nullptr;
     int32_t *d_qbuf = nullptr;  // FILTER-mode candidate queues, [lm_blocks][qcap]
     int32_t qcap = 0;
+    bool use_tma = false;       // TMA-pipelined full pass (else the register-streaming one)
+    TileSeg *d_tsegs = nullptr;
+    int32_t ntseg = 0, stages = 0;
+    int64_t ntiles = 0;
+    size_t tma_smem = 0;
     int32_t *d_scal = nullptr;  // [0] tail [1] iters [2] status [3] passes [4,5] n_accepted
     int32_t *d_facts = nullptr;
     int32_t nfacts = 0;
@@ -171,7 +177,8 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     TRY(dalloc(p, &p->d_model, mw));
 
     // shared-memory plan: exact truth vector if it fits, else a summary
-    int64_t cap = kMaxSmemBytes;
+    // (leave room for a 2-stage TMA ring at least)
+    int64_t cap = std::min<int64_t>(kMaxSmemBytes, kSmemLimit - (int64_t)lm_tma_smem_bytes(0, 2) - 128);
     if (opt && opt->smem_bits_cap > 0) cap = std::min<int64_t>(cap, opt->smem_bits_cap / 8);
     cap = std::max<int64_t>(cap, 16);
     if ((int64_t)p->nwords * 4 <= cap) {
@@ -205,8 +212,39 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(dalloc(p, &p->d_mark, (size_t)L.n_ext));
     }
 
+    // TMA tile plan: every segment cut into 16 KB tiles of
+    // T rows; the head row is staged too when the truth test is exact
+    p->use_tma = (opt && (opt->flags & LP_LOAD_TMA)) && (int)L.segs.size() <= kMaxTileSegs;
+    if (p->use_tma) {
+        std::vector<TileSeg> ts;
+        int64_t toff = 0;
+        const int extra = p->exact ? 1 : 0;
+        for (const Segment &sg : L.segs) {
+            TileSeg t{};
+            t.L = sg.L;
+            t.T = (int32_t)((kStageBytes / (4 * (int64_t)(sg.L + extra))) & ~3LL);
+            if (t.T < 4) { p->use_tma = false; break; }
+            t.tile_off = toff;
+            t.col_off = sg.col_off;
+            t.count_pad = sg.count_pad;
+            t.slot_off = sg.slot_off;
+            toff += (sg.count_pad + t.T - 1) / t.T;
+            ts.push_back(t);
+        }
+        if (p->use_tma) {
+            p->ntiles = toff;
+            p->ntseg = (int32_t)ts.size();
+            TRY(upload(p, &p->d_tsegs, ts));
+            p->stages = (int32_t)std::min<int64_t>(
+                8, (kSmemLimit - (int64_t)lm_tma_smem_bytes(p->sm_words, 0)) / kStageBytes);
+            if (p->stages < 2) p->use_tma = false;
+            p->tma_smem = lm_tma_smem_bytes(p->sm_words, p->stages);
+        }
+    }
+
     CK(prepare_kernels(p->lm_smem, p->st_smem));
-    const int bl = lm_full_blocks_per_sm(p->exact, p->lm_smem);
+    const int bl = p->use_tma ? lm_tma_blocks_per_sm(p->exact, p->tma_smem)
+                              : lm_full_blocks_per_sm(p->exact, p->lm_smem);
     const int bf = lm_frontier_blocks_per_sm();
     const int bs = st_blocks_per_sm(p->st_smem);
     if (bl < 1 || bf < 1 || bs < 1) return set_err(LP_E_CUDA, "persistent kernels do not fit on an SM");
@@ -218,7 +256,10 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         // its queue never overflows (an overflow would still be verified inline)
         const int64_t gthreads = (int64_t)p->lm_blocks * kThreads;
         int64_t cap = 0;
-        for (const Segment &sg : L.segs) cap += 4 * (int64_t)kThreads * (((sg.count_pad >> 2) + gthreads - 1) / gthreads);
+        if (p->use_tma)  // a CTA consumes at most ceil(ntiles / grid) tiles of <= 4096 rows
+            cap = (p->ntiles + p->lm_blocks - 1) / p->lm_blocks * (kStageBytes / 4);
+        else
+            for (const Segment &sg : L.segs) cap += 4 * (int64_t)kThreads * (((sg.count_pad >> 2) + gthreads - 1) / gthreads);
         p->qcap = (int32_t)std::min<int64_t>(std::max<int64_t>(cap, 1024), 1 << 26);
         TRY(dalloc(p, &p->d_qbuf, (size_t)p->lm_blocks * p->qcap));
     }
@@ -312,6 +353,8 @@ extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
     o->truth_mode = p->exact ? 0 : 1;
     o->summary_shift = p->shift;
     o->grid_blocks = p->lm_blocks;
+    o->full_kernel = p->use_tma ? 1 : 0;
+    o->tma_stages = p->stages;
     o->block_threads = p->threads;
     return LP_OK;
 }
@@ -401,6 +444,12 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.dbg = debug_timing();
     q.qbuf = p->d_qbuf;
     q.qcap = p->qcap;
+    q.tsegs = p->d_tsegs;
+    q.ntseg = p->ntseg;
+    q.stages = p->stages;
+    q.ntiles = p->ntiles;
+    q.heads_staged = p->exact ? 1 : 0;
+    q.tma_variant = std::getenv("LP_TMA_VARIANT") ? std::atoi(std::getenv("LP_TMA_VARIANT")) : 0;
 
     CK(launch_lm_init(q, v0d, (int32_t)(mw * 2), p->d_facts, p->nfacts, L.top,
                       p->exact ? nullptr : p->d_summary, p->exact ? 0 : p->sm_words,
@@ -408,6 +457,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     if (frontier) CK(launch_fill_counters(L.segs.data(), (int)L.segs.size(), p->d_cnt, p->cnt_bytes, st));
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
     if (frontier) CK(launch_lm_frontier(q, p->fr_blocks, st));
+    else if (p->use_tma) CK(launch_lm_tma(q, p->exact, p->lm_blocks, p->tma_smem, st));
     else CK(launch_lm_full(q, p->exact, p->lm_blocks, p->lm_smem, st));
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
     unsigned long long *mout = dev ? reinterpret_cast<unsigned long long *>(model_out) : p->d_model;

@@ -169,17 +169,6 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
     if (p.stage) p.stage[h] = c.k + 1;
 }
 
-// EXACT mode: the shared-memory test is exact, so a passing row fires.
-__device__ __forceinline__ void fire_exact(const LMParams &p, const PassCtx &c, const Segment &sg,
-                                           int64_t i0, unsigned fire) {
-    int32_t h[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-        h[e] = ((fire >> e) & 1u) ? __ldg(p.head + sg.slot_off + i0 + e) : 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-        if ((fire >> e) & 1u) emit_head(p, c, h[e], c.sm[h[e] >> 5]);
-}
 
 // FILTER mode: exact test of one candidate row (global slot) against v_k in L2.
 __device__ __noinline__ void check_candidate(const LMParams &p, const PassCtx &c, int32_t slot) {
@@ -222,19 +211,35 @@ __device__ __forceinline__ void enqueue(const LMParams &p, const PassCtx &c, int
     }
 }
 
+// EXACT mode: the shared-memory test is exact, so a passing row fires; its head comes
+// from the head row streamed together with the body positions (no dependent load).
+__device__ __forceinline__ void fire_exact4(const LMParams &p, const PassCtx &c, int4 h,
+                                            unsigned fire) {
+    if (fire & 1u) emit_head(p, c, h.x, c.sm[h.x >> 5]);
+    if (fire & 2u) emit_head(p, c, h.y, c.sm[h.y >> 5]);
+    if (fire & 4u) emit_head(p, c, h.z, c.sm[h.z >> 5]);
+    if (fire & 8u) emit_head(p, c, h.w, c.sm[h.w >> 5]);
+}
+
+// One body-length segment, 4 AND-rows per thread per int4 load, U quads in flight.
+// FILTER mode streams the L body rows (heads are read only for verified candidates);
+// EXACT mode streams the head row as well.
 template <int L, int U, bool EXACT>
 __device__ __forceinline__ void seg_pass(const LMParams &p, const Segment &sg, const PassCtx &c,
                                          int64_t gtid, int64_t gthreads) {
     const int64_t nq = sg.count_pad >> 2;
     const int4 *base = reinterpret_cast<const int4 *>(p.col + sg.col_off);
+    const int4 *hbase = reinterpret_cast<const int4 *>(p.head + sg.slot_off);
     for (int64_t q0 = gtid; q0 < nq; q0 += gthreads * U) {
         int4 v[U][L];
+        int4 hv[EXACT ? U : 1];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t q = q0 + u * gthreads;
 #pragma unroll
             for (int j = 0; j < L; ++j)
                 v[u][j] = q < nq ? ld_stream(base + j * nq + q) : make_int4(0, 0, 0, 0);
+            if (EXACT) hv[EXACT ? u : 0] = q < nq ? ld_stream(hbase + q) : make_int4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -244,7 +249,7 @@ __device__ __forceinline__ void seg_pass(const LMParams &p, const Segment &sg, c
 #pragma unroll
             for (int j = 0; j < L; ++j) fire = test4<EXACT>(v[u][j], fire, c.sm, p.shift);
             if (fire) {
-                if (EXACT) fire_exact(p, c, sg, q * 4, fire);
+                if (EXACT) fire_exact4(p, c, hv[EXACT ? u : 0], fire);
                 else enqueue(p, c, sg.slot_off + q * 4, fire);
             }
         }
@@ -256,12 +261,14 @@ __device__ void seg_pass_generic(const LMParams &p, const Segment &sg, const Pas
                                  int64_t gtid, int64_t gthreads) {
     const int64_t nq = sg.count_pad >> 2;
     const int4 *base = reinterpret_cast<const int4 *>(p.col + sg.col_off);
+    const int4 *hbase = reinterpret_cast<const int4 *>(p.head + sg.slot_off);
     for (int64_t q = gtid; q < nq; q += gthreads) {
+        const int4 hv = EXACT ? ld_stream(hbase + q) : make_int4(0, 0, 0, 0);
         unsigned fire = 0xFu;
 #pragma unroll 4
         for (int32_t j = 0; j < sg.L; ++j) fire = test4<EXACT>(ld_stream(base + j * nq + q), fire, c.sm, p.shift);
         if (fire) {
-            if (EXACT) fire_exact(p, c, sg, q * 4, fire);
+            if (EXACT) fire_exact4(p, c, hv, fire);
             else enqueue(p, c, sg.slot_off + q * 4, fire);
         }
     }
@@ -270,18 +277,24 @@ __device__ void seg_pass_generic(const LMParams &p, const Segment &sg, const Pas
 template <bool EXACT>
 __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c, int64_t gtid,
                                              int64_t gthreads) {
+    // segment s starts at the thread after the one that took the last quad of segment
+    // s-1, so short segments spread over the whole grid instead of piling onto the
+    // lowest thread ids
+    int64_t off = 0;
     for (int32_t s = 0; s < p.nseg; ++s) {
         const Segment sg = p.segs[s];
+        const int64_t gt = gtid >= off ? gtid - off : gtid - off + gthreads;
+        off = (off + (sg.count_pad >> 2)) % gthreads;
         switch (sg.L) {
-            case 1: seg_pass<1, 4, EXACT>(p, sg, c, gtid, gthreads); break;
-            case 2: seg_pass<2, 4, EXACT>(p, sg, c, gtid, gthreads); break;
-            case 3: seg_pass<3, 2, EXACT>(p, sg, c, gtid, gthreads); break;
-            case 4: seg_pass<4, 2, EXACT>(p, sg, c, gtid, gthreads); break;
-            case 5: seg_pass<5, 1, EXACT>(p, sg, c, gtid, gthreads); break;
-            case 6: seg_pass<6, 1, EXACT>(p, sg, c, gtid, gthreads); break;
-            case 7: seg_pass<7, 1, EXACT>(p, sg, c, gtid, gthreads); break;
-            case 8: seg_pass<8, 1, EXACT>(p, sg, c, gtid, gthreads); break;
-            default: seg_pass_generic<EXACT>(p, sg, c, gtid, gthreads); break;
+            case 1: seg_pass<1, 4, EXACT>(p, sg, c, gt, gthreads); break;
+            case 2: seg_pass<2, EXACT ? 2 : 4, EXACT>(p, sg, c, gt, gthreads); break;
+            case 3: seg_pass<3, 2, EXACT>(p, sg, c, gt, gthreads); break;
+            case 4: seg_pass<4, EXACT ? 1 : 2, EXACT>(p, sg, c, gt, gthreads); break;
+            case 5: seg_pass<5, 1, EXACT>(p, sg, c, gt, gthreads); break;
+            case 6: seg_pass<6, 1, EXACT>(p, sg, c, gt, gthreads); break;
+            case 7: seg_pass<7, 1, EXACT>(p, sg, c, gt, gthreads); break;
+            case 8: seg_pass<8, 1, EXACT>(p, sg, c, gt, gthreads); break;
+            default: seg_pass_generic<EXACT>(p, sg, c, gt, gthreads); break;
         }
     }
 }
@@ -368,6 +381,274 @@ cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t sme
                                            dim3(kThreads), args, smem, st);
     return cudaLaunchCooperativeKernel((const void *)lm_full_kernel<false>, dim3(blocks),
                                        dim3(kThreads), args, smem, st);
+}
+
+// ------------------------------------------------------------------------------------
+// least model: fused θ-pass, TMA-pipelined (the dominant kernel on C4)
+// ------------------------------------------------------------------------------------
+//
+// Each CTA owns every gridDim.x-th 16 KB tile of the program matrix.  Thread 0 streams
+// tiles into an S-stage shared-memory ring with cp.async.bulk (TMA bulk copies, one per
+// body position row) completing on an mbarrier; all 32 warps consume a stage (one
+// AND-row per thread, conflict-free LDS of its body atoms, then the bit test against the
+// shared copy of v_k or its summary).  Because the program matrix is the same in every
+// pass, the producer keeps prefetching the next pass's first tiles across the grid
+// barrier, so HBM never idles while the pass is being closed.
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s_plain(void *dst, const void *src, uint32_t bytes,
+                                               uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ int find_tile_seg(const TileSeg *ts, int n, int64_t t) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ts[mid].tile_off <= t) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+size_t lm_tma_smem_bytes(int32_t sm_words, int32_t stages) {
+    const size_t a = ((size_t)sm_words * 4 + 127) / 128 * 128;
+    return a + (size_t)stages * kStageBytes + 16 * (size_t)stages + sizeof(TileSeg) * kMaxTileSegs + 16;
+}
+
+// local tile i of this CTA -> (segment, first row, rows)
+struct TileRef {
+    int seg;
+    int32_t rem;
+    int64_t start;
+};
+
+__device__ __forceinline__ TileRef tile_ref(const TileSeg *ts, int nseg, int64_t t) {
+    TileRef r;
+    r.seg = find_tile_seg(ts, nseg, t);
+    r.start = (t - ts[r.seg].tile_off) * ts[r.seg].T;
+    const int64_t left = ts[r.seg].count_pad - r.start;
+    r.rem = (int32_t)(left < ts[r.seg].T ? left : ts[r.seg].T);
+    return r;
+}
+
+constexpr int kConsumerWarps = kThreads / 32 - 1;   // warp 31 is the TMA producer
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(LMParams p) {
+    extern __shared__ __align__(128) uint8_t smraw[];
+    __shared__ int32_t qcount;
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const bool producer = warp == kConsumerWarps;
+    const int ctid = tid;                             // consumer thread id (< 992)
+    const int nct = kConsumerWarps * 32;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    const int S = p.stages;
+    uint32_t *sm = reinterpret_cast<uint32_t *>(smraw);
+    uint8_t *stage0 = smraw + ((size_t)p.sm_words * 4 + 127) / 128 * 128;
+    uint64_t *full = reinterpret_cast<uint64_t *>(stage0 + (size_t)S * kStageBytes);
+    uint64_t *empty = full + S;
+    TileSeg *ts = reinterpret_cast<TileSeg *>(empty + S);
+
+    const uint32_t *src0 = EXACT ? p.buf0 : p.summary;
+    for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(src0 + w);
+    for (int i = tid; i < p.ntseg; i += blockDim.x) ts[i] = p.tsegs[i];
+    const int32_t n0 = __ldcg(p.tail);
+    if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = n0;
+    if (tid == 0) {
+        qcount = 0;
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    const int64_t my_nt = p.ntiles > b ? (p.ntiles - b + G - 1) / G : 0;
+    const int64_t W = my_nt < S ? my_nt : S;          // tiles in flight
+    const int rows_extra = p.heads_staged;
+    uint64_t policy = 0;
+    uint64_t q_issue = 0;     // producer: ring positions issued since launch
+    uint64_t q_cons = 0;      // consumers: ring positions consumed since launch
+
+    // producer lane 0: stage local tile i into ring position q_issue
+    auto issue = [&](int64_t i) {
+        const int s = (int)(q_issue % (uint64_t)S);
+        if (q_issue >= (uint64_t)S) mbar_wait(empty + s, (uint32_t)((q_issue / S - 1) & 1));
+        const TileRef r = tile_ref(ts, p.ntseg, b + i * G);
+        const TileSeg &sg = ts[r.seg];
+        uint8_t *dst = stage0 + (size_t)s * kStageBytes;
+        mbar_expect_tx(full + s, (uint32_t)r.rem * 4u * (uint32_t)(sg.L + rows_extra));
+        const uint32_t chunk = (p.tma_variant & 2) ? 4096u : 0xFFFFFFFFu;
+        for (int32_t j = 0; j < sg.L + rows_extra; ++j) {
+            const int32_t *src = j < sg.L ? p.col + sg.col_off + (int64_t)j * sg.count_pad + r.start
+                                          : p.head + sg.slot_off + r.start;
+            uint8_t *d = dst + (size_t)j * sg.T * 4;
+            const uint32_t bytes = (uint32_t)r.rem * 4u;
+            for (uint32_t off = 0; off < bytes; off += chunk) {
+                const uint32_t nb = bytes - off < chunk ? bytes - off : chunk;
+                if (p.tma_variant & 1) bulk_g2s_plain(d + off, (const uint8_t *)src + off, nb, full + s);
+                else bulk_g2s(d + off, (const uint8_t *)src + off, nb, full + s, policy);
+            }
+        }
+        ++q_issue;
+    };
+    if (producer && lane == 0) {
+        policy = evict_first_policy();
+        for (int64_t i = 0; i < W; ++i) issue(i);     // first tiles of pass 0
+    }
+
+    int32_t ds = n0, de = n0;
+    for (int k = 0;; ++k) {
+        const uint32_t *rd = (k & 1) ? p.buf1 : p.buf0;
+        uint32_t *wr = (k & 1) ? p.buf0 : p.buf1;
+        if (k > 0) {
+            for (int64_t i = ds + gtid; i < de; i += gthreads) {
+                const int32_t a = __ldcg(p.order + i);
+                atomicOr(wr + (a >> 5), 1u << (a & 31));
+            }
+            if (EXACT && (de - ds) > (p.sm_words >> 2)) {
+                for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(rd + w);
+            } else {
+                for (int64_t i = ds + tid; i < de; i += blockDim.x) {
+                    const uint32_t a = (uint32_t)__ldcg(p.order + i);
+                    const uint32_t g = EXACT ? a : (a >> p.shift);
+                    atomicOr(sm + (g >> 5), 1u << (g & 31));
+                }
+            }
+            __syncthreads();
+        }
+        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k};
+        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 0] = globaltimer();
+        if (producer) {
+            if (lane == 0) {
+                // the rest of this pass, then the first W tiles of the next pass (the
+                // program matrix is the same in every pass)
+                for (int64_t i = W; i < my_nt; ++i) issue(i);
+                for (int64_t i = 0; i < W; ++i) issue(i);
+            }
+            __syncwarp();
+        } else {
+            for (int64_t i = 0; i < my_nt; ++i, ++q_cons) {
+                const int s = (int)(q_cons % (uint64_t)S);
+                mbar_wait(full + s, (uint32_t)((q_cons / S) & 1));
+                const TileRef r = tile_ref(ts, p.ntseg, b + i * G);
+                const TileSeg &sg = ts[r.seg];
+                const int32_t T = sg.T, L = sg.L;
+                const int32_t *tile = reinterpret_cast<const int32_t *>(stage0 + (size_t)s * kStageBytes);
+                for (int32_t row = ctid; row < r.rem; row += nct) {
+                    bool alive = true;
+                    for (int32_t j = 0; j < L && alive; ++j) {
+                        const uint32_t a = (uint32_t)tile[j * T + row];
+                        alive = sm_bit(sm, EXACT ? a : (a >> p.shift));
+                    }
+                    if (!alive) continue;
+                    if (EXACT) {
+                        const int32_t h = tile[L * T + row];
+                        emit_head(p, c, h, sm[h >> 5]);
+                    } else {
+                        const int32_t pos = atomicAdd(&qcount, 1);
+                        const int32_t slot = (int32_t)(sg.slot_off + r.start + row);
+                        if (pos < p.qcap) c.qbuf[pos] = slot;
+                        else check_candidate(p, c, slot);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(empty + s)) : "memory");
+            }
+        }
+        if (!EXACT) {  // epilogue: verify this CTA's queued candidates
+            __syncthreads();
+            const int32_t nc = min(qcount, p.qcap);
+            __syncthreads();
+            if (tid == 0) qcount = 0;
+            for (int32_t i = tid; i < nc; i += blockDim.x) check_candidate(p, c, __ldcg(c.qbuf + i));
+        }
+        if (p.dbg && k < 16) {
+            if ((tid & 31) == 0 && !producer) atomicMax(p.dbg + (k * gridDim.x + blockIdx.x) * 4 + 1, globaltimer());
+            __syncthreads();
+            if (tid == 0) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 2] = globaltimer();
+        }
+        grid.sync();
+        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 3] = globaltimer();
+        const int32_t t = __ldcg(p.tail);
+        const bool lead = blockIdx.x == 0 && tid == 0;
+        const bool done = (t == de) || (k + 1 >= p.max_passes);
+        if (done) {
+            if (lead) { *p.iters_out = k + 1; *p.status_out = (t == de) ? 0 : 1; }
+            // drain the prefetched tiles before the CTA's shared memory is released
+            if (!producer)
+                for (int64_t x = 0; x < W; ++x) {
+                    const uint64_t q = q_cons + (uint64_t)x;
+                    mbar_wait(full + (q % (uint64_t)S), (uint32_t)((q / S) & 1));
+                }
+            return;
+        }
+        if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
+        ds = de;
+        de = t;
+    }
+}
+
+
+cudaError_t launch_lm_tma(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st) {
+    LMParams q = p;
+    void *args[] = {(void *)&q};
+    if (exact)
+        return cudaLaunchCooperativeKernel((const void *)lm_tma_kernel<true>, dim3(blocks),
+                                           dim3(kThreads), args, smem, st);
+    return cudaLaunchCooperativeKernel((const void *)lm_tma_kernel<false>, dim3(blocks),
+                                       dim3(kThreads), args, smem, st);
+}
+
+int lm_tma_blocks_per_sm(bool exact, size_t smem) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &nb, exact ? (const void *)lm_tma_kernel<true> : (const void *)lm_tma_kernel<false>,
+        kThreads, smem);
+    return nb;
 }
 
 // ------------------------------------------------------------------------------------
@@ -625,9 +906,12 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(STParams p) {
             }
             __syncthreads();
         }
+        int64_t off = 0;  // rotate each segment's first warp (see all_segments)
         for (int32_t s = 0; s < p.nseg; ++s) {
             const Segment sg = p.segs[s];
-            for (int64_t base = gwarp * 32; base < sg.count_pad; base += nwarps * 32) {
+            const int64_t gw = gwarp >= off ? gwarp - off : gwarp - off + nwarps;
+            off = (off + (sg.count_pad + 31) / 32) % nwarps;
+            for (int64_t base = gw * 32; base < sg.count_pad; base += nwarps * 32) {
                 const int64_t i = base + lane;
                 bool cand = i < sg.count_pad;
                 for (int32_t j = 0; j < sg.L && cand; ++j)
@@ -729,6 +1013,12 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
         return e;
     if ((e = cudaFuncSetAttribute((const void *)lm_full_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, cap)))
+        return e;
+    if ((e = cudaFuncSetAttribute((const void *)lm_tma_kernel<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)))
+        return e;
+    if ((e = cudaFuncSetAttribute((const void *)lm_tma_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)))
         return e;
     if ((e = cudaFuncSetAttribute((const void *)st_fixpoint_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, cap)))

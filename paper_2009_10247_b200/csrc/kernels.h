@@ -11,6 +11,22 @@ namespace lpb {
 constexpr int kThreads = 1024;          // persistent kernels: 32 warps per CTA
 constexpr int kMaxSmemBytes = 200 * 1024;
 
+constexpr int kStageBytes = 16384;      // one TMA pipeline stage (bulk copies of col rows)
+constexpr int kSmemLimit = 232448 - 1024;  // opt-in smem per CTA on sm_100 minus static
+constexpr int kMaxTileSegs = 64;
+
+// A body-length segment cut into TMA tiles of T rows.  A tile stages R = L (+1 when the
+// head row is staged too) rows of T ints each: row j holds body position j of T
+// consecutive AND-rows, the extra row their heads.
+struct TileSeg {
+    int32_t L;
+    int32_t T;
+    int64_t tile_off;   // first global tile index of this segment
+    int64_t col_off;
+    int64_t count_pad;
+    int64_t slot_off;
+};
+
 // Least-model fixpoint (full θ-pass and frontier variants).
 struct LMParams {
     const Segment *segs;
@@ -45,6 +61,13 @@ struct LMParams {
     // FILTER mode: per-CTA candidate queues (rows that passed the summary test)
     int32_t *qbuf;             // [grid][qcap]
     int32_t qcap;
+    // TMA-pipelined full pass
+    const TileSeg *tsegs;
+    int32_t ntseg;
+    int32_t stages;            // pipeline depth S
+    int64_t ntiles;
+    int32_t heads_staged;      // 1: the head row is part of every tile (EXACT mode)
+    int32_t tma_variant;       // diagnostics (LP_TMA_VARIANT): 1 no L2 hint, 2 4 KB chunks
 };
 
 // profiling hook (not part of the ABI): per-CTA %globaltimer stamps
@@ -77,6 +100,9 @@ cudaError_t launch_lm_init(const LMParams &p, const uint32_t *v0_words32, int32_
                            const int32_t *facts, int32_t nfacts, int32_t top, uint32_t *summary,
                            int32_t sum_words, int blocks, cudaStream_t st);
 cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st);
+cudaError_t launch_lm_tma(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st);
+int lm_tma_blocks_per_sm(bool exact, size_t smem);
+size_t lm_tma_smem_bytes(int32_t sm_words, int32_t stages);
 cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st);
 cudaError_t launch_fill_counters(const Segment *hsegs, int nseg, uint32_t *cnt, int cnt_bytes,
                                  cudaStream_t st);

@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(_HERE, "liblp_b200.so")
 LP_OK, LP_E_INVALID, LP_E_PARSE, LP_E_SEMANTIC, LP_E_CAP = 0, 1, 2, 3, 4
 LP_E_NOMEM, LP_E_CUDA, LP_E_NOT_CONVERGED, LP_E_NODEVICE = 5, 6, 7, 8
 LP_LOAD_NO_FRONTIER = 0x1
+LP_LOAD_TMA = 0x2
 LP_PTR_DEVICE = 0x1
 LP_FRONTIER = 0x2
 
@@ -55,7 +56,8 @@ class lp_info_t(ctypes.Structure):
                 ("sparsity_eq5", ctypes.c_double), ("device_bytes", ctypes.c_int64),
                 ("pass_bytes", ctypes.c_int64), ("truth_mode", ctypes.c_int32),
                 ("summary_shift", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
-                ("block_threads", ctypes.c_int32)]
+                ("block_threads", ctypes.c_int32), ("full_kernel", ctypes.c_int32),
+                ("tma_stages", ctypes.c_int32)]
 
 
 SYMBOLS = ("lp_load", "lp_info", "lp_negated_atoms", "lp_least_model", "lp_stable_models",
@@ -160,7 +162,8 @@ class Program:
     """A loaded program (lp_program handle)."""
 
     def __init__(self, rules, device: int = 0, guess_cap: int = 20, frontier: bool = True,
-                 smem_bits_cap: int = 0, grid_blocks: int = 0, allocator: str = "torch"):
+                 smem_bits_cap: int = 0, grid_blocks: int = 0, allocator: str = "torch",
+                 tma: bool = False):
         lib = library()
         self._keep = []
         head = np.ascontiguousarray(rules.head, dtype=np.int32)
@@ -171,7 +174,7 @@ class Program:
         opt = lp_options()
         opt.device = int(device)
         opt.guess_cap = int(guess_cap)
-        opt.flags = 0 if frontier else LP_LOAD_NO_FRONTIER
+        opt.flags = (0 if frontier else LP_LOAD_NO_FRONTIER) | (LP_LOAD_TMA if tma else 0)
         opt.smem_bits_cap = int(smem_bits_cap)
         opt.grid_blocks = int(grid_blocks)
         if device >= 0 and allocator == "torch":

@@ -86,6 +86,19 @@ def test_forced_summary_mode_and_small_grids(seed, cfg):
         assert prog.info["truth_mode"] == 1 and prog.info["summary_shift"] >= 1
 
 
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("cfg", [dict(tma=True), dict(tma=True, smem_bits_cap=128),
+                                 dict(tma=True, smem_bits_cap=128, grid_blocks=2)])
+def test_tma_kernel_and_edge_grids(seed, cfg):
+    """The TMA-pipelined full θ-pass (LP_LOAD_TMA), exact and summary modes, including
+    more tiles than CTAs, gives the same results as the oracle."""
+    rng = np.random.default_rng([seed, 123])
+    n = int(rng.integers(1200, 6000))
+    P = lpgen.random_program(rng, n, 6 * n, max_len=9, n_facts=n // 30)
+    prog = check_lm(P, **cfg)
+    assert prog.info["full_kernel"] == 1
+
+
 def test_long_bodies_generic_path_and_u32_counters():
     rng = np.random.default_rng(7)
     n = 3000
