@@ -235,8 +235,18 @@ def main():
     hbm_peak, peak_src = _peaks()
     pass_bytes = int(info["pass_bytes"])
     achieved = pass_bytes * iters / (kms_max / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(args.workload)
+        if tr and tr["passes_per_launch"] == iters and info["truth_mode"] == 1:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:  # noqa: BLE001
+        traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                "frac": achieved / hbm_peak, "traffic": traffic,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, bytes per launch)",
+                "algorithmic_bytes_per_launch": pass_bytes * iters, "peak_source": peak_src,
                 "kernel": "lm_full_kernel<false> (persistent, all passes in one launch)",
                 "bytes_per_pass": pass_bytes, "passes_per_launch": iters,
                 "kernel_ms": kms_max}
