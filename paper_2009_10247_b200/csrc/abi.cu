@@ -450,7 +450,6 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.ntiles = p->ntiles;
     q.heads_staged = p->exact ? 1 : 0;
     q.tma_variant = std::getenv("LP_TMA_VARIANT") ? std::atoi(std::getenv("LP_TMA_VARIANT")) : 0;
-
     CK(launch_lm_init(q, v0d, (int32_t)(mw * 2), p->d_facts, p->nfacts, L.top,
                       p->exact ? nullptr : p->d_summary, p->exact ? 0 : p->sm_words,
                       p->sms, st));
@@ -473,6 +472,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
                                  cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     *iters_out = scal[1];
+    if (scal[2] == 2) return set_err(LP_E_CUDA, "internal: candidate queue overflow");
     if (scal[2] != 0) return set_err(LP_E_NOT_CONVERGED, "pass guard exceeded");
     return LP_OK;
 }

@@ -103,10 +103,11 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *
         int64_t l = pos - start;
         if (l > std::numeric_limits<int32_t>::max()) return fail(err, LP_E_INVALID, "body too long");
         len[i] = (int32_t)l;
-        int32_t Le = l == 0 ? 1 : (int32_t)l;   // a fact is the AND-row {⊤}
-        if (Le > maxL) maxL = Le;
+        if ((int32_t)l > maxL) maxL = (int32_t)l;
     }
     L->max_body = maxL;
+    int64_t n_fact_rules = 0;
+    for (int64_t i = 0; i < R; ++i) n_fact_rules += len[i] == 0;
 
     // ---- statistics ----------------------------------------------------------------
     {
@@ -123,8 +124,12 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *
     }
 
     // ---- segments by body length ---------------------------------------------------
+    // A fact is the AND-row {⊤} (reading R2).  Its head is put into v_0 by the init
+    // kernel and the row can never add anything after that, so it is not stored in the
+    // pass segments; nnz still counts its ⊤ entry.
     std::vector<int64_t> cnt((size_t)maxL + 1, 0);
-    for (int64_t i = 0; i < R; ++i) cnt[len[i] == 0 ? 1 : len[i]]++;
+    for (int64_t i = 0; i < R; ++i)
+        if (len[i]) cnt[len[i]]++;
     std::vector<int32_t> segof((size_t)maxL + 1, -1);
     int64_t col_off = 0, slot_off = 0, nnz = 0;
     for (int32_t l = 1; l <= maxL; ++l) {
@@ -143,7 +148,7 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *
     }
     if (slot_off > std::numeric_limits<int32_t>::max())
         return fail(err, LP_E_INVALID, "too many rules for int32 slots");
-    L->nnz = nnz;
+    L->nnz = nnz + n_fact_rules;
     L->n_slots = slot_off;
     L->col.assign((size_t)col_off, L->bot);
     L->head.assign((size_t)slot_off, L->bot);
@@ -151,15 +156,11 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *
     pos = 0;
     for (int64_t i = 0; i < R; ++i) {
         const int32_t l = len[i];
-        const int32_t le = l == 0 ? 1 : l;
-        const Segment &sg = L->segs[segof[le]];
-        const int64_t slot = fillc[segof[le]]++;
+        if (l == 0) continue;   // fact: its head is in v_0 already (row {⊤} never adds anything)
+        const Segment &sg = L->segs[segof[l]];
+        const int64_t slot = fillc[segof[l]]++;
         int32_t *c = L->col.data() + sg.col_off + slot;
-        if (l == 0) {
-            c[0] = L->top;
-        } else {
-            for (int32_t j = 0; j < l; ++j) c[(int64_t)j * sg.count_pad] = ext[pos + j];
-        }
+        for (int32_t j = 0; j < l; ++j) c[(int64_t)j * sg.count_pad] = ext[pos + j];
         pos += l;
         L->head[sg.slot_off + slot] = r->head[i];
     }
@@ -171,8 +172,7 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *
         for (const Segment &sg : L->segs)
             for (int32_t j = 0; j < sg.L; ++j) {
                 const int32_t *c = L->col.data() + sg.col_off + (int64_t)j * sg.count_pad;
-                for (int64_t i = 0; i < sg.count; ++i)
-                    if (c[i] != L->top) L->occ_ptr[c[i] + 1]++;
+                for (int64_t i = 0; i < sg.count; ++i) L->occ_ptr[c[i] + 1]++;
             }
         for (int32_t a = 0; a < L->n_ext; ++a) L->occ_ptr[a + 1] += L->occ_ptr[a];
         L->occ_slot.assign((size_t)std::max<int64_t>(L->occ_ptr[L->n_ext], 1), 0);
@@ -180,8 +180,7 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *
         for (const Segment &sg : L->segs)
             for (int32_t j = 0; j < sg.L; ++j) {
                 const int32_t *c = L->col.data() + sg.col_off + (int64_t)j * sg.count_pad;
-                for (int64_t i = 0; i < sg.count; ++i)
-                    if (c[i] != L->top) L->occ_slot[fo[c[i]]++] = (int32_t)(sg.slot_off + i);
+                for (int64_t i = 0; i < sg.count; ++i) L->occ_slot[fo[c[i]]++] = (int32_t)(sg.slot_off + i);
             }
     }
     return LP_OK;

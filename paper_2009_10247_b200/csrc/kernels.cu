@@ -114,6 +114,7 @@ cudaError_t launch_lm_init(const LMParams &p, const uint32_t *v0_words32, int32_
                            int32_t sum_words, int blocks, cudaStream_t st) {
     cudaError_t e;
     if ((e = cudaMemsetAsync(p.tail, 0, sizeof(int32_t), st))) return e;
+    if ((e = cudaMemsetAsync(p.status_out, 0, sizeof(int32_t), st))) return e;
     if (p.stage && p.n > 0)
         if ((e = cudaMemsetAsync(p.stage, 0xFF, sizeof(int32_t) * (size_t)p.n, st))) return e;
     if (summary && sum_words > 0)
@@ -197,18 +198,18 @@ __device__ __noinline__ void check_candidate(const LMParams &p, const PassCtx &c
 // FILTER mode: rows that passed the summary test are queued and verified in the
 // pass epilogue with many independent L2 requests in flight, so the streaming loop
 // never waits on a dependent L2 round trip.
-__device__ __forceinline__ void enqueue(const LMParams &p, const PassCtx &c, int64_t slot0,
+// (The host sizes qcap so that a CTA's queue can hold every row it streams in a pass;
+// an overflow is impossible by construction and would be reported as status 2.)
+__device__ __forceinline__ void enqueue(const LMParams &p, const PassCtx &c, int32_t slot0,
                                         unsigned fire) {
-    const int cnt = __popc(fire);
-    int32_t pos = atomicAdd(c.qcount, cnt);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        if (!((fire >> e) & 1u)) continue;
-        const int32_t slot = (int32_t)(slot0 + e);
-        if (pos < p.qcap) c.qbuf[pos] = slot;
-        else check_candidate(p, c, slot);                  // queue full: verify inline
-        ++pos;
+    int32_t pos = atomicAdd(c.qcount, __popc(fire));
+    if (pos + 4 > p.qcap) {
+        atomicExch(p.status_out, 2);
+        return;
     }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        if ((fire >> e) & 1u) c.qbuf[pos++] = slot0 + e;
 }
 
 // EXACT mode: the shared-memory test is exact, so a passing row fires; its head comes
@@ -226,31 +227,32 @@ __device__ __forceinline__ void fire_exact4(const LMParams &p, const PassCtx &c,
 // EXACT mode streams the head row as well.
 template <int L, int U, bool EXACT>
 __device__ __forceinline__ void seg_pass(const LMParams &p, const Segment &sg, const PassCtx &c,
-                                         int64_t gtid, int64_t gthreads) {
-    const int64_t nq = sg.count_pad >> 2;
+                                         int32_t gtid, int32_t gthreads) {
+    const int32_t nq = (int32_t)(sg.count_pad >> 2);   // slots < 2^31 (checked at load)
+    const int32_t slot0 = (int32_t)sg.slot_off;
     const int4 *base = reinterpret_cast<const int4 *>(p.col + sg.col_off);
     const int4 *hbase = reinterpret_cast<const int4 *>(p.head + sg.slot_off);
-    for (int64_t q0 = gtid; q0 < nq; q0 += gthreads * U) {
+    for (int32_t q0 = gtid; q0 < nq; q0 += gthreads * U) {
         int4 v[U][L];
         int4 hv[EXACT ? U : 1];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t q = q0 + u * gthreads;
+            const int32_t q = q0 + u * gthreads;
 #pragma unroll
             for (int j = 0; j < L; ++j)
-                v[u][j] = q < nq ? ld_stream(base + j * nq + q) : make_int4(0, 0, 0, 0);
+                v[u][j] = q < nq ? ld_stream(base + (int64_t)j * nq + q) : make_int4(0, 0, 0, 0);
             if (EXACT) hv[EXACT ? u : 0] = q < nq ? ld_stream(hbase + q) : make_int4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t q = q0 + u * gthreads;
+            const int32_t q = q0 + u * gthreads;
             if (q >= nq) break;
             unsigned fire = 0xFu;
 #pragma unroll
             for (int j = 0; j < L; ++j) fire = test4<EXACT>(v[u][j], fire, c.sm, p.shift);
             if (fire) {
                 if (EXACT) fire_exact4(p, c, hv[EXACT ? u : 0], fire);
-                else enqueue(p, c, sg.slot_off + q * 4, fire);
+                else enqueue(p, c, slot0 + q * 4, fire);
             }
         }
     }
@@ -258,18 +260,20 @@ __device__ __forceinline__ void seg_pass(const LMParams &p, const Segment &sg, c
 
 template <bool EXACT>
 __device__ void seg_pass_generic(const LMParams &p, const Segment &sg, const PassCtx &c,
-                                 int64_t gtid, int64_t gthreads) {
-    const int64_t nq = sg.count_pad >> 2;
+                                 int32_t gtid, int32_t gthreads) {
+    const int32_t nq = (int32_t)(sg.count_pad >> 2);
+    const int32_t slot0 = (int32_t)sg.slot_off;
     const int4 *base = reinterpret_cast<const int4 *>(p.col + sg.col_off);
     const int4 *hbase = reinterpret_cast<const int4 *>(p.head + sg.slot_off);
-    for (int64_t q = gtid; q < nq; q += gthreads) {
+    for (int32_t q = gtid; q < nq; q += gthreads) {
         const int4 hv = EXACT ? ld_stream(hbase + q) : make_int4(0, 0, 0, 0);
         unsigned fire = 0xFu;
 #pragma unroll 4
-        for (int32_t j = 0; j < sg.L; ++j) fire = test4<EXACT>(ld_stream(base + j * nq + q), fire, c.sm, p.shift);
+        for (int32_t j = 0; j < sg.L; ++j)
+            fire = test4<EXACT>(ld_stream(base + (int64_t)j * nq + q), fire, c.sm, p.shift);
         if (fire) {
             if (EXACT) fire_exact4(p, c, hv, fire);
-            else enqueue(p, c, sg.slot_off + q * 4, fire);
+            else enqueue(p, c, slot0 + q * 4, fire);
         }
     }
 }
@@ -280,11 +284,13 @@ __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c
     // segment s starts at the thread after the one that took the last quad of segment
     // s-1, so short segments spread over the whole grid instead of piling onto the
     // lowest thread ids
-    int64_t off = 0;
+    const int32_t gth = (int32_t)gthreads;
+    int32_t off = 0;
     for (int32_t s = 0; s < p.nseg; ++s) {
         const Segment sg = p.segs[s];
-        const int64_t gt = gtid >= off ? gtid - off : gtid - off + gthreads;
-        off = (off + (sg.count_pad >> 2)) % gthreads;
+        const int32_t gt = (int32_t)gtid >= off ? (int32_t)gtid - off : (int32_t)gtid - off + gth;
+        off = (int32_t)(((int64_t)off + (sg.count_pad >> 2)) % gth);
+        const int32_t gthreads = gth;
         switch (sg.L) {
             case 1: seg_pass<1, 4, EXACT>(p, sg, c, gt, gthreads); break;
             case 2: seg_pass<2, EXACT ? 2 : 4, EXACT>(p, sg, c, gt, gthreads); break;
@@ -360,12 +366,12 @@ __global__ void __launch_bounds__(kThreads, 1) lm_full_kernel(LMParams p) {
         const int32_t t = __ldcg(p.tail);
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (t == de) {  // u = v: fixpoint
-            if (lead) { *p.iters_out = k + 1; *p.status_out = 0; }
+            if (lead) { *p.iters_out = k + 1; }
             return;
         }
         if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
         if (k + 1 >= p.max_passes) {
-            if (lead) { *p.iters_out = k + 1; *p.status_out = 1; }
+            if (lead) { *p.iters_out = k + 1; atomicMax(p.status_out, 1); }
             return;
         }
         ds = de;
@@ -617,7 +623,10 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(LMParams p) {
         const bool lead = blockIdx.x == 0 && tid == 0;
         const bool done = (t == de) || (k + 1 >= p.max_passes);
         if (done) {
-            if (lead) { *p.iters_out = k + 1; *p.status_out = (t == de) ? 0 : 1; }
+            if (lead) {
+                *p.iters_out = k + 1;
+                if (t != de) atomicMax(p.status_out, 1);
+            }
             // drain the prefetched tiles before the CTA's shared memory is released
             if (!producer)
                 for (int64_t x = 0; x < W; ++x) {
@@ -698,12 +707,12 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(LMParams p) {
         const int32_t t = __ldcg(p.tail);
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (t == qe) {
-            if (lead) { *p.iters_out = k + 1; *p.status_out = 0; }
+            if (lead) { *p.iters_out = k + 1; }
             return;
         }
         if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
         if (k + 1 >= p.max_passes) {
-            if (lead) { *p.iters_out = k + 1; *p.status_out = 1; }
+            if (lead) { *p.iters_out = k + 1; atomicMax(p.status_out, 1); }
             return;
         }
         qs = qe;
@@ -836,6 +845,7 @@ cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_
     if ((e = cudaMemsetAsync(any_bits, 0, sizeof(uint32_t) * (size_t)p.any_words, st))) return e;
     if ((e = cudaMemsetAsync(p.mark, 0, sizeof(int32_t) * (size_t)p.n_ext, st))) return e;
     if ((e = cudaMemsetAsync(p.tail, 0, sizeof(int32_t), st))) return e;
+    if ((e = cudaMemsetAsync(p.status_out, 0, sizeof(int32_t), st))) return e;
     const int64_t total = (1 + (int64_t)nfacts + k) * p.Wp;
     int b = (int)std::min<int64_t>((total + 255) / 256, 8192);
     st_init_kernel<<<std::max(b, 1), 256, 0, st>>>(p, n, k, negated_ext, free_rank, guesses, W, G,
@@ -928,11 +938,11 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(STParams p) {
         const int32_t t = __ldcg(p.tail);
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (t == de) {
-            if (lead) { *p.passes_out = k + 1; *p.status_out = 0; }
+            if (lead) { *p.passes_out = k + 1; }
             return;
         }
         if (k + 1 >= p.max_passes) {
-            if (lead) { *p.passes_out = k + 1; *p.status_out = 1; }
+            if (lead) { *p.passes_out = k + 1; atomicMax(p.status_out, 1); }
             return;
         }
         ds = de;
