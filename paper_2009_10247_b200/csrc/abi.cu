@@ -56,7 +56,11 @@ struct lp_program {
     int32_t ntseg = 0, stages = 0;
     int64_t ntiles = 0;
     size_t tma_smem = 0;
-    int32_t *d_scal = nullptr;  // [0] tail [1] iters [2] status [3] passes [4,5] n_accepted
+    // [0] tail, [2] status (stable path); [1] iters; [3] passes; [4,5] n_accepted;
+    // [8,9] least-model tails and [10,11] statuses, alternating by call parity
+    int32_t *d_scal = nullptr;
+    uint32_t *d_factbits = nullptr;
+    uint64_t lm_runs = 0;
     int32_t *d_facts = nullptr;
     int32_t nfacts = 0;
     int32_t *d_negated = nullptr, *d_negated_ext = nullptr, *d_free_rank = nullptr;
@@ -172,6 +176,12 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     TRY(dalloc(p, &p->d_buf1, p->nwords));
     TRY(dalloc(p, &p->d_order, (size_t)L.n_ext + 1));
     TRY(dalloc(p, &p->d_scal, 16));
+    CK(cudaMemset(p->d_scal, 0, 16 * sizeof(int32_t)));
+    {
+        std::vector<uint32_t> fb((size_t)p->nwords, 0u);   // facts of P (Def. 4)
+        for (int32_t a : L.facts) fb[(size_t)a >> 5] |= 1u << (a & 31);
+        TRY(upload(p, &p->d_factbits, fb));
+    }
     const size_t mw = std::max<size_t>(((size_t)L.n + 63) / 64, 1);
     TRY(dalloc(p, &p->d_v0, mw));
     TRY(dalloc(p, &p->d_model, mw));
@@ -252,15 +262,17 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     auto cap_grid = [&](int b) { return p->grid_cap > 0 ? std::min(b, p->grid_cap) : b; };
     p->lm_blocks = cap_grid(sms * bl);
     if (!p->exact) {
-        // a CTA handles at most 4 * kThreads * ceil(nq / gthreads) slots per segment, so
-        // its queue never overflows (an overflow would still be verified inline)
-        const int64_t gthreads = (int64_t)p->lm_blocks * kThreads;
+        // a CTA handles at most 4 * threads * ceil(nq / gthreads) slots per segment, so
+        // its queue never overflows (an overflow is reported, never silently dropped)
+        const int64_t gthreads = (int64_t)p->lm_blocks * kFullThreads;
         int64_t cap = 0;
         if (p->use_tma)  // a CTA consumes at most ceil(ntiles / grid) tiles of <= 4096 rows
             cap = (p->ntiles + p->lm_blocks - 1) / p->lm_blocks * (kStageBytes / 4);
         else
-            for (const Segment &sg : L.segs) cap += 4 * (int64_t)kThreads * (((sg.count_pad >> 2) + gthreads - 1) / gthreads);
-        p->qcap = (int32_t)std::min<int64_t>(std::max<int64_t>(cap, 1024), 1 << 26);
+            for (const Segment &sg : L.segs)
+                cap += 4 * (int64_t)kFullThreads * (((sg.count_pad >> 2) + gthreads - 1) / gthreads);
+        if (cap + 4 > (1 << 28)) return set_err(LP_E_NOMEM, "candidate queue too large");
+        p->qcap = (int32_t)std::max<int64_t>(cap + 4, 1024);
         TRY(dalloc(p, &p->d_qbuf, (size_t)p->lm_blocks * p->qcap));
     }
     p->fr_blocks = cap_grid(sms * bf);
@@ -355,7 +367,7 @@ extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
     o->grid_blocks = p->lm_blocks;
     o->full_kernel = p->use_tma ? 1 : 0;
     o->tma_stages = p->stages;
-    o->block_threads = p->threads;
+    o->block_threads = p->use_tma ? kThreads : kFullThreads;
     return LP_OK;
 }
 
@@ -430,12 +442,23 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.sm_words = p->sm_words;
     q.shift = p->shift;
     q.order = p->d_order;
-    q.tail = p->d_scal + 0;
+    // run counters alternate between two slots: this call uses slot `par` (zeroed by
+    // the previous call or at load) and zeroes the other one for the next call
+    const int par = (int)(p->lm_runs & 1);
+    q.tail = p->d_scal + 8 + par;
+    q.tail_next = p->d_scal + 8 + (par ^ 1);
+    q.status_out = p->d_scal + 10 + par;
+    q.status_next = p->d_scal + 10 + (par ^ 1);
+    q.v0 = v0d;
+    q.v0_words = (int32_t)(mw * 2);
+    q.factbits = p->d_factbits;
+    q.top = L.top;
+    unsigned long long *mout = dev ? reinterpret_cast<unsigned long long *>(model_out) : p->d_model;
+    q.model_out = mout;
     q.stage = stage;
     q.pops = pops;
     q.pop_cap = pop_cap;
     q.iters_out = dev ? iters_out : p->d_scal + 1;
-    q.status_out = p->d_scal + 2;
     q.max_passes = L.n_ext + 2;
     q.occ_ptr = p->d_occ_ptr;
     q.occ_slot = p->d_occ_slot;
@@ -450,21 +473,17 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.ntiles = p->ntiles;
     q.heads_staged = p->exact ? 1 : 0;
     q.tma_variant = std::getenv("LP_TMA_VARIANT") ? std::atoi(std::getenv("LP_TMA_VARIANT")) : 0;
-    CK(launch_lm_init(q, v0d, (int32_t)(mw * 2), p->d_facts, p->nfacts, L.top,
-                      p->exact ? nullptr : p->d_summary, p->exact ? 0 : p->sm_words,
-                      p->sms, st));
-    if (frontier) CK(launch_fill_counters(L.segs.data(), (int)L.segs.size(), p->d_cnt, p->cnt_bytes, st));
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
     if (frontier) CK(launch_lm_frontier(q, p->fr_blocks, st));
     else if (p->use_tma) CK(launch_lm_tma(q, p->exact, p->lm_blocks, p->tma_smem, st));
     else CK(launch_lm_full(q, p->exact, p->lm_blocks, p->lm_smem, st));
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
-    unsigned long long *mout = dev ? reinterpret_cast<unsigned long long *>(model_out) : p->d_model;
-    CK(launch_extract_model(p->d_buf0, L.n, mout, st));
+    ++p->lm_runs;
     if (dev) return LP_OK;
 
     int32_t scal[3] = {0, 0, 0};
     CK(cudaMemcpyAsync(scal, p->d_scal, sizeof(scal), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(scal + 2, p->d_scal + 10 + par, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     if (mw) CK(cudaMemcpyAsync(model_out, p->d_model, mw * 8, cudaMemcpyDeviceToHost, st));
     if (stage) CK(cudaMemcpyAsync(run->stage_out, stage, sizeof(int32_t) * (size_t)L.n,
                                   cudaMemcpyDeviceToHost, st));

@@ -53,84 +53,73 @@ __device__ __forceinline__ bool sm_bit(const uint32_t *sm, uint32_t x) {
 // least model: initial vector
 // ------------------------------------------------------------------------------------
 
-__global__ void lm_init_words(uint32_t *buf0, uint32_t *buf1, int32_t nwords,
-                              const uint32_t *v0, int32_t v0_words, int32_t n, int32_t top) {
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords;
-         w += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t bits = 0;
-        const int64_t lo = w * 32;
-        if (v0 && w < v0_words && lo < n) {
-            bits = v0[w];
-            if (lo + 32 > n) bits &= (1u << (uint32_t)(n - lo)) - 1u;
-        }
-        if (w == (top >> 5)) bits |= 1u << (top & 31);
-        buf0[w] = bits;
-        buf1[w] = bits;
+// In-kernel prologue of every least-model kernel (no separate init launches):
+//   v_0 word w = (v0[w] restricted to original atoms) | facts[w] | ⊤,
+// written to both buffers; the thread that builds a word also lists its original atoms
+// into the derivation list, writes their stages (0, or -1 for false atoms) and, in
+// summary mode, ORs the word's groups into the summary word it owns.  Work item = one
+// summary word (2^shift truth words) in summary mode, one truth word otherwise, so no
+// two threads touch the same summary word and no grid barrier is needed inside.
+// Also zeroes the other-parity run counters for the next call.
+__device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, int64_t gtid,
+                                         int64_t gthreads) {
+    if (gtid == 0) {
+        *p.tail_next = 0;
+        *p.status_next = 0;
     }
-}
-
-__global__ void lm_init_facts(uint32_t *buf0, uint32_t *buf1, const int32_t *facts,
-                              int32_t nfacts) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nfacts;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t a = facts[i];
-        atomicOr(buf0 + (a >> 5), 1u << (a & 31));
-        atomicOr(buf1 + (a >> 5), 1u << (a & 31));
-    }
-}
-
-// List the initial atoms (original atoms of v_0) into the derivation order list, set
-// their stage to 0 and build the initial summary (FILTER mode).
-__global__ void lm_init_list(const uint32_t *buf0, int32_t n, int32_t top, int32_t *order,
-                             int32_t *tail, int32_t *stage, uint32_t *summary, int32_t shift) {
-    const int64_t nw = ((int64_t)n + 31) >> 5;
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (summary && tid == 0) {
-        const uint32_t g = (uint32_t)top >> shift;
-        atomicOr(summary + (g >> 5), 1u << (g & 31));
-    }
-    for (int64_t w = tid; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t bits = buf0[w];
-        const int64_t lo = w * 32;
-        if (lo + 32 > n) bits &= (1u << (uint32_t)(n - lo)) - 1u;
-        if (!bits) continue;
-        int32_t pos = atomicAdd(tail, __popc(bits));
-        while (bits) {
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int32_t a = (int32_t)(lo + b);
-            order[pos++] = a;
-            if (stage) stage[a] = 0;
-            if (summary) {
-                const uint32_t g = (uint32_t)a >> shift;
-                atomicOr(summary + (g >> 5), 1u << (g & 31));
+    const int wpi = summary_mode ? (1 << p.shift) : 1;     // truth words per item (shift <= 31)
+    const int64_t items = summary_mode ? p.sm_words : p.nwords;
+    for (int64_t it = gtid; it < items; it += gthreads) {
+        uint32_t sumw = 0;
+        for (int x = 0; x < wpi; ++x) {
+            const int64_t w = it * wpi + x;
+            if (w >= p.nwords) break;
+            const int64_t lo = w * 32;
+            uint32_t orig = p.factbits[w];
+            if (p.v0 && w < p.v0_words && lo < p.n) orig |= p.v0[w];
+            if (lo + 32 > p.n) orig &= lo >= p.n ? 0u : ((1u << (uint32_t)(p.n - lo)) - 1u);
+            uint32_t bits = orig;
+            if (w == (p.top >> 5)) bits |= 1u << (p.top & 31);
+            p.buf0[w] = bits;
+            p.buf1[w] = bits;
+            if (orig) {
+                int32_t pos = atomicAdd(p.tail, __popc(orig));
+                uint32_t b = orig;
+                while (b) {
+                    const int i = __ffs(b) - 1;
+                    b &= b - 1;
+                    p.order[pos++] = (int32_t)(lo + i);
+                }
+            }
+            if (p.stage && lo < p.n) {
+                const int m = (int)(p.n - lo < 32 ? p.n - lo : 32);
+                for (int i = 0; i < m; ++i) p.stage[lo + i] = ((orig >> i) & 1u) ? 0 : -1;
+            }
+            if (summary_mode && bits) {
+                if (p.shift >= 5) {
+                    sumw |= 1u << ((uint32_t)(lo >> p.shift) & 31u);
+                } else {
+                    const int gs = 1 << p.shift;
+                    const uint32_t gm = (gs == 32) ? ~0u : ((1u << gs) - 1u);
+                    for (int i = 0; i < 32 / gs; ++i)
+                        if ((bits >> (i * gs)) & gm) sumw |= 1u << ((uint32_t)((lo >> p.shift) + i) & 31u);
+                }
             }
         }
+        if (summary_mode) p.summary[it] = sumw;
     }
 }
 
-cudaError_t launch_lm_init(const LMParams &p, const uint32_t *v0_words32, int32_t v0_words,
-                           const int32_t *facts, int32_t nfacts, int32_t top, uint32_t *summary,
-                           int32_t sum_words, int blocks, cudaStream_t st) {
-    cudaError_t e;
-    if ((e = cudaMemsetAsync(p.tail, 0, sizeof(int32_t), st))) return e;
-    if ((e = cudaMemsetAsync(p.status_out, 0, sizeof(int32_t), st))) return e;
-    if (p.stage && p.n > 0)
-        if ((e = cudaMemsetAsync(p.stage, 0xFF, sizeof(int32_t) * (size_t)p.n, st))) return e;
-    if (summary && sum_words > 0)
-        if ((e = cudaMemsetAsync(summary, 0, sizeof(uint32_t) * (size_t)sum_words, st))) return e;
-    const int tb = 256;
-    int gb = (int)std::min<int64_t>(((int64_t)p.nwords + tb - 1) / tb, (int64_t)blocks * 8);
-    lm_init_words<<<std::max(gb, 1), tb, 0, st>>>(p.buf0, p.buf1, p.nwords, v0_words32, v0_words,
-                                                  p.n, top);
-    if (nfacts > 0) {
-        int fb = (int)std::min<int64_t>(((int64_t)nfacts + tb - 1) / tb, (int64_t)blocks * 8);
-        lm_init_facts<<<std::max(fb, 1), tb, 0, st>>>(p.buf0, p.buf1, facts, nfacts);
+// In-kernel epilogue: the model over the original atoms, LSB-first uint64 words.
+__device__ __noinline__ void lm_extract(const LMParams &p, int64_t gtid, int64_t gthreads) {
+    const int64_t nw = ((int64_t)p.n + 63) >> 6;
+    for (int64_t w = gtid; w < nw; w += gthreads) {
+        unsigned long long v = (unsigned long long)__ldcg(p.buf0 + 2 * w) |
+                               ((unsigned long long)__ldcg(p.buf0 + 2 * w + 1) << 32);
+        const int64_t lo = w * 64;
+        if (lo + 64 > p.n) v &= (1ull << (uint32_t)(p.n - lo)) - 1ull;
+        p.model_out[w] = v;
     }
-    int lb = (int)std::min<int64_t>((((int64_t)p.n + 31) / 32 + tb - 1) / tb, (int64_t)blocks * 8);
-    lm_init_list<<<std::max(lb, 1), tb, 0, st>>>(p.buf0, p.n, top, p.order, p.tail, p.stage,
-                                                 summary, p.shift);
-    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------
@@ -291,6 +280,7 @@ __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c
         const int32_t gt = (int32_t)gtid >= off ? (int32_t)gtid - off : (int32_t)gtid - off + gth;
         off = (int32_t)(((int64_t)off + (sg.count_pad >> 2)) % gth);
         const int32_t gthreads = gth;
+        // U quads in flight per thread: 4-8 int4 loads (EXACT also streams heads)
         switch (sg.L) {
             case 1: seg_pass<1, 4, EXACT>(p, sg, c, gt, gthreads); break;
             case 2: seg_pass<2, EXACT ? 2 : 4, EXACT>(p, sg, c, gt, gthreads); break;
@@ -309,7 +299,7 @@ __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c
 // pass k reads v_k (rd) and writes v_{k+1} (wr); the loop ends after the first pass
 // that derives nothing (u = v), and iters = k + 1 counts that pass too.
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, 1) lm_full_kernel(LMParams p) {
+__global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_constant__ LMParams p) {
     extern __shared__ uint32_t sm[];
     __shared__ int32_t qcount;
     cg::grid_group grid = cg::this_grid();
@@ -317,6 +307,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_full_kernel(LMParams p) {
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
 
+    lm_prologue(p, !EXACT, gtid, gthreads);            // v_0 (row a3), in-kernel
+    grid.sync();
     const uint32_t *src0 = EXACT ? p.buf0 : p.summary;
     for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(src0 + w);
     const int32_t n0 = __ldcg(p.tail);
@@ -365,15 +357,15 @@ __global__ void __launch_bounds__(kThreads, 1) lm_full_kernel(LMParams p) {
         if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 3] = globaltimer();
         const int32_t t = __ldcg(p.tail);
         const bool lead = blockIdx.x == 0 && tid == 0;
-        if (t == de) {  // u = v: fixpoint
-            if (lead) { *p.iters_out = k + 1; }
+        if (t == de || k + 1 >= p.max_passes) {  // u = v: fixpoint (or the pass guard)
+            if (lead) {
+                *p.iters_out = k + 1;
+                if (t != de) atomicMax(p.status_out, 1);
+            }
+            lm_extract(p, gtid, gthreads);
             return;
         }
         if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
-        if (k + 1 >= p.max_passes) {
-            if (lead) { *p.iters_out = k + 1; atomicMax(p.status_out, 1); }
-            return;
-        }
         ds = de;
         de = t;
     }
@@ -384,9 +376,9 @@ cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t sme
     void *args[] = {(void *)&q};
     if (exact)
         return cudaLaunchCooperativeKernel((const void *)lm_full_kernel<true>, dim3(blocks),
-                                           dim3(kThreads), args, smem, st);
+                                           dim3(kFullThreads), args, smem, st);
     return cudaLaunchCooperativeKernel((const void *)lm_full_kernel<false>, dim3(blocks),
-                                       dim3(kThreads), args, smem, st);
+                                       dim3(kFullThreads), args, smem, st);
 }
 
 // ------------------------------------------------------------------------------------
@@ -478,7 +470,7 @@ __device__ __forceinline__ TileRef tile_ref(const TileSeg *ts, int nseg, int64_t
 constexpr int kConsumerWarps = kThreads / 32 - 1;   // warp 31 is the TMA producer
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(LMParams p) {
+__global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_constant__ LMParams p) {
     extern __shared__ __align__(128) uint8_t smraw[];
     __shared__ int32_t qcount;
     cg::grid_group grid = cg::this_grid();
@@ -496,6 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(LMParams p) {
     uint64_t *empty = full + S;
     TileSeg *ts = reinterpret_cast<TileSeg *>(empty + S);
 
+    lm_prologue(p, !EXACT, gtid, gthreads);
+    grid.sync();
     const uint32_t *src0 = EXACT ? p.buf0 : p.summary;
     for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(src0 + w);
     for (int i = tid; i < p.ntseg; i += blockDim.x) ts[i] = p.tsegs[i];
@@ -633,6 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(LMParams p) {
                     const uint64_t q = q_cons + (uint64_t)x;
                     mbar_wait(full + (q % (uint64_t)S), (uint32_t)((q / S) & 1));
                 }
+            lm_extract(p, gtid, gthreads);
             return;
         }
         if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
@@ -668,13 +663,27 @@ int lm_tma_blocks_per_sm(bool exact, size_t smem) {
 // remaining-body counter of every row whose body contains them; a counter reaching 0
 // means body(r) ⊆ I_k, so head(r) ∈ I_{k+1} -- the same stage as the full θ-pass, hence
 // the same model, pass count and popcount trace (reading R6).
-__global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(LMParams p) {
+//
+// The per-row counters hold the number of body atoms still unknown; the prologue sets
+// them to the row's body length L segment by segment (coalesced, overlapping the v_0
+// build), so the hot loop needs no length lookup and nothing has to be cleaned up.
+__global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_constant__ LMParams p) {
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const int64_t gwarp = gtid >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nwarps = gthreads >> 5;
+    lm_prologue(p, false, gtid, gthreads);
+    for (int32_t s = 0; s < p.nseg; ++s) {   // counters <- L (4 rows per word in byte mode)
+        const Segment sg = p.segs[s];
+        const uint32_t v = p.cnt_bytes == 1 ? (uint32_t)sg.L * 0x01010101u : (uint32_t)sg.L;
+        const int64_t w0 = p.cnt_bytes == 1 ? sg.slot_off >> 2 : sg.slot_off;
+        const int64_t nw = p.cnt_bytes == 1 ? sg.count_pad >> 2 : sg.count_pad;
+        for (int64_t w = gtid; w < nw; w += gthreads) p.cnt[w0 + w] = v;
+    }
+    grid.sync();
     int32_t qs = 0, qe = __ldcg(p.tail);
     if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = qe;
     for (int k = 0;; ++k) {
@@ -684,14 +693,13 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(LMParams p) {
             for (int64_t o = o0 + lane; o < o1; o += 32) {
                 const int32_t slot = __ldg(p.occ_slot + o);
                 bool fired;
-                if (p.cnt_bytes == 1) {
+                if (p.cnt_bytes == 1) {   // a byte never underflows: <= L decrements
                     const uint32_t sh = (uint32_t)(slot & 3) << 3;
-                    const uint32_t old = atomicSub(p.cnt + (slot >> 2), 1u << sh);
-                    fired = ((old >> sh) & 0xFFu) == 1u;
+                    fired = ((atomicSub(p.cnt + (slot >> 2), 1u << sh) >> sh) & 0xFFu) == 1u;
                 } else {
                     fired = atomicSub(p.cnt + slot, 1u) == 1u;
                 }
-                if (fired) {
+                if (fired) {                                // body(r) ⊆ I_k
                     const int32_t h = __ldg(p.head + slot);
                     const uint32_t bit = 1u << (h & 31);
                     const uint32_t old = atomicOr(p.buf0 + (h >> 5), bit);
@@ -706,15 +714,15 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(LMParams p) {
         grid.sync();
         const int32_t t = __ldcg(p.tail);
         const bool lead = blockIdx.x == 0 && tid == 0;
-        if (t == qe) {
-            if (lead) { *p.iters_out = k + 1; }
+        if (t == qe || k + 1 >= p.max_passes) {
+            if (lead) {
+                *p.iters_out = k + 1;
+                if (t != qe) atomicMax(p.status_out, 1);
+            }
+            lm_extract(p, gtid, gthreads);
             return;
         }
         if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
-        if (k + 1 >= p.max_passes) {
-            if (lead) { *p.iters_out = k + 1; atomicMax(p.status_out, 1); }
-            return;
-        }
         qs = qe;
         qe = t;
     }
@@ -725,51 +733,6 @@ cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st) {
     void *args[] = {(void *)&q};
     return cudaLaunchCooperativeKernel((const void *)lm_frontier_kernel, dim3(blocks),
                                        dim3(kThreads), args, 0, st);
-}
-
-__global__ void fill_u32(uint32_t *p, uint32_t v, int64_t count) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-         i += (int64_t)gridDim.x * blockDim.x)
-        p[i] = v;
-}
-
-cudaError_t launch_fill_counters(const Segment *hsegs, int nseg, uint32_t *cnt, int cnt_bytes,
-                                 cudaStream_t st) {
-    for (int s = 0; s < nseg; ++s) {
-        const Segment &sg = hsegs[s];
-        cudaError_t e;
-        if (cnt_bytes == 1) {
-            e = cudaMemsetAsync(reinterpret_cast<uint8_t *>(cnt) + sg.slot_off, sg.L,
-                                (size_t)sg.count_pad, st);
-        } else {
-            int b = (int)std::min<int64_t>((sg.count_pad + 255) / 256, 4096);
-            fill_u32<<<std::max(b, 1), 256, 0, st>>>(cnt + sg.slot_off, (uint32_t)sg.L, sg.count_pad);
-            e = cudaGetLastError();
-        }
-        if (e) return e;
-    }
-    return cudaSuccess;
-}
-
-__global__ void extract_model(const uint32_t *truth, int32_t n, unsigned long long *out) {
-    const int64_t nw = ((int64_t)n + 63) >> 6;
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw;
-         w += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long v = (unsigned long long)truth[2 * w] |
-                               ((unsigned long long)truth[2 * w + 1] << 32);
-        const int64_t lo = w * 64;
-        if (lo + 64 > n) v &= (1ull << (uint32_t)(n - lo)) - 1ull;
-        out[w] = v;
-    }
-}
-
-cudaError_t launch_extract_model(const uint32_t *truth, int32_t n, unsigned long long *out,
-                                 cudaStream_t st) {
-    const int64_t nw = ((int64_t)n + 63) >> 6;
-    if (nw == 0) return cudaSuccess;
-    int b = (int)std::min<int64_t>((nw + 255) / 256, 4096);
-    extract_model<<<b, 256, 0, st>>>(truth, n, out);
-    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------
@@ -888,7 +851,7 @@ __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int
 // once, until no word changes.  Shared memory holds one "any guess" bit per extended
 // atom; a row whose body has an atom false in every guess is skipped after the bit
 // test, so only candidate rows gather the 8·Wp-byte guess rows.
-__global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(STParams p) {
+__global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_constant__ STParams p) {
     extern __shared__ uint32_t sm[];
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
@@ -1040,7 +1003,7 @@ int lm_full_blocks_per_sm(bool exact, size_t smem) {
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &nb, exact ? (const void *)lm_full_kernel<true> : (const void *)lm_full_kernel<false>,
-        kThreads, smem);
+        kFullThreads, smem);
     return nb;
 }
 

@@ -9,6 +9,9 @@
 namespace lpb {
 
 constexpr int kThreads = 1024;          // persistent kernels: 32 warps per CTA
+// Register-streaming full θ-pass CTA size.  (512 threads with twice the loads in flight
+// per thread measured no faster on C4 and slower on C3.)
+constexpr int kFullThreads = 1024;
 constexpr int kMaxSmemBytes = 200 * 1024;
 
 constexpr int kStageBytes = 16384;      // one TMA pipeline stage (bulk copies of col rows)
@@ -37,9 +40,17 @@ struct LMParams {
     uint32_t *buf0;            // truth vector v_k (bit a of word a>>5); double buffer
     uint32_t *buf1;
     int32_t nwords;            // 32-bit words per truth buffer
+    // v_0 inputs (the prologue builds v_0 inside the persistent kernel)
+    const uint32_t *v0;        // optional user start set, 32-bit view of the ABI words
+    int32_t v0_words;          // 32-bit words of v0
+    const uint32_t *factbits;  // [nwords] bit vector of the atoms with a fact rule
+    int32_t top;               // ⊤
+    unsigned long long *model_out;  // [ceil(n/64)] written by the epilogue
+    int32_t *tail_next;        // the other-parity run counters, zeroed for the next call
+    int32_t *status_next;
     // shared-memory copy of the truth vector: exact (shift 0) or a summary whose bit g
     // is the OR of atoms [g << shift, (g+1) << shift)
-    const uint32_t *summary;   // initial summary (global), FILTER mode only
+    uint32_t *summary;         // initial summary (global, built by the prologue)
     int32_t sm_words;
     int32_t shift;
     // derivation order list: initial atoms at [0, n0), then every atom in the pass /
@@ -96,18 +107,13 @@ struct STParams {
 };
 
 // ---- launchers (return cudaError_t of the launch) -----------------------------------
-cudaError_t launch_lm_init(const LMParams &p, const uint32_t *v0_words32, int32_t v0_words,
-                           const int32_t *facts, int32_t nfacts, int32_t top, uint32_t *summary,
-                           int32_t sum_words, int blocks, cudaStream_t st);
+// Each least-model call is ONE cooperative launch: v_0 prologue, the fixpoint loop and
+// the model extraction all run inside the persistent kernel.
 cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st);
 cudaError_t launch_lm_tma(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st);
 int lm_tma_blocks_per_sm(bool exact, size_t smem);
 size_t lm_tma_smem_bytes(int32_t sm_words, int32_t stages);
 cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st);
-cudaError_t launch_fill_counters(const Segment *hsegs, int nseg, uint32_t *cnt, int cnt_bytes,
-                                 cudaStream_t st);
-cudaError_t launch_extract_model(const uint32_t *truth, int32_t n, unsigned long long *out,
-                                 cudaStream_t st);
 
 cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_t *negated_ext,
                            const int32_t *free_rank, const unsigned long long *guesses,
