@@ -96,6 +96,11 @@ typedef struct {
 
 #define LP_PTR_DEVICE 0x1u /* pointer args of this call are device pointers; async */
 #define LP_FRONTIER 0x2u   /* least model: frontier (semi-naive) variant            */
+#define LP_FULL_STREAM 0x4u /* full θ-pass: stream every body position in every pass
+                               (default: LEAD passes -- stream the lead atom of each
+                               row, verify the survivors -- until a pass queues more
+                               than 1/16 of the rows).  Same results either way.     */
+#define LP_FULL_LEAD 0x8u   /* full θ-pass: LEAD passes only (never switch)          */
 
 typedef struct {
     void *stream;            /* cudaStream_t (NULL = legacy default stream)          */
@@ -107,6 +112,11 @@ typedef struct {
     void *ev_begin;          /* optional cudaEvent_t recorded on stream immediately
                                 before the fixpoint kernel, ev_end right after it   */
     void *ev_end;
+    uint64_t *stats_out;     /* optional [4], full θ-pass only (zeros otherwise):
+                                [0] algorithmic bytes the fixpoint kernel moved (planes
+                                streamed + 4 B per verified body entry / head + 12 B
+                                per derived atom), [1] LEAD passes, [2] rows queued for
+                                verification, [3] body entries verification loaded   */
 } lp_run;
 
 typedef struct {
@@ -128,6 +138,10 @@ typedef struct {
     int32_t block_threads;
     int32_t full_kernel;      /* 1: TMA-pipelined full θ-pass, 0: register-streaming   */
     int32_t tma_stages;       /* depth of the TMA shared-memory ring                   */
+    int64_t lead_pass_bytes;  /* program bytes a LEAD full θ-pass streams                */
+    int64_t stream_pass_bytes;/* program bytes a STREAM full θ-pass streams              */
+    int32_t key_shift;        /* summary mode: keys per key-summary bit = 1 << key_shift;
+                                 -1 when there is no key plane                         */
 } lp_info_t;
 
 /* Validate, standardize and encode a program, upload it (PAPER.md:62, 82-95,

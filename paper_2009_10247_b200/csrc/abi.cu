@@ -57,8 +57,13 @@ struct lp_program {
     int64_t ntiles = 0;
     size_t tma_smem = 0;
     // [0] tail, [2] status (stable path); [1] iters; [3] passes; [4,5] n_accepted;
-    // [8,9] least-model tails and [10,11] statuses, alternating by call parity
+    // [8,9] least-model tails and [10,11] statuses, alternating by call parity;
+    // [12..14] rows queued per full θ-pass (slot k % 3)
     int32_t *d_scal = nullptr;
+    unsigned long long *d_stats = nullptr;  // full θ-pass work statistics (lp_run.stats_out)
+    int32_t *d_keyplane = nullptr, *d_key_of = nullptr;  // summary-mode key plane
+    uint32_t *d_ksummary = nullptr;
+    int32_t ksm_words = 0, kshift = 0;
     uint32_t *d_factbits = nullptr;
     uint64_t lm_runs = 0;
     int32_t *d_facts = nullptr;
@@ -139,6 +144,20 @@ static lp_status upload(lp_program *p, T **out, const std::vector<T> &v) {
         if (s_ != LP_OK) return s_;     \
     } while (0)
 
+// Program bytes one full θ-pass streams: a LEAD pass reads
+// the lead plane (+ the head plane when the truth test is exact), a STREAM pass every
+// body plane (+ the head plane when exact).  Padding rows included.
+static uint64_t lead_plane_bytes(const lp_program *p) {
+    uint64_t b = 4ull * (uint64_t)p->L.n_slots;
+    return p->exact ? 2 * b : b;
+}
+
+static uint64_t stream_plane_bytes(const lp_program *p) {
+    uint64_t b = 0;
+    for (const Segment &sg : p->L.segs) b += 4ull * (uint64_t)sg.L * (uint64_t)sg.count_pad;
+    return p->exact ? b + 4ull * (uint64_t)p->L.n_slots : b;
+}
+
 // ------------------------------------------------------------------------------------
 // lp_load
 // ------------------------------------------------------------------------------------
@@ -175,8 +194,9 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     TRY(dalloc(p, &p->d_buf0, p->nwords));
     TRY(dalloc(p, &p->d_buf1, p->nwords));
     TRY(dalloc(p, &p->d_order, (size_t)L.n_ext + 1));
-    TRY(dalloc(p, &p->d_scal, 16));
-    CK(cudaMemset(p->d_scal, 0, 16 * sizeof(int32_t)));
+    TRY(dalloc(p, &p->d_scal, 32));
+    CK(cudaMemset(p->d_scal, 0, 32 * sizeof(int32_t)));
+    TRY(dalloc(p, &p->d_stats, 4));
     {
         std::vector<uint32_t> fb((size_t)p->nwords, 0u);   // facts of P (Def. 4)
         for (int32_t a : L.facts) fb[(size_t)a >> 5] |= 1u << (a & 31);
@@ -207,6 +227,49 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(dalloc(p, &p->d_summary, p->sm_words));
     }
     p->lm_smem = (size_t)p->sm_words * 4;
+
+    // key plane (summary mode, register-streaming kernel): the
+    // lead atom of every row is also stored as its key.  Atoms that can become true
+    // without v0 -- heads of stored rows, facts, abar, ⊤ -- get consecutive keys (fine
+    // summary groups); every other atom shares a key with up to 63 of its kind.
+    const bool want_keys = !p->exact && !(opt && (opt->flags & LP_LOAD_TMA)) &&
+                           !std::getenv("LP_NO_KEYS");
+    if (want_keys) {
+        std::vector<uint8_t> der((size_t)L.n_ext, 0);
+        for (int64_t s = 0; s < L.n_slots; ++s) der[(size_t)L.head[(size_t)s]] = 1;
+        for (int32_t a : L.facts) der[(size_t)a] = 1;
+        for (int32_t a = L.n; a < L.bot; ++a) der[(size_t)a] = 1;
+        der[(size_t)L.bot] = 0;
+        std::vector<int32_t> key((size_t)L.n_ext);
+        int64_t nd = 0;
+        for (int32_t a = 0; a < L.n_ext; ++a)
+            if (der[(size_t)a]) key[(size_t)a] = (int32_t)nd++;
+        int64_t nu = 0;
+        for (int32_t a = 0; a < L.n_ext; ++a)
+            if (!der[(size_t)a]) key[(size_t)a] = (int32_t)(nd + (nu++ >> 6));
+        const int64_t nkeys = nd + (nu + 63) / 64;
+        int64_t kcap = kKeySmemBytes;
+        if (opt && opt->smem_bits_cap > 0) kcap = std::min<int64_t>(kcap, opt->smem_bits_cap / 8);
+        kcap = std::max<int64_t>(kcap, 16);
+        int sh = 0;
+        int64_t kw = 0;
+        for (;; ++sh) {
+            const int64_t groups = ((nkeys - 1) >> sh) + 1;
+            kw = ((groups + 31) / 32 + 3) / 4 * 4;
+            if (kw * 4 <= kcap) break;
+        }
+        p->kshift = sh;
+        p->ksm_words = (int32_t)kw;
+        std::vector<int32_t> kp((size_t)std::max<int64_t>(L.n_slots, 1), key[(size_t)L.bot]);
+        for (const Segment &sg : L.segs)
+            for (int64_t i = 0; i < sg.count_pad; ++i)
+                kp[(size_t)(sg.slot_off + i)] = key[(size_t)L.col[(size_t)(sg.col_off + i)]];
+        TRY(upload(p, &p->d_keyplane, kp));
+        TRY(upload(p, &p->d_key_of, key));
+        TRY(dalloc(p, &p->d_ksummary, (size_t)kw));
+        CK(cudaMemset(p->d_ksummary, 0, (size_t)kw * 4));
+        p->lm_smem = std::max(p->lm_smem, (size_t)kw * 4);
+    }
 
     // stable path filter: one bit per extended atom (or per 2^any_shift atoms)
     {
@@ -261,9 +324,10 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     p->grid_cap = (opt && opt->grid_blocks > 0) ? opt->grid_blocks : 0;
     auto cap_grid = [&](int b) { return p->grid_cap > 0 ? std::min(b, p->grid_cap) : b; };
     p->lm_blocks = cap_grid(sms * bl);
-    if (!p->exact) {
+    {
         // a CTA handles at most 4 * threads * ceil(nq / gthreads) slots per segment, so
-        // its queue never overflows (an overflow is reported, never silently dropped)
+        // its queue never overflows (an overflow is reported, never silently dropped);
+        // LEAD passes queue in both truth modes, STREAM passes in summary mode
         const int64_t gthreads = (int64_t)p->lm_blocks * kFullThreads;
         int64_t cap = 0;
         if (p->use_tma)  // a CTA consumes at most ceil(ntiles / grid) tiles of <= 4096 rows
@@ -362,7 +426,10 @@ extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
     int64_t col_entries = 0;
     for (const Segment &sg : L.segs) col_entries += (int64_t)sg.L * sg.count_pad;
     o->pass_bytes = 4 * col_entries + 2 * (int64_t)p->nwords * 4;
+    o->lead_pass_bytes = (int64_t)lead_plane_bytes(p);
+    o->stream_pass_bytes = (int64_t)stream_plane_bytes(p);
     o->truth_mode = p->exact ? 0 : 1;
+    o->key_shift = p->d_keyplane ? p->kshift : -1;
     o->summary_shift = p->shift;
     o->grid_blocks = p->lm_blocks;
     o->full_kernel = p->use_tma ? 1 : 0;
@@ -473,6 +540,25 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.ntiles = p->ntiles;
     q.heads_staged = p->exact ? 1 : 0;
     q.tma_variant = std::getenv("LP_TMA_VARIANT") ? std::atoi(std::getenv("LP_TMA_VARIANT")) : 0;
+    q.pass_mode = (flags & LP_FULL_STREAM) ? 2 : (flags & LP_FULL_LEAD) ? 1 : 0;
+    q.dense_div = std::getenv("LP_DENSE_DIV") ? std::max(1, std::atoi(std::getenv("LP_DENSE_DIV"))) : 16;
+    q.n_slots = L.n_slots;
+    q.cand = p->d_scal + 12;
+    unsigned long long *stats_dev = nullptr;
+    if (run && run->stats_out) stats_dev = dev ? reinterpret_cast<unsigned long long *>(run->stats_out) : p->d_stats;
+    if (stats_dev && (frontier || p->use_tma)) {   // only the register-streaming full pass counts
+        if (dev) CK(cudaMemsetAsync(stats_dev, 0, 4 * sizeof(uint64_t), st));
+        else std::memset(run->stats_out, 0, 4 * sizeof(uint64_t));
+        stats_dev = nullptr;
+    }
+    q.stats = stats_dev;
+    q.keyplane = (frontier || p->use_tma) ? nullptr : p->d_keyplane;
+    q.key_of = p->d_key_of;
+    q.ksummary = p->d_ksummary;
+    q.ksm_words = p->ksm_words;
+    q.kshift = p->kshift;
+    q.lead_bytes = (long long)lead_plane_bytes(p);
+    q.stream_bytes = (long long)stream_plane_bytes(p);
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
     if (frontier) CK(launch_lm_frontier(q, p->fr_blocks, st));
     else if (p->use_tma) CK(launch_lm_tma(q, p->exact, p->lm_blocks, p->tma_smem, st));
@@ -489,6 +575,8 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
                                   cudaMemcpyDeviceToHost, st));
     if (pops) CK(cudaMemcpyAsync(run->popcounts_out, pops, sizeof(int32_t) * (size_t)pop_cap,
                                  cudaMemcpyDeviceToHost, st));
+    if (stats_dev)
+        CK(cudaMemcpyAsync(run->stats_out, stats_dev, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     *iters_out = scal[1];
     if (scal[2] == 2) return set_err(LP_E_CUDA, "internal: candidate queue overflow");

@@ -72,6 +72,12 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *
     L->n_rules = R;
     L->definite = (k == 0);
 
+    // ---- derivability: an atom that is neither a head nor a fact can only be true if
+    // the caller's v0 says so (abar atoms are set by the guesses, so they count as
+    // derivable).  Used below to choose each row's lead atom.
+    std::vector<int32_t> per_head((size_t)n + 1, 0);
+    for (int64_t i = 0; i < R; ++i) per_head[r->head[i]]++;
+
     // ---- per-rule de-duplicated extended bodies -----------------------------------
     std::vector<int32_t> ext((size_t)std::max<int64_t>(nnz_in, 1));
     std::vector<int32_t> len((size_t)std::max<int64_t>(R, 1));
@@ -102,6 +108,17 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *
         }
         int64_t l = pos - start;
         if (l > std::numeric_limits<int32_t>::max()) return fail(err, LP_E_INVALID, "body too long");
+        // lead atom (body position 0, the one the full θ-pass streams first and tests
+        // before anything else is loaded): the first underivable atom if the body has
+        // one, else the input order is kept.  The AND is order-free, so this changes
+        // how many rows need a second look, never a result.
+        for (int64_t q = start; q < pos; ++q) {
+            const int32_t x = ext[q];
+            if (x < n && !per_head[x] && !isfact[x]) {
+                std::swap(ext[start], ext[q]);
+                break;
+            }
+        }
         len[i] = (int32_t)l;
         if ((int32_t)l > maxL) maxL = (int32_t)l;
     }
@@ -111,8 +128,6 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *
 
     // ---- statistics ----------------------------------------------------------------
     {
-        std::vector<int32_t> per_head((size_t)n + 1, 0);
-        for (int64_t i = 0; i < R; ++i) per_head[r->head[i]]++;
         int64_t heads = 0, aux = 0;
         for (int32_t a = 0; a < n; ++a) {
             if (per_head[a]) ++heads;

@@ -67,6 +67,10 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
         *p.tail_next = 0;
         *p.status_next = 0;
     }
+    if (summary_mode && p.keyplane && gtid == 0) {          // ⊤ is always true
+        const uint32_t g = (uint32_t)__ldg(p.key_of + p.top) >> p.kshift;
+        atomicOr(p.ksummary + (g >> 5), 1u << (g & 31));
+    }
     const int wpi = summary_mode ? (1 << p.shift) : 1;     // truth words per item (shift <= 31)
     const int64_t items = summary_mode ? p.sm_words : p.nwords;
     for (int64_t it = gtid; it < items; it += gthreads) {
@@ -89,6 +93,10 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
                     const int i = __ffs(b) - 1;
                     b &= b - 1;
                     p.order[pos++] = (int32_t)(lo + i);
+                    if (summary_mode && p.keyplane) {   // key-space summary of v_0
+                        const uint32_t g = (uint32_t)__ldg(p.key_of + lo + i) >> p.kshift;
+                        atomicOr(p.ksummary + (g >> 5), 1u << (g & 31));
+                    }
                 }
             }
             if (p.stage && lo < p.n) {
@@ -160,8 +168,12 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
 }
 
 
-// FILTER mode: exact test of one candidate row (global slot) against v_k in L2.
-__device__ __noinline__ void check_candidate(const LMParams &p, const PassCtx &c, int32_t slot) {
+// Exact test of one queued row against v_k: the shared copy when it is exact, else the
+// truth vector in L2.  The head is looked at first -- a row whose head is already in
+// v_k cannot change anything -- then body positions j0..L-1 (LEAD passes have already
+// tested position 0 exactly in EXACT mode).  Returns the body entries it loaded.
+template <bool EXACT>
+__device__ __noinline__ int verify_slot(const LMParams &p, const PassCtx &c, int32_t slot, int j0) {
     int lo = 0, hi = p.nseg - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -171,17 +183,23 @@ __device__ __noinline__ void check_candidate(const LMParams &p, const PassCtx &c
     const int64_t cp = __ldg(&p.segs[lo].count_pad);
     const int32_t *colp = p.col + __ldg(&p.segs[lo].col_off) + (slot - __ldg(&p.segs[lo].slot_off));
     const int32_t h = __ldg(p.head + slot);
+    const uint32_t hw = EXACT ? c.sm[h >> 5] : __ldcg(c.rd + (h >> 5));
+    if ((hw >> (h & 31)) & 1u) return 0;
     bool ok = true;
-    for (int32_t j0 = 0; j0 < L && ok; j0 += 4) {
+    int loaded = 0;
+    for (int32_t jb = j0; jb < L && ok; jb += 4) {
         uint32_t a[4], w[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) a[j] = j0 + j < L ? (uint32_t)__ldg(colp + (int64_t)(j0 + j) * cp) : 0u;
+        for (int j = 0; j < 4; ++j) a[j] = jb + j < L ? (uint32_t)__ldg(colp + (int64_t)(jb + j) * cp) : 0u;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) w[j] = j0 + j < L ? __ldcg(c.rd + (a[j] >> 5)) : ~0u;
+        for (int j = 0; j < 4; ++j)
+            w[j] = jb + j < L ? (EXACT ? c.sm[a[j] >> 5] : __ldcg(c.rd + (a[j] >> 5))) : ~0u;
 #pragma unroll
         for (int j = 0; j < 4; ++j) ok = ok && ((w[j] >> (a[j] & 31)) & 1u);
+        loaded += min(4, L - jb);
     }
-    if (ok) emit_head(p, c, h, __ldcg(c.rd + (h >> 5)));
+    if (ok) emit_head(p, c, h, hw);
+    return loaded;
 }
 
 // FILTER mode: rows that passed the summary test are queued and verified in the
@@ -267,12 +285,49 @@ __device__ void seg_pass_generic(const LMParams &p, const Segment &sg, const Pas
     }
 }
 
-template <bool EXACT>
+// LEAD pass over one segment: stream only body position 0 (the lead atom, chosen at
+// load time, encode.cpp) of 4 rows per int4 load, U quads in flight; EXACT mode also
+// streams the head row and drops rows whose head is already in v_k.  Rows that survive
+// go to this CTA's queue and are verified in the pass epilogue (verify_slot), so the
+// other body positions are loaded only for the few rows whose lead atom is true.
+template <int U, bool EXACT>
+__device__ __forceinline__ void seg_lead(const LMParams &p, const Segment &sg, const PassCtx &c,
+                                         int32_t gtid, int32_t gthreads) {
+    const int32_t nq = (int32_t)(sg.count_pad >> 2);
+    const int32_t slot0 = (int32_t)sg.slot_off;
+    const bool keys = !EXACT && p.keyplane;
+    const int shift = keys ? p.kshift : p.shift;
+    const int4 *base = reinterpret_cast<const int4 *>(keys ? p.keyplane + sg.slot_off : p.col + sg.col_off);
+    const int4 *hbase = reinterpret_cast<const int4 *>(p.head + sg.slot_off);
+    for (int32_t q0 = gtid; q0 < nq; q0 += gthreads * U) {
+        int4 v[U];
+        int4 hv[EXACT ? U : 1];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t q = q0 + u * gthreads;
+            v[u] = q < nq ? ld_stream(base + q) : make_int4(0, 0, 0, 0);
+            if (EXACT) hv[EXACT ? u : 0] = q < nq ? ld_stream(hbase + q) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t q = q0 + u * gthreads;
+            if (q >= nq) break;
+            unsigned fire = test4<EXACT>(v[u], 0xFu, c.sm, shift);
+            if (EXACT && fire) {   // keep the rows whose head is not yet in v_k
+                const int4 h = hv[EXACT ? u : 0];
+                fire &= (sm_bit(c.sm, (uint32_t)h.x) ? 0u : 1u) | (sm_bit(c.sm, (uint32_t)h.y) ? 0u : 2u) |
+                        (sm_bit(c.sm, (uint32_t)h.z) ? 0u : 4u) | (sm_bit(c.sm, (uint32_t)h.w) ? 0u : 8u);
+            }
+            if (fire) enqueue(p, c, slot0 + q * 4, fire);
+        }
+    }
+}
+
+// Segment s starts at the thread after the one that took the last quad of segment s-1,
+// so short segments spread over the whole grid instead of piling onto the lowest ids.
+template <bool EXACT, bool LEAD>
 __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c, int64_t gtid,
                                              int64_t gthreads) {
-    // segment s starts at the thread after the one that took the last quad of segment
-    // s-1, so short segments spread over the whole grid instead of piling onto the
-    // lowest thread ids
     const int32_t gth = (int32_t)gthreads;
     int32_t off = 0;
     for (int32_t s = 0; s < p.nseg; ++s) {
@@ -280,6 +335,10 @@ __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c
         const int32_t gt = (int32_t)gtid >= off ? (int32_t)gtid - off : (int32_t)gtid - off + gth;
         off = (int32_t)(((int64_t)off + (sg.count_pad >> 2)) % gth);
         const int32_t gthreads = gth;
+        if (LEAD) {
+            seg_lead<EXACT ? 4 : 8, EXACT>(p, sg, c, gt, gthreads);
+            continue;
+        }
         // U quads in flight per thread: 4-8 int4 loads (EXACT also streams heads)
         switch (sg.L) {
             case 1: seg_pass<1, 4, EXACT>(p, sg, c, gt, gthreads); break;
@@ -298,22 +357,45 @@ __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c
 // One cooperative launch = the whole fixpoint loop of Algorithm 1:
 // pass k reads v_k (rd) and writes v_{k+1} (wr); the loop ends after the first pass
 // that derives nothing (u = v), and iters = k + 1 counts that pass too.
+//
+// Each pass is either a LEAD pass (lead atoms streamed, survivors queued and verified)
+// or a STREAM pass (every body position streamed; the test is complete in EXACT mode,
+// summary survivors are queued).  Both compute exactly θ(M v_k); the schedule only
+// decides which bytes are read (p.pass_mode).
 template <bool EXACT>
 __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_constant__ LMParams p) {
     extern __shared__ uint32_t sm[];
     __shared__ int32_t qcount;
+    __shared__ unsigned long long loaded_cta;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    const bool lead = blockIdx.x == 0 && tid == 0;
 
     lm_prologue(p, !EXACT, gtid, gthreads);            // v_0 (row a3), in-kernel
+    if (gtid == 0) {
+        p.cand[0] = 0;
+        p.cand[1] = 0;
+        p.cand[2] = 0;
+        if (p.stats)
+            for (int i = 0; i < 4; ++i) p.stats[i] = 0;
+    }
     grid.sync();
-    const uint32_t *src0 = EXACT ? p.buf0 : p.summary;
-    for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(src0 + w);
+    bool lead_pass = p.pass_mode != 2;
+    bool keys = !EXACT && p.keyplane && lead_pass;       // shared copy is in key space
+    bool rebuild = false;                                // key space -> atom-id summary
+    {
+        const uint32_t *src0 = EXACT ? p.buf0 : keys ? p.ksummary : p.summary;
+        const int32_t nw0 = keys ? p.ksm_words : p.sm_words;
+        for (int32_t w = tid; w < nw0; w += blockDim.x) sm[w] = __ldcg(src0 + w);
+    }
     const int32_t n0 = __ldcg(p.tail);
-    if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = n0;
-    if (tid == 0) qcount = 0;
+    if (lead && p.pops && p.pop_cap > 0) p.pops[0] = n0;
+    if (tid == 0) {
+        qcount = 0;
+        loaded_cta = 0;
+    }
     __syncthreads();
 
     int32_t ds = n0, de = n0;  // atoms that became true in the previous pass
@@ -329,43 +411,101 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             // shared copy: v_{k-1} -> v_k
             if (EXACT && (de - ds) > (p.sm_words >> 2)) {
                 for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(rd + w);
+            } else if (!EXACT && rebuild) {
+                // first STREAM pass after LEAD passes in key space: the atom-id summary of
+                // v_k from the complete truth vector rd (bit g = OR of atoms g<<shift ..)
+                rebuild = false;
+                for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = 0u;
+                __syncthreads();
+                for (int32_t t = tid; t < p.nwords; t += blockDim.x) {
+                    const uint32_t v = __ldcg(rd + t);
+                    if (!v) continue;
+                    if (p.shift >= 5) {
+                        const uint32_t g = (uint32_t)t >> (p.shift - 5);
+                        atomicOr(sm + (g >> 5), 1u << (g & 31));
+                    } else {
+                        for (uint32_t b = v; b;) {
+                            const uint32_t g = ((uint32_t)t * 32u + (uint32_t)(__ffs(b) - 1)) >> p.shift;
+                            b &= b - 1;
+                            atomicOr(sm + (g >> 5), 1u << (g & 31));
+                        }
+                    }
+                }
             } else {
                 for (int64_t i = ds + tid; i < de; i += blockDim.x) {
                     const uint32_t a = (uint32_t)__ldcg(p.order + i);
-                    const uint32_t g = EXACT ? a : (a >> p.shift);
+                    const uint32_t g = EXACT ? a : keys ? ((uint32_t)__ldg(p.key_of + a) >> p.kshift) : (a >> p.shift);
                     atomicOr(sm + (g >> 5), 1u << (g & 31));
                 }
             }
             __syncthreads();
         }
+        // rows queued in pass k are counted in cand[k % 3]; the slot of pass k+1 was last
+        // read before the previous barrier and is first written after the next one
+        if (lead) p.cand[(k + 1) % 3] = 0;
         const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k};
         if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 0] = globaltimer();
-        all_segments<EXACT>(p, c, gtid, gthreads);
-        if (!EXACT) {  // epilogue: verify this CTA's queued candidates
+        if (lead_pass) all_segments<EXACT, true>(p, c, gtid, gthreads);
+        else all_segments<EXACT, false>(p, c, gtid, gthreads);
+        if (!EXACT || lead_pass) {  // epilogue: verify this CTA's queued rows
             __syncthreads();
             const int32_t nc = min(qcount, p.qcap);
             __syncthreads();
-            if (tid == 0) qcount = 0;
-            for (int32_t i = tid; i < nc; i += blockDim.x) check_candidate(p, c, __ldcg(c.qbuf + i));
+            if (tid == 0) {
+                qcount = 0;
+                if (nc) atomicAdd(p.cand + k % 3, nc);
+            }
+            const int j0 = (EXACT && lead_pass) ? 1 : 0;
+            int loaded = 0;
+            for (int32_t i = tid; i < nc; i += blockDim.x)
+                loaded += verify_slot<EXACT>(p, c, __ldcg(c.qbuf + i), j0);
+            if (p.stats) {
+                for (int o = 16; o; o >>= 1) loaded += __shfl_xor_sync(0xFFFFFFFFu, loaded, o);
+                if ((tid & 31) == 0 && loaded) atomicAdd(&loaded_cta, (unsigned long long)loaded);
+            }
         }
         if (p.dbg && k < 16) {
             if ((tid & 31) == 0) atomicMax(p.dbg + (k * gridDim.x + blockIdx.x) * 4 + 1, globaltimer());
             __syncthreads();
             if (tid == 0) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 2] = globaltimer();
         }
+        if (p.stats) {
+            __syncthreads();
+            if (tid == 0 && loaded_cta) {
+                atomicAdd(p.stats + 3, loaded_cta);
+                loaded_cta = 0;
+            }
+        }
         grid.sync();
         if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 3] = globaltimer();
         const int32_t t = __ldcg(p.tail);
-        const bool lead = blockIdx.x == 0 && tid == 0;
+        const int32_t queued = __ldcg(p.cand + k % 3);
+        if (lead && p.stats) {
+            // algorithmic bytes of this pass: the planes it streamed, 4 B per body entry
+            // and head the verification loaded, the delta list read twice and the truth
+            // words it ORs
+            p.stats[0] += (unsigned long long)(lead_pass ? p.lead_bytes : p.stream_bytes) +
+                          4ull * (unsigned long long)queued + 12ull * (unsigned long long)(t - de);
+            if (lead_pass) p.stats[1] += 1;
+            p.stats[2] += (unsigned long long)queued;
+        }
         if (t == de || k + 1 >= p.max_passes) {  // u = v: fixpoint (or the pass guard)
             if (lead) {
                 *p.iters_out = k + 1;
                 if (t != de) atomicMax(p.status_out, 1);
+                if (p.stats) p.stats[0] += 4ull * p.stats[3];
             }
+            if (!EXACT && p.keyplane)   // the next call scatters v_0 into a zero summary
+                for (int64_t w = gtid; w < p.ksm_words; w += gthreads) p.ksummary[w] = 0u;
             lm_extract(p, gtid, gthreads);
             return;
         }
         if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
+        if (lead_pass && p.pass_mode == 0 && (int64_t)queued * p.dense_div > p.n_slots) {
+            lead_pass = false;
+            rebuild = keys;
+            keys = false;
+        }
         ds = de;
         de = t;
     }
@@ -592,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
                         const int32_t pos = atomicAdd(&qcount, 1);
                         const int32_t slot = (int32_t)(sg.slot_off + r.start + row);
                         if (pos < p.qcap) c.qbuf[pos] = slot;
-                        else check_candidate(p, c, slot);
+                        else verify_slot<false>(p, c, slot, 0);
                     }
                 }
                 __syncwarp();
@@ -604,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
             const int32_t nc = min(qcount, p.qcap);
             __syncthreads();
             if (tid == 0) qcount = 0;
-            for (int32_t i = tid; i < nc; i += blockDim.x) check_candidate(p, c, __ldcg(c.qbuf + i));
+            for (int32_t i = tid; i < nc; i += blockDim.x) verify_slot<false>(p, c, __ldcg(c.qbuf + i), 0);
         }
         if (p.dbg && k < 16) {
             if ((tid & 31) == 0 && !producer) atomicMax(p.dbg + (k * gridDim.x + blockIdx.x) * 4 + 1, globaltimer());
@@ -978,7 +1118,7 @@ cudaError_t launch_st_column(const STParams &p, int32_t n, int64_t g, unsigned l
 
 cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
     cudaError_t e;
-    const int cap = kMaxSmemBytes + 1024;
+    const int cap = std::max(kMaxSmemBytes, kKeySmemBytes) + 1024;
     (void)lm_smem;
     (void)st_smem;
     if ((e = cudaFuncSetAttribute((const void *)lm_full_kernel<true>,

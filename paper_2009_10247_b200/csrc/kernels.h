@@ -13,6 +13,7 @@ constexpr int kThreads = 1024;          // persistent kernels: 32 warps per CTA
 // per thread measured no faster on C4 and slower on C3.)
 constexpr int kFullThreads = 1024;
 constexpr int kMaxSmemBytes = 200 * 1024;
+constexpr int kKeySmemBytes = 216 * 1024;   // key-space summary (register-streaming kernel only)
 
 constexpr int kStageBytes = 16384;      // one TMA pipeline stage (bulk copies of col rows)
 constexpr int kSmemLimit = 232448 - 1024;  // opt-in smem per CTA on sm_100 minus static
@@ -79,6 +80,27 @@ struct LMParams {
     int64_t ntiles;
     int32_t heads_staged;      // 1: the head row is part of every tile (EXACT mode)
     int32_t tma_variant;       // diagnostics (LP_TMA_VARIANT): 1 no L2 hint, 2 4 KB chunks
+    // full θ-pass schedule: LEAD passes stream only the lead
+    // atom of every row (+ the head row when the truth test is exact) and verify the
+    // survivors from a queue; STREAM passes stream every body position.
+    int32_t pass_mode;         // 0 auto (LEAD until a pass queues > n_slots/dense_div
+                               //   rows, STREAM from then on), 1 always LEAD, 2 always STREAM
+    int32_t dense_div;
+    int64_t n_slots;
+    int32_t *cand;             // [3] rows queued per pass (slot k % 3)
+    unsigned long long *stats; // [4] algorithmic bytes, LEAD passes, rows verified,
+                               //     body entries loaded by verification
+    long long lead_bytes;      // bytes one LEAD / STREAM pass streams (program planes only)
+    long long stream_bytes;
+    // summary mode key plane: LEAD passes stream key(lead atom)
+    // instead of the lead atom and test it against a summary in key space, where the
+    // atoms that can become true (heads, facts) get fine groups and the rest share
+    // coarse ones.  STREAM passes switch the shared copy back to the atom-id summary.
+    const int32_t *keyplane;   // [n_slots] or NULL (no key mode)
+    const int32_t *key_of;     // [n_ext] key of every extended atom
+    uint32_t *ksummary;        // [ksm_words] summary of v_0 in key space (zero between calls)
+    int32_t ksm_words;
+    int32_t kshift;
 };
 
 // profiling hook (not part of the ABI): per-CTA %globaltimer stamps

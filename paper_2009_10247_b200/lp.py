@@ -25,6 +25,8 @@ LP_LOAD_NO_FRONTIER = 0x1
 LP_LOAD_TMA = 0x2
 LP_PTR_DEVICE = 0x1
 LP_FRONTIER = 0x2
+LP_FULL_STREAM = 0x4
+LP_FULL_LEAD = 0x8
 
 _P = ctypes.c_void_p
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
@@ -45,7 +47,7 @@ class lp_options(ctypes.Structure):
 class lp_run(ctypes.Structure):
     _fields_ = [("stream", _P), ("flags", ctypes.c_uint32), ("popcounts_out", _P),
                 ("popcounts_cap", ctypes.c_int32), ("stage_out", _P), ("ev_begin", _P),
-                ("ev_end", _P)]
+                ("ev_end", _P), ("stats_out", _P)]
 
 
 class lp_info_t(ctypes.Structure):
@@ -57,7 +59,8 @@ class lp_info_t(ctypes.Structure):
                 ("pass_bytes", ctypes.c_int64), ("truth_mode", ctypes.c_int32),
                 ("summary_shift", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
                 ("block_threads", ctypes.c_int32), ("full_kernel", ctypes.c_int32),
-                ("tma_stages", ctypes.c_int32)]
+                ("tma_stages", ctypes.c_int32), ("lead_pass_bytes", ctypes.c_int64),
+                ("stream_pass_bytes", ctypes.c_int64), ("key_shift", ctypes.c_int32)]
 
 
 SYMBOLS = ("lp_load", "lp_info", "lp_negated_atoms", "lp_least_model", "lp_stable_models",
@@ -209,7 +212,7 @@ class Program:
         return lp_negated_atoms(self)
 
     def least_model(self, v0=None, frontier: bool = False, popcounts: bool = False,
-                    stages: bool = False, stream=None):
+                    stages: bool = False, stream=None, schedule: str = "auto", stats: bool = False):
         """Host-buffer call.  v0: None, a bool mask [n], or an id list.  Returns
         (model uint64[ceil(n/64)], iters, dict(popcounts=..., stage=...))."""
         n = self.n_atoms
@@ -225,9 +228,13 @@ class Program:
         model = np.zeros(max(bits_words(n), 1), dtype=np.uint64)
         pops = np.zeros(n + 3, dtype=np.int32) if popcounts else None
         stage = np.zeros(max(n, 1), dtype=np.int32) if stages else None
+        st = np.zeros(4, dtype=np.uint64) if stats else None
         iters = lp_least_model(self, v0w, model, frontier=frontier, pops=pops, stage=stage,
-                               stream=stream)
+                               stream=stream, schedule=schedule, stats=st)
         extra = {}
+        if stats:
+            extra["stats"] = dict(zip(("bytes", "lead_passes", "rows_verified", "entries_verified"),
+                                      (int(x) for x in st)))
         if popcounts:
             extra["popcounts"] = pops[:iters].tolist()
         if stages:
@@ -294,8 +301,9 @@ def lp_negated_atoms(p: Program):
     return out[:k].tolist()
 
 
-def _run(stream=None, flags=0, pops=None, stage=None, ev_begin=None, ev_end=None):
+def _run(stream=None, flags=0, pops=None, stage=None, ev_begin=None, ev_end=None, stats=None):
     r = lp_run()
+    r.stats_out = _ptr(stats)
     r.stream = _stream_ptr(stream)
     r.flags = flags
     r.popcounts_out = _ptr(pops)
@@ -307,12 +315,14 @@ def _run(stream=None, flags=0, pops=None, stage=None, ev_begin=None, ev_end=None
 
 
 def lp_least_model(p: Program, v0, model_out, frontier=False, pops=None, stage=None, stream=None,
-                   device_ptrs=False, iters_out=None, ev_begin=None, ev_end=None):
+                   device_ptrs=False, iters_out=None, ev_begin=None, ev_end=None, schedule="auto",
+                   stats=None):
     """Marshals lp_least_model.  Host mode (default): numpy buffers, returns iters.
     device_ptrs=True: torch CUDA tensors (v0 int64 words or None, model_out int64
     words, iters_out int32[1], optional pops/stage), asynchronous on ``stream``."""
     flags = (LP_FRONTIER if frontier else 0) | (LP_PTR_DEVICE if device_ptrs else 0)
-    run = _run(stream, flags, pops, stage, ev_begin, ev_end)
+    flags |= {"auto": 0, "stream": LP_FULL_STREAM, "lead": LP_FULL_LEAD}[schedule]
+    run = _run(stream, flags, pops, stage, ev_begin, ev_end, stats)
     if device_ptrs:
         _check(library().lp_least_model(p.handle, _ptr(v0), _ptr(model_out), _ptr(iters_out),
                                          ctypes.byref(run)), "lp_least_model")

@@ -24,15 +24,30 @@ def _oracle_lm(P, v0=None):
     return oracle.pack_bits(model), stage, iters, oracle.popcounts_from_stage(stage, iters)
 
 
-def check_lm(P, v0=None, prog=None, variants=(False, True), jacobi=False, **kw):
+def check_lm(P, v0=None, prog=None, variants=(False, True), jacobi=False,
+             schedules=("auto", "stream", "lead"), **kw):
     om, ostage, oit, opops = _oracle_lm(P, v0)
     if jacobi:
         jm, jit, jpops, conv = oracle.lm_jacobi(P, v0=v0)
         assert conv and jit == oit and jpops == opops and (oracle.pack_bits(jm) == om).all()
     prog = prog or lp.Program(P, **kw)
+    runs = []
     for frontier in variants:
-        model, iters, ex = prog.least_model(v0, frontier=frontier, popcounts=True, stages=True)
-        tag = "frontier" if frontier else "full"
+        if frontier or prog.info["full_kernel"] == 1:
+            runs.append((frontier, "auto"))
+        else:   # every schedule of the full θ-pass (LEAD / STREAM passes) must agree
+            runs += [(False, s) for s in schedules]
+    for frontier, schedule in runs:
+        model, iters, ex = prog.least_model(v0, frontier=frontier, popcounts=True, stages=True,
+                                            schedule=schedule, stats=True)
+        tag = "frontier" if frontier else f"full/{schedule}"
+        st = ex["stats"]
+        if frontier or prog.info["full_kernel"] == 1:
+            assert st["bytes"] == 0
+        else:
+            assert 0 <= st["lead_passes"] <= iters, (tag, st)
+            assert st["lead_passes"] == {"stream": 0, "lead": iters}.get(schedule, st["lead_passes"])
+            assert st["bytes"] >= st["lead_passes"] * prog.info["lead_pass_bytes"]
         assert iters == oit, (tag, iters, oit)
         assert (model == om).all(), tag
         assert ex["popcounts"] == opops, tag
@@ -84,6 +99,10 @@ def test_forced_summary_mode_and_small_grids(seed, cfg):
     prog = check_lm(P, **cfg)
     if cfg.get("smem_bits_cap"):
         assert prog.info["truth_mode"] == 1 and prog.info["summary_shift"] >= 1
+        assert prog.info["key_shift"] >= 0          # LEAD passes stream the key plane
+    # a start set with atoms that are neither heads nor facts (coarse key groups)
+    v0 = rng.choice(n, size=n // 8, replace=False).tolist()
+    check_lm(P, v0=v0, prog=prog)
 
 
 @pytest.mark.parametrize("seed", range(12))
@@ -97,6 +116,22 @@ def test_tma_kernel_and_edge_grids(seed, cfg):
     P = lpgen.random_program(rng, n, 6 * n, max_len=9, n_facts=n // 30)
     prog = check_lm(P, **cfg)
     assert prog.info["full_kernel"] == 1
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("cfg", [dict(), dict(smem_bits_cap=256)])
+def test_auto_schedule_switches_mid_fixpoint(seed, cfg, monkeypatch):
+    """The auto schedule switches from LEAD to STREAM passes once a pass queues more
+    than n_slots / LP_DENSE_DIV rows; with a huge divisor the switch happens right after
+    the first pass that queues anything, so the fixpoint mixes both pass kinds."""
+    monkeypatch.setenv("LP_DENSE_DIV", str(10 ** 9))
+    rng = np.random.default_rng([seed, 4242])
+    n = int(rng.integers(2000, 5000))
+    P = lpgen.random_program(rng, n, 5 * n, max_len=5, n_facts=n // 10)
+    prog = lp.Program(P, **cfg)
+    _, iters, ex = prog.least_model(schedule="auto", stats=True)
+    assert 1 <= ex["stats"]["lead_passes"] < iters
+    check_lm(P, prog=prog, schedules=("auto",))
 
 
 def test_long_bodies_generic_path_and_u32_counters():
@@ -182,6 +217,7 @@ def test_config_c4_parity():
     P = lpgen.config("C4")
     prog = check_lm(P)
     assert prog.info["truth_mode"] == 1     # the 10M-atom truth vector is L2-resident
+    assert prog.info["key_shift"] >= 0
 
 
 # ---------------------------------------------------------------------------------

@@ -18,6 +18,8 @@ from paper_2009_10247_b200 import lp  # noqa: E402
 
 K = int(os.environ.get("STEPS", "20"))
 cfgs = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]
+SCHEDULES = os.environ.get("SCHEDULES", "auto,stream").split(",")
+GRID = int(os.environ.get("GRID", "0"))
 stream = torch.cuda.Stream()
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
 
@@ -41,7 +43,7 @@ def timed(fn, steps=K, warm=3):
 for cfg in cfgs:
     P = lpgen.config(cfg)
     t0 = time.perf_counter()
-    prog = lp.Program(P)
+    prog = lp.Program(P, grid_blocks=GRID)
     load_s = time.perf_counter() - t0
     info = prog.info
     if cfg == "C5":
@@ -60,15 +62,19 @@ for cfg in cfgs:
     Wm = lp.bits_words(P.n_atoms)
     model = torch.zeros(max(Wm, 1), dtype=torch.int64, device="cuda")
     iters = torch.zeros(1, dtype=torch.int32, device="cuda")
-    for frontier in (False, True):
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    variants = [(False, s) for s in SCHEDULES] + [(True, "auto")]
+    for frontier, sched in variants:
         ms, kms = timed(lambda a, b: lp.lp_least_model(prog, None, model, frontier=frontier, stream=stream,
-                                                       device_ptrs=True, iters_out=iters, ev_begin=a, ev_end=b))
+                                                       device_ptrs=True, iters_out=iters, ev_begin=a, ev_end=b,
+                                                       schedule=sched, stats=stats))
         it = int(iters.item())
-        rec = {"cfg": cfg, "variant": "frontier" if frontier else "full", "step_ms": ms, "kernel_ms": kms,
-               "iters": it, "nnz": info["nnz"], "nnz_iter_per_s": info["nnz"] * it / (ms / 1e3),
-               "load_s": load_s, "truth_mode": info["truth_mode"]}
+        rec = {"cfg": cfg, "variant": "frontier" if frontier else f"full/{sched}", "step_ms": ms,
+               "kernel_ms": kms, "iters": it, "nnz": info["nnz"], "nnz_iter_per_s": info["nnz"] * it / (ms / 1e3),
+               "load_s": load_s, "truth_mode": info["truth_mode"], "grid": info["grid_blocks"]}
         if not frontier:
-            rec["pass_GBps"] = info["pass_bytes"] * it / (kms / 1e3) / 1e9
-            rec["us_per_pass"] = kms * 1e3 / it
+            st = [int(x) for x in stats.tolist()]
+            rec.update(alg_bytes=st[0], lead_passes=st[1], rows_verified=st[2], entries_verified=st[3],
+                       GBps=st[0] / (kms / 1e3) / 1e9, us_per_pass=kms * 1e3 / it)
         print(json.dumps(rec), flush=True)
     prog.close()
