@@ -61,8 +61,11 @@ struct lp_program {
     // [12..14] rows queued per full θ-pass (slot k % 3)
     int32_t *d_scal = nullptr;
     unsigned long long *d_stats = nullptr;  // full θ-pass work statistics (lp_run.stats_out)
-    int32_t *d_keyplane = nullptr, *d_key_of = nullptr;  // summary-mode key plane
+    uint16_t *d_lead16 = nullptr;   // summary-mode key plane (low 16 bits of the lead group)
+    uint8_t *d_octet_tag = nullptr;
+    int32_t *d_key_of = nullptr;
     uint32_t *d_ksummary = nullptr;
+    int32_t *d_korder = nullptr;
     int32_t ksm_words = 0, kshift = 0;
     uint32_t *d_factbits = nullptr;
     uint64_t lm_runs = 0;
@@ -148,6 +151,7 @@ static lp_status upload(lp_program *p, T **out, const std::vector<T> &v) {
 // the lead plane (+ the head plane when the truth test is exact), a STREAM pass every
 // body plane (+ the head plane when exact).  Padding rows included.
 static uint64_t lead_plane_bytes(const lp_program *p) {
+    if (p->d_lead16) return 2ull * (uint64_t)p->L.n_slots + (uint64_t)p->L.n_slots / 8;   // key plane + tags
     uint64_t b = 4ull * (uint64_t)p->L.n_slots;
     return p->exact ? 2 * b : b;
 }
@@ -169,9 +173,6 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
     p->sms = sms;
 
-    TRY(upload(p, &p->d_segs, L.segs));
-    TRY(upload(p, &p->d_col, L.col));
-    TRY(upload(p, &p->d_head, L.head));
     TRY(upload(p, &p->d_facts, L.facts));
     p->nfacts = (int32_t)L.facts.size();
     TRY(upload(p, &p->d_negated, L.negated));
@@ -181,13 +182,6 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         for (size_t i = 0; i < L.free_j.size(); ++i) rank[L.free_j[i]] = (int32_t)i;
         TRY(upload(p, &p->d_negated_ext, ext));
         TRY(upload(p, &p->d_free_rank, rank));
-    }
-    if (L.has_occ) {
-        TRY(upload(p, &p->d_occ_ptr, L.occ_ptr));
-        TRY(upload(p, &p->d_occ_slot, L.occ_slot));
-        p->cnt_bytes = L.max_body <= 255 ? 1 : 4;
-        const size_t cw = p->cnt_bytes == 1 ? ((size_t)L.n_slots + 3) / 4 : (size_t)L.n_slots;
-        TRY(dalloc(p, &p->d_cnt, std::max<size_t>(cw, 1)));
     }
     // truth vector: bit a of word a>>5, padded to a multiple of 4 words (int4 loads)
     p->nwords = (int32_t)((((int64_t)L.n_ext + 31) / 32 + 3) / 4 * 4);
@@ -225,50 +219,93 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         }
         p->shift = sh;
         TRY(dalloc(p, &p->d_summary, p->sm_words));
+        CK(cudaMemset(p->d_summary, 0, (size_t)p->sm_words * 4));   // zero between calls
     }
     p->lm_smem = (size_t)p->sm_words * 4;
 
-    // key plane (summary mode, register-streaming kernel): the
-    // lead atom of every row is also stored as its key.  Atoms that can become true
-    // without v0 -- heads of stored rows, facts, abar, ⊤ -- get consecutive keys (fine
-    // summary groups); every other atom shares a key with up to 63 of its kind.
+    // key plane (summary mode, register-streaming kernel): every
+    // extended atom gets a key -- atoms that can become true without v0 (heads of stored
+    // rows, facts, abar, ⊤) consecutive keys, every other atom one key per 256 of its kind
+    // -- and the shared copy of v_k in LEAD passes is a summary over keys (bit g = keys
+    // g << kshift ..), with a per-bucket "any bit" mask on top.  The rows of every segment are bucketed (stably) by the high bits
+    // g >> 16 of their lead atom's group, so a LEAD pass streams only the low 16 bits: one
+    // uint16 per row, runs of one bucket padded to 8 rows.
     const bool want_keys = !p->exact && !(opt && (opt->flags & LP_LOAD_TMA)) &&
                            !std::getenv("LP_NO_KEYS");
+    std::vector<Run> runs;
     if (want_keys) {
         std::vector<uint8_t> der((size_t)L.n_ext, 0);
         for (int64_t s = 0; s < L.n_slots; ++s) der[(size_t)L.head[(size_t)s]] = 1;
         for (int32_t a : L.facts) der[(size_t)a] = 1;
         for (int32_t a = L.n; a < L.bot; ++a) der[(size_t)a] = 1;
         der[(size_t)L.bot] = 0;
-        std::vector<int32_t> key((size_t)L.n_ext);
-        int64_t nd = 0;
-        for (int32_t a = 0; a < L.n_ext; ++a)
-            if (der[(size_t)a]) key[(size_t)a] = (int32_t)nd++;
-        int64_t nu = 0;
-        for (int32_t a = 0; a < L.n_ext; ++a)
-            if (!der[(size_t)a]) key[(size_t)a] = (int32_t)(nd + (nu++ >> 6));
-        const int64_t nkeys = nd + (nu + 63) / 64;
+        // derivable keys [0, nd); the underivable ones (256 atoms per key) follow, starting
+        // at the next bucket boundary (a bucket = 2^16 summary groups) when that costs no
+        // coarser summary, so their buckets hold nothing else
+        int64_t nd = 0, nu = 0;
+        for (int32_t a = 0; a < L.n_ext; ++a) (der[(size_t)a] ? nd : nu)++;
         int64_t kcap = kKeySmemBytes;
         if (opt && opt->smem_bits_cap > 0) kcap = std::min<int64_t>(kcap, opt->smem_bits_cap / 8);
         kcap = std::max<int64_t>(kcap, 16);
+        auto words_for = [&](int64_t base, int s) {
+            const int64_t groups = (((base + (nu + 255) / 256) - 1) >> s) + 1;
+            return ((groups + 31) / 32 + 3) / 4 * 4;
+        };
         int sh = 0;
-        int64_t kw = 0;
-        for (;; ++sh) {
-            const int64_t groups = ((nkeys - 1) >> sh) + 1;
-            kw = ((groups + 31) / 32 + 3) / 4 * 4;
-            if (kw * 4 <= kcap) break;
+        while (words_for(nd, sh) * 4 > kcap) ++sh;
+        const int64_t span = (int64_t)1 << (16 + sh);
+        int64_t nd_pad = (nd + span - 1) / span * span;
+        if (words_for(nd_pad, sh) * 4 > kcap) nd_pad = nd;
+        const int64_t kw = words_for(nd_pad, sh);
+        const int64_t nkeys = nd_pad + (nu + 255) / 256;
+        std::vector<int32_t> key((size_t)L.n_ext);
+        {
+            int64_t id = 0, iu = 0;
+            for (int32_t a = 0; a < L.n_ext; ++a)
+                key[(size_t)a] = der[(size_t)a] ? (int32_t)id++ : (int32_t)(nd_pad + (iu++ >> 8));
         }
         p->kshift = sh;
         p->ksm_words = (int32_t)kw;
-        std::vector<int32_t> kp((size_t)std::max<int64_t>(L.n_slots, 1), key[(size_t)L.bot]);
-        for (const Segment &sg : L.segs)
-            for (int64_t i = 0; i < sg.count_pad; ++i)
-                kp[(size_t)(sg.slot_off + i)] = key[(size_t)L.col[(size_t)(sg.col_off + i)]];
-        TRY(upload(p, &p->d_keyplane, kp));
+        if ((((nkeys - 1) >> sh) >> 16) >= 32) return set_err(LP_E_INVALID, "internal: key bucket >= 32");
+        std::vector<int32_t> bucket((size_t)L.n_ext);
+        for (int32_t a = 0; a < L.n_ext; ++a) bucket[(size_t)a] = (key[(size_t)a] >> sh) >> 16;
+        bucket_rows(&L, bucket, 8, &runs);
+        std::vector<uint16_t> lead16((size_t)std::max<int64_t>(L.n_slots, 8), 0);
+        for (const Run &r : runs) {
+            const Segment &sg = L.segs[(size_t)r.seg];
+            for (int64_t i = 0; i < r.rows; ++i) {
+                const int64_t slot = r.slot_off + i;
+                const int32_t a = L.col[(size_t)(sg.col_off + (slot - sg.slot_off))];
+                lead16[(size_t)slot] = (uint16_t)((key[(size_t)a] >> sh) & 0xFFFF);
+            }
+        }
+        // one tag byte per octet: its bucket (all 8 rows share it) and trailing padding
+        std::vector<uint8_t> tag((size_t)std::max<int64_t>(L.n_slots / 8, 1), 0);
+        for (const Run &r : runs) {
+            for (int64_t o = r.slot_off / 8; o < (r.slot_off + r.rows_pad) / 8; ++o) tag[(size_t)o] = (uint8_t)r.bucket;
+            const int64_t pad = r.rows_pad - r.rows;
+            tag[(size_t)((r.slot_off + r.rows_pad) / 8 - 1)] |= (uint8_t)(pad << 5);
+        }
+        TRY(upload(p, &p->d_lead16, lead16));
+        TRY(upload(p, &p->d_octet_tag, tag));
         TRY(upload(p, &p->d_key_of, key));
         TRY(dalloc(p, &p->d_ksummary, (size_t)kw));
+        TRY(dalloc(p, &p->d_korder, (size_t)L.n_ext + 1));
         CK(cudaMemset(p->d_ksummary, 0, (size_t)kw * 4));
         p->lm_smem = std::max(p->lm_smem, (size_t)kw * 4);
+    }
+
+    // the program planes in their final row order
+    if (L.has_occ) build_occ_lists(&L);
+    TRY(upload(p, &p->d_segs, L.segs));
+    TRY(upload(p, &p->d_col, L.col));
+    TRY(upload(p, &p->d_head, L.head));
+    if (L.has_occ) {
+        TRY(upload(p, &p->d_occ_ptr, L.occ_ptr));
+        TRY(upload(p, &p->d_occ_slot, L.occ_slot));
+        p->cnt_bytes = L.max_body <= 255 ? 1 : 4;
+        const size_t cw = p->cnt_bytes == 1 ? ((size_t)L.n_slots + 3) / 4 : (size_t)L.n_slots;
+        TRY(dalloc(p, &p->d_cnt, std::max<size_t>(cw, 1)));
     }
 
     // stable path filter: one bit per extended atom (or per 2^any_shift atoms)
@@ -335,8 +372,12 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         else
             for (const Segment &sg : L.segs)
                 cap += 4 * (int64_t)kFullThreads * (((sg.count_pad >> 2) + gthreads - 1) / gthreads);
-        if (cap + 4 > (1 << 28)) return set_err(LP_E_NOMEM, "candidate queue too large");
-        p->qcap = (int32_t)std::max<int64_t>(cap + 4, 1024);
+        // key-mode LEAD passes: octets are dealt cyclically over all threads
+        int64_t octets = 0;
+        for (const Run &r : runs) octets += r.rows_pad >> 3;
+        cap = std::max<int64_t>(cap, 8 * (int64_t)kFullThreads * ((octets + gthreads - 1) / gthreads));
+        if (cap + 8 > (1 << 28)) return set_err(LP_E_NOMEM, "candidate queue too large");
+        p->qcap = (int32_t)std::max<int64_t>(cap + 8, 1024);
         TRY(dalloc(p, &p->d_qbuf, (size_t)p->lm_blocks * p->qcap));
     }
     p->fr_blocks = cap_grid(sms * bf);
@@ -429,7 +470,7 @@ extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
     o->lead_pass_bytes = (int64_t)lead_plane_bytes(p);
     o->stream_pass_bytes = (int64_t)stream_plane_bytes(p);
     o->truth_mode = p->exact ? 0 : 1;
-    o->key_shift = p->d_keyplane ? p->kshift : -1;
+    o->key_shift = p->d_lead16 ? p->kshift : -1;
     o->summary_shift = p->shift;
     o->grid_blocks = p->lm_blocks;
     o->full_kernel = p->use_tma ? 1 : 0;
@@ -552,9 +593,11 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
         stats_dev = nullptr;
     }
     q.stats = stats_dev;
-    q.keyplane = (frontier || p->use_tma) ? nullptr : p->d_keyplane;
+    q.lead16 = (frontier || p->use_tma) ? nullptr : p->d_lead16;
+    q.octet_tag = p->d_octet_tag;
     q.key_of = p->d_key_of;
     q.ksummary = p->d_ksummary;
+    q.korder = p->d_korder;
     q.ksm_words = p->ksm_words;
     q.kshift = p->kshift;
     q.lead_bytes = (long long)lead_plane_bytes(p);
@@ -746,7 +789,8 @@ extern "C" const char *lp_status_str(lp_status s) {
 
 extern "C" const char *lp_last_error(void) { return g_err.c_str(); }
 
-// Profiling hook, not part of include/lp.h: a device buffer of 16 passes x grid x 4
-// uint64 %globaltimer stamps per CTA (pass start, last warp done, CTA done, barrier
-// exit) filled by the next full θ-pass launch; NULL disables.
+// Profiling hook, not part of include/lp.h: a device buffer of [16 passes][grid][8]
+// uint64 %globaltimer stamps per CTA (pass top, stream start, stream done, verify done,
+// CTA done, barrier exit; the TMA kernel fills 0, 2, 4, 5) written by the next full
+// θ-pass launch; NULL disables.
 extern "C" void lpdbg_set_timing(void *buf) { set_debug_timing((unsigned long long *)buf); }

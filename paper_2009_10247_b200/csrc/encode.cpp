@@ -180,25 +180,95 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *
         L->head[sg.slot_off + slot] = r->head[i];
     }
 
-    // ---- transposed occurrence lists (frontier variant) ----------
+    // the transposed occurrence lists (frontier variant) are built by the loader after
+    // the final row order is fixed (build_occ_lists)
     L->has_occ = build_occ;
-    if (build_occ) {
-        L->occ_ptr.assign((size_t)L->n_ext + 1, 0);
-        for (const Segment &sg : L->segs)
-            for (int32_t j = 0; j < sg.L; ++j) {
-                const int32_t *c = L->col.data() + sg.col_off + (int64_t)j * sg.count_pad;
-                for (int64_t i = 0; i < sg.count; ++i) L->occ_ptr[c[i] + 1]++;
-            }
-        for (int32_t a = 0; a < L->n_ext; ++a) L->occ_ptr[a + 1] += L->occ_ptr[a];
-        L->occ_slot.assign((size_t)std::max<int64_t>(L->occ_ptr[L->n_ext], 1), 0);
-        std::vector<int64_t> fo(L->occ_ptr.begin(), L->occ_ptr.end() - 1);
-        for (const Segment &sg : L->segs)
-            for (int32_t j = 0; j < sg.L; ++j) {
-                const int32_t *c = L->col.data() + sg.col_off + (int64_t)j * sg.count_pad;
-                for (int64_t i = 0; i < sg.count; ++i) L->occ_slot[fo[c[i]]++] = (int32_t)(sg.slot_off + i);
-            }
-    }
     return LP_OK;
+}
+
+// Transposed occurrence lists over extended atoms (frontier variant, SURVEY.md §8(a)
+// a6): occ_slot[occ_ptr[a] .. occ_ptr[a+1]) = the slots whose body contains a.  Padding
+// rows (body ⊥) are skipped.
+void build_occ_lists(HostLayout *L) {
+    L->occ_ptr.assign((size_t)L->n_ext + 1, 0);
+    for (const Segment &sg : L->segs)
+        for (int32_t j = 0; j < sg.L; ++j) {
+            const int32_t *c = L->col.data() + sg.col_off + (int64_t)j * sg.count_pad;
+            for (int64_t i = 0; i < sg.count_pad; ++i)
+                if (c[i] != L->bot) L->occ_ptr[(size_t)c[i] + 1]++;
+        }
+    for (int32_t a = 0; a < L->n_ext; ++a) L->occ_ptr[(size_t)a + 1] += L->occ_ptr[(size_t)a];
+    L->occ_slot.assign((size_t)std::max<int64_t>(L->occ_ptr[(size_t)L->n_ext], 1), 0);
+    std::vector<int64_t> fo(L->occ_ptr.begin(), L->occ_ptr.end() - 1);
+    for (const Segment &sg : L->segs)
+        for (int32_t j = 0; j < sg.L; ++j) {
+            const int32_t *c = L->col.data() + sg.col_off + (int64_t)j * sg.count_pad;
+            for (int64_t i = 0; i < sg.count_pad; ++i)
+                if (c[i] != L->bot) L->occ_slot[(size_t)fo[(size_t)c[i]]++] = (int32_t)(sg.slot_off + i);
+        }
+}
+
+// Stable reorder of the rows of every segment by bucket(lead atom); every bucket's run
+// is padded with ⊥ rows to a multiple of `align` rows (the AND-rows of a segment are in
+// no particular order, so this changes no result).  Segment offsets are recomputed; the
+// run table lists (segment, bucket, first slot, real rows, padded rows) in slot order.
+void bucket_rows(HostLayout *L, const std::vector<int32_t> &bucket_of_atom, int align,
+                 std::vector<Run> *runs) {
+    std::vector<Segment> segs;
+    std::vector<int32_t> col, head;
+    int64_t col_off = 0, slot_off = 0;
+    runs->clear();
+    // pass 1: sizes
+    std::vector<std::vector<int64_t>> counts(L->segs.size());
+    int32_t nb = 0;
+    for (int32_t x : bucket_of_atom) nb = std::max(nb, x + 1);
+    for (size_t s = 0; s < L->segs.size(); ++s) {
+        const Segment &sg = L->segs[s];
+        counts[s].assign((size_t)nb, 0);
+        const int32_t *c0 = L->col.data() + sg.col_off;
+        for (int64_t i = 0; i < sg.count_pad; ++i)
+            if (c0[i] != L->bot) counts[s][(size_t)bucket_of_atom[(size_t)c0[i]]]++;
+        Segment ns = sg;
+        ns.count = 0;
+        ns.count_pad = 0;
+        for (int32_t b = 0; b < nb; ++b) {
+            const int64_t n = counts[s][(size_t)b];
+            if (!n) continue;
+            const int64_t np = (n + align - 1) / align * align;
+            runs->push_back(Run{(int32_t)s, b, slot_off + ns.count_pad, n, np});
+            ns.count += n;
+            ns.count_pad += np;
+        }
+        ns.col_off = col_off;
+        ns.slot_off = slot_off;
+        col_off += (int64_t)ns.L * ns.count_pad;
+        slot_off += ns.count_pad;
+        segs.push_back(ns);
+    }
+    col.assign((size_t)col_off, L->bot);
+    head.assign((size_t)slot_off, L->bot);
+    // pass 2: stable scatter (bucket runs in ascending bucket order inside each segment)
+    size_t ri = 0;
+    for (size_t s = 0; s < L->segs.size(); ++s) {
+        const Segment &sg = L->segs[s];
+        const Segment &ns = segs[s];
+        std::vector<int64_t> next((size_t)nb, -1);
+        for (; ri < runs->size() && (*runs)[ri].seg == (int32_t)s; ++ri)
+            next[(size_t)(*runs)[ri].bucket] = (*runs)[ri].slot_off - ns.slot_off;
+        const int32_t *c0 = L->col.data() + sg.col_off;
+        for (int64_t i = 0; i < sg.count_pad; ++i) {
+            if (c0[i] == L->bot) continue;
+            const int64_t d = next[(size_t)bucket_of_atom[(size_t)c0[i]]]++;
+            for (int32_t j = 0; j < sg.L; ++j)
+                col[(size_t)(ns.col_off + (int64_t)j * ns.count_pad + d)] =
+                    L->col[(size_t)(sg.col_off + (int64_t)j * sg.count_pad + i)];
+            head[(size_t)(ns.slot_off + d)] = L->head[(size_t)(sg.slot_off + i)];
+        }
+    }
+    L->segs.swap(segs);
+    L->col.swap(col);
+    L->head.swap(head);
+    L->n_slots = slot_off;
 }
 
 }  // namespace lpb

@@ -53,13 +53,52 @@ __device__ __forceinline__ bool sm_bit(const uint32_t *sm, uint32_t x) {
 // least model: initial vector
 // ------------------------------------------------------------------------------------
 
+// Copy nw (multiple of 4) 32-bit words global -> shared with 16-byte loads, 4 in flight.
+__device__ __forceinline__ void smem_fill(uint32_t *sm, const uint32_t *src, int32_t nw) {
+    const int4 *s4 = reinterpret_cast<const int4 *>(src);
+    int4 *d4 = reinterpret_cast<int4 *>(sm);
+    const int32_t n4 = nw >> 2;
+    for (int32_t i0 = threadIdx.x; i0 < n4; i0 += 4 * blockDim.x) {
+        int4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int32_t i = i0 + u * blockDim.x;
+            v[u] = i < n4 ? __ldcg(s4 + i) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int32_t i = i0 + u * blockDim.x;
+            if (i < n4) d4[i] = v[u];
+        }
+    }
+}
+
+// Reserve `cnt` consecutive slots of the derivation list for every lane of a FULL warp
+// with one atomic per warp (the list tail is a single hot address).
+__device__ __forceinline__ int32_t warp_reserve(int32_t *tail, int32_t cnt) {
+    const int lane = threadIdx.x & 31;
+    int32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    int32_t base = 0;
+    if (total) {
+        if (lane == 31) base = atomicAdd(tail, total);
+        base = __shfl_sync(0xFFFFFFFFu, base, 31);
+    }
+    return base + incl - cnt;
+}
+
 // In-kernel prologue of every least-model kernel (no separate init launches):
 //   v_0 word w = (v0[w] restricted to original atoms) | facts[w] | ⊤,
-// written to both buffers; the thread that builds a word also lists its original atoms
-// into the derivation list, writes their stages (0, or -1 for false atoms) and, in
-// summary mode, ORs the word's groups into the summary word it owns.  Work item = one
-// summary word (2^shift truth words) in summary mode, one truth word otherwise, so no
-// two threads touch the same summary word and no grid barrier is needed inside.
+// written to both buffers.  Warps walk consecutive truth words (coalesced); each lane
+// lists the original atoms of its word into the derivation list (slots reserved once
+// per warp), writes their stages (0, or -1 for false atoms; one coalesced row per word
+// of the warp) and, in summary mode, adds the word to the key-space summary (LEAD
+// passes) and/or the atom-id summary (STREAM passes), both zero on entry.
 // Also zeroes the other-parity run counters for the next call.
 __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, int64_t gtid,
                                          int64_t gthreads) {
@@ -67,55 +106,72 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
         *p.tail_next = 0;
         *p.status_next = 0;
     }
-    if (summary_mode && p.keyplane && gtid == 0) {          // ⊤ is always true
+    const bool keys = summary_mode && p.lead16;
+    const bool osum = summary_mode && !(keys && p.pass_mode != 2);
+    if (keys && gtid == 0) {          // ⊤ is always true
         const uint32_t g = (uint32_t)__ldg(p.key_of + p.top) >> p.kshift;
         atomicOr(p.ksummary + (g >> 5), 1u << (g & 31));
     }
-    const int wpi = summary_mode ? (1 << p.shift) : 1;     // truth words per item (shift <= 31)
-    const int64_t items = summary_mode ? p.sm_words : p.nwords;
-    for (int64_t it = gtid; it < items; it += gthreads) {
-        uint32_t sumw = 0;
-        for (int x = 0; x < wpi; ++x) {
-            const int64_t w = it * wpi + x;
-            if (w >= p.nwords) break;
-            const int64_t lo = w * 32;
-            uint32_t orig = p.factbits[w];
-            if (p.v0 && w < p.v0_words && lo < p.n) orig |= p.v0[w];
+    const int lane = threadIdx.x & 31;
+    for (int64_t w0 = gtid - lane; w0 < p.nwords; w0 += gthreads) {
+        const int64_t w = w0 + lane;
+        const int64_t lo = w * 32;
+        uint32_t orig = 0, bits = 0;
+        if (w < p.nwords) {
+            orig = __ldg(p.factbits + w);
+            if (p.v0 && w < p.v0_words && lo < p.n) orig |= __ldg(p.v0 + w);
             if (lo + 32 > p.n) orig &= lo >= p.n ? 0u : ((1u << (uint32_t)(p.n - lo)) - 1u);
-            uint32_t bits = orig;
+            bits = orig;
             if (w == (p.top >> 5)) bits |= 1u << (p.top & 31);
             p.buf0[w] = bits;
             p.buf1[w] = bits;
-            if (orig) {
-                int32_t pos = atomicAdd(p.tail, __popc(orig));
-                uint32_t b = orig;
-                while (b) {
-                    const int i = __ffs(b) - 1;
-                    b &= b - 1;
-                    p.order[pos++] = (int32_t)(lo + i);
-                    if (summary_mode && p.keyplane) {   // key-space summary of v_0
-                        const uint32_t g = (uint32_t)__ldg(p.key_of + lo + i) >> p.kshift;
-                        atomicOr(p.ksummary + (g >> 5), 1u << (g & 31));
-                    }
-                }
+        }
+        int32_t pos = warp_reserve(p.tail, __popc(orig));
+        for (uint32_t b = orig; b;) {
+            const int i = __ffs(b) - 1;
+            b &= b - 1;
+            if (keys) {
+                const int32_t key = __ldg(p.key_of + lo + i);
+                const uint32_t g = (uint32_t)key >> p.kshift;
+                atomicOr(p.ksummary + (g >> 5), 1u << (g & 31));
+                p.korder[pos] = key;
             }
-            if (p.stage && lo < p.n) {
-                const int m = (int)(p.n - lo < 32 ? p.n - lo : 32);
-                for (int i = 0; i < m; ++i) p.stage[lo + i] = ((orig >> i) & 1u) ? 0 : -1;
-            }
-            if (summary_mode && bits) {
-                if (p.shift >= 5) {
-                    sumw |= 1u << ((uint32_t)(lo >> p.shift) & 31u);
-                } else {
-                    const int gs = 1 << p.shift;
-                    const uint32_t gm = (gs == 32) ? ~0u : ((1u << gs) - 1u);
-                    for (int i = 0; i < 32 / gs; ++i)
-                        if ((bits >> (i * gs)) & gm) sumw |= 1u << ((uint32_t)((lo >> p.shift) + i) & 31u);
-                }
+            p.order[pos++] = (int32_t)(lo + i);
+        }
+        if (p.stage) {   // row i of the warp's 32x32 block = word w0+i, lane = bit
+            for (int i = 0; i < 32; ++i) {
+                const uint32_t oi = __shfl_sync(0xFFFFFFFFu, orig, i);
+                const int64_t a = (w0 + i) * 32 + lane;
+                if (a < p.n) p.stage[a] = ((oi >> lane) & 1u) ? 0 : -1;
             }
         }
-        if (summary_mode) p.summary[it] = sumw;
+        if (osum) {   // word w contributes to atom-id summary word w >> shift
+            uint32_t c = 0;
+            if (bits) {
+                if (p.shift >= 5) {
+                    c = 1u << ((uint32_t)(w >> (p.shift - 5)) & 31u);
+                } else {
+                    const int gs = 1 << p.shift;
+                    const uint32_t gm = (1u << gs) - 1u;
+                    for (int i = 0; i < 32 / gs; ++i)
+                        if ((bits >> (i * gs)) & gm) c |= 1u << ((uint32_t)((lo >> p.shift) + i) & 31u);
+                }
+            }
+            const int span = p.shift >= 5 ? 32 : (1 << p.shift);   // lanes per summary word
+            for (int o = 1; o < span; o <<= 1) c |= __shfl_xor_sync(0xFFFFFFFFu, c, o);
+            if ((lane & (span - 1)) == 0 && c) atomicOr(p.summary + (w >> p.shift), c);
+        }
     }
+}
+
+// The summaries are zero on entry to the next call (the prologue ORs into them).
+__device__ __forceinline__ void lm_zero_summaries(const LMParams &p, bool summary_mode, int64_t gtid,
+                                                  int64_t gthreads) {
+    if (!summary_mode) return;
+    if (p.lead16)
+        for (int64_t w = gtid; w < p.ksm_words; w += gthreads) p.ksummary[w] = 0u;
+    if (!(p.lead16 && p.pass_mode != 2))
+        for (int64_t w = gtid; w < p.sm_words; w += gthreads) p.summary[w] = 0u;
 }
 
 // In-kernel epilogue: the model over the original atoms, LSB-first uint64 words.
@@ -141,6 +197,7 @@ struct PassCtx {
     int32_t *qbuf;       // this CTA's candidate queue (global, FILTER mode)
     int32_t *qcount;     // its fill counter (shared memory)
     int k;
+    const uint32_t *bmask;  // key mode: bit b = some summary bit of bucket b is set (shared)
 };
 
 // Smem test of 4 AND-rows at one body position; `fire` bit e = row e still alive.
@@ -162,8 +219,15 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
     if (cur_word & bit) return;                            // already in v_k
     const uint32_t old = atomicOr(c.wr + (h >> 5), bit);
     if (old & bit) return;                                 // another row set it this pass
-    const int32_t pos = atomicAdd(p.tail, 1);
+    // one list reservation per group of converged lanes (the tail is one hot address)
+    const unsigned m = __activemask();
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int32_t base = 0;
+    if (lane == leader) base = atomicAdd(p.tail, __popc(m));
+    base = __shfl_sync(m, base, leader);
+    const int32_t pos = base + __popc(m & ((1u << lane) - 1u));
     p.order[pos] = h;
+    if (p.lead16) p.korder[pos] = __ldg(p.key_of + h);   // once per atom, not per CTA
     if (p.stage) p.stage[h] = c.k + 1;
 }
 
@@ -182,20 +246,32 @@ __device__ __noinline__ int verify_slot(const LMParams &p, const PassCtx &c, int
     const int32_t L = __ldg(&p.segs[lo].L);
     const int64_t cp = __ldg(&p.segs[lo].count_pad);
     const int32_t *colp = p.col + __ldg(&p.segs[lo].col_off) + (slot - __ldg(&p.segs[lo].slot_off));
+    // the head and up to 8 body atoms are loaded together (one memory round trip),
+    // then their truth words (a second one)
+    constexpr int B = 8;
+    uint32_t a[B], w[B];
     const int32_t h = __ldg(p.head + slot);
-    const uint32_t hw = EXACT ? c.sm[h >> 5] : __ldcg(c.rd + (h >> 5));
-    if ((hw >> (h & 31)) & 1u) return 0;
-    bool ok = true;
-    int loaded = 0;
-    for (int32_t jb = j0; jb < L && ok; jb += 4) {
-        uint32_t a[4], w[4];
+    const int n1 = min(B, L - j0);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) a[j] = jb + j < L ? (uint32_t)__ldg(colp + (int64_t)(jb + j) * cp) : 0u;
+    for (int j = 0; j < B; ++j) a[j] = j < n1 ? (uint32_t)__ldg(colp + (int64_t)(j0 + j) * cp) : 0u;
+    const uint32_t hw = EXACT ? c.sm[h >> 5] : __ldcg(c.rd + (h >> 5));
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+        w[j] = j < n1 ? (EXACT ? c.sm[a[j] >> 5] : __ldcg(c.rd + (a[j] >> 5))) : ~0u;
+    if ((hw >> (h & 31)) & 1u) return n1;     // head already in v_k: the row changes nothing
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < B; ++j) ok = ok && ((w[j] >> (a[j] & 31)) & 1u);
+    int loaded = n1;
+    for (int32_t jb = j0 + B; jb < L && ok; jb += 4) {   // bodies longer than 8
+        uint32_t x[4], y[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = jb + j < L ? (uint32_t)__ldg(colp + (int64_t)(jb + j) * cp) : 0u;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            w[j] = jb + j < L ? (EXACT ? c.sm[a[j] >> 5] : __ldcg(c.rd + (a[j] >> 5))) : ~0u;
+            y[j] = jb + j < L ? (EXACT ? c.sm[x[j] >> 5] : __ldcg(c.rd + (x[j] >> 5))) : ~0u;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ok = ok && ((w[j] >> (a[j] & 31)) & 1u);
+        for (int j = 0; j < 4; ++j) ok = ok && ((y[j] >> (x[j] & 31)) & 1u);
         loaded += min(4, L - jb);
     }
     if (ok) emit_head(p, c, h, hw);
@@ -295,9 +371,8 @@ __device__ __forceinline__ void seg_lead(const LMParams &p, const Segment &sg, c
                                          int32_t gtid, int32_t gthreads) {
     const int32_t nq = (int32_t)(sg.count_pad >> 2);
     const int32_t slot0 = (int32_t)sg.slot_off;
-    const bool keys = !EXACT && p.keyplane;
-    const int shift = keys ? p.kshift : p.shift;
-    const int4 *base = reinterpret_cast<const int4 *>(keys ? p.keyplane + sg.slot_off : p.col + sg.col_off);
+    const int shift = p.shift;
+    const int4 *base = reinterpret_cast<const int4 *>(p.col + sg.col_off);
     const int4 *hbase = reinterpret_cast<const int4 *>(p.head + sg.slot_off);
     for (int32_t q0 = gtid; q0 < nq; q0 += gthreads * U) {
         int4 v[U];
@@ -323,6 +398,53 @@ __device__ __forceinline__ void seg_lead(const LMParams &p, const Segment &sg, c
     }
 }
 
+// LEAD pass in key mode: stream the uint16 key plane, 8 rows (one octet) per 16-byte
+// load plus the octet's tag byte (bucket = high bits of the key group, and the number of
+// trailing padding rows), U octets in flight per thread.  Row i is alive iff summary bit
+// (bucket << 16 | lead16[i]) is set.  Thread t takes octets t, t + gthreads, ...
+template <int U>
+__device__ __forceinline__ void octets_lead(const LMParams &p, const PassCtx &c, int64_t gtid,
+                                            int64_t gthreads) {
+    const int32_t no = (int32_t)(p.n_slots >> 3);
+    const int32_t gth = (int32_t)gthreads;
+    const int4 *base = reinterpret_cast<const int4 *>(p.lead16);
+    for (int32_t q0 = (int32_t)gtid; q0 < no; q0 += gth * U) {
+        int4 v[U];
+        uint32_t tag[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t q = q0 + u * gth;
+            v[u] = q < no ? ld_stream(base + q) : make_int4(0, 0, 0, 0);
+            tag[u] = q < no ? (uint32_t)__ldg(p.octet_tag + q) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t q = q0 + u * gth;
+            if (q >= no) break;
+            const uint32_t b = tag[u] & 31u;
+            if (!((*c.bmask >> b) & 1u)) continue;            // bucket with no true key
+            const uint32_t hi = b << 16;
+            const uint32_t w[4] = {(uint32_t)v[u].x, (uint32_t)v[u].y, (uint32_t)v[u].z, (uint32_t)v[u].w};
+            unsigned fire = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                fire |= (unsigned)sm_bit(c.sm, hi | (w[e] & 0xFFFFu)) << (2 * e);
+                fire |= (unsigned)sm_bit(c.sm, hi | (w[e] >> 16)) << (2 * e + 1);
+            }
+            fire &= 0xFFu >> (tag[u] >> 5);                   // trailing padding rows
+            if (fire) {
+                int32_t pos = atomicAdd(c.qcount, __popc(fire));
+                if (pos + __popc(fire) > p.qcap) {
+                    atomicExch(p.status_out, 2);
+                    continue;
+                }
+                const int32_t s0 = q * 8;
+                for (unsigned f = fire; f; f &= f - 1) c.qbuf[pos++] = s0 + __ffs(f) - 1;
+            }
+        }
+    }
+}
+
 // Segment s starts at the thread after the one that took the last quad of segment s-1,
 // so short segments spread over the whole grid instead of piling onto the lowest ids.
 template <bool EXACT, bool LEAD>
@@ -335,7 +457,7 @@ __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c
         const int32_t gt = (int32_t)gtid >= off ? (int32_t)gtid - off : (int32_t)gtid - off + gth;
         off = (int32_t)(((int64_t)off + (sg.count_pad >> 2)) % gth);
         const int32_t gthreads = gth;
-        if (LEAD) {
+        if (LEAD) {   // (key mode streams runs instead, see the caller)
             seg_lead<EXACT ? 4 : 8, EXACT>(p, sg, c, gt, gthreads);
             continue;
         }
@@ -367,11 +489,13 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     extern __shared__ uint32_t sm[];
     __shared__ int32_t qcount;
     __shared__ unsigned long long loaded_cta;
+    __shared__ uint32_t bmask;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const bool lead = blockIdx.x == 0 && tid == 0;
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 6] = globaltimer();
 
     lm_prologue(p, !EXACT, gtid, gthreads);            // v_0 (row a3), in-kernel
     if (gtid == 0) {
@@ -382,13 +506,23 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             for (int i = 0; i < 4; ++i) p.stats[i] = 0;
     }
     grid.sync();
+    if (p.dbg && tid == 0) p.dbg[(2 * gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
     bool lead_pass = p.pass_mode != 2;
-    bool keys = !EXACT && p.keyplane && lead_pass;       // shared copy is in key space
+    bool keys = !EXACT && p.lead16 && lead_pass;         // shared copy is in key space
     bool rebuild = false;                                // key space -> atom-id summary
     {
         const uint32_t *src0 = EXACT ? p.buf0 : keys ? p.ksummary : p.summary;
         const int32_t nw0 = keys ? p.ksm_words : p.sm_words;
-        for (int32_t w = tid; w < nw0; w += blockDim.x) sm[w] = __ldcg(src0 + w);
+        if (tid == 0) bmask = 0u;
+        smem_fill(sm, src0, nw0);
+        if (keys) {   // bucket mask: bucket b = summary words [b << 11, (b + 1) << 11)
+            __syncthreads();
+            uint32_t m = 0;
+            for (int32_t w = tid; w < nw0; w += blockDim.x)
+                if (sm[w]) m |= 1u << ((w >> 11) & 31);
+            m = __reduce_or_sync(0xFFFFFFFFu, m);
+            if ((tid & 31) == 0 && m) atomicOr(&bmask, m);
+        }
     }
     const int32_t n0 = __ldcg(p.tail);
     if (lead && p.pops && p.pop_cap > 0) p.pops[0] = n0;
@@ -397,11 +531,14 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         loaded_cta = 0;
     }
     __syncthreads();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 7] = globaltimer();
 
     int32_t ds = n0, de = n0;  // atoms that became true in the previous pass
     for (int k = 0;; ++k) {
         const uint32_t *rd = (k & 1) ? p.buf1 : p.buf0;
         uint32_t *wr = (k & 1) ? p.buf0 : p.buf1;
+#define DBG_STAMP(i) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + (i)]
+        if (p.dbg && tid == 0 && k < 16) DBG_STAMP(0) = globaltimer();
         if (k > 0) {
             // wr holds v_{k-1}: add the atoms derived in pass k-1 to make it v_k
             for (int64_t i = ds + gtid; i < de; i += gthreads) {
@@ -432,10 +569,31 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                     }
                 }
             } else {
-                for (int64_t i = ds + tid; i < de; i += blockDim.x) {
-                    const uint32_t a = (uint32_t)__ldcg(p.order + i);
-                    const uint32_t g = EXACT ? a : keys ? ((uint32_t)__ldg(p.key_of + a) >> p.kshift) : (a >> p.shift);
-                    atomicOr(sm + (g >> 5), 1u << (g & 31));
+                // 4 independent list reads (and key lookups) in flight per thread
+                for (int64_t i0 = ds + tid; i0 < de; i0 += 4 * (int64_t)blockDim.x) {
+                    uint32_t a[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t i = i0 + u * (int64_t)blockDim.x;
+                        a[u] = i < de ? (uint32_t)__ldcg((keys ? p.korder : p.order) + i) : 0xFFFFFFFFu;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (a[u] == 0xFFFFFFFFu) continue;
+                        a[u] = EXACT ? a[u] : keys ? (a[u] >> p.kshift) : (a[u] >> p.shift);
+                    }
+                    uint32_t m = 0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (a[u] != 0xFFFFFFFFu) {
+                            atomicOr(sm + (a[u] >> 5), 1u << (a[u] & 31));
+                            m |= 1u << ((a[u] >> 16) & 31);
+                        }
+                    if (!EXACT && keys) {   // (lanes of a warp may have left the loop already)
+                        const unsigned act = __activemask();
+                        m = __reduce_or_sync(act, m);
+                        if ((tid & 31) == __ffs(act) - 1 && m) atomicOr(&bmask, m);
+                    }
                 }
             }
             __syncthreads();
@@ -443,10 +601,12 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         // rows queued in pass k are counted in cand[k % 3]; the slot of pass k+1 was last
         // read before the previous barrier and is first written after the next one
         if (lead) p.cand[(k + 1) % 3] = 0;
-        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k};
-        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 0] = globaltimer();
-        if (lead_pass) all_segments<EXACT, true>(p, c, gtid, gthreads);
+        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, &bmask};
+        if (p.dbg && tid == 0 && k < 16) DBG_STAMP(1) = globaltimer();
+        if (!EXACT && keys) octets_lead<4>(p, c, gtid, gthreads);
+        else if (lead_pass) all_segments<EXACT, true>(p, c, gtid, gthreads);
         else all_segments<EXACT, false>(p, c, gtid, gthreads);
+        if (p.dbg && k < 16 && (tid & 31) == 0) atomicMax(&DBG_STAMP(2), globaltimer());
         if (!EXACT || lead_pass) {  // epilogue: verify this CTA's queued rows
             __syncthreads();
             const int32_t nc = min(qcount, p.qcap);
@@ -465,9 +625,9 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             }
         }
         if (p.dbg && k < 16) {
-            if ((tid & 31) == 0) atomicMax(p.dbg + (k * gridDim.x + blockIdx.x) * 4 + 1, globaltimer());
+            if ((tid & 31) == 0) atomicMax(&DBG_STAMP(3), globaltimer());
             __syncthreads();
-            if (tid == 0) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 2] = globaltimer();
+            if (tid == 0) DBG_STAMP(4) = globaltimer();
         }
         if (p.stats) {
             __syncthreads();
@@ -477,7 +637,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             }
         }
         grid.sync();
-        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 3] = globaltimer();
+        if (p.dbg && tid == 0 && k < 16) DBG_STAMP(5) = globaltimer();
+#undef DBG_STAMP
         const int32_t t = __ldcg(p.tail);
         const int32_t queued = __ldcg(p.cand + k % 3);
         if (lead && p.stats) {
@@ -495,9 +656,13 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                 if (t != de) atomicMax(p.status_out, 1);
                 if (p.stats) p.stats[0] += 4ull * p.stats[3];
             }
-            if (!EXACT && p.keyplane)   // the next call scatters v_0 into a zero summary
-                for (int64_t w = gtid; w < p.ksm_words; w += gthreads) p.ksummary[w] = 0u;
+            if (p.dbg && tid == 0) p.dbg[(gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
+            lm_zero_summaries(p, !EXACT, gtid, gthreads);
             lm_extract(p, gtid, gthreads);
+            if (p.dbg) {
+                __syncthreads();
+                if (tid == 0) p.dbg[(gridDim.x + blockIdx.x) * 8 + 7] = globaltimer();
+            }
             return;
         }
         if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
@@ -631,7 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
     lm_prologue(p, !EXACT, gtid, gthreads);
     grid.sync();
     const uint32_t *src0 = EXACT ? p.buf0 : p.summary;
-    for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(src0 + w);
+    smem_fill(sm, src0, p.sm_words);
     for (int i = tid; i < p.ntseg; i += blockDim.x) ts[i] = p.tsegs[i];
     const int32_t n0 = __ldcg(p.tail);
     if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = n0;
@@ -700,8 +865,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
             }
             __syncthreads();
         }
-        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k};
-        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 0] = globaltimer();
+        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, nullptr};
+        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + 0] = globaltimer();
         if (producer) {
             if (lane == 0) {
                 // the rest of this pass, then the first W tiles of the next pass (the
@@ -747,12 +912,12 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
             for (int32_t i = tid; i < nc; i += blockDim.x) verify_slot<false>(p, c, __ldcg(c.qbuf + i), 0);
         }
         if (p.dbg && k < 16) {
-            if ((tid & 31) == 0 && !producer) atomicMax(p.dbg + (k * gridDim.x + blockIdx.x) * 4 + 1, globaltimer());
+            if ((tid & 31) == 0 && !producer) atomicMax(p.dbg + (k * gridDim.x + blockIdx.x) * 8 + 2, globaltimer());
             __syncthreads();
-            if (tid == 0) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 2] = globaltimer();
+            if (tid == 0) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + 4] = globaltimer();
         }
         grid.sync();
-        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 4 + 3] = globaltimer();
+        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + 5] = globaltimer();
         const int32_t t = __ldcg(p.tail);
         const bool lead = blockIdx.x == 0 && tid == 0;
         const bool done = (t == de) || (k + 1 >= p.max_passes);
@@ -767,6 +932,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
                     const uint64_t q = q_cons + (uint64_t)x;
                     mbar_wait(full + (q % (uint64_t)S), (uint32_t)((q / S) & 1));
                 }
+            lm_zero_summaries(p, !EXACT, gtid, gthreads);
             lm_extract(p, gtid, gthreads);
             return;
         }

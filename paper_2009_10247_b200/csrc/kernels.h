@@ -13,7 +13,7 @@ constexpr int kThreads = 1024;          // persistent kernels: 32 warps per CTA
 // per thread measured no faster on C4 and slower on C3.)
 constexpr int kFullThreads = 1024;
 constexpr int kMaxSmemBytes = 200 * 1024;
-constexpr int kKeySmemBytes = 216 * 1024;   // key-space summary (register-streaming kernel only)
+constexpr int kKeySmemBytes = 220 * 1024;   // key-space summary (register-streaming kernel only)
 
 constexpr int kStageBytes = 16384;      // one TMA pipeline stage (bulk copies of col rows)
 constexpr int kSmemLimit = 232448 - 1024;  // opt-in smem per CTA on sm_100 minus static
@@ -92,13 +92,15 @@ struct LMParams {
                                //     body entries loaded by verification
     long long lead_bytes;      // bytes one LEAD / STREAM pass streams (program planes only)
     long long stream_bytes;
-    // summary mode key plane: LEAD passes stream key(lead atom)
-    // instead of the lead atom and test it against a summary in key space, where the
+    // summary mode key plane: LEAD passes stream the key group of
+    // the lead atom (16 bits + a per-run bucket) and test it against a summary in key space, where the
     // atoms that can become true (heads, facts) get fine groups and the rest share
     // coarse ones.  STREAM passes switch the shared copy back to the atom-id summary.
-    const int32_t *keyplane;   // [n_slots] or NULL (no key mode)
+    const uint16_t *lead16;    // [n_slots] low 16 bits of the lead atom's key group, or NULL
+    const uint8_t *octet_tag;  // [n_slots / 8] bucket (group >> 16, < 32) | padding rows << 5
     const int32_t *key_of;     // [n_ext] key of every extended atom
     uint32_t *ksummary;        // [ksm_words] summary of v_0 in key space (zero between calls)
+    int32_t *korder;           // [n_ext + 1] key of order[i] (written with it)
     int32_t ksm_words;
     int32_t kshift;
 };

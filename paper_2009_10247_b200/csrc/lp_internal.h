@@ -54,7 +54,19 @@ struct HostLayout {
     std::vector<int32_t> occ_slot;  // [nnz]
 };
 
+// A run of rows of one segment whose lead atoms share a bucket (key-mode LEAD passes).
+struct Run {
+    int32_t seg;
+    int32_t bucket;
+    int64_t slot_off;   // first slot (multiple of the alignment)
+    int64_t rows;       // real rows
+    int64_t rows_pad;   // rows incl. ⊥ padding (multiple of the alignment)
+};
+
 // encode.cpp
 lp_status encode(const lp_rules *r, bool build_occ, HostLayout *out, std::string *err);
+void build_occ_lists(HostLayout *L);
+void bucket_rows(HostLayout *L, const std::vector<int32_t> &bucket_of_atom, int align,
+                 std::vector<Run> *runs);
 
 }  // namespace lpb

@@ -1,38 +1,50 @@
-"""Per-CTA pass timing of the persistent full θ-pass kernel (profiling aid)."""
+"""Per-CTA pass timing of the persistent full θ-pass kernel (profiling aid).
+
+usage: python tools/dbg_timing.py C4 [grid_blocks=N] [smem_bits_cap=N] [schedule=auto|lead|stream]
+Stamps per pass and CTA (%globaltimer, ns): pass top, stream start (after the delta was
+applied), stream done (last warp), verify done (last warp), CTA done, barrier exit.
+"""
 import ctypes
+import os
 import sys
 
 import numpy as np
 import torch
 
-sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import lpgen  # noqa: E402
 from paper_2009_10247_b200 import lp  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
-kw = {}
+kw, sched = {}, "auto"
 for a in sys.argv[2:]:
     k, v = a.split("=")
-    kw[k] = int(v)
+    if k == "schedule":
+        sched = v
+    else:
+        kw[k] = int(v)
 P = lpgen.config(cfg)
 prog = lp.Program(P, **kw)
 G = prog.info["grid_blocks"]
-buf = torch.zeros(16 * G * 4, dtype=torch.int64, device="cuda")
+buf = torch.zeros(16 * G * 8, dtype=torch.int64, device="cuda")
 lib = lp.library()
 lib.lpdbg_set_timing.argtypes = [ctypes.c_void_p]
 for i in range(3):
-    prog.least_model()
+    prog.least_model(schedule=sched)
 lib.lpdbg_set_timing(buf.data_ptr())
-m, it, _ = prog.least_model()
+m, it, ex = prog.least_model(schedule=sched, stats=True)
 lib.lpdbg_set_timing(None)
-t = buf.cpu().numpy().reshape(16, G, 4).astype(np.float64)
-print(cfg, "iters", it, "grid", G, prog.info["truth_mode"])
+t = buf.cpu().numpy().reshape(16, G, 8).astype(np.float64)
+print(cfg, "iters", it, "grid", G, "truth_mode", prog.info["truth_mode"], ex["stats"])
+ent = t[0, :, 6]
+print(f"prologue: entry spread {(ent.max()-ent.min())/1e3:.1f}us, grid sync exit {(t[2,:,6].min()-ent.min())/1e3:.1f}..{(t[2,:,6].max()-ent.min())/1e3:.1f}us, prologue+smem load done {(t[0,:,7].max()-ent.min())/1e3:.1f}us, "
+      f"first pass top {(t[0,:,0].min()-ent.min())/1e3:.1f}us; epilogue {(t[1,:,7].max()-t[1,:,6].min())/1e3:.1f}us; "
+      f"kernel entry->end {(t[1,:,7].max()-ent.min())/1e3:.1f}us")
 for k in range(min(it, 16)):
-    s = t[k, :, 0]
-    t0 = s.min()
-    work = (t[k, :, 1] - s) / 1e3
-    cta = (t[k, :, 2] - s) / 1e3
-    exit_ = (t[k, :, 3] - t0) / 1e3
-    print(f"pass {k}: start spread {(s.max()-t0)/1e3:7.1f}us  warp-done min/med/max "
-          f"{work.min():7.1f}/{np.median(work):7.1f}/{work.max():7.1f}us  cta-done max {cta.max():7.1f}  "
-          f"barrier exit {exit_.min():7.1f}..{exit_.max():7.1f}us  slowest cta {int(np.argmax(t[k,:,1]-s))}")
+    top = t[k, :, 0]
+    t0 = top.min()
+    rel = lambda i: (t[k, :, i] - t0) / 1e3  # noqa: E731
+    print(f"pass {k:2d}: stream start {rel(1).min():6.1f}..{rel(1).max():6.1f}  "
+          f"stream done med/max {np.median(rel(2)):6.1f}/{rel(2).max():6.1f}  "
+          f"verify done med/max {np.median(rel(3)):6.1f}/{rel(3).max():6.1f}  "
+          f"cta done max {rel(4).max():6.1f}  barrier exit {rel(5).min():6.1f}..{rel(5).max():6.1f} us")
