@@ -23,7 +23,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -33,6 +32,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+KERNEL_REV = "lead16-octets-v1"   # bump when the dominant kernel's traffic changes
 METRIC = ("least-model fixpoint time & nnz·iter/s (HBM GB/s vs peak); "
           "stable-model guesses/s")
 
@@ -47,59 +47,53 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled with NVML every ~1 ms DURING the timed
+    region (a background thread between start() and stop())."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self.t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _loop(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.001)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50", "-i", str(self.index)], stdout=subprocess.PIPE,
-                stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        if self.nv:
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
-        except Exception:  # noqa: BLE001
-            self.proc = None
-
-    def _read(self):
-        for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:  # noqa: BLE001
-            self.proc.kill()
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self._stop.set()
         self.t.join(timeout=2)
-        sm, smax, util, reasons = [], [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                smax.append(float(f[1]))
-                util.append(float(f[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
-        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
-                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
-                "samples": len(sm), "samples_under_load": len([u for u in util if u > 0])}
+        s = self.samples
+        return {"sm_mhz": float(np.median(s)) if s else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s),
+                "source": "NVML every ~1 ms during the timed region"}
 
 
 def _dist():
@@ -150,7 +144,7 @@ def main():
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--stable-workload", default="C5")
     ap.add_argument("--no-extras", action="store_true", help="main line only (for ncu)")
-    ap.add_argument("--cpu-sample-passes", type=int, default=1)
+    ap.add_argument("--cpu-sample-reps", type=int, default=5)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -198,58 +192,77 @@ def main():
     info = prog.info
     n = P.n_atoms
     Wm = lp.bits_words(n)
-    nfacts = int((np.diff(P.body_ptr) == 0).sum())
-    launches_per_call = 3 + (1 if nfacts else 0) + 1
+    launches_per_call = 1      # lp_least_model = one cooperative launch (prologue..extraction)
 
     model = torch.zeros(Wm, dtype=torch.int64, device="cuda")
     iters_d = torch.zeros(1, dtype=torch.int32, device="cuda")
+    stats_d = torch.zeros(6, dtype=torch.int64, device="cuda")
 
     def timed_least_model(frontier, steps, warmup):
-        tot, ker = [], []
+        tot, ker, byts, mhz = [], [], [], []
         for i in range(warmup + steps):
             flush_l2()
             e0, e1, k0, k1 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             e0.record(stream)
             lp.lp_least_model(prog, None, model, frontier=frontier, stream=stream, device_ptrs=True,
-                              iters_out=iters_d, ev_begin=k0, ev_end=k1)
+                              iters_out=iters_d, ev_begin=k0, ev_end=k1, stats=stats_d)
             e1.record(stream)
             stream.synchronize()
             if i >= warmup:
                 tot.append(e0.elapsed_time(e1))
                 ker.append(k0.elapsed_time(k1))
-        return float(np.mean(tot)), float(np.mean(ker)), int(iters_d.item())
+                sd = stats_d.tolist()
+                byts.append(int(sd[0]))
+                if sd[5] > 0:
+                    mhz.append(1e3 * sd[4] / sd[5])
+        dev_clock.extend(mhz)
+        return (float(np.mean(tot)), float(np.mean(ker)), int(iters_d.item()),
+                float(np.mean(byts)) if byts else 0.0, [int(x) for x in stats_d.tolist()])
 
     # ---- main line: full θ-pass fixpoint ---------------------------------------------
+    dev_clock = []
     clocks = ClockSampler(local)
     timed_least_model(False, 0, args.warmup)            # warm-up
     barrier()
     clocks.start()
-    ms, kms, iters = timed_least_model(False, args.steps, 0)
+    dev_clock.clear()
+    ms, kms, iters, alg_bytes, st = timed_least_model(False, args.steps, 0)
     barrier()
     clk = clocks.stop()
+    # the SM clock each timed launch actually ran at (%clock64 / %globaltimer in-kernel)
+    clk["nvml_sm_mhz"] = clk.get("sm_mhz")
+    if dev_clock:
+        clk["sm_mhz"] = float(np.median(dev_clock))
+        clk["sm_mhz_min"] = float(np.min(dev_clock))
+        clk["source"] = ("sm_mhz: device %clock64/%globaltimer over each timed launch (median); "
+                         "reasons: NVML every ~1 ms during the timed region")
     ms_max = allmax(ms)
     kms_max = allmax(kms)
     nnz = int(info["nnz"])
     value = ws * nnz * iters / (ms_max / 1e3)
 
     hbm_peak, peak_src = _peaks()
-    pass_bytes = int(info["pass_bytes"])
-    achieved = pass_bytes * iters / (kms_max / 1e3) / 1e9
+    # algorithmic bytes of the launch, counted by the kernel itself (lp_run.stats_out):
+    # the planes each pass streamed + 4 B per body entry / head the verification loaded +
+    # 12 B per derived atom
+    alg_bytes = allmax(alg_bytes)
+    achieved = alg_bytes / (kms_max / 1e3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f).get(args.workload)
-        if tr and tr["passes_per_launch"] == iters and info["truth_mode"] == 1:
+        if tr and tr["passes_per_launch"] == iters and tr.get("kernel_rev") == KERNEL_REV:
             traffic = tr["dram_bytes_per_launch"]
     except Exception:  # noqa: BLE001
         traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic,
-                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, bytes per launch)",
-                "algorithmic_bytes_per_launch": pass_bytes * iters, "peak_source": peak_src,
-                "kernel": "lm_full_kernel<false> (persistent, all passes in one launch)",
-                "bytes_per_pass": pass_bytes, "passes_per_launch": iters,
-                "kernel_ms": kms_max}
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram bytes per launch)",
+                "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                "kernel": "lm_full_kernel<false> (persistent: all passes of the fixpoint in one launch)",
+                "passes_per_launch": iters, "lead_passes": st[1], "rows_verified": st[2],
+                "lead_pass_bytes": int(info["lead_pass_bytes"]),
+                "stream_pass_bytes": int(info["stream_pass_bytes"]), "kernel_ms": kms_max}
 
     out = {
         "metric": METRIC, "value": value, "unit": "nnz*iter/s", "n_gpus": ws, "steps": args.steps,
@@ -292,7 +305,7 @@ def main():
 
     if not args.no_extras:
         # ---- frontier variant on the same workload --------------------------------------
-        fms, fkms, fit = timed_least_model(True, args.steps, args.warmup)
+        fms, fkms, fit, _, _ = timed_least_model(True, args.steps, args.warmup)
         assert fit == iters
         out["frontier"] = {"ms_per_step": allmax(fms), "kernel_ms": allmax(fkms), "iters": fit,
                            "speedup_vs_full": ms_max / allmax(fms)}
@@ -329,12 +342,18 @@ def main():
         import oracle
         oracle.build()
         t0 = time.perf_counter()
-        _, it_cpu, _, conv = oracle.lm_jacobi(P, max_iters=args.cpu_sample_passes)
+        reps, it_cpu = 0, 0
+        while reps < args.cpu_sample_reps and (reps == 0 or time.perf_counter() - t0 < 10.0):
+            _, it1, _, conv = oracle.lm_jacobi(P)      # the whole fixpoint, as it stands
+            assert conv and it1 == iters
+            it_cpu += it1
+            reps += 1
         dt = time.perf_counter() - t0
         out["cpu_baseline"] = {"value": nnz * it_cpu / dt, "unit": "nnz*iter/s", "cores": 1,
                                "kind": "oracle",
-                               "sample": f"{it_cpu} Jacobi T_P pass(es) of O-LM over all of "
-                                         f"{args.workload} ({dt:.1f} s, single thread)"}
+                               "sample": f"{reps} whole fixpoint(s) of O-LM Jacobi (oracle/lp_oracle.c, "
+                                         f"{it_cpu} T_P passes over all of {args.workload}, {dt:.1f} s, "
+                                         f"single thread)"}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist:

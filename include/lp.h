@@ -112,11 +112,13 @@ typedef struct {
     void *ev_begin;          /* optional cudaEvent_t recorded on stream immediately
                                 before the fixpoint kernel, ev_end right after it   */
     void *ev_end;
-    uint64_t *stats_out;     /* optional [4], full θ-pass only (zeros otherwise):
+    uint64_t *stats_out;     /* optional [6], full θ-pass only (zeros otherwise):
                                 [0] algorithmic bytes the fixpoint kernel moved (planes
                                 streamed + 4 B per verified body entry / head + 12 B
                                 per derived atom), [1] LEAD passes, [2] rows queued for
-                                verification, [3] body entries verification loaded   */
+                                verification, [3] body entries verification loaded,
+                                [4] SM clock cycles and [5] ns the launch took
+                                (%clock64 / %globaltimer of one thread)              */
 } lp_run;
 
 typedef struct {

@@ -190,7 +190,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     TRY(dalloc(p, &p->d_order, (size_t)L.n_ext + 1));
     TRY(dalloc(p, &p->d_scal, 32));
     CK(cudaMemset(p->d_scal, 0, 32 * sizeof(int32_t)));
-    TRY(dalloc(p, &p->d_stats, 4));
+    TRY(dalloc(p, &p->d_stats, 6));
     {
         std::vector<uint32_t> fb((size_t)p->nwords, 0u);   // facts of P (Def. 4)
         for (int32_t a : L.facts) fb[(size_t)a >> 5] |= 1u << (a & 31);
@@ -588,8 +588,8 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     unsigned long long *stats_dev = nullptr;
     if (run && run->stats_out) stats_dev = dev ? reinterpret_cast<unsigned long long *>(run->stats_out) : p->d_stats;
     if (stats_dev && (frontier || p->use_tma)) {   // only the register-streaming full pass counts
-        if (dev) CK(cudaMemsetAsync(stats_dev, 0, 4 * sizeof(uint64_t), st));
-        else std::memset(run->stats_out, 0, 4 * sizeof(uint64_t));
+        if (dev) CK(cudaMemsetAsync(stats_dev, 0, 6 * sizeof(uint64_t), st));
+        else std::memset(run->stats_out, 0, 6 * sizeof(uint64_t));
         stats_dev = nullptr;
     }
     q.stats = stats_dev;
@@ -619,7 +619,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     if (pops) CK(cudaMemcpyAsync(run->popcounts_out, pops, sizeof(int32_t) * (size_t)pop_cap,
                                  cudaMemcpyDeviceToHost, st));
     if (stats_dev)
-        CK(cudaMemcpyAsync(run->stats_out, stats_dev, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(run->stats_out, stats_dev, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     *iters_out = scal[1];
     if (scal[2] == 2) return set_err(LP_E_CUDA, "internal: candidate queue overflow");

@@ -496,6 +496,12 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const bool lead = blockIdx.x == 0 && tid == 0;
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 6] = globaltimer();
+    long long clk0 = 0;
+    unsigned long long ns0 = 0;
+    if (lead) {   // SM clock over the launch: cycles / ns (lp_run.stats_out[4..5])
+        clk0 = clock64();
+        ns0 = globaltimer();
+    }
 
     lm_prologue(p, !EXACT, gtid, gthreads);            // v_0 (row a3), in-kernel
     if (gtid == 0) {
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         p.cand[1] = 0;
         p.cand[2] = 0;
         if (p.stats)
-            for (int i = 0; i < 4; ++i) p.stats[i] = 0;
+            for (int i = 0; i < 6; ++i) p.stats[i] = 0;
     }
     grid.sync();
     if (p.dbg && tid == 0) p.dbg[(2 * gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
@@ -654,7 +660,11 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             if (lead) {
                 *p.iters_out = k + 1;
                 if (t != de) atomicMax(p.status_out, 1);
-                if (p.stats) p.stats[0] += 4ull * p.stats[3];
+                if (p.stats) {
+                    p.stats[0] += 4ull * p.stats[3];
+                    p.stats[4] = (unsigned long long)(clock64() - clk0);
+                    p.stats[5] = globaltimer() - ns0;
+                }
             }
             if (p.dbg && tid == 0) p.dbg[(gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
             lm_zero_summaries(p, !EXACT, gtid, gthreads);

@@ -228,12 +228,13 @@ class Program:
         model = np.zeros(max(bits_words(n), 1), dtype=np.uint64)
         pops = np.zeros(n + 3, dtype=np.int32) if popcounts else None
         stage = np.zeros(max(n, 1), dtype=np.int32) if stages else None
-        st = np.zeros(4, dtype=np.uint64) if stats else None
+        st = np.zeros(6, dtype=np.uint64) if stats else None
         iters = lp_least_model(self, v0w, model, frontier=frontier, pops=pops, stage=stage,
                                stream=stream, schedule=schedule, stats=st)
         extra = {}
         if stats:
-            extra["stats"] = dict(zip(("bytes", "lead_passes", "rows_verified", "entries_verified"),
+            extra["stats"] = dict(zip(("bytes", "lead_passes", "rows_verified", "entries_verified",
+                                       "sm_cycles", "ns"),
                                       (int(x) for x in st)))
         if popcounts:
             extra["popcounts"] = pops[:iters].tolist()
