@@ -310,10 +310,14 @@ def main():
         out["frontier"] = {"ms_per_step": allmax(fms), "kernel_ms": allmax(fkms), "iters": fit,
                            "speedup_vs_full": ms_max / allmax(fms)}
         # ---- stable models ---------------------------------------------------------------
+        # guess-sharded under torchrun: rank r solves its 64-aligned slice
+        # of the 2^f guesses (lp_run.guess_offset), no exchange until the final gather
+        from paper_2009_10247_b200.shard import guess_slices, stable_models_sharded
         S = lpgen.config(args.stable_workload)
         sprog = lp.Program(S, device=local)
-        G = 1 << sprog.info["n_free_negated"]
-        W = (G + 63) // 64
+        G_all = 1 << sprog.info["n_free_negated"]
+        goff, G = guess_slices(G_all, ws)[rank]
+        W = max((G + 63) // 64, 1)
         acc = torch.zeros(W, dtype=torch.int64, device="cuda")
         nacc = torch.zeros(1, dtype=torch.int64, device="cuda")
         passes = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -322,19 +326,29 @@ def main():
             flush_l2()
             e0, e1, k0, k1 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             e0.record(stream)
-            lp.lp_stable_models(sprog, None, G, acc, stream=stream, device_ptrs=True,
-                                n_accepted_out=nacc, passes_out=passes, ev_begin=k0, ev_end=k1)
+            if G > 0:
+                lp.lp_stable_models(sprog, None, G, acc, stream=stream, device_ptrs=True,
+                                    n_accepted_out=nacc, passes_out=passes, ev_begin=k0,
+                                    ev_end=k1, guess_offset=goff)
+            else:
+                k0.record(stream)
+                k1.record(stream)
             e1.record(stream)
             stream.synchronize()
             if i >= args.warmup:
                 st_t.append(e0.elapsed_time(e1))
                 st_k.append(k0.elapsed_time(k1))
         sms = allmax(float(np.mean(st_t)))
-        out["stable"] = {"workload": args.stable_workload, "guesses": G,
-                         "guesses_per_s": ws * G / (sms / 1e3), "ms_per_step": sms,
-                         "kernel_ms": allmax(float(np.mean(st_k))), "passes": int(passes.item()),
-                         "accepted": int(nacc.item()), "n_negated": sprog.info["n_negated"],
-                         "l2": "flushed between steps"}
+        stable = {"workload": args.stable_workload, "guesses": G_all,
+                  "guesses_per_s": G_all / (sms / 1e3), "ms_per_step": sms,
+                  "kernel_ms": allmax(float(np.mean(st_k))), "passes": int(allmax(int(passes.item()))),
+                  "accepted": int(nacc.item()), "n_negated": sprog.info["n_negated"],
+                  "l2": "flushed between steps",
+                  "sharding": f"guesses over {ws} rank(s), slice time max over ranks"}
+        if dist:
+            ids, ps = stable_models_sharded(sprog, sprog.info["n_free_negated"])
+            stable["accepted"], stable["passes"] = int(ids.size), ps
+        out["stable"] = stable
         sprog.close()
 
     # ---- CPU baseline: the oracle as it stands, rank 0, N = 1 only ----------------------

@@ -119,6 +119,10 @@ typedef struct {
                                 verification, [3] body entries verification loaded,
                                 [4] SM clock cycles and [5] ns the launch took
                                 (%clock64 / %globaltimer of one thread)              */
+    int64_t guess_offset;    /* lp_stable_models with guesses == NULL: guess i of this
+                                call is global guess guess_offset + i of the binary
+                                counting order (a multiple of 64; 0 = from the first).
+                                Lets ranks split the 2^f guesses      */
 } lp_run;
 
 typedef struct {
@@ -172,10 +176,12 @@ lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t *model_out,
 /* Stable models (Algorithms 2-3) over a batch of guesses.
  *   guesses    : bit-sliced guess matrix, [k][W] words with W = ceil(n_guesses/64):
  *                bit g of row j is the value of abar_j (1 = a_j assumed false) in
- *                guess g.  NULL = all 2^f assignments of the free negated atoms in
+ *                guess g.  NULL = the 2^f assignments of the free negated atoms in
  *                binary counting order (bit i of g = abar of the i-th free negated
- *                atom; abar of a negated fact fixed to 0, Def. 8 item 3); n_guesses is
- *                then ignored and taken as 2^f (LP_E_CAP if f > guess_cap).
+ *                atom; abar of a negated fact fixed to 0, Def. 8 item 3), starting at
+ *                lp_run.guess_offset; n_guesses <= 0 takes all the remaining ones,
+ *                n_guesses > 0 at most that many (LP_E_CAP if f > guess_cap).
+ *                Local guess i (bit i of accepted_out) is global guess offset + i.
  *   accepted_out : [W] words, bit g set iff guess g's fixpoint column satisfies
  *                a_j + abar_j = 1 for every negated atom (Algorithm 3, reading R7).
  *   n_accepted_out : number of accepted guesses (int64).

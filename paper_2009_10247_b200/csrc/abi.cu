@@ -665,11 +665,17 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
     const bool dev = flags & LP_PTR_DEVICE;
     cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
     int64_t G;
+    const int64_t goff = run ? run->guess_offset : 0;
+    if (goff != 0 && (guesses || goff < 0 || goff % 64))
+        return set_err(LP_E_INVALID, "guess_offset needs guesses == NULL and a multiple of 64");
     if (!guesses) {
         if (L.f > p->guess_cap)
             return set_err(LP_E_CAP, "guess explosion: " + std::to_string(L.f) +
                                          " free negated atoms > guess_cap " + std::to_string(p->guess_cap));
-        G = (int64_t)1 << L.f;
+        const int64_t all = (int64_t)1 << L.f;
+        if (goff >= all) return set_err(LP_E_INVALID, "guess_offset >= 2^f");
+        G = all - goff;
+        if (n_guesses > 0) G = std::min(G, n_guesses);
     } else {
         if (n_guesses < 1) return set_err(LP_E_INVALID, "n_guesses < 1");
         G = n_guesses;
@@ -720,7 +726,7 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
     STParams s = st_params(p);
     if (dev) s.passes_out = passes_out;
     CK(launch_st_init(s, L.n, L.k, p->d_negated_ext, p->d_free_rank, guesses ? gd : nullptr, W, G,
-                      p->d_facts, p->nfacts, L.top, p->d_any, st));
+                      goff / 64, p->d_facts, p->nfacts, L.top, p->d_any, st));
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
     CK(launch_st_fixpoint(s, p->st_blocks, p->st_smem, st));
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));

@@ -1078,8 +1078,8 @@ __device__ __forceinline__ unsigned long long count_pattern(int i, int64_t w) {
 // valid guesses), abar rows from the guesses, every other row zero (memset before).
 __global__ void st_init_kernel(STParams p, int32_t n, int32_t k, const int32_t *negated_ext,
                                const int32_t *free_rank, const unsigned long long *guesses,
-                               int32_t W, int64_t G, const int32_t *facts, int32_t nfacts,
-                               int32_t top, uint32_t *any_bits) {
+                               int32_t W, int64_t G, int64_t woff, const int32_t *facts,
+                               int32_t nfacts, int32_t top, uint32_t *any_bits) {
     const int64_t rows = 1 + (int64_t)nfacts + k;
     const int64_t total = rows * p.Wp;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
@@ -1101,7 +1101,7 @@ __global__ void st_init_kernel(STParams p, int32_t n, int32_t k, const int32_t *
                 v = (w < W ? guesses[(int64_t)j * W + w] : 0ull) & valid;
             } else {
                 const int32_t rank = free_rank[j];
-                v = rank < 0 ? 0ull : (count_pattern(rank, w) & valid);
+                v = rank < 0 ? 0ull : (count_pattern(rank, w + woff) & valid);   // global word
             }
         }
         p.T0[(int64_t)row * p.Wp + w] = v;
@@ -1115,7 +1115,7 @@ __global__ void st_init_kernel(STParams p, int32_t n, int32_t k, const int32_t *
 
 cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_t *negated_ext,
                            const int32_t *free_rank, const unsigned long long *guesses,
-                           int32_t W, int64_t G, const int32_t *facts, int32_t nfacts,
+                           int32_t W, int64_t G, int64_t woff, const int32_t *facts, int32_t nfacts,
                            int32_t top, uint32_t *any_bits, cudaStream_t st) {
     cudaError_t e;
     const size_t tbytes = (size_t)p.n_ext * p.Wp * sizeof(unsigned long long);
@@ -1128,7 +1128,7 @@ cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_
     const int64_t total = (1 + (int64_t)nfacts + k) * p.Wp;
     int b = (int)std::min<int64_t>((total + 255) / 256, 8192);
     st_init_kernel<<<std::max(b, 1), 256, 0, st>>>(p, n, k, negated_ext, free_rank, guesses, W, G,
-                                                   facts, nfacts, top, any_bits);
+                                                   woff, facts, nfacts, top, any_bits);
     return cudaGetLastError();
 }
 

@@ -141,7 +141,7 @@ cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st);
 
 cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_t *negated_ext,
                            const int32_t *free_rank, const unsigned long long *guesses,
-                           int32_t W, int64_t G, const int32_t *facts, int32_t nfacts,
+                           int32_t W, int64_t G, int64_t woff, const int32_t *facts, int32_t nfacts,
                            int32_t top, uint32_t *any_bits, cudaStream_t st);
 cudaError_t launch_st_fixpoint(const STParams &p, int blocks, size_t smem, cudaStream_t st);
 cudaError_t launch_st_check(const STParams &p, int32_t n, int32_t k, const int32_t *negated,

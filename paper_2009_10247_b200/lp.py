@@ -47,7 +47,7 @@ class lp_options(ctypes.Structure):
 class lp_run(ctypes.Structure):
     _fields_ = [("stream", _P), ("flags", ctypes.c_uint32), ("popcounts_out", _P),
                 ("popcounts_cap", ctypes.c_int32), ("stage_out", _P), ("ev_begin", _P),
-                ("ev_end", _P), ("stats_out", _P)]
+                ("ev_end", _P), ("stats_out", _P), ("guess_offset", ctypes.c_int64)]
 
 
 class lp_info_t(ctypes.Structure):
@@ -242,16 +242,19 @@ class Program:
             extra["stage"] = stage[:n]
         return model[:bits_words(n)], iters, extra
 
-    def stable_models(self, guesses=None, n_guesses: int = 0, stream=None):
-        """Host-buffer call.  guesses: None or uint64[k][W].  Returns
-        (accepted guess ids (np.int64), passes, accepted mask words)."""
+    def stable_models(self, guesses=None, n_guesses: int = 0, stream=None, guess_offset: int = 0):
+        """Host-buffer call.  guesses: None or uint64[k][W].  With guesses None the call
+        covers global guesses [guess_offset, guess_offset + n_guesses) (n_guesses 0 = all
+        the rest).  Returns (accepted LOCAL guess ids (np.int64), passes, mask words)."""
         if guesses is None:
-            G = 1 << self.info["n_free_negated"]
+            G = (1 << self.info["n_free_negated"]) - int(guess_offset)
+            if n_guesses > 0:
+                G = min(G, int(n_guesses))
         else:
             G = int(n_guesses)
         W = (G + 63) // 64
         acc = np.zeros(max(W, 1), dtype=np.uint64)
-        nacc, passes = lp_stable_models(self, guesses, G, acc, stream=stream)
+        nacc, passes = lp_stable_models(self, guesses, G, acc, stream=stream, guess_offset=guess_offset)
         bits = np.unpackbits(acc[:W].view(np.uint8), bitorder="little")[:G]
         ids = np.nonzero(bits)[0].astype(np.int64)
         assert ids.size == nacc
@@ -335,13 +338,19 @@ def lp_least_model(p: Program, v0, model_out, frontier=False, pops=None, stage=N
 
 
 def lp_stable_models(p: Program, guesses, n_guesses, accepted_out, stream=None, device_ptrs=False,
-                     n_accepted_out=None, passes_out=None, ev_begin=None, ev_end=None):
+                     n_accepted_out=None, passes_out=None, ev_begin=None, ev_end=None,
+                     guess_offset: int = 0):
     flags = LP_PTR_DEVICE if device_ptrs else 0
     run = _run(stream, flags, ev_begin=ev_begin, ev_end=ev_end)
+    run.guess_offset = int(guess_offset)
     g = None
     if guesses is not None:
         g = guesses if device_ptrs else np.ascontiguousarray(guesses, dtype=np.uint64)
-    p._last_G = int(n_guesses) if guesses is not None else (1 << p.info["n_free_negated"])
+    if guesses is not None:
+        p._last_G = int(n_guesses)
+    else:
+        rest = (1 << p.info["n_free_negated"]) - int(guess_offset)
+        p._last_G = min(rest, int(n_guesses)) if int(n_guesses) > 0 else rest
     if device_ptrs:
         _check(library().lp_stable_models(p.handle, _ptr(g), int(n_guesses), _ptr(accepted_out),
                                            _ptr(n_accepted_out), _ptr(passes_out), ctypes.byref(run)),

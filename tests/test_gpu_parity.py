@@ -304,3 +304,43 @@ def test_config_c5_parity():
     P = lpgen.config("C5")
     prog, o = check_stable(P)
     assert prog.info["n_negated"] == 12
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_guess_offset_slices(seed):
+    """lp_run.guess_offset: rank slices of the 2^f guesses, solved one after another on
+    this GPU (no slice waits on another), concatenate to the whole search."""
+    from paper_2009_10247_b200.shard import guess_slices
+    rng = np.random.default_rng([seed, 31])
+    P = lpgen.random_normal_program(rng, 300, 1200, max_len=4, k_max=9)
+    o = oracle.stable(P, want_models=True)
+    G = 1 << o["f"]
+    prog = lp.Program(P)
+    for world in (1, 2, 3, 8):
+        got, passes = [], 0
+        for off, cnt in guess_slices(G, world):
+            if cnt == 0:
+                continue
+            ids, ps, _ = prog.stable_models(guess_offset=off, n_guesses=cnt)
+            got += (ids + off).tolist()
+            passes = max(passes, ps)
+            g = int(ids[0]) if ids.size else cnt - 1          # a column of this slice
+            assert (prog.guess_model(g) == o["models"][off + g]).all()
+        assert got == np.nonzero(o["accepted"])[0].tolist()
+        assert passes == o["passes"]
+    if G > 64:
+        with pytest.raises(lp.LPError):
+            prog.stable_models(guess_offset=32, n_guesses=8)
+
+
+def test_guess_offset_c5_slices():
+    P = lpgen.config("C5")
+    o = oracle.stable(P)
+    prog = lp.Program(P)
+    from paper_2009_10247_b200.shard import guess_slices
+    got, passes = [], 0
+    for off, cnt in guess_slices(1 << o["f"], 8):
+        ids, ps, _ = prog.stable_models(guess_offset=off, n_guesses=cnt)
+        got += (ids + off).tolist()
+        passes = max(passes, ps)
+    assert got == np.nonzero(o["accepted"])[0].tolist() and passes == o["passes"]

@@ -1,0 +1,89 @@
+"""Multi-process host logic of the multi-GPU path on CPU with gloo:
+guess slicing and the rank-sharded stable-model search (all-gather of accepted masks,
+max-reduce of pass counts).  The per-rank solver here is the CPU oracle standing in for
+the GPU (test infrastructure; the product's default solver is the CUDA path); the GPU
+side of guess slices is covered by tests/test_gpu_parity.py::test_guess_offset_slices."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import lpgen
+import oracle
+from paper_2009_10247_b200.shard import guess_slices
+
+
+def test_guess_slices_cover_exactly_once():
+    for G in (0, 1, 63, 64, 65, 4096, 4097, 1 << 12):
+        for world in (1, 2, 3, 5, 8, 100):
+            s = guess_slices(G, world)
+            assert len(s) == world
+            covered = []
+            for off, cnt in s:
+                assert off % 64 == 0 or cnt == 0
+                covered += list(range(off, off + cnt))
+            assert covered == list(range(G))
+
+
+def _oracle_slice(P, off, cnt):
+    """Explicit guess rows for global ids off..off+cnt (binary counting over the free
+    negated atoms, abar of a negated fact fixed to 0: Def. 8 / reading R8-R9)."""
+    negs = oracle.negated_atoms(P)
+    facts = set(P.head[np.diff(P.body_ptr) == 0].tolist())
+    free = [j for j, a in enumerate(negs) if a not in facts]
+    g = np.zeros((cnt, len(negs)), dtype=np.uint8)
+    ids = np.arange(off, off + cnt)
+    for i, j in enumerate(free):
+        g[:, j] = (ids >> i) & 1
+    o = oracle.stable(P, guesses=g)
+    acc = o["accepted"].astype(np.uint8)
+    W = (cnt + 63) // 64
+    pad = np.zeros(W * 64, dtype=np.uint8)
+    pad[:cnt] = acc
+    return np.packbits(pad, bitorder="little").view(np.uint64), int(o["passes"])
+
+
+def _worker(rank, world, port, seed, q):
+    import torch.distributed as dist
+    from paper_2009_10247_b200.shard import stable_models_sharded
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        rng = np.random.default_rng([seed, 77])
+        P = lpgen.random_normal_program(rng, 40, 120, max_len=3, k_max=7)
+        f = oracle.stable(P)["f"]
+        ids, passes = stable_models_sharded(None, f, solve=lambda o, c: _oracle_slice(P, o, c))
+        q.put((rank, ids.tolist(), passes))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world,seed", [(2, 1), (2, 2), (3, 3), (2, 4)])
+def test_sharded_stable_models_gloo(world, seed):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng([seed, 77])
+    P = lpgen.random_normal_program(rng, 40, 120, max_len=3, k_max=7)
+    o = oracle.stable(P)
+    want = np.nonzero(o["accepted"])[0].tolist()
+    for _, ids, passes in res:
+        assert ids == want
+        assert passes == o["passes"]
