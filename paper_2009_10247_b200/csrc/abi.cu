@@ -58,11 +58,13 @@ struct lp_program {
     size_t tma_smem = 0;
     // [0] tail, [2] status (stable path); [1] iters; [3] passes; [4,5] n_accepted;
     // [8,9] least-model tails and [10,11] statuses, alternating by call parity;
-    // [12..14] rows queued per full θ-pass (slot k % 3)
+    // [12..14] rows queued per full θ-pass (slot k % 3); [16..18] least-model and
+    // [20..22] stable per-pass append counters (slot k % 3)
     int32_t *d_scal = nullptr;
     unsigned long long *d_stats = nullptr;  // full θ-pass work statistics (lp_run.stats_out)
     uint16_t *d_lead16 = nullptr;   // summary-mode key plane (low 16 bits of the lead group)
     uint8_t *d_octet_tag = nullptr;
+    int32_t *d_lead32 = nullptr;    // exact mode: flat lead plane
     int32_t *d_key_of = nullptr;
     uint32_t *d_ksummary = nullptr;
     int32_t *d_korder = nullptr;
@@ -297,6 +299,13 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
 
     // the program planes in their final row order
     if (L.has_occ) build_occ_lists(&L);
+    if (p->exact) {   // flat lead plane for exact-mode LEAD passes (one loop, no segments)
+        std::vector<int32_t> l32((size_t)std::max<int64_t>(L.n_slots, 4), L.bot);
+        for (const Segment &sg : L.segs)
+            for (int64_t i = 0; i < sg.count_pad; ++i)
+                l32[(size_t)(sg.slot_off + i)] = L.col[(size_t)(sg.col_off + i)];
+        TRY(upload(p, &p->d_lead32, l32));
+    }
     TRY(upload(p, &p->d_segs, L.segs));
     TRY(upload(p, &p->d_col, L.col));
     TRY(upload(p, &p->d_head, L.head));
@@ -585,6 +594,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.dense_div = std::getenv("LP_DENSE_DIV") ? std::max(1, std::atoi(std::getenv("LP_DENSE_DIV"))) : 16;
     q.n_slots = L.n_slots;
     q.cand = p->d_scal + 12;
+    q.pcnt = p->d_scal + 16;
     unsigned long long *stats_dev = nullptr;
     if (run && run->stats_out) stats_dev = dev ? reinterpret_cast<unsigned long long *>(run->stats_out) : p->d_stats;
     if (stats_dev && (frontier || p->use_tma)) {   // only the register-streaming full pass counts
@@ -595,6 +605,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.stats = stats_dev;
     q.lead16 = (frontier || p->use_tma) ? nullptr : p->d_lead16;
     q.octet_tag = p->d_octet_tag;
+    q.lead32 = (frontier || p->use_tma) ? nullptr : p->d_lead32;
     q.key_of = p->d_key_of;
     q.ksummary = p->d_ksummary;
     q.korder = p->d_korder;
@@ -647,6 +658,7 @@ static STParams st_params(lp_program *p) {
     s.any_shift = p->any_shift;
     s.order = p->d_order;
     s.tail = p->d_scal + 0;
+    s.pcnt = p->d_scal + 20;
     s.mark = p->d_mark;
     s.passes_out = p->d_scal + 3;
     s.status_out = p->d_scal + 2;

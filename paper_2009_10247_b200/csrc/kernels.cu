@@ -105,6 +105,7 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
     if (gtid == 0) {
         *p.tail_next = 0;
         *p.status_next = 0;
+        p.pcnt[0] = p.pcnt[1] = p.pcnt[2] = 0;
     }
     const bool keys = summary_mode && p.lead16;
     const bool osum = summary_mode && !(keys && p.pass_mode != 2);
@@ -198,7 +199,23 @@ struct PassCtx {
     int32_t *qcount;     // its fill counter (shared memory)
     int k;
     const uint32_t *bmask;  // key mode: bit b = some summary bit of bucket b is set (shared)
+    const Segment *segs;    // the segment table (shared-memory copy when it fits)
+    int32_t *sq;            // the first kSmemQueue queue entries (shared memory), or NULL
+    int32_t *pc;            // this pass's append counter (p.pcnt[k % 3])
+    int32_t base;           // derivation-list index of this pass's first append
 };
+
+// Queue entry i of this CTA: shared memory for the first kSmemQueue entries (no global
+// round trip for the usual few hundred survivors per pass), the global queue after that.
+// (register-streaming kernel only; its PassCtx always has sq)
+__device__ __forceinline__ void qput(const PassCtx &c, int32_t i, int32_t slot) {
+    if (i < kSmemQueue) c.sq[i] = slot;
+    else c.qbuf[i - kSmemQueue] = slot;
+}
+
+__device__ __forceinline__ int32_t qget(const PassCtx &c, int32_t i) {
+    return i < kSmemQueue ? c.sq[i] : __ldcg(c.qbuf + (i - kSmemQueue));
+}
 
 // Smem test of 4 AND-rows at one body position; `fire` bit e = row e still alive.
 template <bool EXACT>
@@ -223,9 +240,9 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
     const unsigned m = __activemask();
     const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
     int32_t base = 0;
-    if (lane == leader) base = atomicAdd(p.tail, __popc(m));
+    if (lane == leader) base = atomicAdd(c.pc, __popc(m));
     base = __shfl_sync(m, base, leader);
-    const int32_t pos = base + __popc(m & ((1u << lane) - 1u));
+    const int32_t pos = c.base + base + __popc(m & ((1u << lane) - 1u));
     p.order[pos] = h;
     if (p.lead16) p.korder[pos] = __ldg(p.key_of + h);   // once per atom, not per CTA
     if (p.stage) p.stage[h] = c.k + 1;
@@ -241,11 +258,11 @@ __device__ __noinline__ int verify_slot(const LMParams &p, const PassCtx &c, int
     int lo = 0, hi = p.nseg - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(&p.segs[mid].slot_off) <= slot) lo = mid; else hi = mid - 1;
+        if (c.segs[mid].slot_off <= slot) lo = mid; else hi = mid - 1;
     }
-    const int32_t L = __ldg(&p.segs[lo].L);
-    const int64_t cp = __ldg(&p.segs[lo].count_pad);
-    const int32_t *colp = p.col + __ldg(&p.segs[lo].col_off) + (slot - __ldg(&p.segs[lo].slot_off));
+    const int32_t L = c.segs[lo].L;
+    const int64_t cp = c.segs[lo].count_pad;
+    const int32_t *colp = p.col + c.segs[lo].col_off + (slot - c.segs[lo].slot_off);
     // the head and up to 8 body atoms are loaded together (one memory round trip),
     // then their truth words (a second one)
     constexpr int B = 8;
@@ -286,13 +303,13 @@ __device__ __noinline__ int verify_slot(const LMParams &p, const PassCtx &c, int
 __device__ __forceinline__ void enqueue(const LMParams &p, const PassCtx &c, int32_t slot0,
                                         unsigned fire) {
     int32_t pos = atomicAdd(c.qcount, __popc(fire));
-    if (pos + 4 > p.qcap) {
+    if (pos + 4 > p.qcap + kSmemQueue) {
         atomicExch(p.status_out, 2);
         return;
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-        if ((fire >> e) & 1u) c.qbuf[pos++] = slot0 + e;
+        if ((fire >> e) & 1u) qput(c, pos++, slot0 + e);
 }
 
 // EXACT mode: the shared-memory test is exact, so a passing row fires; its head comes
@@ -434,13 +451,50 @@ __device__ __forceinline__ void octets_lead(const LMParams &p, const PassCtx &c,
             fire &= 0xFFu >> (tag[u] >> 5);                   // trailing padding rows
             if (fire) {
                 int32_t pos = atomicAdd(c.qcount, __popc(fire));
-                if (pos + __popc(fire) > p.qcap) {
+                if (pos + __popc(fire) > p.qcap + kSmemQueue) {
                     atomicExch(p.status_out, 2);
                     continue;
                 }
                 const int32_t s0 = q * 8;
-                for (unsigned f = fire; f; f &= f - 1) c.qbuf[pos++] = s0 + __ffs(f) - 1;
+                for (unsigned f = fire; f; f &= f - 1) {
+                    const int32_t slot = s0 + __ffs(f) - 1;
+                    qput(c, pos++, slot);
+                }
             }
+        }
+    }
+}
+
+// LEAD pass in exact mode over the flat lead plane: lead32[slot] = body position 0 of
+// every slot, contiguous across segments like the head plane, so one loop over quads
+// covers the whole program (no per-segment bookkeeping): 4 rows per int4 of each plane,
+// U quads in flight; rows with a true lead atom and a false head are queued.
+template <int U>
+__device__ __forceinline__ void flat_lead_exact(const LMParams &p, const PassCtx &c, int64_t gtid,
+                                                int64_t gthreads) {
+    const int32_t nq = (int32_t)(p.n_slots >> 2);
+    const int32_t gth = (int32_t)gthreads;
+    const int4 *lb = reinterpret_cast<const int4 *>(p.lead32);
+    const int4 *hb = reinterpret_cast<const int4 *>(p.head);
+    for (int32_t q0 = (int32_t)gtid; q0 < nq; q0 += gth * U) {
+        int4 v[U], hv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t q = q0 + u * gth;
+            v[u] = q < nq ? ld_stream(lb + q) : make_int4(0, 0, 0, 0);
+            hv[u] = q < nq ? ld_stream(hb + q) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t q = q0 + u * gth;
+            if (q >= nq) break;
+            unsigned fire = test4<true>(v[u], 0xFu, c.sm, 0);
+            if (fire) {
+                const int4 h = hv[u];
+                fire &= (sm_bit(c.sm, (uint32_t)h.x) ? 0u : 1u) | (sm_bit(c.sm, (uint32_t)h.y) ? 0u : 2u) |
+                        (sm_bit(c.sm, (uint32_t)h.z) ? 0u : 4u) | (sm_bit(c.sm, (uint32_t)h.w) ? 0u : 8u);
+            }
+            if (fire) enqueue(p, c, q * 4, fire);
         }
     }
 }
@@ -453,20 +507,20 @@ __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c
     const int32_t gth = (int32_t)gthreads;
     int32_t off = 0;
     for (int32_t s = 0; s < p.nseg; ++s) {
-        const Segment sg = p.segs[s];
+        const Segment sg = c.segs[s];
         const int32_t gt = (int32_t)gtid >= off ? (int32_t)gtid - off : (int32_t)gtid - off + gth;
         off = (int32_t)(((int64_t)off + (sg.count_pad >> 2)) % gth);
         const int32_t gthreads = gth;
-        if (LEAD) {   // (key mode streams runs instead, see the caller)
+        if (LEAD) {   // (used only without a flat lead plane, see the caller)
             seg_lead<EXACT ? 4 : 8, EXACT>(p, sg, c, gt, gthreads);
             continue;
         }
         // U quads in flight per thread: 4-8 int4 loads (EXACT also streams heads)
         switch (sg.L) {
             case 1: seg_pass<1, 4, EXACT>(p, sg, c, gt, gthreads); break;
-            case 2: seg_pass<2, EXACT ? 2 : 4, EXACT>(p, sg, c, gt, gthreads); break;
-            case 3: seg_pass<3, 2, EXACT>(p, sg, c, gt, gthreads); break;
-            case 4: seg_pass<4, EXACT ? 1 : 2, EXACT>(p, sg, c, gt, gthreads); break;
+            case 2: seg_pass<2, 2, EXACT>(p, sg, c, gt, gthreads); break;
+            case 3: seg_pass<3, EXACT ? 2 : 1, EXACT>(p, sg, c, gt, gthreads); break;
+            case 4: seg_pass<4, 1, EXACT>(p, sg, c, gt, gthreads); break;
             case 5: seg_pass<5, 1, EXACT>(p, sg, c, gt, gthreads); break;
             case 6: seg_pass<6, 1, EXACT>(p, sg, c, gt, gthreads); break;
             case 7: seg_pass<7, 1, EXACT>(p, sg, c, gt, gthreads); break;
@@ -490,15 +544,17 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     __shared__ int32_t qcount;
     __shared__ unsigned long long loaded_cta;
     __shared__ uint32_t bmask;
+    __shared__ Segment ssegs[kMaxSmemSegs];
+    __shared__ int32_t squeue[kSmemQueue];
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const bool lead = blockIdx.x == 0 && tid == 0;
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 6] = globaltimer();
-    long long clk0 = 0;
-    unsigned long long ns0 = 0;
-    if (lead) {   // SM clock over the launch: cycles / ns (lp_run.stats_out[4..5])
+    __shared__ long long clk0;          // SM clock over the launch (lp_run.stats_out[4..5]);
+    __shared__ unsigned long long ns0;  // in shared memory: no registers held across passes
+    if (lead) {
         clk0 = clock64();
         ns0 = globaltimer();
     }
@@ -520,6 +576,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         const uint32_t *src0 = EXACT ? p.buf0 : keys ? p.ksummary : p.summary;
         const int32_t nw0 = keys ? p.ksm_words : p.sm_words;
         if (tid == 0) bmask = 0u;
+        if (p.nseg <= kMaxSmemSegs)
+            for (int32_t s = tid; s < p.nseg; s += blockDim.x) ssegs[s] = p.segs[s];
         smem_fill(sm, src0, nw0);
         if (keys) {   // bucket mask: bucket b = summary words [b << 11, (b + 1) << 11)
             __syncthreads();
@@ -546,11 +604,6 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
 #define DBG_STAMP(i) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + (i)]
         if (p.dbg && tid == 0 && k < 16) DBG_STAMP(0) = globaltimer();
         if (k > 0) {
-            // wr holds v_{k-1}: add the atoms derived in pass k-1 to make it v_k
-            for (int64_t i = ds + gtid; i < de; i += gthreads) {
-                const int32_t a = __ldcg(p.order + i);
-                atomicOr(wr + (a >> 5), 1u << (a & 31));
-            }
             // shared copy: v_{k-1} -> v_k
             if (EXACT && (de - ds) > (p.sm_words >> 2)) {
                 for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(rd + w);
@@ -606,16 +659,29 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         }
         // rows queued in pass k are counted in cand[k % 3]; the slot of pass k+1 was last
         // read before the previous barrier and is first written after the next one
-        if (lead) p.cand[(k + 1) % 3] = 0;
-        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, &bmask};
+        if (lead) {
+            p.cand[(k + 1) % 3] = 0;
+            p.pcnt[(k + 1) % 3] = 0;
+        }
+        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, &bmask,
+                        p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, p.pcnt + k % 3, de};
         if (p.dbg && tid == 0 && k < 16) DBG_STAMP(1) = globaltimer();
         if (!EXACT && keys) octets_lead<4>(p, c, gtid, gthreads);
+        else if (EXACT && lead_pass && p.lead32) flat_lead_exact<4>(p, c, gtid, gthreads);
         else if (lead_pass) all_segments<EXACT, true>(p, c, gtid, gthreads);
         else all_segments<EXACT, false>(p, c, gtid, gthreads);
         if (p.dbg && k < 16 && (tid & 31) == 0) atomicMax(&DBG_STAMP(2), globaltimer());
+        // wr still holds v_{k-1}: add the atoms derived in pass k-1 so that it is a superset
+        // of v_k before the barrier (nobody reads wr during pass k -- emit_head tests the
+        // head against v_k first -- so this is off the critical path at the pass top);
+        // spread over all CTAs
+        for (int64_t i = ds + (int64_t)tid * gridDim.x + blockIdx.x; i < de; i += gthreads) {
+            const int32_t a = __ldcg(p.order + i);
+            atomicOr(wr + (a >> 5), 1u << (a & 31));
+        }
         if (!EXACT || lead_pass) {  // epilogue: verify this CTA's queued rows
             __syncthreads();
-            const int32_t nc = min(qcount, p.qcap);
+            const int32_t nc = min(qcount, p.qcap + kSmemQueue);
             __syncthreads();
             if (tid == 0) {
                 qcount = 0;
@@ -624,7 +690,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             const int j0 = (EXACT && lead_pass) ? 1 : 0;
             int loaded = 0;
             for (int32_t i = tid; i < nc; i += blockDim.x)
-                loaded += verify_slot<EXACT>(p, c, __ldcg(c.qbuf + i), j0);
+                loaded += verify_slot<EXACT>(p, c, qget(c, i), j0);
             if (p.stats) {
                 for (int o = 16; o; o >>= 1) loaded += __shfl_xor_sync(0xFFFFFFFFu, loaded, o);
                 if ((tid & 31) == 0 && loaded) atomicAdd(&loaded_cta, (unsigned long long)loaded);
@@ -645,7 +711,9 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         grid.sync();
         if (p.dbg && tid == 0 && k < 16) DBG_STAMP(5) = globaltimer();
 #undef DBG_STAMP
-        const int32_t t = __ldcg(p.tail);
+        // after the barrier: this pass's appends (a slot nobody touches again before the
+        // next barrier -- the shared tail would race with the next pass's appends)
+        const int32_t t = de + __ldcg(p.pcnt + k % 3);
         const int32_t queued = __ldcg(p.cand + k % 3);
         if (lead && p.stats) {
             // algorithmic bytes of this pass: the planes it streamed, 4 B per body entry
@@ -875,7 +943,9 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
             }
             __syncthreads();
         }
-        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, nullptr};
+        if (blockIdx.x == 0 && tid == 0) p.pcnt[(k + 1) % 3] = 0;
+        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, nullptr, p.segs, nullptr,
+                        p.pcnt + k % 3, de};
         if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + 0] = globaltimer();
         if (producer) {
             if (lane == 0) {
@@ -928,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
         }
         grid.sync();
         if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + 5] = globaltimer();
-        const int32_t t = __ldcg(p.tail);
+        const int32_t t = de + __ldcg(p.pcnt + k % 3);   // (see lm_full_kernel)
         const bool lead = blockIdx.x == 0 && tid == 0;
         const bool done = (t == de) || (k + 1 >= p.max_passes);
         if (done) {
@@ -1003,6 +1073,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
     int32_t qs = 0, qe = __ldcg(p.tail);
     if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = qe;
     for (int k = 0;; ++k) {
+        if (blockIdx.x == 0 && tid == 0) p.pcnt[(k + 1) % 3] = 0;   // next level's counter
         for (int64_t i = qs + gwarp; i < qe; i += nwarps) {
             const int32_t a = __ldcg(p.order + i);
             const int64_t o0 = __ldg(p.occ_ptr + a), o1 = __ldg(p.occ_ptr + a + 1);
@@ -1020,7 +1091,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
                     const uint32_t bit = 1u << (h & 31);
                     const uint32_t old = atomicOr(p.buf0 + (h >> 5), bit);
                     if (!(old & bit)) {
-                        const int32_t pos = atomicAdd(p.tail, 1);
+                        const int32_t pos = qe + atomicAdd(p.pcnt + k % 3, 1);
                         p.order[pos] = h;
                         if (p.stage) p.stage[h] = k + 1;
                     }
@@ -1028,7 +1099,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
             }
         }
         grid.sync();
-        const int32_t t = __ldcg(p.tail);
+        const int32_t t = qe + __ldcg(p.pcnt + k % 3);   // (a per-level slot, see lm_full_kernel)
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (t == qe || k + 1 >= p.max_passes) {
             if (lead) {
@@ -1124,6 +1195,7 @@ cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_
     if ((e = cudaMemsetAsync(any_bits, 0, sizeof(uint32_t) * (size_t)p.any_words, st))) return e;
     if ((e = cudaMemsetAsync(p.mark, 0, sizeof(int32_t) * (size_t)p.n_ext, st))) return e;
     if ((e = cudaMemsetAsync(p.tail, 0, sizeof(int32_t), st))) return e;
+    if ((e = cudaMemsetAsync(p.pcnt, 0, 3 * sizeof(int32_t), st))) return e;
     if ((e = cudaMemsetAsync(p.status_out, 0, sizeof(int32_t), st))) return e;
     const int64_t total = (1 + (int64_t)nfacts + k) * p.Wp;
     int b = (int)std::min<int64_t>((total + 255) / 256, 8192);
@@ -1137,7 +1209,7 @@ cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_
 // two words (one 16-byte load per body atom).
 __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int64_t i,
                                        const unsigned long long *rd, unsigned long long *wr,
-                                       int k, int lane) {
+                                       int k, int lane, int32_t *pc, int32_t base) {
     const int32_t h = __ldg(p.head + sg.slot_off + i);
     bool changed = false;
     for (int32_t w = 2 * lane; w < p.Wp; w += 64) {
@@ -1157,7 +1229,7 @@ __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int
     }
     if (__any_sync(0xFFFFFFFFu, changed) && lane == 0) {
         if (atomicExch(p.mark + h, k + 1) != k + 1) {
-            const int32_t pos = atomicAdd(p.tail, 1);
+            const int32_t pos = base + atomicAdd(pc, 1);   // this pass's own counter
             p.order[pos] = h;
         }
     }
@@ -1195,6 +1267,7 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
             }
             __syncthreads();
         }
+        if (blockIdx.x == 0 && tid == 0) p.pcnt[(k + 1) % 3] = 0;   // next pass's counter
         int64_t off = 0;  // rotate each segment's first warp (see all_segments)
         for (int32_t s = 0; s < p.nseg; ++s) {
             const Segment sg = p.segs[s];
@@ -1209,12 +1282,14 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
                 while (m) {
                     const int e = __ffs(m) - 1;
                     m &= m - 1;
-                    st_row(p, sg, base + e, rd, wr, k, lane);
+                    st_row(p, sg, base + e, rd, wr, k, lane, p.pcnt + k % 3, de);
                 }
             }
         }
         grid.sync();
-        const int32_t t = __ldcg(p.tail);
+        // rows changed in this pass: its own counter slot (the next pass appends to
+        // another one, so every CTA reads the same value after the barrier)
+        const int32_t t = de + __ldcg(p.pcnt + k % 3);
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (t == de) {
             if (lead) { *p.passes_out = k + 1; }
@@ -1294,7 +1369,7 @@ cudaError_t launch_st_column(const STParams &p, int32_t n, int64_t g, unsigned l
 
 cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
     cudaError_t e;
-    const int cap = std::max(kMaxSmemBytes, kKeySmemBytes) + 1024;
+    const int cap = std::max(kMaxSmemBytes, kKeySmemBytes);   // + static smem <= 227 KB
     (void)lm_smem;
     (void)st_smem;
     if ((e = cudaFuncSetAttribute((const void *)lm_full_kernel<true>,

@@ -18,6 +18,8 @@ constexpr int kKeySmemBytes = 220 * 1024;   // key-space summary (register-strea
 constexpr int kStageBytes = 16384;      // one TMA pipeline stage (bulk copies of col rows)
 constexpr int kSmemLimit = 232448 - 1024;  // opt-in smem per CTA on sm_100 minus static
 constexpr int kMaxTileSegs = 64;
+constexpr int kMaxSmemSegs = 64;       // segment table copied to shared memory up to this size
+constexpr int kSmemQueue = 768;        // candidate queue entries kept in shared memory per CTA
 
 // A body-length segment cut into TMA tiles of T rows.  A tile stages R = L (+1 when the
 // head row is staged too) rows of T ints each: row j holds body position j of T
@@ -88,6 +90,9 @@ struct LMParams {
     int32_t dense_div;
     int64_t n_slots;
     int32_t *cand;             // [3] rows queued per pass (slot k % 3)
+    int32_t *pcnt;             // [3] atoms appended to the derivation list per pass (slot
+                               //     k % 3): read by every CTA after the pass's barrier,
+                               //     never written again before the next one
     unsigned long long *stats; // [4] algorithmic bytes, LEAD passes, rows verified,
                                //     body entries loaded by verification
     long long lead_bytes;      // bytes one LEAD / STREAM pass streams (program planes only)
@@ -98,6 +103,7 @@ struct LMParams {
     // coarse ones.  STREAM passes switch the shared copy back to the atom-id summary.
     const uint16_t *lead16;    // [n_slots] low 16 bits of the lead atom's key group, or NULL
     const uint8_t *octet_tag;  // [n_slots / 8] bucket (group >> 16, < 32) | padding rows << 5
+    const int32_t *lead32;     // exact mode: [n_slots] body position 0 of every slot (flat)
     const int32_t *key_of;     // [n_ext] key of every extended atom
     uint32_t *ksummary;        // [ksm_words] summary of v_0 in key space (zero between calls)
     int32_t *korder;           // [n_ext + 1] key of order[i] (written with it)
@@ -124,6 +130,7 @@ struct STParams {
     int32_t any_shift;
     int32_t *order;            // rows changed per pass
     int32_t *tail;
+    int32_t *pcnt;             // [3] per-pass append counters (slot k % 3)
     int32_t *mark;             // [n_ext] pass tag of the last push
     int32_t *passes_out;
     int32_t *status_out;

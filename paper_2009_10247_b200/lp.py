@@ -151,8 +151,16 @@ def _torch_allocator(device: int):
         except Exception:  # noqa: BLE001 -- reported to C as NULL -> LP_E_NOMEM
             return None
 
+    cuda = torch.cuda
+
     def _free(ptr, nbytes, ctx):
-        torch.cuda.caching_allocator_delete(ptr)
+        # at interpreter exit the torch module may already be torn down: the process's
+        # device memory goes away with it, so there is nothing left to return
+        if cuda is not None and getattr(cuda, "caching_allocator_delete", None) is not None:
+            try:
+                cuda.caching_allocator_delete(ptr)
+            except Exception:  # noqa: BLE001
+                pass
 
     return ALLOC_FN(_alloc), FREE_FN(_free)
 
