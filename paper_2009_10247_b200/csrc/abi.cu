@@ -66,7 +66,6 @@ struct lp_program {
     uint8_t *d_octet_tag = nullptr;
     int32_t *d_lead32 = nullptr;    // exact mode: flat lead plane
     int32_t *d_key_of = nullptr;
-    uint32_t *d_ksummary = nullptr;
     int32_t *d_korder = nullptr;
     int32_t ksm_words = 0, kshift = 0;
     uint32_t *d_factbits = nullptr;
@@ -291,9 +290,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(upload(p, &p->d_lead16, lead16));
         TRY(upload(p, &p->d_octet_tag, tag));
         TRY(upload(p, &p->d_key_of, key));
-        TRY(dalloc(p, &p->d_ksummary, (size_t)kw));
         TRY(dalloc(p, &p->d_korder, (size_t)L.n_ext + 1));
-        CK(cudaMemset(p->d_ksummary, 0, (size_t)kw * 4));
         p->lm_smem = std::max(p->lm_smem, (size_t)kw * 4);
     }
 
@@ -607,7 +604,6 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.octet_tag = p->d_octet_tag;
     q.lead32 = (frontier || p->use_tma) ? nullptr : p->d_lead32;
     q.key_of = p->d_key_of;
-    q.ksummary = p->d_ksummary;
     q.korder = p->d_korder;
     q.ksm_words = p->ksm_words;
     q.kshift = p->kshift;

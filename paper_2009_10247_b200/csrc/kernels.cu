@@ -97,8 +97,9 @@ __device__ __forceinline__ int32_t warp_reserve(int32_t *tail, int32_t cnt) {
 // written to both buffers.  Warps walk consecutive truth words (coalesced); each lane
 // lists the original atoms of its word into the derivation list (slots reserved once
 // per warp), writes their stages (0, or -1 for false atoms; one coalesced row per word
-// of the warp) and, in summary mode, adds the word to the key-space summary (LEAD
-// passes) and/or the atom-id summary (STREAM passes), both zero on entry.
+// of the warp) and, in summary mode, lists the atoms' keys (LEAD passes: every CTA builds
+// its key-space summary from that list) and/or adds the word to the atom-id summary
+// (STREAM passes, zero on entry).
 // Also zeroes the other-parity run counters for the next call.
 __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, int64_t gtid,
                                          int64_t gthreads) {
@@ -109,10 +110,6 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
     }
     const bool keys = summary_mode && p.lead16;
     const bool osum = summary_mode && !(keys && p.pass_mode != 2);
-    if (keys && gtid == 0) {          // ⊤ is always true
-        const uint32_t g = (uint32_t)__ldg(p.key_of + p.top) >> p.kshift;
-        atomicOr(p.ksummary + (g >> 5), 1u << (g & 31));
-    }
     const int lane = threadIdx.x & 31;
     for (int64_t w0 = gtid - lane; w0 < p.nwords; w0 += gthreads) {
         const int64_t w = w0 + lane;
@@ -131,12 +128,8 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
         for (uint32_t b = orig; b;) {
             const int i = __ffs(b) - 1;
             b &= b - 1;
-            if (keys) {
-                const int32_t key = __ldg(p.key_of + lo + i);
-                const uint32_t g = (uint32_t)key >> p.kshift;
-                atomicOr(p.ksummary + (g >> 5), 1u << (g & 31));
-                p.korder[pos] = key;
-            }
+            if (keys) p.korder[pos] = __ldg(p.key_of + lo + i);   // the CTAs build their
+                                                                // key summaries from it
             p.order[pos++] = (int32_t)(lo + i);
         }
         if (p.stage) {   // row i of the warp's 32x32 block = word w0+i, lane = bit
@@ -169,8 +162,6 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
 __device__ __forceinline__ void lm_zero_summaries(const LMParams &p, bool summary_mode, int64_t gtid,
                                                   int64_t gthreads) {
     if (!summary_mode) return;
-    if (p.lead16)
-        for (int64_t w = gtid; w < p.ksm_words; w += gthreads) p.ksummary[w] = 0u;
     if (!(p.lead16 && p.pass_mode != 2))
         for (int64_t w = gtid; w < p.sm_words; w += gthreads) p.summary[w] = 0u;
 }
@@ -254,7 +245,7 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
 // v_k cannot change anything -- then body positions j0..L-1 (LEAD passes have already
 // tested position 0 exactly in EXACT mode).  Returns the body entries it loaded.
 template <bool EXACT>
-__device__ __noinline__ int verify_slot(const LMParams &p, const PassCtx &c, int32_t slot, int j0) {
+__device__ __forceinline__ int verify_slot(const LMParams &p, const PassCtx &c, int32_t slot, int j0) {
     int lo = 0, hi = p.nseg - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -530,6 +521,39 @@ __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c
     }
 }
 
+// Add derivation-list entries [i0, i1) to a CTA's shared copy of v_k: exact bits
+// (EXACT), key groups (keys: the list's korder twin) or atom-id groups; in key mode the
+// per-bucket any-bit mask too.  4 independent list reads in flight per thread.
+template <bool EXACT>
+__device__ __forceinline__ void add_to_shared(const LMParams &p, uint32_t *sm, uint32_t *bmask,
+                                              int32_t i_begin, int32_t i_end, bool keys) {
+    for (int64_t i0 = i_begin + threadIdx.x; i0 < i_end; i0 += 4 * (int64_t)blockDim.x) {
+        uint32_t a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * (int64_t)blockDim.x;
+            a[u] = i < i_end ? (uint32_t)__ldcg((keys ? p.korder : p.order) + i) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (a[u] == 0xFFFFFFFFu) continue;
+            a[u] = EXACT ? a[u] : keys ? (a[u] >> p.kshift) : (a[u] >> p.shift);
+        }
+        uint32_t m = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (a[u] != 0xFFFFFFFFu) {
+                atomicOr(sm + (a[u] >> 5), 1u << (a[u] & 31));
+                m |= 1u << ((a[u] >> 16) & 31);
+            }
+        if (!EXACT && keys) {   // (lanes of a warp may have left the loop already)
+            const unsigned act = __activemask();
+            m = __reduce_or_sync(act, m);
+            if ((threadIdx.x & 31) == __ffs(act) - 1 && m) atomicOr(bmask, m);
+        }
+    }
+}
+
 // One cooperative launch = the whole fixpoint loop of Algorithm 1:
 // pass k reads v_k (rd) and writes v_{k+1} (wr); the loop ends after the first pass
 // that derives nothing (u = v), and iters = k + 1 counts that pass too.
@@ -572,23 +596,21 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     bool lead_pass = p.pass_mode != 2;
     bool keys = !EXACT && p.lead16 && lead_pass;         // shared copy is in key space
     bool rebuild = false;                                // key space -> atom-id summary
+    const int32_t n0 = __ldcg(p.tail);
     {
-        const uint32_t *src0 = EXACT ? p.buf0 : keys ? p.ksummary : p.summary;
-        const int32_t nw0 = keys ? p.ksm_words : p.sm_words;
         if (tid == 0) bmask = 0u;
         if (p.nseg <= kMaxSmemSegs)
             for (int32_t s = tid; s < p.nseg; s += blockDim.x) ssegs[s] = p.segs[s];
-        smem_fill(sm, src0, nw0);
-        if (keys) {   // bucket mask: bucket b = summary words [b << 11, (b + 1) << 11)
+        if (keys) {   // key summary of v_0 straight from the initial list (bucket b =
+                      // summary words [b << 11, (b + 1) << 11))
+            int4 *s4 = reinterpret_cast<int4 *>(sm);
+            for (int32_t w = tid; w < (p.ksm_words >> 2); w += blockDim.x) s4[w] = make_int4(0, 0, 0, 0);
             __syncthreads();
-            uint32_t m = 0;
-            for (int32_t w = tid; w < nw0; w += blockDim.x)
-                if (sm[w]) m |= 1u << ((w >> 11) & 31);
-            m = __reduce_or_sync(0xFFFFFFFFu, m);
-            if ((tid & 31) == 0 && m) atomicOr(&bmask, m);
+            add_to_shared<EXACT>(p, sm, &bmask, 0, n0, true);
+        } else {
+            smem_fill(sm, EXACT ? p.buf0 : p.summary, p.sm_words);
         }
     }
-    const int32_t n0 = __ldcg(p.tail);
     if (lead && p.pops && p.pop_cap > 0) p.pops[0] = n0;
     if (tid == 0) {
         qcount = 0;
@@ -628,32 +650,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                     }
                 }
             } else {
-                // 4 independent list reads (and key lookups) in flight per thread
-                for (int64_t i0 = ds + tid; i0 < de; i0 += 4 * (int64_t)blockDim.x) {
-                    uint32_t a[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int64_t i = i0 + u * (int64_t)blockDim.x;
-                        a[u] = i < de ? (uint32_t)__ldcg((keys ? p.korder : p.order) + i) : 0xFFFFFFFFu;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (a[u] == 0xFFFFFFFFu) continue;
-                        a[u] = EXACT ? a[u] : keys ? (a[u] >> p.kshift) : (a[u] >> p.shift);
-                    }
-                    uint32_t m = 0;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (a[u] != 0xFFFFFFFFu) {
-                            atomicOr(sm + (a[u] >> 5), 1u << (a[u] & 31));
-                            m |= 1u << ((a[u] >> 16) & 31);
-                        }
-                    if (!EXACT && keys) {   // (lanes of a warp may have left the loop already)
-                        const unsigned act = __activemask();
-                        m = __reduce_or_sync(act, m);
-                        if ((tid & 31) == __ffs(act) - 1 && m) atomicOr(&bmask, m);
-                    }
-                }
+                add_to_shared<EXACT>(p, sm, &bmask, ds, de, keys);
             }
             __syncthreads();
         }

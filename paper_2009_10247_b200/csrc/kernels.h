@@ -105,9 +105,8 @@ struct LMParams {
     const uint8_t *octet_tag;  // [n_slots / 8] bucket (group >> 16, < 32) | padding rows << 5
     const int32_t *lead32;     // exact mode: [n_slots] body position 0 of every slot (flat)
     const int32_t *key_of;     // [n_ext] key of every extended atom
-    uint32_t *ksummary;        // [ksm_words] summary of v_0 in key space (zero between calls)
     int32_t *korder;           // [n_ext + 1] key of order[i] (written with it)
-    int32_t ksm_words;
+    int32_t ksm_words;         // words of the key-space summary (shared memory)
     int32_t kshift;
 };
 
