@@ -75,6 +75,13 @@ typedef void *(*lp_alloc_fn)(size_t bytes, void *ctx);
 typedef void (*lp_free_fn)(void *ptr, size_t bytes, void *ctx);
 
 #define LP_LOAD_NO_FRONTIER 0x1u /* do not build the transposed occurrence lists */
+#define LP_LOAD_PAPER_LAYOUT 0x4u /* standardize into P^δ first: a head with
+                                    k >= 2 rules gets auxiliary atoms x_1..x_k and the
+                                    OR-row h <- x_1 ∨ ... ∨ x_k, as in the paper's matrix
+                                    M_{P^δ}; pass counts and popcount traces (which then
+                                    count the auxiliaries too) follow Algorithms 1-2
+                                    literally (convention (A), R4).  Models,
+                                    stages, v0 and guesses stay over the original atoms */
 #define LP_LOAD_TMA 0x2u         /* use the TMA-pipelined full θ-pass (cp.async.bulk ring)
                                     instead of the register-streaming one; same results,
                                     slower on B200 for HBM-streaming programs */
@@ -148,6 +155,7 @@ typedef struct {
     int64_t stream_pass_bytes;/* program bytes a STREAM full θ-pass streams              */
     int32_t key_shift;        /* summary mode: keys per key-summary bit = 1 << key_shift;
                                  -1 when there is no key plane                         */
+    int32_t n_aux;            /* LP_LOAD_PAPER_LAYOUT: auxiliary atoms of P^δ (else 0)  */
 } lp_info_t;
 
 /* Validate, standardize and encode a program, upload it (PAPER.md:62, 82-95,

@@ -174,8 +174,12 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
     p->sms = sms;
 
-    TRY(upload(p, &p->d_facts, L.facts));
-    p->nfacts = (int32_t)L.facts.size();
+    {   // rows of the stable initial matrix set to 1 (Def. 8 item 2)
+        std::vector<int32_t> sf(L.facts);
+        sf.insert(sf.end(), L.st_facts.begin(), L.st_facts.end());
+        TRY(upload(p, &p->d_facts, sf));
+        p->nfacts = (int32_t)sf.size();
+    }
     TRY(upload(p, &p->d_negated, L.negated));
     {
         std::vector<int32_t> ext(L.k), rank(L.k, -1);
@@ -197,7 +201,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         for (int32_t a : L.facts) fb[(size_t)a >> 5] |= 1u << (a & 31);
         TRY(upload(p, &p->d_factbits, fb));
     }
-    const size_t mw = std::max<size_t>(((size_t)L.n + 63) / 64, 1);
+    const size_t mw = std::max<size_t>(((size_t)L.n_out + 63) / 64, 1);
     TRY(dalloc(p, &p->d_v0, mw));
     TRY(dalloc(p, &p->d_model, mw));
 
@@ -426,7 +430,8 @@ extern "C" lp_status lp_load(const lp_rules *rules, const lp_options *opt, lp_pr
     std::string err;
     lp_status s;
     try {
-        s = encode(rules, occ && p->device >= 0, &p->L, &err);
+        s = encode(rules, occ && p->device >= 0, &p->L, &err,
+                   opt && (opt->flags & LP_LOAD_PAPER_LAYOUT));
     } catch (const std::bad_alloc &) {
         s = LP_E_NOMEM;
         err = "host allocation failed while encoding";
@@ -457,7 +462,8 @@ extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
     if (!p || !o) return set_err(LP_E_INVALID, "NULL argument");
     const HostLayout &L = p->L;
     std::memset(o, 0, sizeof(*o));
-    o->n_atoms = L.n;
+    o->n_atoms = L.n_out;
+    o->n_aux = L.n_aux;
     o->n_rules = L.n_rules;
     o->nnz = L.nnz;
     o->n_heads = L.n_heads;
@@ -509,7 +515,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
         return set_err(LP_E_INVALID, "LP_FRONTIER on a program loaded with LP_LOAD_NO_FRONTIER");
     cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
     CK(cudaSetDevice(p->device));
-    const size_t mw = ((size_t)L.n + 63) / 64;
+    const size_t mw = ((size_t)L.n_out + 63) / 64;
 
     const uint32_t *v0d = nullptr;
     if (v0) {
@@ -521,10 +527,10 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
         }
     }
     int32_t *stage = nullptr;
-    if (run && run->stage_out && L.n > 0) {
+    if (run && run->stage_out && L.n_out > 0) {
         if (dev) stage = run->stage_out;
         else {
-            if (!p->d_stage) TRY(dalloc(p, &p->d_stage, (size_t)L.n));
+            if (!p->d_stage) TRY(dalloc(p, &p->d_stage, (size_t)L.n_out));
             stage = p->d_stage;
         }
     }
@@ -547,6 +553,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.segs = p->d_segs;
     q.nseg = (int32_t)L.segs.size();
     q.n = L.n;
+    q.n_out = L.n_out;
     q.col = p->d_col;
     q.head = p->d_head;
     q.buf0 = p->d_buf0;
@@ -621,7 +628,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     CK(cudaMemcpyAsync(scal, p->d_scal, sizeof(scal), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(scal + 2, p->d_scal + 10 + par, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     if (mw) CK(cudaMemcpyAsync(model_out, p->d_model, mw * 8, cudaMemcpyDeviceToHost, st));
-    if (stage) CK(cudaMemcpyAsync(run->stage_out, stage, sizeof(int32_t) * (size_t)L.n,
+    if (stage) CK(cudaMemcpyAsync(run->stage_out, stage, sizeof(int32_t) * (size_t)L.n_out,
                                   cudaMemcpyDeviceToHost, st));
     if (pops) CK(cudaMemcpyAsync(run->popcounts_out, pops, sizeof(int32_t) * (size_t)pop_cap,
                                  cudaMemcpyDeviceToHost, st));
@@ -760,9 +767,9 @@ extern "C" lp_status lp_stable_matrix(lp_program *p, uint64_t *out, const lp_run
     const bool dev = run && (run->flags & LP_PTR_DEVICE);
     cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
     CK(cudaSetDevice(p->device));
-    if (p->L.n == 0) return LP_OK;
+    if (p->L.n_out == 0) return LP_OK;
     CK(cudaMemcpy2DAsync(out, (size_t)p->W * 8, p->d_T0, (size_t)p->Wp * 8, (size_t)p->W * 8,
-                         (size_t)p->L.n, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+                         (size_t)p->L.n_out, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
     if (!dev) CK(cudaStreamSynchronize(st));
     return LP_OK;
 }
@@ -778,9 +785,9 @@ extern "C" lp_status lp_guess_model(lp_program *p, int64_t guess, uint64_t *mode
     CK(cudaSetDevice(p->device));
     STParams s = st_params(p);
     unsigned long long *o = dev ? reinterpret_cast<unsigned long long *>(model_out) : p->d_model;
-    CK(launch_st_column(s, p->L.n, guess, o, st));
+    CK(launch_st_column(s, p->L.n_out, guess, o, st));
     if (dev) return LP_OK;
-    const size_t mw = ((size_t)p->L.n + 63) / 64;
+    const size_t mw = ((size_t)p->L.n_out + 63) / 64;
     if (mw) CK(cudaMemcpyAsync(model_out, p->d_model, mw * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return LP_OK;

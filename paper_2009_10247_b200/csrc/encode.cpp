@@ -25,7 +25,96 @@ static lp_status fail(std::string *err, lp_status s, const std::string &msg) {
     return s;
 }
 
-lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *err) {
+static lp_status encode_core(const lp_rules *r, bool build_occ, HostLayout *L, std::string *err);
+
+// Standardisation P -> P^δ, used by LP_LOAD_PAPER_LAYOUT: every head h with
+// k >= 2 rules gets fresh auxiliary atoms x_1..x_k (numbered after the originals, heads in
+// ascending order, rules in input order): x_i <- body(r_i) (an auxiliary fact when the
+// body is empty, reading R10) and h <- x_i, i.e. the OR-row h <- x_1 ∨ ... ∨ x_k as k
+// one-atom rules (the kernels OR all rules of a head).  Heads with one rule pass through.
+// Iterating T over P^δ from its facts is Algorithm 1 over the paper's matrix M_{P^δ}:
+// pass counts and popcount traces follow convention (A) (reading R4).
+lp_status encode(const lp_rules *r, bool build_occ, HostLayout *L, std::string *err,
+                 bool paper_layout) {
+    if (!paper_layout || !r) {
+        lp_status s = encode_core(r, build_occ, L, err);
+        if (s == LP_OK) L->n_out = L->n;
+        return s;
+    }
+    // (st_facts: the extra initial-matrix rows of Def. 8, filled in below)
+    if (r->n_atoms < 0 || r->n_rules < 0) return fail(err, LP_E_INVALID, "negative n_atoms or n_rules");
+    const int64_t R = r->n_rules;
+    const int32_t n = r->n_atoms;
+    if (R > 0 && (!r->head || !r->body_ptr)) return fail(err, LP_E_INVALID, "NULL head or body_ptr");
+    for (int64_t i = 0; i < R; ++i)
+        if (r->head[i] < 0 || r->head[i] >= n)
+            return fail(err, LP_E_INVALID, "head out of range at rule " + std::to_string(i));
+    if (R > 0 && r->body_ptr[0] != 0) return fail(err, LP_E_INVALID, "body_ptr[0] != 0");
+    for (int64_t i = 0; i < R; ++i)
+        if (r->body_ptr[i + 1] < r->body_ptr[i])
+            return fail(err, LP_E_INVALID, "body_ptr not non-decreasing at rule " + std::to_string(i));
+    if (R > 0 && r->body_ptr[R] > 0 && !r->body_atom) return fail(err, LP_E_INVALID, "NULL body_atom");
+    for (int64_t j = 0; j < (R > 0 ? r->body_ptr[R] : 0); ++j)
+        if (r->body_atom[j] < 0 || r->body_atom[j] >= n)
+            return fail(err, LP_E_INVALID, "body atom out of range at literal " + std::to_string(j));
+    std::vector<int64_t> per((size_t)n + 1, 0);
+    for (int64_t i = 0; i < R; ++i) per[(size_t)r->head[i]]++;
+    std::vector<int64_t> first_aux((size_t)n + 1, -1);
+    int64_t naux = 0;
+    for (int32_t h = 0; h < n; ++h)
+        if (per[(size_t)h] >= 2) { first_aux[(size_t)h] = naux; naux += per[(size_t)h]; }
+    if ((int64_t)n + naux + 2 > std::numeric_limits<int32_t>::max())
+        return fail(err, LP_E_INVALID, "too many atoms after standardisation");
+    const int64_t nnz_in = R > 0 ? r->body_ptr[R] : 0;
+    std::vector<int32_t> head, atom;
+    std::vector<int64_t> ptr{0};
+    std::vector<uint8_t> neg;
+    std::vector<int64_t> used((size_t)n + 1, 0);
+    head.reserve((size_t)(R + naux));
+    atom.reserve((size_t)(nnz_in + naux));
+    for (int64_t i = 0; i < R; ++i) {
+        const int32_t h = r->head[i];
+        int32_t tgt = h;
+        if (first_aux[(size_t)h] >= 0) {   // x_i <- body(r_i), then h <- x_i
+            tgt = (int32_t)(n + first_aux[(size_t)h] + used[(size_t)h]++);
+        }
+        head.push_back(tgt);
+        for (int64_t j = r->body_ptr[i]; j < r->body_ptr[i + 1]; ++j) {
+            atom.push_back(r->body_atom[j]);
+            neg.push_back(r->body_neg ? r->body_neg[j] : 0);
+        }
+        ptr.push_back((int64_t)atom.size());
+        if (tgt != h) {
+            head.push_back(h);
+            atom.push_back(tgt);
+            neg.push_back(0);
+            ptr.push_back((int64_t)atom.size());
+        }
+    }
+    lp_rules t{(int32_t)(n + naux), (int64_t)head.size(), head.data(), ptr.data(), atom.data(),
+               r->body_neg ? neg.data() : nullptr};
+    lp_status s = encode_core(&t, build_occ, L, err);
+    if (s != LP_OK) return s;
+    L->n_out = n;
+    L->n_aux = (int32_t)naux;
+    L->n_rules = R;
+    // Def. 8 builds the initial guess matrix from the facts of P itself:
+    // item 2 sets the row of every atom with a fact in P (even when P^δ turned that fact
+    // into an auxiliary one), item 3 fixes the abar of such an atom to 0.
+    std::vector<uint8_t> fact_p((size_t)n + 1, 0);
+    for (int64_t i = 0; i < R; ++i)
+        if (r->body_ptr[i] == r->body_ptr[i + 1]) fact_p[(size_t)r->head[i]] = 1;
+    for (int32_t a = 0; a < n; ++a)
+        if (fact_p[(size_t)a] && std::find(L->facts.begin(), L->facts.end(), a) == L->facts.end())
+            L->st_facts.push_back(a);
+    L->free_j.clear();
+    for (int32_t j = 0; j < L->k; ++j)
+        if (!fact_p[(size_t)L->negated[(size_t)j]]) L->free_j.push_back(j);
+    L->f = (int32_t)L->free_j.size();
+    return LP_OK;
+}
+
+static lp_status encode_core(const lp_rules *r, bool build_occ, HostLayout *L, std::string *err) {
     if (!r || !L) return fail(err, LP_E_INVALID, "NULL rules or output");
     const int64_t R = r->n_rules;
     const int32_t n = r->n_atoms;

@@ -117,7 +117,9 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
         uint32_t orig = 0, bits = 0;
         if (w < p.nwords) {
             orig = __ldg(p.factbits + w);
-            if (p.v0 && w < p.v0_words && lo < p.n) orig |= __ldg(p.v0 + w);
+            uint32_t v = (p.v0 && w < p.v0_words) ? __ldg(p.v0 + w) : 0u;   // originals only
+            if (lo + 32 > p.n_out) v &= lo >= p.n_out ? 0u : ((1u << (uint32_t)(p.n_out - lo)) - 1u);
+            orig |= v;
             if (lo + 32 > p.n) orig &= lo >= p.n ? 0u : ((1u << (uint32_t)(p.n - lo)) - 1u);
             bits = orig;
             if (w == (p.top >> 5)) bits |= 1u << (p.top & 31);
@@ -136,7 +138,7 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
             for (int i = 0; i < 32; ++i) {
                 const uint32_t oi = __shfl_sync(0xFFFFFFFFu, orig, i);
                 const int64_t a = (w0 + i) * 32 + lane;
-                if (a < p.n) p.stage[a] = ((oi >> lane) & 1u) ? 0 : -1;
+                if (a < p.n_out) p.stage[a] = ((oi >> lane) & 1u) ? 0 : -1;
             }
         }
         if (osum) {   // word w contributes to atom-id summary word w >> shift
@@ -168,12 +170,12 @@ __device__ __forceinline__ void lm_zero_summaries(const LMParams &p, bool summar
 
 // In-kernel epilogue: the model over the original atoms, LSB-first uint64 words.
 __device__ __noinline__ void lm_extract(const LMParams &p, int64_t gtid, int64_t gthreads) {
-    const int64_t nw = ((int64_t)p.n + 63) >> 6;
+    const int64_t nw = ((int64_t)p.n_out + 63) >> 6;
     for (int64_t w = gtid; w < nw; w += gthreads) {
         unsigned long long v = (unsigned long long)__ldcg(p.buf0 + 2 * w) |
                                ((unsigned long long)__ldcg(p.buf0 + 2 * w + 1) << 32);
         const int64_t lo = w * 64;
-        if (lo + 64 > p.n) v &= (1ull << (uint32_t)(p.n - lo)) - 1ull;
+        if (lo + 64 > p.n_out) v &= (1ull << (uint32_t)(p.n_out - lo)) - 1ull;
         p.model_out[w] = v;
     }
 }
@@ -236,7 +238,7 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
     const int32_t pos = c.base + base + __popc(m & ((1u << lane) - 1u));
     p.order[pos] = h;
     if (p.lead16) p.korder[pos] = __ldg(p.key_of + h);   // once per atom, not per CTA
-    if (p.stage) p.stage[h] = c.k + 1;
+    if (p.stage && h < p.n_out) p.stage[h] = c.k + 1;
 }
 
 
@@ -1090,7 +1092,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
                     if (!(old & bit)) {
                         const int32_t pos = qe + atomicAdd(p.pcnt + k % 3, 1);
                         p.order[pos] = h;
-                        if (p.stage) p.stage[h] = k + 1;
+                        if (p.stage && h < p.n_out) p.stage[h] = k + 1;
                     }
                 }
             }

@@ -37,7 +37,8 @@ struct TileSeg {
 struct LMParams {
     const Segment *segs;
     int32_t nseg;
-    int32_t n;                 // original atoms (stage / popcount range)
+    int32_t n;                 // atoms of the encoded program (originals + P^δ auxiliaries)
+    int32_t n_out;             // original atoms: v0, model and stage range
     const int32_t *col;
     const int32_t *head;
     uint32_t *buf0;            // truth vector v_k (bit a of word a>>5); double buffer

@@ -25,7 +25,9 @@ struct Segment {
 
 // Host-side result of standardisation + encoding.
 struct HostLayout {
-    int32_t n = 0;        // original atoms
+    int32_t n = 0;        // atoms of the encoded program (originals + P^δ auxiliaries)
+    int32_t n_out = 0;    // atoms the caller sees (v0, models, stages): the originals
+    int32_t n_aux = 0;    // LP_LOAD_PAPER_LAYOUT: auxiliary atoms n_out .. n-1
     int32_t k = 0;        // negated atoms (abar_j = n + j)
     int32_t f = 0;        // free negated atoms (not facts)
     int32_t top = 0;      // ⊤ = n + k  (always true; body of every fact)
@@ -44,7 +46,9 @@ struct HostLayout {
     std::vector<int32_t> head;      // per slot
     int64_t n_slots = 0;
 
-    std::vector<int32_t> facts;     // distinct original atoms with a fact rule
+    std::vector<int32_t> facts;     // distinct atoms with a fact rule (in the encoded program)
+    std::vector<int32_t> st_facts;  // LP_LOAD_PAPER_LAYOUT: atoms with a fact in P whose
+                                    // fact became an auxiliary one (Def. 8 item 2 rows)
     std::vector<int32_t> negated;   // k ascending atom ids
     std::vector<int32_t> free_j;    // indices j of the free negated atoms (ascending)
 
@@ -64,7 +68,8 @@ struct Run {
 };
 
 // encode.cpp
-lp_status encode(const lp_rules *r, bool build_occ, HostLayout *out, std::string *err);
+lp_status encode(const lp_rules *r, bool build_occ, HostLayout *out, std::string *err,
+                 bool paper_layout = false);
 void build_occ_lists(HostLayout *L);
 void bucket_rows(HostLayout *L, const std::vector<int32_t> &bucket_of_atom, int align,
                  std::vector<Run> *runs);

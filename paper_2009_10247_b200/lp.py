@@ -23,6 +23,7 @@ LP_OK, LP_E_INVALID, LP_E_PARSE, LP_E_SEMANTIC, LP_E_CAP = 0, 1, 2, 3, 4
 LP_E_NOMEM, LP_E_CUDA, LP_E_NOT_CONVERGED, LP_E_NODEVICE = 5, 6, 7, 8
 LP_LOAD_NO_FRONTIER = 0x1
 LP_LOAD_TMA = 0x2
+LP_LOAD_PAPER_LAYOUT = 0x4
 LP_PTR_DEVICE = 0x1
 LP_FRONTIER = 0x2
 LP_FULL_STREAM = 0x4
@@ -60,7 +61,8 @@ class lp_info_t(ctypes.Structure):
                 ("summary_shift", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
                 ("block_threads", ctypes.c_int32), ("full_kernel", ctypes.c_int32),
                 ("tma_stages", ctypes.c_int32), ("lead_pass_bytes", ctypes.c_int64),
-                ("stream_pass_bytes", ctypes.c_int64), ("key_shift", ctypes.c_int32)]
+                ("stream_pass_bytes", ctypes.c_int64), ("key_shift", ctypes.c_int32),
+                ("n_aux", ctypes.c_int32)]
 
 
 SYMBOLS = ("lp_load", "lp_info", "lp_negated_atoms", "lp_least_model", "lp_stable_models",
@@ -174,7 +176,7 @@ class Program:
 
     def __init__(self, rules, device: int = 0, guess_cap: int = 20, frontier: bool = True,
                  smem_bits_cap: int = 0, grid_blocks: int = 0, allocator: str = "torch",
-                 tma: bool = False):
+                 tma: bool = False, paper_layout: bool = False):
         lib = library()
         self._keep = []
         head = np.ascontiguousarray(rules.head, dtype=np.int32)
@@ -185,7 +187,8 @@ class Program:
         opt = lp_options()
         opt.device = int(device)
         opt.guess_cap = int(guess_cap)
-        opt.flags = (0 if frontier else LP_LOAD_NO_FRONTIER) | (LP_LOAD_TMA if tma else 0)
+        opt.flags = ((0 if frontier else LP_LOAD_NO_FRONTIER) | (LP_LOAD_TMA if tma else 0) |
+                     (LP_LOAD_PAPER_LAYOUT if paper_layout else 0))
         opt.smem_bits_cap = int(smem_bits_cap)
         opt.grid_blocks = int(grid_blocks)
         if device >= 0 and allocator == "torch":
@@ -234,7 +237,7 @@ class Program:
                 mask[a.astype(np.int64)] = True
             v0w = pack_mask(mask)
         model = np.zeros(max(bits_words(n), 1), dtype=np.uint64)
-        pops = np.zeros(n + 3, dtype=np.int32) if popcounts else None
+        pops = np.zeros(n + self.info["n_aux"] + 3, dtype=np.int32) if popcounts else None
         stage = np.zeros(max(n, 1), dtype=np.int32) if stages else None
         st = np.zeros(6, dtype=np.uint64) if stats else None
         iters = lp_least_model(self, v0w, model, frontier=frontier, pops=pops, stage=stage,

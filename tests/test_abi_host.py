@@ -108,3 +108,18 @@ def test_c5_host_encode():
     assert i["n_negated"] == 12 and i["n_free_negated"] == 12
     assert p.negated_atoms() == C.meta["negated_atoms"]
     assert i["nnz"] == C.nnz + 1000          # + ⊤ for every fact
+
+
+def test_paper_layout_host_shapes():
+    """LP_LOAD_PAPER_LAYOUT: the standardized program P^δ has one auxiliary
+    atom per rule of every multi-rule head (oracle/paper.py standardize) and the caller
+    still sees the original atoms."""
+    from oracle import paper
+    rng = np.random.default_rng(3)
+    for _ in range(30):
+        n = int(rng.integers(1, 50))
+        P = lpgen.random_program(rng, n, int(rng.integers(0, 5 * n)), max_len=4)
+        m, _ = paper.standardize(P)
+        info = _host(P, paper_layout=True).info
+        assert info["n_atoms"] == n and info["n_aux"] == m - n
+        assert _host(P).info["n_aux"] == 0

@@ -344,3 +344,61 @@ def test_guess_offset_c5_slices():
         got += (ids + off).tolist()
         passes = max(passes, ps)
     assert got == np.nonzero(o["accepted"])[0].tolist() and passes == o["passes"]
+
+
+# ---------------------------------------------------------------------------------
+# convention (A): the paper's own matrix M_{P^δ} (LP_LOAD_PAPER_LAYOUT)
+# ---------------------------------------------------------------------------------
+
+def test_paper_layout_example1():
+    """Example 1: Algorithm 1 literally takes 3 products with |v|
+    trace 2, 5, 7 (convention (A)); the least model over B_P is {p,q,r,s,t}."""
+    from oracle import paper
+    P = lpgen.from_lists(5, [(0, [1, 2]), (0, [3, 4]), (2, [3]), (1, [4]), (3, []), (4, [])])
+    prog = lp.Program(P, paper_layout=True)
+    assert prog.info["n_aux"] == 2 and prog.info["n_atoms"] == 5
+    for frontier in (False, True):
+        model, iters, ex = prog.least_model(frontier=frontier, popcounts=True, stages=True)
+        assert iters == 3 and ex["popcounts"] == [2, 5, 7]
+        assert lp.unpack_bits(model, 5).tolist() == [1, 1, 1, 1, 1]
+    assert paper.algorithm1(P)["products"] == 3
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_paper_layout_matches_algorithm1(seed):
+    """Pass count and |v| trace of Algorithm 1 in exact rationals over M_{P^δ}
+    (oracle/paper.py) equal the kernels' on the P^δ encoding, every variant."""
+    from oracle import paper
+    rng = np.random.default_rng([seed, 808])
+    n = int(rng.integers(2, 40))
+    P = lpgen.random_program(rng, n, int(rng.integers(0, 4 * n)), max_len=4)
+    alg = paper.algorithm1(P)
+    lm = [a for a in range(n) if alg["v"][a]]
+    for cfg in (dict(), dict(smem_bits_cap=64)):
+        prog = lp.Program(P, paper_layout=True, **cfg)
+        for frontier in (False, True):
+            for sched in (("auto", "stream", "lead") if not frontier else ("auto",)):
+                model, iters, ex = prog.least_model(frontier=frontier, popcounts=True,
+                                                    schedule=sched)
+                assert iters == alg["products"], (frontier, sched)
+                assert ex["popcounts"] == alg["trace"], (frontier, sched)
+                assert np.nonzero(lp.unpack_bits(model, n))[0].tolist() == lm
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_paper_layout_matches_algorithm2_3(seed):
+    from oracle import paper
+    rng = np.random.default_rng([seed, 909])
+    P = lpgen.random_normal_program(rng, int(rng.integers(3, 14)), int(rng.integers(3, 30)),
+                                    max_len=3, k_max=4)
+    alg = paper.algorithm2_3(P)
+    prog = lp.Program(P, paper_layout=True)
+    ids, passes, _ = prog.stable_models()
+    assert ids.tolist() == alg["accepted"]
+    assert passes == alg["products"]
+    M = prog.stable_matrix()
+    n = P.n_atoms
+    G = len(alg["columns"])
+    dev = np.unpackbits(M.view(np.uint8), axis=1, bitorder="little")[:, :G]
+    for g in range(G):
+        assert dev[:, g].tolist() == [alg["columns"][g][a] for a in range(n)]
