@@ -29,7 +29,7 @@ __all__ = [
     "Rules", "from_lists", "config", "CONFIG_NAMES",
     "gen_c1", "gen_c2", "gen_c3", "gen_c4", "gen_c5",
     "random_program", "random_normal_program", "chain", "layered",
-    "tc_program", "random_digraph",
+    "tc_program", "random_digraph", "paper_profile", "PAPER_TABLES", "PAPER_TC_GRAPHS",
 ]
 
 
@@ -90,6 +90,27 @@ def from_lists(n_atoms: int, rules, meta=None) -> Rules:
 # ----------------------------------------------------------------------------------
 # vectorised helpers
 # ----------------------------------------------------------------------------------
+
+def _distinct_rows_long(rng, count: int, L: int, n: int) -> np.ndarray:
+    """int32[count, L] with distinct entries per row, uniform over [0, n), for bodies too
+    long for whole-row rejection (L^2 >~ n): duplicates are redrawn position by position,
+    then every row is shuffled.  Chunked to bound memory."""
+    out = np.empty((count, L), dtype=np.int32)
+    step = max(1, (1 << 24) // max(L, 1))
+    for c0 in range(0, count, step):
+        c1 = min(count, c0 + step)
+        x = rng.integers(0, n, size=(c1 - c0, L), dtype=np.int64)
+        while True:
+            x.sort(axis=1)
+            dup = np.zeros(x.shape, dtype=bool)
+            dup[:, 1:] = x[:, 1:] == x[:, :-1]
+            k = int(dup.sum())
+            if not k:
+                break
+            x[dup] = rng.integers(0, n, size=k)
+        out[c0:c1] = rng.permuted(x, axis=1)
+    return out
+
 
 def _distinct_rows(rng, count: int, L: int, lo, hi, forbid=None) -> np.ndarray:
     """int32[count, L], row entries distinct, uniform in [lo, hi) (lo/hi scalars or
@@ -355,3 +376,71 @@ def tc_program(V: int, edges) -> Rules:
             body = [eid[(x, z)], pid(z, y)]
             rules.append((pid(x, y), body))
     return from_lists(E + V * V, rules, meta={"family": "tc", "V": V, "E": E})
+
+
+# ----------------------------------------------------------------------------------
+# The paper's own workload shapes (Tables 1-6) -- synthetic stand-ins
+# ----------------------------------------------------------------------------------
+
+# (n, m) of Tables 2, 3, 5 and 6: the same twelve shapes in each
+PAPER_TABLES = [(1000, 5000), (1000, 10000), (1600, 24000), (1600, 30000), (2000, 36000),
+                (2000, 40000), (10000, 120000), (10000, 160000), (16000, 200000),
+                (16000, 220000), (20000, 280000), (20000, 320000)]
+
+# Table 4: KONECT graphs (|V|, |E|); the graphs themselves are not in
+# the container -- seeded random digraphs of the same sizes stand in for them
+PAPER_TC_GRAPHS = [("club membership", 65, 95), ("cattle", 28, 217), ("windsurfers", 43, 336),
+                   ("contiguous usa", 49, 107), ("dolphins", 62, 159), ("train bombing", 64, 243),
+                   ("highschool", 70, 366), ("les miserables", 77, 254)]
+
+# Table 1: share of the non-fact rules by body length 1..8
+_TABLE1 = [0.04, 0.04, 0.10, 0.40, 0.35, 0.04, 0.02, 0.01]
+
+
+def paper_profile(n: int, m: int, seed: int = 1, dense: bool = False, k_neg: int = 0) -> Rules:
+    """A random program of the paper's generator shape (reading in
+    DESIGN.md "Input recipe"): m rules over n atoms; n//4 facts on distinct atoms (Table
+    1: "< n/3"), the other m - n//4 rules with body lengths 1..8 in Table 1's
+    proportions, heads uniform, body atoms distinct uniform.  dense=True keeps the facts
+    and the length-1/2 shares and gives the other rules bodies of about 5% of n (uniform
+    in [0.04 n, 0.06 n]; "sparsity ≈ 0.95").  k_neg > 0 turns k_neg body literal
+    occurrences, chosen uniformly, into negations ("randomly changing k (4 <= k <= 8)
+    literals to negations")."""
+    rng = np.random.default_rng([seed, n, m, int(dense), k_neg, 2009])
+    nf = n // 4
+    R = m - nf
+    shares = np.asarray(_TABLE1)
+    counts = np.floor(shares * R).astype(np.int64)
+    counts[3] += R - counts.sum()                      # remainder to the largest bucket
+    lengths = np.repeat(np.arange(1, 9), counts)
+    if dense:
+        lo, hi = max(3, int(0.04 * n)), max(4, int(0.06 * n))
+        big = lengths >= 3
+        lengths[big] = rng.integers(lo, hi + 1, size=int(big.sum()))
+    lengths = np.minimum(lengths, n)
+    rng.shuffle(lengths)
+    heads = rng.integers(0, n, size=R)
+    facts = rng.choice(n, size=nf, replace=False)
+    def fill(idx, L):
+        if L * L > n:   # long bodies (dense profile): whole-row rejection would not end
+            return _distinct_rows_long(rng, idx.size, L, n)
+        return _distinct_rows(rng, idx.size, L, 0, n)
+    P = _assemble(n, heads, lengths, fill, rng,
+                  facts=facts, meta={"family": "paper", "n": n, "m": m, "dense": dense, "k_neg": k_neg})
+    if k_neg:
+        neg = np.zeros(P.body_atom.shape[0], dtype=np.uint8)
+        neg[rng.choice(P.body_atom.shape[0], size=min(k_neg, P.body_atom.shape[0]), replace=False)] = 1
+        P.body_neg = neg
+    return P
+
+
+def paper_tc(name: str, seed: int = 1) -> Rules:
+    """Table 4 stand-in: the transitive-closure grounding (tc_program) of a seeded random
+    digraph with the named KONECT graph's |V| and |E|."""
+    for nm, V, E in PAPER_TC_GRAPHS:
+        if nm == name:
+            rng = np.random.default_rng([seed, V, E, 4])
+            P = tc_program(V, random_digraph(rng, V, E))
+            P.meta.update(graph=name)
+            return P
+    raise KeyError(name)

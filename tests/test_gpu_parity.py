@@ -402,3 +402,26 @@ def test_paper_layout_matches_algorithm2_3(seed):
     dev = np.unpackbits(M.view(np.uint8), axis=1, bitorder="little")[:, :G]
     for g in range(G):
         assert dev[:, g].tolist() == [alg["columns"][g][a] for a in range(n)]
+
+
+@pytest.mark.parametrize("which", ["T2", "T3", "T4", "T5", "T6"])
+def test_paper_profile_shapes(which):
+    """The paper's own workload shapes (first row of Tables 2-6; Table 4: 'cattle'),
+    both conventions, against the oracle."""
+    from oracle import paper  # noqa: F401  (pins of the (A) convention live in paper.py)
+    if which == "T4":
+        P = lpgen.paper_tc("cattle")
+    else:
+        P = lpgen.paper_profile(1000, 5000, dense=which in ("T3", "T6"),
+                                k_neg={"T5": 8, "T6": 7}.get(which, 0))
+    if P.is_definite():
+        check_lm(P, schedules=("auto",))
+        progA = lp.Program(P, paper_layout=True)
+        om, _, _ = oracle.lm_stage(P)
+        model, _, _ = progA.least_model()
+        assert (model == oracle.pack_bits(om)).all()
+    else:
+        check_stable(P)
+        o = oracle.stable(P)
+        ids, _, _ = lp.Program(P, paper_layout=True).stable_models()
+        assert ids.tolist() == np.nonzero(o["accepted"])[0].tolist()
