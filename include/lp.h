@@ -106,7 +106,9 @@ typedef struct {
 #define LP_FULL_STREAM 0x4u /* full θ-pass: stream every body position in every pass
                                (default: LEAD passes -- stream the lead atom of each
                                row, verify the survivors -- until a pass queues more
-                               than 1/16 of the rows).  Same results either way.     */
+                               than 1/16 of the rows or verifies more than 1/8 of the
+                               body entries; programs whose bodies average more than
+                               32 atoms start with STREAM passes).  Same results.    */
 #define LP_FULL_LEAD 0x8u   /* full θ-pass: LEAD passes only (never switch)          */
 
 typedef struct {

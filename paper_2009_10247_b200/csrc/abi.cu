@@ -62,6 +62,7 @@ struct lp_program {
     // [20..22] stable per-pass append counters (slot k % 3)
     int32_t *d_scal = nullptr;
     unsigned long long *d_stats = nullptr;  // full θ-pass work statistics (lp_run.stats_out)
+    unsigned long long *d_vent = nullptr;   // [3] entries verified per pass (schedule)
     uint16_t *d_lead16 = nullptr;   // summary-mode key plane (low 16 bits of the lead group)
     uint8_t *d_octet_tag = nullptr;
     int32_t *d_lead32 = nullptr;    // exact mode: flat lead plane
@@ -196,6 +197,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     TRY(dalloc(p, &p->d_scal, 32));
     CK(cudaMemset(p->d_scal, 0, 32 * sizeof(int32_t)));
     TRY(dalloc(p, &p->d_stats, 6));
+    TRY(dalloc(p, &p->d_vent, 3));
     {
         std::vector<uint32_t> fb((size_t)p->nwords, 0u);   // facts of P (Def. 4)
         for (int32_t a : L.facts) fb[(size_t)a >> 5] |= 1u << (a & 31);
@@ -598,6 +600,15 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.dense_div = std::getenv("LP_DENSE_DIV") ? std::max(1, std::atoi(std::getenv("LP_DENSE_DIV"))) : 16;
     q.n_slots = L.n_slots;
     q.cand = p->d_scal + 12;
+    q.vent = p->d_vent;
+    {
+        long long ent = 0;
+        for (const Segment &sg : L.segs) ent += (long long)sg.L * sg.count_pad;
+        q.stream_entries = ent;
+        // bodies this long make a LEAD verification (one sector per body entry, strided)
+        // dearer than streaming: the auto schedule starts with STREAM passes
+        q.auto_stream_first = (L.n_slots > 0 && ent > 32LL * L.n_slots) ? 1 : 0;
+    }
     q.pcnt = p->d_scal + 16;
     unsigned long long *stats_dev = nullptr;
     if (run && run->stats_out) stats_dev = dev ? reinterpret_cast<unsigned long long *>(run->stats_out) : p->d_stats;

@@ -73,6 +73,12 @@ __device__ __forceinline__ void smem_fill(uint32_t *sm, const uint32_t *src, int
     }
 }
 
+// Does the full θ-pass start with LEAD passes (else STREAM passes, which need the atom-id
+// summary of v_0 in summary mode)?
+__device__ __forceinline__ bool starts_lead(const LMParams &p) {
+    return p.pass_mode == 1 || (p.pass_mode == 0 && !p.auto_stream_first);
+}
+
 // Reserve `cnt` consecutive slots of the derivation list for every lane of a FULL warp
 // with one atomic per warp (the list tail is a single hot address).
 __device__ __forceinline__ int32_t warp_reserve(int32_t *tail, int32_t cnt) {
@@ -109,7 +115,7 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
         p.pcnt[0] = p.pcnt[1] = p.pcnt[2] = 0;
     }
     const bool keys = summary_mode && p.lead16;
-    const bool osum = summary_mode && !(keys && p.pass_mode != 2);
+    const bool osum = summary_mode && !(keys && starts_lead(p));
     const int lane = threadIdx.x & 31;
     for (int64_t w0 = gtid - lane; w0 < p.nwords; w0 += gthreads) {
         const int64_t w = w0 + lane;
@@ -164,7 +170,7 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
 __device__ __forceinline__ void lm_zero_summaries(const LMParams &p, bool summary_mode, int64_t gtid,
                                                   int64_t gthreads) {
     if (!summary_mode) return;
-    if (!(p.lead16 && p.pass_mode != 2))
+    if (!(p.lead16 && starts_lead(p)))
         for (int64_t w = gtid; w < p.sm_words; w += gthreads) p.summary[w] = 0u;
 }
 
@@ -319,8 +325,9 @@ __device__ __forceinline__ void fire_exact4(const LMParams &p, const PassCtx &c,
 // FILTER mode streams the L body rows (heads are read only for verified candidates);
 // EXACT mode streams the head row as well.
 template <int L, int U, bool EXACT>
-__device__ __forceinline__ void seg_pass(const LMParams &p, const Segment &sg, const PassCtx &c,
-                                         int32_t gtid, int32_t gthreads) {
+__device__ __forceinline__ int seg_pass(const LMParams &p, const Segment &sg, const PassCtx &c,
+                                        int32_t gtid, int32_t gthreads) {
+    int loads = 0;
     const int32_t nq = (int32_t)(sg.count_pad >> 2);   // slots < 2^31 (checked at load)
     const int32_t slot0 = (int32_t)sg.slot_off;
     const int4 *base = reinterpret_cast<const int4 *>(p.col + sg.col_off);
@@ -340,6 +347,7 @@ __device__ __forceinline__ void seg_pass(const LMParams &p, const Segment &sg, c
         for (int u = 0; u < U; ++u) {
             const int32_t q = q0 + u * gthreads;
             if (q >= nq) break;
+            loads += L + (EXACT ? 1 : 0);
             unsigned fire = 0xFu;
 #pragma unroll
             for (int j = 0; j < L; ++j) fire = test4<EXACT>(v[u][j], fire, c.sm, p.shift);
@@ -349,26 +357,40 @@ __device__ __forceinline__ void seg_pass(const LMParams &p, const Segment &sg, c
             }
         }
     }
+    return loads;
 }
 
+// Bodies longer than 8: positions in chunks of 8 independent loads, and a quad stops
+// loading once its 4 rows are all dead (short-circuit AND; long bodies usually die early).
+// Returns the int4 loads it issued (the bytes this STREAM pass really read).
 template <bool EXACT>
-__device__ void seg_pass_generic(const LMParams &p, const Segment &sg, const PassCtx &c,
-                                 int32_t gtid, int32_t gthreads) {
+__device__ int seg_pass_generic(const LMParams &p, const Segment &sg, const PassCtx &c,
+                                int32_t gtid, int32_t gthreads) {
     const int32_t nq = (int32_t)(sg.count_pad >> 2);
     const int32_t slot0 = (int32_t)sg.slot_off;
     const int4 *base = reinterpret_cast<const int4 *>(p.col + sg.col_off);
     const int4 *hbase = reinterpret_cast<const int4 *>(p.head + sg.slot_off);
+    int loads = 0;
     for (int32_t q = gtid; q < nq; q += gthreads) {
         const int4 hv = EXACT ? ld_stream(hbase + q) : make_int4(0, 0, 0, 0);
+        loads += EXACT ? 1 : 0;
         unsigned fire = 0xFu;
-#pragma unroll 4
-        for (int32_t j = 0; j < sg.L; ++j)
-            fire = test4<EXACT>(ld_stream(base + (int64_t)j * nq + q), fire, c.sm, p.shift);
+        for (int32_t j0 = 0; j0 < sg.L && fire; j0 += 8) {
+            int4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                v[j] = j0 + j < sg.L ? ld_stream(base + (int64_t)(j0 + j) * nq + q) : make_int4(0, 0, 0, 0);
+            loads += min(8, sg.L - j0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j0 + j < sg.L) fire = test4<EXACT>(v[j], fire, c.sm, p.shift);
+        }
         if (fire) {
             if (EXACT) fire_exact4(p, c, hv, fire);
             else enqueue(p, c, slot0 + q * 4, fire);
         }
     }
+    return loads;
 }
 
 // LEAD pass over one segment: stream only body position 0 (the lead atom, chosen at
@@ -495,10 +517,11 @@ __device__ __forceinline__ void flat_lead_exact(const LMParams &p, const PassCtx
 // Segment s starts at the thread after the one that took the last quad of segment s-1,
 // so short segments spread over the whole grid instead of piling onto the lowest ids.
 template <bool EXACT, bool LEAD>
-__device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c, int64_t gtid,
-                                             int64_t gthreads) {
+__device__ __forceinline__ int all_segments(const LMParams &p, const PassCtx &c, int64_t gtid,
+                                            int64_t gthreads) {
     const int32_t gth = (int32_t)gthreads;
     int32_t off = 0;
+    int loads = 0;
     for (int32_t s = 0; s < p.nseg; ++s) {
         const Segment sg = c.segs[s];
         const int32_t gt = (int32_t)gtid >= off ? (int32_t)gtid - off : (int32_t)gtid - off + gth;
@@ -510,17 +533,18 @@ __device__ __forceinline__ void all_segments(const LMParams &p, const PassCtx &c
         }
         // U quads in flight per thread: 4-8 int4 loads (EXACT also streams heads)
         switch (sg.L) {
-            case 1: seg_pass<1, 4, EXACT>(p, sg, c, gt, gthreads); break;
-            case 2: seg_pass<2, 2, EXACT>(p, sg, c, gt, gthreads); break;
-            case 3: seg_pass<3, EXACT ? 2 : 1, EXACT>(p, sg, c, gt, gthreads); break;
-            case 4: seg_pass<4, 1, EXACT>(p, sg, c, gt, gthreads); break;
-            case 5: seg_pass<5, 1, EXACT>(p, sg, c, gt, gthreads); break;
-            case 6: seg_pass<6, 1, EXACT>(p, sg, c, gt, gthreads); break;
-            case 7: seg_pass<7, 1, EXACT>(p, sg, c, gt, gthreads); break;
-            case 8: seg_pass<8, 1, EXACT>(p, sg, c, gt, gthreads); break;
-            default: seg_pass_generic<EXACT>(p, sg, c, gt, gthreads); break;
+            case 1: loads += seg_pass<1, 4, EXACT>(p, sg, c, gt, gthreads); break;
+            case 2: loads += seg_pass<2, 2, EXACT>(p, sg, c, gt, gthreads); break;
+            case 3: loads += seg_pass<3, EXACT ? 2 : 1, EXACT>(p, sg, c, gt, gthreads); break;
+            case 4: loads += seg_pass<4, 1, EXACT>(p, sg, c, gt, gthreads); break;
+            case 5: loads += seg_pass<5, 1, EXACT>(p, sg, c, gt, gthreads); break;
+            case 6: loads += seg_pass<6, 1, EXACT>(p, sg, c, gt, gthreads); break;
+            case 7: loads += seg_pass<7, 1, EXACT>(p, sg, c, gt, gthreads); break;
+            case 8: loads += seg_pass<8, 1, EXACT>(p, sg, c, gt, gthreads); break;
+            default: loads += seg_pass_generic<EXACT>(p, sg, c, gt, gthreads); break;
         }
     }
+    return loads;
 }
 
 // Add derivation-list entries [i0, i1) to a CTA's shared copy of v_k: exact bits
@@ -590,12 +614,13 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         p.cand[0] = 0;
         p.cand[1] = 0;
         p.cand[2] = 0;
+        p.vent[0] = p.vent[1] = p.vent[2] = 0;
         if (p.stats)
             for (int i = 0; i < 6; ++i) p.stats[i] = 0;
     }
     grid.sync();
     if (p.dbg && tid == 0) p.dbg[(2 * gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
-    bool lead_pass = p.pass_mode != 2;
+    bool lead_pass = starts_lead(p);
     bool keys = !EXACT && p.lead16 && lead_pass;         // shared copy is in key space
     bool rebuild = false;                                // key space -> atom-id summary
     const int32_t n0 = __ldcg(p.tail);
@@ -660,6 +685,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         // read before the previous barrier and is first written after the next one
         if (lead) {
             p.cand[(k + 1) % 3] = 0;
+            p.vent[(k + 1) % 3] = 0;
             p.pcnt[(k + 1) % 3] = 0;
         }
         const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, &bmask,
@@ -668,7 +694,13 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         if (!EXACT && keys) octets_lead<4>(p, c, gtid, gthreads);
         else if (EXACT && lead_pass && p.lead32) flat_lead_exact<4>(p, c, gtid, gthreads);
         else if (lead_pass) all_segments<EXACT, true>(p, c, gtid, gthreads);
-        else all_segments<EXACT, false>(p, c, gtid, gthreads);
+        else {
+            int sl = all_segments<EXACT, false>(p, c, gtid, gthreads);   // int4 loads issued
+            if (p.stats) {
+                for (int o = 16; o; o >>= 1) sl += __shfl_xor_sync(0xFFFFFFFFu, sl, o);
+                if ((tid & 31) == 0 && sl) atomicAdd(p.stats + 0, 16ull * (unsigned long long)sl);
+            }
+        }
         if (p.dbg && k < 16 && (tid & 31) == 0) atomicMax(&DBG_STAMP(2), globaltimer());
         // wr still holds v_{k-1}: add the atoms derived in pass k-1 so that it is a superset
         // of v_k before the barrier (nobody reads wr during pass k -- emit_head tests the
@@ -690,22 +722,19 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             int loaded = 0;
             for (int32_t i = tid; i < nc; i += blockDim.x)
                 loaded += verify_slot<EXACT>(p, c, qget(c, i), j0);
-            if (p.stats) {
-                for (int o = 16; o; o >>= 1) loaded += __shfl_xor_sync(0xFFFFFFFFu, loaded, o);
-                if ((tid & 31) == 0 && loaded) atomicAdd(&loaded_cta, (unsigned long long)loaded);
-            }
+            for (int o = 16; o; o >>= 1) loaded += __shfl_xor_sync(0xFFFFFFFFu, loaded, o);
+            if ((tid & 31) == 0 && loaded) atomicAdd(&loaded_cta, (unsigned long long)loaded);
         }
         if (p.dbg && k < 16) {
             if ((tid & 31) == 0) atomicMax(&DBG_STAMP(3), globaltimer());
             __syncthreads();
             if (tid == 0) DBG_STAMP(4) = globaltimer();
         }
-        if (p.stats) {
-            __syncthreads();
-            if (tid == 0 && loaded_cta) {
-                atomicAdd(p.stats + 3, loaded_cta);
-                loaded_cta = 0;
-            }
+        __syncthreads();
+        if (tid == 0 && loaded_cta) {   // body entries the verification loaded (schedule + stats)
+            atomicAdd(p.vent + k % 3, loaded_cta);
+            if (p.stats) atomicAdd(p.stats + 3, loaded_cta);
+            loaded_cta = 0;
         }
         grid.sync();
         if (p.dbg && tid == 0 && k < 16) DBG_STAMP(5) = globaltimer();
@@ -718,8 +747,9 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             // algorithmic bytes of this pass: the planes it streamed, 4 B per body entry
             // and head the verification loaded, the delta list read twice and the truth
             // words it ORs
-            p.stats[0] += (unsigned long long)(lead_pass ? p.lead_bytes : p.stream_bytes) +
-                          4ull * (unsigned long long)queued + 12ull * (unsigned long long)(t - de);
+            // (STREAM passes added the int4 loads they issued themselves, atomically)
+            atomicAdd(p.stats + 0, (unsigned long long)(lead_pass ? p.lead_bytes : 0) +
+                                       4ull * (unsigned long long)queued + 12ull * (unsigned long long)(t - de));
             if (lead_pass) p.stats[1] += 1;
             p.stats[2] += (unsigned long long)queued;
         }
@@ -728,7 +758,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                 *p.iters_out = k + 1;
                 if (t != de) atomicMax(p.status_out, 1);
                 if (p.stats) {
-                    p.stats[0] += 4ull * p.stats[3];
+                    atomicAdd(p.stats + 0, 4ull * p.stats[3]);
                     p.stats[4] = (unsigned long long)(clock64() - clk0);
                     p.stats[5] = globaltimer() - ns0;
                 }
@@ -743,7 +773,12 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             return;
         }
         if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
-        if (lead_pass && p.pass_mode == 0 && (int64_t)queued * p.dense_div > p.n_slots) {
+        // auto schedule: STREAM from the first LEAD pass that queued more than 1/dense_div of
+        // the rows or whose verification loaded more than 1/8 of the entries a STREAM pass
+        // reads (a verified entry costs a 32-byte sector, a streamed one 4 bytes)
+        const unsigned long long vq = __ldcg(p.vent + k % 3);
+        if (lead_pass && p.pass_mode == 0 &&
+            ((int64_t)queued * p.dense_div > p.n_slots || (long long)vq * 8 > p.stream_entries)) {
             lead_pass = false;
             rebuild = keys;
             keys = false;

@@ -91,6 +91,9 @@ struct LMParams {
     int32_t dense_div;
     int64_t n_slots;
     int32_t *cand;             // [3] rows queued per pass (slot k % 3)
+    unsigned long long *vent;  // [3] body entries the verification loaded per pass (k % 3)
+    long long stream_entries;  // body entries (incl. padding) one STREAM pass reads
+    int32_t auto_stream_first; // auto schedule starts with STREAM passes (long bodies)
     int32_t *pcnt;             // [3] atoms appended to the derivation list per pass (slot
                                //     k % 3): read by every CTA after the pass's barrier,
                                //     never written again before the next one

@@ -425,3 +425,19 @@ def test_paper_profile_shapes(which):
         o = oracle.stable(P)
         ids, _, _ = lp.Program(P, paper_layout=True).stable_models()
         assert ids.tolist() == np.nonzero(o["accepted"])[0].tolist()
+
+
+@pytest.mark.parametrize("cfg", [dict(), dict(smem_bits_cap=256)])
+def test_long_bodies_stream_first(cfg):
+    """Bodies averaging > 32 atoms: the auto schedule starts with STREAM passes (in
+    summary mode the atom-id summary of v_0 is built for them); LEAD-only must agree."""
+    rng = np.random.default_rng(11)
+    n = 2500
+    rules = [(int(rng.integers(0, n)), rng.choice(n, size=int(rng.integers(34, 70)), replace=False).tolist())
+             for _ in range(3000)]
+    rules += [(int(rng.integers(0, n)), [int(rng.integers(0, n))]) for _ in range(300)]
+    rules += [(a, []) for a in rng.choice(n, size=2000, replace=False).tolist()]
+    P = lpgen.from_lists(n, rules)
+    prog = check_lm(P, **cfg)
+    _, iters, ex = prog.least_model(schedule="auto", stats=True)
+    assert ex["stats"]["lead_passes"] == 0
