@@ -303,6 +303,30 @@ def main():
                   "h2d_bytes_per_step": Wm * 8, "d2h_bytes_per_step": Wm * 8 + 12,
                   "ms_per_step": e2e_ms, "api": "lp_least_model (host pointers, synchronous)"}
 
+    if not args.no_extras and dist:
+        # ---- strong-scaling extra: ONE C4 least model sharded by head ranges over the
+        # ranks, one all-gather + OR per pass (shard.py) -------------------
+        from paper_2009_10247_b200.shard import head_ranges, least_model_sharded, sub_program
+        lo, hi = head_ranges(P, ws)[rank]
+        sprog_lm = lp.Program(sub_program(P, lo, hi), device=local)
+        sh_t = []
+        for i in range(1 + min(args.steps, 5)):
+            flush_l2()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            m_sh, it_sh, _ = least_model_sharded(P, program=sprog_lm, popcounts=False)
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 1:
+                sh_t.append(e0.elapsed_time(e1))
+        assert it_sh == iters
+        sh_ms = allmax(float(np.mean(sh_t)))
+        out["sharded"] = {"ms_per_step": sh_ms, "value": nnz * iters / (sh_ms / 1e3),
+                          "unit": "nnz*iter/s", "iters": it_sh, "ranks": ws,
+                          "what": "one program, head ranges per rank, all-gather + OR per pass"}
+        sprog_lm.close()
+
     if not args.no_extras:
         # ---- frontier variant on the same workload --------------------------------------
         fms, fkms, fit, _, _ = timed_least_model(True, args.steps, args.warmup)

@@ -128,6 +128,13 @@ typedef struct {
                                 verification, [3] body entries verification loaded,
                                 [4] SM clock cycles and [5] ns the launch took
                                 (%clock64 / %globaltimer of one thread)              */
+    int32_t max_passes;      /* lp_least_model: stop after this many θ-passes even if the
+                                last one derived something (0 = run to the fixpoint);
+                                not an error -- iters_out = passes run.  One pass from a
+                                v0 is one T_P evaluation over this program's rules: the
+                                step of the head-range-sharded multi-GPU loop (shard.py) */
+    int32_t *converged_out;  /* optional (host pointer, host-mode calls only): 1 if the
+                                last pass derived nothing (u = v), else 0            */
     int64_t guess_offset;    /* lp_stable_models with guesses == NULL: guess i of this
                                 call is global guess guess_offset + i of the binary
                                 counting order (a multiple of 64; 0 = from the first).

@@ -583,6 +583,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.pop_cap = pop_cap;
     q.iters_out = dev ? iters_out : p->d_scal + 1;
     q.max_passes = L.n_ext + 2;
+    q.user_cap = (run && run->max_passes > 0) ? run->max_passes : 0;
     q.occ_ptr = p->d_occ_ptr;
     q.occ_slot = p->d_occ_slot;
     q.cnt = p->d_cnt;
@@ -647,9 +648,10 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
         CK(cudaMemcpyAsync(run->stats_out, stats_dev, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     *iters_out = scal[1];
+    if (run && run->converged_out) *run->converged_out = scal[2] == 0 ? 1 : 0;
     if (scal[2] == 2) return set_err(LP_E_CUDA, "internal: candidate queue overflow");
-    if (scal[2] != 0) return set_err(LP_E_NOT_CONVERGED, "pass guard exceeded");
-    return LP_OK;
+    if (scal[2] == 1) return set_err(LP_E_NOT_CONVERGED, "pass guard exceeded");
+    return LP_OK;   // (status 3: stopped at lp_run.max_passes before the fixpoint)
 }
 
 // ------------------------------------------------------------------------------------

@@ -175,11 +175,14 @@ __device__ __forceinline__ void lm_zero_summaries(const LMParams &p, bool summar
 }
 
 // In-kernel epilogue: the model over the original atoms, LSB-first uint64 words.
-__device__ __noinline__ void lm_extract(const LMParams &p, int64_t gtid, int64_t gthreads) {
+// `v` = the buffer the last pass wrote (v_{k+1}: complete after its barrier; at a
+// fixpoint both buffers hold the model, after a capped pass only this one does).
+__device__ __noinline__ void lm_extract(const LMParams &p, int64_t gtid, int64_t gthreads,
+                                        const uint32_t *v_last) {
     const int64_t nw = ((int64_t)p.n_out + 63) >> 6;
     for (int64_t w = gtid; w < nw; w += gthreads) {
-        unsigned long long v = (unsigned long long)__ldcg(p.buf0 + 2 * w) |
-                               ((unsigned long long)__ldcg(p.buf0 + 2 * w + 1) << 32);
+        unsigned long long v = (unsigned long long)__ldcg(v_last + 2 * w) |
+                               ((unsigned long long)__ldcg(v_last + 2 * w + 1) << 32);
         const int64_t lo = w * 64;
         if (lo + 64 > p.n_out) v &= (1ull << (uint32_t)(p.n_out - lo)) - 1ull;
         p.model_out[w] = v;
@@ -753,10 +756,10 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             if (lead_pass) p.stats[1] += 1;
             p.stats[2] += (unsigned long long)queued;
         }
-        if (t == de || k + 1 >= p.max_passes) {  // u = v: fixpoint (or the pass guard)
+        if (t == de || k + 1 >= p.max_passes || k + 1 == p.user_cap) {  // u = v: fixpoint (or a cap)
             if (lead) {
                 *p.iters_out = k + 1;
-                if (t != de) atomicMax(p.status_out, 1);
+                if (t != de) atomicMax(p.status_out, k + 1 == p.user_cap ? 3 : 1);
                 if (p.stats) {
                     atomicAdd(p.stats + 0, 4ull * p.stats[3]);
                     p.stats[4] = (unsigned long long)(clock64() - clk0);
@@ -765,7 +768,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             }
             if (p.dbg && tid == 0) p.dbg[(gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
             lm_zero_summaries(p, !EXACT, gtid, gthreads);
-            lm_extract(p, gtid, gthreads);
+            lm_extract(p, gtid, gthreads, wr);
             if (p.dbg) {
                 __syncthreads();
                 if (tid == 0) p.dbg[(gridDim.x + blockIdx.x) * 8 + 7] = globaltimer();
@@ -1034,11 +1037,11 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
         if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + 5] = globaltimer();
         const int32_t t = de + __ldcg(p.pcnt + k % 3);   // (see lm_full_kernel)
         const bool lead = blockIdx.x == 0 && tid == 0;
-        const bool done = (t == de) || (k + 1 >= p.max_passes);
+        const bool done = (t == de) || (k + 1 >= p.max_passes) || (k + 1 == p.user_cap);
         if (done) {
             if (lead) {
                 *p.iters_out = k + 1;
-                if (t != de) atomicMax(p.status_out, 1);
+                if (t != de) atomicMax(p.status_out, k + 1 == p.user_cap ? 3 : 1);
             }
             // drain the prefetched tiles before the CTA's shared memory is released
             if (!producer)
@@ -1047,7 +1050,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
                     mbar_wait(full + (q % (uint64_t)S), (uint32_t)((q / S) & 1));
                 }
             lm_zero_summaries(p, !EXACT, gtid, gthreads);
-            lm_extract(p, gtid, gthreads);
+            lm_extract(p, gtid, gthreads, wr);
             return;
         }
         if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
@@ -1135,12 +1138,12 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
         grid.sync();
         const int32_t t = qe + __ldcg(p.pcnt + k % 3);   // (a per-level slot, see lm_full_kernel)
         const bool lead = blockIdx.x == 0 && tid == 0;
-        if (t == qe || k + 1 >= p.max_passes) {
+        if (t == qe || k + 1 >= p.max_passes || k + 1 == p.user_cap) {
             if (lead) {
                 *p.iters_out = k + 1;
-                if (t != qe) atomicMax(p.status_out, 1);
+                if (t != qe) atomicMax(p.status_out, k + 1 == p.user_cap ? 3 : 1);
             }
-            lm_extract(p, gtid, gthreads);
+            lm_extract(p, gtid, gthreads, p.buf0);
             return;
         }
         if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;

@@ -65,8 +65,9 @@ struct LMParams {
     int32_t *pops;             // optional [pop_cap]
     int32_t pop_cap;
     int32_t *iters_out;
-    int32_t *status_out;       // 0 ok, 1 not converged
-    int32_t max_passes;
+    int32_t *status_out;       // 0 ok, 1 pass guard hit, 2 queue overflow, 3 stopped at user_cap
+    int32_t max_passes;        // guard (n_ext + 2)
+    int32_t user_cap;          // lp_run.max_passes (0 = to the fixpoint)
     // frontier variant
     const int64_t *occ_ptr;
     const int32_t *occ_slot;

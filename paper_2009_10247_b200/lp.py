@@ -48,7 +48,8 @@ class lp_options(ctypes.Structure):
 class lp_run(ctypes.Structure):
     _fields_ = [("stream", _P), ("flags", ctypes.c_uint32), ("popcounts_out", _P),
                 ("popcounts_cap", ctypes.c_int32), ("stage_out", _P), ("ev_begin", _P),
-                ("ev_end", _P), ("stats_out", _P), ("guess_offset", ctypes.c_int64)]
+                ("ev_end", _P), ("stats_out", _P), ("max_passes", ctypes.c_int32),
+                ("converged_out", _P), ("guess_offset", ctypes.c_int64)]
 
 
 class lp_info_t(ctypes.Structure):
@@ -223,7 +224,8 @@ class Program:
         return lp_negated_atoms(self)
 
     def least_model(self, v0=None, frontier: bool = False, popcounts: bool = False,
-                    stages: bool = False, stream=None, schedule: str = "auto", stats: bool = False):
+                    stages: bool = False, stream=None, schedule: str = "auto", stats: bool = False,
+                    max_passes: int = 0):
         """Host-buffer call.  v0: None, a bool mask [n], or an id list.  Returns
         (model uint64[ceil(n/64)], iters, dict(popcounts=..., stage=...))."""
         n = self.n_atoms
@@ -240,9 +242,11 @@ class Program:
         pops = np.zeros(n + self.info["n_aux"] + 3, dtype=np.int32) if popcounts else None
         stage = np.zeros(max(n, 1), dtype=np.int32) if stages else None
         st = np.zeros(6, dtype=np.uint64) if stats else None
+        conv = ctypes.c_int32(-1)
         iters = lp_least_model(self, v0w, model, frontier=frontier, pops=pops, stage=stage,
-                               stream=stream, schedule=schedule, stats=st)
-        extra = {}
+                               stream=stream, schedule=schedule, stats=st, max_passes=max_passes,
+                               converged=conv)
+        extra = {"converged": bool(conv.value)}
         if stats:
             extra["stats"] = dict(zip(("bytes", "lead_passes", "rows_verified", "entries_verified",
                                        "sm_cycles", "ns"),
@@ -331,13 +335,16 @@ def _run(stream=None, flags=0, pops=None, stage=None, ev_begin=None, ev_end=None
 
 def lp_least_model(p: Program, v0, model_out, frontier=False, pops=None, stage=None, stream=None,
                    device_ptrs=False, iters_out=None, ev_begin=None, ev_end=None, schedule="auto",
-                   stats=None):
+                   stats=None, max_passes=0, converged=None):
     """Marshals lp_least_model.  Host mode (default): numpy buffers, returns iters.
     device_ptrs=True: torch CUDA tensors (v0 int64 words or None, model_out int64
     words, iters_out int32[1], optional pops/stage), asynchronous on ``stream``."""
     flags = (LP_FRONTIER if frontier else 0) | (LP_PTR_DEVICE if device_ptrs else 0)
     flags |= {"auto": 0, "stream": LP_FULL_STREAM, "lead": LP_FULL_LEAD}[schedule]
     run = _run(stream, flags, pops, stage, ev_begin, ev_end, stats)
+    run.max_passes = int(max_passes)
+    if converged is not None and not device_ptrs:
+        run.converged_out = ctypes.addressof(converged)
     if device_ptrs:
         _check(library().lp_least_model(p.handle, _ptr(v0), _ptr(model_out), _ptr(iters_out),
                                          ctypes.byref(run)), "lp_least_model")

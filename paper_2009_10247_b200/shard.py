@@ -8,8 +8,15 @@ with no exchange during the fixpoint; afterwards the accepted masks are all-gath
 (<= G/8 bytes in total) and the pass counts max-reduced (the whole-matrix pass count is the
 maximum over columns).  NCCL on GPUs, gloo in the CPU tests.
 
-The least model of ONE program does not partition without a per-pass exchange (DESIGN.md
-§8); bench.py runs it as replicas (independent programs, weak scaling).
+The least model of ONE program partitions by head ranges with one exchange per pass
+(SURVEY.md §8(e)): rank r owns the atoms [lo_r, hi_r) (64-aligned, balanced by the body
+entries of the rules whose head they are) and loads only those rules.  Pass k: every rank
+evaluates T over its rules from the same v_k (one θ-pass, lp_run.max_passes = 1), the
+full-length results are all-gathered and OR-ed into v_{k+1}; the loop stops after the first
+pass that changed nothing anywhere.  The union of the ranks' passes is one T_P evaluation
+over all of P, so model, pass count and popcount trace equal the single-GPU ones.
+bench.py's main line runs independent replicas (weak scaling); this path is its strong-
+scaling extra.
 
 This module only moves buffers between ranks; every step of the path runs in the CUDA
 kernels behind lp.Program (the `solve` hook exists so the CPU tests can drive the same
@@ -78,3 +85,98 @@ def stable_models_sharded(prog, n_free: int, group=None,
     words = allw.cpu().numpy().view(np.uint64)[: (G + 63) // 64]
     bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:G]
     return np.nonzero(bits)[0].astype(np.int64), int(p.item())
+
+
+def head_ranges(rules, world: int) -> List[Tuple[int, int]]:
+    """Contiguous, 64-aligned atom ranges [lo, hi), one per rank, covering [0, n), balanced
+    by the rule weight (body length + 1) of the heads they contain."""
+    n = int(rules.n_atoms)
+    lens = np.diff(np.asarray(rules.body_ptr, dtype=np.int64)) + 1
+    w = np.bincount(np.asarray(rules.head, dtype=np.int64), weights=lens, minlength=n)[:n]
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    total = cum[-1]
+    bounds = [0]
+    for r in range(1, world):
+        a = int(np.searchsorted(cum, total * r / world))
+        a = min(n, max(bounds[-1], (a + 63) // 64 * 64))
+        bounds.append(a)
+    bounds.append(n)
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def sub_program(rules, lo: int, hi: int):
+    """The rules whose head is in [lo, hi), over the same atoms (lpgen.Rules)."""
+    import lpgen
+    head = np.asarray(rules.head)
+    ptr = np.asarray(rules.body_ptr, dtype=np.int64)
+    keep = np.nonzero((head >= lo) & (head < hi))[0]
+    lens = ptr[keep + 1] - ptr[keep]
+    nptr = np.zeros(keep.size + 1, dtype=np.int64)
+    np.cumsum(lens, out=nptr[1:])
+    idx = (np.repeat(ptr[keep], lens) + np.arange(int(nptr[-1])) - np.repeat(nptr[:-1], lens)).astype(np.int64)
+    atoms = np.asarray(rules.body_atom)[idx].astype(np.int32)
+    return lpgen.Rules(n_atoms=int(rules.n_atoms), head=head[keep].astype(np.int32), body_ptr=nptr,
+                       body_atom=atoms, body_neg=None, meta={"shard": (lo, hi)})
+
+
+def _gpu_one_pass(prog):
+    import torch
+
+    from . import lp
+    it = None
+
+    def one_pass(v):
+        nonlocal it
+        if it is None:
+            it = torch.zeros(1, dtype=torch.int32, device=v.device)
+        out = torch.empty_like(v)
+        lp.lp_least_model(prog, v, out, device_ptrs=True, iters_out=it, max_passes=1,
+                          stream=torch.cuda.current_stream(v.device))
+        return out
+    return one_pass
+
+
+def least_model_sharded(rules, group=None, v0=None, one_pass=None, device=None, program=None,
+                        popcounts: bool = True):
+    """Head-range-sharded least model of a definite program (module docstring).
+
+    Every rank passes the whole program (it keeps only its rules); ``v0`` optional start
+    set (bool mask over the atoms).  Returns (model words uint64[ceil(n/64)], iters,
+    popcount trace) on every rank.  ``one_pass(v: int64 tensor of model words) -> int64
+    tensor`` defaults to one θ-pass of the CUDA kernels over this rank's rules."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n = int(rules.n_atoms)
+    W = max((n + 63) // 64, 1)
+    lo, hi = head_ranges(rules, world)[rank]
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    if one_pass is None:
+        from . import lp
+        prog = program or lp.Program(sub_program(rules, lo, hi), device=torch.cuda.current_device())
+        one_pass = _gpu_one_pass(prog)
+    # I_0 = v0 ∪ facts(P): the facts of every rank's rules
+    ptr = np.asarray(rules.body_ptr)
+    start = np.zeros(W * 64, dtype=np.uint8)
+    start[np.asarray(rules.head)[ptr[1:] == ptr[:-1]]] = 1
+    if v0 is not None:
+        start[:n] |= np.asarray(v0, dtype=bool).astype(np.uint8)
+    v = torch.from_numpy(np.packbits(start, bitorder="little").view(np.int64).copy()).to(device)
+    buf = torch.empty(world * W, dtype=torch.int64, device=device)
+    pops = [int(start.sum())]
+    iters = 0
+    while True:
+        mine = one_pass(v)
+        dist.all_gather_into_tensor(buf, mine, group=group)
+        nxt = buf.view(world, W)[0].clone()
+        for r in range(1, world):
+            nxt.bitwise_or_(buf.view(world, W)[r])
+        iters += 1
+        if torch.equal(nxt, v):
+            break
+        v = nxt
+        if popcounts:
+            pops.append(int(np.unpackbits(v.cpu().numpy().view(np.uint8)).sum()))
+    return v.cpu().numpy().view(np.uint64)[: (n + 63) // 64].copy(), iters, pops

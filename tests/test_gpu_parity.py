@@ -441,3 +441,57 @@ def test_long_bodies_stream_first(cfg):
     prog = check_lm(P, **cfg)
     _, iters, ex = prog.least_model(schedule="auto", stats=True)
     assert ex["stats"]["lead_passes"] == 0
+
+
+def test_max_passes_cap():
+    """lp_run.max_passes stops after that many θ-passes without an error: on a chain the
+    model after p passes holds the first p + 1 atoms."""
+    P = lpgen.chain(50)
+    prog = lp.Program(P)
+    for frontier in (False, True):
+        for p_ in (1, 2, 7, 49, 50, 60):
+            model, iters, ex = prog.least_model(frontier=frontier, max_passes=p_)
+            assert iters == min(p_, 50)
+            assert ex["converged"] == (p_ >= 50)
+            bits = lp.unpack_bits(model, 50)
+            assert bits.sum() == min(p_ + 1, 50)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+@pytest.mark.parametrize("cfg", ["rand", "C2"])
+def test_head_range_shards_one_pass_each(world, cfg):
+    """The head-range-sharded least model, its ranks run one after another on this GPU
+    (each pass: every rank's one-θ-pass call from the same v_k, then the OR of the
+    results -- shard.least_model_sharded without the all-gather): same model, pass
+    count and popcounts as the oracle."""
+    import torch
+    from paper_2009_10247_b200.shard import head_ranges, sub_program
+    if cfg == "rand":
+        rng = np.random.default_rng(world)
+        P = lpgen.random_program(rng, 3000, 12000, max_len=5, n_facts=100)
+    else:
+        P = lpgen.config("C2")
+    om, stage, oit = oracle.lm_stage(P)
+    n = P.n_atoms
+    W = (n + 63) // 64
+    progs = [lp.Program(sub_program(P, lo, hi)) for lo, hi in head_ranges(P, world)]
+    ptr = np.asarray(P.body_ptr)
+    start = np.zeros(W * 64, dtype=np.uint8)
+    start[np.asarray(P.head)[ptr[1:] == ptr[:-1]]] = 1
+    v = torch.from_numpy(np.packbits(start, bitorder="little").view(np.int64).copy()).cuda()
+    it_d = torch.zeros(1, dtype=torch.int32, device="cuda")
+    iters, pops = 0, [int(start.sum())]
+    while True:
+        nxt = torch.zeros_like(v)
+        for prog in progs:
+            out = torch.empty_like(v)
+            lp.lp_least_model(prog, v, out, device_ptrs=True, iters_out=it_d, max_passes=1)
+            nxt |= out
+        iters += 1
+        if torch.equal(nxt, v):
+            break
+        v = nxt
+        pops.append(int(np.unpackbits(v.cpu().numpy().view(np.uint8)).sum()))
+    assert iters == oit
+    assert (v.cpu().numpy().view(np.uint64)[:W] == oracle.pack_bits(om)).all()
+    assert pops == oracle.popcounts_from_stage(stage, oit)

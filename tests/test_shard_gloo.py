@@ -1,6 +1,7 @@
 """Multi-process host logic of the multi-GPU path on CPU with gloo:
 guess slicing and the rank-sharded stable-model search (all-gather of accepted masks,
-max-reduce of pass counts).  The per-rank solver here is the CPU oracle standing in for
+max-reduce of pass counts); head ranges and the head-range-sharded least model (one
+all-gather + OR per pass).  The per-rank solver here is the CPU oracle standing in for
 the GPU (test infrastructure; the product's default solver is the CUDA path); the GPU
 side of guess slices is covered by tests/test_gpu_parity.py::test_guess_offset_slices."""
 import os
@@ -12,7 +13,7 @@ import torch.multiprocessing as mp
 
 import lpgen
 import oracle
-from paper_2009_10247_b200.shard import guess_slices
+from paper_2009_10247_b200.shard import guess_slices, head_ranges, sub_program
 
 
 def test_guess_slices_cover_exactly_once():
@@ -87,3 +88,69 @@ def test_sharded_stable_models_gloo(world, seed):
     for _, ids, passes in res:
         assert ids == want
         assert passes == o["passes"]
+
+
+def test_head_ranges_partition_the_rules():
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        n = int(rng.integers(1, 700))
+        P = lpgen.random_program(rng, n, int(rng.integers(0, 4 * n)), max_len=5)
+        for world in (1, 2, 3, 8):
+            rs = head_ranges(P, world)
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            assert all(lo % 64 == 0 or lo == n for lo, _ in rs)
+            subs = [sub_program(P, lo, hi) for lo, hi in rs]
+            assert sum(s.n_rules for s in subs) == P.n_rules
+            for (lo, hi), s in zip(rs, subs):
+                assert ((s.head >= lo) & (s.head < hi)).all()
+
+
+def _oracle_one_pass(sub):
+    """One T_P evaluation of `sub` from the given words (stand-in for the GPU pass)."""
+    import torch
+
+    def one_pass(v):
+        n = sub.n_atoms
+        bits = np.unpackbits(v.numpy().view(np.uint8), bitorder="little")[:n].astype(bool)
+        m, it, _, _ = oracle.lm_jacobi(sub, v0=bits, max_iters=1)
+        return torch.from_numpy(oracle.pack_bits(m).view(np.int64).copy())
+    return one_pass
+
+
+def _lm_worker(rank, world, port, seed, q):
+    import torch.distributed as dist
+    from paper_2009_10247_b200.shard import least_model_sharded
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        rng = np.random.default_rng([seed, 91])
+        n = int(rng.integers(50, 400))
+        P = lpgen.random_program(rng, n, 4 * n, max_len=4, n_facts=n // 10)
+        lo, hi = head_ranges(P, world)[rank]
+        model, iters, pops = least_model_sharded(P, one_pass=_oracle_one_pass(sub_program(P, lo, hi)))
+        q.put((rank, model.tolist(), iters, pops))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,seed", [(2, 1), (3, 2), (2, 3)])
+def test_sharded_least_model_gloo(world, seed):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lm_worker, args=(r, world, port, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng([seed, 91])
+    n = int(rng.integers(50, 400))
+    P = lpgen.random_program(rng, n, 4 * n, max_len=4, n_facts=n // 10)
+    om, stage, oit = oracle.lm_stage(P)
+    for _, model, iters, pops in res:
+        assert np.array_equal(np.asarray(model, dtype=np.uint64), oracle.pack_bits(om))
+        assert iters == oit
+        assert pops == oracle.popcounts_from_stage(stage, oit)
