@@ -83,8 +83,9 @@ struct lp_program {
     int32_t W = 0, Wp = 0;
     int64_t G = 0;
     bool stable_valid = false;
-    uint32_t *d_any = nullptr;
+    uint32_t *d_any = nullptr, *d_gfull = nullptr;
     int32_t any_words = 0, any_shift = 0;
+    bool st_full = false;
     int32_t *d_mark = nullptr;
     unsigned long long *d_acc = nullptr, *d_guess = nullptr;
     size_t acc_words_alloc = 0, guess_words_alloc = 0;
@@ -329,8 +330,11 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
             if (w * 4 <= cap) { p->any_words = (int32_t)w; break; }
         }
         p->any_shift = sh;
-        p->st_smem = (size_t)p->any_words * 4;
+        // + the "true in every guess" bits when the filter is exact and they fit
+        p->st_full = sh == 0 && 2 * (int64_t)p->any_words * 4 <= cap;
+        p->st_smem = (size_t)p->any_words * 4 * (p->st_full ? 2 : 1);
         TRY(dalloc(p, &p->d_any, p->any_words));
+        TRY(dalloc(p, &p->d_gfull, p->any_words));
         TRY(dalloc(p, &p->d_mark, (size_t)L.n_ext));
     }
 
@@ -670,6 +674,14 @@ static STParams st_params(lp_program *p) {
     s.T1 = p->d_T1;
     s.Wp = p->Wp;
     s.any_init = p->d_any;
+    s.gfull = p->d_gfull;
+    s.use_full = p->st_full ? 1 : 0;
+    s.dbg = debug_timing();
+    // the flat lead plane holds extended-atom ids: usable when the any-filter is exact
+    s.lead32 = (p->any_shift == 0) ? p->d_lead32 : nullptr;
+    s.n_slots = L.n_slots;
+    s.W = p->W;
+    s.G = p->G;
     s.any_words = p->any_words;
     s.any_shift = p->any_shift;
     s.order = p->d_order;

@@ -1233,6 +1233,7 @@ cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_
     if ((e = cudaMemsetAsync(p.mark, 0, sizeof(int32_t) * (size_t)p.n_ext, st))) return e;
     if ((e = cudaMemsetAsync(p.tail, 0, sizeof(int32_t), st))) return e;
     if ((e = cudaMemsetAsync(p.pcnt, 0, 3 * sizeof(int32_t), st))) return e;
+    if ((e = cudaMemsetAsync(p.gfull, 0, sizeof(uint32_t) * (size_t)p.any_words, st))) return e;
     if ((e = cudaMemsetAsync(p.status_out, 0, sizeof(int32_t), st))) return e;
     const int64_t total = (1 + (int64_t)nfacts + k) * p.Wp;
     int b = (int)std::min<int64_t>((total + 255) / 256, 8192);
@@ -1250,19 +1251,27 @@ __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int
     const int32_t h = __ldg(p.head + sg.slot_off + i);
     bool changed = false;
     for (int32_t w = 2 * lane; w < p.Wp; w += 64) {
-        ulonglong2 acc = make_ulonglong2(~0ull, ~0ull);
-        for (int32_t j = 0; j < sg.L; ++j) {
-            const int32_t a = __ldg(p.col + sg.col_off + (int64_t)j * sg.count_pad + i);
-            const ulonglong2 r = __ldcg(reinterpret_cast<const ulonglong2 *>(rd + (int64_t)a * p.Wp + w));
-            acc.x &= r.x;
-            acc.y &= r.y;
-            if (!(acc.x | acc.y)) break;
-        }
-        if (!(acc.x | acc.y)) continue;
+        // start from the guesses whose head is still false: nothing to do for this word
+        // pair if there are none (most heads are true in every guess after a few passes),
+        // and the AND over the body stops as soon as no such guess survives
+        // (body rows 4 at a time: 4 independent id loads, then 4 independent row loads)
         const ulonglong2 hv = __ldcg(reinterpret_cast<const ulonglong2 *>(rd + (int64_t)h * p.Wp + w));
-        const unsigned long long nx = acc.x & ~hv.x, ny = acc.y & ~hv.y;
-        if (nx) { atomicOr(wr + (int64_t)h * p.Wp + w, nx); changed = true; }
-        if (ny) { atomicOr(wr + (int64_t)h * p.Wp + w + 1, ny); changed = true; }
+        ulonglong2 acc = make_ulonglong2(~hv.x, ~hv.y);
+        for (int32_t j0 = 0; j0 < sg.L && (acc.x | acc.y); j0 += 4) {
+            int32_t a[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                a[j] = j0 + j < sg.L ? __ldg(p.col + sg.col_off + (int64_t)(j0 + j) * sg.count_pad + i) : -1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (a[j] >= 0) {
+                    const ulonglong2 r = __ldcg(reinterpret_cast<const ulonglong2 *>(rd + (int64_t)a[j] * p.Wp + w));
+                    acc.x &= r.x;
+                    acc.y &= r.y;
+                }
+        }
+        if (acc.x) { atomicOr(wr + (int64_t)h * p.Wp + w, acc.x); changed = true; }
+        if (acc.y) { atomicOr(wr + (int64_t)h * p.Wp + w + 1, acc.y); changed = true; }
     }
     if (__any_sync(0xFFFFFFFFu, changed) && lane == 0) {
         if (atomicExch(p.mark + h, k + 1) != k + 1) {
@@ -1284,42 +1293,138 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const int64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
-    for (int32_t w = tid; w < p.any_words; w += blockDim.x) sm[w] = __ldcg(p.any_init + w);
+    // shared memory: "true in some guess" bits, then (exact filter only) "true in every
+    // guess" bits -- a row whose head is full can change nothing
+    uint32_t *full = sm + p.any_words;
+    const bool use_full = p.use_full;
+    for (int32_t w = tid; w < p.any_words; w += blockDim.x) {
+        sm[w] = __ldcg(p.any_init + w);
+        if (use_full) full[w] = 0u;
+    }
     __syncthreads();
-    int32_t ds = 0, de = 0;
+    int32_t ds = 0, de = 0, ds2 = 0, de2 = 0;   // rows changed in pass k-1 and in pass k-2
     for (int k = 0;; ++k) {
         const unsigned long long *rd = (k & 1) ? p.T1 : p.T0;
         unsigned long long *wr = (k & 1) ? p.T0 : p.T1;
         if (k > 0) {
-            const int64_t tot = (int64_t)(de - ds) * p.Wp;
-            for (int64_t x = gtid; x < tot; x += gthreads) {
-                const int32_t h = __ldcg(p.order + ds + x / p.Wp);
-                const int64_t off = (int64_t)h * p.Wp + x % p.Wp;
-                const unsigned long long v = __ldcg(rd + off);
-                if (v != __ldcg(wr + off)) atomicOr(wr + off, v);
+            // rows changed in pass k-1: copy T_k's words into the other buffer (a warp per
+            // row) and mark the rows that are now true in every guess (global, read by
+            // every CTA one pass later)
+            for (int64_t i = ds + gwarp; i < de; i += nwarps) {
+                const int32_t h = __ldcg(p.order + i);
+                bool all1 = true;
+                for (int32_t w = lane; w < p.Wp; w += 32) {
+                    const int64_t off = (int64_t)h * p.Wp + w;
+                    const unsigned long long v = __ldcg(rd + off);
+                    if (v != __ldcg(wr + off)) atomicOr(wr + off, v);
+                    const unsigned long long valid = valid_word(w, p.W, p.G);
+                    all1 = all1 && ((v & valid) == valid);
+                }
+                if (use_full && __all_sync(0xFFFFFFFFu, all1) && lane == 0)
+                    atomicOr(p.gfull + (h >> 5), 1u << (h & 31));
             }
             for (int64_t i = ds + tid; i < de; i += blockDim.x) {
                 const uint32_t g = (uint32_t)__ldcg(p.order + i) >> p.any_shift;
                 atomicOr(sm + (g >> 5), 1u << (g & 31));
             }
+            if (use_full)   // the full marks made during pass k-1 (rows changed in pass k-2)
+                for (int64_t i = ds2 + tid; i < de2; i += blockDim.x) {
+                    const uint32_t h = (uint32_t)__ldcg(p.order + i);
+                    if ((__ldcg(p.gfull + (h >> 5)) >> (h & 31)) & 1u) atomicOr(full + (h >> 5), 1u << (h & 31));
+                }
             __syncthreads();
         }
         if (blockIdx.x == 0 && tid == 0) p.pcnt[(k + 1) % 3] = 0;   // next pass's counter
+        // candidate scan: a lane tests 4 rows (one 16-byte load per body position, lead
+        // position first -- usually an atom that is true in no guess -- and the heads
+        // against the "full" bits); the warp then processes the candidates one by one.
+        // With the flat lead plane (exact mode) one loop covers every segment.
+        if (p.lead32) {
+            const int64_t nq = p.n_slots >> 2;
+            const int4 *lb = reinterpret_cast<const int4 *>(p.lead32);
+            const int4 *hb = reinterpret_cast<const int4 *>(p.head);
+            for (int64_t q0 = gwarp * 32; q0 < nq; q0 += nwarps * 32) {
+                const int64_t q = q0 + lane;
+                unsigned alive = 0;
+                int sgi = 0;
+                if (q < nq) {
+                    const int4 a = ld_stream(lb + q);
+                    alive = (sm_bit(sm, (uint32_t)a.x) ? 1u : 0u) | (sm_bit(sm, (uint32_t)a.y) ? 2u : 0u) |
+                            (sm_bit(sm, (uint32_t)a.z) ? 4u : 0u) | (sm_bit(sm, (uint32_t)a.w) ? 8u : 0u);
+                    if (alive && use_full) {
+                        const int4 h = ld_stream(hb + q);
+                        alive &= (sm_bit(full, (uint32_t)h.x) ? 0u : 1u) | (sm_bit(full, (uint32_t)h.y) ? 0u : 2u) |
+                                 (sm_bit(full, (uint32_t)h.z) ? 0u : 4u) | (sm_bit(full, (uint32_t)h.w) ? 0u : 8u);
+                    }
+                    if (alive) {   // the quad's segment (quads never straddle segments here)
+                        int lo = 0, hi = p.nseg - 1;
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (__ldg(&p.segs[mid].slot_off) <= q * 4) lo = mid; else hi = mid - 1;
+                        }
+                        sgi = lo;
+                        const int32_t L = __ldg(&p.segs[lo].L);
+                        const int64_t cpq = __ldg(&p.segs[lo].count_pad) >> 2;
+                        const int4 *cb = reinterpret_cast<const int4 *>(p.col + __ldg(&p.segs[lo].col_off)) +
+                                         (q - (__ldg(&p.segs[lo].slot_off) >> 2));
+                        for (int32_t j = 1; j < L && alive; ++j) {
+                            const int4 c = ld_stream(cb + (int64_t)j * cpq);
+                            alive &= (sm_bit(sm, (uint32_t)c.x) ? 1u : 0u) | (sm_bit(sm, (uint32_t)c.y) ? 2u : 0u) |
+                                     (sm_bit(sm, (uint32_t)c.z) ? 4u : 0u) | (sm_bit(sm, (uint32_t)c.w) ? 8u : 0u);
+                        }
+                    }
+                }
+                if (p.dbg && alive) atomicAdd(p.dbg + 2 * (k & 63) + 1, (unsigned long long)__popc(alive));
+                for (int e = 0; e < 4; ++e) {
+                    unsigned m = __ballot_sync(0xFFFFFFFFu, (alive >> e) & 1u);
+                    while (m) {
+                        const int l = __ffs(m) - 1;
+                        m &= m - 1;
+                        const int s = __shfl_sync(0xFFFFFFFFu, sgi, l);
+                        const Segment sg = p.segs[s];
+                        st_row(p, sg, (q0 + l) * 4 + e - sg.slot_off, rd, wr, k, lane, p.pcnt + k % 3, de);
+                    }
+                }
+            }
+        }
         int64_t off = 0;  // rotate each segment's first warp (see all_segments)
-        for (int32_t s = 0; s < p.nseg; ++s) {
+        for (int32_t s = 0; s < (p.lead32 ? 0 : p.nseg); ++s) {
             const Segment sg = p.segs[s];
+            const int64_t nq = sg.count_pad >> 2;
             const int64_t gw = gwarp >= off ? gwarp - off : gwarp - off + nwarps;
-            off = (off + (sg.count_pad + 31) / 32) % nwarps;
-            for (int64_t base = gw * 32; base < sg.count_pad; base += nwarps * 32) {
-                const int64_t i = base + lane;
-                bool cand = i < sg.count_pad;
-                for (int32_t j = 0; j < sg.L && cand; ++j)
-                    cand = sm_bit(sm, (uint32_t)__ldg(p.col + sg.col_off + (int64_t)j * sg.count_pad + i) >> p.any_shift);
-                unsigned m = __ballot_sync(0xFFFFFFFFu, cand);
-                while (m) {
-                    const int e = __ffs(m) - 1;
-                    m &= m - 1;
-                    st_row(p, sg, base + e, rd, wr, k, lane, p.pcnt + k % 3, de);
+            off = (off + (nq + 31) / 32) % nwarps;
+            const int4 *cb = reinterpret_cast<const int4 *>(p.col + sg.col_off);
+            const int4 *hb = reinterpret_cast<const int4 *>(p.head + sg.slot_off);
+            for (int64_t q0 = gw * 32; q0 < nq; q0 += nwarps * 32) {
+                const int64_t q = q0 + lane;
+                unsigned alive = 0;
+                if (q < nq) {
+                    const int4 a = ld_stream(cb + q);
+                    alive = (sm_bit(sm, (uint32_t)a.x >> p.any_shift) ? 1u : 0u) |
+                            (sm_bit(sm, (uint32_t)a.y >> p.any_shift) ? 2u : 0u) |
+                            (sm_bit(sm, (uint32_t)a.z >> p.any_shift) ? 4u : 0u) |
+                            (sm_bit(sm, (uint32_t)a.w >> p.any_shift) ? 8u : 0u);
+                    if (alive && use_full) {
+                        const int4 h = ld_stream(hb + q);
+                        alive &= (sm_bit(full, (uint32_t)h.x) ? 0u : 1u) | (sm_bit(full, (uint32_t)h.y) ? 0u : 2u) |
+                                 (sm_bit(full, (uint32_t)h.z) ? 0u : 4u) | (sm_bit(full, (uint32_t)h.w) ? 0u : 8u);
+                    }
+                    for (int32_t j = 1; j < sg.L && alive; ++j) {
+                        const int4 c = ld_stream(cb + (int64_t)j * nq + q);
+                        alive &= (sm_bit(sm, (uint32_t)c.x >> p.any_shift) ? 1u : 0u) |
+                                 (sm_bit(sm, (uint32_t)c.y >> p.any_shift) ? 2u : 0u) |
+                                 (sm_bit(sm, (uint32_t)c.z >> p.any_shift) ? 4u : 0u) |
+                                 (sm_bit(sm, (uint32_t)c.w >> p.any_shift) ? 8u : 0u);
+                    }
+                }
+                if (p.dbg && alive) atomicAdd(p.dbg + 2 * (k & 63) + 1, (unsigned long long)__popc(alive));
+                for (int e = 0; e < 4; ++e) {
+                    unsigned m = __ballot_sync(0xFFFFFFFFu, (alive >> e) & 1u);
+                    while (m) {
+                        const int l = __ffs(m) - 1;
+                        m &= m - 1;
+                        st_row(p, sg, (q0 + l) * 4 + e, rd, wr, k, lane, p.pcnt + k % 3, de);
+                    }
                 }
             }
         }
@@ -1328,6 +1433,7 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
         // another one, so every CTA reads the same value after the barrier)
         const int32_t t = de + __ldcg(p.pcnt + k % 3);
         const bool lead = blockIdx.x == 0 && tid == 0;
+        if (p.dbg && lead && k < 64) p.dbg[2 * k] = globaltimer();   // profiling hook
         if (t == de) {
             if (lead) { *p.passes_out = k + 1; }
             return;
@@ -1336,6 +1442,8 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
             if (lead) { *p.passes_out = k + 1; atomicMax(p.status_out, 1); }
             return;
         }
+        ds2 = ds;
+        de2 = de;
         ds = de;
         de = t;
     }

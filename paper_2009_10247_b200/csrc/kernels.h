@@ -135,6 +135,13 @@ struct STParams {
     int32_t *order;            // rows changed per pass
     int32_t *tail;
     int32_t *pcnt;             // [3] per-pass append counters (slot k % 3)
+    uint32_t *gfull;           // [any_words] rows true in every guess (use_full only)
+    int32_t use_full;          // exact any-filter with room for the full bits
+    unsigned long long *dbg;   // optional [64][2]: barrier-exit time, candidate rows per pass
+    const int32_t *lead32;     // exact mode: flat lead plane (one scan loop), else NULL
+    int64_t n_slots;
+    int32_t W;                 // guess words in use (the rest of Wp is padding)
+    int64_t G;                 // guesses
     int32_t *mark;             // [n_ext] pass tag of the last push
     int32_t *passes_out;
     int32_t *status_out;
