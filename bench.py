@@ -216,17 +216,22 @@ def main():
                 if sd[5] > 0:
                     mhz.append(1e3 * sd[4] / sd[5])
         dev_clock.extend(mhz)
+        if tot:
+            trial_stats.update(mean_ms=float(np.mean(tot)), median_ms=float(np.median(tot)),
+                               min_ms=float(np.min(tot)), stdev_ms=float(np.std(tot)), trials=len(tot))
         return (float(np.mean(tot)), float(np.mean(ker)), int(iters_d.item()),
                 float(np.mean(byts)) if byts else 0.0, [int(x) for x in stats_d.tolist()])
 
     # ---- main line: full θ-pass fixpoint ---------------------------------------------
     dev_clock = []
+    trial_stats = {}
     clocks = ClockSampler(local)
     timed_least_model(False, 0, args.warmup)            # warm-up
     barrier()
     clocks.start()
     dev_clock.clear()
     ms, kms, iters, alg_bytes, st = timed_least_model(False, args.steps, 0)
+    main_trials = dict(trial_stats)
     barrier()
     clk = clocks.stop()
     # the SM clock each timed launch actually ran at (%clock64 / %globaltimer in-kernel)
@@ -274,7 +279,7 @@ def main():
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "truth_mode": "summary-in-smem" if info["truth_mode"] else "exact-in-smem",
                    "grid": [int(info["grid_blocks"]), int(info["block_threads"])]},
-        "fixpoint_ms": ms_max, "kernel_ms": kms_max,
+        "fixpoint_ms": ms_max, "kernel_ms": kms_max, "trials": main_trials,
         "gpu_launches": launches_per_call * args.steps,
         "roofline": roofline, "clocks": clk,
         "load": {"generate_s": t_gen, "lp_load_s": t_load, "device_bytes": int(info["device_bytes"])},
@@ -387,8 +392,14 @@ def main():
             it_cpu += it1
             reps += 1
         dt = time.perf_counter() - t0
+        cpu_model = ""
+        try:
+            with open("/proc/cpuinfo") as f:
+                cpu_model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+        except OSError:
+            pass
         out["cpu_baseline"] = {"value": nnz * it_cpu / dt, "unit": "nnz*iter/s", "cores": 1,
-                               "kind": "oracle",
+                               "kind": "oracle", "cpu": cpu_model, "host_cores": os.cpu_count(),
                                "sample": f"{reps} whole fixpoint(s) of O-LM Jacobi (oracle/lp_oracle.c, "
                                          f"{it_cpu} T_P passes over all of {args.workload}, {dt:.1f} s, "
                                          f"single thread)"}

@@ -307,6 +307,25 @@ def lp_load(rules, **kw) -> Program:
     return Program(rules, **kw)
 
 
+class _Rules:
+    def __init__(self, n_atoms, head, body_ptr, body_atom, body_neg):
+        self.n_atoms, self.head, self.body_ptr = n_atoms, head, body_ptr
+        self.body_atom, self.body_neg = body_atom, body_neg
+
+
+def load(head, body_ptr, body_atom, body_neg=None, n_atoms=None, **kw) -> Program:
+    """SURVEY §8(b)'s shim: a program from flat rule arrays (lp_rules layout: head[R],
+    body_ptr[R+1], body_atom[nnz], optional body_neg[nnz] with 1 = 'not atom');
+    n_atoms defaults to 1 + the largest atom id."""
+    head = np.ascontiguousarray(head, dtype=np.int32)
+    body_ptr = np.ascontiguousarray(body_ptr, dtype=np.int64)
+    body_atom = np.ascontiguousarray(body_atom, dtype=np.int32)
+    if n_atoms is None:
+        n_atoms = int(max(head.max(initial=-1), body_atom.max(initial=-1))) + 1
+    neg = None if body_neg is None else np.ascontiguousarray(body_neg, dtype=np.uint8)
+    return Program(_Rules(int(n_atoms), head, body_ptr, body_atom, neg), **kw)
+
+
 def lp_info(p: Program) -> dict:
     info = lp_info_t()
     _check(library().lp_info(p.handle, ctypes.byref(info)), "lp_info")

@@ -123,3 +123,12 @@ def test_paper_layout_host_shapes():
         info = _host(P, paper_layout=True).info
         assert info["n_atoms"] == n and info["n_aux"] == m - n
         assert _host(P).info["n_aux"] == 0
+
+
+def test_load_shim_from_flat_arrays():
+    """SURVEY §8(b)'s Python shim: lp.load(head, body_ptr, body_atom, body_neg)."""
+    P = lpgen.config("C1")
+    a = lp.load(P.head, P.body_ptr, P.body_atom, device=-1, allocator="none")
+    b = _host(P)
+    for key in ("n_atoms", "n_rules", "nnz", "n_heads", "max_body", "n_segments"):
+        assert a.info[key] == b.info[key]
