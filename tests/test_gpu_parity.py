@@ -495,3 +495,40 @@ def test_head_range_shards_one_pass_each(world, cfg):
     assert iters == oit
     assert (v.cpu().numpy().view(np.uint64)[:W] == oracle.pack_bits(om)).all()
     assert pops == oracle.popcounts_from_stage(stage, oit)
+
+
+def test_edge_cases_new_controls():
+    """Degenerate programs through every control added to lp_run / lp_load: empty and
+    facts-only programs with the paper layout, pass caps with a start set, the last guess
+    slice, one-rank shards."""
+    from paper_2009_10247_b200.shard import guess_slices, head_ranges, sub_program
+    for P in [lpgen.from_lists(0, []), lpgen.from_lists(3, []), lpgen.from_lists(3, [(1, []), (1, [])]),
+              lpgen.from_lists(4, [(0, []), (0, [1]), (2, [0]), (2, [3])])]:
+        om, _, oit = oracle.lm_stage(P)
+        for kw in (dict(), dict(paper_layout=True)):
+            prog = lp.Program(P, **kw)
+            model, iters, ex = prog.least_model(popcounts=True)
+            assert (model == oracle.pack_bits(om)[:len(model)]).all()
+            if not kw:
+                assert iters == oit
+            m1, it1, ex1 = prog.least_model(max_passes=1, v0=[0] if P.n_atoms else None)
+            assert it1 == 1
+    # capped run from a start set = one T_P evaluation of P ∪ v0-as-facts
+    rng = np.random.default_rng(9)
+    P = lpgen.random_program(rng, 500, 2000, max_len=3, n_facts=10)
+    v0 = rng.choice(500, size=40, replace=False).tolist()
+    om, _, _, _ = oracle.lm_jacobi(P, v0=v0, max_iters=1)
+    m, it, _ = lp.Program(P).least_model(v0=v0, max_passes=1)
+    assert it == 1 and (m == oracle.pack_bits(om)).all()
+    # the last, partial guess slice
+    N = lpgen.random_normal_program(np.random.default_rng(3), 200, 800, max_len=3, k_max=8)
+    o = oracle.stable(N)
+    G = 1 << o["f"]
+    prog = lp.Program(N)
+    off, cnt = guess_slices(G, 3)[-1]
+    if cnt:
+        ids, _, _ = prog.stable_models(guess_offset=off, n_guesses=cnt)
+        assert (ids + off).tolist() == [g for g in np.nonzero(o["accepted"])[0].tolist() if g >= off]
+    # a single rank owns everything
+    (lo, hi), = head_ranges(P, 1)
+    assert (lo, hi) == (0, P.n_atoms) and sub_program(P, lo, hi).n_rules == P.n_rules
