@@ -392,6 +392,10 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         int64_t octets = 0;
         for (const Run &r : runs) octets += r.rows_pad >> 3;
         cap = std::max<int64_t>(cap, 8 * (int64_t)kFullThreads * ((octets + gthreads - 1) / gthreads));
+        // overlapped LEAD passes deal octets / quads over the streaming warps only
+        const int64_t sth = (int64_t)p->lm_blocks * kStreamWarps * 32;
+        cap = std::max<int64_t>(cap, 8 * (int64_t)kStreamWarps * 32 * ((octets + sth - 1) / sth));
+        cap = std::max<int64_t>(cap, 4 * (int64_t)kStreamWarps * 32 * (((L.n_slots >> 2) + sth - 1) / sth));
         if (cap + 8 > (1 << 28)) return set_err(LP_E_NOMEM, "candidate queue too large");
         p->qcap = (int32_t)std::max<int64_t>(cap + 8, 1024);
         TRY(dalloc(p, &p->d_qbuf, (size_t)p->lm_blocks * p->qcap));
@@ -606,6 +610,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.n_slots = L.n_slots;
     q.cand = p->d_scal + 12;
     q.vent = p->d_vent;
+    q.overlap = std::getenv("LP_NO_OVERLAP") ? 0 : 1;
     {
         long long ent = 0;
         for (const Segment &sg : L.segs) ent += (long long)sg.L * sg.count_pad;

@@ -20,6 +20,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef LP_OCT_U
+#define LP_OCT_U 4   // key-plane octets in flight per thread (LEAD passes)
+#endif
+
 namespace lpb {
 
 // ------------------------------------------------------------------------------------
@@ -210,9 +214,11 @@ struct PassCtx {
 // Queue entry i of this CTA: shared memory for the first kSmemQueue entries (no global
 // round trip for the usual few hundred survivors per pass), the global queue after that.
 // (register-streaming kernel only; its PassCtx always has sq)
-__device__ __forceinline__ void qput(const PassCtx &c, int32_t i, int32_t slot) {
+// An entry past both parts is dropped (the caller reports the overflow as status 2);
+// shared-memory entries are always written, so a verifier waiting for one never hangs.
+__device__ __forceinline__ void qput(const LMParams &p, const PassCtx &c, int32_t i, int32_t slot) {
     if (i < kSmemQueue) c.sq[i] = slot;
-    else c.qbuf[i - kSmemQueue] = slot;
+    else if (i - kSmemQueue < p.qcap) c.qbuf[i - kSmemQueue] = slot;
 }
 
 __device__ __forceinline__ int32_t qget(const PassCtx &c, int32_t i) {
@@ -305,13 +311,10 @@ __device__ __forceinline__ int verify_slot(const LMParams &p, const PassCtx &c, 
 __device__ __forceinline__ void enqueue(const LMParams &p, const PassCtx &c, int32_t slot0,
                                         unsigned fire) {
     int32_t pos = atomicAdd(c.qcount, __popc(fire));
-    if (pos + 4 > p.qcap + kSmemQueue) {
-        atomicExch(p.status_out, 2);
-        return;
-    }
+    if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-        if ((fire >> e) & 1u) qput(c, pos++, slot0 + e);
+        if ((fire >> e) & 1u) qput(p, c, pos++, slot0 + e);
 }
 
 // EXACT mode: the shared-memory test is exact, so a passing row fires; its head comes
@@ -469,15 +472,9 @@ __device__ __forceinline__ void octets_lead(const LMParams &p, const PassCtx &c,
             fire &= 0xFFu >> (tag[u] >> 5);                   // trailing padding rows
             if (fire) {
                 int32_t pos = atomicAdd(c.qcount, __popc(fire));
-                if (pos + __popc(fire) > p.qcap + kSmemQueue) {
-                    atomicExch(p.status_out, 2);
-                    continue;
-                }
+                if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
                 const int32_t s0 = q * 8;
-                for (unsigned f = fire; f; f &= f - 1) {
-                    const int32_t slot = s0 + __ffs(f) - 1;
-                    qput(c, pos++, slot);
-                }
+                for (unsigned f = fire; f; f &= f - 1) qput(p, c, pos++, s0 + __ffs(f) - 1);
             }
         }
     }
@@ -599,6 +596,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     __shared__ uint32_t bmask;
     __shared__ Segment ssegs[kMaxSmemSegs];
     __shared__ int32_t squeue[kSmemQueue];
+    __shared__ int32_t streamers_done;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
@@ -655,6 +653,11 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         uint32_t *wr = (k & 1) ? p.buf0 : p.buf1;
 #define DBG_STAMP(i) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + (i)]
         if (p.dbg && tid == 0 && k < 16) DBG_STAMP(0) = globaltimer();
+        if (p.overlap && !EXACT) {   // empty shared queue for this pass (last reader: before the barrier)
+            for (int32_t i = tid; i < kSmemQueue; i += blockDim.x) squeue[i] = -1;
+            if (tid == 0) streamers_done = 0;
+            if (k == 0) __syncthreads();   // (later passes sync after the delta below)
+        }
         if (k > 0) {
             // shared copy: v_{k-1} -> v_k
             if (EXACT && (de - ds) > (p.sm_words >> 2)) {
@@ -694,7 +697,47 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, &bmask,
                         p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, p.pcnt + k % 3, de};
         if (p.dbg && tid == 0 && k < 16) DBG_STAMP(1) = globaltimer();
-        if (!EXACT && keys) octets_lead<4>(p, c, gtid, gthreads);
+        const int j0 = (EXACT && lead_pass) ? 1 : 0;
+        int loaded = 0;
+        // Overlapped LEAD pass: kStreamWarps warps stream, the others verify the shared
+        // queue entries while they appear (an entry is written right after its slot is
+        // reserved; -1 = not yet), so only the tail of the verification is left after
+        // the stream.  Entries past the shared part wait for the epilogue.
+        // (key mode only: with the exact in-smem truth the stream is L2-fast and 4 fewer
+        // streaming warps cost more than the overlap saves -- measured C2 +20 %, C3 +6 %)
+        const bool overlap = p.overlap && !EXACT && keys;
+        if (overlap) {
+            const int warp = tid >> 5;
+            const int64_t sthreads = (int64_t)gridDim.x * (kStreamWarps * 32);
+            if (warp < kStreamWarps) {
+                const int64_t sgtid = (int64_t)blockIdx.x * (kStreamWarps * 32) + tid;
+                octets_lead<LP_OCT_U>(p, c, sgtid, sthreads);
+                __syncwarp();
+                if ((tid & 31) == 0) {
+                    __threadfence_block();
+                    atomicAdd(&streamers_done, 1);
+                }
+            } else {
+                const int vthreads = blockDim.x - kStreamWarps * 32;
+                for (int32_t i = tid - kStreamWarps * 32; i < kSmemQueue; i += vthreads) {
+                    bool have = false;
+                    for (;;) {   // wait until entry i is reserved, or the stream is over
+                        if (i < *(volatile int32_t *)&qcount) { have = true; break; }
+                        if (*(volatile int32_t *)&streamers_done == kStreamWarps) {
+                            __threadfence_block();
+                            have = i < *(volatile int32_t *)&qcount;
+                            break;
+                        }
+                        __nanosleep(64);
+                    }
+                    if (!have) break;
+                    int32_t s;
+                    while ((s = *(volatile int32_t *)&squeue[i]) < 0) __nanosleep(32);
+                    loaded += verify_slot<EXACT>(p, c, s, j0);
+                }
+            }
+        }
+        else if (!EXACT && keys) octets_lead<LP_OCT_U>(p, c, gtid, gthreads);
         else if (EXACT && lead_pass && p.lead32) flat_lead_exact<4>(p, c, gtid, gthreads);
         else if (lead_pass) all_segments<EXACT, true>(p, c, gtid, gthreads);
         else {
@@ -721,9 +764,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                 qcount = 0;
                 if (nc) atomicAdd(p.cand + k % 3, nc);
             }
-            const int j0 = (EXACT && lead_pass) ? 1 : 0;
-            int loaded = 0;
-            for (int32_t i = tid; i < nc; i += blockDim.x)
+            for (int32_t i = (overlap ? min(nc, kSmemQueue) : 0) + tid; i < nc; i += blockDim.x)
                 loaded += verify_slot<EXACT>(p, c, qget(c, i), j0);
             for (int o = 16; o; o >>= 1) loaded += __shfl_xor_sync(0xFFFFFFFFu, loaded, o);
             if ((tid & 31) == 0 && loaded) atomicAdd(&loaded_cta, (unsigned long long)loaded);

@@ -20,6 +20,7 @@ constexpr int kSmemLimit = 232448 - 1024;  // opt-in smem per CTA on sm_100 minu
 constexpr int kMaxTileSegs = 64;
 constexpr int kMaxSmemSegs = 64;       // segment table copied to shared memory up to this size
 constexpr int kSmemQueue = 768;        // candidate queue entries kept in shared memory per CTA
+constexpr int kStreamWarps = 28;       // overlapped LEAD passes: streaming warps (the rest verify)
 
 // A body-length segment cut into TMA tiles of T rows.  A tile stages R = L (+1 when the
 // head row is staged too) rows of T ints each: row j holds body position j of T
@@ -95,6 +96,7 @@ struct LMParams {
     unsigned long long *vent;  // [3] body entries the verification loaded per pass (k % 3)
     long long stream_entries;  // body entries (incl. padding) one STREAM pass reads
     int32_t auto_stream_first; // auto schedule starts with STREAM passes (long bodies)
+    int32_t overlap;           // LEAD passes verify while they stream (warp-specialised)
     int32_t *pcnt;             // [3] atoms appended to the derivation list per pass (slot
                                //     k % 3): read by every CTA after the pass's barrier,
                                //     never written again before the next one

@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblp_b200.so")
+LIB_PATH = os.environ.get("LP_LIB") or os.path.join(_HERE, "liblp_b200.so")   # (LP_LIB: A/B builds)
 
 LP_OK, LP_E_INVALID, LP_E_PARSE, LP_E_SEMANTIC, LP_E_CAP = 0, 1, 2, 3, 4
 LP_E_NOMEM, LP_E_CUDA, LP_E_NOT_CONVERGED, LP_E_NODEVICE = 5, 6, 7, 8

@@ -532,3 +532,22 @@ def test_edge_cases_new_controls():
     # a single rank owns everything
     (lo, hi), = head_ranges(P, 1)
     assert (lo, hi) == (0, P.n_atoms) and sub_program(P, lo, hi).n_rules == P.n_rules
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_overlapped_lead_pass_queue_overflow(seed, monkeypatch):
+    """Key-mode LEAD passes verify while they stream; with one CTA and a coarse summary
+    far more than the 768 shared queue entries survive per pass, so the global part of
+    the queue is used too (verified after the stream).  Overlap on and off agree."""
+    rng = np.random.default_rng([seed, 606])
+    P = lpgen.random_program(rng, 5000, 20000, max_len=4, n_facts=600)
+    om, stage, oit = oracle.lm_stage(P)
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("LP_NO_OVERLAP", env)
+        prog = lp.Program(P, smem_bits_cap=128, grid_blocks=1)
+        assert prog.info["key_shift"] >= 0
+        model, iters, ex = prog.least_model(schedule="lead", stats=True, stages=True)
+        assert iters == oit and (model == oracle.pack_bits(om)).all()
+        assert (ex["stage"] == stage).all()
+        assert ex["stats"]["rows_verified"] > 768 * iters // 2
