@@ -69,7 +69,9 @@ struct lp_program {
     int32_t *d_key_of = nullptr;
     int32_t *d_korder = nullptr;
     int32_t ksm_words = 0, kshift = 0;
-    uint32_t *d_factbits = nullptr;
+    uint32_t *d_factbits = nullptr, *d_init_bits = nullptr;
+    int32_t *d_init_list = nullptr, *d_init_klist = nullptr;
+    int32_t n_init = 0;
     uint64_t lm_runs = 0;
     int32_t *d_facts = nullptr;
     int32_t nfacts = 0;
@@ -203,6 +205,10 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         std::vector<uint32_t> fb((size_t)p->nwords, 0u);   // facts of P (Def. 4)
         for (int32_t a : L.facts) fb[(size_t)a >> 5] |= 1u << (a & 31);
         TRY(upload(p, &p->d_factbits, fb));
+        fb[(size_t)L.top >> 5] |= 1u << (L.top & 31);        // v_0 for v0 == NULL: + ⊤
+        TRY(upload(p, &p->d_init_bits, fb));
+        TRY(upload(p, &p->d_init_list, L.facts));           // its derivation list (ids ascending)
+        p->n_init = (int32_t)L.facts.size();
     }
     const size_t mw = std::max<size_t>(((size_t)L.n_out + 63) / 64, 1);
     TRY(dalloc(p, &p->d_v0, mw));
@@ -297,6 +303,9 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(upload(p, &p->d_lead16, lead16));
         TRY(upload(p, &p->d_octet_tag, tag));
         TRY(upload(p, &p->d_key_of, key));
+        std::vector<int32_t> kl;
+        for (int32_t a : L.facts) kl.push_back(key[(size_t)a]);
+        TRY(upload(p, &p->d_init_klist, kl));
         TRY(dalloc(p, &p->d_korder, (size_t)L.n_ext + 1));
         p->lm_smem = std::max(p->lm_smem, (size_t)kw * 4);
     }
@@ -583,6 +592,10 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.v0 = v0d;
     q.v0_words = (int32_t)(mw * 2);
     q.factbits = p->d_factbits;
+    q.init_bits = p->d_init_bits;
+    q.init_list = p->d_init_list;
+    q.init_klist = p->d_init_klist;
+    q.n_init = p->n_init;
     q.top = L.top;
     unsigned long long *mout = dev ? reinterpret_cast<unsigned long long *>(model_out) : p->d_model;
     q.model_out = mout;

@@ -120,6 +120,27 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
     }
     const bool keys = summary_mode && p.lead16;
     const bool osum = summary_mode && !(keys && starts_lead(p));
+    if (!p.v0 && !osum && p.init_list) {
+        // v0 = facts only: the initial words and list were built at load, so
+        // this is a plain copy -- no per-warp reservations on the list tail
+        const int4 *ib = reinterpret_cast<const int4 *>(p.init_bits);
+        int4 *b0 = reinterpret_cast<int4 *>(p.buf0);
+        int4 *b1 = reinterpret_cast<int4 *>(p.buf1);
+        for (int64_t w = gtid; w < (p.nwords >> 2); w += gthreads) {
+            const int4 v = __ldg(ib + w);
+            b0[w] = v;
+            b1[w] = v;
+        }
+        for (int64_t i = gtid; i < p.n_init; i += gthreads) {
+            p.order[i] = __ldg(p.init_list + i);
+            if (keys) p.korder[i] = __ldg(p.init_klist + i);
+        }
+        if (p.stage)
+            for (int64_t a = gtid; a < p.n_out; a += gthreads)
+                p.stage[a] = ((__ldg(p.init_bits + (a >> 5)) >> (a & 31)) & 1u) ? 0 : -1;
+        if (gtid == 0) *p.tail = p.n_init;
+        return;
+    }
     const int lane = threadIdx.x & 31;
     for (int64_t w0 = gtid - lane; w0 < p.nwords; w0 += gthreads) {
         const int64_t w = w0 + lane;

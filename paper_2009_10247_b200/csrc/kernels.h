@@ -49,6 +49,11 @@ struct LMParams {
     const uint32_t *v0;        // optional user start set, 32-bit view of the ABI words
     int32_t v0_words;          // 32-bit words of v0
     const uint32_t *factbits;  // [nwords] bit vector of the atoms with a fact rule
+    // v0 == NULL: v_0 precomputed at load (facts | ⊤ words, the facts in id order, keys)
+    const uint32_t *init_bits;
+    const int32_t *init_list;
+    const int32_t *init_klist; // (key mode)
+    int32_t n_init;
     int32_t top;               // ⊤
     unsigned long long *model_out;  // [ceil(n/64)] written by the epilogue
     int32_t *tail_next;        // the other-parity run counters, zeroed for the next call
