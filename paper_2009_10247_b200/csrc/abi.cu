@@ -66,6 +66,7 @@ struct lp_program {
     uint16_t *d_lead16 = nullptr;   // summary-mode key plane (low 16 bits of the lead group)
     uint8_t *d_octet_tag = nullptr;
     int32_t *d_lead32 = nullptr;    // exact mode: flat lead plane
+    uint16_t *d_xlead16 = nullptr, *d_xhead16 = nullptr, *d_xtag = nullptr;   // exact 16-bit planes
     int32_t *d_key_of = nullptr;
     int32_t *d_korder = nullptr;
     int32_t ksm_words = 0, kshift = 0;
@@ -157,6 +158,7 @@ static lp_status upload(lp_program *p, T **out, const std::vector<T> &v) {
 // body plane (+ the head plane when exact).  Padding rows included.
 static uint64_t lead_plane_bytes(const lp_program *p) {
     if (p->d_lead16) return 2ull * (uint64_t)p->L.n_slots + (uint64_t)p->L.n_slots / 8;   // key plane + tags
+    if (p->d_xlead16) return 4ull * (uint64_t)p->L.n_slots + (uint64_t)p->L.n_slots / 4;  // 16-bit lead + head + tags
     uint64_t b = 4ull * (uint64_t)p->L.n_slots;
     return p->exact ? 2 * b : b;
 }
@@ -308,6 +310,32 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(upload(p, &p->d_init_klist, kl));
         TRY(dalloc(p, &p->d_korder, (size_t)L.n_ext + 1));
         p->lm_smem = std::max(p->lm_smem, (size_t)kw * 4);
+    }
+
+    // exact mode, ids < 2^21: rows bucketed by (lead >> 16, head >> 16) so a LEAD pass
+    // streams 16-bit lead and head planes + a 16-bit tag per 8-row octet (lead bucket |
+    // head bucket << 5 | trailing padding << 10): 4.25 bytes per row instead of 8
+    // (programs of >= 1 M rows: below that the stream is a few microseconds either way and
+    // 8-row octets leave more threads idle than 4-row quads -- C2 measured 6 % slower)
+    if (p->exact && L.n_ext <= (1 << 21) && L.n_slots >= (1 << 20) &&
+        !(opt && (opt->flags & LP_LOAD_TMA)) && !std::getenv("LP_NO_EXACT16")) {
+        std::vector<Run> xr;
+        bucket_rows_by(&L, [](int32_t lead, int32_t head) { return (lead >> 16) | ((head >> 16) << 5); }, 8, &xr);
+        std::vector<uint16_t> l16((size_t)std::max<int64_t>(L.n_slots, 8), 0), h16(l16.size(), 0);
+        std::vector<uint16_t> tag((size_t)std::max<int64_t>(L.n_slots / 8, 1), 0);
+        for (const Run &r : xr) {
+            const Segment &sg = L.segs[(size_t)r.seg];
+            for (int64_t i = 0; i < r.rows; ++i) {
+                const int64_t slot = r.slot_off + i;
+                l16[(size_t)slot] = (uint16_t)(L.col[(size_t)(sg.col_off + (slot - sg.slot_off))] & 0xFFFF);
+                h16[(size_t)slot] = (uint16_t)(L.head[(size_t)slot] & 0xFFFF);
+            }
+            for (int64_t o = r.slot_off / 8; o < (r.slot_off + r.rows_pad) / 8; ++o) tag[(size_t)o] = (uint16_t)r.bucket;
+            tag[(size_t)((r.slot_off + r.rows_pad) / 8 - 1)] |= (uint16_t)((r.rows_pad - r.rows) << 10);
+        }
+        TRY(upload(p, &p->d_xlead16, l16));
+        TRY(upload(p, &p->d_xhead16, h16));
+        TRY(upload(p, &p->d_xtag, tag));
     }
 
     // the program planes in their final row order
@@ -644,6 +672,9 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.lead16 = (frontier || p->use_tma) ? nullptr : p->d_lead16;
     q.octet_tag = p->d_octet_tag;
     q.lead32 = (frontier || p->use_tma) ? nullptr : p->d_lead32;
+    q.xlead16 = (frontier || p->use_tma) ? nullptr : p->d_xlead16;
+    q.xhead16 = p->d_xhead16;
+    q.xtag = p->d_xtag;
     q.key_of = p->d_key_of;
     q.korder = p->d_korder;
     q.ksm_words = p->ksm_words;

@@ -13,6 +13,7 @@
 //   * AND-rows are bucketed by body length L into position-major segments so a
 //     thread streams 4 rules per int4 load with no row-pointer array.
 #include <algorithm>
+#include <functional>
 #include <cstring>
 #include <limits>
 
@@ -303,6 +304,11 @@ void build_occ_lists(HostLayout *L) {
 // run table lists (segment, bucket, first slot, real rows, padded rows) in slot order.
 void bucket_rows(HostLayout *L, const std::vector<int32_t> &bucket_of_atom, int align,
                  std::vector<Run> *runs) {
+    bucket_rows_by(L, [&](int32_t lead, int32_t) { return bucket_of_atom[(size_t)lead]; }, align, runs);
+}
+
+void bucket_rows_by(HostLayout *L, const std::function<int32_t(int32_t, int32_t)> &bucket_of,
+                    int align, std::vector<Run> *runs) {
     std::vector<Segment> segs;
     std::vector<int32_t> col, head;
     int64_t col_off = 0, slot_off = 0;
@@ -310,13 +316,17 @@ void bucket_rows(HostLayout *L, const std::vector<int32_t> &bucket_of_atom, int 
     // pass 1: sizes
     std::vector<std::vector<int64_t>> counts(L->segs.size());
     int32_t nb = 0;
-    for (int32_t x : bucket_of_atom) nb = std::max(nb, x + 1);
+    for (const Segment &sg : L->segs) {
+        const int32_t *c0 = L->col.data() + sg.col_off;
+        for (int64_t i = 0; i < sg.count_pad; ++i)
+            if (c0[i] != L->bot) nb = std::max(nb, bucket_of(c0[i], L->head[(size_t)(sg.slot_off + i)]) + 1);
+    }
     for (size_t s = 0; s < L->segs.size(); ++s) {
         const Segment &sg = L->segs[s];
         counts[s].assign((size_t)nb, 0);
         const int32_t *c0 = L->col.data() + sg.col_off;
         for (int64_t i = 0; i < sg.count_pad; ++i)
-            if (c0[i] != L->bot) counts[s][(size_t)bucket_of_atom[(size_t)c0[i]]]++;
+            if (c0[i] != L->bot) counts[s][(size_t)bucket_of(c0[i], L->head[(size_t)(sg.slot_off + i)])]++;
         Segment ns = sg;
         ns.count = 0;
         ns.count_pad = 0;
@@ -347,7 +357,7 @@ void bucket_rows(HostLayout *L, const std::vector<int32_t> &bucket_of_atom, int 
         const int32_t *c0 = L->col.data() + sg.col_off;
         for (int64_t i = 0; i < sg.count_pad; ++i) {
             if (c0[i] == L->bot) continue;
-            const int64_t d = next[(size_t)bucket_of_atom[(size_t)c0[i]]]++;
+            const int64_t d = next[(size_t)bucket_of(c0[i], L->head[(size_t)(sg.slot_off + i)])]++;
             for (int32_t j = 0; j < sg.L; ++j)
                 col[(size_t)(ns.col_off + (int64_t)j * ns.count_pad + d)] =
                     L->col[(size_t)(sg.col_off + (int64_t)j * sg.count_pad + i)];

@@ -501,6 +501,48 @@ __device__ __forceinline__ void octets_lead(const LMParams &p, const PassCtx &c,
     }
 }
 
+// LEAD pass in exact mode over the 16-bit planes: 8 rows per 16-byte load of each plane
+// plus the octet's tag; a row is queued when its lead atom is in v_k and its head is not.
+template <int U>
+__device__ __forceinline__ void octets_exact16(const LMParams &p, const PassCtx &c, int64_t gtid,
+                                               int64_t gthreads) {
+    const int32_t no = (int32_t)(p.n_slots >> 3);
+    const int32_t gth = (int32_t)gthreads;
+    const int4 *lb = reinterpret_cast<const int4 *>(p.xlead16);
+    const int4 *hb = reinterpret_cast<const int4 *>(p.xhead16);
+    for (int32_t q0 = (int32_t)gtid; q0 < no; q0 += gth * U) {
+        int4 lv[U], hv[U];
+        uint32_t tag[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t q = q0 + u * gth;
+            lv[u] = q < no ? ld_stream(lb + q) : make_int4(0, 0, 0, 0);
+            hv[u] = q < no ? ld_stream(hb + q) : make_int4(0, 0, 0, 0);
+            tag[u] = q < no ? (uint32_t)__ldg(p.xtag + q) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t q = q0 + u * gth;
+            if (q >= no) break;
+            const uint32_t lhi = (tag[u] & 31u) << 16, hhi = ((tag[u] >> 5) & 31u) << 16;
+            const uint32_t lw[4] = {(uint32_t)lv[u].x, (uint32_t)lv[u].y, (uint32_t)lv[u].z, (uint32_t)lv[u].w};
+            const uint32_t hw[4] = {(uint32_t)hv[u].x, (uint32_t)hv[u].y, (uint32_t)hv[u].z, (uint32_t)hv[u].w};
+            unsigned fire = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                fire |= (unsigned)(sm_bit(c.sm, lhi | (lw[e] & 0xFFFFu)) && !sm_bit(c.sm, hhi | (hw[e] & 0xFFFFu))) << (2 * e);
+                fire |= (unsigned)(sm_bit(c.sm, lhi | (lw[e] >> 16)) && !sm_bit(c.sm, hhi | (hw[e] >> 16))) << (2 * e + 1);
+            }
+            fire &= 0xFFu >> (tag[u] >> 10);                  // trailing padding rows
+            if (fire) {
+                int32_t pos = atomicAdd(c.qcount, __popc(fire));
+                if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
+                for (unsigned f = fire; f; f &= f - 1) qput(p, c, pos++, q * 8 + __ffs(f) - 1);
+            }
+        }
+    }
+}
+
 // LEAD pass in exact mode over the flat lead plane: lead32[slot] = body position 0 of
 // every slot, contiguous across segments like the head plane, so one loop over quads
 // covers the whole program (no per-segment bookkeeping): 4 rows per int4 of each plane,
@@ -759,6 +801,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             }
         }
         else if (!EXACT && keys) octets_lead<LP_OCT_U>(p, c, gtid, gthreads);
+        else if (EXACT && lead_pass && p.xlead16) octets_exact16<4>(p, c, gtid, gthreads);
         else if (EXACT && lead_pass && p.lead32) flat_lead_exact<4>(p, c, gtid, gthreads);
         else if (lead_pass) all_segments<EXACT, true>(p, c, gtid, gthreads);
         else {

@@ -116,6 +116,9 @@ struct LMParams {
     const uint16_t *lead16;    // [n_slots] low 16 bits of the lead atom's key group, or NULL
     const uint8_t *octet_tag;  // [n_slots / 8] bucket (group >> 16, < 32) | padding rows << 5
     const int32_t *lead32;     // exact mode: [n_slots] body position 0 of every slot (flat)
+    const uint16_t *xlead16;   // exact mode, ids < 2^21: low 16 bits of lead / head, and per
+    const uint16_t *xhead16;   //   octet lead bucket | head bucket << 5 | padding << 10
+    const uint16_t *xtag;
     const int32_t *key_of;     // [n_ext] key of every extended atom
     int32_t *korder;           // [n_ext + 1] key of order[i] (written with it)
     int32_t ksm_words;         // words of the key-space summary (shared memory)

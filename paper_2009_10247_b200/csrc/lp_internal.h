@@ -2,6 +2,7 @@
 // (kernels.cu) and the ABI glue (abi.cu).  Not part of the public ABI.
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -73,5 +74,8 @@ lp_status encode(const lp_rules *r, bool build_occ, HostLayout *out, std::string
 void build_occ_lists(HostLayout *L);
 void bucket_rows(HostLayout *L, const std::vector<int32_t> &bucket_of_atom, int align,
                  std::vector<Run> *runs);
+// the same with the bucket a function of (lead atom, head) of a row
+void bucket_rows_by(HostLayout *L, const std::function<int32_t(int32_t, int32_t)> &bucket_of,
+                    int align, std::vector<Run> *runs);
 
 }  // namespace lpb

@@ -551,3 +551,12 @@ def test_overlapped_lead_pass_queue_overflow(seed, monkeypatch):
         assert iters == oit and (model == oracle.pack_bits(om)).all()
         assert (ex["stage"] == stage).all()
         assert ex["stats"]["rows_verified"] > 768 * iters // 2
+
+
+def test_exact16_planes_large_program():
+    """Exact mode with >= 1 M rows streams 16-bit lead/head planes (rows bucketed by the
+    high bits of lead and head); all schedules agree with the oracle."""
+    P = lpgen.layered(200, 1000, 1_200_000, 3, seed=7)
+    prog = check_lm(P)
+    assert prog.info["truth_mode"] == 0
+    assert prog.info["lead_pass_bytes"] < 5 * prog.info["n_rules"]
