@@ -601,6 +601,8 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.nseg = (int32_t)L.segs.size();
     q.n = L.n;
     q.n_out = L.n_out;
+    q.n_ext_atoms = L.n_ext;
+    q.n_order_cap = L.n_ext + 1;
     q.col = p->d_col;
     q.head = p->d_head;
     q.buf0 = p->d_buf0;

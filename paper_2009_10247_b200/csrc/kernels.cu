@@ -20,6 +20,21 @@
 
 namespace cg = cooperative_groups;
 
+// Bounds checks of the derived indices (build with -DLP_CHECKS; tools/checked_build.sh):
+// a failed check prints the site and traps, so the call fails with a CUDA error.
+#ifdef LP_CHECKS
+#include <cstdio>
+#define LP_CHECK(cond)                                                                     \
+    do {                                                                                   \
+        if (!(cond)) {                                                                     \
+            printf("LP_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);            \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define LP_CHECK(cond) do { } while (0)
+#endif
+
 #ifndef LP_OCT_U
 #define LP_OCT_U 4   // key-plane octets in flight per thread (LEAD passes)
 #endif
@@ -161,6 +176,7 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
         for (uint32_t b = orig; b;) {
             const int i = __ffs(b) - 1;
             b &= b - 1;
+            LP_CHECK(pos >= 0 && pos < p.n_order_cap);
             if (keys) p.korder[pos] = __ldg(p.key_of + lo + i);   // the CTAs build their
                                                                 // key summaries from it
             p.order[pos++] = (int32_t)(lo + i);
@@ -272,6 +288,7 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
     if (lane == leader) base = atomicAdd(c.pc, __popc(m));
     base = __shfl_sync(m, base, leader);
     const int32_t pos = c.base + base + __popc(m & ((1u << lane) - 1u));
+    LP_CHECK(pos >= 0 && pos <= p.n_order_cap && h >= 0 && h < p.n_ext_atoms);
     p.order[pos] = h;
     if (p.lead16) p.korder[pos] = __ldg(p.key_of + h);   // once per atom, not per CTA
     if (p.stage && h < p.n_out) p.stage[h] = c.k + 1;
@@ -289,6 +306,7 @@ __device__ __forceinline__ int verify_slot(const LMParams &p, const PassCtx &c, 
         const int mid = (lo + hi + 1) >> 1;
         if (c.segs[mid].slot_off <= slot) lo = mid; else hi = mid - 1;
     }
+    LP_CHECK(slot >= 0 && slot < p.n_slots);
     const int32_t L = c.segs[lo].L;
     const int64_t cp = c.segs[lo].count_pad;
     const int32_t *colp = p.col + c.segs[lo].col_off + (slot - c.segs[lo].slot_off);
@@ -627,6 +645,7 @@ __device__ __forceinline__ void add_to_shared(const LMParams &p, uint32_t *sm, u
         for (int u = 0; u < 4; ++u) {
             if (a[u] == 0xFFFFFFFFu) continue;
             a[u] = EXACT ? a[u] : keys ? (a[u] >> p.kshift) : (a[u] >> p.shift);
+            LP_CHECK((a[u] >> 5) < (uint32_t)(keys ? p.ksm_words : p.sm_words));
         }
         uint32_t m = 0;
 #pragma unroll
@@ -1234,6 +1253,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
                     const uint32_t old = atomicOr(p.buf0 + (h >> 5), bit);
                     if (!(old & bit)) {
                         const int32_t pos = qe + atomicAdd(p.pcnt + k % 3, 1);
+                        LP_CHECK(pos < p.n_order_cap && slot >= 0 && slot < p.n_slots);
                         p.order[pos] = h;
                         if (p.stage && h < p.n_out) p.stage[h] = k + 1;
                     }

@@ -40,6 +40,8 @@ struct LMParams {
     int32_t nseg;
     int32_t n;                 // atoms of the encoded program (originals + P^δ auxiliaries)
     int32_t n_out;             // original atoms: v0, model and stage range
+    int32_t n_ext_atoms;       // extended atoms (bounds checks)
+    int32_t n_order_cap;       // entries of the derivation list (bounds checks)
     const int32_t *col;
     const int32_t *head;
     uint32_t *buf0;            // truth vector v_k (bit a of word a>>5); double buffer
