@@ -98,23 +98,32 @@ __device__ __forceinline__ bool starts_lead(const LMParams &p) {
     return p.pass_mode == 1 || (p.pass_mode == 0 && !p.auto_stream_first);
 }
 
-// Reserve `cnt` consecutive slots of the derivation list for every lane of a FULL warp
-// with one atomic per warp (the list tail is a single hot address).
-__device__ __forceinline__ int32_t warp_reserve(int32_t *tail, int32_t cnt) {
-    const int lane = threadIdx.x & 31;
+// Reserve `cnt` consecutive list slots for every thread of the CTA with ONE atomic (all
+// threads of the block must call it; two barriers).
+__device__ __forceinline__ int32_t block_reserve(int32_t *tail, int32_t cnt) {
+    __shared__ int32_t wsum[33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int32_t incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if (lane >= o) incl += y;
     }
-    const int32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-    int32_t base = 0;
-    if (total) {
-        if (lane == 31) base = atomicAdd(tail, total);
-        base = __shfl_sync(0xFFFFFFFFu, base, 31);
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t run = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            const int32_t t = wsum[i];
+            wsum[i] = run;
+            run += t;
+        }
+        wsum[32] = run ? atomicAdd(tail, run) : 0;
     }
-    return base + incl - cnt;
+    __syncthreads();
+    const int32_t r = wsum[32] + wsum[warp] + incl - cnt;
+    __syncthreads();   // (wsum is reused by the next call)
+    return r;
 }
 
 // In-kernel prologue of every least-model kernel (no separate init launches):
@@ -157,8 +166,10 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
         return;
     }
     const int lane = threadIdx.x & 31;
-    for (int64_t w0 = gtid - lane; w0 < p.nwords; w0 += gthreads) {
-        const int64_t w = w0 + lane;
+    // block-uniform loop: list slots are reserved once per CTA and iteration
+    for (int64_t b0 = gtid - threadIdx.x; b0 < p.nwords; b0 += gthreads) {
+        const int64_t w0 = b0 + (threadIdx.x & ~31);
+        const int64_t w = b0 + threadIdx.x;
         const int64_t lo = w * 32;
         uint32_t orig = 0, bits = 0;
         if (w < p.nwords) {
@@ -172,7 +183,7 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
             p.buf0[w] = bits;
             p.buf1[w] = bits;
         }
-        int32_t pos = warp_reserve(p.tail, __popc(orig));
+        int32_t pos = block_reserve(p.tail, __popc(orig));
         for (uint32_t b = orig; b;) {
             const int i = __ffs(b) - 1;
             b &= b - 1;
