@@ -90,6 +90,9 @@ struct lp_program {
     int32_t any_words = 0, any_shift = 0;
     bool st_full = false;
     int32_t *d_mark = nullptr;
+    int32_t *d_st_ring = nullptr;   // stable: per-pass lists (ring of 3)
+    bool st_dirty_ok = false;   // T holds only the previous call's dirty rows (same Wp)
+    int32_t st_last_Wp = 0;
     unsigned long long *d_acc = nullptr, *d_guess = nullptr;
     size_t acc_words_alloc = 0, guess_words_alloc = 0;
 
@@ -373,6 +376,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(dalloc(p, &p->d_any, p->any_words));
         TRY(dalloc(p, &p->d_gfull, p->any_words));
         TRY(dalloc(p, &p->d_mark, (size_t)L.n_ext));
+        TRY(dalloc(p, &p->d_st_ring, 3 * ((size_t)L.n_ext + 1)));
     }
 
     // TMA tile plan: every segment cut into 16 KB tiles of
@@ -735,7 +739,8 @@ static STParams st_params(lp_program *p) {
     s.G = p->G;
     s.any_words = p->any_words;
     s.any_shift = p->any_shift;
-    s.order = p->d_order;
+    s.order = p->d_st_ring;
+    s.ring_cap = L.n_ext + 1;
     s.tail = p->d_scal + 0;
     s.pcnt = p->d_scal + 20;
     s.mark = p->d_mark;
@@ -783,6 +788,7 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
         TRY(dalloc(p, &p->d_T0, need));
         TRY(dalloc(p, &p->d_T1, need));
         p->T_words_alloc = need;
+        p->st_dirty_ok = false;
     }
     p->W = W;
     p->Wp = Wp;
@@ -816,8 +822,11 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
                           : reinterpret_cast<long long *>(p->d_scal + 4);
     STParams s = st_params(p);
     if (dev) s.passes_out = passes_out;
+    const bool full_clear = !(p->st_dirty_ok && p->st_last_Wp == Wp);
     CK(launch_st_init(s, L.n, L.k, p->d_negated_ext, p->d_free_rank, guesses ? gd : nullptr, W, G,
-                      goff / 64, p->d_facts, p->nfacts, L.top, p->d_any, st));
+                      goff / 64, p->d_facts, p->nfacts, L.top, p->d_any, full_clear, st));
+    p->st_dirty_ok = true;   // (stream order: the next call's clear runs after this one)
+    p->st_last_Wp = Wp;
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
     CK(launch_st_fixpoint(s, p->st_blocks, p->st_smem, st));
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));

@@ -1357,14 +1357,40 @@ __global__ void st_init_kernel(STParams p, int32_t n, int32_t k, const int32_t *
     }
 }
 
+// Zero the matrix rows the previous stable call changed -- exactly the rows with a pass
+// tag in mark[] -- in both buffers; rows it did not change are still zero.  A warp per
+// row, lanes over its words.
+__global__ void st_clear_kernel(STParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t h0 = warp * 32; h0 < p.n_ext; h0 += nwarps * 32) {
+        const int64_t h = h0 + lane;
+        unsigned m = __ballot_sync(0xFFFFFFFFu, h < p.n_ext && __ldg(p.mark + h) != 0);
+        while (m) {
+            const int e = __ffs(m) - 1;
+            m &= m - 1;
+            for (int32_t w = lane; w < p.Wp; w += 32) {
+                p.T0[(h0 + e) * p.Wp + w] = 0ull;
+                p.T1[(h0 + e) * p.Wp + w] = 0ull;
+            }
+        }
+    }
+}
+
 cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_t *negated_ext,
                            const int32_t *free_rank, const unsigned long long *guesses,
                            int32_t W, int64_t G, int64_t woff, const int32_t *facts, int32_t nfacts,
-                           int32_t top, uint32_t *any_bits, cudaStream_t st) {
+                           int32_t top, uint32_t *any_bits, bool full_clear, cudaStream_t st) {
     cudaError_t e;
     const size_t tbytes = (size_t)p.n_ext * p.Wp * sizeof(unsigned long long);
-    if ((e = cudaMemsetAsync(p.T0, 0, tbytes, st))) return e;
-    if ((e = cudaMemsetAsync(p.T1, 0, tbytes, st))) return e;
+    if (full_clear) {   // first call, or a new matrix layout
+        if ((e = cudaMemsetAsync(p.T0, 0, tbytes, st))) return e;
+        if ((e = cudaMemsetAsync(p.T1, 0, tbytes, st))) return e;
+    } else {            // only the rows the previous call changed are not zero
+        st_clear_kernel<<<592, 256, 0, st>>>(p);
+        if ((e = cudaGetLastError())) return e;
+    }
     if ((e = cudaMemsetAsync(any_bits, 0, sizeof(uint32_t) * (size_t)p.any_words, st))) return e;
     if ((e = cudaMemsetAsync(p.mark, 0, sizeof(int32_t) * (size_t)p.n_ext, st))) return e;
     if ((e = cudaMemsetAsync(p.tail, 0, sizeof(int32_t), st))) return e;
@@ -1411,8 +1437,10 @@ __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int
     }
     if (__any_sync(0xFFFFFFFFu, changed) && lane == 0) {
         if (atomicExch(p.mark + h, k + 1) != k + 1) {
-            const int32_t pos = base + atomicAdd(pc, 1);   // this pass's own counter
-            p.order[pos] = h;
+            // this pass's list (ring segment k % 3, its own counter)
+            const int32_t pos = atomicAdd(pc, 1);
+            LP_CHECK(pos < p.ring_cap);
+            p.order[base + pos] = h;   // (mark[h] != 0 afterwards: the next call clears row h)
         }
     }
 }
@@ -1438,7 +1466,9 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
         if (use_full) full[w] = 0u;
     }
     __syncthreads();
-    int32_t ds = 0, de = 0, ds2 = 0, de2 = 0;   // rows changed in pass k-1 and in pass k-2
+    // rows changed in pass k-1 and in pass k-2: counts, their lists in ring segments
+    // (k-1) % 3 and (k-2) % 3 of p.order (pass k appends to segment k % 3)
+    int32_t n1 = 0, n2 = 0;
     for (int k = 0;; ++k) {
         const unsigned long long *rd = (k & 1) ? p.T1 : p.T0;
         unsigned long long *wr = (k & 1) ? p.T0 : p.T1;
@@ -1446,8 +1476,10 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
             // rows changed in pass k-1: copy T_k's words into the other buffer (a warp per
             // row) and mark the rows that are now true in every guess (global, read by
             // every CTA one pass later)
-            for (int64_t i = ds + gwarp; i < de; i += nwarps) {
-                const int32_t h = __ldcg(p.order + i);
+            const int32_t *l1 = p.order + (int64_t)((k + 2) % 3) * p.ring_cap;
+            const int32_t *l2 = p.order + (int64_t)((k + 1) % 3) * p.ring_cap;
+            for (int64_t i = gwarp; i < n1; i += nwarps) {
+                const int32_t h = __ldcg(l1 + i);
                 bool all1 = true;
                 for (int32_t w = lane; w < p.Wp; w += 32) {
                     const int64_t off = (int64_t)h * p.Wp + w;
@@ -1459,13 +1491,13 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
                 if (use_full && __all_sync(0xFFFFFFFFu, all1) && lane == 0)
                     atomicOr(p.gfull + (h >> 5), 1u << (h & 31));
             }
-            for (int64_t i = ds + tid; i < de; i += blockDim.x) {
-                const uint32_t g = (uint32_t)__ldcg(p.order + i) >> p.any_shift;
+            for (int64_t i = tid; i < n1; i += blockDim.x) {
+                const uint32_t g = (uint32_t)__ldcg(l1 + i) >> p.any_shift;
                 atomicOr(sm + (g >> 5), 1u << (g & 31));
             }
             if (use_full)   // the full marks made during pass k-1 (rows changed in pass k-2)
-                for (int64_t i = ds2 + tid; i < de2; i += blockDim.x) {
-                    const uint32_t h = (uint32_t)__ldcg(p.order + i);
+                for (int64_t i = tid; i < n2; i += blockDim.x) {
+                    const uint32_t h = (uint32_t)__ldcg(l2 + i);
                     if ((__ldcg(p.gfull + (h >> 5)) >> (h & 31)) & 1u) atomicOr(full + (h >> 5), 1u << (h & 31));
                 }
             __syncthreads();
@@ -1518,7 +1550,8 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
                         m &= m - 1;
                         const int s = __shfl_sync(0xFFFFFFFFu, sgi, l);
                         const Segment sg = p.segs[s];
-                        st_row(p, sg, (q0 + l) * 4 + e - sg.slot_off, rd, wr, k, lane, p.pcnt + k % 3, de);
+                        st_row(p, sg, (q0 + l) * 4 + e - sg.slot_off, rd, wr, k, lane, p.pcnt + k % 3,
+                               (k % 3) * p.ring_cap);
                     }
                 }
             }
@@ -1559,7 +1592,7 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
                     while (m) {
                         const int l = __ffs(m) - 1;
                         m &= m - 1;
-                        st_row(p, sg, (q0 + l) * 4 + e, rd, wr, k, lane, p.pcnt + k % 3, de);
+                        st_row(p, sg, (q0 + l) * 4 + e, rd, wr, k, lane, p.pcnt + k % 3, (k % 3) * p.ring_cap);
                     }
                 }
             }
@@ -1567,10 +1600,10 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
         grid.sync();
         // rows changed in this pass: its own counter slot (the next pass appends to
         // another one, so every CTA reads the same value after the barrier)
-        const int32_t t = de + __ldcg(p.pcnt + k % 3);
+        const int32_t cnt = __ldcg(p.pcnt + k % 3);
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (p.dbg && lead && k < 64) p.dbg[2 * k] = globaltimer();   // profiling hook
-        if (t == de) {
+        if (cnt == 0) {
             if (lead) { *p.passes_out = k + 1; }
             return;
         }
@@ -1578,10 +1611,8 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
             if (lead) { *p.passes_out = k + 1; atomicMax(p.status_out, 1); }
             return;
         }
-        ds2 = ds;
-        de2 = de;
-        ds = de;
-        de = t;
+        n2 = n1;
+        n1 = cnt;
     }
 }
 

@@ -144,7 +144,8 @@ struct STParams {
     const uint32_t *any_init;  // bit g: some row of atoms [g<<any_shift, (g+1)<<any_shift)
     int32_t any_words;         //        is nonzero in T_0 (a superset filter)
     int32_t any_shift;
-    int32_t *order;            // rows changed per pass
+    int32_t *order;            // [3][ring_cap] rows changed in pass k: segment k % 3
+    int32_t ring_cap;          // n_ext + 1 (a row is listed at most once per pass)
     int32_t *tail;
     int32_t *pcnt;             // [3] per-pass append counters (slot k % 3)
     uint32_t *gfull;           // [any_words] rows true in every guess (use_full only)
@@ -154,7 +155,7 @@ struct STParams {
     int64_t n_slots;
     int32_t W;                 // guess words in use (the rest of Wp is padding)
     int64_t G;                 // guesses
-    int32_t *mark;             // [n_ext] pass tag of the last push
+    int32_t *mark;             // [n_ext] pass tag of the last push (0: row never changed)
     int32_t *passes_out;
     int32_t *status_out;
     int32_t max_passes;
@@ -172,7 +173,7 @@ cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st);
 cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_t *negated_ext,
                            const int32_t *free_rank, const unsigned long long *guesses,
                            int32_t W, int64_t G, int64_t woff, const int32_t *facts, int32_t nfacts,
-                           int32_t top, uint32_t *any_bits, cudaStream_t st);
+                           int32_t top, uint32_t *any_bits, bool full_clear, cudaStream_t st);
 cudaError_t launch_st_fixpoint(const STParams &p, int blocks, size_t smem, cudaStream_t st);
 cudaError_t launch_st_check(const STParams &p, int32_t n, int32_t k, const int32_t *negated,
                             int32_t W, int64_t G, unsigned long long *accepted,

@@ -560,3 +560,19 @@ def test_exact16_planes_large_program():
     prog = check_lm(P)
     assert prog.info["truth_mode"] == 0
     assert prog.info["lead_pass_bytes"] < 5 * prog.info["n_rules"]
+
+
+def test_repeated_stable_calls_reuse_the_matrix():
+    """Consecutive stable searches with the same matrix width clear only the rows the
+    previous call changed; different guess sets, widths and offsets in any order must
+    each give the oracle's accepted guesses and whole fixpoint matrix."""
+    rng = np.random.default_rng(77)
+    P = lpgen.random_normal_program(rng, 400, 1600, max_len=3, k_max=8)
+    prog = lp.Program(P)
+    k = len(oracle.negated_atoms(P))
+    for trial in range(6):
+        G = [130, 130, 64, 130, 200, 130][trial]
+        g = (rng.random((G, k)) < 0.5).astype(np.uint8)
+        check_stable(P, guesses_u8=g, prog=prog)
+        if trial == 2:
+            check_stable(P, prog=prog)                  # all 2^f guesses in between
