@@ -20,7 +20,10 @@ constexpr int kSmemLimit = 232448 - 1024;  // opt-in smem per CTA on sm_100 minu
 constexpr int kMaxTileSegs = 64;
 constexpr int kMaxSmemSegs = 64;       // segment table copied to shared memory up to this size
 constexpr int kSmemQueue = 768;        // candidate queue entries kept in shared memory per CTA
-constexpr int kStreamWarps = 28;       // overlapped LEAD passes: streaming warps (the rest verify)
+#ifndef LP_STREAM_WARPS
+#define LP_STREAM_WARPS 28
+#endif
+constexpr int kStreamWarps = LP_STREAM_WARPS;   // overlapped LEAD passes: streaming warps (the rest verify)
 
 // A body-length segment cut into TMA tiles of T rows.  A tile stages R = L (+1 when the
 // head row is staged too) rows of T ints each: row j holds body position j of T
