@@ -243,8 +243,9 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     p->lm_smem = (size_t)p->sm_words * 4;
 
     // key plane (summary mode, register-streaming kernel): every
-    // extended atom gets a key -- atoms that can become true without v0 (heads of stored
-    // rows, facts, abar, ⊤) consecutive keys, every other atom one key per 256 of its kind
+    // extended atom gets a key -- atoms that can become true without v0 (D2: facts and the
+    // heads of rules whose bodies are heads or facts; abar, ⊤) consecutive keys, every
+    // other atom one key per 256 of its kind
     // -- and the shared copy of v_k in LEAD passes is a summary over keys (bit g = keys
     // g << kshift ..), with a per-bucket "any bit" mask on top.  The rows of every segment are bucketed (stably) by the high bits
     // g >> 16 of their lead atom's group, so a LEAD pass streams only the low 16 bits: one
@@ -253,8 +254,8 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
                            !std::getenv("LP_NO_KEYS");
     std::vector<Run> runs;
     if (want_keys) {
-        std::vector<uint8_t> der((size_t)L.n_ext, 0);
-        for (int64_t s = 0; s < L.n_slots; ++s) der[(size_t)L.head[(size_t)s]] = 1;
+        std::vector<uint8_t> der((size_t)L.n_ext, 0);   // D2 (encode.cpp), abar atoms, ⊤
+        for (int32_t a = 0; a < L.n; ++a) der[(size_t)a] = L.deriv2[(size_t)a];
         for (int32_t a : L.facts) der[(size_t)a] = 1;
         for (int32_t a = L.n; a < L.bot; ++a) der[(size_t)a] = 1;
         der[(size_t)L.bot] = 0;

@@ -162,9 +162,7 @@ static lp_status encode_core(const lp_rules *r, bool build_occ, HostLayout *L, s
     L->n_rules = R;
     L->definite = (k == 0);
 
-    // ---- derivability: an atom that is neither a head nor a fact can only be true if
-    // the caller's v0 says so (abar atoms are set by the guesses, so they count as
-    // derivable).  Used below to choose each row's lead atom.
+    // ---- rules per head (statistics, and the derivability sets below)
     std::vector<int32_t> per_head((size_t)n + 1, 0);
     for (int64_t i = 0; i < R; ++i) per_head[r->head[i]]++;
 
@@ -198,21 +196,44 @@ static lp_status encode_core(const lp_rules *r, bool build_occ, HostLayout *L, s
         }
         int64_t l = pos - start;
         if (l > std::numeric_limits<int32_t>::max()) return fail(err, LP_E_INVALID, "body too long");
-        // lead atom (body position 0, the one the full θ-pass streams first and tests
-        // before anything else is loaded): the first underivable atom if the body has
-        // one, else the input order is kept.  The AND is order-free, so this changes
-        // how many rows need a second look, never a result.
-        for (int64_t q = start; q < pos; ++q) {
-            const int32_t x = ext[q];
-            if (x < n && !per_head[x] && !isfact[x]) {
-                std::swap(ext[start], ext[q]);
-                break;
-            }
-        }
         len[i] = (int32_t)l;
         if ((int32_t)l > maxL) maxL = (int32_t)l;
     }
     L->max_body = maxL;
+
+    // ---- a static over-approximation of the atoms that can become true from the facts
+    // alone: D1 = heads ∪ facts, D2 = facts ∪ {head(r) : body(r) ⊆ D1} (abar atoms count
+    // as true: the guesses set them).  Two unfoldings only -- a layout heuristic, computed
+    // from the program, never from v0: an atom outside D2 is true only if v0 says so.
+    // It picks each row's lead atom here and the fine/coarse key groups at load.
+    L->deriv2.assign((size_t)n, 0);
+    {
+        auto in_d1 = [&](int32_t x) { return x >= n || per_head[(size_t)x] || isfact[(size_t)x]; };
+        int64_t q = 0;
+        for (int64_t i = 0; i < R; ++i) {
+            bool all = true;
+            for (int64_t j = q; j < q + len[i] && all; ++j) all = in_d1(ext[j]);
+            if (all) L->deriv2[(size_t)r->head[i]] = 1;   // (facts: empty body)
+            q += len[i];
+        }
+    }
+    // lead atom (body position 0, the one the full θ-pass streams first and tests before
+    // anything else is loaded): the first body atom outside D2 if there is one, else the
+    // input order is kept.  The AND is order-free, so this changes how many rows need a
+    // second look, never a result.
+    {
+        int64_t q = 0;
+        for (int64_t i = 0; i < R; ++i) {
+            for (int64_t j = q; j < q + len[i]; ++j) {
+                const int32_t x = ext[j];
+                if (x < n && !L->deriv2[(size_t)x]) {
+                    std::swap(ext[q], ext[j]);
+                    break;
+                }
+            }
+            q += len[i];
+        }
+    }
     int64_t n_fact_rules = 0;
     for (int64_t i = 0; i < R; ++i) n_fact_rules += len[i] == 0;
 
