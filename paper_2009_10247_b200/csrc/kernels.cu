@@ -491,42 +491,58 @@ __device__ __forceinline__ void seg_lead(const LMParams &p, const Segment &sg, c
 // trailing padding rows), U octets in flight per thread.  Row i is alive iff summary bit
 // (bucket << 16 | lead16[i]) is set.  Thread t takes octets t, t + gthreads, ...
 template <int U>
+__device__ __forceinline__ void oct_load(const LMParams &p, int32_t q0, int32_t gth, int4 (&v)[U],
+                                         uint32_t (&tag)[U]) {
+    const int32_t no = (int32_t)(p.n_slots >> 3);
+    const int4 *base = reinterpret_cast<const int4 *>(p.lead16);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int32_t q = q0 + u * gth;
+        v[u] = q < no ? ld_stream(base + q) : make_int4(0, 0, 0, 0);
+        tag[u] = q < no ? (uint32_t)__ldg(p.octet_tag + q) : 0u;
+    }
+}
+
+template <int U>
+__device__ __forceinline__ void oct_test(const LMParams &p, const PassCtx &c, int32_t q0, int32_t gth,
+                                         const int4 (&v)[U], const uint32_t (&tag)[U]) {
+    const int32_t no = (int32_t)(p.n_slots >> 3);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int32_t q = q0 + u * gth;
+        if (q >= no) break;
+        const uint32_t b = tag[u] & 31u;
+        if (!((*c.bmask >> b) & 1u)) continue;            // bucket with no true key
+        const uint32_t hi = b << 16;
+        const uint32_t w[4] = {(uint32_t)v[u].x, (uint32_t)v[u].y, (uint32_t)v[u].z, (uint32_t)v[u].w};
+        unsigned fire = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            fire |= (unsigned)sm_bit(c.sm, hi | (w[e] & 0xFFFFu)) << (2 * e);
+            fire |= (unsigned)sm_bit(c.sm, hi | (w[e] >> 16)) << (2 * e + 1);
+        }
+        fire &= 0xFFu >> (tag[u] >> 5);                   // trailing padding rows
+        if (fire) {
+            int32_t pos = atomicAdd(c.qcount, __popc(fire));
+            if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
+            const int32_t s0 = q * 8;
+            for (unsigned f = fire; f; f &= f - 1) qput(p, c, pos++, s0 + __ffs(f) - 1);
+        }
+    }
+}
+
+// (issuing the first loads before the pass-top delta update, so they overlap its
+// latency, measured slower: they compete with the delta's loads and add spills)
+template <int U>
 __device__ __forceinline__ void octets_lead(const LMParams &p, const PassCtx &c, int64_t gtid,
                                             int64_t gthreads) {
     const int32_t no = (int32_t)(p.n_slots >> 3);
     const int32_t gth = (int32_t)gthreads;
-    const int4 *base = reinterpret_cast<const int4 *>(p.lead16);
     for (int32_t q0 = (int32_t)gtid; q0 < no; q0 += gth * U) {
         int4 v[U];
         uint32_t tag[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int32_t q = q0 + u * gth;
-            v[u] = q < no ? ld_stream(base + q) : make_int4(0, 0, 0, 0);
-            tag[u] = q < no ? (uint32_t)__ldg(p.octet_tag + q) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int32_t q = q0 + u * gth;
-            if (q >= no) break;
-            const uint32_t b = tag[u] & 31u;
-            if (!((*c.bmask >> b) & 1u)) continue;            // bucket with no true key
-            const uint32_t hi = b << 16;
-            const uint32_t w[4] = {(uint32_t)v[u].x, (uint32_t)v[u].y, (uint32_t)v[u].z, (uint32_t)v[u].w};
-            unsigned fire = 0;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                fire |= (unsigned)sm_bit(c.sm, hi | (w[e] & 0xFFFFu)) << (2 * e);
-                fire |= (unsigned)sm_bit(c.sm, hi | (w[e] >> 16)) << (2 * e + 1);
-            }
-            fire &= 0xFFu >> (tag[u] >> 5);                   // trailing padding rows
-            if (fire) {
-                int32_t pos = atomicAdd(c.qcount, __popc(fire));
-                if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
-                const int32_t s0 = q * 8;
-                for (unsigned f = fire; f; f &= f - 1) qput(p, c, pos++, s0 + __ffs(f) - 1);
-            }
-        }
+        oct_load<U>(p, q0, gth, v, tag);
+        oct_test<U>(p, c, q0, gth, v, tag);
     }
 }
 
@@ -778,7 +794,9 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             } else {
                 add_to_shared<EXACT>(p, sm, &bmask, ds, de, keys);
             }
+            if (p.dbg && tid == 0 && k >= 3 && k < 16) DBG_STAMP(6) = globaltimer();
             __syncthreads();
+            if (p.dbg && tid == 0 && k >= 3 && k < 16) DBG_STAMP(7) = globaltimer();
         }
         // rows queued in pass k are counted in cand[k % 3]; the slot of pass k+1 was last
         // read before the previous barrier and is first written after the next one

@@ -47,4 +47,6 @@ for k in range(min(it, 16)):
     print(f"pass {k:2d}: stream start {rel(1).min():6.1f}..{rel(1).max():6.1f}  "
           f"stream done med/max {np.median(rel(2)):6.1f}/{rel(2).max():6.1f}  "
           f"verify done med/max {np.median(rel(3)):6.1f}/{rel(3).max():6.1f}  "
-          f"cta done max {rel(4).max():6.1f}  barrier exit {rel(5).min():6.1f}..{rel(5).max():6.1f} us")
+          f"cta done max {rel(4).max():6.1f}  barrier exit {rel(5).min():6.1f}..{rel(5).max():6.1f} us"
+          + (f"  [thread 0's delta share done med/max {np.median(rel(6)):5.1f}/{rel(6).max():5.1f}, sync {np.median(rel(7)):5.1f}/{rel(7).max():5.1f}]"
+             if k >= 3 else ""))
