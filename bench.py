@@ -158,7 +158,7 @@ def main():
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
     dist = None
-    if ws > 1:
+    if ws > 1 or os.environ.get("BENCH_FORCE_DIST"):   # (FORCE: exercise the N>1 code on one GPU)
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
@@ -219,8 +219,9 @@ def main():
         if tot:
             trial_stats.update(mean_ms=float(np.mean(tot)), median_ms=float(np.median(tot)),
                                min_ms=float(np.min(tot)), stdev_ms=float(np.std(tot)), trials=len(tot))
-        return (float(np.mean(tot)), float(np.mean(ker)), int(iters_d.item()),
-                float(np.mean(byts)) if byts else 0.0, [int(x) for x in stats_d.tolist()])
+        return (float(np.mean(tot)) if tot else 0.0, float(np.mean(ker)) if ker else 0.0,
+                int(iters_d.item()), float(np.mean(byts)) if byts else 0.0,
+                [int(x) for x in stats_d.tolist()])
 
     # ---- main line: full θ-pass fixpoint ---------------------------------------------
     dev_clock = []
@@ -311,16 +312,15 @@ def main():
     if not args.no_extras and dist:
         # ---- strong-scaling extra: ONE C4 least model sharded by head ranges over the
         # ranks, one all-gather + OR per pass (shard.py) -------------------
-        from paper_2009_10247_b200.shard import head_ranges, least_model_sharded, sub_program
-        lo, hi = head_ranges(P, ws)[rank]
-        sprog_lm = lp.Program(sub_program(P, lo, hi), device=local)
+        from paper_2009_10247_b200.shard import ShardedLeastModel
+        sharded = ShardedLeastModel(P)             # setup: head range, sub-program upload
         sh_t = []
         for i in range(1 + min(args.steps, 5)):
             flush_l2()
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            m_sh, it_sh, _ = least_model_sharded(P, program=sprog_lm, popcounts=False)
+            m_sh, it_sh, _ = sharded.run(popcounts=False)
             e1.record()
             torch.cuda.synchronize()
             if i >= 1:
@@ -330,7 +330,7 @@ def main():
         out["sharded"] = {"ms_per_step": sh_ms, "value": nnz * iters / (sh_ms / 1e3),
                           "unit": "nnz*iter/s", "iters": it_sh, "ranks": ws,
                           "what": "one program, head ranges per rank, all-gather + OR per pass"}
-        sprog_lm.close()
+        del sharded
 
     if not args.no_extras:
         # ---- frontier variant on the same workload --------------------------------------

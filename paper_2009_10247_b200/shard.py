@@ -136,47 +136,71 @@ def _gpu_one_pass(prog):
     return one_pass
 
 
-def least_model_sharded(rules, group=None, v0=None, one_pass=None, device=None, program=None,
-                        popcounts: bool = True):
+class ShardedLeastModel:
     """Head-range-sharded least model of a definite program (module docstring).
 
-    Every rank passes the whole program (it keeps only its rules); ``v0`` optional start
-    set (bool mask over the atoms).  Returns (model words uint64[ceil(n/64)], iters,
-    popcount trace) on every rank.  ``one_pass(v: int64 tensor of model words) -> int64
-    tensor`` defaults to one θ-pass of the CUDA kernels over this rank's rules."""
-    import torch
-    import torch.distributed as dist
+    Setup (once per program, host side): this rank's head range, its sub-program on the
+    GPU and the initial words I_0 = facts(P).  ``run`` is the per-call device loop.
+    ``one_pass(v: int64 tensor of model words) -> int64 tensor`` defaults to one θ-pass
+    of the CUDA kernels over this rank's rules (the CPU tests pass a stand-in)."""
 
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    n = int(rules.n_atoms)
-    W = max((n + 63) // 64, 1)
-    lo, hi = head_ranges(rules, world)[rank]
-    if device is None:
-        device = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
-    if one_pass is None:
-        from . import lp
-        prog = program or lp.Program(sub_program(rules, lo, hi), device=torch.cuda.current_device())
-        one_pass = _gpu_one_pass(prog)
-    # I_0 = v0 ∪ facts(P): the facts of every rank's rules
-    ptr = np.asarray(rules.body_ptr)
-    start = np.zeros(W * 64, dtype=np.uint8)
-    start[np.asarray(rules.head)[ptr[1:] == ptr[:-1]]] = 1
-    if v0 is not None:
-        start[:n] |= np.asarray(v0, dtype=bool).astype(np.uint8)
-    v = torch.from_numpy(np.packbits(start, bitorder="little").view(np.int64).copy()).to(device)
-    buf = torch.empty(world * W, dtype=torch.int64, device=device)
-    pops = [int(start.sum())]
-    iters = 0
-    while True:
-        mine = one_pass(v)
-        dist.all_gather_into_tensor(buf, mine, group=group)
-        nxt = buf.view(world, W)[0].clone()
-        for r in range(1, world):
-            nxt.bitwise_or_(buf.view(world, W)[r])
-        iters += 1
-        if torch.equal(nxt, v):
-            break
-        v = nxt
-        if popcounts:
-            pops.append(int(np.unpackbits(v.cpu().numpy().view(np.uint8)).sum()))
-    return v.cpu().numpy().view(np.uint64)[: (n + 63) // 64].copy(), iters, pops
+    def __init__(self, rules, group=None, one_pass=None, device=None, program=None):
+        import torch
+        import torch.distributed as dist
+
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.n = int(rules.n_atoms)
+        self.W = max((self.n + 63) // 64, 1)
+        self.lo, self.hi = head_ranges(rules, self.world)[self.rank]
+        if device is None:
+            device = (torch.device("cuda", torch.cuda.current_device())
+                      if dist.get_backend(group) == "nccl" else "cpu")
+        self.device = device
+        if one_pass is None:
+            from . import lp
+            prog = program or lp.Program(sub_program(rules, self.lo, self.hi),
+                                         device=torch.cuda.current_device())
+            one_pass = _gpu_one_pass(prog)
+        self.one_pass = one_pass
+        ptr = np.asarray(rules.body_ptr)
+        start = np.zeros(self.W * 64, dtype=np.uint8)        # I_0 = facts of every rank's rules
+        start[np.asarray(rules.head)[ptr[1:] == ptr[:-1]]] = 1
+        self.start = start
+        self.facts_words = torch.from_numpy(np.packbits(start, bitorder="little").view(np.int64).copy()).to(device)
+        self.buf = torch.empty(self.world * self.W, dtype=torch.int64, device=device)
+
+    def run(self, v0=None, popcounts: bool = True):
+        """Returns (model words uint64[ceil(n/64)], iters, popcount trace or [])."""
+        import torch
+        import torch.distributed as dist
+
+        if v0 is None:
+            v = self.facts_words.clone()
+            pops = [int(self.start.sum())] if popcounts else []
+        else:
+            st = self.start.copy()
+            st[:self.n] |= np.asarray(v0, dtype=bool).astype(np.uint8)
+            v = torch.from_numpy(np.packbits(st, bitorder="little").view(np.int64).copy()).to(self.device)
+            pops = [int(st.sum())] if popcounts else []
+        W, world = self.W, self.world
+        iters = 0
+        while True:
+            mine = self.one_pass(v)
+            dist.all_gather_into_tensor(self.buf, mine, group=self.group)
+            nxt = self.buf.view(world, W)[0].clone()
+            for r in range(1, world):
+                nxt.bitwise_or_(self.buf.view(world, W)[r])
+            iters += 1
+            if torch.equal(nxt, v):
+                break
+            v = nxt
+            if popcounts:
+                pops.append(int(np.unpackbits(v.cpu().numpy().view(np.uint8)).sum()))
+        return v.cpu().numpy().view(np.uint64)[: (self.n + 63) // 64].copy(), iters, pops
+
+
+def least_model_sharded(rules, group=None, v0=None, one_pass=None, device=None, program=None,
+                        popcounts: bool = True):
+    """One-shot ShardedLeastModel(...).run(v0): (model words, iters, popcount trace)."""
+    return ShardedLeastModel(rules, group, one_pass, device, program).run(v0, popcounts)
