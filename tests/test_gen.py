@@ -81,3 +81,41 @@ def test_c4_scaled_zipf():
     assert abs(top[0] / 1e6 - 1 / Hn) < 0.01
     assert top[1] < top[0]
     _check_bodies_distinct(P)
+
+
+@pytest.mark.parametrize("dense,k_neg", [(False, 0), (True, 0), (False, 6), (True, 8)])
+def test_paper_profile_shapes(dense, k_neg):
+    """lpgen.paper_profile follows reading R22: n//4 distinct facts, Table 1's body-length
+    shares over the other rules (dense: lengths >= 3 become U[0.04 n, 0.06 n]), distinct
+    body atoms, k_neg negated literal occurrences; deterministic."""
+    n, m = 2000, 36000
+    P = lpgen.paper_profile(n, m, dense=dense, k_neg=k_neg)
+    Q = lpgen.paper_profile(n, m, dense=dense, k_neg=k_neg)
+    assert (P.head == Q.head).all() and (P.body_atom == Q.body_atom).all()
+    assert P.n_atoms == n and P.n_rules == m
+    L = np.diff(P.body_ptr)
+    facts = P.head[L == 0]
+    assert facts.size == n // 4 and np.unique(facts).size == n // 4
+    R = m - n // 4
+    share = {l: (L == l).sum() / R for l in (1, 2)}
+    assert abs(share[1] - 0.04) < 0.002 and abs(share[2] - 0.04) < 0.002
+    if dense:
+        big = L[L >= 3]
+        assert big.min() >= int(0.04 * n) and big.max() <= int(0.06 * n)
+    else:
+        for l, s in zip(range(3, 9), (0.10, 0.40, 0.35, 0.04, 0.02, 0.01)):
+            assert abs((L == l).sum() / R - s) < 0.002, l
+    _check_bodies_distinct(P)
+    if k_neg:
+        assert int(P.body_neg.sum()) == k_neg
+    else:
+        assert P.body_neg is None
+
+
+def test_paper_tc_sizes():
+    for name, V, E in lpgen.PAPER_TC_GRAPHS:
+        P = lpgen.paper_tc(name)
+        facts = int((np.diff(P.body_ptr) == 0).sum())
+        assert facts == E                            # one edge fact per edge
+        assert P.n_atoms == E + V * V
+        assert P.n_rules == 2 * E + E * V            # edges, base paths, recursive paths
