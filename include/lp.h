@@ -82,6 +82,10 @@ typedef void (*lp_free_fn)(void *ptr, size_t bytes, void *ctx);
                                     count the auxiliaries too) follow Algorithms 1-2
                                     literally (convention (A), R4).  Models,
                                     stages, v0 and guesses stay over the original atoms */
+#define LP_LOAD_KEY8 0x8u        /* summary mode: stream 8-bit key codes (1.25 B/row) instead
+                                    of 16-bit ones (2.125 B/row).  On C4 the per-pass plane
+                                    then stays L2-resident: 17% faster, L2/latency-bound
+                                    rather than HBM-bound       */
 #define LP_LOAD_TMA 0x2u         /* use the TMA-pipelined full θ-pass (cp.async.bulk ring)
                                     instead of the register-streaming one; same results,
                                     slower on B200 for HBM-streaming programs */

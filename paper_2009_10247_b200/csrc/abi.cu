@@ -63,8 +63,9 @@ struct lp_program {
     int32_t *d_scal = nullptr;
     unsigned long long *d_stats = nullptr;  // full θ-pass work statistics (lp_run.stats_out)
     unsigned long long *d_vent = nullptr;   // [3] entries verified per pass (schedule)
-    uint16_t *d_lead16 = nullptr;   // summary-mode key plane (low 16 bits of the lead group)
-    uint8_t *d_octet_tag = nullptr;
+    void *d_lead_codes = nullptr;   // summary-mode key plane (low key_bits bits of the lead group)
+    void *d_octet_tag = nullptr;    // per-octet bucket | padding tags
+    int key_bits = 16;
     int32_t *d_lead32 = nullptr;    // exact mode: flat lead plane
     uint16_t *d_xlead16 = nullptr, *d_xhead16 = nullptr, *d_xtag = nullptr;   // exact 16-bit planes
     int32_t *d_key_of = nullptr;
@@ -160,7 +161,9 @@ static lp_status upload(lp_program *p, T **out, const std::vector<T> &v) {
 // the lead plane (+ the head plane when the truth test is exact), a STREAM pass every
 // body plane (+ the head plane when exact).  Padding rows included.
 static uint64_t lead_plane_bytes(const lp_program *p) {
-    if (p->d_lead16) return 2ull * (uint64_t)p->L.n_slots + (uint64_t)p->L.n_slots / 8;   // key plane + tags
+    if (p->d_lead_codes)   // key plane + octet tags
+        return p->key_bits == 8 ? (uint64_t)p->L.n_slots + (uint64_t)p->L.n_slots / 4
+                                : 2ull * (uint64_t)p->L.n_slots + (uint64_t)p->L.n_slots / 8;
     if (p->d_xlead16) return 4ull * (uint64_t)p->L.n_slots + (uint64_t)p->L.n_slots / 4;  // 16-bit lead + head + tags
     uint64_t b = 4ull * (uint64_t)p->L.n_slots;
     return p->exact ? 2 * b : b;
@@ -248,8 +251,10 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     // other atom one key per 256 of its kind
     // -- and the shared copy of v_k in LEAD passes is a summary over keys (bit g = keys
     // g << kshift ..), with a per-bucket "any bit" mask on top.  The rows of every segment are bucketed (stably) by the high bits
-    // g >> 16 of their lead atom's group, so a LEAD pass streams only the low 16 bits: one
-    // uint16 per row, runs of one bucket padded to 8 rows.
+    // g >> kb of their lead atom's group, so a LEAD pass streams only the low kb bits:
+    // kb = 16 (default: a uint16 per row + a uint8 tag per 8-row octet, 2.125 B/row) or
+    // kb = 8 (LP_LOAD_KEY8: a byte per row + a uint16 tag per octet, 1.25 B/row); runs of
+    // one bucket padded to 8 rows.
     const bool want_keys = !p->exact && !(opt && (opt->flags & LP_LOAD_TMA)) &&
                            !std::getenv("LP_NO_KEYS");
     std::vector<Run> runs;
@@ -273,7 +278,9 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         };
         int sh = 0;
         while (words_for(nd, sh) * 4 > kcap) ++sh;
-        const int64_t span = (int64_t)1 << (16 + sh);
+        const int kb = (opt && (opt->flags & LP_LOAD_KEY8)) ? 8 : 16;   // code bits per row
+        p->key_bits = kb;
+        const int64_t span = (int64_t)1 << (kb + sh);   // one bucket = 2^kb groups
         int64_t nd_pad = (nd + span - 1) / span * span;
         if (words_for(nd_pad, sh) * 4 > kcap) nd_pad = nd;
         const int64_t kw = words_for(nd_pad, sh);
@@ -286,28 +293,50 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         }
         p->kshift = sh;
         p->ksm_words = (int32_t)kw;
-        if ((((nkeys - 1) >> sh) >> 16) >= 32) return set_err(LP_E_INVALID, "internal: key bucket >= 32");
+        const int64_t nbuckets = (((nkeys - 1) >> sh) >> kb) + 1;
+        if (nbuckets > (kb == 16 ? 32 : 32 * kBucketWords))
+            return set_err(LP_E_INVALID, "internal: key bucket out of range");
         std::vector<int32_t> bucket((size_t)L.n_ext);
-        for (int32_t a = 0; a < L.n_ext; ++a) bucket[(size_t)a] = (key[(size_t)a] >> sh) >> 16;
+        for (int32_t a = 0; a < L.n_ext; ++a) bucket[(size_t)a] = (key[(size_t)a] >> sh) >> kb;
         bucket_rows(&L, bucket, 8, &runs);
-        std::vector<uint16_t> lead16((size_t)std::max<int64_t>(L.n_slots, 8), 0);
+        const size_t nsl = (size_t)std::max<int64_t>(L.n_slots, 8), noct = (size_t)std::max<int64_t>(L.n_slots / 8, 1);
+        std::vector<uint16_t> code16(kb == 16 ? nsl : 0, 0);
+        std::vector<uint8_t> code8(kb == 8 ? nsl : 0, 0);
+        std::vector<uint8_t> tag8(kb == 16 ? noct : 0, 0);
+        std::vector<uint16_t> tag16(kb == 8 ? noct : 0, 0);
+        const int pshift = kb == 16 ? 5 : 13;
         for (const Run &r : runs) {
             const Segment &sg = L.segs[(size_t)r.seg];
             for (int64_t i = 0; i < r.rows; ++i) {
                 const int64_t slot = r.slot_off + i;
                 const int32_t a = L.col[(size_t)(sg.col_off + (slot - sg.slot_off))];
-                lead16[(size_t)slot] = (uint16_t)((key[(size_t)a] >> sh) & 0xFFFF);
+                const uint32_t g = (uint32_t)(key[(size_t)a] >> sh);
+                if (kb == 16) code16[(size_t)slot] = (uint16_t)(g & 0xFFFF);
+                else code8[(size_t)slot] = (uint8_t)(g & 0xFF);
+            }
+            // one tag per octet: its bucket (all 8 rows share it) and trailing padding
+            const int64_t pad = r.rows_pad - r.rows;
+            for (int64_t o = r.slot_off / 8; o < (r.slot_off + r.rows_pad) / 8; ++o) {
+                const uint32_t t = (uint32_t)r.bucket | ((o == (r.slot_off + r.rows_pad) / 8 - 1) ? (uint32_t)pad << pshift : 0u);
+                if (kb == 16) tag8[(size_t)o] = (uint8_t)t;
+                else tag16[(size_t)o] = (uint16_t)t;
             }
         }
-        // one tag byte per octet: its bucket (all 8 rows share it) and trailing padding
-        std::vector<uint8_t> tag((size_t)std::max<int64_t>(L.n_slots / 8, 1), 0);
-        for (const Run &r : runs) {
-            for (int64_t o = r.slot_off / 8; o < (r.slot_off + r.rows_pad) / 8; ++o) tag[(size_t)o] = (uint8_t)r.bucket;
-            const int64_t pad = r.rows_pad - r.rows;
-            tag[(size_t)((r.slot_off + r.rows_pad) / 8 - 1)] |= (uint8_t)(pad << 5);
+        if (kb == 16) {
+            uint16_t *c;
+            uint8_t *t;
+            TRY(upload(p, &c, code16));
+            TRY(upload(p, &t, tag8));
+            p->d_lead_codes = c;
+            p->d_octet_tag = t;
+        } else {
+            uint8_t *c;
+            uint16_t *t;
+            TRY(upload(p, &c, code8));
+            TRY(upload(p, &t, tag16));
+            p->d_lead_codes = c;
+            p->d_octet_tag = t;
         }
-        TRY(upload(p, &p->d_lead16, lead16));
-        TRY(upload(p, &p->d_octet_tag, tag));
         TRY(upload(p, &p->d_key_of, key));
         std::vector<int32_t> kl;
         for (int32_t a : L.facts) kl.push_back(key[(size_t)a]);
@@ -534,7 +563,7 @@ extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
     o->lead_pass_bytes = (int64_t)lead_plane_bytes(p);
     o->stream_pass_bytes = (int64_t)stream_plane_bytes(p);
     o->truth_mode = p->exact ? 0 : 1;
-    o->key_shift = p->d_lead16 ? p->kshift : -1;
+    o->key_shift = p->d_lead_codes ? p->kshift : -1;
     o->summary_shift = p->shift;
     o->grid_blocks = p->lm_blocks;
     o->full_kernel = p->use_tma ? 1 : 0;
@@ -676,8 +705,9 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
         stats_dev = nullptr;
     }
     q.stats = stats_dev;
-    q.lead16 = (frontier || p->use_tma) ? nullptr : p->d_lead16;
+    q.lead_codes = (frontier || p->use_tma) ? nullptr : p->d_lead_codes;
     q.octet_tag = p->d_octet_tag;
+    q.key_bits = p->key_bits;
     q.lead32 = (frontier || p->use_tma) ? nullptr : p->d_lead32;
     q.xlead16 = (frontier || p->use_tma) ? nullptr : p->d_xlead16;
     q.xhead16 = p->d_xhead16;

@@ -16,6 +16,8 @@
 // paper they implement.
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "kernels.h"
 
 namespace cg = cooperative_groups;
@@ -36,7 +38,7 @@ namespace cg = cooperative_groups;
 #endif
 
 #ifndef LP_OCT_U
-#define LP_OCT_U 4   // key-plane octets in flight per thread (LEAD passes)
+#define LP_OCT_U 8   // 8-bit key plane: octets in flight per thread (8 measured best)
 #endif
 
 namespace lpb {
@@ -142,7 +144,7 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
         *p.status_next = 0;
         p.pcnt[0] = p.pcnt[1] = p.pcnt[2] = 0;
     }
-    const bool keys = summary_mode && p.lead16;
+    const bool keys = summary_mode && p.lead_codes;
     const bool osum = summary_mode && !(keys && starts_lead(p));
     if (!p.v0 && !osum && p.init_list) {
         // v0 = facts only: the initial words and list were built at load, so
@@ -222,7 +224,7 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
 __device__ __forceinline__ void lm_zero_summaries(const LMParams &p, bool summary_mode, int64_t gtid,
                                                   int64_t gthreads) {
     if (!summary_mode) return;
-    if (!(p.lead16 && starts_lead(p)))
+    if (!(p.lead_codes && starts_lead(p)))
         for (int64_t w = gtid; w < p.sm_words; w += gthreads) p.summary[w] = 0u;
 }
 
@@ -252,7 +254,7 @@ struct PassCtx {
     int32_t *qbuf;       // this CTA's candidate queue (global, FILTER mode)
     int32_t *qcount;     // its fill counter (shared memory)
     int k;
-    const uint32_t *bmask;  // key mode: bit b = some summary bit of bucket b is set (shared)
+    const uint32_t *bmask;  // key mode: bit b = some summary bit of bucket b is set (shared bitmap)
     const Segment *segs;    // the segment table (shared-memory copy when it fits)
     int32_t *sq;            // the first kSmemQueue queue entries (shared memory), or NULL
     int32_t *pc;            // this pass's append counter (p.pcnt[k % 3])
@@ -301,7 +303,7 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
     const int32_t pos = c.base + base + __popc(m & ((1u << lane) - 1u));
     LP_CHECK(pos >= 0 && pos <= p.n_order_cap && h >= 0 && h < p.n_ext_atoms);
     p.order[pos] = h;
-    if (p.lead16) p.korder[pos] = __ldg(p.key_of + h);   // once per atom, not per CTA
+    if (p.lead_codes) p.korder[pos] = __ldg(p.key_of + h);   // once per atom, not per CTA
     if (p.stage && h < p.n_out) p.stage[h] = c.k + 1;
 }
 
@@ -486,42 +488,81 @@ __device__ __forceinline__ void seg_lead(const LMParams &p, const Segment &sg, c
     }
 }
 
-// LEAD pass in key mode: stream the uint16 key plane, 8 rows (one octet) per 16-byte
-// load plus the octet's tag byte (bucket = high bits of the key group, and the number of
-// trailing padding rows), U octets in flight per thread.  Row i is alive iff summary bit
-// (bucket << 16 | lead16[i]) is set.  Thread t takes octets t, t + gthreads, ...
-template <int U>
-__device__ __forceinline__ void oct_load(const LMParams &p, int32_t q0, int32_t gth, int4 (&v)[U],
-                                         uint32_t (&tag)[U]) {
+// LEAD pass in key mode: stream the key plane, 8 rows (one octet) per load of their
+// codes plus the octet's tag (bucket = key group >> key_bits, and the number of trailing
+// padding rows), U octets in flight per thread.  Row i is alive iff summary bit
+// (bucket << key_bits | code[i]) is set; an octet whose bucket has no set bit is dead
+// without a lookup.  Thread t takes octets t, t + gthreads, ...
+__device__ __forceinline__ uint2 ld_stream8(const uint2 *p) {
+    uint2 r;
+    asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ bool bucket_any(const uint32_t *bm, uint32_t b) {
+    return (bm[b >> 5] >> (b & 31)) & 1u;
+}
+
+// KB = bits of the key group each row carries (16: uint16 codes, uint8 tags with 5 bucket
+// bits; 8: uint8 codes, uint16 tags with 13 bucket bits); the octet's bucket is
+// group >> KB and the tag's top 3 bits count its trailing padding rows.
+template <int KB>
+struct OctT {
+    using vec = typename std::conditional<KB == 16, int4, uint2>::type;   // 8 codes
+    using tag = typename std::conditional<KB == 16, uint8_t, uint16_t>::type;
+    static constexpr uint32_t bmask = KB == 16 ? 31u : 0x1FFFu;
+    static constexpr int pshift = KB == 16 ? 5 : 13;
+    static __device__ __forceinline__ vec load(const vec *p) {
+        if constexpr (KB == 16) return ld_stream(p);
+        else return ld_stream8(p);
+    }
+    static __device__ __forceinline__ uint32_t code(const vec &v, int e) {   // row e of 8
+        if constexpr (KB == 16) {
+            const uint32_t w = e < 2 ? (uint32_t)v.x : e < 4 ? (uint32_t)v.y : e < 6 ? (uint32_t)v.z : (uint32_t)v.w;
+            return (e & 1) ? (w >> 16) : (w & 0xFFFFu);
+        } else {
+            const uint32_t w = e < 4 ? v.x : v.y;
+            return (w >> (8 * (e & 3))) & 0xFFu;
+        }
+    }
+};
+
+template <int U, int KB>
+__device__ __forceinline__ void oct_load(const LMParams &p, int32_t q0, int32_t gth,
+                                         typename OctT<KB>::vec (&v)[U], uint32_t (&tag)[U]) {
+    using T = OctT<KB>;
     const int32_t no = (int32_t)(p.n_slots >> 3);
-    const int4 *base = reinterpret_cast<const int4 *>(p.lead16);
+    const typename T::vec *base = reinterpret_cast<const typename T::vec *>(p.lead_codes);
+    const typename T::tag *tb = reinterpret_cast<const typename T::tag *>(p.octet_tag);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int32_t q = q0 + u * gth;
-        v[u] = q < no ? ld_stream(base + q) : make_int4(0, 0, 0, 0);
-        tag[u] = q < no ? (uint32_t)__ldg(p.octet_tag + q) : 0u;
+        if (q < no) {
+            v[u] = T::load(base + q);
+            tag[u] = (uint32_t)__ldg(tb + q);
+        } else {
+            v[u] = typename T::vec{};
+            tag[u] = 0u;
+        }
     }
 }
 
-template <int U>
+template <int U, int KB>
 __device__ __forceinline__ void oct_test(const LMParams &p, const PassCtx &c, int32_t q0, int32_t gth,
-                                         const int4 (&v)[U], const uint32_t (&tag)[U]) {
+                                         const typename OctT<KB>::vec (&v)[U], const uint32_t (&tag)[U]) {
+    using T = OctT<KB>;
     const int32_t no = (int32_t)(p.n_slots >> 3);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int32_t q = q0 + u * gth;
         if (q >= no) break;
-        const uint32_t b = tag[u] & 31u;
-        if (!((*c.bmask >> b) & 1u)) continue;            // bucket with no true key
-        const uint32_t hi = b << 16;
-        const uint32_t w[4] = {(uint32_t)v[u].x, (uint32_t)v[u].y, (uint32_t)v[u].z, (uint32_t)v[u].w};
+        const uint32_t b = tag[u] & T::bmask;
+        if (!bucket_any(c.bmask, b)) continue;            // bucket with no true key
+        const uint32_t hi = b << KB;
         unsigned fire = 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            fire |= (unsigned)sm_bit(c.sm, hi | (w[e] & 0xFFFFu)) << (2 * e);
-            fire |= (unsigned)sm_bit(c.sm, hi | (w[e] >> 16)) << (2 * e + 1);
-        }
-        fire &= 0xFFu >> (tag[u] >> 5);                   // trailing padding rows
+        for (int e = 0; e < 8; ++e) fire |= (unsigned)sm_bit(c.sm, hi | T::code(v[u], e)) << e;
+        fire &= 0xFFu >> (tag[u] >> T::pshift);           // trailing padding rows
         if (fire) {
             int32_t pos = atomicAdd(c.qcount, __popc(fire));
             if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
@@ -533,17 +574,24 @@ __device__ __forceinline__ void oct_test(const LMParams &p, const PassCtx &c, in
 
 // (issuing the first loads before the pass-top delta update, so they overlap its
 // latency, measured slower: they compete with the delta's loads and add spills)
-template <int U>
-__device__ __forceinline__ void octets_lead(const LMParams &p, const PassCtx &c, int64_t gtid,
-                                            int64_t gthreads) {
+template <int U, int KB>
+__device__ __forceinline__ void octets_lead_kb(const LMParams &p, const PassCtx &c, int64_t gtid,
+                                               int64_t gthreads) {
     const int32_t no = (int32_t)(p.n_slots >> 3);
     const int32_t gth = (int32_t)gthreads;
     for (int32_t q0 = (int32_t)gtid; q0 < no; q0 += gth * U) {
-        int4 v[U];
+        typename OctT<KB>::vec v[U];
         uint32_t tag[U];
-        oct_load<U>(p, q0, gth, v, tag);
-        oct_test<U>(p, c, q0, gth, v, tag);
+        oct_load<U, KB>(p, q0, gth, v, tag);
+        oct_test<U, KB>(p, c, q0, gth, v, tag);
     }
+}
+
+// (16-bit codes: 4 octets = 64 bytes in flight per thread; 8-bit codes: 8 octets)
+__device__ __forceinline__ void octets_lead(const LMParams &p, const PassCtx &c, int64_t gtid,
+                                            int64_t gthreads) {
+    if (p.key_bits == 8) octets_lead_kb<LP_OCT_U, 8>(p, c, gtid, gthreads);
+    else octets_lead_kb<4, 16>(p, c, gtid, gthreads);
 }
 
 // LEAD pass in exact mode over the 16-bit planes: 8 rows per 16-byte load of each plane
@@ -674,18 +722,15 @@ __device__ __forceinline__ void add_to_shared(const LMParams &p, uint32_t *sm, u
             a[u] = EXACT ? a[u] : keys ? (a[u] >> p.kshift) : (a[u] >> p.shift);
             LP_CHECK((a[u] >> 5) < (uint32_t)(keys ? p.ksm_words : p.sm_words));
         }
-        uint32_t m = 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (a[u] != 0xFFFFFFFFu) {
                 atomicOr(sm + (a[u] >> 5), 1u << (a[u] & 31));
-                m |= 1u << ((a[u] >> 16) & 31);
+                if (!EXACT && keys) {   // the group's bucket (group >> key_bits) now has a set bit
+                    const uint32_t bk = a[u] >> p.key_bits;
+                    atomicOr(bmask + (bk >> 5), 1u << (bk & 31));
+                }
             }
-        if (!EXACT && keys) {   // (lanes of a warp may have left the loop already)
-            const unsigned act = __activemask();
-            m = __reduce_or_sync(act, m);
-            if ((threadIdx.x & 31) == __ffs(act) - 1 && m) atomicOr(bmask, m);
-        }
     }
 }
 
@@ -702,7 +747,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     extern __shared__ uint32_t sm[];
     __shared__ int32_t qcount;
     __shared__ unsigned long long loaded_cta;
-    __shared__ uint32_t bmask;
+    __shared__ uint32_t bmask[kBucketWords];   // key mode: bucket b has a set summary bit
     __shared__ Segment ssegs[kMaxSmemSegs];
     __shared__ int32_t squeue[kSmemQueue];
     __shared__ int32_t streamers_done;
@@ -731,11 +776,11 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     grid.sync();
     if (p.dbg && tid == 0) p.dbg[(2 * gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
     bool lead_pass = starts_lead(p);
-    bool keys = !EXACT && p.lead16 && lead_pass;         // shared copy is in key space
+    bool keys = !EXACT && p.lead_codes && lead_pass;         // shared copy is in key space
     bool rebuild = false;                                // key space -> atom-id summary
     const int32_t n0 = __ldcg(p.tail);
     {
-        if (tid == 0) bmask = 0u;
+        for (int32_t w = tid; w < kBucketWords; w += blockDim.x) bmask[w] = 0u;
         if (p.nseg <= kMaxSmemSegs)
             for (int32_t s = tid; s < p.nseg; s += blockDim.x) ssegs[s] = p.segs[s];
         if (keys) {   // key summary of v_0 straight from the initial list (bucket b =
@@ -743,7 +788,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             int4 *s4 = reinterpret_cast<int4 *>(sm);
             for (int32_t w = tid; w < (p.ksm_words >> 2); w += blockDim.x) s4[w] = make_int4(0, 0, 0, 0);
             __syncthreads();
-            add_to_shared<EXACT>(p, sm, &bmask, 0, n0, true);
+            __syncthreads();
+            add_to_shared<EXACT>(p, sm, bmask, 0, n0, true);
         } else {
             smem_fill(sm, EXACT ? p.buf0 : p.summary, p.sm_words);
         }
@@ -792,7 +838,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                     }
                 }
             } else {
-                add_to_shared<EXACT>(p, sm, &bmask, ds, de, keys);
+                add_to_shared<EXACT>(p, sm, bmask, ds, de, keys);
             }
             if (p.dbg && tid == 0 && k >= 3 && k < 16) DBG_STAMP(6) = globaltimer();
             __syncthreads();
@@ -805,7 +851,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             p.vent[(k + 1) % 3] = 0;
             p.pcnt[(k + 1) % 3] = 0;
         }
-        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, &bmask,
+        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, bmask,
                         p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, p.pcnt + k % 3, de};
         if (p.dbg && tid == 0 && k < 16) DBG_STAMP(1) = globaltimer();
         const int j0 = (EXACT && lead_pass) ? 1 : 0;
@@ -822,7 +868,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             const int64_t sthreads = (int64_t)gridDim.x * (kStreamWarps * 32);
             if (warp < kStreamWarps) {
                 const int64_t sgtid = (int64_t)blockIdx.x * (kStreamWarps * 32) + tid;
-                octets_lead<LP_OCT_U>(p, c, sgtid, sthreads);
+                octets_lead(p, c, sgtid, sthreads);
                 __syncwarp();
                 if ((tid & 31) == 0) {
                     __threadfence_block();
@@ -848,7 +894,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                 }
             }
         }
-        else if (!EXACT && keys) octets_lead<LP_OCT_U>(p, c, gtid, gthreads);
+        else if (!EXACT && keys) octets_lead(p, c, gtid, gthreads);
         else if (EXACT && lead_pass && p.xlead16) octets_exact16<4>(p, c, gtid, gthreads);
         else if (EXACT && lead_pass && p.lead32) flat_lead_exact<4>(p, c, gtid, gthreads);
         else if (lead_pass) all_segments<EXACT, true>(p, c, gtid, gthreads);

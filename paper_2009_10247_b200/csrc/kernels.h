@@ -23,7 +23,8 @@ constexpr int kSmemQueue = 768;        // candidate queue entries kept in shared
 #ifndef LP_STREAM_WARPS
 #define LP_STREAM_WARPS 28
 #endif
-constexpr int kStreamWarps = LP_STREAM_WARPS;   // overlapped LEAD passes: streaming warps (the rest verify)
+constexpr int kStreamWarps = LP_STREAM_WARPS;
+constexpr int kBucketWords = 256;      // key mode: buckets (group >> 8) of the summary, bitmap words   // overlapped LEAD passes: streaming warps (the rest verify)
 
 // A body-length segment cut into TMA tiles of T rows.  A tile stages R = L (+1 when the
 // head row is staged too) rows of T ints each: row j holds body position j of T
@@ -115,11 +116,14 @@ struct LMParams {
     long long lead_bytes;      // bytes one LEAD / STREAM pass streams (program planes only)
     long long stream_bytes;
     // summary mode key plane: LEAD passes stream the key group of
-    // the lead atom (16 bits + a per-run bucket) and test it against a summary in key space, where the
+    // the lead atom (8 bits + a per-octet bucket) and test it against a summary in key space, where the
     // atoms that can become true (heads, facts) get fine groups and the rest share
     // coarse ones.  STREAM passes switch the shared copy back to the atom-id summary.
-    const uint16_t *lead16;    // [n_slots] low 16 bits of the lead atom's key group, or NULL
-    const uint8_t *octet_tag;  // [n_slots / 8] bucket (group >> 16, < 32) | padding rows << 5
+    const void *lead_codes;    // [n_slots] low key_bits bits of the lead atom's key group
+                               //   (uint16 or uint8), or NULL (no key mode)
+    const void *octet_tag;     // [n_slots / 8] bucket (group >> key_bits) | padding << 5 (uint8,
+                               //   16-bit codes) or << 13 (uint16, 8-bit codes)
+    int32_t key_bits;          // 16 (default) or 8 (LP_LOAD_KEY8)
     const int32_t *lead32;     // exact mode: [n_slots] body position 0 of every slot (flat)
     const uint16_t *xlead16;   // exact mode, ids < 2^21: low 16 bits of lead / head, and per
     const uint16_t *xhead16;   //   octet lead bucket | head bucket << 5 | padding << 10

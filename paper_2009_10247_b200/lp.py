@@ -24,6 +24,7 @@ LP_E_NOMEM, LP_E_CUDA, LP_E_NOT_CONVERGED, LP_E_NODEVICE = 5, 6, 7, 8
 LP_LOAD_NO_FRONTIER = 0x1
 LP_LOAD_TMA = 0x2
 LP_LOAD_PAPER_LAYOUT = 0x4
+LP_LOAD_KEY8 = 0x8
 LP_PTR_DEVICE = 0x1
 LP_FRONTIER = 0x2
 LP_FULL_STREAM = 0x4
@@ -177,7 +178,7 @@ class Program:
 
     def __init__(self, rules, device: int = 0, guess_cap: int = 20, frontier: bool = True,
                  smem_bits_cap: int = 0, grid_blocks: int = 0, allocator: str = "torch",
-                 tma: bool = False, paper_layout: bool = False):
+                 tma: bool = False, paper_layout: bool = False, key8: bool = False):
         lib = library()
         self._keep = []
         head = np.ascontiguousarray(rules.head, dtype=np.int32)
@@ -189,7 +190,7 @@ class Program:
         opt.device = int(device)
         opt.guess_cap = int(guess_cap)
         opt.flags = ((0 if frontier else LP_LOAD_NO_FRONTIER) | (LP_LOAD_TMA if tma else 0) |
-                     (LP_LOAD_PAPER_LAYOUT if paper_layout else 0))
+                     (LP_LOAD_PAPER_LAYOUT if paper_layout else 0) | (LP_LOAD_KEY8 if key8 else 0))
         opt.smem_bits_cap = int(smem_bits_cap)
         opt.grid_blocks = int(grid_blocks)
         if device >= 0 and allocator == "torch":

@@ -90,7 +90,8 @@ def test_random_programs(seed):
 
 @pytest.mark.parametrize("seed", range(20))
 @pytest.mark.parametrize("cfg", [dict(smem_bits_cap=128), dict(smem_bits_cap=1024, grid_blocks=3),
-                                 dict(grid_blocks=1)])
+                                 dict(grid_blocks=1), dict(smem_bits_cap=128, key8=True),
+                                 dict(smem_bits_cap=1024, key8=True, grid_blocks=5)])
 def test_forced_summary_mode_and_small_grids(seed, cfg):
     """FILTER mode (summary in shared memory, exact test in L2) and tiny grids."""
     rng = np.random.default_rng([seed, 99])
@@ -218,6 +219,13 @@ def test_config_c4_parity():
     prog = check_lm(P)
     assert prog.info["truth_mode"] == 1     # the 10M-atom truth vector is L2-resident
     assert prog.info["key_shift"] >= 0
+    prog.close()
+    # the 8-bit key plane (LP_LOAD_KEY8) on the same program
+    om, ostage, oit = oracle.lm_stage(P)
+    p8 = lp.Program(P, key8=True, frontier=False)
+    model, iters, ex = p8.least_model(stages=True, stats=True)
+    assert iters == oit and (model == oracle.pack_bits(om)).all() and (ex["stage"] == ostage).all()
+    assert p8.info["lead_pass_bytes"] < 0.7 * prog.info["lead_pass_bytes"]
 
 
 # ---------------------------------------------------------------------------------
