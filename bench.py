@@ -32,7 +32,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-KERNEL_REV = "lead8-octets-d2"   # bump when the dominant kernel's traffic changes
+KERNEL_REV = "lead16-octets-d2"   # bump when the dominant kernel's traffic changes
 METRIC = ("least-model fixpoint time & nnz·iter/s (HBM GB/s vs peak); "
           "stable-model guesses/s")
 
@@ -333,6 +333,29 @@ def main():
         del sharded
 
     if not args.no_extras:
+        # ---- the 8-bit key plane (LP_LOAD_KEY8) on the same workload: fewer bytes per
+        # pass, which then stay L2-resident across passes ----------
+        prog8 = lp.Program(P, device=local, frontier=False, key8=True)
+        k8 = []
+        for i in range(args.warmup + args.steps):
+            flush_l2()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            lp.lp_least_model(prog8, None, model, stream=stream, device_ptrs=True, iters_out=iters_d,
+                              stats=stats_d)
+            e1.record(stream)
+            stream.synchronize()
+            if i >= args.warmup:
+                k8.append(e0.elapsed_time(e1))
+        assert int(iters_d.item()) == iters
+        k8ms = allmax(float(np.mean(k8)))
+        out["key8"] = {"ms_per_step": k8ms, "value": ws * nnz * iters / (k8ms / 1e3), "unit": "nnz*iter/s",
+                       "algorithmic_bytes_per_launch": int(stats_d[0].item()),
+                       "lead_pass_bytes": int(prog8.info["lead_pass_bytes"]),
+                       "note": "8-bit key codes: the per-pass plane fits L2, so this variant is "
+                               "L2/latency-bound, not HBM-bound (ncu: profiles/r01_ncu_full_c4_key8.md)"}
+        prog8.close()
+
         # ---- frontier variant on the same workload --------------------------------------
         fms, fkms, fit, _, _ = timed_least_model(True, args.steps, args.warmup)
         assert fit == iters
