@@ -766,6 +766,7 @@ static STParams st_params(lp_program *p) {
     // the flat lead plane holds extended-atom ids: usable when the any-filter is exact
     s.lead32 = (p->any_shift == 0) ? p->d_lead32 : nullptr;
     s.n_slots = L.n_slots;
+    s.cta_queue = (L.n_slots < (1LL << 27) && L.segs.size() <= 32) ? 1 : 0;
     s.W = p->W;
     s.G = p->G;
     s.any_words = p->any_words;

@@ -1521,6 +1521,8 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const int64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
+    __shared__ uint32_t st_q[kStQueue];  // candidate rows of this CTA's scan: slot | segment << 27
+    __shared__ int32_t st_qn, st_qover;
     // shared memory: "true in some guess" bits, then (exact filter only) "true in every
     // guess" bits -- a row whose head is full can change nothing
     uint32_t *full = sm + p.any_words;
@@ -1566,6 +1568,12 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
                 }
             __syncthreads();
         }
+        if (tid == 0) {
+            st_qn = 0;
+            st_qover = 0;
+        }
+        __syncthreads();
+        if (p.dbg && tid == 0 && k < 64) atomicMax(p.dbg + 4 * k + 2, globaltimer());   // pass top done
         if (blockIdx.x == 0 && tid == 0) p.pcnt[(k + 1) % 3] = 0;   // next pass's counter
         // candidate scan: a lane tests 4 rows (one 16-byte load per body position, lead
         // position first -- usually an atom that is true in no guess -- and the heads
@@ -1606,18 +1614,38 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
                         }
                     }
                 }
-                if (p.dbg && alive) atomicAdd(p.dbg + 2 * (k & 63) + 1, (unsigned long long)__popc(alive));
-                for (int e = 0; e < 4; ++e) {
-                    unsigned m = __ballot_sync(0xFFFFFFFFu, (alive >> e) & 1u);
-                    while (m) {
-                        const int l = __ffs(m) - 1;
-                        m &= m - 1;
-                        const int s = __shfl_sync(0xFFFFFFFFu, sgi, l);
-                        const Segment sg = p.segs[s];
-                        st_row(p, sg, (q0 + l) * 4 + e - sg.slot_off, rd, wr, k, lane, p.pcnt + k % 3,
-                               (k % 3) * p.ring_cap);
+                if (p.dbg && alive) atomicAdd(p.dbg + 4 * (k & 63) + 1, (unsigned long long)__popc(alive));
+                // candidates go to the CTA's shared queue (slot | segment << 27) so that all
+                // warps share them; a full queue is drained by the finding warp itself
+                for (unsigned f = alive; f && p.cta_queue; f &= f - 1) {
+                    const int e = __ffs(f) - 1;
+                    const int32_t pos = atomicAdd(&st_qn, 1);
+                    if (pos < kStQueue) st_q[pos] = (uint32_t)(q * 4 + e) | ((uint32_t)sgi << 27);
+                    else atomicAdd(&st_qover, 1);
+                }
+                if (!p.cta_queue && alive) st_qover = 1;   // (huge programs: the direct path)
+                if (__any_sync(0xFFFFFFFFu, st_qover != 0)) {   // (rare) overflow: old path
+                    for (int e = 0; e < 4; ++e) {
+                        unsigned m = __ballot_sync(0xFFFFFFFFu, (alive >> e) & 1u);
+                        while (m) {
+                            const int l = __ffs(m) - 1;
+                            m &= m - 1;
+                            const int s = __shfl_sync(0xFFFFFFFFu, sgi, l);
+                            const Segment sg = p.segs[s];
+                            st_row(p, sg, (q0 + l) * 4 + e - sg.slot_off, rd, wr, k, lane, p.pcnt + k % 3,
+                                   (k % 3) * p.ring_cap);
+                        }
                     }
                 }
+            }
+            __syncthreads();
+            // every warp takes candidates from the shared queue
+            const int32_t nq_c = min(st_qn, kStQueue);
+            for (int32_t i = tid >> 5; i < nq_c && p.cta_queue; i += blockDim.x >> 5) {
+                const uint32_t ent = st_q[i];
+                const Segment sg = p.segs[ent >> 27];
+                st_row(p, sg, (int64_t)(ent & 0x7FFFFFFu) - sg.slot_off, rd, wr, k, lane, p.pcnt + k % 3,
+                       (k % 3) * p.ring_cap);
             }
         }
         int64_t off = 0;  // rotate each segment's first warp (see all_segments)
@@ -1650,7 +1678,7 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
                                  (sm_bit(sm, (uint32_t)c.w >> p.any_shift) ? 8u : 0u);
                     }
                 }
-                if (p.dbg && alive) atomicAdd(p.dbg + 2 * (k & 63) + 1, (unsigned long long)__popc(alive));
+                if (p.dbg && alive) atomicAdd(p.dbg + 4 * (k & 63) + 1, (unsigned long long)__popc(alive));
                 for (int e = 0; e < 4; ++e) {
                     unsigned m = __ballot_sync(0xFFFFFFFFu, (alive >> e) & 1u);
                     while (m) {
@@ -1661,12 +1689,16 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
                 }
             }
         }
+        if (p.dbg && k < 64) {
+            __syncthreads();
+            if (tid == 0) atomicMax(p.dbg + 4 * k + 3, globaltimer());     // CTA's scan done
+        }
         grid.sync();
         // rows changed in this pass: its own counter slot (the next pass appends to
         // another one, so every CTA reads the same value after the barrier)
         const int32_t cnt = __ldcg(p.pcnt + k % 3);
         const bool lead = blockIdx.x == 0 && tid == 0;
-        if (p.dbg && lead && k < 64) p.dbg[2 * k] = globaltimer();   // profiling hook
+        if (p.dbg && lead && k < 64) p.dbg[4 * k] = globaltimer();   // profiling hook
         if (cnt == 0) {
             if (lead) { *p.passes_out = k + 1; }
             return;
@@ -1760,8 +1792,8 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
     if ((e = cudaFuncSetAttribute((const void *)lm_tma_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)))
         return e;
-    if ((e = cudaFuncSetAttribute((const void *)st_fixpoint_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, cap)))
+    if ((e = cudaFuncSetAttribute((const void *)st_fixpoint_kernel,   // (+ its static candidate queue)
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
         return e;
     return cudaSuccess;
 }

@@ -24,7 +24,8 @@ constexpr int kSmemQueue = 768;        // candidate queue entries kept in shared
 #define LP_STREAM_WARPS 28
 #endif
 constexpr int kStreamWarps = LP_STREAM_WARPS;
-constexpr int kBucketWords = 256;      // key mode: buckets (group >> 8) of the summary, bitmap words   // overlapped LEAD passes: streaming warps (the rest verify)
+constexpr int kBucketWords = 256;
+constexpr int kStQueue = 2048;         // stable search: candidate rows queued per CTA and pass      // key mode: buckets (group >> 8) of the summary, bitmap words   // overlapped LEAD passes: streaming warps (the rest verify)
 
 // A body-length segment cut into TMA tiles of T rows.  A tile stages R = L (+1 when the
 // head row is staged too) rows of T ints each: row j holds body position j of T
@@ -157,8 +158,10 @@ struct STParams {
     int32_t *pcnt;             // [3] per-pass append counters (slot k % 3)
     uint32_t *gfull;           // [any_words] rows true in every guess (use_full only)
     int32_t use_full;          // exact any-filter with room for the full bits
-    unsigned long long *dbg;   // optional [64][2]: barrier-exit time, candidate rows per pass
+    unsigned long long *dbg;   // optional [64][4]: barrier exit, candidate rows, last CTA's
+                               //   pass-top done, last CTA's scan done (per pass)
     const int32_t *lead32;     // exact mode: flat lead plane (one scan loop), else NULL
+    int32_t cta_queue;         // candidates shared by the CTA's warps (slots < 2^27, <= 32 segments)
     int64_t n_slots;
     int32_t W;                 // guess words in use (the rest of Wp is padding)
     int64_t G;                 // guesses

@@ -12,7 +12,7 @@ from paper_2009_10247_b200 import lp  # noqa: E402
 
 P = lpgen.config(sys.argv[1] if len(sys.argv) > 1 else "C5")
 prog = lp.Program(P)
-buf = torch.zeros(128, dtype=torch.int64, device="cuda")
+buf = torch.zeros(256, dtype=torch.int64, device="cuda")
 lib = lp.library()
 lib.lpdbg_set_timing.argtypes = [ctypes.c_void_p]
 for _ in range(3):
@@ -20,10 +20,9 @@ for _ in range(3):
 lib.lpdbg_set_timing(buf.data_ptr())
 ids, passes, _ = prog.stable_models()
 lib.lpdbg_set_timing(None)
-t = buf.cpu().numpy().reshape(64, 2)
-t0 = t[0, 0]
-prev = None
-for k in range(passes):
-    dt = (t[k, 0] - prev) / 1e3 if prev is not None else float("nan")
-    print(f"pass {k:2d}: barrier at {(t[k, 0] - t0) / 1e3:8.1f} us (+{dt:6.1f})  candidates {t[k, 1]}")
-    prev = t[k, 0]
+t = buf.cpu().numpy().reshape(64, 4).astype(np.float64)
+# pass k runs from barrier exit of k-1 to barrier exit of k
+for k in range(1, passes):
+    b0 = t[k - 1, 0]
+    print(f"pass {k:2d}: top done +{(t[k, 2] - b0) / 1e3:5.1f}  scan+rows done +{(t[k, 3] - b0) / 1e3:5.1f}  "
+          f"barrier exit +{(t[k, 0] - b0) / 1e3:5.1f} us   candidates {int(t[k, 1])}")
