@@ -73,6 +73,7 @@ struct lp_program {
     int32_t ksm_words = 0, kshift = 0;
     uint32_t *d_factbits = nullptr, *d_init_bits = nullptr;
     int32_t *d_init_list = nullptr, *d_init_klist = nullptr;
+    uint32_t *d_init_ksum = nullptr;
     int32_t n_init = 0;
     uint64_t lm_runs = 0;
     int32_t *d_facts = nullptr;
@@ -341,6 +342,15 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         std::vector<int32_t> kl;
         for (int32_t a : L.facts) kl.push_back(key[(size_t)a]);
         TRY(upload(p, &p->d_init_klist, kl));
+        if (kw % 4 == 0) {   // the v_0 key summary image (LEAD passes, v0 = NULL)
+            std::vector<uint32_t> ks((size_t)kw + kBucketWords, 0u);
+            for (int32_t c : kl) {
+                const uint32_t g = (uint32_t)c >> sh, bk = g >> kb;
+                ks[g >> 5] |= 1u << (g & 31);
+                ks[(size_t)kw + (bk >> 5)] |= 1u << (bk & 31);
+            }
+            TRY(upload(p, &p->d_init_ksum, ks));
+        }
         TRY(dalloc(p, &p->d_korder, (size_t)L.n_ext + 1));
         p->lm_smem = std::max(p->lm_smem, (size_t)kw * 4);
     }
@@ -659,6 +669,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.init_bits = p->d_init_bits;
     q.init_list = p->d_init_list;
     q.init_klist = p->d_init_klist;
+    q.init_ksum = std::getenv("LP_NO_KSUM_IMAGE") ? nullptr : p->d_init_ksum;
     q.n_init = p->n_init;
     q.top = L.top;
     unsigned long long *mout = dev ? reinterpret_cast<unsigned long long *>(model_out) : p->d_model;

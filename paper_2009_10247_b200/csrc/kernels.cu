@@ -75,6 +75,63 @@ __device__ __forceinline__ bool sm_bit(const uint32_t *sm, uint32_t x) {
 // ------------------------------------------------------------------------------------
 
 // Copy nw (multiple of 4) 32-bit words global -> shared with 16-byte loads, 4 in flight.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s_plain(void *dst, const void *src, uint32_t bytes,
+                                               uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+
+// Copy nw words (nw % 4 == 0, src 16-byte aligned) global -> shared with TMA bulk copies
+// completing on `bar` (single use, phase 0; all threads of the CTA call it and return
+// once the data has landed).
+__device__ __forceinline__ void smem_fill_bulk(uint32_t *sm, const uint32_t *src, int32_t nw, uint64_t *bar) {
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t bytes = (uint32_t)nw * 4u;
+        mbar_expect_tx(bar, bytes);
+        constexpr uint32_t kChunk = 32768;
+        for (uint32_t o = 0; o < bytes; o += kChunk)
+            bulk_g2s_plain(reinterpret_cast<char *>(sm) + o, reinterpret_cast<const char *>(src) + o,
+                           bytes - o < kChunk ? bytes - o : kChunk, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+}
+
 __device__ __forceinline__ void smem_fill(uint32_t *sm, const uint32_t *src, int32_t nw) {
     const int4 *s4 = reinterpret_cast<const int4 *>(src);
     int4 *d4 = reinterpret_cast<int4 *>(sm);
@@ -744,13 +801,14 @@ __device__ __forceinline__ void add_to_shared(const LMParams &p, uint32_t *sm, u
 // decides which bytes are read (p.pass_mode).
 template <bool EXACT>
 __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_constant__ LMParams p) {
-    extern __shared__ uint32_t sm[];
+    extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t qcount;
     __shared__ unsigned long long loaded_cta;
     __shared__ uint32_t bmask[kBucketWords];   // key mode: bucket b has a set summary bit
     __shared__ Segment ssegs[kMaxSmemSegs];
     __shared__ int32_t squeue[kSmemQueue];
     __shared__ int32_t streamers_done;
+    __shared__ __align__(8) uint64_t fill_bar;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
@@ -783,11 +841,14 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         for (int32_t w = tid; w < kBucketWords; w += blockDim.x) bmask[w] = 0u;
         if (p.nseg <= kMaxSmemSegs)
             for (int32_t s = tid; s < p.nseg; s += blockDim.x) ssegs[s] = p.segs[s];
-        if (keys) {   // key summary of v_0 straight from the initial list (bucket b =
-                      // summary words [b << 11, (b + 1) << 11))
+        if (keys && !p.v0 && p.init_ksum) {   // v_0 = facts: key summary + bucket mask
+                                              // images built at load, copied in
+            smem_fill_bulk(sm, p.init_ksum, p.ksm_words, &fill_bar);
+            for (int32_t w = tid; w < kBucketWords; w += blockDim.x) bmask[w] = __ldg(p.init_ksum + p.ksm_words + w);
+        } else if (keys) {   // key summary of v_0 straight from the initial list (bucket b =
+                             // summary words [b << 11, (b + 1) << 11))
             int4 *s4 = reinterpret_cast<int4 *>(sm);
             for (int32_t w = tid; w < (p.ksm_words >> 2); w += blockDim.x) s4[w] = make_int4(0, 0, 0, 0);
-            __syncthreads();
             __syncthreads();
             add_to_shared<EXACT>(p, sm, bmask, 0, n0, true);
         } else {
@@ -1011,44 +1072,6 @@ cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t sme
 // shared copy of v_k or its summary).  Because the program matrix is the same in every
 // pass, the producer keeps prefetching the next pass's first tiles across the grid
 // barrier, so HBM never idles while the pass is being closed.
-
-__device__ __forceinline__ uint32_t smem_addr(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-                 "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-        "r"(parity) : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
-                                         uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy) : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s_plain(void *dst, const void *src, uint32_t bytes,
-                                               uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
-}
 
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t pol;

@@ -60,6 +60,7 @@ struct LMParams {
     const uint32_t *init_bits;
     const int32_t *init_list;
     const int32_t *init_klist; // (key mode)
+    const uint32_t *init_ksum; // (key mode) v_0's key summary [ksm_words] + bucket mask [kBucketWords]
     int32_t n_init;
     int32_t top;               // ⊤
     unsigned long long *model_out;  // [ceil(n/64)] written by the epilogue
