@@ -864,6 +864,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 7] = globaltimer();
 
     int32_t ds = n0, de = n0;  // atoms that became true in the previous pass
+    constexpr int kSpec = 4;
+    uint32_t spec[kSpec];      // the next delta's first list entries, loaded with its count
     for (int k = 0;; ++k) {
         const uint32_t *rd = (k & 1) ? p.buf1 : p.buf0;
         uint32_t *wr = (k & 1) ? p.buf0 : p.buf1;
@@ -898,6 +900,21 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                         }
                     }
                 }
+            } else if (EXACT || keys) {
+                // the first kSpec x blockDim entries were loaded right after the barrier
+#pragma unroll
+                for (int u = 0; u < kSpec; ++u) {
+                    const int32_t i = ds + tid + u * (int32_t)blockDim.x;
+                    if (i < de) {
+                        const uint32_t g = EXACT ? spec[u] : (spec[u] >> p.kshift);
+                        atomicOr(sm + (g >> 5), 1u << (g & 31));
+                        if (!EXACT && keys) {
+                            const uint32_t bk = g >> p.key_bits;
+                            atomicOr(bmask + (bk >> 5), 1u << (bk & 31));
+                        }
+                    }
+                }
+                add_to_shared<EXACT>(p, sm, bmask, ds + kSpec * (int32_t)blockDim.x, de, keys);
             } else {
                 add_to_shared<EXACT>(p, sm, bmask, ds, de, keys);
             }
@@ -1004,6 +1021,17 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
 #undef DBG_STAMP
         // after the barrier: this pass's appends (a slot nobody touches again before the
         // next barrier -- the shared tail would race with the next pass's appends)
+        if (EXACT || keys) {
+            // load the first list slots of this pass's appends together with their count
+            // instead of after it (one L2 round trip less before the next stream); slots at
+            // or past the count are not used (the next pass may be appending there already)
+            const int32_t *lst = EXACT ? p.order : p.korder;
+#pragma unroll
+            for (int u = 0; u < kSpec; ++u) {
+                const int32_t i = de + tid + u * (int32_t)blockDim.x;
+                spec[u] = i < p.n_order_cap ? (uint32_t)__ldcg(lst + i) : 0u;
+            }
+        }
         const int32_t t = de + __ldcg(p.pcnt + k % 3);
         const int32_t queued = __ldcg(p.cand + k % 3);
         if (lead && p.stats) {
