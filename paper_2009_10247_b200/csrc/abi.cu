@@ -395,7 +395,16 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     TRY(upload(p, &p->d_head, L.head));
     if (L.has_occ) {
         TRY(upload(p, &p->d_occ_ptr, L.occ_ptr));
-        TRY(upload(p, &p->d_occ_slot, L.occ_slot));
+        {   // (slot, head(slot)) pairs: a firing row's head comes with its slot, one
+            // dependent load less per level
+            std::vector<int32_t> sh(2 * L.occ_slot.size());
+            for (size_t i = 0; i < L.occ_slot.size(); ++i) {
+                sh[2 * i] = L.occ_slot[i];
+                const size_t s = (size_t)L.occ_slot[i];   // (a placeholder entry if nnz = 0)
+                sh[2 * i + 1] = s < L.head.size() ? L.head[s] : 0;
+            }
+            TRY(upload(p, &p->d_occ_slot, sh));
+        }
         p->cnt_bytes = L.max_body <= 255 ? 1 : 4;
         const size_t cw = p->cnt_bytes == 1 ? ((size_t)L.n_slots + 3) / 4 : (size_t)L.n_slots;
         TRY(dalloc(p, &p->d_cnt, std::max<size_t>(cw, 1)));

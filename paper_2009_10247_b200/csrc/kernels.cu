@@ -1359,13 +1359,16 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
     grid.sync();
     int32_t qs = 0, qe = __ldcg(p.tail);
     if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = qe;
+    int32_t a_first = (int64_t)qs + gwarp < qe ? __ldcg(p.order + qs + gwarp) : 0;
+    const int2 *occ = reinterpret_cast<const int2 *>(p.occ_slot);
     for (int k = 0;; ++k) {
         if (blockIdx.x == 0 && tid == 0) p.pcnt[(k + 1) % 3] = 0;   // next level's counter
         for (int64_t i = qs + gwarp; i < qe; i += nwarps) {
-            const int32_t a = __ldcg(p.order + i);
+            const int32_t a = i == qs + gwarp ? a_first : __ldcg(p.order + i);
             const int64_t o0 = __ldg(p.occ_ptr + a), o1 = __ldg(p.occ_ptr + a + 1);
             for (int64_t o = o0 + lane; o < o1; o += 32) {
-                const int32_t slot = __ldg(p.occ_slot + o);
+                const int2 sh = __ldg(occ + o);
+                const int32_t slot = sh.x;
                 bool fired;
                 if (p.cnt_bytes == 1) {   // a byte never underflows: <= L decrements
                     const uint32_t sh = (uint32_t)(slot & 3) << 3;
@@ -1374,7 +1377,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
                     fired = atomicSub(p.cnt + slot, 1u) == 1u;
                 }
                 if (fired) {                                // body(r) ⊆ I_k
-                    const int32_t h = __ldg(p.head + slot);
+                    const int32_t h = sh.y;
                     const uint32_t bit = 1u << (h & 31);
                     const uint32_t old = atomicOr(p.buf0 + (h >> 5), bit);
                     if (!(old & bit)) {
@@ -1387,6 +1390,9 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
             }
         }
         grid.sync();
+        // this level's first atom for this warp, loaded together with the level's count
+        // (unused if past it: the next level may be appending there already)
+        a_first = (int64_t)qe + gwarp < p.n_order_cap ? __ldcg(p.order + qe + gwarp) : 0;
         const int32_t t = qe + __ldcg(p.pcnt + k % 3);   // (a per-level slot, see lm_full_kernel)
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (t == qe || k + 1 >= p.max_passes || k + 1 == p.user_cap) {
