@@ -114,6 +114,11 @@ typedef struct {
                                body entries; programs whose bodies average more than
                                32 atoms start with STREAM passes).  Same results.    */
 #define LP_FULL_LEAD 0x8u   /* full θ-pass: LEAD passes only (never switch)          */
+#define LP_FULL_NO_PIPE 0x10u /* full θ-pass, key-space LEAD passes: do not pipeline
+                               (default: pass k+1's lead stream, filtered by v_k,
+                               runs while pass k's rows are verified; the rows whose
+                               lead atom became true in pass k are added from the
+                               lead-occurrence lists).  Same results.               */
 
 typedef struct {
     void *stream;            /* cudaStream_t (NULL = legacy default stream)          */

@@ -74,6 +74,7 @@ struct lp_program {
     uint32_t *d_factbits = nullptr, *d_init_bits = nullptr;
     int32_t *d_init_list = nullptr, *d_init_klist = nullptr;
     uint32_t *d_init_ksum = nullptr;
+    int32_t *d_locc_ptr = nullptr, *d_locc_slot = nullptr;
     int32_t n_init = 0;
     uint64_t lm_runs = 0;
     int32_t *d_facts = nullptr;
@@ -338,6 +339,24 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
             p->d_lead_codes = c;
             p->d_octet_tag = t;
         }
+        {   // lead-occurrence lists (pipelined LEAD passes): slots by body position 0
+            std::vector<int32_t> lp((size_t)L.n_ext + 1, 0), ls;
+            for (const Segment &sg : L.segs)
+                for (int64_t i = 0; i < sg.count_pad; ++i) {
+                    const int32_t a = L.col[(size_t)(sg.col_off + i)];
+                    if (a != L.bot && a >= 0 && a < L.n_ext) lp[(size_t)a + 1]++;
+                }
+            for (int32_t a = 0; a < L.n_ext; ++a) lp[(size_t)a + 1] += lp[(size_t)a];
+            ls.assign((size_t)std::max<int32_t>(lp[(size_t)L.n_ext], 1), 0);
+            std::vector<int32_t> fo(lp.begin(), lp.end() - 1);
+            for (const Segment &sg : L.segs)
+                for (int64_t i = 0; i < sg.count_pad; ++i) {
+                    const int32_t a = L.col[(size_t)(sg.col_off + i)];
+                    if (a != L.bot && a >= 0 && a < L.n_ext) ls[(size_t)fo[(size_t)a]++] = (int32_t)(sg.slot_off + i);
+                }
+            TRY(upload(p, &p->d_locc_ptr, lp));
+            TRY(upload(p, &p->d_locc_slot, ls));
+        }
         TRY(upload(p, &p->d_key_of, key));
         std::vector<int32_t> kl;
         for (int32_t a : L.facts) kl.push_back(key[(size_t)a]);
@@ -488,7 +507,9 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         cap = std::max<int64_t>(cap, 4 * (int64_t)kStreamWarps * 32 * (((L.n_slots >> 2) + sth - 1) / sth));
         if (cap + 8 > (1 << 28)) return set_err(LP_E_NOMEM, "candidate queue too large");
         p->qcap = (int32_t)std::max<int64_t>(cap + 8, 1024);
-        TRY(dalloc(p, &p->d_qbuf, (size_t)p->lm_blocks * p->qcap));
+        // (two queues per CTA when LEAD passes are pipelined: pass k+1's candidates are
+        // streamed while pass k's are verified)
+        TRY(dalloc(p, &p->d_qbuf, (size_t)p->lm_blocks * p->qcap * (p->d_locc_ptr ? 2 : 1)));
     }
     p->fr_blocks = cap_grid(sms * bf);
     p->st_blocks = cap_grid(sms * bs);
@@ -708,6 +729,10 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.cand = p->d_scal + 12;
     q.vent = p->d_vent;
     q.overlap = std::getenv("LP_NO_OVERLAP") ? 0 : 1;
+    const bool pipe = q.overlap && !(flags & LP_FULL_NO_PIPE) && !std::getenv("LP_NO_PIPE");
+    q.locc_ptr = pipe ? p->d_locc_ptr : nullptr;
+    q.locc_slot = p->d_locc_slot;
+    q.pbar = reinterpret_cast<uint32_t *>(p->d_scal + 24);
     {
         long long ent = 0;
         for (const Segment &sg : L.segs) ent += (long long)sg.L * sg.count_pad;

@@ -200,6 +200,7 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
         *p.tail_next = 0;
         *p.status_next = 0;
         p.pcnt[0] = p.pcnt[1] = p.pcnt[2] = 0;
+        if (p.pbar) *p.pbar = 0u;
     }
     const bool keys = summary_mode && p.lead_codes;
     const bool osum = summary_mode && !(keys && starts_lead(p));
@@ -791,6 +792,276 @@ __device__ __forceinline__ void add_to_shared(const LMParams &p, uint32_t *sm, u
     }
 }
 
+// ------------------------------------------------------------------------------------
+// least model: pipelined key-space LEAD passes
+// ------------------------------------------------------------------------------------
+//
+// A LEAD pass's stream only needs the key summary, and the rows it finds with the
+// summary of v_k are the rows with a true lead atom in v_{k+1} minus those whose lead
+// atom became true in pass k.  Those few are listed by the lead-occurrence lists
+// (locc: rows by body position 0).  So pass k+1's stream, filtered by v_k, runs while
+// pass k's candidates are verified, and the barrier that closes pass k waits behind it:
+//
+//   phase k (after the barrier of pass k-1 and the delta Δ_{k-1} folded into the summary
+//   of v_k):  28 warps stream the lead plane against summary(v_k) -> queue S_{k+1};
+//              4 warps verify S_k ∪ locc(Δ_{k-1}) against v_k (body ⊆ v_k, head emitted
+//              into v_{k+1}), arrive at the split barrier of pass k and wait for it;
+//   then Δ_k is folded into the summary (v_{k+1}) and phase k+1 starts.
+//
+// Candidates are tested exactly (verify_slot), so the result is θ(M v_k) as in the
+// unpipelined pass; S_1 = S_0 (both are the rows passing summary(v_0)).  The stream of
+// the phase whose pass turns out to be the last one is abandoned when its barrier
+// opens.  Queues: two per CTA (384 shared-memory entries + qcap global each), S_j in
+// half h(j) = (j + 1) & 1 for j >= 1, S_0 in half 0.
+constexpr int kPipeSq = kSmemQueue / 2;
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *a) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ int32_t pipe_qget(const int32_t *sq, const int32_t *gq, int32_t i) {
+    return i < kPipeSq ? sq[i] : __ldcg(gq + (i - kPipeSq));
+}
+
+template <int U, int KB>
+__device__ __forceinline__ void pipe_stream_kb(const LMParams &p, const uint32_t *sm, const uint32_t *bmask,
+                                               int32_t *sq, int32_t *gq, int32_t *qcnt,
+                                               const volatile int32_t *abandon, int64_t gtid,
+                                               int64_t gthreads) {
+    using T = OctT<KB>;
+    const int32_t no = (int32_t)(p.n_slots >> 3);
+    const int32_t gth = (int32_t)gthreads;
+    for (int32_t q0 = (int32_t)gtid; q0 < no; q0 += gth * U) {
+        if (*abandon) break;
+        typename T::vec v[U];
+        uint32_t tag[U];
+        oct_load<U, KB>(p, q0, gth, v, tag);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t q = q0 + u * gth;
+            if (q >= no) break;
+            const uint32_t b = tag[u] & T::bmask;
+            if (!bucket_any(bmask, b)) continue;
+            const uint32_t hi = b << KB;
+            unsigned fire = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) fire |= (unsigned)sm_bit(sm, hi | T::code(v[u], e)) << e;
+            fire &= 0xFFu >> (tag[u] >> T::pshift);
+            if (fire) {
+                int32_t pos = atomicAdd(qcnt, __popc(fire));
+                if (pos + __popc(fire) > p.qcap + kPipeSq) atomicExch(p.status_out, 2);
+                const int32_t s0 = q * 8;
+                for (unsigned f = fire; f; f &= f - 1, ++pos) {
+                    if (pos < kPipeSq) sq[pos] = s0 + __ffs(f) - 1;
+                    else if (pos - kPipeSq < p.qcap) gq[pos - kPipeSq] = s0 + __ffs(f) - 1;
+                }
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void pipe_stream(const LMParams &p, const uint32_t *sm, const uint32_t *bmask,
+                                            int32_t *sq, int32_t *gq, int32_t *qcnt,
+                                            const volatile int32_t *abandon, int64_t gtid, int64_t gthreads) {
+    if (p.key_bits == 8) pipe_stream_kb<LP_OCT_U, 8>(p, sm, bmask, sq, gq, qcnt, abandon, gtid, gthreads);
+    else pipe_stream_kb<4, 16>(p, sm, bmask, sq, gq, qcnt, abandon, gtid, gthreads);
+}
+
+struct PipeExit {
+    int k;            // last pass run
+    int32_t ds, de;   // its appends [ds, de) (the old loop resumes at pass k + 1)
+    int done;         // 1: fixpoint (or cap) reached, model written
+};
+
+// Runs key-space LEAD passes from pass 0 until the fixpoint (returns done = 1 after the
+// epilogue) or until the auto schedule asks for STREAM passes (returns the state the
+// unpipelined loop resumes from).  All threads of the CTA call it; the shared key
+// summary of v_0 is already built.
+__device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32_t *bmask,
+                                         const Segment *segs, int32_t *squeue, int32_t n0,
+                                         long long clk0, unsigned long long ns0) {
+    __shared__ int32_t qcnt[2];
+    __shared__ int32_t abandon;
+    __shared__ int32_t s_t, s_queued;
+    __shared__ unsigned long long s_vq, s_loaded;
+    __shared__ int32_t s_nl;
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    const bool lead = blockIdx.x == 0 && tid == 0;
+    const int vbase = kStreamWarps * 32;
+    const int nvt = (int)blockDim.x - vbase;             // verifier threads
+    const bool verifier = tid >= vbase;
+    const int vtid = tid - vbase;
+    int32_t *gq[2] = {p.qbuf + (int64_t)blockIdx.x * p.qcap,
+                      p.qbuf + ((int64_t)gridDim.x + blockIdx.x) * p.qcap};
+    int32_t *sq[2] = {squeue, squeue + kPipeSq};
+#define PDBG(k, i) p.dbg[((k) * gridDim.x + blockIdx.x) * 8 + (i)]
+    if (tid == 0) {
+        qcnt[0] = qcnt[1] = 0;
+        abandon = 0;
+        s_loaded = 0;
+        s_nl = 0;
+    }
+    __syncthreads();
+    // ---- pass 0: S_0 streamed by all threads, then verified by all threads
+    if (p.dbg && tid == 0) PDBG(0, 0) = PDBG(0, 1) = globaltimer();
+    if (lead) {
+        p.cand[1] = 0;
+        p.vent[1] = 0;
+        p.pcnt[1] = 0;
+    }
+    pipe_stream(p, sm, bmask, sq[0], gq[0], &qcnt[0], &abandon, gtid, gthreads);
+    __syncthreads();
+    if (p.dbg && tid == 0) PDBG(0, 2) = globaltimer();
+    {
+        const PassCtx c{p.buf0, p.buf1, sm, nullptr, nullptr, 0, bmask, segs, nullptr, p.pcnt, n0};
+        const int32_t nc = min(qcnt[0], p.qcap + kPipeSq);
+        int loaded = 0;
+        for (int32_t i = tid; i < nc; i += blockDim.x) loaded += verify_slot<false>(p, c, pipe_qget(sq[0], gq[0], i), 0);
+        for (int o = 16; o; o >>= 1) loaded += __shfl_xor_sync(0xFFFFFFFFu, loaded, o);
+        if (lane == 0 && loaded) atomicAdd(&s_loaded, (unsigned long long)loaded);
+        __syncthreads();
+        if (tid == 0) {
+            if (nc) atomicAdd(p.cand + 0, nc);
+            if (s_loaded) {
+                atomicAdd(p.vent + 0, s_loaded);
+                if (p.stats) atomicAdd(p.stats + 3, s_loaded);
+            }
+            s_loaded = 0;
+        }
+        if (p.dbg && tid == 0) PDBG(0, 3) = PDBG(0, 4) = globaltimer();
+    }
+    grid.sync();
+    if (p.dbg && tid == 0) PDBG(0, 5) = globaltimer();
+    int32_t t = n0 + __ldcg(p.pcnt + 0);
+    int32_t queued = __ldcg(p.cand + 0);
+    unsigned long long vq = __ldcg(p.vent + 0);
+    int32_t ds = n0, de = n0;
+    for (int k = 0;; ++k) {
+        // ---- pass k is complete: [de, t) are its appends
+        const uint32_t *wr_k = (k & 1) ? p.buf0 : p.buf1;
+        if (lead && p.stats) {
+            atomicAdd(p.stats + 0, (unsigned long long)p.lead_bytes + 4ull * (unsigned long long)queued +
+                                       12ull * (unsigned long long)(t - de));
+            p.stats[1] += 1;
+            p.stats[2] += (unsigned long long)queued;
+        }
+        if (t == de || k + 1 >= p.max_passes || k + 1 == p.user_cap) {
+            if (lead) {
+                *p.iters_out = k + 1;
+                if (t != de) atomicMax(p.status_out, k + 1 == p.user_cap ? 3 : 1);
+                if (p.stats) {
+                    atomicAdd(p.stats + 0, 4ull * p.stats[3]);
+                    p.stats[4] = (unsigned long long)(clock64() - clk0);
+                    p.stats[5] = globaltimer() - ns0;
+                }
+            }
+            if (p.dbg && tid == 0) p.dbg[(gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
+            lm_extract(p, gtid, gthreads, wr_k);
+            if (p.dbg) {
+                __syncthreads();
+                if (tid == 0) p.dbg[(gridDim.x + blockIdx.x) * 8 + 7] = globaltimer();
+            }
+            return PipeExit{k, de, t, 1};
+        }
+        if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
+        if (p.pass_mode == 0 &&
+            ((int64_t)queued * p.dense_div > p.n_slots || (long long)vq * 8 > p.stream_entries))
+            return PipeExit{k, de, t, 0};   // the auto schedule switches to STREAM passes
+        // ---- Δ_k into the key summary: summary(v_{k+1})
+        add_to_shared<false>(p, sm, bmask, de, t, true);
+        if (tid == 0) {
+            qcnt[(k + 1) & 1] = 0;   // (S_{k+1} half: verified in phase k, streamed into next)
+            abandon = 0;
+        }
+        __syncthreads();
+        ds = de;
+        de = t;
+        // ---- phase j = k + 1
+        const int j = k + 1;
+        if (p.dbg && tid == 0 && j < 16) PDBG(j, 0) = PDBG(j, 1) = globaltimer();
+        if (verifier) {
+            const uint32_t *rd = (j & 1) ? p.buf1 : p.buf0;
+            uint32_t *wr = (j & 1) ? p.buf0 : p.buf1;
+            if (blockIdx.x == 0 && vtid == 0) {
+                p.cand[(j + 1) % 3] = 0;
+                p.vent[(j + 1) % 3] = 0;
+                p.pcnt[(j + 1) % 3] = 0;
+            }
+            const PassCtx c{rd, wr, sm, nullptr, nullptr, j, bmask, segs, nullptr, p.pcnt + j % 3, de};
+            // wr still holds v_{j-1}: add Δ_{j-1} (spread over all CTAs)
+            for (int64_t i = ds + (int64_t)vtid * gridDim.x + blockIdx.x; i < de; i += (int64_t)gridDim.x * nvt) {
+                const int32_t a = __ldcg(p.order + i);
+                atomicOr(wr + (a >> 5), 1u << (a & 31));
+            }
+            const int h = (j + 1) & 1;
+            const int32_t nc = min(qcnt[h], p.qcap + kPipeSq);
+            int loaded = 0, nl = 0;
+            for (int32_t i = vtid; i < nc; i += nvt) loaded += verify_slot<false>(p, c, pipe_qget(sq[h], gq[h], i), 0);
+            // rows whose lead atom became true in pass j - 1 (a warp per atom)
+            const int nvw = nvt >> 5;
+            for (int64_t i = ds + (int64_t)blockIdx.x * nvw + (vtid >> 5); i < de; i += (int64_t)gridDim.x * nvw) {
+                const int32_t a = __ldcg(p.order + i);
+                const int32_t o0 = __ldg(p.locc_ptr + a), o1 = __ldg(p.locc_ptr + a + 1);
+                for (int32_t o = o0 + lane; o < o1; o += 32) {
+                    loaded += verify_slot<false>(p, c, __ldg(p.locc_slot + o), 0);
+                    ++nl;
+                }
+            }
+            for (int o = 16; o; o >>= 1) {
+                loaded += __shfl_xor_sync(0xFFFFFFFFu, loaded, o);
+                nl += __shfl_xor_sync(0xFFFFFFFFu, nl, o);
+            }
+            if (lane == 0) {
+                if (loaded) atomicAdd(&s_loaded, (unsigned long long)loaded);
+                if (nl) atomicAdd(&s_nl, nl);
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(nvt) : "memory");   // the verifier warps
+            if (vtid == 0) {
+                if (nc + s_nl) atomicAdd(p.cand + j % 3, nc + s_nl);
+                if (s_loaded) {
+                    atomicAdd(p.vent + j % 3, s_loaded);
+                    if (p.stats) atomicAdd(p.stats + 3, s_loaded);
+                }
+                s_loaded = 0;
+                s_nl = 0;
+                if (p.dbg && j < 16) PDBG(j, 3) = PDBG(j, 4) = globaltimer();
+                __threadfence();
+                atomicAdd(p.pbar, 1u);                                   // arrive (pass j)
+                const uint32_t target = (uint32_t)j * gridDim.x;
+                while (ld_acquire_u32(p.pbar) < target) {}
+                if (p.dbg && j < 16) PDBG(j, 5) = globaltimer();
+                const int32_t tj = de + __ldcg(p.pcnt + j % 3);
+                const int32_t qj = __ldcg(p.cand + j % 3);
+                const unsigned long long vj = __ldcg(p.vent + j % 3);
+                s_t = tj;
+                s_queued = qj;
+                s_vq = vj;
+                if (tj == de || j + 1 >= p.max_passes || j + 1 == p.user_cap ||
+                    (p.pass_mode == 0 && ((int64_t)qj * p.dense_div > p.n_slots || (long long)vj * 8 > p.stream_entries)))
+                    abandon = 1;   // the stream running now will not be used
+            }
+        } else {
+            // pass j+1's candidates: rows whose lead key is in summary(v_j)
+            const int64_t sgtid = (int64_t)blockIdx.x * vbase + tid;
+            pipe_stream(p, sm, bmask, sq[j & 1], gq[j & 1], &qcnt[j & 1], &abandon, sgtid,
+                        (int64_t)gridDim.x * vbase);
+            if (p.dbg && j < 16 && lane == 0) atomicMax(&PDBG(j, 2), globaltimer());
+        }
+        __syncthreads();
+        t = s_t;
+        queued = s_queued;
+        vq = s_vq;
+        k = j - 1;   // (the loop's ++k makes it j)
+    }
+#undef PDBG
+}
+
 // One cooperative launch = the whole fixpoint loop of Algorithm 1:
 // pass k reads v_k (rd) and writes v_{k+1} (wr); the loop ends after the first pass
 // that derives nothing (u = v), and iters = k + 1 counts that pass too.
@@ -864,9 +1135,23 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 7] = globaltimer();
 
     int32_t ds = n0, de = n0;  // atoms that became true in the previous pass
+    int k_start = 0;
+    if (!EXACT && keys && p.locc_ptr) {   // pipelined key-space LEAD passes
+        const PipeExit e = lm_pipe(p, sm, bmask, p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, n0,
+                                   lead ? clk0 : 0, lead ? ns0 : 0);
+        if (e.done) return;
+        // the auto schedule switched: STREAM passes from pass e.k + 1 on (the summary is
+        // rebuilt in atom-id space from v_{e.k+1})
+        k_start = e.k + 1;
+        ds = e.ds;
+        de = e.de;
+        lead_pass = false;
+        keys = false;
+        rebuild = true;
+    }
     constexpr int kSpec = 4;
     uint32_t spec[kSpec];      // the next delta's first list entries, loaded with its count
-    for (int k = 0;; ++k) {
+    for (int k = k_start;; ++k) {
         const uint32_t *rd = (k & 1) ? p.buf1 : p.buf0;
         uint32_t *wr = (k & 1) ? p.buf0 : p.buf1;
 #define DBG_STAMP(i) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + (i)]

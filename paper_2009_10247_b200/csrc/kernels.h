@@ -110,6 +110,11 @@ struct LMParams {
     long long stream_entries;  // body entries (incl. padding) one STREAM pass reads
     int32_t auto_stream_first; // auto schedule starts with STREAM passes (long bodies)
     int32_t overlap;           // LEAD passes verify while they stream (warp-specialised)
+    // pipelined key-mode LEAD passes (lm_pipe): rows by lead atom, and the counter of the
+    // split grid barrier; locc_ptr == NULL = not pipelined
+    const int32_t *locc_ptr;   // [n_ext + 1]
+    const int32_t *locc_slot;  // [rows]: the slots whose body position 0 is atom a
+    uint32_t *pbar;
     int32_t *pcnt;             // [3] atoms appended to the derivation list per pass (slot
                                //     k % 3): read by every CTA after the pass's barrier,
                                //     never written again before the next one

@@ -29,6 +29,7 @@ LP_PTR_DEVICE = 0x1
 LP_FRONTIER = 0x2
 LP_FULL_STREAM = 0x4
 LP_FULL_LEAD = 0x8
+LP_FULL_NO_PIPE = 0x10
 
 _P = ctypes.c_void_p
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
@@ -226,7 +227,7 @@ class Program:
 
     def least_model(self, v0=None, frontier: bool = False, popcounts: bool = False,
                     stages: bool = False, stream=None, schedule: str = "auto", stats: bool = False,
-                    max_passes: int = 0):
+                    max_passes: int = 0, pipeline: bool = True):
         """Host-buffer call.  v0: None, a bool mask [n], or an id list.  Returns
         (model uint64[ceil(n/64)], iters, dict(popcounts=..., stage=...))."""
         n = self.n_atoms
@@ -246,7 +247,7 @@ class Program:
         conv = ctypes.c_int32(-1)
         iters = lp_least_model(self, v0w, model, frontier=frontier, pops=pops, stage=stage,
                                stream=stream, schedule=schedule, stats=st, max_passes=max_passes,
-                               converged=conv)
+                               converged=conv, pipeline=pipeline)
         extra = {"converged": bool(conv.value)}
         if stats:
             extra["stats"] = dict(zip(("bytes", "lead_passes", "rows_verified", "entries_verified",
@@ -355,12 +356,13 @@ def _run(stream=None, flags=0, pops=None, stage=None, ev_begin=None, ev_end=None
 
 def lp_least_model(p: Program, v0, model_out, frontier=False, pops=None, stage=None, stream=None,
                    device_ptrs=False, iters_out=None, ev_begin=None, ev_end=None, schedule="auto",
-                   stats=None, max_passes=0, converged=None):
+                   stats=None, max_passes=0, converged=None, pipeline=True):
     """Marshals lp_least_model.  Host mode (default): numpy buffers, returns iters.
     device_ptrs=True: torch CUDA tensors (v0 int64 words or None, model_out int64
     words, iters_out int32[1], optional pops/stage), asynchronous on ``stream``."""
     flags = (LP_FRONTIER if frontier else 0) | (LP_PTR_DEVICE if device_ptrs else 0)
     flags |= {"auto": 0, "stream": LP_FULL_STREAM, "lead": LP_FULL_LEAD}[schedule]
+    flags |= 0 if pipeline else LP_FULL_NO_PIPE
     run = _run(stream, flags, pops, stage, ev_begin, ev_end, stats)
     run.max_passes = int(max_passes)
     if converged is not None and not device_ptrs:

@@ -32,15 +32,18 @@ def check_lm(P, v0=None, prog=None, variants=(False, True), jacobi=False,
         assert conv and jit == oit and jpops == opops and (oracle.pack_bits(jm) == om).all()
     prog = prog or lp.Program(P, **kw)
     runs = []
+    keyspace = prog.info["truth_mode"] == 1 and prog.info["key_shift"] >= 0
     for frontier in variants:
         if frontier or prog.info["full_kernel"] == 1:
-            runs.append((frontier, "auto"))
+            runs.append((frontier, "auto", True))
         else:   # every schedule of the full θ-pass (LEAD / STREAM passes) must agree
-            runs += [(False, s) for s in schedules]
-    for frontier, schedule in runs:
+            runs += [(False, s, True) for s in schedules]
+            if keyspace:   # key-space LEAD passes pipelined (default) and not
+                runs += [(False, s, False) for s in schedules if s != "stream"]
+    for frontier, schedule, pipeline in runs:
         model, iters, ex = prog.least_model(v0, frontier=frontier, popcounts=True, stages=True,
-                                            schedule=schedule, stats=True)
-        tag = "frontier" if frontier else f"full/{schedule}"
+                                            schedule=schedule, stats=True, pipeline=pipeline)
+        tag = "frontier" if frontier else f"full/{schedule}" + ("" if pipeline else "/nopipe")
         st = ex["stats"]
         if frontier or prog.info["full_kernel"] == 1:
             assert st["bytes"] == 0
@@ -130,8 +133,9 @@ def test_auto_schedule_switches_mid_fixpoint(seed, cfg, monkeypatch):
     n = int(rng.integers(2000, 5000))
     P = lpgen.random_program(rng, n, 5 * n, max_len=5, n_facts=n // 10)
     prog = lp.Program(P, **cfg)
-    _, iters, ex = prog.least_model(schedule="auto", stats=True)
-    assert 1 <= ex["stats"]["lead_passes"] < iters
+    for pipeline in (True, False):   # (key space: the pipelined passes hand over too)
+        _, iters, ex = prog.least_model(schedule="auto", stats=True, pipeline=pipeline)
+        assert 1 <= ex["stats"]["lead_passes"] < iters
     check_lm(P, prog=prog, schedules=("auto",))
 
 
@@ -463,6 +467,51 @@ def test_max_passes_cap():
             assert ex["converged"] == (p_ >= 50)
             bits = lp.unpack_bits(model, 50)
             assert bits.sum() == min(p_ + 1, 50)
+
+
+@pytest.mark.parametrize("pipeline", [True, False])
+def test_max_passes_cap_key_space(pipeline):
+    """The cap in key-space LEAD passes (pipelined or not): the model after p passes of
+    a chain holds the first p + 1 atoms, stages and the popcount trace up to the cap."""
+    n = 3000
+    P = lpgen.chain(n)
+    prog = lp.Program(P, smem_bits_cap=128)
+    assert prog.info["truth_mode"] == 1 and prog.info["key_shift"] >= 0
+    for p_ in (1, 2, 3, 17, n - 1, n, n + 5):
+        model, iters, ex = prog.least_model(max_passes=p_, schedule="lead", pipeline=pipeline,
+                                            popcounts=True)
+        assert iters == min(p_, n)
+        assert ex["converged"] == (p_ >= n)
+        assert lp.unpack_bits(model, n).sum() == min(p_ + 1, n)
+        assert ex["popcounts"] == list(range(1, min(p_, n) + 1))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_pipelined_lead_passes_hub_leads(seed):
+    """Pipelined key-space LEAD passes on programs where a few atoms lead many rows
+    (long lead-occurrence lists, many rows added per pass through them), with start
+    sets, one CTA and several."""
+    rng = np.random.default_rng([seed, 777])
+    n = int(rng.integers(3000, 8000))
+    m = 6 * n
+    hubs = rng.choice(n, size=8, replace=False)
+    head = rng.integers(0, n, size=m).astype(np.int32)
+    lens = rng.integers(1, 5, size=m)
+    ptr = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    body = rng.integers(0, n, size=int(ptr[-1])).astype(np.int32)
+    hub_rows = rng.random(m) < 0.3
+    body[ptr[:-1][hub_rows]] = rng.choice(hubs, size=int(hub_rows.sum()))
+    rows = [(int(head[r]), sorted(set(body[ptr[r]:ptr[r + 1]].tolist()) - {int(head[r])}))
+            for r in range(m)]
+    rows = [(h, b) for h, b in rows if b]
+    facts = rng.choice(n, size=n // 25, replace=False)
+    rows += [(int(a), []) for a in facts]
+    P = lpgen.from_lists(n, rows)
+    for cfg in (dict(smem_bits_cap=128), dict(smem_bits_cap=256, grid_blocks=2),
+                dict(smem_bits_cap=128, key8=True, grid_blocks=7)):
+        prog = check_lm(P, variants=(False,), **cfg)
+        check_lm(P, v0=rng.choice(n, size=n // 10, replace=False).tolist(), prog=prog, variants=(False,))
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 5])
