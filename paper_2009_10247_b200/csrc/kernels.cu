@@ -974,7 +974,7 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
             ((int64_t)queued * p.dense_div > p.n_slots || (long long)vq * 8 > p.stream_entries))
             return PipeExit{k, de, t, 0};   // the auto schedule switches to STREAM passes
         // ---- Δ_k into the key summary: summary(v_{k+1})
-        add_to_shared<false>(p, sm, bmask, de, t, true);
+        if (k == 0) add_to_shared<false>(p, sm, bmask, de, t, true);   // (later: in the phase)
         if (tid == 0) {
             qcnt[(k + 1) & 1] = 0;   // (S_{k+1} half: verified in phase k, streamed into next)
             abandon = 0;
@@ -984,28 +984,29 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         de = t;
         // ---- phase j = k + 1
         const int j = k + 1;
-        if (p.dbg && tid == 0 && j < 16) PDBG(j, 0) = PDBG(j, 1) = globaltimer();
-        if (verifier) {
-            const uint32_t *rd = (j & 1) ? p.buf1 : p.buf0;
-            uint32_t *wr = (j & 1) ? p.buf0 : p.buf1;
-            if (blockIdx.x == 0 && vtid == 0) {
-                p.cand[(j + 1) % 3] = 0;
-                p.vent[(j + 1) % 3] = 0;
-                p.pcnt[(j + 1) % 3] = 0;
-            }
-            const PassCtx c{rd, wr, sm, nullptr, nullptr, j, bmask, segs, nullptr, p.pcnt + j % 3, de};
+        if (p.dbg && tid == 0 && j < 16) PDBG(j, 0) = globaltimer();
+        const uint32_t *rd = (j & 1) ? p.buf1 : p.buf0;
+        uint32_t *wr = (j & 1) ? p.buf0 : p.buf1;
+        if (blockIdx.x == 0 && tid == 0) {
+            p.cand[(j + 1) % 3] = 0;
+            p.vent[(j + 1) % 3] = 0;
+            p.pcnt[(j + 1) % 3] = 0;
+        }
+        const PassCtx c{rd, wr, sm, nullptr, nullptr, j, bmask, segs, nullptr, p.pcnt + j % 3, de};
+        const int h = (j + 1) & 1;
+        const int32_t nc = min(qcnt[h], p.qcap + kPipeSq);
+        // pass j's verification by nt of the CTA's threads (ti = index among them)
+        auto verify_pass = [&](int ti, int nt) {
             // wr still holds v_{j-1}: add Δ_{j-1} (spread over all CTAs)
-            for (int64_t i = ds + (int64_t)vtid * gridDim.x + blockIdx.x; i < de; i += (int64_t)gridDim.x * nvt) {
+            for (int64_t i = ds + (int64_t)ti * gridDim.x + blockIdx.x; i < de; i += (int64_t)gridDim.x * nt) {
                 const int32_t a = __ldcg(p.order + i);
                 atomicOr(wr + (a >> 5), 1u << (a & 31));
             }
-            const int h = (j + 1) & 1;
-            const int32_t nc = min(qcnt[h], p.qcap + kPipeSq);
             int loaded = 0, nl = 0;
-            for (int32_t i = vtid; i < nc; i += nvt) loaded += verify_slot<false>(p, c, pipe_qget(sq[h], gq[h], i), 0);
+            for (int32_t i = ti; i < nc; i += nt) loaded += verify_slot<false>(p, c, pipe_qget(sq[h], gq[h], i), 0);
             // rows whose lead atom became true in pass j - 1 (a warp per atom)
-            const int nvw = nvt >> 5;
-            for (int64_t i = ds + (int64_t)blockIdx.x * nvw + (vtid >> 5); i < de; i += (int64_t)gridDim.x * nvw) {
+            const int nw = nt >> 5;
+            for (int64_t i = ds + (int64_t)blockIdx.x * nw + (ti >> 5); i < de; i += (int64_t)gridDim.x * nw) {
                 const int32_t a = __ldcg(p.order + i);
                 const int32_t o0 = __ldg(p.locc_ptr + a), o1 = __ldg(p.locc_ptr + a + 1);
                 for (int32_t o = o0 + lane; o < o1; o += 32) {
@@ -1021,6 +1022,16 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
                 if (loaded) atomicAdd(&s_loaded, (unsigned long long)loaded);
                 if (nl) atomicAdd(&s_nl, nl);
             }
+        };
+        // pass 1 verifies S_1 = S_0 (pass 0's whole candidate set again) with every thread
+        // before its stream starts; later passes' sets are verified by the verifier warps
+        // beside the stream
+        if (j == 1) {
+            verify_pass(tid, blockDim.x);
+            __syncthreads();
+        }
+        if (verifier) {
+            if (j != 1) verify_pass(vtid, nvt);
             asm volatile("bar.sync 1, %0;" ::"r"(nvt) : "memory");   // the verifier warps
             if (vtid == 0) {
                 if (nc + s_nl) atomicAdd(p.cand + j % 3, nc + s_nl);
@@ -1028,9 +1039,13 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
                     atomicAdd(p.vent + j % 3, s_loaded);
                     if (p.stats) atomicAdd(p.stats + 3, s_loaded);
                 }
+                if (p.dbg && j < 16) PDBG(j, 3) = PDBG(j, 4) = globaltimer();
+                if (p.dbg && j >= 3 && j < 16) {   // (slots 6, 7: this CTA's S_j and locc rows)
+                    PDBG(j, 6) = (unsigned long long)nc;
+                    PDBG(j, 7) = (unsigned long long)s_nl;
+                }
                 s_loaded = 0;
                 s_nl = 0;
-                if (p.dbg && j < 16) PDBG(j, 3) = PDBG(j, 4) = globaltimer();
                 __threadfence();
                 atomicAdd(p.pbar, 1u);                                   // arrive (pass j)
                 const uint32_t target = (uint32_t)j * gridDim.x;
@@ -1046,6 +1061,30 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
                     (p.pass_mode == 0 && ((int64_t)qj * p.dense_div > p.n_slots || (long long)vj * 8 > p.stream_entries)))
                     abandon = 1;   // the stream running now will not be used
             }
+            // Δ_j into the key summary right away, while S_{j+1} is still being streamed
+            // against it: a row the stream then queues for a lead atom of Δ_j is also
+            // reached through locc(Δ_j) -- verified twice, same result -- and the summary
+            // stays a superset of summary(v_j), so S_{j+1} misses nothing
+            asm volatile("bar.sync 1, %0;" ::"r"(nvt) : "memory");
+            if (!*(volatile int32_t *)&abandon) {
+                const int32_t tj = *(volatile int32_t *)&s_t;
+                for (int32_t i0 = de + vtid; i0 < tj; i0 += 4 * nvt) {
+                    uint32_t a[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int32_t i = i0 + u * nvt;
+                        a[u] = i < tj ? (uint32_t)__ldcg(p.korder + i) : 0xFFFFFFFFu;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (a[u] != 0xFFFFFFFFu) {
+                            const uint32_t g = a[u] >> p.kshift;
+                            atomicOr(sm + (g >> 5), 1u << (g & 31));
+                            const uint32_t bk = g >> p.key_bits;
+                            atomicOr(bmask + (bk >> 5), 1u << (bk & 31));
+                        }
+                }
+            }
         } else {
             // pass j+1's candidates: rows whose lead key is in summary(v_j)
             const int64_t sgtid = (int64_t)blockIdx.x * vbase + tid;
@@ -1054,6 +1093,7 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
             if (p.dbg && j < 16 && lane == 0) atomicMax(&PDBG(j, 2), globaltimer());
         }
         __syncthreads();
+        if (p.dbg && tid == 0 && j < 16) PDBG(j, 1) = globaltimer();   // (phase over)
         t = s_t;
         queued = s_queued;
         vq = s_vq;

@@ -48,5 +48,15 @@ for k in range(min(it, 16)):
           f"stream done med/max {np.median(rel(2)):6.1f}/{rel(2).max():6.1f}  "
           f"verify done med/max {np.median(rel(3)):6.1f}/{rel(3).max():6.1f}  "
           f"cta done max {rel(4).max():6.1f}  barrier exit {rel(5).min():6.1f}..{rel(5).max():6.1f} us"
+          + (f"  [S_k rows med/max {np.median(t[k,:,6]):.0f}/{t[k,:,6].max():.0f}, lead-occ rows med/max {np.median(t[k,:,7]):.0f}/{t[k,:,7].max():.0f}]"
+             if k >= 3 and t[k, :, 6].max() < 1e9 else "")
           + (f"  [thread 0's delta share done med/max {np.median(rel(6)):5.1f}/{rel(6).max():5.1f}, sync {np.median(rel(7)):5.1f}/{rel(7).max():5.1f}]"
-             if k >= 3 else ""))
+             if k >= 3 and t[k, :, 6].max() >= 1e9 else ""))
+# per-CTA durations within each pass/phase (relative to that CTA's own pass start)
+print("per-CTA (own start = 0): stream / verify / barrier seen / next start, med|max us")
+for k in range(min(it, 16) - 1):
+    s0 = t[k, :, 0]
+    d = lambda i: (t[k, :, i] - s0) / 1e3  # noqa: E731
+    nxt = (t[k + 1, :, 0] - s0) / 1e3
+    print(f"pass {k:2d}: stream {np.median(d(2)):5.1f}|{d(2).max():5.1f}  verify {np.median(d(3)):5.1f}|{d(3).max():5.1f}"
+          f"  barrier {np.median(d(5)):5.1f}|{d(5).max():5.1f}  phase over {np.median(d(1)):5.1f}|{d(1).max():5.1f}  next start {np.median(nxt):5.1f}|{nxt.max():5.1f}")
