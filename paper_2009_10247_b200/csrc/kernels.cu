@@ -887,6 +887,7 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
     __shared__ int32_t s_t, s_queued;
     __shared__ unsigned long long s_vq, s_loaded;
     __shared__ int32_t s_nl;
+    __shared__ int32_t s_sdone;   // pass 0: streaming warps done
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -906,23 +907,52 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         abandon = 0;
         s_loaded = 0;
         s_nl = 0;
+        s_sdone = 0;
     }
+    for (int32_t i = tid; i < kPipeSq; i += blockDim.x) sq[0][i] = -1;   // (pass 0: not yet written)
     __syncthreads();
-    // ---- pass 0: S_0 streamed by all threads, then verified by all threads
+    // ---- pass 0: S_0 streamed by the streaming warps and verified by the verifier warps
+    // as it appears in the shared queue (-1 = reserved, not yet written); the global part
+    // of the queue is verified by all threads after the stream
     if (p.dbg && tid == 0) PDBG(0, 0) = PDBG(0, 1) = globaltimer();
     if (lead) {
         p.cand[1] = 0;
         p.vent[1] = 0;
         p.pcnt[1] = 0;
     }
-    pipe_stream(p, sm, bmask, sq[0], gq[0], &qcnt[0], &abandon, gtid, gthreads);
-    __syncthreads();
-    if (p.dbg && tid == 0) PDBG(0, 2) = globaltimer();
     {
         const PassCtx c{p.buf0, p.buf1, sm, nullptr, nullptr, 0, bmask, segs, nullptr, p.pcnt, n0};
-        const int32_t nc = min(qcnt[0], p.qcap + kPipeSq);
         int loaded = 0;
-        for (int32_t i = tid; i < nc; i += blockDim.x) loaded += verify_slot<false>(p, c, pipe_qget(sq[0], gq[0], i), 0);
+        if (!verifier) {
+            pipe_stream(p, sm, bmask, sq[0], gq[0], &qcnt[0], &abandon, (int64_t)blockIdx.x * vbase + tid,
+                        (int64_t)gridDim.x * vbase);
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                atomicAdd(&s_sdone, 1);
+            }
+        } else {
+            for (int32_t i = vtid; i < kPipeSq; i += nvt) {
+                bool have = false;
+                for (;;) {   // wait until entry i is reserved, or the stream is over
+                    if (i < *(volatile int32_t *)&qcnt[0]) { have = true; break; }
+                    if (*(volatile int32_t *)&s_sdone == kStreamWarps) {
+                        __threadfence_block();
+                        have = i < *(volatile int32_t *)&qcnt[0];
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+                if (!have) break;
+                int32_t s;
+                while ((s = *(volatile int32_t *)&sq[0][i]) < 0) __nanosleep(32);
+                loaded += verify_slot<false>(p, c, s, 0);
+            }
+        }
+        __syncthreads();
+        if (p.dbg && tid == 0) PDBG(0, 2) = globaltimer();
+        const int32_t nc = min(qcnt[0], p.qcap + kPipeSq);
+        for (int32_t i = kPipeSq + tid; i < nc; i += blockDim.x) loaded += verify_slot<false>(p, c, pipe_qget(sq[0], gq[0], i), 0);
         for (int o = 16; o; o >>= 1) loaded += __shfl_xor_sync(0xFFFFFFFFu, loaded, o);
         if (lane == 0 && loaded) atomicAdd(&s_loaded, (unsigned long long)loaded);
         __syncthreads();
