@@ -32,7 +32,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-KERNEL_REV = "lead16-octets-d2"   # bump when the dominant kernel's traffic changes
+KERNEL_REV = "lead16-octets-d2-pipe"   # bump when the dominant kernel's traffic changes
 METRIC = ("least-model fixpoint time & nnz·iter/s (HBM GB/s vs peak); "
           "stable-model guesses/s")
 
