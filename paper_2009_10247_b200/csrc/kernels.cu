@@ -113,25 +113,6 @@ __device__ __forceinline__ void bulk_g2s_plain(void *dst, const void *src, uint3
         "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
 }
 
-// Copy nw words (nw % 4 == 0, src 16-byte aligned) global -> shared with TMA bulk copies
-// completing on `bar` (single use, phase 0; all threads of the CTA call it and return
-// once the data has landed).
-__device__ __forceinline__ void smem_fill_bulk(uint32_t *sm, const uint32_t *src, int32_t nw, uint64_t *bar) {
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t bytes = (uint32_t)nw * 4u;
-        mbar_expect_tx(bar, bytes);
-        constexpr uint32_t kChunk = 32768;
-        for (uint32_t o = 0; o < bytes; o += kChunk)
-            bulk_g2s_plain(reinterpret_cast<char *>(sm) + o, reinterpret_cast<const char *>(src) + o,
-                           bytes - o < kChunk ? bytes - o : kChunk, bar);
-    }
-    __syncthreads();
-    mbar_wait(bar, 0);
-}
-
 __device__ __forceinline__ void smem_fill(uint32_t *sm, const uint32_t *src, int32_t nw) {
     const int4 *s4 = reinterpret_cast<const int4 *>(src);
     int4 *d4 = reinterpret_cast<int4 *>(sm);
@@ -1145,7 +1126,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t qcount;
     __shared__ unsigned long long loaded_cta;
-    __shared__ uint32_t bmask[kBucketWords];   // key mode: bucket b has a set summary bit
+    __shared__ __align__(16) uint32_t bmask[kBucketWords];   // key mode: bucket b has a set summary bit
     __shared__ Segment ssegs[kMaxSmemSegs];
     __shared__ int32_t squeue[kSmemQueue];
     __shared__ int32_t streamers_done;
@@ -1163,6 +1144,23 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         ns0 = globaltimer();
     }
 
+    bool lead_pass = starts_lead(p);
+    bool keys = !EXACT && p.lead_codes && lead_pass;         // shared copy is in key space
+    // v_0 = facts: the key summary and bucket mask images built at load are bulk-copied in
+    // while the prologue runs (waited for after its barrier)
+    const bool ksum_image = keys && !p.v0 && p.init_ksum;
+    if (ksum_image && tid == 0) {
+        mbar_init(&fill_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t bytes = (uint32_t)p.ksm_words * 4u, bb = kBucketWords * 4u;
+        mbar_expect_tx(&fill_bar, bytes + bb);
+        constexpr uint32_t kChunk = 32768;
+        for (uint32_t o = 0; o < bytes; o += kChunk)
+            bulk_g2s_plain(reinterpret_cast<char *>(sm) + o, reinterpret_cast<const char *>(p.init_ksum) + o,
+                           bytes - o < kChunk ? bytes - o : kChunk, &fill_bar);
+        bulk_g2s_plain(bmask, p.init_ksum + p.ksm_words, bb, &fill_bar);
+    }
     lm_prologue(p, !EXACT, gtid, gthreads);            // v_0 (row a3), in-kernel
     if (gtid == 0) {
         p.cand[0] = 0;
@@ -1174,18 +1172,15 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     }
     grid.sync();
     if (p.dbg && tid == 0) p.dbg[(2 * gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
-    bool lead_pass = starts_lead(p);
-    bool keys = !EXACT && p.lead_codes && lead_pass;         // shared copy is in key space
     bool rebuild = false;                                // key space -> atom-id summary
     const int32_t n0 = __ldcg(p.tail);
     {
-        for (int32_t w = tid; w < kBucketWords; w += blockDim.x) bmask[w] = 0u;
+        if (!ksum_image)
+            for (int32_t w = tid; w < kBucketWords; w += blockDim.x) bmask[w] = 0u;
         if (p.nseg <= kMaxSmemSegs)
             for (int32_t s = tid; s < p.nseg; s += blockDim.x) ssegs[s] = p.segs[s];
-        if (keys && !p.v0 && p.init_ksum) {   // v_0 = facts: key summary + bucket mask
-                                              // images built at load, copied in
-            smem_fill_bulk(sm, p.init_ksum, p.ksm_words, &fill_bar);
-            for (int32_t w = tid; w < kBucketWords; w += blockDim.x) bmask[w] = __ldg(p.init_ksum + p.ksm_words + w);
+        if (ksum_image) {
+            mbar_wait(&fill_bar, 0);
         } else if (keys) {   // key summary of v_0 straight from the initial list (bucket b =
                              // summary words [b << 11, (b + 1) << 11))
             int4 *s4 = reinterpret_cast<int4 *>(sm);
