@@ -1942,37 +1942,35 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
     // rows changed in pass k-1 and in pass k-2: counts, their lists in ring segments
     // (k-1) % 3 and (k-2) % 3 of p.order (pass k appends to segment k % 3)
     int32_t n1 = 0, n2 = 0;
+    constexpr int kStSpec = 2;
+    int32_t s1[kStSpec] = {-1, -1}, s2[kStSpec] = {-1, -1};   // this thread's first entries of both lists
     for (int k = 0;; ++k) {
         const unsigned long long *rd = (k & 1) ? p.T1 : p.T0;
         unsigned long long *wr = (k & 1) ? p.T0 : p.T1;
+        const int32_t *l1 = p.order + (int64_t)((k + 2) % 3) * p.ring_cap;   // changed in pass k-1
         if (k > 0) {
-            // rows changed in pass k-1: copy T_k's words into the other buffer (a warp per
-            // row) and mark the rows that are now true in every guess (global, read by
-            // every CTA one pass later)
-            const int32_t *l1 = p.order + (int64_t)((k + 2) % 3) * p.ring_cap;
             const int32_t *l2 = p.order + (int64_t)((k + 1) % 3) * p.ring_cap;
-            for (int64_t i = gwarp; i < n1; i += nwarps) {
-                const int32_t h = __ldcg(l1 + i);
-                bool all1 = true;
-                for (int32_t w = lane; w < p.Wp; w += 32) {
-                    const int64_t off = (int64_t)h * p.Wp + w;
-                    const unsigned long long v = __ldcg(rd + off);
-                    if (v != __ldcg(wr + off)) atomicOr(wr + off, v);
-                    const unsigned long long valid = valid_word(w, p.W, p.G);
-                    all1 = all1 && ((v & valid) == valid);
+            // (the first kStSpec x blockDim entries of both lists are in registers: loaded
+            // with the count after the barrier)
+            for (int u = 0; u < kStSpec; ++u)
+                if (s1[u] >= 0) {
+                    const uint32_t g = (uint32_t)s1[u] >> p.any_shift;
+                    atomicOr(sm + (g >> 5), 1u << (g & 31));
                 }
-                if (use_full && __all_sync(0xFFFFFFFFu, all1) && lane == 0)
-                    atomicOr(p.gfull + (h >> 5), 1u << (h & 31));
-            }
-            for (int64_t i = tid; i < n1; i += blockDim.x) {
+            for (int64_t i = tid + kStSpec * blockDim.x; i < n1; i += blockDim.x) {
                 const uint32_t g = (uint32_t)__ldcg(l1 + i) >> p.any_shift;
                 atomicOr(sm + (g >> 5), 1u << (g & 31));
             }
-            if (use_full)   // the full marks made during pass k-1 (rows changed in pass k-2)
-                for (int64_t i = tid; i < n2; i += blockDim.x) {
+            if (use_full) {   // the full marks made during pass k-1 (rows changed in pass k-2)
+                uint32_t fw[kStSpec];
+                for (int u = 0; u < kStSpec; ++u) fw[u] = s2[u] >= 0 ? __ldcg(p.gfull + (s2[u] >> 5)) : 0u;
+                for (int u = 0; u < kStSpec; ++u)
+                    if (s2[u] >= 0 && ((fw[u] >> (s2[u] & 31)) & 1u)) atomicOr(full + (s2[u] >> 5), 1u << (s2[u] & 31));
+                for (int64_t i = tid + kStSpec * blockDim.x; i < n2; i += blockDim.x) {
                     const uint32_t h = (uint32_t)__ldcg(l2 + i);
                     if ((__ldcg(p.gfull + (h >> 5)) >> (h & 31)) & 1u) atomicOr(full + (h >> 5), 1u << (h & 31));
                 }
+            }
             __syncthreads();
         }
         if (tid == 0) {
@@ -2096,13 +2094,39 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
                 }
             }
         }
+        if (k > 0) {
+            // rows changed in pass k-1: copy T_k's words into the other buffer (a warp per
+            // row; ORs commute with this pass's, so it only has to finish before the
+            // barrier) and mark the rows that are now true in every guess (global, read by
+            // every CTA one pass later)
+            for (int64_t i = gwarp; i < n1; i += nwarps) {
+                const int32_t h = __ldcg(l1 + i);
+                bool all1 = true;
+                for (int32_t w = lane; w < p.Wp; w += 32) {
+                    const int64_t off = (int64_t)h * p.Wp + w;
+                    const unsigned long long v = __ldcg(rd + off);
+                    if (v != __ldcg(wr + off)) atomicOr(wr + off, v);
+                    const unsigned long long valid = valid_word(w, p.W, p.G);
+                    all1 = all1 && ((v & valid) == valid);
+                }
+                if (use_full && __all_sync(0xFFFFFFFFu, all1) && lane == 0)
+                    atomicOr(p.gfull + (h >> 5), 1u << (h & 31));
+            }
+        }
         if (p.dbg && k < 64) {
             __syncthreads();
             if (tid == 0) atomicMax(p.dbg + 4 * k + 3, globaltimer());     // CTA's scan done
         }
         grid.sync();
         // rows changed in this pass: its own counter slot (the next pass appends to
-        // another one, so every CTA reads the same value after the barrier)
+        // another one, so every CTA reads the same value after the barrier); this
+        // thread's first entries of the list are loaded together with it (slots past the
+        // count hold stale entries of an earlier pass and are dropped)
+        int32_t nx[kStSpec];
+        for (int u = 0; u < kStSpec; ++u) {
+            const int64_t i = tid + (int64_t)u * blockDim.x;
+            nx[u] = i < p.ring_cap ? __ldcg(p.order + (int64_t)(k % 3) * p.ring_cap + i) : -1;
+        }
         const int32_t cnt = __ldcg(p.pcnt + k % 3);
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (p.dbg && lead && k < 64) p.dbg[4 * k] = globaltimer();   // profiling hook
@@ -2116,6 +2140,10 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
         }
         n2 = n1;
         n1 = cnt;
+        for (int u = 0; u < kStSpec; ++u) {
+            s2[u] = s1[u];
+            s1[u] = tid + u * (int)blockDim.x < cnt ? nx[u] : -1;
+        }
     }
 }
 
