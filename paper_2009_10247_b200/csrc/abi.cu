@@ -900,14 +900,31 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
     STParams s = st_params(p);
     if (dev) s.passes_out = passes_out;
     const bool full_clear = !(p->st_dirty_ok && p->st_last_Wp == Wp);
-    CK(launch_st_init(s, L.n, L.k, p->d_negated_ext, p->d_free_rank, guesses ? gd : nullptr, W, G,
-                      goff / 64, p->d_facts, p->nfacts, L.top, p->d_any, full_clear, st));
+    if (full_clear) {   // first call, or a new matrix layout: both buffers from zero
+        const size_t tbytes = (size_t)L.n_ext * Wp * sizeof(unsigned long long);
+        CK(cudaMemsetAsync(p->d_T0, 0, tbytes, st));
+        CK(cudaMemsetAsync(p->d_T1, 0, tbytes, st));
+    }
+    s.clear_rows = full_clear ? 0 : 1;   // else only the rows the previous call changed
+    s.n_atoms = L.n;
+    s.k = L.k;
+    s.negated = p->d_negated;
+    s.negated_ext = p->d_negated_ext;
+    s.free_rank = p->d_free_rank;
+    s.guesses = guesses ? gd : nullptr;
+    s.woff = goff / 64;
+    s.facts = p->d_facts;
+    s.nfacts = p->nfacts;
+    s.top = L.top;
+    s.any_rw = p->d_any;
+    s.accepted = acc;
+    s.n_accepted = nacc;
     p->st_dirty_ok = true;   // (stream order: the next call's clear runs after this one)
     p->st_last_Wp = Wp;
+    // ONE cooperative launch: clear, T_0, the fixpoint loop, the stability check
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
-    CK(launch_st_fixpoint(s, p->st_blocks, p->st_smem, st));
+    CK(launch_st_fused(s, p->st_blocks, p->st_smem, st));
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
-    CK(launch_st_check(s, L.n, L.k, p->d_negated, W, G, acc, nacc, st));
     p->stable_valid = true;
     if (dev) return LP_OK;
     int32_t scal[6] = {0, 0, 0, 0, 0, 0};

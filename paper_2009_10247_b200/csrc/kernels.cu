@@ -8,9 +8,10 @@
 //                      fixpoint                               (rows a4, a5; Alg. 1)
 //   lm_frontier_kernel level-synchronous semi-naive variant: only the rows whose
 //                      bodies contain newly-true atoms are touched   (row a6)
-//   st_init_kernel     bit-sliced initial matrix, 64 guesses per word (row a7; Def. 8)
-//   st_fixpoint_kernel batched θ-pass loop over the guess matrix    (row a8; Alg. 2)
-//   st_check_kernel    complementarity test a_j + abar_j = 1 per guess (row a9; Alg. 3)
+//   st_fixpoint_kernel one cooperative launch per stable call: bit-sliced initial
+//                      matrix, 64 guesses per word (row a7; Def. 8), the batched
+//                      θ-pass loop over it (row a8; Alg. 2) and the complementarity
+//                      test a_j + abar_j = 1 per guess (row a9; Alg. 3)
 //
 // See DESIGN.md for the layout, the roofline of each kernel and the readings of the
 // paper they implement.
@@ -1791,54 +1792,52 @@ __device__ __forceinline__ unsigned long long count_pattern(int i, int64_t w) {
 
 // Initial matrix M_0 (Def. 8): ⊤ and fact rows all ones (over the
 // valid guesses), abar rows from the guesses, every other row zero (memset before).
-__global__ void st_init_kernel(STParams p, int32_t n, int32_t k, const int32_t *negated_ext,
-                               const int32_t *free_rank, const unsigned long long *guesses,
-                               int32_t W, int64_t G, int64_t woff, const int32_t *facts,
-                               int32_t nfacts, int32_t top, uint32_t *any_bits) {
-    const int64_t rows = 1 + (int64_t)nfacts + k;
+__device__ void st_init_phase(const STParams &p, int64_t gtid, int64_t gthreads) {
+    const int64_t rows = 1 + (int64_t)p.nfacts + p.k;
     const int64_t total = rows * p.Wp;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
-         x += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t x = gtid; x < total; x += gthreads) {
         const int64_t r = x / p.Wp, w = x % p.Wp;
-        const unsigned long long valid = valid_word(w, W, G);
+        const unsigned long long valid = valid_word(w, p.W, p.G);
         int32_t row;
         unsigned long long v;
         if (r == 0) {
-            row = top;
+            row = p.top;
             v = valid;
-        } else if (r <= nfacts) {
-            row = facts[r - 1];
+        } else if (r <= p.nfacts) {
+            row = p.facts[r - 1];
             v = valid;
         } else {
-            const int32_t j = (int32_t)(r - 1 - nfacts);
-            row = negated_ext[j];
-            if (guesses) {
-                v = (w < W ? guesses[(int64_t)j * W + w] : 0ull) & valid;
+            const int32_t j = (int32_t)(r - 1 - p.nfacts);
+            row = p.negated_ext[j];
+            if (p.guesses) {
+                v = (w < p.W ? p.guesses[(int64_t)j * p.W + w] : 0ull) & valid;
             } else {
-                const int32_t rank = free_rank[j];
-                v = rank < 0 ? 0ull : (count_pattern(rank, w + woff) & valid);   // global word
+                const int32_t rank = p.free_rank[j];
+                v = rank < 0 ? 0ull : (count_pattern(rank, w + p.woff) & valid);   // global word
             }
         }
         p.T0[(int64_t)row * p.Wp + w] = v;
         p.T1[(int64_t)row * p.Wp + w] = v;
         if (v) {
             const uint32_t g = (uint32_t)row >> p.any_shift;
-            atomicOr(any_bits + (g >> 5), 1u << (g & 31));
+            atomicOr(p.any_rw + (g >> 5), 1u << (g & 31));
         }
     }
 }
 
 // Zero the matrix rows the previous stable call changed -- exactly the rows with a pass
-// tag in mark[] -- in both buffers; rows it did not change are still zero.  A warp per
-// row, lanes over its words.
-__global__ void st_clear_kernel(STParams p) {
+// tag in mark[] -- in both buffers (rows it did not change are still zero), the tags
+// themselves and the call's counters.  A warp per row, lanes over its words.
+__device__ void st_clear_phase(const STParams &p, int64_t gtid, int64_t gthreads) {
     const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t warp = gtid >> 5;
+    const int64_t nwarps = gthreads >> 5;
     for (int64_t h0 = warp * 32; h0 < p.n_ext; h0 += nwarps * 32) {
         const int64_t h = h0 + lane;
-        unsigned m = __ballot_sync(0xFFFFFFFFu, h < p.n_ext && __ldg(p.mark + h) != 0);
-        while (m) {
+        const bool tagged = h < p.n_ext && __ldcg(p.mark + h) != 0;
+        unsigned m = __ballot_sync(0xFFFFFFFFu, tagged);
+        if (tagged) p.mark[h] = 0;
+        while (m && p.clear_rows) {
             const int e = __ffs(m) - 1;
             m &= m - 1;
             for (int32_t w = lane; w < p.Wp; w += 32) {
@@ -1847,32 +1846,27 @@ __global__ void st_clear_kernel(STParams p) {
             }
         }
     }
+    for (int64_t w = gtid; w < p.any_words; w += gthreads) {
+        p.any_rw[w] = 0u;
+        p.gfull[w] = 0u;
+    }
+    if (gtid == 0) {
+        *p.tail = 0;
+        p.pcnt[0] = p.pcnt[1] = p.pcnt[2] = 0;
+        *p.status_out = 0;
+        *p.n_accepted = 0;
+    }
 }
 
-cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_t *negated_ext,
-                           const int32_t *free_rank, const unsigned long long *guesses,
-                           int32_t W, int64_t G, int64_t woff, const int32_t *facts, int32_t nfacts,
-                           int32_t top, uint32_t *any_bits, bool full_clear, cudaStream_t st) {
-    cudaError_t e;
-    const size_t tbytes = (size_t)p.n_ext * p.Wp * sizeof(unsigned long long);
-    if (full_clear) {   // first call, or a new matrix layout
-        if ((e = cudaMemsetAsync(p.T0, 0, tbytes, st))) return e;
-        if ((e = cudaMemsetAsync(p.T1, 0, tbytes, st))) return e;
-    } else {            // only the rows the previous call changed are not zero
-        st_clear_kernel<<<592, 256, 0, st>>>(p);
-        if ((e = cudaGetLastError())) return e;
+// Algorithm 3's test for every guess word: accept iff a_j ∈ M ⟺ b̄_j ∉ M for every j.
+__device__ void st_check_phase(const STParams &p, int64_t gtid, int64_t gthreads) {
+    for (int64_t w = gtid; w < p.W; w += gthreads) {
+        unsigned long long ok = valid_word(w, p.W, p.G);
+        for (int32_t j = 0; j < p.k; ++j)
+            ok &= __ldcg(p.T0 + (int64_t)p.negated[j] * p.Wp + w) ^ __ldcg(p.T0 + (int64_t)(p.n_atoms + j) * p.Wp + w);
+        p.accepted[w] = ok;
+        if (ok) atomicAdd((unsigned long long *)p.n_accepted, (unsigned long long)__popcll(ok));
     }
-    if ((e = cudaMemsetAsync(any_bits, 0, sizeof(uint32_t) * (size_t)p.any_words, st))) return e;
-    if ((e = cudaMemsetAsync(p.mark, 0, sizeof(int32_t) * (size_t)p.n_ext, st))) return e;
-    if ((e = cudaMemsetAsync(p.tail, 0, sizeof(int32_t), st))) return e;
-    if ((e = cudaMemsetAsync(p.pcnt, 0, 3 * sizeof(int32_t), st))) return e;
-    if ((e = cudaMemsetAsync(p.gfull, 0, sizeof(uint32_t) * (size_t)p.any_words, st))) return e;
-    if ((e = cudaMemsetAsync(p.status_out, 0, sizeof(int32_t), st))) return e;
-    const int64_t total = (1 + (int64_t)nfacts + k) * p.Wp;
-    int b = (int)std::min<int64_t>((total + 255) / 256, 8192);
-    st_init_kernel<<<std::max(b, 1), 256, 0, st>>>(p, n, k, negated_ext, free_rank, guesses, W, G,
-                                                   woff, facts, nfacts, top, any_bits);
-    return cudaGetLastError();
 }
 
 // One candidate AND-row, all guess words: acc = AND of the body rows of T_k; the new
@@ -1930,6 +1924,12 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
     const int64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
     __shared__ uint32_t st_q[kStQueue];  // candidate rows of this CTA's scan: slot | segment << 27
     __shared__ int32_t st_qn, st_qover;
+    // the call's set-up, in the same launch: the previous call's rows and this call's
+    // counters cleared, then T_0 (Def. 8) and its "any" bits
+    st_clear_phase(p, gtid, gthreads);
+    grid.sync();
+    st_init_phase(p, gtid, gthreads);
+    grid.sync();
     // shared memory: "true in some guess" bits, then (exact filter only) "true in every
     // guess" bits -- a row whose head is full can change nothing
     uint32_t *full = sm + p.any_words;
@@ -2132,11 +2132,11 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
         if (p.dbg && lead && k < 64) p.dbg[4 * k] = globaltimer();   // profiling hook
         if (cnt == 0) {
             if (lead) { *p.passes_out = k + 1; }
-            return;
+            break;
         }
         if (k + 1 >= p.max_passes) {
             if (lead) { *p.passes_out = k + 1; atomicMax(p.status_out, 1); }
-            return;
+            break;
         }
         n2 = n1;
         n1 = cnt;
@@ -2145,9 +2145,11 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
             s1[u] = tid + u * (int)blockDim.x < cnt ? nx[u] : -1;
         }
     }
+    // both buffers hold the fixpoint (rows changed in the last pass were copied during it)
+    st_check_phase(p, gtid, gthreads);
 }
 
-cudaError_t launch_st_fixpoint(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
+cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
     STParams q = p;
     void *args[] = {(void *)&q};
     return cudaLaunchCooperativeKernel((const void *)st_fixpoint_kernel, dim3(blocks),
@@ -2156,30 +2158,6 @@ cudaError_t launch_st_fixpoint(const STParams &p, int blocks, size_t smem, cudaS
 
 // Algorithm 3 (reading R7): guess g is accepted iff for every negated
 // atom a_j, T[a_j] + T[abar_j] = 1 in column g, i.e. the XOR of the two rows is 1.
-__global__ void st_check_kernel(const unsigned long long *T, int32_t Wp, int32_t n, int32_t k,
-                                const int32_t *negated, int32_t W, int64_t G,
-                                unsigned long long *accepted, long long *n_accepted) {
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
-         w += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long ok = valid_word(w, W, G);
-        for (int32_t j = 0; j < k; ++j)
-            ok &= T[(int64_t)negated[j] * Wp + w] ^ T[(int64_t)(n + j) * Wp + w];
-        accepted[w] = ok;
-        if (ok) atomicAdd((unsigned long long *)n_accepted, (unsigned long long)__popcll(ok));
-    }
-}
-
-cudaError_t launch_st_check(const STParams &p, int32_t n, int32_t k, const int32_t *negated,
-                            int32_t W, int64_t G, unsigned long long *accepted,
-                            long long *n_accepted, cudaStream_t st) {
-    cudaError_t e;
-    if ((e = cudaMemsetAsync(n_accepted, 0, sizeof(long long), st))) return e;
-    int b = (int)std::min<int64_t>((W + 255) / 256, 1024);
-    st_check_kernel<<<std::max(b, 1), 256, 0, st>>>(p.T0, p.Wp, n, k, negated, W, G, accepted,
-                                                    n_accepted);
-    return cudaGetLastError();
-}
-
 __global__ void st_column_kernel(const unsigned long long *T, int32_t Wp, int32_t n, int64_t g,
                                  unsigned long long *out) {
     const int64_t nw = ((int64_t)n + 63) >> 6;

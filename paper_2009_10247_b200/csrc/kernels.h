@@ -175,6 +175,22 @@ struct STParams {
     int32_t *passes_out;
     int32_t *status_out;
     int32_t max_passes;
+    // the rest of the call, fused into the same cooperative launch (clear -> T_0 -> fixpoint
+    // -> stability check, grid barriers in between)
+    int32_t n_atoms;                    // n: row of b̄_j is n + j
+    int32_t k;                          // negated atoms
+    const int32_t *negated;             // [k] atom a_j (check: a_j ∈ LM ⟺ b̄_j = 0)
+    const int32_t *negated_ext;         // [k] row of b̄_j
+    const int32_t *free_rank;           // [k] bit of b̄_j in the binary-counting guess id, -1: forced 0
+    const unsigned long long *guesses;  // [k][W] the caller's guesses, or NULL (binary counting)
+    int64_t woff;                       // first guess word (guess_offset / 64)
+    const int32_t *facts;               // [nfacts] rows all-ones in T_0 (with ⊤ = top)
+    int32_t nfacts;
+    int32_t top;
+    uint32_t *any_rw;                   // = any_init, built by the T_0 phase
+    int32_t clear_rows;                 // zero the rows the previous call changed (mark != 0)
+    unsigned long long *accepted;       // [W] accepted-guess mask (check)
+    long long *n_accepted;
 };
 
 // ---- launchers (return cudaError_t of the launch) -----------------------------------
@@ -186,14 +202,9 @@ int lm_tma_blocks_per_sm(bool exact, size_t smem);
 size_t lm_tma_smem_bytes(int32_t sm_words, int32_t stages);
 cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st);
 
-cudaError_t launch_st_init(const STParams &p, int32_t n, int32_t k, const int32_t *negated_ext,
-                           const int32_t *free_rank, const unsigned long long *guesses,
-                           int32_t W, int64_t G, int64_t woff, const int32_t *facts, int32_t nfacts,
-                           int32_t top, uint32_t *any_bits, bool full_clear, cudaStream_t st);
-cudaError_t launch_st_fixpoint(const STParams &p, int blocks, size_t smem, cudaStream_t st);
-cudaError_t launch_st_check(const STParams &p, int32_t n, int32_t k, const int32_t *negated,
-                            int32_t W, int64_t G, unsigned long long *accepted,
-                            long long *n_accepted, cudaStream_t st);
+// One cooperative launch per stable call: clear the previous call's rows, build T_0, the
+// fixpoint loop, the stability check.
+cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st);
 cudaError_t launch_st_column(const STParams &p, int32_t n, int64_t g, unsigned long long *out,
                              cudaStream_t st);
 
