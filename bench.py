@@ -395,7 +395,7 @@ def main():
                   "guesses_per_s": G_all / (sms / 1e3), "ms_per_step": sms,
                   "kernel_ms": allmax(float(np.mean(st_k))), "passes": int(allmax(int(passes.item()))),
                   "accepted": int(nacc.item()), "n_negated": sprog.info["n_negated"],
-                  "l2": "flushed between steps",
+                  "l2": "flushed between steps", "launches_per_call": 1,
                   "sharding": f"guesses over {ws} rank(s), slice time max over ranks"}
         if dist:
             ids, ps = stable_models_sharded(sprog, sprog.info["n_free_negated"])
