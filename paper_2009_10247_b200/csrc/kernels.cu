@@ -67,6 +67,27 @@ static unsigned long long *g_dbg = nullptr;
 void set_debug_timing(unsigned long long *buf) { g_dbg = buf; }
 unsigned long long *debug_timing() { return g_dbg; }
 
+// The per-pass counters every thread needs right after a grid barrier are loaded by ONE
+// thread per CTA and broadcast through shared memory: the same address from every warp
+// of the grid (~4.7 k requests) queues on one L2 slice for microseconds.
+struct PassCounts {
+    int32_t appended;           // pcnt[k % 3]
+    int32_t queued;             // cand[k % 3]
+    unsigned long long vent;    // vent[k % 3]
+};
+
+__device__ __forceinline__ PassCounts cta_pass_counts(const int32_t *pcnt, const int32_t *cand,
+                                                      const unsigned long long *vent) {
+    __shared__ PassCounts s;
+    if (threadIdx.x == 0) {
+        s.appended = __ldcg(pcnt);
+        s.queued = cand ? __ldcg(cand) : 0;
+        s.vent = vent ? __ldcg(vent) : 0ull;
+    }
+    __syncthreads();
+    return s;   // (every call site reaches a grid barrier before the next call rewrites s)
+}
+
 __device__ __forceinline__ bool sm_bit(const uint32_t *sm, uint32_t x) {
     return (sm[x >> 5] >> (x & 31)) & 1u;
 }
@@ -950,9 +971,10 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
     }
     grid.sync();
     if (p.dbg && tid == 0) PDBG(0, 5) = globaltimer();
-    int32_t t = n0 + __ldcg(p.pcnt + 0);
-    int32_t queued = __ldcg(p.cand + 0);
-    unsigned long long vq = __ldcg(p.vent + 0);
+    const PassCounts pc0 = cta_pass_counts(p.pcnt + 0, p.cand + 0, p.vent + 0);
+    int32_t t = n0 + pc0.appended;
+    int32_t queued = pc0.queued;
+    unsigned long long vq = pc0.vent;
     int32_t ds = n0, de = n0;
     for (int k = 0;; ++k) {
         // ---- pass k is complete: [de, t) are its appends
@@ -1174,7 +1196,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     grid.sync();
     if (p.dbg && tid == 0) p.dbg[(2 * gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
     bool rebuild = false;                                // key space -> atom-id summary
-    const int32_t n0 = __ldcg(p.tail);
+    const int32_t n0 = cta_pass_counts(p.tail, nullptr, nullptr).appended;
     {
         if (!ksum_image)
             for (int32_t w = tid; w < kBucketWords; w += blockDim.x) bmask[w] = 0u;
@@ -1383,8 +1405,9 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                 spec[u] = i < p.n_order_cap ? (uint32_t)__ldcg(lst + i) : 0u;
             }
         }
-        const int32_t t = de + __ldcg(p.pcnt + k % 3);
-        const int32_t queued = __ldcg(p.cand + k % 3);
+        const PassCounts pcs = cta_pass_counts(p.pcnt + k % 3, p.cand + k % 3, p.vent + k % 3);
+        const int32_t t = de + pcs.appended;
+        const int32_t queued = pcs.queued;
         if (lead && p.stats) {
             // algorithmic bytes of this pass: the planes it streamed, 4 B per body entry
             // and head the verification loaded, the delta list read twice and the truth
@@ -1418,7 +1441,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         // auto schedule: STREAM from the first LEAD pass that queued more than 1/dense_div of
         // the rows or whose verification loaded more than 1/8 of the entries a STREAM pass
         // reads (a verified entry costs a 32-byte sector, a streamed one 4 bytes)
-        const unsigned long long vq = __ldcg(p.vent + k % 3);
+        const unsigned long long vq = pcs.vent;
         if (lead_pass && p.pass_mode == 0 &&
             ((int64_t)queued * p.dense_div > p.n_slots || (long long)vq * 8 > p.stream_entries)) {
             lead_pass = false;
@@ -1514,7 +1537,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
     const uint32_t *src0 = EXACT ? p.buf0 : p.summary;
     smem_fill(sm, src0, p.sm_words);
     for (int i = tid; i < p.ntseg; i += blockDim.x) ts[i] = p.tsegs[i];
-    const int32_t n0 = __ldcg(p.tail);
+    const int32_t n0 = cta_pass_counts(p.tail, nullptr, nullptr).appended;
     if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = n0;
     if (tid == 0) {
         qcount = 0;
@@ -1636,7 +1659,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_consta
         }
         grid.sync();
         if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + 5] = globaltimer();
-        const int32_t t = de + __ldcg(p.pcnt + k % 3);   // (see lm_full_kernel)
+        const int32_t t = de + cta_pass_counts(p.pcnt + k % 3, nullptr, nullptr).appended;   // (see lm_full_kernel)
         const bool lead = blockIdx.x == 0 && tid == 0;
         const bool done = (t == de) || (k + 1 >= p.max_passes) || (k + 1 == p.user_cap);
         if (done) {
@@ -1708,7 +1731,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
         for (int64_t w = gtid; w < nw; w += gthreads) p.cnt[w0 + w] = v;
     }
     grid.sync();
-    int32_t qs = 0, qe = __ldcg(p.tail);
+    int32_t qs = 0, qe = cta_pass_counts(p.tail, nullptr, nullptr).appended;
     if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = qe;
     int32_t a_first = (int64_t)qs + gwarp < qe ? __ldcg(p.order + qs + gwarp) : 0;
     const int2 *occ = reinterpret_cast<const int2 *>(p.occ_slot);
@@ -1744,7 +1767,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
         // this level's first atom for this warp, loaded together with the level's count
         // (unused if past it: the next level may be appending there already)
         a_first = (int64_t)qe + gwarp < p.n_order_cap ? __ldcg(p.order + qe + gwarp) : 0;
-        const int32_t t = qe + __ldcg(p.pcnt + k % 3);   // (a per-level slot, see lm_full_kernel)
+        const int32_t t = qe + cta_pass_counts(p.pcnt + k % 3, nullptr, nullptr).appended;   // (a per-level slot, see lm_full_kernel)
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (t == qe || k + 1 >= p.max_passes || k + 1 == p.user_cap) {
             if (lead) {
@@ -2127,7 +2150,7 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
             const int64_t i = tid + (int64_t)u * blockDim.x;
             nx[u] = i < p.ring_cap ? __ldcg(p.order + (int64_t)(k % 3) * p.ring_cap + i) : -1;
         }
-        const int32_t cnt = __ldcg(p.pcnt + k % 3);
+        const int32_t cnt = cta_pass_counts(p.pcnt + k % 3, nullptr, nullptr).appended;
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (p.dbg && lead && k < 64) p.dbg[4 * k] = globaltimer();   // profiling hook
         if (cnt == 0) {
