@@ -32,14 +32,13 @@ def check_lm(P, v0=None, prog=None, variants=(False, True), jacobi=False,
         assert conv and jit == oit and jpops == opops and (oracle.pack_bits(jm) == om).all()
     prog = prog or lp.Program(P, **kw)
     runs = []
-    keyspace = prog.info["truth_mode"] == 1 and prog.info["key_shift"] >= 0
     for frontier in variants:
         if frontier or prog.info["full_kernel"] == 1:
             runs.append((frontier, "auto", True))
-        else:   # every schedule of the full θ-pass (LEAD / STREAM passes) must agree
+        else:   # every schedule of the full θ-pass (LEAD / STREAM passes) must agree,
+                # LEAD passes pipelined (default) and not
             runs += [(False, s, True) for s in schedules]
-            if keyspace:   # key-space LEAD passes pipelined (default) and not
-                runs += [(False, s, False) for s in schedules if s != "stream"]
+            runs += [(False, s, False) for s in schedules if s != "stream"]
     for frontier, schedule, pipeline in runs:
         model, iters, ex = prog.least_model(v0, frontier=frontier, popcounts=True, stages=True,
                                             schedule=schedule, stats=True, pipeline=pipeline)
@@ -467,6 +466,22 @@ def test_max_passes_cap():
             assert ex["converged"] == (p_ >= 50)
             bits = lp.unpack_bits(model, 50)
             assert bits.sum() == min(p_ + 1, 50)
+
+
+@pytest.mark.parametrize("pipeline", [True, False])
+def test_max_passes_cap_exact_pipelined(pipeline):
+    """The cap in exact-mode LEAD passes, pipelined or not (chain of 3,000 atoms)."""
+    n = 3000
+    P = lpgen.chain(n)
+    prog = lp.Program(P)
+    assert prog.info["truth_mode"] == 0
+    for p_ in (1, 2, 3, 17, n - 1, n, n + 5):
+        model, iters, ex = prog.least_model(max_passes=p_, schedule="lead", pipeline=pipeline,
+                                            popcounts=True)
+        assert iters == min(p_, n)
+        assert ex["converged"] == (p_ >= n)
+        assert lp.unpack_bits(model, n).sum() == min(p_ + 1, n)
+        assert ex["popcounts"] == list(range(1, min(p_, n) + 1))
 
 
 @pytest.mark.parametrize("pipeline", [True, False])
