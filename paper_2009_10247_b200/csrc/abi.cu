@@ -408,21 +408,6 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
             for (int64_t i = 0; i < sg.count_pad; ++i)
                 l32[(size_t)(sg.slot_off + i)] = L.col[(size_t)(sg.col_off + i)];
         TRY(upload(p, &p->d_lead32, l32));
-        // lead-occurrence lists (pipelined LEAD passes): slots by their lead atom
-        std::vector<int32_t> lp((size_t)L.n_ext + 1, 0), ls;
-        for (int64_t s = 0; s < L.n_slots; ++s) {
-            const int32_t a = l32[(size_t)s];
-            if (a != L.bot && a >= 0 && a < L.n_ext) lp[(size_t)a + 1]++;
-        }
-        for (int32_t a = 0; a < L.n_ext; ++a) lp[(size_t)a + 1] += lp[(size_t)a];
-        ls.assign((size_t)std::max<int32_t>(lp[(size_t)L.n_ext], 1), 0);
-        std::vector<int32_t> fo(lp.begin(), lp.end() - 1);
-        for (int64_t s = 0; s < L.n_slots; ++s) {
-            const int32_t a = l32[(size_t)s];
-            if (a != L.bot && a >= 0 && a < L.n_ext) ls[(size_t)fo[(size_t)a]++] = (int32_t)s;
-        }
-        TRY(upload(p, &p->d_locc_ptr, lp));
-        TRY(upload(p, &p->d_locc_slot, ls));
     }
     TRY(upload(p, &p->d_segs, L.segs));
     TRY(upload(p, &p->d_col, L.col));

@@ -320,7 +320,6 @@ struct PassCtx {
     int32_t *sq;            // the first kSmemQueue queue entries (shared memory), or NULL
     int32_t *pc;            // this pass's append counter (p.pcnt[k % 3])
     int32_t base;           // derivation-list index of this pass's first append
-    int32_t sqcap;          // queue entries in shared memory (sq), the rest in qbuf
 };
 
 // Queue entry i of this CTA: shared memory for the first kSmemQueue entries (no global
@@ -329,12 +328,12 @@ struct PassCtx {
 // An entry past both parts is dropped (the caller reports the overflow as status 2);
 // shared-memory entries are always written, so a verifier waiting for one never hangs.
 __device__ __forceinline__ void qput(const LMParams &p, const PassCtx &c, int32_t i, int32_t slot) {
-    if (i < c.sqcap) c.sq[i] = slot;
-    else if (i - c.sqcap < p.qcap) c.qbuf[i - c.sqcap] = slot;
+    if (i < kSmemQueue) c.sq[i] = slot;
+    else if (i - kSmemQueue < p.qcap) c.qbuf[i - kSmemQueue] = slot;
 }
 
 __device__ __forceinline__ int32_t qget(const PassCtx &c, int32_t i) {
-    return i < c.sqcap ? c.sq[i] : __ldcg(c.qbuf + (i - c.sqcap));
+    return i < kSmemQueue ? c.sq[i] : __ldcg(c.qbuf + (i - kSmemQueue));
 }
 
 // Smem test of 4 AND-rows at one body position; `fire` bit e = row e still alive.
@@ -425,7 +424,7 @@ __device__ __forceinline__ int verify_slot(const LMParams &p, const PassCtx &c, 
 __device__ __forceinline__ void enqueue(const LMParams &p, const PassCtx &c, int32_t slot0,
                                         unsigned fire) {
     int32_t pos = atomicAdd(c.qcount, __popc(fire));
-    if (pos + __popc(fire) > p.qcap + c.sqcap) atomicExch(p.status_out, 2);
+    if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
 #pragma unroll
     for (int e = 0; e < 4; ++e)
         if ((fire >> e) & 1u) qput(p, c, pos++, slot0 + e);
@@ -627,7 +626,7 @@ __device__ __forceinline__ void oct_test(const LMParams &p, const PassCtx &c, in
         fire &= 0xFFu >> (tag[u] >> T::pshift);           // trailing padding rows
         if (fire) {
             int32_t pos = atomicAdd(c.qcount, __popc(fire));
-            if (pos + __popc(fire) > p.qcap + c.sqcap) atomicExch(p.status_out, 2);
+            if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
             const int32_t s0 = q * 8;
             for (unsigned f = fire; f; f &= f - 1) qput(p, c, pos++, s0 + __ffs(f) - 1);
         }
@@ -691,7 +690,7 @@ __device__ __forceinline__ void octets_exact16(const LMParams &p, const PassCtx 
             fire &= 0xFFu >> (tag[u] >> 10);                  // trailing padding rows
             if (fire) {
                 int32_t pos = atomicAdd(c.qcount, __popc(fire));
-                if (pos + __popc(fire) > p.qcap + c.sqcap) atomicExch(p.status_out, 2);
+                if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
                 for (unsigned f = fire; f; f &= f - 1) qput(p, c, pos++, q * 8 + __ffs(f) - 1);
             }
         }
@@ -879,14 +878,10 @@ struct PipeExit {
     int done;         // 1: fixpoint (or cap) reached, model written
 };
 
-// Runs LEAD passes from pass 0 until the fixpoint (returns done = 1 after the epilogue)
-// or until the auto schedule asks for STREAM passes (returns the state the unpipelined
-// loop resumes from).  All threads of the CTA call it; the shared copy of v_0 (its key
-// summary, or the exact bits when EXACT) is already built.
-// EXACT: the shared truth is exact and is what the verification reads, so Δ_k is folded
-// into it only after the phase (stream and verification of v_k) is over; the stream is
-// the exact-mode LEAD stream (rows with a true lead atom and a false head).
-template <bool EXACT>
+// Runs key-space LEAD passes from pass 0 until the fixpoint (returns done = 1 after the
+// epilogue) or until the auto schedule asks for STREAM passes (returns the state the
+// unpipelined loop resumes from).  All threads of the CTA call it; the shared key
+// summary of v_0 is already built.
 __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32_t *bmask,
                                          const Segment *segs, int32_t *squeue, int32_t n0,
                                          long long clk0, unsigned long long ns0) {
@@ -909,17 +904,6 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
     int32_t *gq[2] = {p.qbuf + (int64_t)blockIdx.x * p.qcap,
                       p.qbuf + ((int64_t)gridDim.x + blockIdx.x) * p.qcap};
     int32_t *sq[2] = {squeue, squeue + kPipeSq};
-    constexpr int j0 = EXACT ? 1 : 0;   // (exact LEAD streams test the lead atom exactly)
-    // the LEAD stream of one pass into queue half h (filter: the shared copy of v_k)
-    auto stream_into = [&](int h, int64_t sgtid, int64_t sthreads) {
-        if constexpr (EXACT) {
-            const PassCtx cs{nullptr, nullptr, sm, gq[h], &qcnt[h], 0, bmask, segs, sq[h], nullptr, 0, kPipeSq};
-            if (p.xlead16) octets_exact16<4>(p, cs, sgtid, sthreads);
-            else flat_lead_exact<4>(p, cs, sgtid, sthreads);
-        } else {
-            pipe_stream(p, sm, bmask, sq[h], gq[h], &qcnt[h], &abandon, sgtid, sthreads);
-        }
-    };
 #define PDBG(k, i) p.dbg[((k) * gridDim.x + blockIdx.x) * 8 + (i)]
     if (tid == 0) {
         qcnt[0] = qcnt[1] = 0;
@@ -940,10 +924,11 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         p.pcnt[1] = 0;
     }
     {
-        const PassCtx c{p.buf0, p.buf1, sm, nullptr, nullptr, 0, bmask, segs, nullptr, p.pcnt, n0, 0};
+        const PassCtx c{p.buf0, p.buf1, sm, nullptr, nullptr, 0, bmask, segs, nullptr, p.pcnt, n0};
         int loaded = 0;
         if (!verifier) {
-            stream_into(0, (int64_t)blockIdx.x * vbase + tid, (int64_t)gridDim.x * vbase);
+            pipe_stream(p, sm, bmask, sq[0], gq[0], &qcnt[0], &abandon, (int64_t)blockIdx.x * vbase + tid,
+                        (int64_t)gridDim.x * vbase);
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
@@ -964,13 +949,13 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
                 if (!have) break;
                 int32_t s;
                 while ((s = *(volatile int32_t *)&sq[0][i]) < 0) __nanosleep(32);
-                loaded += verify_slot<EXACT>(p, c, s, j0);
+                loaded += verify_slot<false>(p, c, s, 0);
             }
         }
         __syncthreads();
         if (p.dbg && tid == 0) PDBG(0, 2) = globaltimer();
         const int32_t nc = min(qcnt[0], p.qcap + kPipeSq);
-        for (int32_t i = kPipeSq + tid; i < nc; i += blockDim.x) loaded += verify_slot<EXACT>(p, c, pipe_qget(sq[0], gq[0], i), j0);
+        for (int32_t i = kPipeSq + tid; i < nc; i += blockDim.x) loaded += verify_slot<false>(p, c, pipe_qget(sq[0], gq[0], i), 0);
         for (int o = 16; o; o >>= 1) loaded += __shfl_xor_sync(0xFFFFFFFFu, loaded, o);
         if (lane == 0 && loaded) atomicAdd(&s_loaded, (unsigned long long)loaded);
         __syncthreads();
@@ -1022,14 +1007,8 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         if (p.pass_mode == 0 &&
             ((int64_t)queued * p.dense_div > p.n_slots || (long long)vq * 8 > p.stream_entries))
             return PipeExit{k, de, t, 0};   // the auto schedule switches to STREAM passes
-        // ---- Δ_k into the shared copy: v_{k+1} (key mode: only after pass 0 here, later
-        // passes fold it during their phase)
-        if (EXACT) {
-            if ((t - de) > (p.sm_words >> 2)) smem_fill(sm, wr_k, p.sm_words);
-            else add_to_shared<true>(p, sm, bmask, de, t, false);
-        } else if (k == 0) {
-            add_to_shared<false>(p, sm, bmask, de, t, true);
-        }
+        // ---- Δ_k into the key summary: summary(v_{k+1})
+        if (k == 0) add_to_shared<false>(p, sm, bmask, de, t, true);   // (later: in the phase)
         if (tid == 0) {
             qcnt[(k + 1) & 1] = 0;   // (S_{k+1} half: verified in phase k, streamed into next)
             abandon = 0;
@@ -1047,7 +1026,7 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
             p.vent[(j + 1) % 3] = 0;
             p.pcnt[(j + 1) % 3] = 0;
         }
-        const PassCtx c{rd, wr, sm, nullptr, nullptr, j, bmask, segs, nullptr, p.pcnt + j % 3, de, 0};
+        const PassCtx c{rd, wr, sm, nullptr, nullptr, j, bmask, segs, nullptr, p.pcnt + j % 3, de};
         const int h = (j + 1) & 1;
         const int32_t nc = min(qcnt[h], p.qcap + kPipeSq);
         // pass j's verification by nt of the CTA's threads (ti = index among them)
@@ -1058,14 +1037,14 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
                 atomicOr(wr + (a >> 5), 1u << (a & 31));
             }
             int loaded = 0, nl = 0;
-            for (int32_t i = ti; i < nc; i += nt) loaded += verify_slot<EXACT>(p, c, pipe_qget(sq[h], gq[h], i), j0);
+            for (int32_t i = ti; i < nc; i += nt) loaded += verify_slot<false>(p, c, pipe_qget(sq[h], gq[h], i), 0);
             // rows whose lead atom became true in pass j - 1 (a warp per atom)
             const int nw = nt >> 5;
             for (int64_t i = ds + (int64_t)blockIdx.x * nw + (ti >> 5); i < de; i += (int64_t)gridDim.x * nw) {
                 const int32_t a = __ldcg(p.order + i);
                 const int32_t o0 = __ldg(p.locc_ptr + a), o1 = __ldg(p.locc_ptr + a + 1);
                 for (int32_t o = o0 + lane; o < o1; o += 32) {
-                    loaded += verify_slot<EXACT>(p, c, __ldg(p.locc_slot + o), j0);
+                    loaded += verify_slot<false>(p, c, __ldg(p.locc_slot + o), 0);
                     ++nl;
                 }
             }
@@ -1121,7 +1100,7 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
             // reached through locc(Δ_j) -- verified twice, same result -- and the summary
             // stays a superset of summary(v_j), so S_{j+1} misses nothing
             asm volatile("bar.sync 1, %0;" ::"r"(nvt) : "memory");
-            if (!EXACT && !*(volatile int32_t *)&abandon) {
+            if (!*(volatile int32_t *)&abandon) {
                 const int32_t tj = *(volatile int32_t *)&s_t;
                 for (int32_t i0 = de + vtid; i0 < tj; i0 += 4 * nvt) {
                     uint32_t a[4];
@@ -1143,7 +1122,8 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         } else {
             // pass j+1's candidates: rows whose lead key is in summary(v_j)
             const int64_t sgtid = (int64_t)blockIdx.x * vbase + tid;
-            stream_into(j & 1, sgtid, (int64_t)gridDim.x * vbase);
+            pipe_stream(p, sm, bmask, sq[j & 1], gq[j & 1], &qcnt[j & 1], &abandon, sgtid,
+                        (int64_t)gridDim.x * vbase);
             if (p.dbg && j < 16 && lane == 0) atomicMax(&PDBG(j, 2), globaltimer());
         }
         __syncthreads();
@@ -1243,28 +1223,22 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 7] = globaltimer();
 
     int32_t ds = n0, de = n0;  // atoms that became true in the previous pass
-    constexpr int kSpec = 4;
-    uint32_t spec[kSpec];      // the next delta's first list entries, loaded with its count
     int k_start = 0;
-    if (p.locc_ptr && lead_pass && (EXACT ? (p.xlead16 || p.lead32) : keys)) {   // pipelined LEAD passes
-        const PipeExit e = lm_pipe<EXACT>(p, sm, bmask, p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, n0,
-                                          lead ? clk0 : 0, lead ? ns0 : 0);
+    if (!EXACT && keys && p.locc_ptr) {   // pipelined key-space LEAD passes
+        const PipeExit e = lm_pipe(p, sm, bmask, p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, n0,
+                                   lead ? clk0 : 0, lead ? ns0 : 0);
         if (e.done) return;
-        // the auto schedule switched: STREAM passes from pass e.k + 1 on (key mode: the
-        // summary is rebuilt in atom-id space from v_{e.k+1}; exact mode: Δ_{e.k} is
-        // folded at the pass top, its first entries from spec as after a barrier)
+        // the auto schedule switched: STREAM passes from pass e.k + 1 on (the summary is
+        // rebuilt in atom-id space from v_{e.k+1})
         k_start = e.k + 1;
         ds = e.ds;
         de = e.de;
         lead_pass = false;
         keys = false;
-        rebuild = !EXACT;
-        if (EXACT)
-            for (int u = 0; u < kSpec; ++u) {
-                const int32_t i = ds + tid + u * (int32_t)blockDim.x;
-                spec[u] = i < de ? (uint32_t)__ldcg(p.order + i) : 0u;
-            }
+        rebuild = true;
     }
+    constexpr int kSpec = 4;
+    uint32_t spec[kSpec];      // the next delta's first list entries, loaded with its count
     for (int k = k_start;; ++k) {
         const uint32_t *rd = (k & 1) ? p.buf1 : p.buf0;
         uint32_t *wr = (k & 1) ? p.buf0 : p.buf1;
@@ -1329,7 +1303,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             p.pcnt[(k + 1) % 3] = 0;
         }
         const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, bmask,
-                        p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, p.pcnt + k % 3, de, kSmemQueue};
+                        p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, p.pcnt + k % 3, de};
         if (p.dbg && tid == 0 && k < 16) DBG_STAMP(1) = globaltimer();
         const int j0 = (EXACT && lead_pass) ? 1 : 0;
         int loaded = 0;

@@ -469,22 +469,6 @@ def test_max_passes_cap():
 
 
 @pytest.mark.parametrize("pipeline", [True, False])
-def test_max_passes_cap_exact_pipelined(pipeline):
-    """The cap in exact-mode LEAD passes, pipelined or not (chain of 3,000 atoms)."""
-    n = 3000
-    P = lpgen.chain(n)
-    prog = lp.Program(P)
-    assert prog.info["truth_mode"] == 0
-    for p_ in (1, 2, 3, 17, n - 1, n, n + 5):
-        model, iters, ex = prog.least_model(max_passes=p_, schedule="lead", pipeline=pipeline,
-                                            popcounts=True)
-        assert iters == min(p_, n)
-        assert ex["converged"] == (p_ >= n)
-        assert lp.unpack_bits(model, n).sum() == min(p_ + 1, n)
-        assert ex["popcounts"] == list(range(1, min(p_, n) + 1))
-
-
-@pytest.mark.parametrize("pipeline", [True, False])
 def test_max_passes_cap_key_space(pipeline):
     """The cap in key-space LEAD passes (pipelined or not): the model after p passes of
     a chain holds the first p + 1 atoms, stages and the popcount trace up to the cap."""
