@@ -41,6 +41,7 @@ struct lp_program {
     int32_t *d_col = nullptr, *d_head = nullptr;
     int64_t *d_occ_ptr = nullptr;
     int32_t *d_occ_slot = nullptr;
+    int32_t *d_fq = nullptr;   // frontier level queues [2][n_ext + 1] x (atom, occ range, -)
     uint32_t *d_cnt = nullptr;
     int cnt_bytes = 1;
     uint32_t *d_buf0 = nullptr, *d_buf1 = nullptr;
@@ -414,15 +415,23 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     TRY(upload(p, &p->d_head, L.head));
     if (L.has_occ) {
         TRY(upload(p, &p->d_occ_ptr, L.occ_ptr));
-        {   // (slot, head(slot)) pairs: a firing row's head comes with its slot, one
-            // dependent load less per level
-            std::vector<int32_t> sh(2 * L.occ_slot.size());
+        {   // (slot, head(slot), occurrence range of that head): a firing row's head comes
+            // with its slot and is queued with its own occurrence range -- two dependent
+            // loads less per level
+            if (L.occ_ptr[(size_t)L.n_ext] >= ((int64_t)1 << 31))
+                return set_err(LP_E_INVALID, "frontier variant: more than 2^31 body entries");
+            std::vector<int32_t> sh(4 * L.occ_slot.size());
             for (size_t i = 0; i < L.occ_slot.size(); ++i) {
-                sh[2 * i] = L.occ_slot[i];
                 const size_t s = (size_t)L.occ_slot[i];   // (a placeholder entry if nnz = 0)
-                sh[2 * i + 1] = s < L.head.size() ? L.head[s] : 0;
+                const int32_t h = s < L.head.size() ? L.head[s] : 0;
+                sh[4 * i] = L.occ_slot[i];
+                sh[4 * i + 1] = h;
+                sh[4 * i + 2] = (int32_t)L.occ_ptr[(size_t)h];
+                sh[4 * i + 3] = (int32_t)L.occ_ptr[(size_t)h + 1];
             }
             TRY(upload(p, &p->d_occ_slot, sh));
+            TRY(dalloc(p, &p->d_fq, (size_t)8 * ((size_t)L.n_ext + 1)));
+            CK(cudaMemset(p->d_fq, 0xFF, (size_t)8 * ((size_t)L.n_ext + 1) * sizeof(int32_t)));
         }
         p->cnt_bytes = L.max_body <= 255 ? 1 : 4;
         const size_t cw = p->cnt_bytes == 1 ? ((size_t)L.n_slots + 3) / 4 : (size_t)L.n_slots;
@@ -712,6 +721,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.user_cap = (run && run->max_passes > 0) ? run->max_passes : 0;
     q.occ_ptr = p->d_occ_ptr;
     q.occ_slot = p->d_occ_slot;
+    q.fq = p->d_fq;
     q.cnt = p->d_cnt;
     q.cnt_bytes = p->cnt_bytes;
     q.dbg = debug_timing();

@@ -1731,55 +1731,81 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
         for (int64_t w = gtid; w < nw; w += gthreads) p.cnt[w0 + w] = v;
     }
     grid.sync();
-    int32_t qs = 0, qe = cta_pass_counts(p.tail, nullptr, nullptr).appended;
-    if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = qe;
-    int32_t a_first = (int64_t)qs + gwarp < qe ? __ldcg(p.order + qs + gwarp) : 0;
-    const int2 *occ = reinterpret_cast<const int2 *>(p.occ_slot);
-    for (int k = 0;; ++k) {
-        if (blockIdx.x == 0 && tid == 0) p.pcnt[(k + 1) % 3] = 0;   // next level's counter
-        for (int64_t i = qs + gwarp; i < qe; i += nwarps) {
-            const int32_t a = i == qs + gwarp ? a_first : __ldcg(p.order + i);
-            const int64_t o0 = __ldg(p.occ_ptr + a), o1 = __ldg(p.occ_ptr + a + 1);
-            for (int64_t o = o0 + lane; o < o1; o += 32) {
-                const int2 sh = __ldg(occ + o);
-                const int32_t slot = sh.x;
-                bool fired;
-                if (p.cnt_bytes == 1) {   // a byte never underflows: <= L decrements
-                    const uint32_t sh = (uint32_t)(slot & 3) << 3;
-                    fired = ((atomicSub(p.cnt + (slot >> 2), 1u << sh) >> sh) & 0xFFu) == 1u;
-                } else {
-                    fired = atomicSub(p.cnt + slot, 1u) == 1u;
-                }
-                if (fired) {                                // body(r) ⊆ I_k
-                    const int32_t h = sh.y;
-                    const uint32_t bit = 1u << (h & 31);
-                    const uint32_t old = atomicOr(p.buf0 + (h >> 5), bit);
-                    if (!(old & bit)) {
-                        const int32_t pos = qe + atomicAdd(p.pcnt + k % 3, 1);
-                        LP_CHECK(pos < p.n_order_cap && slot >= 0 && slot < p.n_slots);
-                        p.order[pos] = h;
-                        if (p.stage && h < p.n_out) p.stage[h] = k + 1;
-                    }
+    const int32_t n0 = cta_pass_counts(p.tail, nullptr, nullptr).appended;
+    const bool lead = blockIdx.x == 0 && tid == 0;
+    if (lead && p.pops && p.pop_cap > 0) p.pops[0] = n0;
+    // occurrences as (slot, head(slot), occ range of that head): a firing row's head is
+    // queued for the next level together with its own occurrence range
+    const int4 *occ = reinterpret_cast<const int4 *>(p.occ_slot);
+    int4 *const fq0 = reinterpret_cast<int4 *>(p.fq);   // queue of level l: fq0 + (l & 1) * n_order_cap
+    // level kk: push one newly true atom's occurrences; heads that become true go to the
+    // queue of level kk + 1 (slot count in pcnt[kk % 3])
+    auto push = [&](int32_t o0, int32_t o1, int kk) {
+        for (int32_t o = o0 + lane; o < o1; o += 32) {
+            const int4 e = __ldg(occ + o);
+            const int32_t slot = e.x;
+            bool fired;
+            if (p.cnt_bytes == 1) {   // a byte never underflows: <= L decrements
+                const uint32_t sh = (uint32_t)(slot & 3) << 3;
+                fired = ((atomicSub(p.cnt + (slot >> 2), 1u << sh) >> sh) & 0xFFu) == 1u;
+            } else {
+                fired = atomicSub(p.cnt + slot, 1u) == 1u;
+            }
+            if (fired) {                                // body(r) ⊆ I_kk
+                const int32_t h = e.y;
+                const uint32_t bit = 1u << (h & 31);
+                const uint32_t old = atomicOr(p.buf0 + (h >> 5), bit);
+                if (!(old & bit)) {
+                    const int32_t pos = atomicAdd(p.pcnt + kk % 3, 1);
+                    LP_CHECK(pos < p.n_order_cap && slot >= 0 && slot < p.n_slots);
+                    fq0[(int64_t)((kk + 1) & 1) * p.n_order_cap + pos] = make_int4(h, e.z, e.w, 0);
+                    if (p.stage && h < p.n_out) p.stage[h] = kk + 1;
                 }
             }
         }
+    };
+    // level 0: the atoms of v_0 (the prologue's derivation list)
+    if (lead) p.pcnt[1] = 0;
+    for (int64_t i = gwarp; i < n0; i += nwarps) {
+        const int32_t a = __ldcg(p.order + i);
+        push((int32_t)__ldg(p.occ_ptr + a), (int32_t)__ldg(p.occ_ptr + a + 1), 0);
+    }
+    __shared__ int32_t s_cnt;
+    int32_t total = n0;
+    for (int k = 0;; ++k) {
         grid.sync();
-        // this level's first atom for this warp, loaded together with the level's count
-        // (unused if past it: the next level may be appending there already)
-        a_first = (int64_t)qe + gwarp < p.n_order_cap ? __ldcg(p.order + qe + gwarp) : 0;
-        const int32_t t = qe + cta_pass_counts(p.pcnt + k % 3, nullptr, nullptr).appended;   // (a per-level slot, see lm_full_kernel)
-        const bool lead = blockIdx.x == 0 && tid == 0;
-        if (t == qe || k + 1 >= p.max_passes || k + 1 == p.user_cap) {
+        // level k is complete; level j = k + 1 starts at once from its queue (entries are
+        // -1 past its end: no count needed to start), while one thread per CTA fetches
+        // level k's append count (termination, popcount trace) -- if it is 0 the queue
+        // is empty and level j does nothing
+        const int j = k + 1;
+        const bool capped = j >= p.max_passes || j == p.user_cap;
+        int4 *q = fq0 + (int64_t)(j & 1) * p.n_order_cap;
+        int4 e0 = make_int4(-1, 0, 0, 0);
+        if (!capped && gwarp < p.n_order_cap) e0 = __ldcg(q + gwarp);
+        if (tid == 0) s_cnt = __ldcg(p.pcnt + k % 3);
+        if (lead) p.pcnt[(j + 1) % 3] = 0;   // (level j appends to pcnt[j % 3])
+        if (!capped)
+            for (int64_t i = gwarp;; i += nwarps) {
+                const int4 e = i == gwarp ? e0 : (i < p.n_order_cap ? __ldcg(q + i) : make_int4(-1, 0, 0, 0));
+                if (e.x < 0) break;
+                if (lane == 0) q[i].x = -1;   // consumed (the queue is reused two levels on)
+                push(e.y, e.z, j);
+            }
+        __syncthreads();
+        const int32_t cnt = s_cnt;
+        if (cnt == 0 || capped) {
             if (lead) {
                 *p.iters_out = k + 1;
-                if (t != qe) atomicMax(p.status_out, k + 1 == p.user_cap ? 3 : 1);
+                if (cnt != 0) atomicMax(p.status_out, k + 1 == p.user_cap ? 3 : 1);
             }
+            if (capped)   // level j's queue was not consumed
+                for (int64_t i = gtid; i < cnt; i += gthreads) q[i].x = -1;
             lm_extract(p, gtid, gthreads, p.buf0);
             return;
         }
-        if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
-        qs = qe;
-        qe = t;
+        total += cnt;
+        if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = total;
     }
 }
 

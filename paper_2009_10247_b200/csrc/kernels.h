@@ -84,7 +84,8 @@ struct LMParams {
     int32_t user_cap;          // lp_run.max_passes (0 = to the fixpoint)
     // frontier variant
     const int64_t *occ_ptr;
-    const int32_t *occ_slot;   // [2 * nnz]: (slot, head(slot)) per occurrence
+    const int32_t *occ_slot;   // [4 * nnz]: (slot, head(slot), occ range of that head) per occurrence
+    int32_t *fq;               // [2][n_order_cap][4] frontier level queues (atom, occ range), -1 = empty
     uint32_t *cnt;             // per-slot remaining-body counters
     int32_t cnt_bytes;         // 1: uint8 packed 4 per word; 4: uint32
     unsigned long long *dbg;   // optional profiling timestamps (lpdbg_set_timing)
