@@ -191,7 +191,9 @@ lp_status lp_negated_atoms(const lp_program *p, int32_t *out);
  *   v0        : optional start set, bits over the original atoms ([ceil(n/64)] words);
  *               NULL = the paper's initial vector (facts only, Def. 4).  The computed
  *               model is LM(P ∪ {a <- : a ∈ v0}); facts are always included.
- *   model_out : [ceil(n/64)] words, required.
+ *   model_out : [ceil(n/64)] words, required.  Host mode: a page-locked host buffer
+ *               (cudaHostAlloc, pinned torch tensor) is written by the kernel itself
+ *               over PCIe; pageable memory is filled by a staged copy.
  *   iters_out : required; the number of T_P evaluations (θ-passes) including the
  *               final one that finds no change (reading R4).
  * Identical results (model, iters, popcounts, stages) with and without LP_FRONTIER.

@@ -632,3 +632,26 @@ def test_repeated_stable_calls_reuse_the_matrix():
         check_stable(P, guesses_u8=g, prog=prog)
         if trial == 2:
             check_stable(P, prog=prog)                  # all 2^f guesses in between
+
+
+@pytest.mark.parametrize("frontier", [False, True])
+def test_pinned_host_model_out_written_by_the_kernel(frontier):
+    """Host-pointer call with a page-locked model buffer: the epilogue writes it over PCIe
+    (no staged copy); same model and iters as a pageable buffer and as the oracle, for the
+    exact and the key-space truth."""
+    import torch
+    rng = np.random.default_rng(2024)
+    n = 5000
+    P = lpgen.random_program(rng, n, 20000, max_len=5, n_facts=250)
+    om, _, oit = oracle.lm_stage(P)
+    for kw in (dict(), dict(smem_bits_cap=128)):
+        prog = lp.Program(P, **kw)
+        W = lp.bits_words(n)
+        pinned = torch.full((W,), -1, dtype=torch.int64).pin_memory()
+        it = lp.lp_least_model(prog, None, pinned, frontier=frontier)
+        assert it == oit
+        assert (pinned.numpy().view(np.uint64)[:W] == oracle.pack_bits(om)).all()
+        pageable = np.zeros(W, dtype=np.uint64)
+        assert lp.lp_least_model(prog, None, pageable, frontier=frontier) == oit
+        assert (pageable == oracle.pack_bits(om)).all()
+        prog.close()
