@@ -16,23 +16,27 @@ import lpgen  # noqa: E402
 from paper_2009_10247_b200 import lp  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
-kw, sched = {}, "auto"
+kw, sched, v0 = {}, "auto", None
 for a in sys.argv[2:]:
     k, v = a.split("=")
     if k == "schedule":
         sched = v
+    elif k == "v0":   # v0=facts: pass the facts as an explicit start set (the generic prologue)
+        v0 = "facts"
     else:
         kw[k] = int(v)
 P = lpgen.config(cfg)
 prog = lp.Program(P, **kw)
+if v0 == "facts":
+    v0 = np.isin(np.arange(P.n_atoms), P.head[np.diff(P.body_ptr) == 0])
 G = prog.info["grid_blocks"]
 buf = torch.zeros(16 * G * 8, dtype=torch.int64, device="cuda")
 lib = lp.library()
 lib.lpdbg_set_timing.argtypes = [ctypes.c_void_p]
 for i in range(3):
-    prog.least_model(schedule=sched)
+    prog.least_model(v0, schedule=sched)
 lib.lpdbg_set_timing(buf.data_ptr())
-m, it, ex = prog.least_model(schedule=sched, stats=True)
+m, it, ex = prog.least_model(v0, schedule=sched, stats=True)
 lib.lpdbg_set_timing(None)
 t = buf.cpu().numpy().reshape(16, G, 8).astype(np.float64)
 print(cfg, "iters", it, "grid", G, "truth_mode", prog.info["truth_mode"], ex["stats"])
