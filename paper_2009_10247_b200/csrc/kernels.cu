@@ -764,6 +764,14 @@ __device__ __forceinline__ int all_segments(const LMParams &p, const PassCtx &c,
     return loads;
 }
 
+// Mark bucket bk in the shared bucket mask.  With 16-bit codes all buckets live in one
+// word, so a delta of thousands of atoms would serialise on it: test first, the atomic
+// only for a bit not yet set.
+__device__ __forceinline__ void set_bucket(uint32_t *bmask, uint32_t bk) {
+    const uint32_t bit = 1u << (bk & 31);
+    if (!(*(volatile uint32_t *)(bmask + (bk >> 5)) & bit)) atomicOr(bmask + (bk >> 5), bit);
+}
+
 // Add derivation-list entries [i0, i1) to a CTA's shared copy of v_k: exact bits
 // (EXACT), key groups (keys: the list's korder twin) or atom-id groups; in key mode the
 // per-bucket any-bit mask too.  4 independent list reads in flight per thread.
@@ -789,7 +797,7 @@ __device__ __forceinline__ void add_to_shared(const LMParams &p, uint32_t *sm, u
                 atomicOr(sm + (a[u] >> 5), 1u << (a[u] & 31));
                 if (!EXACT && keys) {   // the group's bucket (group >> key_bits) now has a set bit
                     const uint32_t bk = a[u] >> p.key_bits;
-                    atomicOr(bmask + (bk >> 5), 1u << (bk & 31));
+                    set_bucket(bmask, bk);
                 }
             }
     }
@@ -1115,7 +1123,7 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
                             const uint32_t g = a[u] >> p.kshift;
                             atomicOr(sm + (g >> 5), 1u << (g & 31));
                             const uint32_t bk = g >> p.key_bits;
-                            atomicOr(bmask + (bk >> 5), 1u << (bk & 31));
+                            set_bucket(bmask, bk);
                         }
                 }
             }
@@ -1283,7 +1291,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                         atomicOr(sm + (g >> 5), 1u << (g & 31));
                         if (!EXACT && keys) {
                             const uint32_t bk = g >> p.key_bits;
-                            atomicOr(bmask + (bk >> 5), 1u << (bk & 31));
+                            set_bucket(bmask, bk);
                         }
                     }
                 }
