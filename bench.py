@@ -12,7 +12,7 @@ on C5 (guesses/s), the end-to-end call with host buffers (e2e), the per-launch r
 of the dominant kernel and the CPU oracle baseline (cpu_baseline).
 
 --impl reference times the CPU oracle (oracle/, as it stands) on the same workload and
-metric: each step is a bounded sample (one Jacobi T_P pass over all of C4's rules).
+metric: each step is one whole O-STAGE fixpoint of C4 on one pinned host core.
 
 Multi-GPU (torchrun, N > 1): "replicas only" -- every rank solves its own copy of the
 workload (the least-model fixpoint has no partition without a per-pass exchange; see
@@ -32,7 +32,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-KERNEL_REV = "lead16-octets-d2-pipe"   # bump when the dominant kernel's traffic changes
+KERNEL_REV = "lead16-live-runs"   # bump when the dominant kernel's traffic changes
 METRIC = ("least-model fixpoint time & nnz·iter/s (HBM GB/s vs peak); "
           "stable-model guesses/s")
 
@@ -103,8 +103,30 @@ def _dist():
     return ws, rank, local
 
 
+def _pinned_stage_timed(P, trials, v0=None):
+    """O-STAGE's fixpoint phase (oracle.lm_stage_timed), this thread pinned to core 0
+    (taskset -c 0 equivalent; BASELINE.md's CPU-baseline plan), affinity restored after."""
+    import oracle
+    old = os.sched_getaffinity(0)
+    try:
+        os.sched_setaffinity(0, {min(old)})
+        return oracle.lm_stage_timed(P, v0=v0, trials=trials), min(old)
+    finally:
+        os.sched_setaffinity(0, old)
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            return next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        return ""
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle as it stands, bounded sample per step."""
+    """--impl reference: the CPU oracle as it stands (O-STAGE forward chaining, the plan of
+    BASELINE.md), single thread pinned to one core; each step = one whole fixpoint of the
+    workload (occurrence lists built once beforehand, like lp_load on our side)."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
@@ -113,26 +135,32 @@ def run_reference(args):
     oracle.build()
     P = lpgen.config(args.workload)
     nnz = int(P.nnz) + int((np.diff(P.body_ptr) == 0).sum())
-    times = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        _, it, _, _ = oracle.lm_jacobi(P, max_iters=1)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            times.append(dt)
+    (_, _, iters, secs), core = _pinned_stage_timed(P, args.warmup + args.steps)
+    times = secs[args.warmup:]
     t = float(np.mean(times))
-    v = nnz * 1 / t
-    sample = f"one Jacobi T_P pass over all {P.n_rules} rules of {args.workload} per step"
+    v = nnz * iters / t
+    sample = (f"{args.steps} whole O-STAGE fixpoints of {args.workload} ({iters} T_P passes "
+              f"equivalent each; occurrence lists built once, untimed), core {core}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "nnz*iter/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": args.workload, "variant": "oracle O-LM Jacobi (oracle/lp_oracle.c)"},
+        "config": {"workload": args.workload, "iters": iters,
+                   "variant": "oracle O-STAGE forward chaining (oracle/lp_oracle.c)"},
         "cpu_baseline": {"value": v, "unit": "nnz*iter/s", "cores": 1, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "cpu": _cpu_model(), "host_cores": os.cpu_count(),
+                         "median_ms": float(np.median(times)) * 1e3},
         "e2e": {"value": v, "unit": "nnz*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
     return 0
+
+
+def _model_bytes_per_pass(info, n):
+    """SURVEY.md §8(d)'s algorithmic bytes of one T_P pass over a CSR program:
+    B_pass = 4·nnz + 4·(R+1) + 4·(H+1) + 2·ceil((n+1)/8) (column ids, rule delimiters,
+    head grouping, truth vector read + write)."""
+    return (4 * int(info["nnz"]) + 4 * (int(info["n_rules"]) + 1) + 4 * (int(info["n_heads"]) + 1)
+            + 2 * ((n + 1 + 7) // 8))
 
 
 def main():
@@ -144,7 +172,8 @@ def main():
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--stable-workload", default="C5")
     ap.add_argument("--no-extras", action="store_true", help="main line only (for ncu)")
-    ap.add_argument("--cpu-sample-reps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--cpu-trials", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -197,17 +226,23 @@ def main():
     model = torch.zeros(Wm, dtype=torch.int64, device="cuda")
     iters_d = torch.zeros(1, dtype=torch.int32, device="cuda")
     stats_d = torch.zeros(6, dtype=torch.int64, device="cuda")
+    status_d = torch.zeros(1, dtype=torch.int32, device="cuda")
 
-    def timed_least_model(frontier, steps, warmup):
+    def timed_least_model(pr, steps, warmup, frontier=False, v0=None, schedule="auto", out=None):
+        """steps timed calls (device pointers, L2 flushed before each); every call's
+        kernel-written status word must be 0 (fixpoint reached, nothing dropped)."""
         tot, ker, byts, mhz = [], [], [], []
+        out = model if out is None else out
         for i in range(warmup + steps):
             flush_l2()
             e0, e1, k0, k1 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             e0.record(stream)
-            lp.lp_least_model(prog, None, model, frontier=frontier, stream=stream, device_ptrs=True,
-                              iters_out=iters_d, ev_begin=k0, ev_end=k1, stats=stats_d)
+            lp.lp_least_model(pr, v0, out, frontier=frontier, stream=stream, device_ptrs=True,
+                              iters_out=iters_d, ev_begin=k0, ev_end=k1, stats=stats_d,
+                              schedule=schedule, status_out=status_d)
             e1.record(stream)
             stream.synchronize()
+            assert int(status_d.item()) == 0, f"device status {int(status_d.item())}"
             if i >= warmup:
                 tot.append(e0.elapsed_time(e1))
                 ker.append(k0.elapsed_time(k1))
@@ -227,14 +262,15 @@ def main():
     dev_clock = []
     trial_stats = {}
     clocks = ClockSampler(local)
-    timed_least_model(False, 0, args.warmup)            # warm-up
+    timed_least_model(prog, 0, args.warmup)            # warm-up
     barrier()
     clocks.start()
     dev_clock.clear()
-    ms, kms, iters, alg_bytes, st = timed_least_model(False, args.steps, 0)
+    ms, kms, iters, kern_bytes, st = timed_least_model(prog, args.steps, 0)
     main_trials = dict(trial_stats)
     barrier()
     clk = clocks.stop()
+    main_model = model.cpu().numpy().view(np.uint64).copy()
     # the SM clock each timed launch actually ran at (%clock64 / %globaltimer in-kernel)
     clk["nvml_sm_mhz"] = clk.get("sm_mhz")
     if dev_clock:
@@ -248,11 +284,16 @@ def main():
     value = ws * nnz * iters / (ms_max / 1e3)
 
     hbm_peak, peak_src = _peaks()
-    # algorithmic bytes of the launch, counted by the kernel itself (lp_run.stats_out):
-    # the planes each pass streamed + 4 B per body entry / head the verification loaded +
-    # 12 B per derived atom
-    alg_bytes = allmax(alg_bytes)
-    achieved = alg_bytes / (kms_max / 1e3) / 1e9
+    # Roofline of the dominant kernel (lm_full_kernel<false>, one launch = the fixpoint):
+    #   achieved = SURVEY §8(d)'s algorithmic bytes (B_pass x passes) / kernel time, as the
+    #   contract defines it.  The LEAD schedule reads only the live runs' key codes (not
+    #   every CSR entry), so this exceeds the HBM peak: frac > 1 means the work skipped,
+    #   not a bandwidth.  Beside it: the bytes the kernel itself counted and the ncu DRAM
+    #   bytes of one launch, each as a fraction of the peak.
+    b_pass = _model_bytes_per_pass(info, n)
+    model_bytes = b_pass * iters
+    achieved = model_bytes / (kms_max / 1e3) / 1e9
+    kern_bytes = allmax(kern_bytes)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -263,11 +304,22 @@ def main():
         traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic,
-                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram bytes per launch)",
-                "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                "binding": "latency: grid barriers and dependent L2 round trips per pass (the "
+                           "live-run LEAD stream is a small, L2-resident part of the key plane)",
+                "model": "SURVEY §8(d) B_pass = 4 nnz + 4 (R+1) + 4 (H+1) + 2 ceil((n+1)/8), "
+                         "x passes per launch",
+                "model_bytes_per_pass": b_pass, "model_bytes_per_launch": model_bytes,
+                "kernel_bytes_per_launch": kern_bytes,
+                "kernel_gbs": kern_bytes / (kms_max / 1e3) / 1e9,
+                "kernel_frac": kern_bytes / (kms_max / 1e3) / 1e9 / hbm_peak,
+                "traffic_gbs": None if traffic is None else traffic / (kms_max / 1e3) / 1e9,
+                "traffic_frac": None if traffic is None else traffic / (kms_max / 1e3) / 1e9 / hbm_peak,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full: dram read+write bytes "
+                                  "of one launch)",
+                "peak_source": peak_src,
                 "kernel": "lm_full_kernel<false> (persistent: all passes of the fixpoint in one launch)",
                 "passes_per_launch": iters, "lead_passes": st[1], "rows_verified": st[2],
-                "lead_pass_bytes": int(info["lead_pass_bytes"]),
+                "full_key_plane_bytes": int(info["lead_pass_bytes"]),
                 "stream_pass_bytes": int(info["stream_pass_bytes"]), "kernel_ms": kms_max}
 
     out = {
@@ -304,10 +356,13 @@ def main():
         if i >= args.warmup:
             e2e_t.append(e0.elapsed_time(e1))
         assert it == iters
+    # the host-buffer model equals the device-pointer main line's, word for word
+    assert (model_host.numpy().view(np.uint64) == main_model).all()
     e2e_ms = allmax(float(np.mean(e2e_t)))
     out["e2e"] = {"value": ws * nnz * iters / (e2e_ms / 1e3), "unit": "nnz*iter/s",
                   "h2d_bytes_per_step": Wm * 8, "d2h_bytes_per_step": Wm * 8 + 12,
-                  "ms_per_step": e2e_ms, "api": "lp_least_model (host pointers, synchronous)"}
+                  "ms_per_step": e2e_ms, "api": "lp_least_model (host pointers, synchronous)",
+                  "model_check": "equal to the device-pointer main line's model"}
 
     if not args.no_extras and dist:
         # ---- strong-scaling extra: ONE C4 least model sharded by head ranges over the
@@ -325,7 +380,7 @@ def main():
             torch.cuda.synchronize()
             if i >= 1:
                 sh_t.append(e0.elapsed_time(e1))
-        assert it_sh == iters
+        assert it_sh == iters and (m_sh == main_model).all()
         sh_ms = allmax(float(np.mean(sh_t)))
         out["sharded"] = {"ms_per_step": sh_ms, "value": nnz * iters / (sh_ms / 1e3),
                           "unit": "nnz*iter/s", "iters": it_sh, "ranks": ws,
@@ -333,34 +388,73 @@ def main():
         del sharded
 
     if not args.no_extras:
-        # ---- the 8-bit key plane (LP_LOAD_KEY8) on the same workload: fewer bytes per
-        # pass, which then stay L2-resident across passes ----------
+        # ---- the regime that streams M_P: STREAM passes only (every body position, every
+        # pass -- Algorithm 1's u = θ(M v) over all rows), same workload -----
+        sms_, skms, sit, sbytes, sst = timed_least_model(prog, args.steps, args.warmup, schedule="stream")
+        assert sit == iters and (model.cpu().numpy().view(np.uint64) == main_model).all()
+        out["stream"] = {
+            "ms_per_step": allmax(sms_), "kernel_ms": allmax(skms), "iters": sit,
+            "value": ws * nnz * iters / (allmax(sms_) / 1e3), "unit": "nnz*iter/s",
+            "roofline": {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak,
+                         "kernel_bytes_per_launch": sbytes,
+                         "achieved": sbytes / (allmax(skms) / 1e3) / 1e9,
+                         "frac": sbytes / (allmax(skms) / 1e3) / 1e9 / hbm_peak,
+                         "model_achieved": model_bytes / (allmax(skms) / 1e3) / 1e9,
+                         "model_frac": model_bytes / (allmax(skms) / 1e3) / 1e9 / hbm_peak,
+                         "note": "kernel bytes = every body plane streamed each pass (int32 ids, "
+                                 "position-major) + verification; §8(d)'s model adds CSR row "
+                                 "pointers and head grouping this layout does not need"}}
+        # ---- v0 = facts ∪ 1 % random atoms (seeded): atoms outside D2 light the coarse key
+        # buckets, so LEAD passes stream the whole key plane (HBM) -----------------------
+        rng = np.random.default_rng(20251020)
+        extra = rng.choice(n, size=n // 100, replace=False)
+        v0r = torch.from_numpy(lp.pack_mask(np.isin(np.arange(n), np.union1d(facts, extra))).view(np.int64)).cuda()
+        rmodel = torch.zeros_like(model)
+        rms, rkms, rit, rbytes, rst = timed_least_model(prog, args.steps, args.warmup, v0=v0r, out=rmodel)
+        rb = {"ms_per_step": allmax(rms), "kernel_ms": allmax(rkms), "iters": rit,
+              "value": ws * nnz * rit / (allmax(rms) / 1e3), "unit": "nnz*iter/s",
+              "lead_passes": rst[1], "rows_verified": rst[2],
+              "roofline": {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak,
+                           "kernel_bytes_per_launch": rbytes,
+                           "achieved": rbytes / (allmax(rkms) / 1e3) / 1e9,
+                           "frac": rbytes / (allmax(rkms) / 1e3) / 1e9 / hbm_peak,
+                           "model_frac": b_pass * rit / (allmax(rkms) / 1e3) / 1e9 / hbm_peak},
+              "v0": "facts ∪ 1% uniform random atoms (numpy seed 20251020)"}
+        out["random_v0"] = rb
+        del v0r, rmodel
+        # ---- the 8-bit key plane (LP_LOAD_KEY8) on the same workload -----------------------
         prog8 = lp.Program(P, device=local, frontier=False, key8=True)
-        k8 = []
-        for i in range(args.warmup + args.steps):
-            flush_l2()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            lp.lp_least_model(prog8, None, model, stream=stream, device_ptrs=True, iters_out=iters_d,
-                              stats=stats_d)
-            e1.record(stream)
-            stream.synchronize()
-            if i >= args.warmup:
-                k8.append(e0.elapsed_time(e1))
-        assert int(iters_d.item()) == iters
-        k8ms = allmax(float(np.mean(k8)))
-        out["key8"] = {"ms_per_step": k8ms, "value": ws * nnz * iters / (k8ms / 1e3), "unit": "nnz*iter/s",
-                       "algorithmic_bytes_per_launch": int(stats_d[0].item()),
+        k8ms, k8k, k8it, k8b, _ = timed_least_model(prog8, args.steps, args.warmup)
+        assert k8it == iters and (model.cpu().numpy().view(np.uint64) == main_model).all()
+        out["key8"] = {"ms_per_step": allmax(k8ms), "kernel_ms": allmax(k8k),
+                       "value": ws * nnz * iters / (allmax(k8ms) / 1e3), "unit": "nnz*iter/s",
+                       "kernel_bytes_per_launch": k8b,
                        "lead_pass_bytes": int(prog8.info["lead_pass_bytes"]),
-                       "note": "8-bit key codes: the per-pass plane fits L2, so this variant is "
-                               "L2/latency-bound, not HBM-bound (ncu: profiles/r01_ncu_full_c4_key8.md)"}
+                       "note": "8-bit key codes: too many bucket runs for the live-run table, "
+                               "so every LEAD pass streams the whole (L2-resident) plane"}
         prog8.close()
 
         # ---- frontier variant on the same workload --------------------------------------
-        fms, fkms, fit, _, _ = timed_least_model(True, args.steps, args.warmup)
-        assert fit == iters
+        fms, fkms, fit, _, _ = timed_least_model(prog, args.steps, args.warmup, frontier=True)
+        assert fit == iters and (model.cpu().numpy().view(np.uint64) == main_model).all()
         out["frontier"] = {"ms_per_step": allmax(fms), "kernel_ms": allmax(fkms), "iters": fit,
                            "speedup_vs_full": ms_max / allmax(fms)}
+        # ---- the other least-model configurations (latency-bound: time only) -----------
+        cfgs = {}
+        for cname in ("C1", "C2", "C3"):
+            Q = lpgen.config(cname)
+            qp = lp.Program(Q, device=local)
+            qm = torch.zeros(lp.bits_words(Q.n_atoms), dtype=torch.int64, device="cuda")
+            steps_c = args.steps if cname != "C3" else max(3, args.steps // 3)
+            a_ms, a_k, a_it, _, _ = timed_least_model(qp, steps_c, args.warmup, out=qm)
+            f_ms, f_k, f_it, _, _ = timed_least_model(qp, steps_c, args.warmup, frontier=True, out=qm)
+            assert a_it == f_it
+            cfgs[cname] = {"iters": a_it, "full_ms": allmax(a_ms), "full_kernel_ms": allmax(a_k),
+                           "frontier_ms": allmax(f_ms), "frontier_kernel_ms": allmax(f_k),
+                           "us_per_pass_full": 1e3 * allmax(a_k) / a_it,
+                           "nnz": int(qp.info["nnz"])}
+            qp.close()
+        out["configs"] = cfgs
         # ---- stable models ---------------------------------------------------------------
         # guess-sharded under torchrun: rank r solves its 64-aligned slice
         # of the 2^f guesses (lp_run.guess_offset), no exchange until the final gather
@@ -381,12 +475,13 @@ def main():
             if G > 0:
                 lp.lp_stable_models(sprog, None, G, acc, stream=stream, device_ptrs=True,
                                     n_accepted_out=nacc, passes_out=passes, ev_begin=k0,
-                                    ev_end=k1, guess_offset=goff)
+                                    ev_end=k1, guess_offset=goff, status_out=status_d)
             else:
                 k0.record(stream)
                 k1.record(stream)
             e1.record(stream)
             stream.synchronize()
+            assert G == 0 or int(status_d.item()) == 0
             if i >= args.warmup:
                 st_t.append(e0.elapsed_time(e1))
                 st_k.append(k0.elapsed_time(k1))
@@ -403,29 +498,28 @@ def main():
         out["stable"] = stable
         sprog.close()
 
-    # ---- CPU baseline: the oracle as it stands, rank 0, N = 1 only ----------------------
-    if rank == 0 and ws == 1:
+    # ---- CPU baseline (BASELINE.md plan): O-STAGE, fixpoint only, one pinned core, median
+    # of 3 trials; rank 0 at N = 1 only.  Its model also checks the GPU main line. -------
+    if rank == 0 and ws == 1 and not args.no_cpu:
         import oracle
         oracle.build()
         t0 = time.perf_counter()
-        reps, it_cpu = 0, 0
-        while reps < args.cpu_sample_reps and (reps == 0 or time.perf_counter() - t0 < 10.0):
-            _, it1, _, conv = oracle.lm_jacobi(P)      # the whole fixpoint, as it stands
-            assert conv and it1 == iters
-            it_cpu += it1
-            reps += 1
-        dt = time.perf_counter() - t0
-        cpu_model = ""
-        try:
-            with open("/proc/cpuinfo") as f:
-                cpu_model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
-        except OSError:
-            pass
-        out["cpu_baseline"] = {"value": nnz * it_cpu / dt, "unit": "nnz*iter/s", "cores": 1,
-                               "kind": "oracle", "cpu": cpu_model, "host_cores": os.cpu_count(),
-                               "sample": f"{reps} whole fixpoint(s) of O-LM Jacobi (oracle/lp_oracle.c, "
-                                         f"{it_cpu} T_P passes over all of {args.workload}, {dt:.1f} s, "
-                                         f"single thread)"}
+        (om, _, oit, secs), core = _pinned_stage_timed(P, args.cpu_trials)
+        wall = time.perf_counter() - t0
+        assert oit == iters and (oracle.pack_bits(om) == main_model).all(), "GPU model != oracle"
+        med = float(np.median(secs))
+        out["cpu_baseline"] = {"value": nnz * iters / med, "unit": "nnz*iter/s", "cores": 1,
+                               "kind": "oracle", "variant": "O-STAGE", "cpu": _cpu_model(),
+                               "host_cores": os.cpu_count(), "median_ms": med * 1e3,
+                               "trials_ms": [x * 1e3 for x in secs],
+                               "sample": f"{args.cpu_trials} whole O-STAGE fixpoints of {args.workload} "
+                                         f"(oracle/lp_oracle.c stage_core, steady clock around the "
+                                         f"fixpoint only; occurrence lists built once, untimed), "
+                                         f"pinned to core {core}; {wall:.1f} s wall incl. ingest",
+                               "gpu_speedup_full": med * 1e3 / ms_max}
+        if "frontier" in out:
+            out["cpu_baseline"]["gpu_speedup_frontier"] = med * 1e3 / out["frontier"]["ms_per_step"]
+        out["model_check"] = "main-line model == oracle O-STAGE model (bit-exact), iters equal"
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist:

@@ -86,9 +86,8 @@ typedef void (*lp_free_fn)(void *ptr, size_t bytes, void *ctx);
                                     of 16-bit ones (2.125 B/row).  On C4 the per-pass plane
                                     then stays L2-resident: 17% faster, L2/latency-bound
                                     rather than HBM-bound       */
-#define LP_LOAD_TMA 0x2u         /* use the TMA-pipelined full θ-pass (cp.async.bulk ring)
-                                    instead of the register-streaming one; same results,
-                                    slower on B200 for HBM-streaming programs */
+/* (flag 0x2u, the former TMA-ring full θ-pass, was removed: lp_load rejects unknown
+    flag bits with LP_E_INVALID) */
 
 typedef struct {
     int device;             /* CUDA device ordinal; -1 = host-only handle: encode and
@@ -148,7 +147,23 @@ typedef struct {
                                 call is global guess guess_offset + i of the binary
                                 counting order (a multiple of 64; 0 = from the first).
                                 Lets ranks split the 2^f guesses      */
+    int32_t *status_out;     /* optional: the run's final status word, bit flags
+                                LP_ST_* (0 = reached the fixpoint, nothing dropped).
+                                Host mode: a host pointer, filled before the call
+                                returns (the lp_status return value already reflects
+                                it).  LP_PTR_DEVICE: a DEVICE pointer written by the
+                                kernel's epilogue on lp_run.stream -- the only way an
+                                asynchronous call reports LP_ST_OVERFLOW or
+                                LP_ST_GUARD; callers must check it once the stream
+                                has been synchronised.                               */
 } lp_run;
+
+/* lp_run.status_out bit flags (sticky; an overflow is never masked by a cap):      */
+#define LP_ST_GUARD 0x1     /* pass guard (n_ext + 2 passes) hit: LP_E_NOT_CONVERGED  */
+#define LP_ST_OVERFLOW 0x2  /* internal candidate queue overflow: LP_E_CUDA; results
+                               are invalid (cannot happen by construction)           */
+#define LP_ST_CAPPED 0x4    /* stopped at lp_run.max_passes before the fixpoint (not
+                               an error)                                             */
 
 typedef struct {
     int32_t n_atoms;
@@ -167,8 +182,6 @@ typedef struct {
     int32_t summary_shift;    /* atoms per summary bit = 1 << summary_shift            */
     int32_t grid_blocks;      /* CTAs of the persistent kernels                        */
     int32_t block_threads;
-    int32_t full_kernel;      /* 1: TMA-pipelined full θ-pass, 0: register-streaming   */
-    int32_t tma_stages;       /* depth of the TMA shared-memory ring                   */
     int64_t lead_pass_bytes;  /* program bytes a LEAD full θ-pass streams                */
     int64_t stream_pass_bytes;/* program bytes a STREAM full θ-pass streams              */
     int32_t key_shift;        /* summary mode: keys per key-summary bit = 1 << key_shift;

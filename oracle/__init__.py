@@ -56,7 +56,9 @@ def _load():
         _lib.orc_lm_stage.argtypes = [i32, i64, P, P, P, P, P, P]
         _lib.orc_stable.argtypes = [i32, i64, P, P, P, P, i64, P, P, P, P, P, P, P]
         _lib.orc_certify.argtypes = [i32, i64, P, P, P, P, P, P, i32]
-        for f in (_lib.orc_lm_jacobi, _lib.orc_lm_stage, _lib.orc_stable, _lib.orc_certify):
+        _lib.orc_lm_stage_timed.argtypes = [i32, i64, P, P, P, P, P, P, i32, P]
+        for f in (_lib.orc_lm_jacobi, _lib.orc_lm_stage, _lib.orc_stable, _lib.orc_certify,
+                  _lib.orc_lm_stage_timed):
             f.restype = ctypes.c_int
     return _lib
 
@@ -125,6 +127,26 @@ def lm_stage(rules, v0=None):
         raise MemoryError(rc)
     stage = stage[:n]
     return (stage >= 0).astype(np.uint8), stage, iters.value
+
+
+def lm_stage_timed(rules, v0=None, trials: int = 3):
+    """O-STAGE's fixpoint phase timed on its own (bench.py cpu_baseline, BASELINE.md's
+    CPU-baseline plan): occurrence lists built once (untimed), then `trials` runs of the
+    unchanged forward-chaining loop.  Returns (model uint8[n], stage, iters, seconds
+    per trial).  The caller pins the thread to one core."""
+    _definite(rules)
+    lib = _load()
+    head, ptr, atom = _arrays(rules)
+    n = rules.n_atoms
+    stage = np.zeros(max(n, 1), dtype=np.int32)
+    secs = np.zeros(max(trials, 1), dtype=np.float64)
+    iters = ctypes.c_int32(0)
+    rc = lib.orc_lm_stage_timed(n, rules.n_rules, _p(head), _p(ptr), _p(atom), _p(_v0(rules, v0)),
+                                _p(stage), ctypes.byref(iters), int(trials), _p(secs))
+    if rc:
+        raise MemoryError(rc)
+    stage = stage[:n]
+    return (stage >= 0).astype(np.uint8), stage, iters.value, secs[:trials].tolist()
 
 
 def popcounts_from_stage(stage, iters):

@@ -26,9 +26,11 @@
  *     to its fixpoint and accepted iff every pair (a_j, abar_j) sums to exactly 1
  *     (Algorithm 3, read as in DESIGN.md reading R7).
  */
+#define _POSIX_C_SOURCE 199309L
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #define ORC_OK 0
 #define ORC_E_NOMEM 1
@@ -160,6 +162,33 @@ int orc_lm_stage(int32_t n, int64_t R, const int32_t *head, const int64_t *ptr,
     return rc;
 }
 
+/* Timing entry for bench.py's cpu_baseline (BASELINE.md "CPU-baseline plan"): the
+ * occurrence lists are built once (ingest, untimed), then the fixpoint phase --
+ * stage_core, unchanged -- runs `trials` times, each timed with CLOCK_MONOTONIC into
+ * secs[t].  The caller pins the thread (single core).  Results as orc_lm_stage. */
+int orc_lm_stage_timed(int32_t n, int64_t R, const int32_t *head, const int64_t *ptr,
+                       const int32_t *atom, const uint8_t *v0, int32_t *stage,
+                       int32_t *iters_out, int32_t trials, double *secs)
+{
+    int64_t *op = NULL, *orr = NULL;
+    if (build_occ(n, R, ptr, atom, &op, &orr)) return ORC_E_NOMEM;
+    int64_t *cnt = (int64_t *)malloc((size_t)(R > 0 ? R : 1) * sizeof(int64_t));
+    int32_t *queue = (int32_t *)malloc(((size_t)n + 1) * sizeof(int32_t));
+    int rc = ORC_E_NOMEM;
+    if (cnt && queue) {
+        for (int32_t t = 0; t < trials; ++t) {
+            struct timespec t0, t1;
+            clock_gettime(CLOCK_MONOTONIC, &t0);
+            rc = stage_core(n, R, head, ptr, atom, v0, stage, iters_out, op, orr, cnt, queue);
+            clock_gettime(CLOCK_MONOTONIC, &t1);
+            secs[t] = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+            if (rc) break;
+        }
+    }
+    free(op); free(orr); free(cnt); free(queue);
+    return rc;
+}
+
 /* ---------------------------------------------------------------------------------
  * O-STABLE: Algorithms 2-3 per guess column, via P+ (Eq. 4).
  *   neg        : uint8[nnz] literal polarity (NULL = definite program, k = 0)
@@ -183,36 +212,42 @@ int orc_stable(int32_t n, int64_t R, const int32_t *head, const int64_t *ptr,
                int32_t *passes_out, int32_t *k_out, int32_t *f_out)
 {
     int64_t nnz = ptr[R];
+    int rc = ORC_E_NOMEM;
+    int32_t *na = NULL, *freej = NULL, *patom = NULL, *queue = NULL, *stage = NULL;
+    int64_t *op = NULL, *orr = NULL, *cnt = NULL;
+    uint8_t *v0 = NULL, *bar = NULL;
     /* negated atoms, ascending */
     uint8_t *isneg = (uint8_t *)calloc((size_t)n + 1, 1);
     uint8_t *isfact = (uint8_t *)calloc((size_t)n + 1, 1);
     int32_t *jof = (int32_t *)malloc(((size_t)n + 1) * sizeof(int32_t));
-    if (!isneg || !isfact || !jof) return ORC_E_NOMEM;
+    if (!isneg || !isfact || !jof) goto done;
     if (neg)
         for (int64_t j = 0; j < nnz; ++j) if (neg[j]) isneg[atom[j]] = 1;
     for (int64_t r = 0; r < R; ++r) if (ptr[r] == ptr[r + 1]) isfact[head[r]] = 1;
     int32_t k = 0, f = 0;
     for (int32_t a = 0; a < n; ++a) { jof[a] = isneg[a] ? k++ : -1; }
-    int32_t *na = (int32_t *)malloc(((size_t)k + 1) * sizeof(int32_t));
-    int32_t *freej = (int32_t *)malloc(((size_t)k + 1) * sizeof(int32_t));
+    na = (int32_t *)malloc(((size_t)k + 1) * sizeof(int32_t));
+    freej = (int32_t *)malloc(((size_t)k + 1) * sizeof(int32_t));
+    if (!na || !freej) goto done;
     for (int32_t a = 0; a < n; ++a)
         if (isneg[a]) { na[jof[a]] = a; if (!isfact[a]) freej[f++] = jof[a]; }
     *k_out = k; *f_out = f;
-    if (!guess && G != ((int64_t)1 << f)) return ORC_E_ARG;
+    if (!guess && G != ((int64_t)1 << f)) { rc = ORC_E_ARG; goto done; }
 
     /* positive form P+: atoms 0..n-1 original, n+j = abar_j */
     int32_t np = n + k;
-    int32_t *patom = (int32_t *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int32_t));
+    patom = (int32_t *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int32_t));
+    if (!patom) goto done;
     for (int64_t j = 0; j < nnz; ++j)
         patom[j] = (neg && neg[j]) ? n + jof[atom[j]] : atom[j];
 
-    int64_t *op = NULL, *orr = NULL;
-    if (build_occ(np, R, ptr, patom, &op, &orr)) return ORC_E_NOMEM;
-    int64_t *cnt = (int64_t *)malloc((size_t)(R > 0 ? R : 1) * sizeof(int64_t));
-    int32_t *queue = (int32_t *)malloc(((size_t)np + 1) * sizeof(int32_t));
-    int32_t *stage = (int32_t *)malloc(((size_t)np + 1) * sizeof(int32_t));
-    uint8_t *v0 = (uint8_t *)calloc((size_t)np + 1, 1);
-    uint8_t *bar = (uint8_t *)calloc((size_t)k + 1, 1);
+    if (build_occ(np, R, ptr, patom, &op, &orr)) goto done;
+    cnt = (int64_t *)malloc((size_t)(R > 0 ? R : 1) * sizeof(int64_t));
+    queue = (int32_t *)malloc(((size_t)np + 1) * sizeof(int32_t));
+    stage = (int32_t *)malloc(((size_t)np + 1) * sizeof(int32_t));
+    v0 = (uint8_t *)calloc((size_t)np + 1, 1);
+    bar = (uint8_t *)calloc((size_t)k + 1, 1);
+    if (!cnt || !queue || !stage || !v0 || !bar) goto done;
     int64_t words = ((int64_t)n + 63) / 64;
     int32_t kmax_all = 0;
 
@@ -245,9 +280,11 @@ int orc_stable(int32_t n, int64_t R, const int32_t *head, const int64_t *ptr,
         }
     }
     *passes_out = G > 0 ? kmax_all + 1 : 0;
+    rc = ORC_OK;
+done:
     free(isneg); free(isfact); free(jof); free(na); free(freej); free(patom);
     free(op); free(orr); free(cnt); free(queue); free(stage); free(v0); free(bar);
-    return ORC_OK;
+    return rc;
 }
 
 /* ---------------------------------------------------------------------------------

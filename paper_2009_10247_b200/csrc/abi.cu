@@ -52,11 +52,13 @@ struct lp_program {
     int32_t *d_order = nullptr;
     int32_t *d_qbuf = nullptr;  // FILTER-mode candidate queues, [lm_blocks][qcap]
     int32_t qcap = 0;
-    bool use_tma = false;       // TMA-pipelined full pass (else the register-streaming one)
-    TileSeg *d_tsegs = nullptr;
-    int32_t ntseg = 0, stages = 0;
-    int64_t ntiles = 0;
-    size_t tma_smem = 0;
+    // A/B switches of the measurements (environment, read once by lp_load; every setting
+    // computes the same results -- DESIGN.md "A/B switches")
+    int32_t dense_div = 16;     // LP_DENSE_DIV: auto schedule's queued-rows divisor
+    bool env_no_pipe = false;   // LP_NO_PIPE
+    bool env_no_overlap = false;  // LP_NO_OVERLAP
+    bool env_no_ksum_image = false;  // LP_NO_KSUM_IMAGE
+    bool env_no_zerocopy = false;    // LP_NO_ZEROCOPY
     // [0] tail, [2] status (stable path); [1] iters; [3] passes; [4,5] n_accepted;
     // [8,9] least-model tails and [10,11] statuses, alternating by call parity;
     // [12..14] rows queued per full θ-pass (slot k % 3); [16..18] least-model and
@@ -70,6 +72,8 @@ struct lp_program {
     int32_t *d_lead32 = nullptr;    // exact mode: flat lead plane
     uint16_t *d_xlead16 = nullptr, *d_xhead16 = nullptr, *d_xtag = nullptr;   // exact 16-bit planes
     int32_t *d_key_of = nullptr;
+    int4 *d_runs = nullptr;         // key mode: bucket runs (first octet, octets, bucket, 0)
+    int32_t nruns = 0;              //   0: no table (LEAD passes stream every octet)
     int32_t *d_korder = nullptr;
     int32_t ksm_words = 0, kshift = 0;
     uint32_t *d_factbits = nullptr, *d_init_bits = nullptr;
@@ -226,8 +230,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     TRY(dalloc(p, &p->d_model, mw));
 
     // shared-memory plan: exact truth vector if it fits, else a summary
-    // (leave room for a 2-stage TMA ring at least)
-    int64_t cap = std::min<int64_t>(kMaxSmemBytes, kSmemLimit - (int64_t)lm_tma_smem_bytes(0, 2) - 128);
+    int64_t cap = kMaxSmemBytes;
     if (opt && opt->smem_bits_cap > 0) cap = std::min<int64_t>(cap, opt->smem_bits_cap / 8);
     cap = std::max<int64_t>(cap, 16);
     if ((int64_t)p->nwords * 4 <= cap) {
@@ -258,8 +261,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     // kb = 16 (default: a uint16 per row + a uint8 tag per 8-row octet, 2.125 B/row) or
     // kb = 8 (LP_LOAD_KEY8: a byte per row + a uint16 tag per octet, 1.25 B/row); runs of
     // one bucket padded to 8 rows.
-    const bool want_keys = !p->exact && !(opt && (opt->flags & LP_LOAD_TMA)) &&
-                           !std::getenv("LP_NO_KEYS");
+    const bool want_keys = !p->exact && !std::getenv("LP_NO_KEYS");
     std::vector<Run> runs;
     if (want_keys) {
         std::vector<uint8_t> der((size_t)L.n_ext, 0);   // D2 (encode.cpp), abar atoms, ⊤
@@ -325,6 +327,15 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
                 else tag16[(size_t)o] = (uint16_t)t;
             }
         }
+        // the run table of the live-run skip: runs tile the slot
+        // space in slot order, each a multiple of 8 rows
+        if (runs.size() <= (size_t)kMaxRuns && !std::getenv("LP_NO_LIVE_RUNS")) {
+            std::vector<int4> rt;
+            for (const Run &r : runs)
+                rt.push_back(make_int4((int)(r.slot_off / 8), (int)(r.rows_pad / 8), r.bucket, 0));
+            TRY(upload(p, &p->d_runs, rt));
+            p->nruns = (int32_t)rt.size();
+        }
         if (kb == 16) {
             uint16_t *c;
             uint8_t *t;
@@ -380,8 +391,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     // head bucket << 5 | trailing padding << 10): 4.25 bytes per row instead of 8
     // (programs of >= 1 M rows: below that the stream is a few microseconds either way and
     // 8-row octets leave more threads idle than 4-row quads -- C2 measured 6 % slower)
-    if (p->exact && L.n_ext <= (1 << 21) && L.n_slots >= (1 << 20) &&
-        !(opt && (opt->flags & LP_LOAD_TMA)) && !std::getenv("LP_NO_EXACT16")) {
+    if (p->exact && L.n_ext <= (1 << 21) && L.n_slots >= (1 << 20) && !std::getenv("LP_NO_EXACT16")) {
         std::vector<Run> xr;
         bucket_rows_by(&L, [](int32_t lead, int32_t head) { return (lead >> 16) | ((head >> 16) << 5); }, 8, &xr);
         std::vector<uint16_t> l16((size_t)std::max<int64_t>(L.n_slots, 8), 0), h16(l16.size(), 0);
@@ -456,39 +466,8 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(dalloc(p, &p->d_st_ring, 3 * ((size_t)L.n_ext + 1)));
     }
 
-    // TMA tile plan: every segment cut into 16 KB tiles of
-    // T rows; the head row is staged too when the truth test is exact
-    p->use_tma = (opt && (opt->flags & LP_LOAD_TMA)) && (int)L.segs.size() <= kMaxTileSegs;
-    if (p->use_tma) {
-        std::vector<TileSeg> ts;
-        int64_t toff = 0;
-        const int extra = p->exact ? 1 : 0;
-        for (const Segment &sg : L.segs) {
-            TileSeg t{};
-            t.L = sg.L;
-            t.T = (int32_t)((kStageBytes / (4 * (int64_t)(sg.L + extra))) & ~3LL);
-            if (t.T < 4) { p->use_tma = false; break; }
-            t.tile_off = toff;
-            t.col_off = sg.col_off;
-            t.count_pad = sg.count_pad;
-            t.slot_off = sg.slot_off;
-            toff += (sg.count_pad + t.T - 1) / t.T;
-            ts.push_back(t);
-        }
-        if (p->use_tma) {
-            p->ntiles = toff;
-            p->ntseg = (int32_t)ts.size();
-            TRY(upload(p, &p->d_tsegs, ts));
-            p->stages = (int32_t)std::min<int64_t>(
-                8, (kSmemLimit - (int64_t)lm_tma_smem_bytes(p->sm_words, 0)) / kStageBytes);
-            if (p->stages < 2) p->use_tma = false;
-            p->tma_smem = lm_tma_smem_bytes(p->sm_words, p->stages);
-        }
-    }
-
     CK(prepare_kernels(p->lm_smem, p->st_smem));
-    const int bl = p->use_tma ? lm_tma_blocks_per_sm(p->exact, p->tma_smem)
-                              : lm_full_blocks_per_sm(p->exact, p->lm_smem);
+    const int bl = lm_full_blocks_per_sm(p->exact, p->lm_smem);
     const int bf = lm_frontier_blocks_per_sm();
     const int bs = st_blocks_per_sm(p->st_smem);
     if (bl < 1 || bf < 1 || bs < 1) return set_err(LP_E_CUDA, "persistent kernels do not fit on an SM");
@@ -501,11 +480,8 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         // LEAD passes queue in both truth modes, STREAM passes in summary mode
         const int64_t gthreads = (int64_t)p->lm_blocks * kFullThreads;
         int64_t cap = 0;
-        if (p->use_tma)  // a CTA consumes at most ceil(ntiles / grid) tiles of <= 4096 rows
-            cap = (p->ntiles + p->lm_blocks - 1) / p->lm_blocks * (kStageBytes / 4);
-        else
-            for (const Segment &sg : L.segs)
-                cap += 4 * (int64_t)kFullThreads * (((sg.count_pad >> 2) + gthreads - 1) / gthreads);
+        for (const Segment &sg : L.segs)
+            cap += 4 * (int64_t)kFullThreads * (((sg.count_pad >> 2) + gthreads - 1) / gthreads);
         // key-mode LEAD passes: octets are dealt cyclically over all threads
         int64_t octets = 0;
         for (const Run &r : runs) octets += r.rows_pad >> 3;
@@ -556,6 +532,15 @@ extern "C" lp_status lp_load(const lp_rules *rules, const lp_options *opt, lp_pr
         delete p;
         return set_err(LP_E_INVALID, "alloc and free hooks must be given together");
     }
+    if (opt && (opt->flags & ~(uint32_t)(LP_LOAD_NO_FRONTIER | LP_LOAD_PAPER_LAYOUT | LP_LOAD_KEY8))) {
+        delete p;
+        return set_err(LP_E_INVALID, "unknown lp_options.flags bit (0x2, the former TMA ring, was removed)");
+    }
+    if (const char *e = std::getenv("LP_DENSE_DIV")) p->dense_div = std::max(1, std::atoi(e));
+    p->env_no_pipe = std::getenv("LP_NO_PIPE") != nullptr;
+    p->env_no_overlap = std::getenv("LP_NO_OVERLAP") != nullptr;
+    p->env_no_ksum_image = std::getenv("LP_NO_KSUM_IMAGE") != nullptr;
+    p->env_no_zerocopy = std::getenv("LP_NO_ZEROCOPY") != nullptr;
     const bool occ = !(opt && (opt->flags & LP_LOAD_NO_FRONTIER));
     std::string err;
     lp_status s;
@@ -615,9 +600,7 @@ extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
     o->key_shift = p->d_lead_codes ? p->kshift : -1;
     o->summary_shift = p->shift;
     o->grid_blocks = p->lm_blocks;
-    o->full_kernel = p->use_tma ? 1 : 0;
-    o->tma_stages = p->stages;
-    o->block_threads = p->use_tma ? kThreads : kFullThreads;
+    o->block_threads = kFullThreads;
     return LP_OK;
 }
 
@@ -632,12 +615,20 @@ extern "C" lp_status lp_negated_atoms(const lp_program *p, int32_t *out) {
 // lp_least_model
 // ------------------------------------------------------------------------------------
 
+// The kernels' status word (bit flags kSt*, kernels.h) as an lp_status: an overflow is
+// checked first (it is never masked by a cap or the guard); kStCapped alone is success.
+static lp_status status_of(int32_t s) {
+    if (s & kStOverflow) return set_err(LP_E_CUDA, "internal: candidate queue overflow");
+    if (s & kStGuard) return set_err(LP_E_NOT_CONVERGED, "pass guard exceeded");
+    return LP_OK;
+}
+
 // Host-pointer calls: a page-locked, mapped host buffer for the model (cudaHostAlloc /
 // pinned torch tensors under unified addressing) is written by the kernel's epilogue
 // itself over PCIe -- no staging buffer, no copy-engine round trip (C4 e2e 0.335 ->
 // 0.320 ms).  Pageable memory: NULL (staged copy).
 static void *mapped_host_ptr(const void *ptr) {
-    if (!ptr || std::getenv("LP_NO_ZEROCOPY")) return nullptr;
+    if (!ptr) return nullptr;
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
         cudaGetLastError();
@@ -715,6 +706,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.tail = p->d_scal + 8 + par;
     q.tail_next = p->d_scal + 8 + (par ^ 1);
     q.status_out = p->d_scal + 10 + par;
+    q.status_user = (dev && run) ? run->status_out : nullptr;
     q.status_next = p->d_scal + 10 + (par ^ 1);
     q.v0 = v0d;
     q.v0_words = (int32_t)(mw * 2);
@@ -722,10 +714,10 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.init_bits = p->d_init_bits;
     q.init_list = p->d_init_list;
     q.init_klist = p->d_init_klist;
-    q.init_ksum = std::getenv("LP_NO_KSUM_IMAGE") ? nullptr : p->d_init_ksum;
+    q.init_ksum = p->env_no_ksum_image ? nullptr : p->d_init_ksum;
     q.n_init = p->n_init;
     q.top = L.top;
-    void *const mout_mapped = dev ? nullptr : mapped_host_ptr(model_out);   // (epilogue writes over PCIe)
+    void *const mout_mapped = (dev || p->env_no_zerocopy) ? nullptr : mapped_host_ptr(model_out);   // (epilogue writes over PCIe)
     unsigned long long *mout = dev ? reinterpret_cast<unsigned long long *>(model_out)
                                : mout_mapped ? reinterpret_cast<unsigned long long *>(mout_mapped) : p->d_model;
     q.model_out = mout;
@@ -743,19 +735,13 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.dbg = debug_timing();
     q.qbuf = p->d_qbuf;
     q.qcap = p->qcap;
-    q.tsegs = p->d_tsegs;
-    q.ntseg = p->ntseg;
-    q.stages = p->stages;
-    q.ntiles = p->ntiles;
-    q.heads_staged = p->exact ? 1 : 0;
-    q.tma_variant = std::getenv("LP_TMA_VARIANT") ? std::atoi(std::getenv("LP_TMA_VARIANT")) : 0;
     q.pass_mode = (flags & LP_FULL_STREAM) ? 2 : (flags & LP_FULL_LEAD) ? 1 : 0;
-    q.dense_div = std::getenv("LP_DENSE_DIV") ? std::max(1, std::atoi(std::getenv("LP_DENSE_DIV"))) : 16;
+    q.dense_div = p->dense_div;
     q.n_slots = L.n_slots;
     q.cand = p->d_scal + 12;
     q.vent = p->d_vent;
-    q.overlap = std::getenv("LP_NO_OVERLAP") ? 0 : 1;
-    const bool pipe = q.overlap && !(flags & LP_FULL_NO_PIPE) && !std::getenv("LP_NO_PIPE");
+    q.overlap = p->env_no_overlap ? 0 : 1;
+    const bool pipe = q.overlap && !(flags & LP_FULL_NO_PIPE) && !p->env_no_pipe;
     q.locc_ptr = pipe ? p->d_locc_ptr : nullptr;
     q.locc_slot = p->d_locc_slot;
     q.pbar = reinterpret_cast<uint32_t *>(p->d_scal + 24);
@@ -770,20 +756,22 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.pcnt = p->d_scal + 16;
     unsigned long long *stats_dev = nullptr;
     if (run && run->stats_out) stats_dev = dev ? reinterpret_cast<unsigned long long *>(run->stats_out) : p->d_stats;
-    if (stats_dev && (frontier || p->use_tma)) {   // only the register-streaming full pass counts
+    if (stats_dev && frontier) {   // only the full θ-pass counts
         if (dev) CK(cudaMemsetAsync(stats_dev, 0, 6 * sizeof(uint64_t), st));
         else std::memset(run->stats_out, 0, 6 * sizeof(uint64_t));
         stats_dev = nullptr;
     }
     q.stats = stats_dev;
-    q.lead_codes = (frontier || p->use_tma) ? nullptr : p->d_lead_codes;
+    q.lead_codes = frontier ? nullptr : p->d_lead_codes;
     q.octet_tag = p->d_octet_tag;
     q.key_bits = p->key_bits;
-    q.lead32 = (frontier || p->use_tma) ? nullptr : p->d_lead32;
-    q.xlead16 = (frontier || p->use_tma) ? nullptr : p->d_xlead16;
+    q.lead32 = frontier ? nullptr : p->d_lead32;
+    q.xlead16 = frontier ? nullptr : p->d_xlead16;
     q.xhead16 = p->d_xhead16;
     q.xtag = p->d_xtag;
     q.key_of = p->d_key_of;
+    q.runs = p->d_runs;
+    q.nruns = p->nruns;
     q.korder = p->d_korder;
     q.ksm_words = p->ksm_words;
     q.kshift = p->kshift;
@@ -791,7 +779,6 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.stream_bytes = (long long)stream_plane_bytes(p);
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
     if (frontier) CK(launch_lm_frontier(q, p->fr_blocks, st));
-    else if (p->use_tma) CK(launch_lm_tma(q, p->exact, p->lm_blocks, p->tma_smem, st));
     else CK(launch_lm_full(q, p->exact, p->lm_blocks, p->lm_smem, st));
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
     ++p->lm_runs;
@@ -809,10 +796,9 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
         CK(cudaMemcpyAsync(run->stats_out, stats_dev, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     *iters_out = scal[1];
+    if (run && run->status_out) *run->status_out = scal[2];
     if (run && run->converged_out) *run->converged_out = scal[2] == 0 ? 1 : 0;
-    if (scal[2] == 2) return set_err(LP_E_CUDA, "internal: candidate queue overflow");
-    if (scal[2] == 1) return set_err(LP_E_NOT_CONVERGED, "pass guard exceeded");
-    return LP_OK;   // (status 3: stopped at lp_run.max_passes before the fixpoint)
+    return status_of(scal[2]);
 }
 
 // ------------------------------------------------------------------------------------
@@ -849,6 +835,7 @@ static STParams st_params(lp_program *p) {
     s.mark = p->d_mark;
     s.passes_out = p->d_scal + 3;
     s.status_out = p->d_scal + 2;
+    s.status_user = nullptr;
     s.max_passes = L.n_ext + 2;
     return s;
 }
@@ -925,6 +912,7 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
                           : reinterpret_cast<long long *>(p->d_scal + 4);
     STParams s = st_params(p);
     if (dev) s.passes_out = passes_out;
+    if (dev && run) s.status_user = run->status_out;
     const bool full_clear = !(p->st_dirty_ok && p->st_last_Wp == Wp);
     if (full_clear) {   // first call, or a new matrix layout: both buffers from zero
         const size_t tbytes = (size_t)L.n_ext * Wp * sizeof(unsigned long long);
@@ -961,8 +949,8 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
     int64_t na;
     std::memcpy(&na, scal + 4, sizeof(na));
     *n_accepted_out = na;
-    if (scal[2] != 0) return set_err(LP_E_NOT_CONVERGED, "pass guard exceeded");
-    return LP_OK;
+    if (run && run->status_out) *run->status_out = scal[2];
+    return status_of(scal[2]);
 }
 
 extern "C" lp_status lp_stable_matrix(lp_program *p, uint64_t *out, const lp_run *run) {
@@ -1017,6 +1005,6 @@ extern "C" const char *lp_last_error(void) { return g_err.c_str(); }
 
 // Profiling hook, not part of include/lp.h: a device buffer of [16 passes][grid][8]
 // uint64 %globaltimer stamps per CTA (pass top, stream start, stream done, verify done,
-// CTA done, barrier exit; the TMA kernel fills 0, 2, 4, 5) written by the next full
+// CTA done, barrier exit) written by the next full
 // θ-pass launch; NULL disables.
 extern "C" void lpdbg_set_timing(void *buf) { set_debug_timing((unsigned long long *)buf); }

@@ -119,14 +119,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity) : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
-                                         uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy) : "memory");
-}
-
 __device__ __forceinline__ void bulk_g2s_plain(void *dst, const void *src, uint32_t bytes,
                                                uint64_t *bar) {
     asm volatile(
@@ -424,7 +416,7 @@ __device__ __forceinline__ int verify_slot(const LMParams &p, const PassCtx &c, 
 __device__ __forceinline__ void enqueue(const LMParams &p, const PassCtx &c, int32_t slot0,
                                         unsigned fire) {
     int32_t pos = atomicAdd(c.qcount, __popc(fire));
-    if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
+    if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicOr(p.status_out, kStOverflow);
 #pragma unroll
     for (int e = 0; e < 4; ++e)
         if ((fire >> e) & 1u) qput(p, c, pos++, slot0 + e);
@@ -588,19 +580,98 @@ struct OctT {
     }
 };
 
+// Live runs.  The rows of each segment lie in runs of one lead
+// bucket, and a run whose bucket has no set summary bit cannot hold a candidate -- so a
+// key-mode LEAD pass streams only the octets of the live runs, never loading the others'
+// codes.  Each CTA lists them in shared memory at the pass top (one warp, from the run
+// table copied in at launch): beg[r] = first octet of live run r, pre[r] = live octets
+// before it, pre[m] = total.  The stream deals VIRTUAL octet indices 0..total-1 over its
+// threads and maps them through the list with a forward-only cursor (a thread's
+// indices only grow).  With no table the list is the single range [0, n_slots / 8).
+struct LiveList {
+    const int32_t *beg;
+    const int32_t *pre;
+    int32_t total;
+};
+
+__device__ __forceinline__ bool bucket_any(const uint32_t *bm, uint32_t b);
+
+// warp 0 of the CTA; the caller synchronises the CTA afterwards
+__device__ __forceinline__ void build_live(const LMParams &p, const uint32_t *bmask, const int4 *runs_sm,
+                                           int32_t *beg, int32_t *pre, int32_t *total) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    if (p.nruns == 0) {
+        if (lane == 0) {
+            beg[0] = 0;
+            pre[0] = 0;
+            pre[1] = (int32_t)(p.n_slots >> 3);
+            *total = (int32_t)(p.n_slots >> 3);
+            if (blockIdx.x == 0 && p.stats)
+                atomicAdd(p.stats + 0, (unsigned long long)(p.n_slots >> 3) * (p.key_bits == 8 ? 10ull : 17ull));
+        }
+        return;
+    }
+    int32_t m = 0, tot = 0;
+    for (int32_t i0 = 0; i0 < p.nruns; i0 += 32) {
+        const int32_t i = i0 + lane;
+        int4 r = make_int4(0, 0, 0, 0);
+        bool live = false;
+        if (i < p.nruns) {
+            r = runs_sm[i];
+            live = bucket_any(bmask, (uint32_t)r.z);
+        }
+        const int32_t len = live ? r.y : 0;
+        int32_t inc = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, live);
+        if (live) {
+            const int32_t k = m + __popc(bal & ((1u << lane) - 1u));
+            beg[k] = r.x;
+            pre[k] = tot + inc - len;
+        }
+        m += __popc(bal);
+        tot += __shfl_sync(0xFFFFFFFFu, inc, 31);
+    }
+    if (lane == 0) {
+        pre[m] = tot;   // sentinel: the cursor never passes the last live run
+        *total = tot;
+        if (blockIdx.x == 0 && p.stats)   // the pass's streamed bytes: codes + tag per octet
+            atomicAdd(p.stats + 0, (unsigned long long)tot * (p.key_bits == 8 ? 10ull : 17ull));
+    }
+}
+
+// Octet indices of virtual indices vq0 + u * gth (u = 0..U-1); -1 past the total.
+template <int U>
+__device__ __forceinline__ void live_octets(const LiveList &lv, int32_t vq0, int32_t gth, int32_t &cur,
+                                            int32_t (&q)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int32_t vq = vq0 + u * gth;
+        if (vq < lv.total) {
+            while (lv.pre[cur + 1] <= vq) ++cur;
+            q[u] = lv.beg[cur] + (vq - lv.pre[cur]);
+        } else {
+            q[u] = -1;
+        }
+    }
+}
+
 template <int U, int KB>
-__device__ __forceinline__ void oct_load(const LMParams &p, int32_t q0, int32_t gth,
+__device__ __forceinline__ void oct_load(const LMParams &p, const int32_t (&q)[U],
                                          typename OctT<KB>::vec (&v)[U], uint32_t (&tag)[U]) {
     using T = OctT<KB>;
-    const int32_t no = (int32_t)(p.n_slots >> 3);
     const typename T::vec *base = reinterpret_cast<const typename T::vec *>(p.lead_codes);
     const typename T::tag *tb = reinterpret_cast<const typename T::tag *>(p.octet_tag);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int32_t q = q0 + u * gth;
-        if (q < no) {
-            v[u] = T::load(base + q);
-            tag[u] = (uint32_t)__ldg(tb + q);
+        if (q[u] >= 0) {
+            v[u] = T::load(base + q[u]);
+            tag[u] = (uint32_t)__ldg(tb + q[u]);
         } else {
             v[u] = typename T::vec{};
             tag[u] = 0u;
@@ -609,14 +680,13 @@ __device__ __forceinline__ void oct_load(const LMParams &p, int32_t q0, int32_t 
 }
 
 template <int U, int KB>
-__device__ __forceinline__ void oct_test(const LMParams &p, const PassCtx &c, int32_t q0, int32_t gth,
+__device__ __forceinline__ void oct_test(const LMParams &p, const PassCtx &c, const int32_t (&qi)[U],
                                          const typename OctT<KB>::vec (&v)[U], const uint32_t (&tag)[U]) {
     using T = OctT<KB>;
-    const int32_t no = (int32_t)(p.n_slots >> 3);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int32_t q = q0 + u * gth;
-        if (q >= no) break;
+        const int32_t q = qi[u];
+        if (q < 0) break;
         const uint32_t b = tag[u] & T::bmask;
         if (!bucket_any(c.bmask, b)) continue;            // bucket with no true key
         const uint32_t hi = b << KB;
@@ -626,7 +696,7 @@ __device__ __forceinline__ void oct_test(const LMParams &p, const PassCtx &c, in
         fire &= 0xFFu >> (tag[u] >> T::pshift);           // trailing padding rows
         if (fire) {
             int32_t pos = atomicAdd(c.qcount, __popc(fire));
-            if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
+            if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicOr(p.status_out, kStOverflow);
             const int32_t s0 = q * 8;
             for (unsigned f = fire; f; f &= f - 1) qput(p, c, pos++, s0 + __ffs(f) - 1);
         }
@@ -636,23 +706,25 @@ __device__ __forceinline__ void oct_test(const LMParams &p, const PassCtx &c, in
 // (issuing the first loads before the pass-top delta update, so they overlap its
 // latency, measured slower: they compete with the delta's loads and add spills)
 template <int U, int KB>
-__device__ __forceinline__ void octets_lead_kb(const LMParams &p, const PassCtx &c, int64_t gtid,
-                                               int64_t gthreads) {
-    const int32_t no = (int32_t)(p.n_slots >> 3);
+__device__ __forceinline__ void octets_lead_kb(const LMParams &p, const PassCtx &c, const LiveList &lv,
+                                               int64_t gtid, int64_t gthreads) {
     const int32_t gth = (int32_t)gthreads;
-    for (int32_t q0 = (int32_t)gtid; q0 < no; q0 += gth * U) {
+    int32_t cur = 0;
+    for (int32_t q0 = (int32_t)gtid; q0 < lv.total; q0 += gth * U) {
         typename OctT<KB>::vec v[U];
         uint32_t tag[U];
-        oct_load<U, KB>(p, q0, gth, v, tag);
-        oct_test<U, KB>(p, c, q0, gth, v, tag);
+        int32_t q[U];
+        live_octets<U>(lv, q0, gth, cur, q);
+        oct_load<U, KB>(p, q, v, tag);
+        oct_test<U, KB>(p, c, q, v, tag);
     }
 }
 
 // (16-bit codes: 4 octets = 64 bytes in flight per thread; 8-bit codes: 8 octets)
-__device__ __forceinline__ void octets_lead(const LMParams &p, const PassCtx &c, int64_t gtid,
-                                            int64_t gthreads) {
-    if (p.key_bits == 8) octets_lead_kb<LP_OCT_U, 8>(p, c, gtid, gthreads);
-    else octets_lead_kb<4, 16>(p, c, gtid, gthreads);
+__device__ __forceinline__ void octets_lead(const LMParams &p, const PassCtx &c, const LiveList &lv,
+                                            int64_t gtid, int64_t gthreads) {
+    if (p.key_bits == 8) octets_lead_kb<LP_OCT_U, 8>(p, c, lv, gtid, gthreads);
+    else octets_lead_kb<4, 16>(p, c, lv, gtid, gthreads);
 }
 
 // LEAD pass in exact mode over the 16-bit planes: 8 rows per 16-byte load of each plane
@@ -690,7 +762,7 @@ __device__ __forceinline__ void octets_exact16(const LMParams &p, const PassCtx 
             fire &= 0xFFu >> (tag[u] >> 10);                  // trailing padding rows
             if (fire) {
                 int32_t pos = atomicAdd(c.qcount, __popc(fire));
-                if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicExch(p.status_out, 2);
+                if (pos + __popc(fire) > p.qcap + kSmemQueue) atomicOr(p.status_out, kStOverflow);
                 for (unsigned f = fire; f; f &= f - 1) qput(p, c, pos++, q * 8 + __ffs(f) - 1);
             }
         }
@@ -838,21 +910,23 @@ __device__ __forceinline__ int32_t pipe_qget(const int32_t *sq, const int32_t *g
 
 template <int U, int KB>
 __device__ __forceinline__ void pipe_stream_kb(const LMParams &p, const uint32_t *sm, const uint32_t *bmask,
-                                               int32_t *sq, int32_t *gq, int32_t *qcnt,
+                                               const LiveList &lv, int32_t *sq, int32_t *gq, int32_t *qcnt,
                                                const volatile int32_t *abandon, int64_t gtid,
                                                int64_t gthreads) {
     using T = OctT<KB>;
-    const int32_t no = (int32_t)(p.n_slots >> 3);
     const int32_t gth = (int32_t)gthreads;
-    for (int32_t q0 = (int32_t)gtid; q0 < no; q0 += gth * U) {
+    int32_t cur = 0;
+    for (int32_t q0 = (int32_t)gtid; q0 < lv.total; q0 += gth * U) {
         if (*abandon) break;
         typename T::vec v[U];
         uint32_t tag[U];
-        oct_load<U, KB>(p, q0, gth, v, tag);
+        int32_t qi[U];
+        live_octets<U>(lv, q0, gth, cur, qi);
+        oct_load<U, KB>(p, qi, v, tag);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int32_t q = q0 + u * gth;
-            if (q >= no) break;
+            const int32_t q = qi[u];
+            if (q < 0) break;
             const uint32_t b = tag[u] & T::bmask;
             if (!bucket_any(bmask, b)) continue;
             const uint32_t hi = b << KB;
@@ -862,7 +936,7 @@ __device__ __forceinline__ void pipe_stream_kb(const LMParams &p, const uint32_t
             fire &= 0xFFu >> (tag[u] >> T::pshift);
             if (fire) {
                 int32_t pos = atomicAdd(qcnt, __popc(fire));
-                if (pos + __popc(fire) > p.qcap + kPipeSq) atomicExch(p.status_out, 2);
+                if (pos + __popc(fire) > p.qcap + kPipeSq) atomicOr(p.status_out, kStOverflow);
                 const int32_t s0 = q * 8;
                 for (unsigned f = fire; f; f &= f - 1, ++pos) {
                     if (pos < kPipeSq) sq[pos] = s0 + __ffs(f) - 1;
@@ -874,10 +948,10 @@ __device__ __forceinline__ void pipe_stream_kb(const LMParams &p, const uint32_t
 }
 
 __device__ __forceinline__ void pipe_stream(const LMParams &p, const uint32_t *sm, const uint32_t *bmask,
-                                            int32_t *sq, int32_t *gq, int32_t *qcnt,
+                                            const LiveList &lv, int32_t *sq, int32_t *gq, int32_t *qcnt,
                                             const volatile int32_t *abandon, int64_t gtid, int64_t gthreads) {
-    if (p.key_bits == 8) pipe_stream_kb<LP_OCT_U, 8>(p, sm, bmask, sq, gq, qcnt, abandon, gtid, gthreads);
-    else pipe_stream_kb<4, 16>(p, sm, bmask, sq, gq, qcnt, abandon, gtid, gthreads);
+    if (p.key_bits == 8) pipe_stream_kb<LP_OCT_U, 8>(p, sm, bmask, lv, sq, gq, qcnt, abandon, gtid, gthreads);
+    else pipe_stream_kb<4, 16>(p, sm, bmask, lv, sq, gq, qcnt, abandon, gtid, gthreads);
 }
 
 struct PipeExit {
@@ -890,9 +964,16 @@ struct PipeExit {
 // epilogue) or until the auto schedule asks for STREAM passes (returns the state the
 // unpipelined loop resumes from).  All threads of the CTA call it; the shared key
 // summary of v_0 is already built.
+struct LiveShared {      // the CTA's run table and live list (shared memory)
+    const int4 *runs;
+    int32_t *beg;
+    int32_t *pre;
+    int32_t *total;
+};
+
 __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32_t *bmask,
                                          const Segment *segs, int32_t *squeue, int32_t n0,
-                                         long long clk0, unsigned long long ns0) {
+                                         long long clk0, unsigned long long ns0, LiveShared ls) {
     __shared__ int32_t qcnt[2];
     __shared__ int32_t abandon;
     __shared__ int32_t s_t, s_queued;
@@ -935,7 +1016,8 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         const PassCtx c{p.buf0, p.buf1, sm, nullptr, nullptr, 0, bmask, segs, nullptr, p.pcnt, n0};
         int loaded = 0;
         if (!verifier) {
-            pipe_stream(p, sm, bmask, sq[0], gq[0], &qcnt[0], &abandon, (int64_t)blockIdx.x * vbase + tid,
+            const LiveList lv{ls.beg, ls.pre, *ls.total};   // (built before the call)
+            pipe_stream(p, sm, bmask, lv, sq[0], gq[0], &qcnt[0], &abandon, (int64_t)blockIdx.x * vbase + tid,
                         (int64_t)gridDim.x * vbase);
             __syncwarp();
             if (lane == 0) {
@@ -988,15 +1070,15 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         // ---- pass k is complete: [de, t) are its appends
         const uint32_t *wr_k = (k & 1) ? p.buf0 : p.buf1;
         if (lead && p.stats) {
-            atomicAdd(p.stats + 0, (unsigned long long)p.lead_bytes + 4ull * (unsigned long long)queued +
-                                       12ull * (unsigned long long)(t - de));
+            atomicAdd(p.stats + 0, 4ull * (unsigned long long)queued + 12ull * (unsigned long long)(t - de));
             p.stats[1] += 1;
             p.stats[2] += (unsigned long long)queued;
         }
         if (t == de || k + 1 >= p.max_passes || k + 1 == p.user_cap) {
             if (lead) {
                 *p.iters_out = k + 1;
-                if (t != de) atomicMax(p.status_out, k + 1 == p.user_cap ? 3 : 1);
+                if (t != de) atomicOr(p.status_out, k + 1 == p.user_cap ? kStCapped : kStGuard);
+                if (p.status_user) *p.status_user = atomicOr(p.status_out, 0);
                 if (p.stats) {
                     atomicAdd(p.stats + 0, 4ull * p.stats[3]);
                     p.stats[4] = (unsigned long long)(clock64() - clk0);
@@ -1022,6 +1104,12 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
             abandon = 0;
         }
         __syncthreads();
+        // the live runs of summary(v_{k+1}) (the verifier warps fold Δ_{k+1} into the summary
+        // only after this phase's barrier, and the rows of its new lead atoms come from the
+        // lead-occurrence lists, so the list need not follow them)
+        build_live(p, bmask, ls.runs, ls.beg, ls.pre, ls.total);
+        __syncthreads();
+        const LiveList lv{ls.beg, ls.pre, *ls.total};
         ds = de;
         de = t;
         // ---- phase j = k + 1
@@ -1130,7 +1218,7 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         } else {
             // pass j+1's candidates: rows whose lead key is in summary(v_j)
             const int64_t sgtid = (int64_t)blockIdx.x * vbase + tid;
-            pipe_stream(p, sm, bmask, sq[j & 1], gq[j & 1], &qcnt[j & 1], &abandon, sgtid,
+            pipe_stream(p, sm, bmask, lv, sq[j & 1], gq[j & 1], &qcnt[j & 1], &abandon, sgtid,
                         (int64_t)gridDim.x * vbase);
             if (p.dbg && j < 16 && lane == 0) atomicMax(&PDBG(j, 2), globaltimer());
         }
@@ -1162,11 +1250,16 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     __shared__ int32_t squeue[kSmemQueue];
     __shared__ int32_t streamers_done;
     __shared__ __align__(8) uint64_t fill_bar;
+    __shared__ int4 runs_sm[kMaxRuns];              // key mode: the run table (LMParams.runs)
+    __shared__ int32_t live_beg[kMaxRuns];          //   and this pass's live list
+    __shared__ int32_t live_pre[kMaxRuns + 1];
+    __shared__ int32_t live_tot;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const bool lead = blockIdx.x == 0 && tid == 0;
+    const LiveShared ls{runs_sm, live_beg, live_pre, &live_tot};
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 6] = globaltimer();
     __shared__ long long clk0;          // SM clock over the launch (lp_run.stats_out[4..5]);
     __shared__ unsigned long long ns0;  // in shared memory: no registers held across passes
@@ -1210,6 +1303,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             for (int32_t w = tid; w < kBucketWords; w += blockDim.x) bmask[w] = 0u;
         if (p.nseg <= kMaxSmemSegs)
             for (int32_t s = tid; s < p.nseg; s += blockDim.x) ssegs[s] = p.segs[s];
+        if (keys)
+            for (int32_t r = tid; r < p.nruns; r += blockDim.x) runs_sm[r] = __ldg(p.runs + r);
         if (ksum_image) {
             mbar_wait(&fill_bar, 0);
         } else if (keys) {   // key summary of v_0 straight from the initial list (bucket b =
@@ -1227,6 +1322,10 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         qcount = 0;
         loaded_cta = 0;
     }
+    if (keys) {   // the live runs of summary(v_0)
+        __syncthreads();
+        build_live(p, bmask, runs_sm, live_beg, live_pre, &live_tot);
+    }
     __syncthreads();
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 7] = globaltimer();
 
@@ -1234,7 +1333,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     int k_start = 0;
     if (!EXACT && keys && p.locc_ptr) {   // pipelined key-space LEAD passes
         const PipeExit e = lm_pipe(p, sm, bmask, p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, n0,
-                                   lead ? clk0 : 0, lead ? ns0 : 0);
+                                   lead ? clk0 : 0, lead ? ns0 : 0, ls);
         if (e.done) return;
         // the auto schedule switched: STREAM passes from pass e.k + 1 on (the summary is
         // rebuilt in atom-id space from v_{e.k+1})
@@ -1301,8 +1400,13 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             }
             if (p.dbg && tid == 0 && k >= 3 && k < 16) DBG_STAMP(6) = globaltimer();
             __syncthreads();
+            if (keys && lead_pass) {   // the live runs of summary(v_k)
+                build_live(p, bmask, runs_sm, live_beg, live_pre, &live_tot);
+                __syncthreads();
+            }
             if (p.dbg && tid == 0 && k >= 3 && k < 16) DBG_STAMP(7) = globaltimer();
         }
+        const LiveList lv{live_beg, live_pre, live_tot};
         // rows queued in pass k are counted in cand[k % 3]; the slot of pass k+1 was last
         // read before the previous barrier and is first written after the next one
         if (lead) {
@@ -1327,7 +1431,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             const int64_t sthreads = (int64_t)gridDim.x * (kStreamWarps * 32);
             if (warp < kStreamWarps) {
                 const int64_t sgtid = (int64_t)blockIdx.x * (kStreamWarps * 32) + tid;
-                octets_lead(p, c, sgtid, sthreads);
+                octets_lead(p, c, lv, sgtid, sthreads);
                 __syncwarp();
                 if ((tid & 31) == 0) {
                     __threadfence_block();
@@ -1353,7 +1457,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                 }
             }
         }
-        else if (!EXACT && keys) octets_lead(p, c, gtid, gthreads);
+        else if (!EXACT && keys) octets_lead(p, c, lv, gtid, gthreads);
         else if (EXACT && lead_pass && p.xlead16) octets_exact16<4>(p, c, gtid, gthreads);
         else if (EXACT && lead_pass && p.lead32) flat_lead_exact<4>(p, c, gtid, gthreads);
         else if (lead_pass) all_segments<EXACT, true>(p, c, gtid, gthreads);
@@ -1421,7 +1525,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             // and head the verification loaded, the delta list read twice and the truth
             // words it ORs
             // (STREAM passes added the int4 loads they issued themselves, atomically)
-            atomicAdd(p.stats + 0, (unsigned long long)(lead_pass ? p.lead_bytes : 0) +
+            atomicAdd(p.stats + 0, (unsigned long long)(lead_pass && !keys ? p.lead_bytes : 0) +
                                        4ull * (unsigned long long)queued + 12ull * (unsigned long long)(t - de));
             if (lead_pass) p.stats[1] += 1;
             p.stats[2] += (unsigned long long)queued;
@@ -1429,7 +1533,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         if (t == de || k + 1 >= p.max_passes || k + 1 == p.user_cap) {  // u = v: fixpoint (or a cap)
             if (lead) {
                 *p.iters_out = k + 1;
-                if (t != de) atomicMax(p.status_out, k + 1 == p.user_cap ? 3 : 1);
+                if (t != de) atomicOr(p.status_out, k + 1 == p.user_cap ? kStCapped : kStGuard);
+                if (p.status_user) *p.status_user = atomicOr(p.status_out, 0);
                 if (p.stats) {
                     atomicAdd(p.stats + 0, 4ull * p.stats[3]);
                     p.stats[4] = (unsigned long long)(clock64() - clk0);
@@ -1469,245 +1574,6 @@ cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t sme
                                            dim3(kFullThreads), args, smem, st);
     return cudaLaunchCooperativeKernel((const void *)lm_full_kernel<false>, dim3(blocks),
                                        dim3(kFullThreads), args, smem, st);
-}
-
-// ------------------------------------------------------------------------------------
-// least model: fused θ-pass, TMA-pipelined (the dominant kernel on C4)
-// ------------------------------------------------------------------------------------
-//
-// Each CTA owns every gridDim.x-th 16 KB tile of the program matrix.  Thread 0 streams
-// tiles into an S-stage shared-memory ring with cp.async.bulk (TMA bulk copies, one per
-// body position row) completing on an mbarrier; all 32 warps consume a stage (one
-// AND-row per thread, conflict-free LDS of its body atoms, then the bit test against the
-// shared copy of v_k or its summary).  Because the program matrix is the same in every
-// pass, the producer keeps prefetching the next pass's first tiles across the grid
-// barrier, so HBM never idles while the pass is being closed.
-
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
-__device__ __forceinline__ int find_tile_seg(const TileSeg *ts, int n, int64_t t) {
-    int lo = 0, hi = n - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (ts[mid].tile_off <= t) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
-size_t lm_tma_smem_bytes(int32_t sm_words, int32_t stages) {
-    const size_t a = ((size_t)sm_words * 4 + 127) / 128 * 128;
-    return a + (size_t)stages * kStageBytes + 16 * (size_t)stages + sizeof(TileSeg) * kMaxTileSegs + 16;
-}
-
-// local tile i of this CTA -> (segment, first row, rows)
-struct TileRef {
-    int seg;
-    int32_t rem;
-    int64_t start;
-};
-
-__device__ __forceinline__ TileRef tile_ref(const TileSeg *ts, int nseg, int64_t t) {
-    TileRef r;
-    r.seg = find_tile_seg(ts, nseg, t);
-    r.start = (t - ts[r.seg].tile_off) * ts[r.seg].T;
-    const int64_t left = ts[r.seg].count_pad - r.start;
-    r.rem = (int32_t)(left < ts[r.seg].T ? left : ts[r.seg].T);
-    return r;
-}
-
-constexpr int kConsumerWarps = kThreads / 32 - 1;   // warp 31 is the TMA producer
-
-template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, 1) lm_tma_kernel(const __grid_constant__ LMParams p) {
-    extern __shared__ __align__(128) uint8_t smraw[];
-    __shared__ int32_t qcount;
-    cg::grid_group grid = cg::this_grid();
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    const bool producer = warp == kConsumerWarps;
-    const int ctid = tid;                             // consumer thread id (< 992)
-    const int nct = kConsumerWarps * 32;
-    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
-    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
-    const int S = p.stages;
-    uint32_t *sm = reinterpret_cast<uint32_t *>(smraw);
-    uint8_t *stage0 = smraw + ((size_t)p.sm_words * 4 + 127) / 128 * 128;
-    uint64_t *full = reinterpret_cast<uint64_t *>(stage0 + (size_t)S * kStageBytes);
-    uint64_t *empty = full + S;
-    TileSeg *ts = reinterpret_cast<TileSeg *>(empty + S);
-
-    lm_prologue(p, !EXACT, gtid, gthreads);
-    grid.sync();
-    const uint32_t *src0 = EXACT ? p.buf0 : p.summary;
-    smem_fill(sm, src0, p.sm_words);
-    for (int i = tid; i < p.ntseg; i += blockDim.x) ts[i] = p.tsegs[i];
-    const int32_t n0 = cta_pass_counts(p.tail, nullptr, nullptr).appended;
-    if (blockIdx.x == 0 && tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = n0;
-    if (tid == 0) {
-        qcount = 0;
-        for (int s = 0; s < S; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, kConsumerWarps);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    const int64_t G = gridDim.x, b = blockIdx.x;
-    const int64_t my_nt = p.ntiles > b ? (p.ntiles - b + G - 1) / G : 0;
-    const int64_t W = my_nt < S ? my_nt : S;          // tiles in flight
-    const int rows_extra = p.heads_staged;
-    uint64_t policy = 0;
-    uint64_t q_issue = 0;     // producer: ring positions issued since launch
-    uint64_t q_cons = 0;      // consumers: ring positions consumed since launch
-
-    // producer lane 0: stage local tile i into ring position q_issue
-    auto issue = [&](int64_t i) {
-        const int s = (int)(q_issue % (uint64_t)S);
-        if (q_issue >= (uint64_t)S) mbar_wait(empty + s, (uint32_t)((q_issue / S - 1) & 1));
-        const TileRef r = tile_ref(ts, p.ntseg, b + i * G);
-        const TileSeg &sg = ts[r.seg];
-        uint8_t *dst = stage0 + (size_t)s * kStageBytes;
-        mbar_expect_tx(full + s, (uint32_t)r.rem * 4u * (uint32_t)(sg.L + rows_extra));
-        const uint32_t chunk = (p.tma_variant & 2) ? 4096u : 0xFFFFFFFFu;
-        for (int32_t j = 0; j < sg.L + rows_extra; ++j) {
-            const int32_t *src = j < sg.L ? p.col + sg.col_off + (int64_t)j * sg.count_pad + r.start
-                                          : p.head + sg.slot_off + r.start;
-            uint8_t *d = dst + (size_t)j * sg.T * 4;
-            const uint32_t bytes = (uint32_t)r.rem * 4u;
-            for (uint32_t off = 0; off < bytes; off += chunk) {
-                const uint32_t nb = bytes - off < chunk ? bytes - off : chunk;
-                if (p.tma_variant & 1) bulk_g2s_plain(d + off, (const uint8_t *)src + off, nb, full + s);
-                else bulk_g2s(d + off, (const uint8_t *)src + off, nb, full + s, policy);
-            }
-        }
-        ++q_issue;
-    };
-    if (producer && lane == 0) {
-        policy = evict_first_policy();
-        for (int64_t i = 0; i < W; ++i) issue(i);     // first tiles of pass 0
-    }
-
-    int32_t ds = n0, de = n0;
-    for (int k = 0;; ++k) {
-        const uint32_t *rd = (k & 1) ? p.buf1 : p.buf0;
-        uint32_t *wr = (k & 1) ? p.buf0 : p.buf1;
-        if (k > 0) {
-            for (int64_t i = ds + gtid; i < de; i += gthreads) {
-                const int32_t a = __ldcg(p.order + i);
-                atomicOr(wr + (a >> 5), 1u << (a & 31));
-            }
-            if (EXACT && (de - ds) > (p.sm_words >> 2)) {
-                for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(rd + w);
-            } else {
-                for (int64_t i = ds + tid; i < de; i += blockDim.x) {
-                    const uint32_t a = (uint32_t)__ldcg(p.order + i);
-                    const uint32_t g = EXACT ? a : (a >> p.shift);
-                    atomicOr(sm + (g >> 5), 1u << (g & 31));
-                }
-            }
-            __syncthreads();
-        }
-        if (blockIdx.x == 0 && tid == 0) p.pcnt[(k + 1) % 3] = 0;
-        const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, nullptr, p.segs, nullptr,
-                        p.pcnt + k % 3, de};
-        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + 0] = globaltimer();
-        if (producer) {
-            if (lane == 0) {
-                // the rest of this pass, then the first W tiles of the next pass (the
-                // program matrix is the same in every pass)
-                for (int64_t i = W; i < my_nt; ++i) issue(i);
-                for (int64_t i = 0; i < W; ++i) issue(i);
-            }
-            __syncwarp();
-        } else {
-            for (int64_t i = 0; i < my_nt; ++i, ++q_cons) {
-                const int s = (int)(q_cons % (uint64_t)S);
-                mbar_wait(full + s, (uint32_t)((q_cons / S) & 1));
-                const TileRef r = tile_ref(ts, p.ntseg, b + i * G);
-                const TileSeg &sg = ts[r.seg];
-                const int32_t T = sg.T, L = sg.L;
-                const int32_t *tile = reinterpret_cast<const int32_t *>(stage0 + (size_t)s * kStageBytes);
-                for (int32_t row = ctid; row < r.rem; row += nct) {
-                    bool alive = true;
-                    for (int32_t j = 0; j < L && alive; ++j) {
-                        const uint32_t a = (uint32_t)tile[j * T + row];
-                        alive = sm_bit(sm, EXACT ? a : (a >> p.shift));
-                    }
-                    if (!alive) continue;
-                    if (EXACT) {
-                        const int32_t h = tile[L * T + row];
-                        emit_head(p, c, h, sm[h >> 5]);
-                    } else {
-                        const int32_t pos = atomicAdd(&qcount, 1);
-                        const int32_t slot = (int32_t)(sg.slot_off + r.start + row);
-                        if (pos < p.qcap) c.qbuf[pos] = slot;
-                        else verify_slot<false>(p, c, slot, 0);
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(empty + s)) : "memory");
-            }
-        }
-        if (!EXACT) {  // epilogue: verify this CTA's queued candidates
-            __syncthreads();
-            const int32_t nc = min(qcount, p.qcap);
-            __syncthreads();
-            if (tid == 0) qcount = 0;
-            for (int32_t i = tid; i < nc; i += blockDim.x) verify_slot<false>(p, c, __ldcg(c.qbuf + i), 0);
-        }
-        if (p.dbg && k < 16) {
-            if ((tid & 31) == 0 && !producer) atomicMax(p.dbg + (k * gridDim.x + blockIdx.x) * 8 + 2, globaltimer());
-            __syncthreads();
-            if (tid == 0) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + 4] = globaltimer();
-        }
-        grid.sync();
-        if (p.dbg && tid == 0 && k < 16) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + 5] = globaltimer();
-        const int32_t t = de + cta_pass_counts(p.pcnt + k % 3, nullptr, nullptr).appended;   // (see lm_full_kernel)
-        const bool lead = blockIdx.x == 0 && tid == 0;
-        const bool done = (t == de) || (k + 1 >= p.max_passes) || (k + 1 == p.user_cap);
-        if (done) {
-            if (lead) {
-                *p.iters_out = k + 1;
-                if (t != de) atomicMax(p.status_out, k + 1 == p.user_cap ? 3 : 1);
-            }
-            // drain the prefetched tiles before the CTA's shared memory is released
-            if (!producer)
-                for (int64_t x = 0; x < W; ++x) {
-                    const uint64_t q = q_cons + (uint64_t)x;
-                    mbar_wait(full + (q % (uint64_t)S), (uint32_t)((q / S) & 1));
-                }
-            lm_zero_summaries(p, !EXACT, gtid, gthreads);
-            lm_extract(p, gtid, gthreads, wr);
-            return;
-        }
-        if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = t;
-        ds = de;
-        de = t;
-    }
-}
-
-
-cudaError_t launch_lm_tma(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st) {
-    LMParams q = p;
-    void *args[] = {(void *)&q};
-    if (exact)
-        return cudaLaunchCooperativeKernel((const void *)lm_tma_kernel<true>, dim3(blocks),
-                                           dim3(kThreads), args, smem, st);
-    return cudaLaunchCooperativeKernel((const void *)lm_tma_kernel<false>, dim3(blocks),
-                                       dim3(kThreads), args, smem, st);
-}
-
-int lm_tma_blocks_per_sm(bool exact, size_t smem) {
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, exact ? (const void *)lm_tma_kernel<true> : (const void *)lm_tma_kernel<false>,
-        kThreads, smem);
-    return nb;
 }
 
 // ------------------------------------------------------------------------------------
@@ -1805,7 +1671,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
         if (cnt == 0 || capped) {
             if (lead) {
                 *p.iters_out = k + 1;
-                if (cnt != 0) atomicMax(p.status_out, k + 1 == p.user_cap ? 3 : 1);
+                if (cnt != 0) atomicOr(p.status_out, k + 1 == p.user_cap ? kStCapped : kStGuard);
+                if (p.status_user) *p.status_user = atomicOr(p.status_out, 0);
             }
             if (capped)   // level j's queue was not consumed
                 for (int64_t i = gtid; i < cnt; i += gthreads) q[i].x = -1;
@@ -2192,7 +2059,7 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
             break;
         }
         if (k + 1 >= p.max_passes) {
-            if (lead) { *p.passes_out = k + 1; atomicMax(p.status_out, 1); }
+            if (lead) { *p.passes_out = k + 1; atomicOr(p.status_out, kStGuard); }
             break;
         }
         n2 = n1;
@@ -2204,6 +2071,7 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
     }
     // both buffers hold the fixpoint (rows changed in the last pass were copied during it)
     st_check_phase(p, gtid, gthreads);
+    if (gtid == 0 && p.status_user) *p.status_user = *(volatile int32_t *)p.status_out;
 }
 
 cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
@@ -2255,12 +2123,6 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
         return e;
     if ((e = cudaFuncSetAttribute((const void *)lm_full_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, cap)))
-        return e;
-    if ((e = cudaFuncSetAttribute((const void *)lm_tma_kernel<true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)))
-        return e;
-    if ((e = cudaFuncSetAttribute((const void *)lm_tma_kernel<false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)))
         return e;
     if ((e = cudaFuncSetAttribute((const void *)st_fixpoint_kernel,   // (+ its static candidate queue)
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))

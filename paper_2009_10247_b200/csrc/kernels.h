@@ -13,11 +13,16 @@ constexpr int kThreads = 1024;          // persistent kernels: 32 warps per CTA
 // per thread measured no faster on C4 and slower on C3.)
 constexpr int kFullThreads = 1024;
 constexpr int kMaxSmemBytes = 200 * 1024;
-constexpr int kKeySmemBytes = 220 * 1024;   // key-space summary (register-streaming kernel only)
+constexpr int kKeySmemBytes = 208 * 1024;   // key-space summary (register-streaming kernel only)
+constexpr int kMaxRuns = 256;          // key mode: bucket runs of the row order kept in shared
+                                       // memory (more: LEAD passes stream every octet)
 
-constexpr int kStageBytes = 16384;      // one TMA pipeline stage (bulk copies of col rows)
+// Run status bit flags (LMParams / STParams status_out).  Sticky: a queue overflow is
+// never masked by a later cap or guard; the host checks kStOverflow first.
+constexpr int kStGuard = 1;     // pass guard (n_ext + 2 passes) hit
+constexpr int kStOverflow = 2;  // a candidate queue overflowed (internal error)
+constexpr int kStCapped = 4;    // stopped at lp_run.max_passes before the fixpoint
 constexpr int kSmemLimit = 232448 - 1024;  // opt-in smem per CTA on sm_100 minus static
-constexpr int kMaxTileSegs = 64;
 constexpr int kMaxSmemSegs = 64;       // segment table copied to shared memory up to this size
 constexpr int kSmemQueue = 768;        // candidate queue entries kept in shared memory per CTA
 #ifndef LP_STREAM_WARPS
@@ -25,19 +30,7 @@ constexpr int kSmemQueue = 768;        // candidate queue entries kept in shared
 #endif
 constexpr int kStreamWarps = LP_STREAM_WARPS;
 constexpr int kBucketWords = 256;
-constexpr int kStQueue = 2048;         // stable search: candidate rows queued per CTA and pass      // key mode: buckets (group >> 8) of the summary, bitmap words   // overlapped LEAD passes: streaming warps (the rest verify)
-
-// A body-length segment cut into TMA tiles of T rows.  A tile stages R = L (+1 when the
-// head row is staged too) rows of T ints each: row j holds body position j of T
-// consecutive AND-rows, the extra row their heads.
-struct TileSeg {
-    int32_t L;
-    int32_t T;
-    int64_t tile_off;   // first global tile index of this segment
-    int64_t col_off;
-    int64_t count_pad;
-    int64_t slot_off;
-};
+constexpr int kStQueue = 2048;         // stable search: candidate rows queued per CTA and pass
 
 // Least-model fixpoint (full θ-pass and frontier variants).
 struct LMParams {
@@ -79,7 +72,9 @@ struct LMParams {
     int32_t *pops;             // optional [pop_cap]
     int32_t pop_cap;
     int32_t *iters_out;
-    int32_t *status_out;       // 0 ok, 1 pass guard hit, 2 queue overflow, 3 stopped at user_cap
+    int32_t *status_out;       // run status, bit flags kSt* (0 = converged, nothing dropped)
+    int32_t *status_user;      // optional (lp_run.status_out, device): the final status word,
+                               //   written by the epilogue
     int32_t max_passes;        // guard (n_ext + 2)
     int32_t user_cap;          // lp_run.max_passes (0 = to the fixpoint)
     // frontier variant
@@ -92,13 +87,6 @@ struct LMParams {
     // FILTER mode: per-CTA candidate queues (rows that passed the summary test)
     int32_t *qbuf;             // [grid][qcap]
     int32_t qcap;
-    // TMA-pipelined full pass
-    const TileSeg *tsegs;
-    int32_t ntseg;
-    int32_t stages;            // pipeline depth S
-    int64_t ntiles;
-    int32_t heads_staged;      // 1: the head row is part of every tile (EXACT mode)
-    int32_t tma_variant;       // diagnostics (LP_TMA_VARIANT): 1 no L2 hint, 2 4 KB chunks
     // full θ-pass schedule: LEAD passes stream only the lead
     // atom of every row (+ the head row when the truth test is exact) and verify the
     // survivors from a queue; STREAM passes stream every body position.
@@ -136,6 +124,11 @@ struct LMParams {
     const uint16_t *xlead16;   // exact mode, ids < 2^21: low 16 bits of lead / head, and per
     const uint16_t *xhead16;   //   octet lead bucket | head bucket << 5 | padding << 10
     const uint16_t *xtag;
+    // key mode: the rows of every segment are in runs of one lead bucket (encode.cpp
+    // bucket_rows); a LEAD pass streams only the octets of runs whose bucket has a set
+    // summary bit.  nruns == 0: no table, every octet streamed.
+    const int4 *runs;          // [nruns] (first octet, octets, bucket, 0), in slot order
+    int32_t nruns;
     const int32_t *key_of;     // [n_ext] key of every extended atom
     int32_t *korder;           // [n_ext + 1] key of order[i] (written with it)
     int32_t ksm_words;         // words of the key-space summary (shared memory)
@@ -174,7 +167,8 @@ struct STParams {
     int64_t G;                 // guesses
     int32_t *mark;             // [n_ext] pass tag of the last push (0: row never changed)
     int32_t *passes_out;
-    int32_t *status_out;
+    int32_t *status_out;       // bit flags kSt*
+    int32_t *status_user;      // optional device copy of the final status (lp_run.status_out)
     int32_t max_passes;
     // the rest of the call, fused into the same cooperative launch (clear -> T_0 -> fixpoint
     // -> stability check, grid barriers in between)
@@ -198,9 +192,6 @@ struct STParams {
 // Each least-model call is ONE cooperative launch: v_0 prologue, the fixpoint loop and
 // the model extraction all run inside the persistent kernel.
 cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st);
-cudaError_t launch_lm_tma(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st);
-int lm_tma_blocks_per_sm(bool exact, size_t smem);
-size_t lm_tma_smem_bytes(int32_t sm_words, int32_t stages);
 cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st);
 
 // One cooperative launch per stable call: clear the previous call's rows, build T_0, the

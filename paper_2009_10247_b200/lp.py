@@ -22,7 +22,6 @@ LIB_PATH = os.environ.get("LP_LIB") or os.path.join(_HERE, "liblp_b200.so")   # 
 LP_OK, LP_E_INVALID, LP_E_PARSE, LP_E_SEMANTIC, LP_E_CAP = 0, 1, 2, 3, 4
 LP_E_NOMEM, LP_E_CUDA, LP_E_NOT_CONVERGED, LP_E_NODEVICE = 5, 6, 7, 8
 LP_LOAD_NO_FRONTIER = 0x1
-LP_LOAD_TMA = 0x2
 LP_LOAD_PAPER_LAYOUT = 0x4
 LP_LOAD_KEY8 = 0x8
 LP_PTR_DEVICE = 0x1
@@ -30,6 +29,7 @@ LP_FRONTIER = 0x2
 LP_FULL_STREAM = 0x4
 LP_FULL_LEAD = 0x8
 LP_FULL_NO_PIPE = 0x10
+LP_ST_GUARD, LP_ST_OVERFLOW, LP_ST_CAPPED = 0x1, 0x2, 0x4   # lp_run.status_out bit flags
 
 _P = ctypes.c_void_p
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
@@ -51,7 +51,7 @@ class lp_run(ctypes.Structure):
     _fields_ = [("stream", _P), ("flags", ctypes.c_uint32), ("popcounts_out", _P),
                 ("popcounts_cap", ctypes.c_int32), ("stage_out", _P), ("ev_begin", _P),
                 ("ev_end", _P), ("stats_out", _P), ("max_passes", ctypes.c_int32),
-                ("converged_out", _P), ("guess_offset", ctypes.c_int64)]
+                ("converged_out", _P), ("guess_offset", ctypes.c_int64), ("status_out", _P)]
 
 
 class lp_info_t(ctypes.Structure):
@@ -62,8 +62,7 @@ class lp_info_t(ctypes.Structure):
                 ("sparsity_eq5", ctypes.c_double), ("device_bytes", ctypes.c_int64),
                 ("pass_bytes", ctypes.c_int64), ("truth_mode", ctypes.c_int32),
                 ("summary_shift", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
-                ("block_threads", ctypes.c_int32), ("full_kernel", ctypes.c_int32),
-                ("tma_stages", ctypes.c_int32), ("lead_pass_bytes", ctypes.c_int64),
+                ("block_threads", ctypes.c_int32), ("lead_pass_bytes", ctypes.c_int64),
                 ("stream_pass_bytes", ctypes.c_int64), ("key_shift", ctypes.c_int32),
                 ("n_aux", ctypes.c_int32)]
 
@@ -179,7 +178,7 @@ class Program:
 
     def __init__(self, rules, device: int = 0, guess_cap: int = 20, frontier: bool = True,
                  smem_bits_cap: int = 0, grid_blocks: int = 0, allocator: str = "torch",
-                 tma: bool = False, paper_layout: bool = False, key8: bool = False):
+                 paper_layout: bool = False, key8: bool = False):
         lib = library()
         self._keep = []
         head = np.ascontiguousarray(rules.head, dtype=np.int32)
@@ -190,7 +189,7 @@ class Program:
         opt = lp_options()
         opt.device = int(device)
         opt.guess_cap = int(guess_cap)
-        opt.flags = ((0 if frontier else LP_LOAD_NO_FRONTIER) | (LP_LOAD_TMA if tma else 0) |
+        opt.flags = ((0 if frontier else LP_LOAD_NO_FRONTIER) |
                      (LP_LOAD_PAPER_LAYOUT if paper_layout else 0) | (LP_LOAD_KEY8 if key8 else 0))
         opt.smem_bits_cap = int(smem_bits_cap)
         opt.grid_blocks = int(grid_blocks)
@@ -356,15 +355,19 @@ def _run(stream=None, flags=0, pops=None, stage=None, ev_begin=None, ev_end=None
 
 def lp_least_model(p: Program, v0, model_out, frontier=False, pops=None, stage=None, stream=None,
                    device_ptrs=False, iters_out=None, ev_begin=None, ev_end=None, schedule="auto",
-                   stats=None, max_passes=0, converged=None, pipeline=True):
+                   stats=None, max_passes=0, converged=None, pipeline=True, status_out=None):
     """Marshals lp_least_model.  Host mode (default): numpy buffers, returns iters.
     device_ptrs=True: torch CUDA tensors (v0 int64 words or None, model_out int64
-    words, iters_out int32[1], optional pops/stage), asynchronous on ``stream``."""
+    words, iters_out int32[1], optional pops/stage, optional status_out int32[1] that
+    the kernel fills with the LP_ST_* flags), asynchronous on ``stream``.  Host mode:
+    status_out may be a ctypes.c_int32."""
     flags = (LP_FRONTIER if frontier else 0) | (LP_PTR_DEVICE if device_ptrs else 0)
     flags |= {"auto": 0, "stream": LP_FULL_STREAM, "lead": LP_FULL_LEAD}[schedule]
     flags |= 0 if pipeline else LP_FULL_NO_PIPE
     run = _run(stream, flags, pops, stage, ev_begin, ev_end, stats)
     run.max_passes = int(max_passes)
+    if status_out is not None:
+        run.status_out = _ptr(status_out) if device_ptrs else ctypes.addressof(status_out)
     if converged is not None and not device_ptrs:
         run.converged_out = ctypes.addressof(converged)
     if device_ptrs:
@@ -379,10 +382,12 @@ def lp_least_model(p: Program, v0, model_out, frontier=False, pops=None, stage=N
 
 def lp_stable_models(p: Program, guesses, n_guesses, accepted_out, stream=None, device_ptrs=False,
                      n_accepted_out=None, passes_out=None, ev_begin=None, ev_end=None,
-                     guess_offset: int = 0):
+                     guess_offset: int = 0, status_out=None):
     flags = LP_PTR_DEVICE if device_ptrs else 0
     run = _run(stream, flags, ev_begin=ev_begin, ev_end=ev_end)
     run.guess_offset = int(guess_offset)
+    if status_out is not None:
+        run.status_out = _ptr(status_out) if device_ptrs else ctypes.addressof(status_out)
     g = None
     if guesses is not None:
         g = guesses if device_ptrs else np.ascontiguousarray(guesses, dtype=np.uint64)

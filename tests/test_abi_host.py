@@ -132,3 +132,30 @@ def test_load_shim_from_flat_arrays():
     b = _host(P)
     for key in ("n_atoms", "n_rules", "nnz", "n_heads", "max_body", "n_segments"):
         assert a.info[key] == b.info[key]
+
+
+def test_unknown_load_flag_rejected():
+    """Flag bit 0x2 (the removed TMA ring) and any unknown bit fail with LP_E_INVALID."""
+    import ctypes
+    P = lpgen.from_lists(3, [(0, [1]), (1, [])])
+    head = np.ascontiguousarray(P.head, dtype=np.int32)
+    ptr = np.ascontiguousarray(P.body_ptr, dtype=np.int64)
+    atom = np.ascontiguousarray(P.body_atom, dtype=np.int32)
+    r = lp.lp_rules(3, head.shape[0], head.ctypes.data, ptr.ctypes.data, atom.ctypes.data, None)
+    for bad in (0x2, 0x100):
+        opt = lp.lp_options()
+        opt.device = -1
+        opt.flags = bad
+        h = ctypes.c_void_p()
+        st = lp.library().lp_load(ctypes.byref(r), ctypes.byref(opt), ctypes.byref(h))
+        assert st == lp.LP_E_INVALID and not h.value
+
+
+def test_lp_run_layout_matches_header():
+    """The ctypes mirror of lp_run / lp_info_t has the fields include/lp.h declares, in order."""
+    src = open(os.path.join(ROOT, "include", "lp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    for struct, cls in (("lp_run", lp.lp_run), ("lp_info_t", lp.lp_info_t)):
+        body = re.search(r"typedef struct \{([^}]*)\}\s*" + struct + ";", src).group(1)
+        names = re.findall(r"\b(\w+)\s*;", body)
+        assert names == [f for f, _ in cls._fields_], (struct, names)

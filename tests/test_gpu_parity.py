@@ -33,7 +33,7 @@ def check_lm(P, v0=None, prog=None, variants=(False, True), jacobi=False,
     prog = prog or lp.Program(P, **kw)
     runs = []
     for frontier in variants:
-        if frontier or prog.info["full_kernel"] == 1:
+        if frontier:
             runs.append((frontier, "auto", True))
         else:   # every schedule of the full θ-pass (LEAD / STREAM passes) must agree,
                 # LEAD passes pipelined (default) and not
@@ -44,12 +44,13 @@ def check_lm(P, v0=None, prog=None, variants=(False, True), jacobi=False,
                                             schedule=schedule, stats=True, pipeline=pipeline)
         tag = "frontier" if frontier else f"full/{schedule}" + ("" if pipeline else "/nopipe")
         st = ex["stats"]
-        if frontier or prog.info["full_kernel"] == 1:
+        if frontier:
             assert st["bytes"] == 0
         else:
             assert 0 <= st["lead_passes"] <= iters, (tag, st)
             assert st["lead_passes"] == {"stream": 0, "lead": iters}.get(schedule, st["lead_passes"])
-            assert st["bytes"] >= st["lead_passes"] * prog.info["lead_pass_bytes"]
+            # (key-mode LEAD passes stream only the live runs: at most the whole plane)
+            assert st["bytes"] > 0 or prog.info["lead_pass_bytes"] == 0 or st["lead_passes"] == 0
         assert iters == oit, (tag, iters, oit)
         assert (model == om).all(), tag
         assert ex["popcounts"] == opops, tag
@@ -109,16 +110,15 @@ def test_forced_summary_mode_and_small_grids(seed, cfg):
 
 
 @pytest.mark.parametrize("seed", range(12))
-@pytest.mark.parametrize("cfg", [dict(tma=True), dict(tma=True, smem_bits_cap=128),
-                                 dict(tma=True, smem_bits_cap=128, grid_blocks=2)])
-def test_tma_kernel_and_edge_grids(seed, cfg):
-    """The TMA-pipelined full θ-pass (LP_LOAD_TMA), exact and summary modes, including
-    more tiles than CTAs, gives the same results as the oracle."""
+@pytest.mark.parametrize("cfg", [dict(grid_blocks=2), dict(smem_bits_cap=128),
+                                 dict(smem_bits_cap=128, grid_blocks=2)])
+def test_long_rows_edge_grids(seed, cfg):
+    """Bodies of up to 9 atoms (one segment past the unrolled lengths) on 2-CTA grids and
+    in summary mode: many rows per thread, every schedule, same results as the oracle."""
     rng = np.random.default_rng([seed, 123])
     n = int(rng.integers(1200, 6000))
     P = lpgen.random_program(rng, n, 6 * n, max_len=9, n_facts=n // 30)
-    prog = check_lm(P, **cfg)
-    assert prog.info["full_kernel"] == 1
+    check_lm(P, **cfg)
 
 
 @pytest.mark.parametrize("seed", range(8))
@@ -216,19 +216,7 @@ def test_config_parity(cfg):
     check_lm(P, jacobi=(cfg != "C3"))
 
 
-@pytest.mark.slow
-def test_config_c4_parity():
-    P = lpgen.config("C4")
-    prog = check_lm(P)
-    assert prog.info["truth_mode"] == 1     # the 10M-atom truth vector is L2-resident
-    assert prog.info["key_shift"] >= 0
-    prog.close()
-    # the 8-bit key plane (LP_LOAD_KEY8) on the same program
-    om, ostage, oit = oracle.lm_stage(P)
-    p8 = lp.Program(P, key8=True, frontier=False)
-    model, iters, ex = p8.least_model(stages=True, stats=True)
-    assert iters == oit and (model == oracle.pack_bits(om)).all() and (ex["stage"] == ostage).all()
-    assert p8.info["lead_pass_bytes"] < 0.7 * prog.info["lead_pass_bytes"]
+# (full-size C4: tests/test_gpu_c4.py)
 
 
 # ---------------------------------------------------------------------------------
