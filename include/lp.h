@@ -102,6 +102,13 @@ typedef struct {
     lp_alloc_fn alloc;      /* device allocator hook (NULL = cudaMalloc)           */
     lp_free_fn free;
     void *alloc_ctx;
+    const uint8_t *derivable; /* optional [n_atoms] layout hint, 1 = the atom may become
+                               true from the facts (D2);
+                               NULL = computed from this program.  Never affects a
+                               result.  A head-range shard of a larger program passes
+                               the whole program's D2 (shard.py), so atoms derived on
+                               other GPUs keep fine key groups.  Ignored with
+                               LP_LOAD_PAPER_LAYOUT.                                */
 } lp_options;
 
 #define LP_PTR_DEVICE 0x1u /* pointer args of this call are device pointers; async */
@@ -156,6 +163,11 @@ typedef struct {
                                 asynchronous call reports LP_ST_OVERFLOW or
                                 LP_ST_GUARD; callers must check it once the stream
                                 has been synchronised.                               */
+    int64_t out_word_lo;     /* lp_least_model: with out_word_count > 0, only model  */
+    int64_t out_word_count;  /* words [out_word_lo, out_word_lo + out_word_count) are
+                                written, to model_out[0 .. out_word_count) (a head-
+                                range shard's owned words, shard.py); 0 = the whole
+                                model                                               */
 } lp_run;
 
 /* lp_run.status_out bit flags (sticky; an overflow is never masked by a cap):      */
@@ -233,11 +245,41 @@ lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, int64_t n_gue
                            uint64_t *accepted_out, int64_t *n_accepted_out,
                            int32_t *passes_out, const lp_run *run);
 
-/* After lp_stable_models: the fixpoint rows of the original atoms, [n_atoms][W]
- * words (row a, bit g = atom a true in guess g's fixpoint column). */
+/* Guess-space reduction by sampling + local search (Conclusion: "prepare
+ * some manageable size of the initial matrix, and if all guesses fail we do some local
+ * search and replace column vectors by new assignments then repeat it until a stable
+ * model is found"; details fixed by DESIGN.md reading R23).  For programs whose 2^f
+ * guesses cannot be enumerated (lp_stable_models returns LP_E_CAP).
+ *   h          : columns of the initial matrix per round (>= 1), W = ceil(h/64) words.
+ *                Round 0: column g gives abar_j the bit rand64(seed, 0, g, j) >> 63 for
+ *                every free negated atom j, 0 for a negated fact (Def. 8 item 3).
+ *   seed       : of the counter-based generator rand64(seed, r, g, j) =
+ *                mix(mix(mix(mix(seed) ^ r) ^ g) ^ j), mix = SplitMix64's output function.
+ *   max_rounds : >= 1.  Each round is Algorithms 2-3 on the h columns (as
+ *                lp_stable_models with explicit guesses); the search stops at the first
+ *                round with an accepted column, else every column g is moved: the
+ *                violated pairs V_g = {j : [a_j in LM_g] + abar_j != 1} with
+ *                rand64(seed, r+1, g, j) >> 63 = 1 are flipped, or, if none is, the one
+ *                V_g[rand64(seed, r+1, g, k) mod |V_g|].
+ *   guesses_out    : optional [k][W] words: the last round's columns (bit g of row j =
+ *                    abar_j in column g), the assignments behind accepted_out.
+ *   accepted_out   : [W] words: the last round's accepted columns (all zero if none).
+ *   n_accepted_out : accepted columns of the last round (0 = no stable model found
+ *                    within max_rounds; not an error).
+ *   rounds_out     : rounds run (the accepting round's number + 1, or max_rounds).
+ *   passes_out     : whole-matrix θ-passes summed over the rounds.
+ * All rounds run in ONE cooperative launch.  Afterwards lp_stable_matrix and
+ * lp_guess_model read the last round's fixpoint matrix. */
+lp_status lp_stable_search(lp_program *p, int64_t h, uint64_t seed, int32_t max_rounds,
+                           uint64_t *guesses_out, uint64_t *accepted_out,
+                           int64_t *n_accepted_out, int32_t *rounds_out, int32_t *passes_out,
+                           const lp_run *run);
+
+/* After lp_stable_models / lp_stable_search: the fixpoint rows of the original atoms,
+ * [n_atoms][W] words (row a, bit g = atom a true in guess g's fixpoint column). */
 lp_status lp_stable_matrix(lp_program *p, uint64_t *out, const lp_run *run);
 
-/* After lp_stable_models: column `guess` of the fixpoint as a model bit vector over
+/* After lp_stable_models / lp_stable_search: column `guess` of the fixpoint as a model bit vector over
  * the original atoms, [ceil(n/64)] words. */
 lp_status lp_guess_model(lp_program *p, int64_t guess, uint64_t *model_out,
                          const lp_run *run);

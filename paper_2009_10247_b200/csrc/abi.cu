@@ -59,7 +59,10 @@ struct lp_program {
     bool env_no_overlap = false;  // LP_NO_OVERLAP
     bool env_no_ksum_image = false;  // LP_NO_KSUM_IMAGE
     bool env_no_zerocopy = false;    // LP_NO_ZEROCOPY
+    long long overlap_min_bytes = 16ll << 20;   // LP_OVERLAP_MIN_MB: overlapped / pipelined
+                                                // LEAD passes from this live stream size on
     // [0] tail, [2] status (stable path); [1] iters; [3] passes; [4,5] n_accepted;
+    // [6] search rounds, [7] search passes (sum over rounds);
     // [8,9] least-model tails and [10,11] statuses, alternating by call parity;
     // [12..14] rows queued per full θ-pass (slot k % 3); [16..18] least-model and
     // [20..22] stable per-pass append counters (slot k % 3)
@@ -103,6 +106,8 @@ struct lp_program {
     int32_t st_last_Wp = 0;
     unsigned long long *d_acc = nullptr, *d_guess = nullptr;
     size_t acc_words_alloc = 0, guess_words_alloc = 0;
+    unsigned long long *d_sguess = nullptr;   // lp_stable_search: the round's columns [k][W]
+    size_t sguess_words_alloc = 0;
 
     int sms = 0, threads = kThreads;
     int lm_blocks = 0, fr_blocks = 0, st_blocks = 0, grid_cap = 0;
@@ -541,6 +546,8 @@ extern "C" lp_status lp_load(const lp_rules *rules, const lp_options *opt, lp_pr
     p->env_no_overlap = std::getenv("LP_NO_OVERLAP") != nullptr;
     p->env_no_ksum_image = std::getenv("LP_NO_KSUM_IMAGE") != nullptr;
     p->env_no_zerocopy = std::getenv("LP_NO_ZEROCOPY") != nullptr;
+    if (const char *e = std::getenv("LP_OVERLAP_MIN_MB")) p->overlap_min_bytes = (long long)std::atoll(e) << 20;
+    if (opt && opt->derivable && !(opt->flags & LP_LOAD_PAPER_LAYOUT)) p->L.deriv_hint = opt->derivable;
     const bool occ = !(opt && (opt->flags & LP_LOAD_NO_FRONTIER));
     std::string err;
     lp_status s;
@@ -651,6 +658,13 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
     CK(cudaSetDevice(p->device));
     const size_t mw = ((size_t)L.n_out + 63) / 64;
+    // output window (lp_run.out_word_lo / out_word_count): model words [w0, w0 + ow)
+    int64_t w0 = 0, ow = (int64_t)mw;
+    if (run && run->out_word_count > 0) {
+        w0 = run->out_word_lo;
+        ow = run->out_word_count;
+        if (w0 < 0 || w0 + ow > (int64_t)mw) return set_err(LP_E_INVALID, "output word window out of range");
+    }
 
     const uint32_t *v0d = nullptr;
     if (v0) {
@@ -721,6 +735,8 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     unsigned long long *mout = dev ? reinterpret_cast<unsigned long long *>(model_out)
                                : mout_mapped ? reinterpret_cast<unsigned long long *>(mout_mapped) : p->d_model;
     q.model_out = mout;
+    q.out_w0 = w0;
+    q.out_wn = ow;
     q.stage = stage;
     q.pops = pops;
     q.pop_cap = pop_cap;
@@ -741,6 +757,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.cand = p->d_scal + 12;
     q.vent = p->d_vent;
     q.overlap = p->env_no_overlap ? 0 : 1;
+    q.overlap_min_bytes = p->overlap_min_bytes;
     const bool pipe = q.overlap && !(flags & LP_FULL_NO_PIPE) && !p->env_no_pipe;
     q.locc_ptr = pipe ? p->d_locc_ptr : nullptr;
     q.locc_slot = p->d_locc_slot;
@@ -787,7 +804,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     int32_t scal[3] = {0, 0, 0};
     CK(cudaMemcpyAsync(scal, p->d_scal, sizeof(scal), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(scal + 2, p->d_scal + 10 + par, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    if (mw && !mout_mapped) CK(cudaMemcpyAsync(model_out, p->d_model, mw * 8, cudaMemcpyDeviceToHost, st));
+    if (ow && !mout_mapped) CK(cudaMemcpyAsync(model_out, p->d_model, (size_t)ow * 8, cudaMemcpyDeviceToHost, st));
     if (stage) CK(cudaMemcpyAsync(run->stage_out, stage, sizeof(int32_t) * (size_t)L.n_out,
                                   cudaMemcpyDeviceToHost, st));
     if (pops) CK(cudaMemcpyAsync(run->popcounts_out, pops, sizeof(int32_t) * (size_t)pop_cap,
@@ -804,6 +821,43 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
 // ------------------------------------------------------------------------------------
 // lp_stable_models
 // ------------------------------------------------------------------------------------
+
+// The bit-sliced matrix T (two buffers of n_ext rows x Wp words) for G guess columns.
+static lp_status st_matrix(lp_program *p, int64_t G) {
+    const int64_t W64 = (G + 63) / 64;
+    if (W64 > (1 << 26)) return set_err(LP_E_INVALID, "too many guesses");
+    const int32_t W = (int32_t)W64, Wp = (W + 1) / 2 * 2;
+    const size_t need = (size_t)p->L.n_ext * Wp;
+    if (need > p->T_words_alloc) {
+        if (p->d_T0) dev_release(p, p->d_T0);
+        if (p->d_T1) dev_release(p, p->d_T1);
+        p->d_T0 = p->d_T1 = nullptr;
+        TRY(dalloc(p, &p->d_T0, need));
+        TRY(dalloc(p, &p->d_T1, need));
+        p->T_words_alloc = need;
+        p->st_dirty_ok = false;
+    }
+    p->W = W;
+    p->Wp = Wp;
+    p->G = G;
+    p->stable_valid = false;
+    return LP_OK;
+}
+
+// Rows of T left by the previous call: cleared by the kernel's first phase when the
+// layout is unchanged (only the rows it changed), else both buffers zeroed here.
+static lp_status st_clear_plan(lp_program *p, cudaStream_t st, STParams *s) {
+    const bool full_clear = !(p->st_dirty_ok && p->st_last_Wp == p->Wp);
+    if (full_clear) {   // first call, or a new matrix layout: both buffers from zero
+        const size_t tbytes = (size_t)p->L.n_ext * p->Wp * sizeof(unsigned long long);
+        CK(cudaMemsetAsync(p->d_T0, 0, tbytes, st));
+        CK(cudaMemsetAsync(p->d_T1, 0, tbytes, st));
+    }
+    s->clear_rows = full_clear ? 0 : 1;
+    p->st_dirty_ok = true;   // (stream order: the next call's clear runs after this one)
+    p->st_last_Wp = p->Wp;
+    return LP_OK;
+}
 
 static STParams st_params(lp_program *p) {
     const HostLayout &L = p->L;
@@ -866,24 +920,9 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
         if (n_guesses < 1) return set_err(LP_E_INVALID, "n_guesses < 1");
         G = n_guesses;
     }
-    const int64_t W64 = (G + 63) / 64;
-    if (W64 > (1 << 26)) return set_err(LP_E_INVALID, "too many guesses");
-    const int32_t W = (int32_t)W64, Wp = (W + 1) / 2 * 2;
     CK(cudaSetDevice(p->device));
-    const size_t need = (size_t)L.n_ext * Wp;
-    if (need > p->T_words_alloc) {
-        if (p->d_T0) dev_release(p, p->d_T0);
-        if (p->d_T1) dev_release(p, p->d_T1);
-        p->d_T0 = p->d_T1 = nullptr;
-        TRY(dalloc(p, &p->d_T0, need));
-        TRY(dalloc(p, &p->d_T1, need));
-        p->T_words_alloc = need;
-        p->st_dirty_ok = false;
-    }
-    p->W = W;
-    p->Wp = Wp;
-    p->G = G;
-    p->stable_valid = false;
+    TRY(st_matrix(p, G));
+    const int32_t W = p->W, Wp = p->Wp;
     const unsigned long long *gd = nullptr;
     if (guesses && L.k > 0) {
         if (dev) gd = reinterpret_cast<const unsigned long long *>(guesses);
@@ -913,13 +952,7 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
     STParams s = st_params(p);
     if (dev) s.passes_out = passes_out;
     if (dev && run) s.status_user = run->status_out;
-    const bool full_clear = !(p->st_dirty_ok && p->st_last_Wp == Wp);
-    if (full_clear) {   // first call, or a new matrix layout: both buffers from zero
-        const size_t tbytes = (size_t)L.n_ext * Wp * sizeof(unsigned long long);
-        CK(cudaMemsetAsync(p->d_T0, 0, tbytes, st));
-        CK(cudaMemsetAsync(p->d_T1, 0, tbytes, st));
-    }
-    s.clear_rows = full_clear ? 0 : 1;   // else only the rows the previous call changed
+    TRY(st_clear_plan(p, st, &s));
     s.n_atoms = L.n;
     s.k = L.k;
     s.negated = p->d_negated;
@@ -933,8 +966,6 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
     s.any_rw = p->d_any;
     s.accepted = acc;
     s.n_accepted = nacc;
-    p->st_dirty_ok = true;   // (stream order: the next call's clear runs after this one)
-    p->st_last_Wp = Wp;
     // ONE cooperative launch: clear, T_0, the fixpoint loop, the stability check
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
     CK(launch_st_fused(s, p->st_blocks, p->st_smem, st));
@@ -949,6 +980,85 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
     int64_t na;
     std::memcpy(&na, scal + 4, sizeof(na));
     *n_accepted_out = na;
+    if (run && run->status_out) *run->status_out = scal[2];
+    return status_of(scal[2]);
+}
+
+// ------------------------------------------------------------------------------------
+// lp_stable_search (guess-space reduction, reading R23)
+// ------------------------------------------------------------------------------------
+
+extern "C" lp_status lp_stable_search(lp_program *p, int64_t h, uint64_t seed, int32_t max_rounds,
+                                      uint64_t *guesses_out, uint64_t *accepted_out,
+                                      int64_t *n_accepted_out, int32_t *rounds_out,
+                                      int32_t *passes_out, const lp_run *run) {
+    if (!p || !accepted_out || !n_accepted_out || !rounds_out || !passes_out)
+        return set_err(LP_E_INVALID, "NULL argument");
+    if (p->device < 0) return set_err(LP_E_NODEVICE, "host-only handle");
+    if (h < 1) return set_err(LP_E_INVALID, "h < 1");
+    if (max_rounds < 1) return set_err(LP_E_INVALID, "max_rounds < 1");
+    const HostLayout &L = p->L;
+    const bool dev = run && (run->flags & LP_PTR_DEVICE);
+    cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
+    CK(cudaSetDevice(p->device));
+    TRY(st_matrix(p, h));
+    const int32_t W = p->W;
+    const size_t gw = std::max<size_t>((size_t)L.k * W, 1);
+    if (gw > p->sguess_words_alloc) {
+        if (p->d_sguess) dev_release(p, p->d_sguess);
+        TRY(dalloc(p, &p->d_sguess, gw));
+        p->sguess_words_alloc = gw;
+    }
+    unsigned long long *acc;
+    if (dev) acc = reinterpret_cast<unsigned long long *>(accepted_out);
+    else {
+        if ((size_t)W > p->acc_words_alloc) {
+            if (p->d_acc) dev_release(p, p->d_acc);
+            TRY(dalloc(p, &p->d_acc, (size_t)W));
+            p->acc_words_alloc = W;
+        }
+        acc = p->d_acc;
+    }
+    STParams s = st_params(p);
+    TRY(st_clear_plan(p, st, &s));
+    s.n_atoms = L.n;
+    s.k = L.k;
+    s.negated = p->d_negated;
+    s.negated_ext = p->d_negated_ext;
+    s.free_rank = p->d_free_rank;
+    s.guesses = p->d_sguess;       // the round's columns
+    s.gbuf = p->d_sguess;
+    s.woff = 0;
+    s.facts = p->d_facts;
+    s.nfacts = p->nfacts;
+    s.top = L.top;
+    s.any_rw = p->d_any;
+    s.accepted = acc;
+    s.n_accepted = dev ? reinterpret_cast<long long *>(n_accepted_out)
+                       : reinterpret_cast<long long *>(p->d_scal + 4);
+    s.passes_out = p->d_scal + 3;   // (per round; the sum goes to passes_sum_out)
+    s.seed = (unsigned long long)seed;
+    s.max_rounds = max_rounds;
+    s.rounds_out = dev ? rounds_out : p->d_scal + 6;
+    s.passes_sum_out = dev ? passes_out : p->d_scal + 7;
+    s.status_user = (dev && run) ? run->status_out : nullptr;
+    if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
+    CK(launch_st_search(s, p->st_blocks, p->st_smem, st));
+    if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
+    p->stable_valid = true;
+    if (guesses_out && L.k > 0)
+        CK(cudaMemcpyAsync(guesses_out, p->d_sguess, (size_t)L.k * W * 8,
+                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (dev) return LP_OK;
+    int32_t scal[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(scal, p->d_scal, sizeof(scal), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(accepted_out, acc, (size_t)W * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int64_t na;
+    std::memcpy(&na, scal + 4, sizeof(na));
+    *n_accepted_out = na;
+    *rounds_out = scal[6];
+    *passes_out = scal[7];
     if (run && run->status_out) *run->status_out = scal[2];
     return status_of(scal[2]);
 }

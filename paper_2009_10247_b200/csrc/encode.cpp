@@ -207,7 +207,10 @@ static lp_status encode_core(const lp_rules *r, bool build_occ, HostLayout *L, s
     // from the program, never from v0: an atom outside D2 is true only if v0 says so.
     // It picks each row's lead atom here and the fine/coarse key groups at load.
     L->deriv2.assign((size_t)n, 0);
-    {
+    if (L->deriv_hint) {   // the caller's D2 (lp_options.derivable: e.g. of the whole program
+                           // when this one is a head-range shard of it)
+        for (int32_t a = 0; a < n; ++a) L->deriv2[(size_t)a] = L->deriv_hint[a] ? 1 : 0;
+    } else {
         auto in_d1 = [&](int32_t x) { return x >= n || per_head[(size_t)x] || isfact[(size_t)x]; };
         int64_t q = 0;
         for (int64_t i = 0; i < R; ++i) {
@@ -217,6 +220,8 @@ static lp_status encode_core(const lp_rules *r, bool build_occ, HostLayout *L, s
             q += len[i];
         }
     }
+    for (int64_t i = 0; i < R; ++i)   // (facts are always derivable)
+        if (len[i] == 0) L->deriv2[(size_t)r->head[i]] = 1;
     // lead atom (body position 0, the one the full θ-pass streams first and tests before
     // anything else is loaded): the first body atom outside D2 if there is one, else the
     // input order is kept.  The AND is order-free, so this changes how many rows need a

@@ -286,13 +286,16 @@ __device__ __forceinline__ void lm_zero_summaries(const LMParams &p, bool summar
 // fixpoint both buffers hold the model, after a capped pass only this one does).
 __device__ __noinline__ void lm_extract(const LMParams &p, int64_t gtid, int64_t gthreads,
                                         const uint32_t *v_last) {
-    const int64_t nw = ((int64_t)p.n_out + 63) >> 6;
-    for (int64_t w = gtid; w < nw; w += gthreads) {
+    // (lp_run.out_word_lo / out_word_count: only model words [w0, w0 + nw) are written,
+    // to model_out[0 .. nw) -- a head-range shard's owned words)
+    const int64_t nw = p.out_wn;
+    for (int64_t i = gtid; i < nw; i += gthreads) {
+        const int64_t w = p.out_w0 + i;
         unsigned long long v = (unsigned long long)__ldcg(v_last + 2 * w) |
                                ((unsigned long long)__ldcg(v_last + 2 * w + 1) << 32);
         const int64_t lo = w * 64;
         if (lo + 64 > p.n_out) v &= (1ull << (uint32_t)(p.n_out - lo)) - 1ull;
-        p.model_out[w] = v;
+        p.model_out[i] = v;
     }
 }
 
@@ -1232,6 +1235,32 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
 #undef PDBG
 }
 
+// Estimated rows a key-mode LEAD pass would queue: Σ over live runs of rows x (set
+// summary bits of the run's bucket / groups per bucket).  All threads of the CTA call it
+// (the key summary in sm, 16-bit codes: bucket b = summary words [b << 11, (b+1) << 11)).
+__device__ __noinline__ bool lead_start_too_dense(const LMParams &p, const uint32_t *sm, const int4 *runs_sm) {
+    __shared__ uint32_t bc[32];
+    __shared__ unsigned long long est;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid < 32) bc[tid] = 0u;
+    if (tid == 0) est = 0ull;
+    __syncthreads();
+    for (int32_t w0 = tid & ~31; w0 < p.ksm_words; w0 += blockDim.x) {   // a warp's 32 words: one bucket
+        const int32_t w = w0 + lane;
+        uint32_t c = w < p.ksm_words ? (uint32_t)__popc(sm[w]) : 0u;
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+        if (lane == 0 && c) atomicAdd(&bc[(w0 >> 11) & 31], c);
+    }
+    __syncthreads();
+    for (int32_t r = tid; r < p.nruns; r += blockDim.x) {
+        const int4 ru = runs_sm[r];
+        const unsigned long long e = (unsigned long long)ru.y * 8ull * bc[ru.z & 31] >> 16;
+        if (e) atomicAdd(&est, e);
+    }
+    __syncthreads();
+    return (long long)est * p.dense_div > p.n_slots;
+}
+
 // One cooperative launch = the whole fixpoint loop of Algorithm 1:
 // pass k reads v_k (rd) and writes v_{k+1} (wr); the loop ends after the first pass
 // that derives nothing (u = v), and iters = k + 1 counts that pass too.
@@ -1296,7 +1325,6 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     }
     grid.sync();
     if (p.dbg && tid == 0) p.dbg[(2 * gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
-    bool rebuild = false;                                // key space -> atom-id summary
     const int32_t n0 = cta_pass_counts(p.tail, nullptr, nullptr).appended;
     {
         if (!ksum_image)
@@ -1331,7 +1359,23 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
 
     int32_t ds = n0, de = n0;  // atoms that became true in the previous pass
     int k_start = 0;
-    if (!EXACT && keys && p.locc_ptr) {   // pipelined key-space LEAD passes
+    bool rebuild = false;                                // key space -> atom-id summary
+    // Predictive start (auto schedule, 16-bit key plane): the rows a first LEAD pass would
+    // queue are estimated from the live runs and the density of set bits in their buckets;
+    // more than n_slots / dense_div -> start with STREAM passes instead of verifying them
+    // (a v0 with many atoms outside D2 lights the coarse buckets: DESIGN.md "Schedule")
+    if (!EXACT && keys && p.pass_mode == 0 && p.key_bits == 16 && p.nruns > 0 &&
+        lead_start_too_dense(p, sm, runs_sm)) {
+        lead_pass = false;
+        keys = false;
+        rebuild = true;
+    }
+    // the live stream of a key-mode LEAD pass is long enough to hide verification and the
+    // barrier behind it (else all warps stream, then all verify: fewer round trips per
+    // row on the critical path -- DESIGN.md "Live runs")
+    const long long oct_bytes = p.key_bits == 8 ? 10 : 17;
+    if (!EXACT && keys && p.locc_ptr && (long long)live_tot * oct_bytes >= p.overlap_min_bytes) {
+        // pipelined key-space LEAD passes
         const PipeExit e = lm_pipe(p, sm, bmask, p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, n0,
                                    lead ? clk0 : 0, lead ? ns0 : 0, ls);
         if (e.done) return;
@@ -1356,7 +1400,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             if (tid == 0) streamers_done = 0;
             if (k == 0) __syncthreads();   // (later passes sync after the delta below)
         }
-        if (k > 0) {
+        if (k > 0 || rebuild) {
             // shared copy: v_{k-1} -> v_k
             if (EXACT && (de - ds) > (p.sm_words >> 2)) {
                 for (int32_t w = tid; w < p.sm_words; w += blockDim.x) sm[w] = __ldcg(rd + w);
@@ -1425,7 +1469,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         // the stream.  Entries past the shared part wait for the epilogue.
         // (key mode only: with the exact in-smem truth the stream is L2-fast and 4 fewer
         // streaming warps cost more than the overlap saves -- measured C2 +20 %, C3 +6 %)
-        const bool overlap = p.overlap && !EXACT && keys;
+        const bool overlap = p.overlap && !EXACT && keys && (long long)lv.total * oct_bytes >= p.overlap_min_bytes;
         if (overlap) {
             const int warp = tid >> 5;
             const int64_t sthreads = (int64_t)gridDim.x * (kStreamWarps * 32);
@@ -1752,7 +1796,7 @@ __device__ void st_init_phase(const STParams &p, int64_t gtid, int64_t gthreads)
 // Zero the matrix rows the previous stable call changed -- exactly the rows with a pass
 // tag in mark[] -- in both buffers (rows it did not change are still zero), the tags
 // themselves and the call's counters.  A warp per row, lanes over its words.
-__device__ void st_clear_phase(const STParams &p, int64_t gtid, int64_t gthreads) {
+__device__ void st_clear_phase(const STParams &p, int32_t clear_rows, int64_t gtid, int64_t gthreads) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = gtid >> 5;
     const int64_t nwarps = gthreads >> 5;
@@ -1761,7 +1805,7 @@ __device__ void st_clear_phase(const STParams &p, int64_t gtid, int64_t gthreads
         const bool tagged = h < p.n_ext && __ldcg(p.mark + h) != 0;
         unsigned m = __ballot_sync(0xFFFFFFFFu, tagged);
         if (tagged) p.mark[h] = 0;
-        while (m && p.clear_rows) {
+        while (m && clear_rows) {
             const int e = __ffs(m) - 1;
             m &= m - 1;
             for (int32_t w = lane; w < p.Wp; w += 32) {
@@ -1838,7 +1882,7 @@ __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int
 // once, until no word changes.  Shared memory holds one "any guess" bit per extended
 // atom; a row whose body has an atom false in every guess is skipped after the bit
 // test, so only candidate rows gather the 8·Wp-byte guess rows.
-__global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_constant__ STParams p) {
+__device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
     extern __shared__ uint32_t sm[];
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
@@ -1850,7 +1894,7 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
     __shared__ int32_t st_qn, st_qover;
     // the call's set-up, in the same launch: the previous call's rows and this call's
     // counters cleared, then T_0 (Def. 8) and its "any" bits
-    st_clear_phase(p, gtid, gthreads);
+    st_clear_phase(p, clear_rows, gtid, gthreads);
     grid.sync();
     st_init_phase(p, gtid, gthreads);
     grid.sync();
@@ -2071,7 +2115,128 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
     }
     // both buffers hold the fixpoint (rows changed in the last pass were copied during it)
     st_check_phase(p, gtid, gthreads);
-    if (gtid == 0 && p.status_user) *p.status_user = *(volatile int32_t *)p.status_out;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_constant__ STParams p) {
+    st_run(p, p.clear_rows);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && p.status_user)
+        *p.status_user = *(volatile int32_t *)p.status_out;
+}
+
+// ------------------------------------------------------------------------------------
+// guess-space reduction: sampling + local search (reading R23)
+// ------------------------------------------------------------------------------------
+//
+// h columns per round: round 0 samples abar_j = rbit(seed, 0, g, j) for every free
+// negated atom; a round runs the whole stable call above (clear, T_0 from the columns,
+// Algorithm 2's loop, Algorithm 3's test); with no accepted column every column g flips
+// the violated pairs j (a_j ∈ LM_g  ==  abar_j) whose rbit(seed, r+1, g, j) is 1, or one
+// violated pair chosen by rand64(seed, r+1, g, k) if none is; then the next round -- all
+// rounds in ONE cooperative launch.  Counter-based SplitMix64 (Steele, Lea, Flood 2014):
+// rand64(seed, r, g, j) = mix(mix(mix(mix(seed) ^ r) ^ g) ^ j), rbit = rand64 >> 63.
+
+__device__ __forceinline__ unsigned long long sm64_mix(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// round 0: the columns of the initial matrix (a warp per (row j, 32 columns))
+__device__ void search_sample(const STParams &p, int64_t gtid, int64_t gthreads) {
+    const int lane = threadIdx.x & 31;
+    const int64_t hw_n = 2 * (int64_t)p.W;                     // 32-column groups
+    uint32_t *g32 = reinterpret_cast<uint32_t *>(p.gbuf);     // row j: 2W words
+    const unsigned long long m1 = sm64_mix(sm64_mix(p.seed) ^ 0ull);
+    for (int64_t t = gtid >> 5; t < (int64_t)p.k * hw_n; t += gthreads >> 5) {
+        const int32_t j = (int32_t)(t / hw_n);
+        const int64_t hw = t % hw_n;
+        const int64_t g = hw * 32 + lane;
+        bool b = false;
+        if (g < p.G && p.free_rank[j] >= 0)
+            b = (sm64_mix(sm64_mix(m1 ^ (unsigned long long)g) ^ (unsigned long long)j) >> 63) != 0;
+        const unsigned w = __ballot_sync(0xFFFFFFFFu, b);
+        if (lane == 0) g32[(int64_t)j * hw_n + hw] = w;
+    }
+}
+
+// the local-search move from the fixpoint columns of round r_next - 1 (a warp per 32
+// columns; T0 holds the fixpoint, gbuf the round's columns)
+__device__ void search_move(const STParams &p, int32_t r_next, int64_t gtid, int64_t gthreads) {
+    const int lane = threadIdx.x & 31;
+    const int64_t hw_n = 2 * (int64_t)p.W;
+    uint32_t *g32 = reinterpret_cast<uint32_t *>(p.gbuf);
+    const uint32_t *T32 = reinterpret_cast<const uint32_t *>(p.T0);   // row a: 2Wp words
+    const unsigned long long m2 = sm64_mix(sm64_mix(p.seed) ^ (unsigned long long)r_next);
+    for (int64_t hw = gtid >> 5; hw < hw_n; hw += gthreads >> 5) {
+        const int64_t g = hw * 32 + lane;
+        const bool valid = g < p.G;
+        const unsigned long long m3 = sm64_mix(m2 ^ (unsigned long long)g);
+        int32_t nviol = 0, nflip = 0;
+        for (int32_t j = 0; j < p.k; ++j) {
+            const uint32_t bar = (__ldcg(g32 + (int64_t)j * hw_n + hw) >> lane) & 1u;
+            const uint32_t inlm = (__ldcg(T32 + (int64_t)p.negated[j] * 2 * p.Wp + hw) >> lane) & 1u;
+            const bool viol = bar + inlm != 1u;
+            nviol += viol;
+            nflip += viol && (sm64_mix(m3 ^ (unsigned long long)j) >> 63);
+        }
+        // no flip drawn: the violated pair number rand64(seed, r_next, g, k) mod |V_g|
+        const int32_t sel = (nflip == 0 && nviol > 0)
+                                ? (int32_t)(sm64_mix(m3 ^ (unsigned long long)p.k) % (unsigned long long)nviol)
+                                : -1;
+        int32_t cnt = 0;
+        for (int32_t j = 0; j < p.k; ++j) {
+            uint32_t *wp = g32 + (int64_t)j * hw_n + hw;
+            const uint32_t bar = (__ldcg(wp) >> lane) & 1u;
+            const uint32_t inlm = (__ldcg(T32 + (int64_t)p.negated[j] * 2 * p.Wp + hw) >> lane) & 1u;
+            const bool viol = bar + inlm != 1u;
+            bool flip;
+            if (sel >= 0) {
+                flip = viol && cnt == sel;
+                cnt += viol;
+            } else {
+                flip = viol && (sm64_mix(m3 ^ (unsigned long long)j) >> 63);
+            }
+            const unsigned w = __ballot_sync(0xFFFFFFFFu, valid && ((bar ^ (flip ? 1u : 0u)) != 0u));
+            if (lane == 0) *wp = w;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) st_search_kernel(const __grid_constant__ STParams p) {
+    cg::grid_group grid = cg::this_grid();
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    __shared__ long long s_nacc;
+    search_sample(p, gtid, gthreads);
+    grid.sync();
+    int32_t passes = 0;
+    for (int32_t r = 0;; ++r) {
+        st_run(p, r == 0 ? p.clear_rows : 1);
+        grid.sync();   // (the check phase's accepted words and count are complete)
+        if (threadIdx.x == 0) s_nacc = __ldcg(reinterpret_cast<const long long *>(p.n_accepted));
+        __syncthreads();
+        const long long nacc = s_nacc;
+        if (lead) passes += *(volatile int32_t *)p.passes_out;
+        if (nacc > 0 || r + 1 >= p.max_rounds) {
+            if (lead) {
+                *p.rounds_out = r + 1;
+                *p.passes_sum_out = passes;
+                if (p.status_user) *p.status_user = *(volatile int32_t *)p.status_out;
+            }
+            return;
+        }
+        search_move(p, r + 1, gtid, gthreads);
+        grid.sync();
+    }
+}
+
+cudaError_t launch_st_search(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
+    STParams q = p;
+    void *args[] = {(void *)&q};
+    return cudaLaunchCooperativeKernel((const void *)st_search_kernel, dim3(blocks), dim3(kThreads), args,
+                                       smem, st);
 }
 
 cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
@@ -2127,6 +2292,9 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
     if ((e = cudaFuncSetAttribute((const void *)st_fixpoint_kernel,   // (+ its static candidate queue)
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
         return e;
+    if ((e = cudaFuncSetAttribute((const void *)st_search_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
+        return e;
     return cudaSuccess;
 }
 
@@ -2147,7 +2315,9 @@ int lm_frontier_blocks_per_sm() {
 int st_blocks_per_sm(size_t smem) {
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)st_fixpoint_kernel, kThreads, smem);
-    return nb;
+    int ns = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ns, (const void *)st_search_kernel, kThreads, smem);
+    return std::min(nb, ns);   // (both launch on the same grid)
 }
 
 }  // namespace lpb

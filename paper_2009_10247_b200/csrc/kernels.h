@@ -56,7 +56,8 @@ struct LMParams {
     const uint32_t *init_ksum; // (key mode) v_0's key summary [ksm_words] + bucket mask [kBucketWords]
     int32_t n_init;
     int32_t top;               // ⊤
-    unsigned long long *model_out;  // [ceil(n/64)] written by the epilogue
+    unsigned long long *model_out;  // [out_wn] written by the epilogue: model words out_w0..
+    int64_t out_w0, out_wn;
     int32_t *tail_next;        // the other-parity run counters, zeroed for the next call
     int32_t *status_next;
     // shared-memory copy of the truth vector: exact (shift 0) or a summary whose bit g
@@ -99,6 +100,7 @@ struct LMParams {
     long long stream_entries;  // body entries (incl. padding) one STREAM pass reads
     int32_t auto_stream_first; // auto schedule starts with STREAM passes (long bodies)
     int32_t overlap;           // LEAD passes verify while they stream (warp-specialised)
+    long long overlap_min_bytes;  // ... when the pass streams at least this many bytes
     // pipelined key-mode LEAD passes (lm_pipe): rows by lead atom, and the counter of the
     // split grid barrier; locc_ptr == NULL = not pipelined
     const int32_t *locc_ptr;   // [n_ext + 1]
@@ -186,6 +188,13 @@ struct STParams {
     int32_t clear_rows;                 // zero the rows the previous call changed (mark != 0)
     unsigned long long *accepted;       // [W] accepted-guess mask (check)
     long long *n_accepted;
+    // guess-space reduction (st_search_kernel, lp_stable_search): the round's columns are
+    // gbuf ([k][W], = guesses), rewritten in place by the local-search move
+    unsigned long long *gbuf;
+    unsigned long long seed;
+    int32_t max_rounds;
+    int32_t *rounds_out;
+    int32_t *passes_sum_out;            // whole-matrix passes summed over the rounds
 };
 
 // ---- launchers (return cudaError_t of the launch) -----------------------------------
@@ -197,6 +206,8 @@ cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st);
 // One cooperative launch per stable call: clear the previous call's rows, build T_0, the
 // fixpoint loop, the stability check.
 cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st);
+// Guess-space reduction: all rounds of sampling + local search in one cooperative launch.
+cudaError_t launch_st_search(const STParams &p, int blocks, size_t smem, cudaStream_t st);
 cudaError_t launch_st_column(const STParams &p, int32_t n, int64_t g, unsigned long long *out,
                              cudaStream_t st);
 

@@ -49,6 +49,7 @@ struct HostLayout {
 
     std::vector<int32_t> facts;     // distinct atoms with a fact rule (in the encoded program)
     std::vector<uint8_t> deriv2;    // [n] atom in D2 (encode.cpp): may become true from the facts
+    const uint8_t *deriv_hint = nullptr;   // [n] caller's D2 (lp_options.derivable), or NULL
     std::vector<int32_t> st_facts;  // LP_LOAD_PAPER_LAYOUT: atoms with a fact in P whose
                                     // fact became an auxiliary one (Def. 8 item 2 rows)
     std::vector<int32_t> negated;   // k ascending atom ids

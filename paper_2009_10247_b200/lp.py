@@ -44,14 +44,15 @@ class lp_rules(ctypes.Structure):
 class lp_options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("guess_cap", ctypes.c_int), ("flags", ctypes.c_uint32),
                 ("smem_bits_cap", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
-                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", _P)]
+                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", _P), ("derivable", _P)]
 
 
 class lp_run(ctypes.Structure):
     _fields_ = [("stream", _P), ("flags", ctypes.c_uint32), ("popcounts_out", _P),
                 ("popcounts_cap", ctypes.c_int32), ("stage_out", _P), ("ev_begin", _P),
                 ("ev_end", _P), ("stats_out", _P), ("max_passes", ctypes.c_int32),
-                ("converged_out", _P), ("guess_offset", ctypes.c_int64), ("status_out", _P)]
+                ("converged_out", _P), ("guess_offset", ctypes.c_int64), ("status_out", _P),
+                ("out_word_lo", ctypes.c_int64), ("out_word_count", ctypes.c_int64)]
 
 
 class lp_info_t(ctypes.Structure):
@@ -68,7 +69,8 @@ class lp_info_t(ctypes.Structure):
 
 
 SYMBOLS = ("lp_load", "lp_info", "lp_negated_atoms", "lp_least_model", "lp_stable_models",
-           "lp_stable_matrix", "lp_guess_model", "lp_free", "lp_status_str", "lp_last_error")
+           "lp_stable_search", "lp_stable_matrix", "lp_guess_model", "lp_free", "lp_status_str",
+           "lp_last_error")
 
 _lib = None
 
@@ -92,6 +94,9 @@ def library():
         lib.lp_least_model.restype = st
         lib.lp_stable_models.argtypes = [_P, _P, ctypes.c_int64, _P, _P, _P, ctypes.POINTER(lp_run)]
         lib.lp_stable_models.restype = st
+        lib.lp_stable_search.argtypes = [_P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, _P, _P,
+                                         _P, _P, _P, ctypes.POINTER(lp_run)]
+        lib.lp_stable_search.restype = st
         lib.lp_stable_matrix.argtypes = [_P, _P, ctypes.POINTER(lp_run)]
         lib.lp_stable_matrix.restype = st
         lib.lp_guess_model.argtypes = [_P, ctypes.c_int64, _P, ctypes.POINTER(lp_run)]
@@ -178,7 +183,7 @@ class Program:
 
     def __init__(self, rules, device: int = 0, guess_cap: int = 20, frontier: bool = True,
                  smem_bits_cap: int = 0, grid_blocks: int = 0, allocator: str = "torch",
-                 paper_layout: bool = False, key8: bool = False):
+                 paper_layout: bool = False, key8: bool = False, derivable=None):
         lib = library()
         self._keep = []
         head = np.ascontiguousarray(rules.head, dtype=np.int32)
@@ -192,6 +197,11 @@ class Program:
         opt.flags = ((0 if frontier else LP_LOAD_NO_FRONTIER) |
                      (LP_LOAD_PAPER_LAYOUT if paper_layout else 0) | (LP_LOAD_KEY8 if key8 else 0))
         opt.smem_bits_cap = int(smem_bits_cap)
+        if derivable is not None:
+            der = np.ascontiguousarray(derivable, dtype=np.uint8)
+            assert der.shape[0] >= int(rules.n_atoms)
+            self._keep.append(der)
+            opt.derivable = der.ctypes.data
         opt.grid_blocks = int(grid_blocks)
         if device >= 0 and allocator == "torch":
             a, f = _torch_allocator(device)
@@ -276,6 +286,23 @@ class Program:
         assert ids.size == nacc
         return ids, passes, acc[:W]
 
+    def stable_search(self, h: int, seed: int, max_rounds: int, stream=None):
+        """Guess-space reduction (lp_stable_search).  Host-buffer call.
+        Returns dict(accepted=local column ids of the last round (np.int64), rounds,
+        passes, guesses=uint8[h][k] abar values of the last round)."""
+        k = self.info["n_negated"]
+        W = (int(h) + 63) // 64
+        acc = np.zeros(max(W, 1), dtype=np.uint64)
+        gs = np.zeros((max(k, 1), max(W, 1)), dtype=np.uint64)
+        nacc, rounds, passes = lp_stable_search(self, h, seed, max_rounds, gs, acc, stream=stream)
+        bits = np.unpackbits(acc[:W].view(np.uint8), bitorder="little")[:h]
+        ids = np.nonzero(bits)[0].astype(np.int64)
+        assert ids.size == nacc
+        cols = np.zeros((int(h), k), dtype=np.uint8)
+        for j in range(k):
+            cols[:, j] = np.unpackbits(gs[j, :W].view(np.uint8), bitorder="little")[:h]
+        return dict(accepted=ids, rounds=rounds, passes=passes, guesses=cols)
+
     def stable_matrix(self, stream=None):
         G = self._last_G
         W = (G + 63) // 64
@@ -355,7 +382,8 @@ def _run(stream=None, flags=0, pops=None, stage=None, ev_begin=None, ev_end=None
 
 def lp_least_model(p: Program, v0, model_out, frontier=False, pops=None, stage=None, stream=None,
                    device_ptrs=False, iters_out=None, ev_begin=None, ev_end=None, schedule="auto",
-                   stats=None, max_passes=0, converged=None, pipeline=True, status_out=None):
+                   stats=None, max_passes=0, converged=None, pipeline=True, status_out=None,
+                   out_words=None):
     """Marshals lp_least_model.  Host mode (default): numpy buffers, returns iters.
     device_ptrs=True: torch CUDA tensors (v0 int64 words or None, model_out int64
     words, iters_out int32[1], optional pops/stage, optional status_out int32[1] that
@@ -368,6 +396,8 @@ def lp_least_model(p: Program, v0, model_out, frontier=False, pops=None, stage=N
     run.max_passes = int(max_passes)
     if status_out is not None:
         run.status_out = _ptr(status_out) if device_ptrs else ctypes.addressof(status_out)
+    if out_words is not None:                 # (first word, word count) of the model written
+        run.out_word_lo, run.out_word_count = int(out_words[0]), int(out_words[1])
     if converged is not None and not device_ptrs:
         run.converged_out = ctypes.addressof(converged)
     if device_ptrs:
@@ -407,6 +437,30 @@ def lp_stable_models(p: Program, guesses, n_guesses, accepted_out, stream=None, 
                                        ctypes.addressof(na), ctypes.addressof(ps), ctypes.byref(run)),
            "lp_stable_models")
     return na.value, ps.value
+
+
+def lp_stable_search(p: Program, h, seed, max_rounds, guesses_out, accepted_out, stream=None,
+                     device_ptrs=False, n_accepted_out=None, rounds_out=None, passes_out=None,
+                     ev_begin=None, ev_end=None, status_out=None):
+    """Marshals lp_stable_search.  Host mode: numpy buffers (guesses_out uint64[k][W] or
+    None, accepted_out uint64[W]); returns (n_accepted, rounds, passes).  device_ptrs:
+    torch CUDA tensors, asynchronous on ``stream``."""
+    run = _run(stream, LP_PTR_DEVICE if device_ptrs else 0, ev_begin=ev_begin, ev_end=ev_end)
+    if status_out is not None:
+        run.status_out = _ptr(status_out) if device_ptrs else ctypes.addressof(status_out)
+    p._last_G = int(h)
+    if device_ptrs:
+        _check(library().lp_stable_search(p.handle, int(h), int(seed) & ((1 << 64) - 1), int(max_rounds),
+                                           _ptr(guesses_out), _ptr(accepted_out), _ptr(n_accepted_out),
+                                           _ptr(rounds_out), _ptr(passes_out), ctypes.byref(run)),
+               "lp_stable_search")
+        return None
+    na, rd, ps = ctypes.c_int64(0), ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(library().lp_stable_search(p.handle, int(h), int(seed) & ((1 << 64) - 1), int(max_rounds),
+                                       _ptr(guesses_out), _ptr(accepted_out), ctypes.addressof(na),
+                                       ctypes.addressof(rd), ctypes.addressof(ps), ctypes.byref(run)),
+           "lp_stable_search")
+    return na.value, rd.value, ps.value
 
 
 def lp_stable_matrix(p: Program, out, stream=None, device_ptrs=False):

@@ -50,6 +50,18 @@ def test_c4_v0_null_all_schedules(c4):
     assert ex["stats"]["bytes"] < 0.2 * full, (ex["stats"], full)
 
 
+def test_c4_v0_null_pipelined(c4, monkeypatch):
+    """The pipelined key-space LEAD passes (taken by default only for live streams of at
+    least LP_OVERLAP_MIN_MB) on C4 from the facts."""
+    P, _ = c4
+    monkeypatch.setenv("LP_OVERLAP_MIN_MB", "0")
+    prog = lp.Program(P, frontier=False)
+    try:
+        check_lm(P, prog=prog, variants=(False,))
+    finally:
+        prog.close()
+
+
 def test_c4_key8(c4):
     P, prog = c4
     om, ostage, oit, opops = _oracle_lm(P)

@@ -19,6 +19,21 @@ def _need_gpu():
         pytest.skip("no CUDA device (these tests run on the B200 box)")
 
 
+@pytest.fixture(scope="module", autouse=True)
+def _overlap_always():
+    """Programs here are small, so by default their key-mode LEAD passes would never take
+    the overlapped / pipelined path (LP_OVERLAP_MIN_MB, read by lp_load): force it, so
+    every parity case covers it; test_default_overlap_threshold covers the default."""
+    import os
+    old = os.environ.get("LP_OVERLAP_MIN_MB")
+    os.environ["LP_OVERLAP_MIN_MB"] = "0"
+    yield
+    if old is None:
+        del os.environ["LP_OVERLAP_MIN_MB"]
+    else:
+        os.environ["LP_OVERLAP_MIN_MB"] = old
+
+
 def _oracle_lm(P, v0=None):
     model, stage, iters = oracle.lm_stage(P, v0=v0)
     return oracle.pack_bits(model), stage, iters, oracle.popcounts_from_stage(stage, iters)
@@ -106,6 +121,21 @@ def test_forced_summary_mode_and_small_grids(seed, cfg):
         assert prog.info["key_shift"] >= 0          # LEAD passes stream the key plane
     # a start set with atoms that are neither heads nor facts (coarse key groups)
     v0 = rng.choice(n, size=n // 8, replace=False).tolist()
+    check_lm(P, v0=v0, prog=prog)
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("cfg", [dict(smem_bits_cap=128), dict(smem_bits_cap=1024, grid_blocks=3)])
+def test_default_overlap_threshold(seed, cfg, monkeypatch):
+    """Key-mode LEAD passes with the default LP_OVERLAP_MIN_MB: small live streams take
+    the plain pass (all warps stream, then all verify), as bench.py's main line does."""
+    monkeypatch.delenv("LP_OVERLAP_MIN_MB")
+    rng = np.random.default_rng([seed, 404])
+    n = int(rng.integers(1500, 4000))
+    P = lpgen.random_program(rng, n, 5 * n, max_len=5, n_facts=n // 25)
+    prog = check_lm(P, **cfg)
+    assert prog.info["key_shift"] >= 0
+    v0 = rng.choice(n, size=n // 10, replace=False).tolist()
     check_lm(P, v0=v0, prog=prog)
 
 
