@@ -5,7 +5,7 @@ Main line: least-model fixpoint of configuration C4 (10M atoms, 50M rules, ~150M
 nonzeros; BASELINE.json configs[3], the configuration the roofline target is quoted on)
 with the full fused θ-pass kernel (Algorithm 1), v0 = facts.  A step = one whole
 fixpoint (init + all θ-passes until no change + model extraction) through the C ABI,
-inputs resident in HBM.  value = nnz · iters / step time, summed over ranks.
+inputs resident in HBM.  value = nnz · iters / step time.
 
 Also measured (extra keys): the frontier variant on C4, the batched stable-model search
 on C5 (guesses/s), the end-to-end call with host buffers (e2e), the per-launch roofline
@@ -14,9 +14,12 @@ of the dominant kernel and the CPU oracle baseline (cpu_baseline).
 --impl reference times the CPU oracle (oracle/, as it stands) on the same workload and
 metric: each step is one whole O-STAGE fixpoint of C4 on one pinned host core.
 
-Multi-GPU (torchrun, N > 1): "replicas only" -- every rank solves its own copy of the
-workload (the least-model fixpoint has no partition without a per-pass exchange; see
-DESIGN.md), timing is the max over ranks, value the sum of units over ranks.
+Multi-GPU (torchrun, N > 1): ONE C4 least model sharded by head ranges over the ranks
+(shard.py): per pass a θ-pass of each rank's rules, an NCCL all-gather of the
+owned words + status word and the device combine kernel (lp_shard_combine); "scaling":
+"strong" (the same program for every N), time = max over ranks.  The stable-model search
+on C5 is guess-sharded (no exchange until the final mask gather) in the "stable" key.
+BENCH_FORCE_DIST=1 runs that path with one rank on one GPU.
 """
 from __future__ import annotations
 
@@ -364,27 +367,49 @@ def main():
                   "ms_per_step": e2e_ms, "api": "lp_least_model (host pointers, synchronous)",
                   "model_check": "equal to the device-pointer main line's model"}
 
-    if not args.no_extras and dist:
-        # ---- strong-scaling extra: ONE C4 least model sharded by head ranges over the
-        # ranks, one all-gather + OR per pass (shard.py) -------------------
+    if dist:
+        # ---- N > 1 main line: ONE C4 least model sharded by head ranges over the ranks
+        # (strong scaling): per pass one θ-pass per rank (owned words +
+        # status word), one NCCL all-gather of the payloads, one combine kernel on the
+        # device (OR, changed flag); the host reads pass k's flag after queuing pass k+1 ---
         from paper_2009_10247_b200.shard import ShardedLeastModel
         sharded = ShardedLeastModel(P)             # setup: head range, sub-program upload
         sh_t = []
-        for i in range(1 + min(args.steps, 5)):
+        for i in range(args.warmup + args.steps):
             flush_l2()
+            stream.synchronize()
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             m_sh, it_sh, _ = sharded.run(popcounts=False)
             e1.record()
             torch.cuda.synchronize()
-            if i >= 1:
+            if i >= args.warmup:
                 sh_t.append(e0.elapsed_time(e1))
         assert it_sh == iters and (m_sh == main_model).all()
         sh_ms = allmax(float(np.mean(sh_t)))
-        out["sharded"] = {"ms_per_step": sh_ms, "value": nnz * iters / (sh_ms / 1e3),
-                          "unit": "nnz*iter/s", "iters": it_sh, "ranks": ws,
-                          "what": "one program, head ranges per rank, all-gather + OR per pass"}
+        out["single_gpu"] = {"ms_per_step": ms_max, "kernel_ms": kms_max, "value": nnz * iters / (ms_max / 1e3),
+                             "what": "the one-GPU fused fixpoint on each rank (replica)"}
+        out.update(value=nnz * iters / (sh_ms / 1e3), ms_per_step=sh_ms, scaling="strong",
+                   gpu_launches=2 * (iters + 1) * args.steps)
+        out["config"]["parallelism"] = f"head-range shards x{ws} (one program)"
+        out["config"]["variant"] = ("head-range-sharded T_P passes: per pass one θ-pass per rank, NCCL "
+                                    "all-gather of owned words + status, device combine (lp_shard_combine)")
+        out["sharded"] = {"ms_per_step": sh_ms, "iters": it_sh, "ranks": ws,
+                          "words_per_rank": sharded.stride - 1, "lag": "host reads pass k's flag after queuing k+1"}
+        # e2e: host v0 in, host model out, through the sharded public API
+        fm = np.isin(np.arange(n), P.head[np.diff(P.body_ptr) == 0])
+        e2e_s = []
+        for i in range(args.warmup + args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            m_e, it_e, _ = sharded.run(v0=fm, popcounts=False)
+            e2e_s.append(time.perf_counter() - t0)
+        assert it_e == iters and (m_e == main_model).all()
+        e2e_sh = allmax(float(np.mean(e2e_s[args.warmup:])) * 1e3)
+        out["e2e"] = {"value": nnz * iters / (e2e_sh / 1e3), "unit": "nnz*iter/s",
+                      "h2d_bytes_per_step": Wm * 8, "d2h_bytes_per_step": Wm * 8,
+                      "ms_per_step": e2e_sh, "api": "shard.ShardedLeastModel.run(v0=host mask) -> host words"}
         del sharded
 
     if not args.no_extras:
@@ -497,6 +522,35 @@ def main():
             stable["accepted"], stable["passes"] = int(ids.size), ps
         out["stable"] = stable
         sprog.close()
+        # ---- guess-space reduction (lp_stable_search, reading R23): C5's
+        # recipe with k = 32 negated atoms -- 2^32 guesses, enumeration refused (LP_E_CAP);
+        # 128 sampled columns per round + local search, all rounds in one launch ----------
+        S32 = lpgen.gen_c5(seed=3, n=100_000, R=500_000, k=32)
+        sp32 = lp.Program(S32, device=local)
+        h, kk = 128, sp32.info["n_negated"]
+        gs = torch.zeros((kk, 2), dtype=torch.int64, device="cuda")
+        acc2 = torch.zeros(2, dtype=torch.int64, device="cuda")
+        na2 = torch.zeros(1, dtype=torch.int64, device="cuda")
+        rd2 = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ps2 = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ss_t = []
+        for i in range(args.warmup + args.steps):
+            flush_l2()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            lp.lp_stable_search(sp32, h, 5, 40, gs, acc2, stream=stream, device_ptrs=True, n_accepted_out=na2,
+                                rounds_out=rd2, passes_out=ps2, status_out=status_d)
+            e1.record(stream)
+            stream.synchronize()
+            assert int(status_d.item()) == 0
+            if i >= args.warmup:
+                ss_t.append(e0.elapsed_time(e1))
+        out["stable_search"] = {"workload": "C5 recipe, k = 32 (lpgen.gen_c5(seed=3, k=32))",
+                                "columns_per_round": h, "seed": 5, "rounds": int(rd2.item()),
+                                "passes": int(ps2.item()), "accepted": int(na2.item()),
+                                "ms_per_search": allmax(float(np.mean(ss_t))), "launches_per_call": 1,
+                                "enumeration": "2^32 guesses: lp_stable_models refuses (LP_E_CAP)"}
+        sp32.close()
 
     # ---- CPU baseline (BASELINE.md plan): O-STAGE, fixpoint only, one pinned core, median
     # of 3 trials; rank 0 at N = 1 only.  Its model also checks the GPU main line. -------

@@ -199,6 +199,9 @@ typedef struct {
     int32_t key_shift;        /* summary mode: keys per key-summary bit = 1 << key_shift;
                                  -1 when there is no key plane                         */
     int32_t n_aux;            /* LP_LOAD_PAPER_LAYOUT: auxiliary atoms of P^δ (else 0)  */
+    int32_t cluster_ctas;     /* > 0: the full θ-pass (auto schedule) runs in ONE thread-
+                                 block cluster of this many CTAs (truth in shared memory,
+                                 DSMEM exchange); 0: the persistent grid kernel         */
 } lp_info_t;
 
 /* Validate, standardize and encode a program, upload it (PAPER.md:62, 82-95,
@@ -283,6 +286,29 @@ lp_status lp_stable_matrix(lp_program *p, uint64_t *out, const lp_run *run);
  * the original atoms, [ceil(n/64)] words. */
 lp_status lp_guess_model(lp_program *p, int64_t guess, uint64_t *model_out,
                          const lp_run *run);
+
+/* Multi-GPU least model: the exchange step of one pass
+ * over head-range shards.  Rank r loads the rules whose head lies in its 64-aligned atom
+ * range (owned model words [word_lo[r], word_lo[r] + word_cnt[r])), runs ONE θ-pass
+ * from the common v_k (lp_least_model with max_passes = 1, its owned words written via
+ * lp_run.out_word_lo/count and its status word via lp_run.status_out into its payload),
+ * and the payloads are all-gathered (NCCL; the caller's plumbing).  This call then
+ * computes, on the device, v_{k+1} = v_k OR every rank's owned words -- T_P's OR clause
+ * across GPUs -- and whether any rank's pass derived an atom (u != v of Algorithm 1,
+ * PAPER.md:167).
+ *   gathered      : device [world][stride] words; rank r's row: its owned words at
+ *                   0 .. word_cnt[r]-1, its pass's lp_run.status_out word in the low 32
+ *                   bits of word stride-1 (LP_ST_CAPPED = the pass derived an atom).
+ *   word_lo, word_cnt : HOST [world] arrays; the ranges tile [0, n_words) in rank order,
+ *                   word_cnt[r] <= stride - 1.  world in [1, 64].
+ *   v, v_next     : device [n_words] model words (distinct buffers).
+ *   changed_out   : device or mapped pinned host int32, set to 1/0.
+ *   popcount_inout: optional device int32, |v_{k+1}| is ADDED to it (zero it first).
+ *   stream        : cudaStream_t; asynchronous. */
+lp_status lp_shard_combine(const uint64_t *gathered, int32_t world, int64_t stride,
+                           const int64_t *word_lo, const int64_t *word_cnt,
+                           const uint64_t *v, uint64_t *v_next, int64_t n_words,
+                           int32_t *changed_out, int32_t *popcount_inout, void *stream);
 
 /* Release the handle and its device memory (NULL is a no-op). */
 void lp_free(lp_program *p);

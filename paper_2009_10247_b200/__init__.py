@@ -8,8 +8,8 @@ Python binding of that ABI; PyTorch is used only for device memory and streams.
 """
 from .lp import (LIB_PATH, LPError, Program, bits_words, library, lp_free, lp_guess_model,
                  lp_info, lp_least_model, lp_load, lp_negated_atoms, lp_stable_matrix,
-                 lp_stable_models, lp_stable_search, pack_mask, unpack_bits)
+                 lp_shard_combine, lp_stable_models, lp_stable_search, pack_mask, unpack_bits)
 
 __all__ = ["LIB_PATH", "LPError", "Program", "bits_words", "library", "lp_free", "lp_guess_model",
            "lp_info", "lp_least_model", "lp_load", "lp_negated_atoms", "lp_stable_matrix",
-           "lp_stable_models", "lp_stable_search", "pack_mask", "unpack_bits"]
+           "lp_shard_combine", "lp_stable_models", "lp_stable_search", "pack_mask", "unpack_bits"]

@@ -56,6 +56,7 @@ struct lp_program {
     // computes the same results -- DESIGN.md "A/B switches")
     int32_t dense_div = 16;     // LP_DENSE_DIV: auto schedule's queued-rows divisor
     bool env_no_pipe = false;   // LP_NO_PIPE
+    bool env_no_predict = false;  // LP_NO_PREDICT
     bool env_no_overlap = false;  // LP_NO_OVERLAP
     bool env_no_ksum_image = false;  // LP_NO_KSUM_IMAGE
     bool env_no_zerocopy = false;    // LP_NO_ZEROCOPY
@@ -109,6 +110,9 @@ struct lp_program {
     unsigned long long *d_sguess = nullptr;   // lp_stable_search: the round's columns [k][W]
     size_t sguess_words_alloc = 0;
 
+    int cluster = 0;            // > 0: exact-mode program run by ONE cluster of this many CTAs
+    size_t cluster_smem = 0;
+    bool cluster_stage = false; // ... with the program planes staged in shared memory
     int sms = 0, threads = kThreads;
     int lm_blocks = 0, fr_blocks = 0, st_blocks = 0, grid_cap = 0;
     size_t lm_smem = 0, st_smem = 0;
@@ -502,6 +506,26 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(dalloc(p, &p->d_qbuf, (size_t)p->lm_blocks * p->qcap * (p->d_locc_ptr ? 2 : 1)));
     }
     p->fr_blocks = cap_grid(sms * bf);
+    // one thread-block cluster for exact-mode programs whose two truth buffers fit shared
+    // memory and whose flat lead / head planes a few SMs stream in a microsecond or two
+    // (DESIGN.md "Cluster kernel"); the grid_blocks test hook keeps the persistent grid
+    {
+        const size_t cs = 3 * (size_t)p->nwords * 4;   // (three truth buffers in rotation)
+        int64_t max_slots = (int64_t)1 << 16;   // (two CTAs at most: measured)
+        if (const char *e = std::getenv("LP_CLUSTER_MAX_SLOTS")) max_slots = std::atoll(e);
+        int64_t ent = 0;
+        for (const Segment &sg : L.segs) ent += (int64_t)sg.L * sg.count_pad;
+        const bool long_bodies = L.n_slots > 0 && ent > 32 * L.n_slots;   // (auto: STREAM first)
+        if (p->exact && p->d_lead32 && p->grid_cap == 0 && cs <= (size_t)kMaxSmemBytes && !long_bodies &&
+            L.n_slots <= max_slots && !std::getenv("LP_NO_CLUSTER")) {
+            const int want = (int)std::min<int64_t>(16, std::max<int64_t>(1, (L.n_slots + 32767) / 32768));
+            // one CTA and the planes fit next to the truth buffers: stage them in shared memory
+            const size_t planes = 4 * (2 * (size_t)L.n_slots + (size_t)ent);
+            p->cluster_stage = want == 1 && cs + planes <= (size_t)kMaxSmemBytes;
+            p->cluster_smem = cs + (p->cluster_stage ? planes : 0);
+            p->cluster = lm_cluster_max(want, p->cluster_smem);
+        }
+    }
     p->st_blocks = cap_grid(sms * bs);
     CK(cudaDeviceSynchronize());
 
@@ -543,6 +567,7 @@ extern "C" lp_status lp_load(const lp_rules *rules, const lp_options *opt, lp_pr
     }
     if (const char *e = std::getenv("LP_DENSE_DIV")) p->dense_div = std::max(1, std::atoi(e));
     p->env_no_pipe = std::getenv("LP_NO_PIPE") != nullptr;
+    p->env_no_predict = std::getenv("LP_NO_PREDICT") != nullptr;
     p->env_no_overlap = std::getenv("LP_NO_OVERLAP") != nullptr;
     p->env_no_ksum_image = std::getenv("LP_NO_KSUM_IMAGE") != nullptr;
     p->env_no_zerocopy = std::getenv("LP_NO_ZEROCOPY") != nullptr;
@@ -608,6 +633,7 @@ extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
     o->summary_shift = p->shift;
     o->grid_blocks = p->lm_blocks;
     o->block_threads = kFullThreads;
+    o->cluster_ctas = p->cluster;
     return LP_OK;
 }
 
@@ -753,10 +779,12 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.qcap = p->qcap;
     q.pass_mode = (flags & LP_FULL_STREAM) ? 2 : (flags & LP_FULL_LEAD) ? 1 : 0;
     q.dense_div = p->dense_div;
+    q.predict = p->env_no_predict ? 0 : 1;
     q.n_slots = L.n_slots;
     q.cand = p->d_scal + 12;
     q.vent = p->d_vent;
     q.overlap = p->env_no_overlap ? 0 : 1;
+    q.stage_planes = p->cluster_stage ? 1 : 0;
     q.overlap_min_bytes = p->overlap_min_bytes;
     const bool pipe = q.overlap && !(flags & LP_FULL_NO_PIPE) && !p->env_no_pipe;
     q.locc_ptr = pipe ? p->d_locc_ptr : nullptr;
@@ -795,7 +823,13 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.lead_bytes = (long long)lead_plane_bytes(p);
     q.stream_bytes = (long long)stream_plane_bytes(p);
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
+    // the auto schedule of an exact-mode program that fits one cluster runs there; the
+    // explicit schedules (LP_FULL_STREAM / LP_FULL_LEAD / LP_FULL_NO_PIPE) keep the
+    // persistent grid kernel (A/B and tests)
+    const bool use_cluster = !frontier && p->cluster > 0 &&
+                             !(flags & (LP_FULL_STREAM | LP_FULL_LEAD | LP_FULL_NO_PIPE));
     if (frontier) CK(launch_lm_frontier(q, p->fr_blocks, st));
+    else if (use_cluster) CK(launch_lm_cluster(q, p->cluster, p->cluster_smem, st));
     else CK(launch_lm_full(q, p->exact, p->lm_blocks, p->lm_smem, st));
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
     ++p->lm_runs;
@@ -1093,6 +1127,40 @@ extern "C" lp_status lp_guess_model(lp_program *p, int64_t guess, uint64_t *mode
     const size_t mw = ((size_t)p->L.n_out + 63) / 64;
     if (mw) CK(cudaMemcpyAsync(model_out, p->d_model, mw * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    return LP_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// lp_shard_combine (multi-GPU exchange step)
+// ------------------------------------------------------------------------------------
+
+extern "C" lp_status lp_shard_combine(const uint64_t *gathered, int32_t world, int64_t stride,
+                                      const int64_t *word_lo, const int64_t *word_cnt,
+                                      const uint64_t *v, uint64_t *v_next, int64_t n_words,
+                                      int32_t *changed_out, int32_t *popcount_inout, void *stream) {
+    if (!gathered || !word_lo || !word_cnt || !v || !v_next || !changed_out)
+        return set_err(LP_E_INVALID, "NULL argument");
+    if (world < 1 || world > kMaxRanks) return set_err(LP_E_INVALID, "world out of [1, 64]");
+    if (stride < 2 || n_words < 0) return set_err(LP_E_INVALID, "stride < 2 or n_words < 0");
+    ShardCombineParams q{};
+    q.gathered = reinterpret_cast<const unsigned long long *>(gathered);
+    q.world = world;
+    q.stride = stride;
+    int64_t next = 0;
+    for (int32_t r = 0; r < world; ++r) {
+        if (word_lo[r] != next || word_cnt[r] < 0 || word_cnt[r] > stride - 1)
+            return set_err(LP_E_INVALID, "word ranges must tile [0, n_words) in rank order and fit stride - 1");
+        q.word_lo[r] = word_lo[r];
+        q.word_cnt[r] = word_cnt[r];
+        next += word_cnt[r];
+    }
+    if (next != n_words) return set_err(LP_E_INVALID, "word ranges do not cover n_words");
+    q.v = reinterpret_cast<const unsigned long long *>(v);
+    q.v_next = reinterpret_cast<unsigned long long *>(v_next);
+    q.n_words = n_words;
+    q.changed = changed_out;
+    q.pops = popcount_inout;
+    CK(launch_shard_combine(q, (cudaStream_t)stream));
     return LP_OK;
 }
 

@@ -1074,8 +1074,8 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         const uint32_t *wr_k = (k & 1) ? p.buf0 : p.buf1;
         if (lead && p.stats) {
             atomicAdd(p.stats + 0, 4ull * (unsigned long long)queued + 12ull * (unsigned long long)(t - de));
-            p.stats[1] += 1;
-            p.stats[2] += (unsigned long long)queued;
+            atomicAdd(p.stats + 1, 1ull);   // (reductions: no load on the lead thread's
+            atomicAdd(p.stats + 2, (unsigned long long)queued);   //  critical path)
         }
         if (t == de || k + 1 >= p.max_passes || k + 1 == p.user_cap) {
             if (lead) {
@@ -1364,7 +1364,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     // queue are estimated from the live runs and the density of set bits in their buckets;
     // more than n_slots / dense_div -> start with STREAM passes instead of verifying them
     // (a v0 with many atoms outside D2 lights the coarse buckets: DESIGN.md "Schedule")
-    if (!EXACT && keys && p.pass_mode == 0 && p.key_bits == 16 && p.nruns > 0 &&
+    if (!EXACT && keys && p.pass_mode == 0 && p.key_bits == 16 && p.nruns > 0 && p.predict &&
         lead_start_too_dense(p, sm, runs_sm)) {
         lead_pass = false;
         keys = false;
@@ -1571,8 +1571,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             // (STREAM passes added the int4 loads they issued themselves, atomically)
             atomicAdd(p.stats + 0, (unsigned long long)(lead_pass && !keys ? p.lead_bytes : 0) +
                                        4ull * (unsigned long long)queued + 12ull * (unsigned long long)(t - de));
-            if (lead_pass) p.stats[1] += 1;
-            p.stats[2] += (unsigned long long)queued;
+            if (lead_pass) atomicAdd(p.stats + 1, 1ull);   // (reductions: no load on the
+            atomicAdd(p.stats + 2, (unsigned long long)queued);   //  lead thread's critical path)
         }
         if (t == de || k + 1 >= p.max_passes || k + 1 == p.user_cap) {  // u = v: fixpoint (or a cap)
             if (lead) {
@@ -1736,6 +1736,305 @@ cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------------------------
+// least model: ONE thread-block cluster for programs whose truth vector fits shared memory
+// ------------------------------------------------------------------------------------
+//
+// Small exact-mode programs are latency-bound on the persistent grid (a 148-CTA grid
+// barrier, counters in L2, dependent L2 round trips per pass: C1 ~7 us per pass).  Here a
+// cluster of S CTAs runs the whole fixpoint: every CTA keeps v_k and v_{k+1} EXACTLY in
+// its shared memory and streams its share of the flat lead / head planes (LEAD pass: a row
+// whose lead atom is in v_k and whose head is not is queued in shared memory); the queue
+// is verified after the stream by all threads (the other body atoms: one round trip,
+// tested in shared memory) and a firing head is ORed into the CTA's own v_{k+1} (a
+// shared-memory atomic).  Then every CTA ORs the words its pass changed into the other
+// CTAs' v_{k+1} (distributed shared memory, fire-and-forget reductions), one cluster
+// barrier (release / acquire) makes them visible, and every CTA -- holding the same
+// complete v_{k+1} -- counts the new atoms (u != v, the popcount trace) on its own and
+// writes the stages of the new atoms in the words it owns (word w: CTA w mod S).  The
+// buffer that held v_k is brought up to v_{k+1} at the next pass top (atomicOr: the next
+// pass's remote ORs may already arrive; ORs commute).  Same θ(M v_k) per pass as the
+// other kernels: same model, iters, popcounts, stages.
+constexpr int kClQueue = 4096;   // candidate rows a CTA queues per pass (shared memory)
+
+// The other body atoms of a queued row (lead in v_k, head not): one round trip for up to 8
+// of them, tested exactly against v_k; a firing row's head goes into this CTA's v_{k+1}.
+__device__ __forceinline__ void cl_verify(const LMParams &p, const Segment *segs, const int32_t *colg,
+                                          const int32_t *heads, const uint32_t *rd, uint32_t *wr, int32_t slot) {
+    int lo = 0, hi = p.nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (segs[mid].slot_off <= slot) lo = mid; else hi = mid - 1;
+    }
+    const int32_t L = segs[lo].L;
+    const int64_t cp = segs[lo].count_pad;
+    const int32_t *colp = colg + segs[lo].col_off + (slot - segs[lo].slot_off);
+    const int32_t h = heads[slot];
+    bool ok = true;
+    for (int32_t j0 = 1; j0 < L && ok; j0 += 8) {
+        uint32_t x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = j0 + j < L ? (uint32_t)colp[(int64_t)(j0 + j) * cp] : 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ok = ok && (x[j] == 0xFFFFFFFFu || sm_bit(rd, x[j]));
+    }
+    if (ok) atomicOr(wr + (h >> 5), 1u << (h & 31));
+}
+
+__global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_constant__ LMParams p) {
+    extern __shared__ __align__(16) uint32_t cbuf[];
+    __shared__ int32_t s_cnt, s_qn;
+    __shared__ int32_t cl_q[kClQueue];     // this pass's candidate rows
+    __shared__ Segment ssegs[kMaxSmemSegs];
+    __shared__ long long clk0;
+    __shared__ unsigned long long ns0;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int S = (int)cluster.num_blocks();
+    const int cr = (int)cluster.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31;
+    const bool lead = cr == 0 && tid == 0;
+    const int32_t nw = p.nwords;
+    // three truth buffers in rotation: pass k reads v_k from buf(k) and writes v_{k+1} into
+    // buf(k+1); the other CTAs' ORs of pass k+1 land in buf(k+2), which nobody reads while
+    // pass k's new atoms are counted after the barrier
+    auto buf = [&](int i) { return cbuf + (int64_t)i * nw; };
+    if (lead) {
+        clk0 = clock64();
+        ns0 = globaltimer();
+        *p.tail_next = 0;
+        *p.status_next = 0;
+        if (p.stats)
+            for (int i = 0; i < 6; ++i) p.stats[i] = 0;
+    }
+    if (p.nseg <= kMaxSmemSegs)
+        for (int32_t s = tid; s < p.nseg; s += blockDim.x) ssegs[s] = p.segs[s];
+    const Segment *segs = p.nseg <= kMaxSmemSegs ? ssegs : p.segs;
+    // the program planes: staged in shared memory after the truth buffers when they fit
+    // (one CTA, small programs: every pass then runs out of shared memory), else read
+    // from global memory (L2) each pass
+    const int32_t nq = (int32_t)(p.n_slots >> 2);
+    const int4 *lb = reinterpret_cast<const int4 *>(p.lead32);
+    const int4 *hb = reinterpret_cast<const int4 *>(p.head);
+    const int32_t *colg = p.col;
+    if (p.stage_planes) {
+        int4 *sl = reinterpret_cast<int4 *>(cbuf + 3 * nw);
+        int4 *sh = sl + nq;
+        int4 *sc = sh + nq;
+        const int64_t ncol4 = p.stream_entries >> 2;
+        for (int32_t i = tid; i < nq; i += blockDim.x) {
+            sl[i] = __ldg(lb + i);
+            sh[i] = __ldg(hb + i);
+        }
+        for (int64_t i = tid; i < ncol4; i += blockDim.x) sc[i] = __ldg(reinterpret_cast<const int4 *>(p.col) + i);
+        lb = sl;
+        hb = sh;
+        colg = reinterpret_cast<const int32_t *>(sc);
+    }
+    // block-wide sum of one value per thread (the count of new atoms); two barriers
+    auto block_sum = [&](int32_t x) {
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+        if (tid == 0) s_cnt = 0;
+        __syncthreads();
+        if (lane == 0 && x) atomicAdd(&s_cnt, x);
+        __syncthreads();
+        return s_cnt;
+    };
+    // v_0 = (v0 restricted to the original atoms) | facts | ⊤ in both buffers (Def. 4), its
+    // size, and the stages of the original atoms (this CTA's words)
+    int32_t pc = 0;
+    for (int32_t w = tid; w < nw; w += blockDim.x) {
+        const int64_t lo = (int64_t)w * 32;
+        uint32_t orig = __ldg(p.factbits + w);
+        if (p.v0 && w < p.v0_words) {
+            uint32_t v = __ldg(p.v0 + w);
+            if (lo + 32 > p.n_out) v &= lo >= p.n_out ? 0u : ((1u << (uint32_t)(p.n_out - lo)) - 1u);
+            orig |= v;
+        }
+        if (lo + 32 > p.n) orig &= lo >= p.n ? 0u : ((1u << (uint32_t)(p.n - lo)) - 1u);
+        uint32_t bits = orig;
+        if (w == (p.top >> 5)) bits |= 1u << (p.top & 31);
+        buf(0)[w] = bits;
+        buf(1)[w] = bits;
+        buf(2)[w] = bits;
+        pc += __popc(orig);
+        if (p.stage && (w % S) == cr)
+            for (int b = 0; b < 32 && lo + b < p.n_out; ++b) p.stage[lo + b] = ((orig >> b) & 1u) ? 0 : -1;
+    }
+    int32_t total = block_sum(pc);
+    cluster.sync();   // (every CTA's buffers initialised before any remote OR)
+    if (lead && p.pops && p.pop_cap > 0) p.pops[0] = total;
+    constexpr int U = 4;   // quads of the lead / head planes in flight per thread
+    const int32_t step = S * (int32_t)blockDim.x;
+#define CDBG(k, i) p.dbg[((k) * gridDim.x + blockIdx.x) * 8 + (i)]
+    if (p.dbg && tid == 0) CDBG(0, 6) = ns0;
+    for (int k = 0;; ++k) {
+        uint32_t *rd = buf(k % 3);
+        uint32_t *wr = buf((k + 1) % 3);
+        if (p.dbg && tid == 0 && k < 16) CDBG(k, 0) = globaltimer();
+        if (k > 0)   // wr held v_{k-2}: bring it up to v_k (remote ORs may already arrive)
+            for (int32_t w = tid; w < nw; w += blockDim.x) {
+                const uint32_t x = rd[w] & ~wr[w];
+                if (x) atomicOr(wr + w, x);
+            }
+        if (tid == 0) s_qn = 0;
+        __syncthreads();
+        if (p.dbg && tid == 0 && k < 16) CDBG(k, 1) = globaltimer();
+        // LEAD pass over this CTA's quads of the flat planes: a row whose lead atom is in v_k
+        // and whose head is not is queued (one reservation per warp and quad step); the
+        // queue is verified after the stream with every thread.  A full queue verifies the
+        // row at once.  (warp-uniform trip count: the loop body has warp collectives)
+        for (int32_t q0 = cr * (int32_t)blockDim.x + tid; q0 - lane < nq; q0 += step * U) {
+            int4 a[U], h[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int32_t q = q0 + u * step;
+                a[u] = q < nq ? lb[q] : make_int4(p.n_ext_atoms - 1, 0, 0, 0);
+                h[u] = q < nq ? hb[q] : make_int4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int32_t q = q0 + u * step;
+                const int32_t av[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, hv[4] = {h[u].x, h[u].y, h[u].z, h[u].w};
+                unsigned cand = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    cand |= (q < nq && sm_bit(rd, (uint32_t)av[e]) && !sm_bit(rd, (uint32_t)hv[e])) ? (1u << e) : 0u;
+                const unsigned any = __ballot_sync(0xFFFFFFFFu, cand != 0);
+                if (!any) continue;
+                const int c = __popc(cand);
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                int base = 0;
+                if (lane == 31) base = atomicAdd(&s_qn, incl);
+                base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - c;
+                for (unsigned f = cand; f; f &= f - 1, ++base) {
+                    const int32_t slot = q * 4 + __ffs(f) - 1;
+                    if (base < kClQueue) cl_q[base] = slot;
+                    else cl_verify(p, segs, colg, reinterpret_cast<const int32_t *>(hb), rd, wr, slot);
+                }
+            }
+        }
+        __syncthreads();
+        {
+            const int32_t nc = min(s_qn, kClQueue);
+            for (int32_t i = tid; i < nc; i += blockDim.x)
+                cl_verify(p, segs, colg, reinterpret_cast<const int32_t *>(hb), rd, wr, cl_q[i]);
+        }
+        if (p.dbg && k < 16 && lane == 0) atomicMax(&CDBG(k, 2), globaltimer());
+        if (S > 1) {   // this CTA's new bits into every other CTA's v_{k+1}
+            __syncthreads();
+            for (int32_t w = tid; w < nw; w += blockDim.x) {
+                const uint32_t d = wr[w] & ~rd[w];
+                if (d)
+                    for (int r = 1; r < S; ++r) {
+                        const int t = cr + r < S ? cr + r : cr + r - S;
+                        atomicOr(cluster.map_shared_rank(wr, t) + w, d);
+                    }
+            }
+        }
+        cluster.sync();
+        if (p.dbg && tid == 0 && k < 16) CDBG(k, 3) = globaltimer();
+        // the new atoms of pass k: counted by every CTA over all words (the same complete
+        // v_{k+1} everywhere), stages written by each word's owner
+        int32_t nn = 0;
+        for (int32_t w = tid; w < nw; w += blockDim.x) {
+            const uint32_t d = wr[w] & ~rd[w];
+            if (!d) continue;
+            nn += __popc(d & (w == (p.top >> 5) ? ~(1u << (p.top & 31)) : ~0u));
+            if (p.stage && (w % S) == cr)
+                for (uint32_t b = d; b;) {
+                    const int i = __ffs(b) - 1;
+                    b &= b - 1;
+                    const int64_t a = (int64_t)w * 32 + i;
+                    if (a < p.n_out) p.stage[a] = k + 1;
+                }
+        }
+        const int32_t sum = block_sum(nn);
+        if (p.dbg && tid == 0 && k < 16) CDBG(k, 5) = globaltimer();
+        if (lead && p.stats)
+            atomicAdd(p.stats + 0, (p.stage_planes ? 0ull : 8ull * (unsigned long long)p.n_slots) +
+                                       4ull * (unsigned long long)sum);
+        if (sum == 0 || k + 1 >= p.max_passes || k + 1 == p.user_cap) {
+            if (lead) {
+                *p.iters_out = k + 1;
+                if (sum != 0) atomicOr(p.status_out, k + 1 == p.user_cap ? kStCapped : kStGuard);
+                if (p.status_user) *p.status_user = atomicOr(p.status_out, 0);
+                if (p.stats) {
+                    if (p.stage_planes)   // (the planes were read once, into shared memory)
+                        atomicAdd(p.stats + 0, 8ull * (unsigned long long)p.n_slots +
+                                                   4ull * (unsigned long long)p.stream_entries);
+                    p.stats[1] = (unsigned long long)(k + 1);   // (every pass is a LEAD pass)
+                    p.stats[4] = (unsigned long long)(clock64() - clk0);
+                    p.stats[5] = globaltimer() - ns0;
+                }
+            }
+            // the model (v_{k+1}, in wr) over the original atoms, this CTA's words
+            for (int64_t i = cr * (int64_t)blockDim.x + tid; i < p.out_wn; i += (int64_t)S * blockDim.x) {
+                const int64_t w = p.out_w0 + i;
+                unsigned long long v = (unsigned long long)wr[2 * w] | ((unsigned long long)wr[2 * w + 1] << 32);
+                const int64_t lo = w * 64;
+                if (lo + 64 > p.n_out) v &= (1ull << (uint32_t)(p.n_out - lo)) - 1ull;
+                p.model_out[i] = v;
+            }
+            if (p.dbg && tid == 0) CDBG(1, 7) = globaltimer();
+            return;   // (no remote access follows the last cluster barrier)
+        }
+        total += sum;
+        if (lead && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = total;
+    }
+#undef CDBG
+}
+
+cudaError_t launch_lm_cluster(const LMParams &p, int cluster, size_t smem, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cluster);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, lm_cluster_kernel, p);
+}
+
+// The largest cluster (<= want) of lm_cluster_kernel that fits with `smem` bytes per CTA.
+int lm_cluster_max(int want, size_t smem) {
+    // (the attribute is the kernel's, shared by every loaded program: set the maximum)
+    if (cudaFuncSetAttribute((const void *)lm_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute((const void *)lm_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kMaxSmemBytes) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    for (int c = want; c >= 1; --c) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)c);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)c;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, (const void *)lm_cluster_kernel, &cfg) == cudaSuccess && n >= 1)
+            return c;
+        cudaGetLastError();
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------------------------------
 // stable models: bit-sliced guess matrix, 64 guesses per uint64 word
 // ------------------------------------------------------------------------------------
 
@@ -1843,16 +2142,31 @@ __device__ void st_check_phase(const STParams &p, int64_t gtid, int64_t gthreads
 __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int64_t i,
                                        const unsigned long long *rd, unsigned long long *wr,
                                        int k, int lane, int32_t *pc, int32_t base) {
+    // the head and the first kB body ids in one round trip, then the head row and those body
+    // rows in a second one (independent loads in flight), then the new bits of the guesses
+    // whose head is still false; positions past kB (long bodies) 4 at a time with the
+    // short-circuit
+    constexpr int kB = 6;
     const int32_t h = __ldg(p.head + sg.slot_off + i);
+    int32_t a0[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j)
+        a0[j] = j < sg.L ? __ldg(p.col + sg.col_off + (int64_t)j * sg.count_pad + i) : -1;
     bool changed = false;
     for (int32_t w = 2 * lane; w < p.Wp; w += 64) {
-        // start from the guesses whose head is still false: nothing to do for this word
-        // pair if there are none (most heads are true in every guess after a few passes),
-        // and the AND over the body stops as soon as no such guess survives
-        // (body rows 4 at a time: 4 independent id loads, then 4 independent row loads)
         const ulonglong2 hv = __ldcg(reinterpret_cast<const ulonglong2 *>(rd + (int64_t)h * p.Wp + w));
+        ulonglong2 r0[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j)
+            r0[j] = a0[j] >= 0 ? __ldcg(reinterpret_cast<const ulonglong2 *>(rd + (int64_t)a0[j] * p.Wp + w))
+                               : make_ulonglong2(~0ull, ~0ull);
         ulonglong2 acc = make_ulonglong2(~hv.x, ~hv.y);
-        for (int32_t j0 = 0; j0 < sg.L && (acc.x | acc.y); j0 += 4) {
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            acc.x &= r0[j].x;
+            acc.y &= r0[j].y;
+        }
+        for (int32_t j0 = kB; j0 < sg.L && (acc.x | acc.y); j0 += 4) {
             int32_t a[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -2271,6 +2585,50 @@ cudaError_t launch_st_column(const STParams &p, int32_t n, int64_t g, unsigned l
     if (nw == 0) return cudaSuccess;
     int b = (int)std::min<int64_t>((nw + 255) / 256, 4096);
     st_column_kernel<<<b, 256, 0, st>>>(p.T0, p.Wp, n, g, out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// multi-GPU least model: the exchange step of a head-range-sharded pass
+// ------------------------------------------------------------------------------------
+//
+// After every rank ran ONE θ-pass of its rules (heads in its 64-aligned atom range) from
+// the same v_k and the ranks' owned words were all-gathered: v_{k+1} = v_k with each
+// rank's owned words ORed in (the OR clause of T_P over rules split across GPUs), the
+// changed flag = some rank's pass derived an atom (its status word has LP_ST_CAPPED), and
+// optionally |v_{k+1}| added to *pops.  Block 0 writes the flag (a plain store: the host
+// may read it from mapped memory once the stream passed the kernel).
+__global__ void shard_combine_kernel(const __grid_constant__ ShardCombineParams q) {
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    int32_t pc = 0;
+    for (int64_t w = gtid; w < q.n_words; w += gthreads) {
+        int r = 0;
+        while (r + 1 < q.world && q.word_lo[r + 1] <= w) ++r;   // (ranges ascending, <= 64)
+        unsigned long long v = __ldg(q.v + w);
+        const int64_t i = w - q.word_lo[r];
+        if (i < q.word_cnt[r]) v |= __ldg(q.gathered + (int64_t)r * q.stride + i);
+        q.v_next[w] = v;
+        pc += __popcll(v);
+    }
+    if (q.pops) {
+        for (int o = 16; o; o >>= 1) pc += __shfl_xor_sync(0xFFFFFFFFu, pc, o);
+        if ((threadIdx.x & 31) == 0 && pc) atomicAdd(q.pops, pc);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        int32_t ch = 0;
+        for (int r = threadIdx.x; r < q.world; r += 32) {
+            const int32_t st = (int32_t)__ldg(q.gathered + (int64_t)r * q.stride + (q.stride - 1));
+            ch |= (st & kStCapped) ? 1 : 0;
+        }
+        ch = __any_sync(0xFFFFFFFFu, ch != 0) ? 1 : 0;
+        if (threadIdx.x == 0) *(volatile int32_t *)q.changed = ch;
+    }
+}
+
+cudaError_t launch_shard_combine(const ShardCombineParams &q, cudaStream_t st) {
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((q.n_words + 255) / 256, 4 * 148));
+    shard_combine_kernel<<<(unsigned)blocks, 256, 0, st>>>(q);
     return cudaGetLastError();
 }
 

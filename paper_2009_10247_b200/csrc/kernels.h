@@ -94,11 +94,13 @@ struct LMParams {
     int32_t pass_mode;         // 0 auto (LEAD until a pass queues > n_slots/dense_div
                                //   rows, STREAM from then on), 1 always LEAD, 2 always STREAM
     int32_t dense_div;
+    int32_t predict;           // auto schedule: estimate the first LEAD pass (LP_NO_PREDICT: off)
     int64_t n_slots;
     int32_t *cand;             // [3] rows queued per pass (slot k % 3)
     unsigned long long *vent;  // [3] body entries the verification loaded per pass (k % 3)
     long long stream_entries;  // body entries (incl. padding) one STREAM pass reads
     int32_t auto_stream_first; // auto schedule starts with STREAM passes (long bodies)
+    int32_t stage_planes;      // cluster kernel: lead / head / col planes copied to shared memory
     int32_t overlap;           // LEAD passes verify while they stream (warp-specialised)
     long long overlap_min_bytes;  // ... when the pass streams at least this many bytes
     // pipelined key-mode LEAD passes (lm_pipe): rows by lead atom, and the counter of the
@@ -197,11 +199,31 @@ struct STParams {
     int32_t *passes_sum_out;            // whole-matrix passes summed over the rounds
 };
 
+// Multi-GPU exchange step (lp_shard_combine).
+constexpr int kMaxRanks = 64;
+struct ShardCombineParams {
+    const unsigned long long *gathered;  // [world][stride]: owned words, status word last
+    int32_t world;
+    int64_t stride;
+    int64_t word_lo[kMaxRanks];
+    int64_t word_cnt[kMaxRanks];
+    const unsigned long long *v;         // [n_words] v_k
+    unsigned long long *v_next;          // [n_words] v_{k+1}
+    int64_t n_words;
+    int32_t *changed;                    // 1: some rank's pass derived an atom
+    int32_t *pops;                       // optional: += |v_{k+1}|
+};
+
 // ---- launchers (return cudaError_t of the launch) -----------------------------------
+cudaError_t launch_shard_combine(const ShardCombineParams &q, cudaStream_t st);
 // Each least-model call is ONE cooperative launch: v_0 prologue, the fixpoint loop and
 // the model extraction all run inside the persistent kernel.
 cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st);
 cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st);
+// Exact-mode programs small enough for one thread-block cluster (truth in shared memory,
+// DSMEM exchange, cluster barriers): the whole fixpoint in one cluster launch.
+cudaError_t launch_lm_cluster(const LMParams &p, int cluster, size_t smem, cudaStream_t st);
+int lm_cluster_max(int want, size_t smem);
 
 // One cooperative launch per stable call: clear the previous call's rows, build T_0, the
 // fixpoint loop, the stability check.

@@ -65,12 +65,12 @@ class lp_info_t(ctypes.Structure):
                 ("summary_shift", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
                 ("block_threads", ctypes.c_int32), ("lead_pass_bytes", ctypes.c_int64),
                 ("stream_pass_bytes", ctypes.c_int64), ("key_shift", ctypes.c_int32),
-                ("n_aux", ctypes.c_int32)]
+                ("n_aux", ctypes.c_int32), ("cluster_ctas", ctypes.c_int32)]
 
 
 SYMBOLS = ("lp_load", "lp_info", "lp_negated_atoms", "lp_least_model", "lp_stable_models",
-           "lp_stable_search", "lp_stable_matrix", "lp_guess_model", "lp_free", "lp_status_str",
-           "lp_last_error")
+           "lp_stable_search", "lp_stable_matrix", "lp_guess_model", "lp_shard_combine", "lp_free",
+           "lp_status_str", "lp_last_error")
 
 _lib = None
 
@@ -97,6 +97,9 @@ def library():
         lib.lp_stable_search.argtypes = [_P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, _P, _P,
                                          _P, _P, _P, ctypes.POINTER(lp_run)]
         lib.lp_stable_search.restype = st
+        lib.lp_shard_combine.argtypes = [_P, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P, ctypes.c_int64,
+                                         _P, _P, _P]
+        lib.lp_shard_combine.restype = st
         lib.lp_stable_matrix.argtypes = [_P, _P, ctypes.POINTER(lp_run)]
         lib.lp_stable_matrix.restype = st
         lib.lp_guess_model.argtypes = [_P, ctypes.c_int64, _P, ctypes.POINTER(lp_run)]
@@ -461,6 +464,18 @@ def lp_stable_search(p: Program, h, seed, max_rounds, guesses_out, accepted_out,
                                        ctypes.addressof(rd), ctypes.addressof(ps), ctypes.byref(run)),
            "lp_stable_search")
     return na.value, rd.value, ps.value
+
+
+def lp_shard_combine(gathered, world, stride, word_lo, word_cnt, v, v_next, changed_out,
+                     popcount_inout=None, stream=None):
+    """Marshals lp_shard_combine: torch CUDA tensors (gathered int64 [world*stride], v and
+    v_next int64 [n_words], changed_out int32[1], optional popcount_inout int32[1]) and
+    host int64 arrays word_lo / word_cnt; asynchronous on ``stream``."""
+    lo = np.ascontiguousarray(word_lo, dtype=np.int64)
+    cnt = np.ascontiguousarray(word_cnt, dtype=np.int64)
+    _check(library().lp_shard_combine(_ptr(gathered), int(world), int(stride), _ptr(lo), _ptr(cnt), _ptr(v),
+                                       _ptr(v_next), int(v.numel()), _ptr(changed_out), _ptr(popcount_inout),
+                                       _stream_ptr(stream)), "lp_shard_combine")
 
 
 def lp_stable_matrix(p: Program, out, stream=None, device_ptrs=False):

@@ -10,17 +10,20 @@ maximum over columns).  NCCL on GPUs, gloo in the CPU tests.
 
 The least model of ONE program partitions by head ranges with one exchange per pass
 (SURVEY.md §8(e)): rank r owns the atoms [lo_r, hi_r) (64-aligned, balanced by the body
-entries of the rules whose head they are) and loads only those rules.  Pass k: every rank
-evaluates T over its rules from the same v_k (one θ-pass, lp_run.max_passes = 1), the
-full-length results are all-gathered and OR-ed into v_{k+1}; the loop stops after the first
-pass that changed nothing anywhere.  The union of the ranks' passes is one T_P evaluation
-over all of P, so model, pass count and popcount trace equal the single-GPU ones.
-bench.py's main line runs independent replicas (weak scaling); this path is its strong-
-scaling extra.
+entries of the rules whose head they are) and loads only those rules (with the whole
+program's D2 as layout hint).  Pass k: every rank runs ONE θ-pass of its rules from the
+same v_k (lp_run.max_passes = 1) writing only its owned words and its status word into a
+payload; the payloads are all-gathered (NCCL, ~W/N words per rank); lp_shard_combine
+(a CUDA kernel) ORs them into v_{k+1}, sets the changed flag and counts |v_{k+1}|.  The
+host reads pass k's flag after it queued pass k+1 (one extra, idempotent pass at the
+end; no host sync per pass).  The union of the ranks' passes is one T_P evaluation over
+all of P, so model, pass count and popcount trace equal the single-GPU ones.  Under
+torchrun (N > 1) this is bench.py's main line (strong scaling: one C4 for all ranks).
 
 This module only moves buffers between ranks; every step of the path runs in the CUDA
-kernels behind lp.Program (the `solve` hook exists so the CPU tests can drive the same
-host logic with a stand-in solver -- the product never passes one).
+kernels behind lp.Program and lp_shard_combine (the `solve` / `backend` hooks exist so
+the CPU tests can drive the same host logic with a stand-in -- the product never passes
+one).
 """
 from __future__ import annotations
 
@@ -104,6 +107,18 @@ def head_ranges(rules, world: int) -> List[Tuple[int, int]]:
     return [(bounds[r], bounds[r + 1]) for r in range(world)]
 
 
+def owned_words(rules, world: int) -> List[Tuple[int, int]]:
+    """(first word, word count) of each rank's atom range: the model words only its rules
+    can set.  The ranges tile [0, ceil(n/64)) in rank order."""
+    W = (int(rules.n_atoms) + 63) // 64
+    out = []
+    for lo, hi in head_ranges(rules, world):
+        w0 = -(-lo // 64)                      # (lo is 64-aligned, or n for an empty tail)
+        w1 = W if hi >= int(rules.n_atoms) else hi // 64
+        out.append((w0, max(0, w1 - w0)))
+    return out
+
+
 def sub_program(rules, lo: int, hi: int):
     """The rules whose head is in [lo, hi), over the same atoms (lpgen.Rules)."""
     import lpgen
@@ -119,32 +134,131 @@ def sub_program(rules, lo: int, hi: int):
                        body_atom=atoms, body_neg=None, meta={"shard": (lo, hi)})
 
 
-def _gpu_one_pass(prog):
-    import torch
+def derivable_mask(rules) -> np.ndarray:
+    """The whole program's D2 (facts ∪ heads of rules whose body lies in heads ∪ facts):
+    the layout hint (lp_options.derivable) every shard loads with, so atoms derived on
+    another GPU keep fine key groups.  A layout heuristic only: never a result."""
+    n = int(rules.n_atoms)
+    head = np.asarray(rules.head, dtype=np.int64)
+    ptr = np.asarray(rules.body_ptr, dtype=np.int64)
+    atom = np.asarray(rules.body_atom, dtype=np.int64)
+    lens = np.diff(ptr)
+    d1 = np.zeros(n, dtype=bool)
+    d1[head] = True
+    ok = np.ones(head.size, dtype=bool)
+    nz = lens > 0
+    if atom.size:
+        ok[nz] = np.logical_and.reduceat(d1[atom], ptr[:-1][nz])
+    d2 = np.zeros(n, dtype=np.uint8)
+    d2[head[ok]] = 1
+    return d2
 
-    from . import lp
-    it = None
 
-    def one_pass(v):
-        nonlocal it
-        if it is None:
-            it = torch.zeros(1, dtype=torch.int32, device=v.device)
-        out = torch.empty_like(v)
-        lp.lp_least_model(prog, v, out, device_ptrs=True, iters_out=it, max_passes=1,
-                          stream=torch.cuda.current_stream(v.device))
-        return out
-    return one_pass
+def _mapped_device_ptr(host_ptr: int) -> int:
+    """Device address of page-locked host memory (the same address under unified
+    addressing; cudaPointerGetAttributes says so)."""
+    try:
+        from cuda.bindings import runtime as rt
+        err, at = rt.cudaPointerGetAttributes(host_ptr)
+        if int(err) == 0 and int(at.devicePointer):
+            return int(at.devicePointer)
+    except Exception:  # noqa: BLE001 -- no cuda-python: unified addressing's identity
+        pass
+    return host_ptr
+
+
+class _GpuShard:
+    """This rank's side of the device exchange: ONE θ-pass of its rules (CUDA kernels
+    behind lp_least_model, max_passes = 1) writing its owned words and its status word into
+    the payload, and the combine step (lp_shard_combine) computing v_{k+1}, the changed
+    flag and |v_{k+1}| on the device.  The combine kernel writes pass k's flag straight into
+    page-locked host memory (mapped: the device pointer is the host pointer under unified
+    addressing); the host reads it behind an event one pass later.  Every ctypes argument
+    is prepared once, so a pass costs two library calls, the all-gather and an event."""
+
+    def __init__(self, rules, lo, hi, word_lo, word_cnt, stride, world, device, program=None,
+                 cap=None):
+        import ctypes
+
+        import torch
+
+        from . import lp
+        self.lp = lp
+        self.torch = torch
+        self.device = device
+        self.prog = program or lp.Program(sub_program(rules, lo, hi), device=device.index or 0,
+                                          derivable=derivable_mask(rules))
+        self.word_lo = np.ascontiguousarray(word_lo, dtype=np.int64)
+        self.word_cnt = np.ascontiguousarray(word_cnt, dtype=np.int64)
+        self.stride, self.world = stride, world
+        cap = cap or (int(rules.n_atoms) + 3)
+        self.it = torch.zeros(1, dtype=torch.int32, device=device)
+        self.flags_host = torch.zeros(cap, dtype=torch.int32).pin_memory()   # written by the kernel
+        self.flags_dev = _mapped_device_ptr(self.flags_host.data_ptr())
+        self.pops = torch.zeros(cap, dtype=torch.int32, device=device)
+        self.events = [torch.cuda.Event() for _ in range(cap)]
+        self.stream = torch.cuda.current_stream(device)
+        self.lib = lp.library()
+        self.run = None      # lp_run of this rank's pass (set on the first pass: needs the payload)
+        self.c_int = ctypes
+
+    def reset(self):
+        self.pops.zero_()
+
+    def _prepare(self, rank, payload):
+        lp = self.lp
+        r = lp.lp_run()
+        r.stream = int(self.stream.cuda_stream)
+        r.flags = lp.LP_PTR_DEVICE
+        r.max_passes = 1
+        r.status_out = payload.data_ptr() + 8 * (self.stride - 1)   # low half of the last word
+        r.out_word_lo = int(self.word_lo[rank])
+        r.out_word_count = int(self.word_cnt[rank])
+        self.run = r
+        self.payload_ptr = payload.data_ptr()
+
+    def one_pass(self, rank, v, payload):
+        """payload[:cnt] = this rank's owned words of v ∪ T_{P_r}(v); the low half of
+        payload[stride - 1] = its status word (LP_ST_CAPPED: the pass derived an atom)."""
+        if int(self.word_cnt[rank]) == 0:   # (an empty trailing range: nothing to derive)
+            payload.zero_()
+            return
+        if self.run is None or self.payload_ptr != payload.data_ptr():
+            self._prepare(rank, payload)
+        st = self.lib.lp_least_model(self.prog.handle, v.data_ptr(), self.payload_ptr, self.it.data_ptr(),
+                                     self.c_int.byref(self.run))
+        if st != self.lp.LP_OK:
+            raise self.lp.LPError(st, "lp_least_model (shard pass)")
+
+    def combine(self, k, gathered, v, v_next):
+        st = self.lib.lp_shard_combine(gathered.data_ptr(), self.world, self.stride, self.word_lo.ctypes.data,
+                                       self.word_cnt.ctypes.data, v.data_ptr(), v_next.data_ptr(),
+                                       v.numel(), self.flags_dev + 4 * k,
+                                       self.pops.data_ptr() + 4 * (k + 1), int(self.stream.cuda_stream))
+        if st != self.lp.LP_OK:
+            raise self.lp.LPError(st, "lp_shard_combine")
+        self.events[k].record(self.stream)
+
+    def changed(self, k) -> bool:
+        self.events[k].synchronize()
+        return bool(int(self.flags_host[k]))
+
+    def popcounts(self, iters):
+        return self.pops[1:iters].cpu().tolist()
 
 
 class ShardedLeastModel:
     """Head-range-sharded least model of a definite program (module docstring).
 
-    Setup (once per program, host side): this rank's head range, its sub-program on the
-    GPU and the initial words I_0 = facts(P).  ``run`` is the per-call device loop.
-    ``one_pass(v: int64 tensor of model words) -> int64 tensor`` defaults to one θ-pass
-    of the CUDA kernels over this rank's rules (the CPU tests pass a stand-in)."""
+    Setup (once per program, host side): this rank's head range and owned words, its
+    sub-program on the GPU (loaded with the whole program's D2), the initial words
+    I_0 = facts(P) and the payload / gather buffers.  ``run`` is the per-call loop: per pass
+    one θ-pass on every rank, one all-gather of the owned words + status word (NCCL), one
+    combine kernel; the host checks pass k's changed flag after enqueuing pass k+1.
+    ``backend`` defaults to the CUDA path (_GpuShard); the CPU tests pass a stand-in with
+    the same methods (one_pass, combine, changed, popcounts, reset)."""
 
-    def __init__(self, rules, group=None, one_pass=None, device=None, program=None):
+    def __init__(self, rules, group=None, backend=None, device=None, program=None):
         import torch
         import torch.distributed as dist
 
@@ -153,22 +267,25 @@ class ShardedLeastModel:
         self.n = int(rules.n_atoms)
         self.W = max((self.n + 63) // 64, 1)
         self.lo, self.hi = head_ranges(rules, self.world)[self.rank]
+        ow = owned_words(rules, self.world)
+        self.word_lo = [w for w, _ in ow]
+        self.word_cnt = [c for _, c in ow]
+        self.stride = max(self.word_cnt) + 1       # owned words + the status word
         if device is None:
             device = (torch.device("cuda", torch.cuda.current_device())
-                      if dist.get_backend(group) == "nccl" else "cpu")
+                      if dist.get_backend(group) == "nccl" else torch.device("cpu"))
         self.device = device
-        if one_pass is None:
-            from . import lp
-            prog = program or lp.Program(sub_program(rules, self.lo, self.hi),
-                                         device=torch.cuda.current_device())
-            one_pass = _gpu_one_pass(prog)
-        self.one_pass = one_pass
+        self.backend = backend or _GpuShard(rules, self.lo, self.hi, self.word_lo, self.word_cnt,
+                                            self.stride, self.world, device, program)
         ptr = np.asarray(rules.body_ptr)
         start = np.zeros(self.W * 64, dtype=np.uint8)        # I_0 = facts of every rank's rules
         start[np.asarray(rules.head)[ptr[1:] == ptr[:-1]]] = 1
         self.start = start
         self.facts_words = torch.from_numpy(np.packbits(start, bitorder="little").view(np.int64).copy()).to(device)
-        self.buf = torch.empty(self.world * self.W, dtype=torch.int64, device=device)
+        self.v = [torch.zeros(self.W, dtype=torch.int64, device=device) for _ in range(2)]
+        self.payload = torch.zeros(self.stride, dtype=torch.int64, device=device)
+        self.gathered = torch.zeros(self.world * self.stride, dtype=torch.int64, device=device)
+        self.max_passes = self.n + 3
 
     def run(self, v0=None, popcounts: bool = True):
         """Returns (model words uint64[ceil(n/64)], iters, popcount trace or [])."""
@@ -176,31 +293,36 @@ class ShardedLeastModel:
         import torch.distributed as dist
 
         if v0 is None:
-            v = self.facts_words.clone()
-            pops = [int(self.start.sum())] if popcounts else []
+            self.v[0].copy_(self.facts_words)
+            pop0 = int(self.start.sum())
         else:
             st = self.start.copy()
             st[:self.n] |= np.asarray(v0, dtype=bool).astype(np.uint8)
-            v = torch.from_numpy(np.packbits(st, bitorder="little").view(np.int64).copy()).to(self.device)
-            pops = [int(st.sum())] if popcounts else []
-        W, world = self.W, self.world
-        iters = 0
+            self.v[0].copy_(torch.from_numpy(np.packbits(st, bitorder="little").view(np.int64).copy()))
+            pop0 = int(st.sum())
+        b = self.backend
+        b.reset()
+        k = 0
         while True:
-            mine = self.one_pass(v)
-            dist.all_gather_into_tensor(self.buf, mine, group=self.group)
-            nxt = self.buf.view(world, W)[0].clone()
-            for r in range(1, world):
-                nxt.bitwise_or_(self.buf.view(world, W)[r])
-            iters += 1
-            if torch.equal(nxt, v):
+            if k >= self.max_passes:
+                raise RuntimeError("sharded least model: pass guard exceeded")
+            v, v_next = self.v[k & 1], self.v[(k + 1) & 1]
+            b.one_pass(self.rank, v, self.payload)
+            dist.all_gather_into_tensor(self.gathered, self.payload, group=self.group)
+            b.combine(k, self.gathered, v, v_next)
+            # pass k-1's flag (pass k is already queued behind it): u = v -> fixpoint
+            if k >= 1 and not b.changed(k - 1):
+                iters = k
                 break
-            v = nxt
-            if popcounts:
-                pops.append(int(np.unpackbits(v.cpu().numpy().view(np.uint8)).sum()))
-        return v.cpu().numpy().view(np.uint64)[: (self.n + 63) // 64].copy(), iters, pops
+            k += 1
+        if self.device.type == "cuda":
+            torch.cuda.current_stream(self.device).synchronize()
+        model = self.v[iters & 1].cpu().numpy().view(np.uint64)[: (self.n + 63) // 64].copy()
+        pops = ([pop0] + b.popcounts(iters)) if popcounts else []
+        return model, iters, pops
 
 
-def least_model_sharded(rules, group=None, v0=None, one_pass=None, device=None, program=None,
+def least_model_sharded(rules, group=None, v0=None, backend=None, device=None, program=None,
                         popcounts: bool = True):
     """One-shot ShardedLeastModel(...).run(v0): (model words, iters, popcount trace)."""
-    return ShardedLeastModel(rules, group, one_pass, device, program).run(v0, popcounts)
+    return ShardedLeastModel(rules, group, backend, device, program).run(v0, popcounts)

@@ -158,6 +158,8 @@ def test_auto_schedule_switches_mid_fixpoint(seed, cfg, monkeypatch):
     than n_slots / LP_DENSE_DIV rows; with a huge divisor the switch happens right after
     the first pass that queues anything, so the fixpoint mixes both pass kinds."""
     monkeypatch.setenv("LP_DENSE_DIV", str(10 ** 9))
+    monkeypatch.setenv("LP_NO_PREDICT", "1")   # (no predicted STREAM start: switch mid-way)
+    monkeypatch.setenv("LP_NO_CLUSTER", "1")   # (the persistent grid kernel's auto schedule)
     rng = np.random.default_rng([seed, 4242])
     n = int(rng.integers(2000, 5000))
     P = lpgen.random_program(rng, n, 5 * n, max_len=5, n_facts=n // 10)
@@ -166,6 +168,35 @@ def test_auto_schedule_switches_mid_fixpoint(seed, cfg, monkeypatch):
         _, iters, ex = prog.least_model(schedule="auto", stats=True, pipeline=pipeline)
         assert 1 <= ex["stats"]["lead_passes"] < iters
     check_lm(P, prog=prog, schedules=("auto",))
+    # the predicted start: a start set lighting most key buckets begins with STREAM passes
+    monkeypatch.delenv("LP_NO_PREDICT")
+    monkeypatch.delenv("LP_NO_CLUSTER")
+    monkeypatch.delenv("LP_DENSE_DIV")
+    q = lp.Program(P, **cfg)
+    v0 = rng.choice(n, size=n // 3, replace=False).tolist()
+    check_lm(P, v0=v0, prog=q, schedules=("auto",))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_cluster_kernel(seed, monkeypatch):
+    """Exact-mode programs on ONE thread-block cluster (lm_cluster_kernel): one or two CTAs,
+    the planes staged in shared memory or read from L2, random start sets; and the same
+    program forced onto the persistent grid (LP_NO_CLUSTER) for comparison."""
+    rng = np.random.default_rng([seed, 777])
+    n = int(rng.integers(50, 8000))
+    R = int(rng.integers(n, 8 * n))
+    P = lpgen.random_program(rng, n, R, max_len=int(rng.integers(1, 9)), n_facts=max(1, n // 40))
+    prog = lp.Program(P)
+    assert prog.info["cluster_ctas"] >= 1, prog.info
+    check_lm(P, prog=prog, schedules=("auto",), variants=(False,))
+    v0 = rng.choice(n, size=max(1, n // 20), replace=False).tolist()
+    check_lm(P, v0=v0, prog=prog, schedules=("auto",), variants=(False,))
+    model, iters, ex = prog.least_model(max_passes=2, stats=True)
+    assert iters == min(2, _oracle_lm(P)[2])
+    monkeypatch.setenv("LP_NO_CLUSTER", "1")
+    q = lp.Program(P, frontier=False)
+    assert q.info["cluster_ctas"] == 0
+    check_lm(P, prog=q, schedules=("auto",), variants=(False,))
 
 
 def test_long_bodies_generic_path_and_u32_counters():
@@ -532,43 +563,62 @@ def test_pipelined_lead_passes_hub_leads(seed):
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 5])
-@pytest.mark.parametrize("cfg", ["rand", "C2"])
-def test_head_range_shards_one_pass_each(world, cfg):
-    """The head-range-sharded least model, its ranks run one after another on this GPU
-    (each pass: every rank's one-θ-pass call from the same v_k, then the OR of the
-    results -- shard.least_model_sharded without the all-gather): same model, pass
-    count and popcounts as the oracle."""
+@pytest.mark.parametrize("cfg", ["rand", "C2", "tiny"])
+def test_head_range_shards_device_exchange(world, cfg):
+    """The head-range-sharded least model's device path (shard.py / lp_shard_combine), its
+    ranks run one after another on this GPU with their payloads written straight into the
+    rows of the gathered buffer (the all-gather's result): per pass every rank's one-θ-pass
+    call (owned words + status word only, shards loaded with the whole program's D2), then
+    the combine kernel (OR, changed flag, popcount).  Same model, pass count and popcounts
+    as the oracle."""
     import torch
-    from paper_2009_10247_b200.shard import head_ranges, sub_program
+    from paper_2009_10247_b200.shard import derivable_mask, head_ranges, owned_words, sub_program
     if cfg == "rand":
         rng = np.random.default_rng(world)
         P = lpgen.random_program(rng, 3000, 12000, max_len=5, n_facts=100)
+    elif cfg == "tiny":     # fewer words than ranks: empty trailing ranges
+        rng = np.random.default_rng(world + 10)
+        P = lpgen.random_program(rng, 70, 300, max_len=3, n_facts=7)
     else:
         P = lpgen.config("C2")
     om, stage, oit = oracle.lm_stage(P)
     n = P.n_atoms
     W = (n + 63) // 64
-    progs = [lp.Program(sub_program(P, lo, hi)) for lo, hi in head_ranges(P, world)]
+    der = derivable_mask(P)
+    ranges = head_ranges(P, world)
+    ow = owned_words(P, world)
+    progs = [lp.Program(sub_program(P, lo, hi), derivable=der) for lo, hi in ranges]
+    stride = max(c for _, c in ow) + 1
+    gathered = torch.zeros(world * stride, dtype=torch.int64, device="cuda")
     ptr = np.asarray(P.body_ptr)
     start = np.zeros(W * 64, dtype=np.uint8)
     start[np.asarray(P.head)[ptr[1:] == ptr[:-1]]] = 1
-    v = torch.from_numpy(np.packbits(start, bitorder="little").view(np.int64).copy()).cuda()
+    v = [torch.from_numpy(np.packbits(start, bitorder="little").view(np.int64).copy()).cuda(),
+         torch.zeros(W, dtype=torch.int64, device="cuda")]
     it_d = torch.zeros(1, dtype=torch.int32, device="cuda")
-    iters, pops = 0, [int(start.sum())]
+    changed = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pops_d = torch.zeros(n + 3, dtype=torch.int32, device="cuda")
+    k = 0
     while True:
-        nxt = torch.zeros_like(v)
-        for prog in progs:
-            out = torch.empty_like(v)
-            lp.lp_least_model(prog, v, out, device_ptrs=True, iters_out=it_d, max_passes=1)
-            nxt |= out
-        iters += 1
-        if torch.equal(nxt, v):
+        cur, nxt = v[k & 1], v[(k + 1) & 1]
+        for r, prog in enumerate(progs):
+            row = gathered[r * stride:(r + 1) * stride]
+            status = row.view(torch.int32)[2 * (stride - 1):2 * (stride - 1) + 1]
+            w0, cnt = ow[r]
+            if cnt == 0:
+                status.zero_()
+                continue
+            lp.lp_least_model(prog, cur, row, device_ptrs=True, iters_out=it_d, max_passes=1,
+                              status_out=status, out_words=(w0, cnt))
+        lp.lp_shard_combine(gathered, world, stride, [w for w, _ in ow], [c for _, c in ow], cur, nxt,
+                            changed, pops_d[k + 1:k + 2])
+        k += 1
+        if int(changed.item()) == 0:
             break
-        v = nxt
-        pops.append(int(np.unpackbits(v.cpu().numpy().view(np.uint8)).sum()))
-    assert iters == oit
-    assert (v.cpu().numpy().view(np.uint64)[:W] == oracle.pack_bits(om)).all()
-    assert pops == oracle.popcounts_from_stage(stage, oit)
+        assert k <= n + 2
+    assert k == oit
+    assert (v[k & 1].cpu().numpy().view(np.uint64)[:W] == oracle.pack_bits(om)).all()
+    assert [int(start.sum())] + pops_d[1:k].cpu().tolist() == oracle.popcounts_from_stage(stage, oit)
 
 
 def test_edge_cases_new_controls():

@@ -13,7 +13,8 @@ import torch.multiprocessing as mp
 
 import lpgen
 import oracle
-from paper_2009_10247_b200.shard import guess_slices, head_ranges, sub_program
+from paper_2009_10247_b200.shard import (derivable_mask, guess_slices, head_ranges, owned_words,
+                                          sub_program)
 
 
 def test_guess_slices_cover_exactly_once():
@@ -100,22 +101,71 @@ def test_head_ranges_partition_the_rules():
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             assert all(lo % 64 == 0 or lo == n for lo, _ in rs)
+            ow = owned_words(P, world)
+            W = (n + 63) // 64
+            assert ow[0][0] == 0 and sum(c for _, c in ow) == W
+            assert all(a[0] + a[1] == b[0] for a, b in zip(ow, ow[1:]))
+            for (lo, hi), (w0, c) in zip(rs, ow):    # a rank's heads lie in its owned words
+                assert c == 0 or (lo // 64 == w0 and (hi + 63) // 64 == w0 + c)
             subs = [sub_program(P, lo, hi) for lo, hi in rs]
             assert sum(s.n_rules for s in subs) == P.n_rules
             for (lo, hi), s in zip(rs, subs):
                 assert ((s.head >= lo) & (s.head < hi)).all()
 
 
-def _oracle_one_pass(sub):
-    """One T_P evaluation of `sub` from the given words (stand-in for the GPU pass)."""
-    import torch
+class _OracleShard:
+    """CPU stand-in for the CUDA side of one rank (test infrastructure): ONE T_P
+    evaluation of the rank's sub-program by the oracle writes the owned words and the
+    status word into the payload; the combine step in numpy.  The host loop, the payload
+    layout and the all-gather (gloo) are the product's (shard.ShardedLeastModel)."""
 
-    def one_pass(v):
-        n = sub.n_atoms
-        bits = np.unpackbits(v.numpy().view(np.uint8), bitorder="little")[:n].astype(bool)
-        m, it, _, _ = oracle.lm_jacobi(sub, v0=bits, max_iters=1)
-        return torch.from_numpy(oracle.pack_bits(m).view(np.int64).copy())
-    return one_pass
+    def __init__(self, P, rank, world):
+        lo, hi = head_ranges(P, world)[rank]
+        self.sub = sub_program(P, lo, hi)
+        ow = owned_words(P, world)
+        self.word_lo = [w for w, _ in ow]
+        self.word_cnt = [c for _, c in ow]
+        self.stride = max(self.word_cnt) + 1
+        self.world = world
+        self.n = P.n_atoms
+        self.flags, self.pops = {}, {}
+
+    def reset(self):
+        self.flags, self.pops = {}, {}
+
+    def one_pass(self, rank, v, payload):
+        import torch
+        bits = np.unpackbits(v.numpy().view(np.uint8), bitorder="little")[:self.n].astype(bool)
+        m, _, _, conv = oracle.lm_jacobi(self.sub, v0=bits, max_iters=1)
+        words = oracle.pack_bits(m).view(np.int64)
+        w0, cnt = self.word_lo[rank], self.word_cnt[rank]
+        out = np.zeros(self.stride, dtype=np.int64)
+        out[:cnt] = words[w0:w0 + cnt]
+        out[self.stride - 1] = 0 if conv else 4          # LP_ST_CAPPED: derived an atom
+        payload.copy_(torch.from_numpy(out))
+
+    def combine(self, k, gathered, v, v_next):
+        import torch
+        g = gathered.numpy().reshape(self.world, self.stride)
+        nv = v.numpy().copy()
+        for r in range(self.world):
+            w0, cnt = self.word_lo[r], self.word_cnt[r]
+            nv[w0:w0 + cnt] |= g[r, :cnt]
+        v_next.copy_(torch.from_numpy(nv))
+        self.flags[k] = bool((g[:, self.stride - 1] & 4).any())
+        self.pops[k + 1] = int(np.unpackbits(nv.view(np.uint8)).sum())
+
+    def changed(self, k):
+        return self.flags[k]
+
+    def popcounts(self, iters):
+        return [self.pops[j] for j in range(1, iters)]
+
+
+def _lm_program(seed):
+    rng = np.random.default_rng([seed, 91])
+    n = int(rng.integers(50, 400)) if seed != 4 else 70     # (seed 4: empty trailing ranges)
+    return lpgen.random_program(rng, n, 4 * n, max_len=4, n_facts=n // 10)
 
 
 def _lm_worker(rank, world, port, seed, q):
@@ -124,17 +174,14 @@ def _lm_worker(rank, world, port, seed, q):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
-        rng = np.random.default_rng([seed, 91])
-        n = int(rng.integers(50, 400))
-        P = lpgen.random_program(rng, n, 4 * n, max_len=4, n_facts=n // 10)
-        lo, hi = head_ranges(P, world)[rank]
-        model, iters, pops = least_model_sharded(P, one_pass=_oracle_one_pass(sub_program(P, lo, hi)))
+        P = _lm_program(seed)
+        model, iters, pops = least_model_sharded(P, backend=_OracleShard(P, rank, world))
         q.put((rank, model.tolist(), iters, pops))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,seed", [(2, 1), (3, 2), (2, 3)])
+@pytest.mark.parametrize("world,seed", [(2, 1), (3, 2), (2, 3), (3, 4)])
 def test_sharded_least_model_gloo(world, seed):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -146,11 +193,25 @@ def test_sharded_least_model_gloo(world, seed):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    rng = np.random.default_rng([seed, 91])
-    n = int(rng.integers(50, 400))
-    P = lpgen.random_program(rng, n, 4 * n, max_len=4, n_facts=n // 10)
+    P = _lm_program(seed)
     om, stage, oit = oracle.lm_stage(P)
     for _, model, iters, pops in res:
         assert np.array_equal(np.asarray(model, dtype=np.uint64), oracle.pack_bits(om))
         assert iters == oit
         assert pops == oracle.popcounts_from_stage(stage, oit)
+
+
+def test_derivable_mask_is_d2():
+    """D2 = facts ∪ {head(r) : body(r) ⊆ heads ∪ facts}, checked rule by rule."""
+    rng = np.random.default_rng(8)
+    for _ in range(30):
+        n = int(rng.integers(1, 200))
+        P = lpgen.random_program(rng, n, int(rng.integers(0, 3 * n)), max_len=4)
+        d1 = set(P.head.tolist())
+        want = set()
+        for r in range(P.n_rules):
+            body = P.body_atom[P.body_ptr[r]:P.body_ptr[r + 1]].tolist()
+            if all(b in d1 for b in body):
+                want.add(int(P.head[r]))
+        got = set(np.nonzero(derivable_mask(P))[0].tolist())
+        assert got == want
