@@ -158,6 +158,19 @@ def run_reference(args):
     return 0
 
 
+def _ncu_traffic(key, iters):
+    """dram read+write bytes of one launch from a committed ncu capture
+    (profiles/ncu_traffic.json), when its pass count and kernel revision match."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(key)
+        if tr and tr["passes_per_launch"] == iters and tr.get("kernel_rev") == KERNEL_REV:
+            return tr["dram_bytes_per_launch"]
+    except Exception:  # noqa: BLE001
+        pass
+    return None
+
+
 def _model_bytes_per_pass(info, n):
     """SURVEY.md §8(d)'s algorithmic bytes of one T_P pass over a CSR program:
     B_pass = 4·nnz + 4·(R+1) + 4·(H+1) + 2·ceil((n+1)/8) (column ids, rule delimiters,
@@ -297,14 +310,7 @@ def main():
     model_bytes = b_pass * iters
     achieved = model_bytes / (kms_max / 1e3) / 1e9
     kern_bytes = allmax(kern_bytes)
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(args.workload)
-        if tr and tr["passes_per_launch"] == iters and tr.get("kernel_rev") == KERNEL_REV:
-            traffic = tr["dram_bytes_per_launch"]
-    except Exception:  # noqa: BLE001
-        traffic = None
+    traffic = _ncu_traffic(args.workload, iters)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic,
                 "binding": "latency: grid barriers and dependent L2 round trips per pass (the "
@@ -424,6 +430,7 @@ def main():
                          "kernel_bytes_per_launch": sbytes,
                          "achieved": sbytes / (allmax(skms) / 1e3) / 1e9,
                          "frac": sbytes / (allmax(skms) / 1e3) / 1e9 / hbm_peak,
+                         "traffic": _ncu_traffic(args.workload + "_stream", iters),
                          "model_achieved": model_bytes / (allmax(skms) / 1e3) / 1e9,
                          "model_frac": model_bytes / (allmax(skms) / 1e3) / 1e9 / hbm_peak,
                          "note": "kernel bytes = every body plane streamed each pass (int32 ids, "

@@ -202,6 +202,9 @@ typedef struct {
     int32_t cluster_ctas;     /* > 0: the full θ-pass (auto schedule) runs in ONE thread-
                                  block cluster of this many CTAs (truth in shared memory,
                                  DSMEM exchange); 0: the persistent grid kernel         */
+    int32_t frontier_cluster_ctas; /* > 0: the frontier variant runs as ONE cluster of
+                                 this many CTAs (cluster barriers); 0: the grid         */
+    int32_t stable_cluster_ctas;   /* the same for lp_stable_models / lp_stable_search */
 } lp_info_t;
 
 /* Validate, standardize and encode a program, upload it (PAPER.md:62, 82-95,

@@ -67,6 +67,16 @@ static unsigned long long *g_dbg = nullptr;
 void set_debug_timing(unsigned long long *buf) { g_dbg = buf; }
 unsigned long long *debug_timing() { return g_dbg; }
 
+// The barrier between passes: the whole cooperative grid, or -- for kernels launched as ONE
+// thread-block cluster (small programs: DESIGN.md "Cluster launches") -- the cluster
+// barrier (release / acquire at cluster scope, which orders the CTAs' global-memory
+// accesses too).
+template <bool CL>
+__device__ __forceinline__ void pass_barrier() {
+    if constexpr (CL) cg::this_cluster().sync();
+    else cg::this_grid().sync();
+}
+
 // The per-pass counters every thread needs right after a grid barrier are loaded by ONE
 // thread per CTA and broadcast through shared memory: the same address from every warp
 // of the grid (~4.7 k requests) queues on one L2 slice for microseconds.
@@ -345,7 +355,7 @@ __device__ __forceinline__ unsigned test4(int4 a, unsigned fire, const uint32_t 
 // OR a firing row's head into v_{k+1}; the thread that sets a new bit appends the head
 // to the derivation list (the pass's "changed" signal) and records its stage.
 __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, int32_t h,
-                                          uint32_t cur_word) {
+                                          uint32_t cur_word, int32_t hkey = -1) {
     const uint32_t bit = 1u << (h & 31);
     if (cur_word & bit) return;                            // already in v_k
     const uint32_t old = atomicOr(c.wr + (h >> 5), bit);
@@ -359,7 +369,7 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
     const int32_t pos = c.base + base + __popc(m & ((1u << lane) - 1u));
     LP_CHECK(pos >= 0 && pos <= p.n_order_cap && h >= 0 && h < p.n_ext_atoms);
     p.order[pos] = h;
-    if (p.lead_codes) p.korder[pos] = __ldg(p.key_of + h);   // once per atom, not per CTA
+    if (p.lead_codes) p.korder[pos] = hkey >= 0 ? hkey : __ldg(p.key_of + h);   // once per atom
     if (p.stage && h < p.n_out) p.stage[h] = c.k + 1;
 }
 
@@ -388,6 +398,10 @@ __device__ __forceinline__ int verify_slot(const LMParams &p, const PassCtx &c, 
 #pragma unroll
     for (int j = 0; j < B; ++j) a[j] = j < n1 ? (uint32_t)__ldg(colp + (int64_t)(j0 + j) * cp) : 0u;
     const uint32_t hw = EXACT ? c.sm[h >> 5] : __ldcg(c.rd + (h >> 5));
+    // (key mode: the head's key, loaded with the truth words -- the emit needs it for the
+    // derivation list's key twin, and a load after the list reservation would add a round
+    // trip before this thread reaches the barrier)
+    const int32_t hkey = (!EXACT && p.lead_codes) ? __ldg(p.key_of + h) : -1;
 #pragma unroll
     for (int j = 0; j < B; ++j)
         w[j] = j < n1 ? (EXACT ? c.sm[a[j] >> 5] : __ldcg(c.rd + (a[j] >> 5))) : ~0u;
@@ -407,7 +421,7 @@ __device__ __forceinline__ int verify_slot(const LMParams &p, const PassCtx &c, 
         for (int j = 0; j < 4; ++j) ok = ok && ((y[j] >> (x[j] & 31)) & 1u);
         loaded += min(4, L - jb);
     }
-    if (ok) emit_head(p, c, h, hw);
+    if (ok) emit_head(p, c, h, hw, hkey);
     return loaded;
 }
 
@@ -842,9 +856,14 @@ __device__ __forceinline__ int all_segments(const LMParams &p, const PassCtx &c,
 // Mark bucket bk in the shared bucket mask.  With 16-bit codes all buckets live in one
 // word, so a delta of thousands of atoms would serialise on it: test first, the atomic
 // only for a bit not yet set.
+__shared__ int32_t s_bmask_changed;   // a bucket bit was set since the live list was built
+
 __device__ __forceinline__ void set_bucket(uint32_t *bmask, uint32_t bk) {
     const uint32_t bit = 1u << (bk & 31);
-    if (!(*(volatile uint32_t *)(bmask + (bk >> 5)) & bit)) atomicOr(bmask + (bk >> 5), bit);
+    if (!(*(volatile uint32_t *)(bmask + (bk >> 5)) & bit)) {
+        atomicOr(bmask + (bk >> 5), bit);
+        s_bmask_changed = 1;
+    }
 }
 
 // Add derivation-list entries [i0, i1) to a CTA's shared copy of v_k: exact bits
@@ -1353,6 +1372,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     if (keys) {   // the live runs of summary(v_0)
         __syncthreads();
         build_live(p, bmask, runs_sm, live_beg, live_pre, &live_tot);
+        if (tid == 0) s_bmask_changed = 0;
     }
     __syncthreads();
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 7] = globaltimer();
@@ -1444,9 +1464,10 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             }
             if (p.dbg && tid == 0 && k >= 3 && k < 16) DBG_STAMP(6) = globaltimer();
             __syncthreads();
-            if (keys && lead_pass) {   // the live runs of summary(v_k)
+            if (keys && lead_pass && s_bmask_changed) {   // the live runs of summary(v_k)
                 build_live(p, bmask, runs_sm, live_beg, live_pre, &live_tot);
                 __syncthreads();
+                if (tid == 0) s_bmask_changed = 0;   // (read again only after the next fold)
             }
             if (p.dbg && tid == 0 && k >= 3 && k < 16) DBG_STAMP(7) = globaltimer();
         }
@@ -1632,8 +1653,8 @@ cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t sme
 // The per-row counters hold the number of body atoms still unknown; the prologue sets
 // them to the row's body length L segment by segment (coalesced, overlapping the v_0
 // build), so the hot loop needs no length lookup and nothing has to be cleaned up.
+template <bool CL>
 __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_constant__ LMParams p) {
-    cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
@@ -1648,7 +1669,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
         const int64_t nw = p.cnt_bytes == 1 ? sg.count_pad >> 2 : sg.count_pad;
         for (int64_t w = gtid; w < nw; w += gthreads) p.cnt[w0 + w] = v;
     }
-    grid.sync();
+    pass_barrier<CL>();
     const int32_t n0 = cta_pass_counts(p.tail, nullptr, nullptr).appended;
     const bool lead = blockIdx.x == 0 && tid == 0;
     if (lead && p.pops && p.pop_cap > 0) p.pops[0] = n0;
@@ -1691,7 +1712,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
     __shared__ int32_t s_cnt;
     int32_t total = n0;
     for (int k = 0;; ++k) {
-        grid.sync();
+        pass_barrier<CL>();
         // level k is complete; level j = k + 1 starts at once from its queue (entries are
         // -1 past its end: no count needed to start), while one thread per CTA fetches
         // level k's append count (termination, popcount trace) -- if it is 0 the queue
@@ -1728,11 +1749,33 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
     }
 }
 
-cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st) {
+// Launch a kernel either cooperatively over `blocks` CTAs or as ONE cluster of `cluster` CTAs.
+template <class K>
+static cudaError_t launch_grid_or_cluster(K kernel_grid, K kernel_cluster, const void *param, size_t psize,
+                                          int blocks, int cluster, size_t smem, cudaStream_t st) {
+    (void)psize;
+    void *args[] = {const_cast<void *>(param)};
+    if (cluster <= 0)
+        return cudaLaunchCooperativeKernel((const void *)kernel_grid, dim3(blocks), dim3(kThreads), args, smem, st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cluster);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, (const void *)kernel_cluster, args);
+}
+
+cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st, int cluster) {
     LMParams q = p;
-    void *args[] = {(void *)&q};
-    return cudaLaunchCooperativeKernel((const void *)lm_frontier_kernel, dim3(blocks),
-                                       dim3(kThreads), args, 0, st);
+    return launch_grid_or_cluster(lm_frontier_kernel<false>, lm_frontier_kernel<true>, &q, sizeof(q), blocks,
+                                  cluster, 0, st);
 }
 
 // ------------------------------------------------------------------------------------
@@ -1780,6 +1823,9 @@ __device__ __forceinline__ void cl_verify(const LMParams &p, const Segment *segs
     if (ok) atomicOr(wr + (h >> 5), 1u << (h & 31));
 }
 
+// U = quads of the lead / head planes in flight per thread (1 when the cluster has at most
+// two quads per thread: the unrolled padding would only add instructions)
+template <int U>
 __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_constant__ LMParams p) {
     extern __shared__ __align__(16) uint32_t cbuf[];
     __shared__ int32_t s_cnt, s_qn;
@@ -1862,7 +1908,6 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
     int32_t total = block_sum(pc);
     cluster.sync();   // (every CTA's buffers initialised before any remote OR)
     if (lead && p.pops && p.pop_cap > 0) p.pops[0] = total;
-    constexpr int U = 4;   // quads of the lead / head planes in flight per thread
     const int32_t step = S * (int32_t)blockDim.x;
 #define CDBG(k, i) p.dbg[((k) * gridDim.x + blockIdx.x) * 8 + (i)]
     if (p.dbg && tid == 0) CDBG(0, 6) = ns0;
@@ -1935,7 +1980,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
                     }
             }
         }
-        cluster.sync();
+        if (S > 1) cluster.sync();
+        else __syncthreads();
         if (p.dbg && tid == 0 && k < 16) CDBG(k, 3) = globaltimer();
         // the new atoms of pass k: counted by every CTA over all words (the same complete
         // v_{k+1} everywhere), stages written by each word's owner
@@ -2001,19 +2047,20 @@ cudaError_t launch_lm_cluster(const LMParams &p, int cluster, size_t smem, cudaS
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, lm_cluster_kernel, p);
+    if ((p.n_slots >> 2) <= 2LL * cluster * kThreads) return cudaLaunchKernelEx(&cfg, lm_cluster_kernel<1>, p);
+    return cudaLaunchKernelEx(&cfg, lm_cluster_kernel<4>, p);
 }
 
 // The largest cluster (<= want) of lm_cluster_kernel that fits with `smem` bytes per CTA.
 int lm_cluster_max(int want, size_t smem) {
-    // (the attribute is the kernel's, shared by every loaded program: set the maximum)
-    if (cudaFuncSetAttribute((const void *)lm_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute((const void *)lm_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kMaxSmemBytes) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
+    // (the attributes are the kernels', shared by every loaded program: set the maximum)
+    const void *ks[2] = {(const void *)lm_cluster_kernel<1>, (const void *)lm_cluster_kernel<4>};
+    for (const void *k : ks)
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
     for (int c = want; c >= 1; --c) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)c);
@@ -2026,8 +2073,9 @@ int lm_cluster_max(int want, size_t smem) {
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, (const void *)lm_cluster_kernel, &cfg) == cudaSuccess && n >= 1)
+        int n1 = 0, n4 = 0;
+        if (cudaOccupancyMaxActiveClusters(&n1, ks[0], &cfg) == cudaSuccess && n1 >= 1 &&
+            cudaOccupancyMaxActiveClusters(&n4, ks[1], &cfg) == cudaSuccess && n4 >= 1)
             return c;
         cudaGetLastError();
     }
@@ -2196,9 +2244,9 @@ __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int
 // once, until no word changes.  Shared memory holds one "any guess" bit per extended
 // atom; a row whose body has an atom false in every guess is skipped after the bit
 // test, so only candidate rows gather the 8·Wp-byte guess rows.
+template <bool CL>
 __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
     extern __shared__ uint32_t sm[];
-    cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
@@ -2209,9 +2257,9 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
     // the call's set-up, in the same launch: the previous call's rows and this call's
     // counters cleared, then T_0 (Def. 8) and its "any" bits
     st_clear_phase(p, clear_rows, gtid, gthreads);
-    grid.sync();
+    pass_barrier<CL>();
     st_init_phase(p, gtid, gthreads);
-    grid.sync();
+    pass_barrier<CL>();
     // shared memory: "true in some guess" bits, then (exact filter only) "true in every
     // guess" bits -- a row whose head is full can change nothing
     uint32_t *full = sm + p.any_words;
@@ -2399,7 +2447,7 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
             __syncthreads();
             if (tid == 0) atomicMax(p.dbg + 4 * k + 3, globaltimer());     // CTA's scan done
         }
-        grid.sync();
+        pass_barrier<CL>();
         // rows changed in this pass: its own counter slot (the next pass appends to
         // another one, so every CTA reads the same value after the barrier); this
         // thread's first entries of the list are loaded together with it (slots past the
@@ -2431,8 +2479,9 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
     st_check_phase(p, gtid, gthreads);
 }
 
+template <bool CL>
 __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_constant__ STParams p) {
-    st_run(p, p.clear_rows);
+    st_run<CL>(p, p.clear_rows);
     if (blockIdx.x == 0 && threadIdx.x == 0 && p.status_user)
         *p.status_user = *(volatile int32_t *)p.status_out;
 }
@@ -2517,18 +2566,18 @@ __device__ void search_move(const STParams &p, int32_t r_next, int64_t gtid, int
     }
 }
 
+template <bool CL>
 __global__ void __launch_bounds__(kThreads, 1) st_search_kernel(const __grid_constant__ STParams p) {
-    cg::grid_group grid = cg::this_grid();
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
     __shared__ long long s_nacc;
     search_sample(p, gtid, gthreads);
-    grid.sync();
+    pass_barrier<CL>();
     int32_t passes = 0;
     for (int32_t r = 0;; ++r) {
-        st_run(p, r == 0 ? p.clear_rows : 1);
-        grid.sync();   // (the check phase's accepted words and count are complete)
+        st_run<CL>(p, r == 0 ? p.clear_rows : 1);
+        pass_barrier<CL>();   // (the check phase's accepted words and count are complete)
         if (threadIdx.x == 0) s_nacc = __ldcg(reinterpret_cast<const long long *>(p.n_accepted));
         __syncthreads();
         const long long nacc = s_nacc;
@@ -2542,22 +2591,20 @@ __global__ void __launch_bounds__(kThreads, 1) st_search_kernel(const __grid_con
             return;
         }
         search_move(p, r + 1, gtid, gthreads);
-        grid.sync();
+        pass_barrier<CL>();
     }
 }
 
-cudaError_t launch_st_search(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
+cudaError_t launch_st_search(const STParams &p, int blocks, size_t smem, cudaStream_t st, int cluster) {
     STParams q = p;
-    void *args[] = {(void *)&q};
-    return cudaLaunchCooperativeKernel((const void *)st_search_kernel, dim3(blocks), dim3(kThreads), args,
-                                       smem, st);
+    return launch_grid_or_cluster(st_search_kernel<false>, st_search_kernel<true>, &q, sizeof(q), blocks, cluster,
+                                  smem, st);
 }
 
-cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
+cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st, int cluster) {
     STParams q = p;
-    void *args[] = {(void *)&q};
-    return cudaLaunchCooperativeKernel((const void *)st_fixpoint_kernel, dim3(blocks),
-                                       dim3(kThreads), args, smem, st);
+    return launch_grid_or_cluster(st_fixpoint_kernel<false>, st_fixpoint_kernel<true>, &q, sizeof(q), blocks,
+                                  cluster, smem, st);
 }
 
 // Algorithm 3 (reading R7): guess g is accepted iff for every negated
@@ -2647,12 +2694,19 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
     if ((e = cudaFuncSetAttribute((const void *)lm_full_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, cap)))
         return e;
-    if ((e = cudaFuncSetAttribute((const void *)st_fixpoint_kernel,   // (+ its static candidate queue)
+    if ((e = cudaFuncSetAttribute((const void *)st_fixpoint_kernel<false>,   // (+ its static candidate queue)
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
         return e;
-    if ((e = cudaFuncSetAttribute((const void *)st_search_kernel,
+    if ((e = cudaFuncSetAttribute((const void *)st_search_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
         return e;
+    // the one-cluster launches of the same kernels (16 CTAs: a non-portable cluster size)
+    const void *cl[3] = {(const void *)st_fixpoint_kernel<true>, (const void *)st_search_kernel<true>,
+                         (const void *)lm_frontier_kernel<true>};
+    for (const void *k : cl) {
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes))) return e;
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1))) return e;
+    }
     return cudaSuccess;
 }
 
@@ -2666,16 +2720,47 @@ int lm_full_blocks_per_sm(bool exact, size_t smem) {
 
 int lm_frontier_blocks_per_sm() {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)lm_frontier_kernel, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)lm_frontier_kernel<false>, kThreads, 0);
     return nb;
 }
 
 int st_blocks_per_sm(size_t smem) {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)st_fixpoint_kernel, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)st_fixpoint_kernel<false>, kThreads, smem);
     int ns = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ns, (const void *)st_search_kernel, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ns, (const void *)st_search_kernel<false>, kThreads, smem);
     return std::min(nb, ns);   // (both launch on the same grid)
 }
 
+}  // namespace lpb
+
+namespace lpb {
+// The largest one-cluster launch (<= want CTAs) of the cluster instantiation of a
+// persistent kernel with `smem` bytes: 0 if none fits.  which: 0 frontier, 1 stable.
+int cluster_size_for(int which, int want, size_t smem) {
+    const void *ks[2][2] = {{(const void *)lm_frontier_kernel<true>, nullptr},
+                            {(const void *)st_fixpoint_kernel<true>, (const void *)st_search_kernel<true>}};
+    for (int c = want; c >= 1; --c) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)c);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)c;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        bool ok = true;
+        for (const void *k : ks[which]) {
+            int n = 0;
+            if (!k) continue;
+            if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n < 1) ok = false;
+        }
+        cudaGetLastError();
+        if (ok) return c;
+    }
+    return 0;
+}
 }  // namespace lpb

@@ -219,7 +219,10 @@ cudaError_t launch_shard_combine(const ShardCombineParams &q, cudaStream_t st);
 // Each least-model call is ONE cooperative launch: v_0 prologue, the fixpoint loop and
 // the model extraction all run inside the persistent kernel.
 cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st);
-cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st);
+// cluster > 0: ONE thread-block cluster of that many CTAs with cluster barriers between
+// passes (small programs); else the cooperative grid
+cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st, int cluster);
+int cluster_size_for(int which, int want, size_t smem);
 // Exact-mode programs small enough for one thread-block cluster (truth in shared memory,
 // DSMEM exchange, cluster barriers): the whole fixpoint in one cluster launch.
 cudaError_t launch_lm_cluster(const LMParams &p, int cluster, size_t smem, cudaStream_t st);
@@ -227,9 +230,9 @@ int lm_cluster_max(int want, size_t smem);
 
 // One cooperative launch per stable call: clear the previous call's rows, build T_0, the
 // fixpoint loop, the stability check.
-cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st);
+cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st, int cluster);
 // Guess-space reduction: all rounds of sampling + local search in one cooperative launch.
-cudaError_t launch_st_search(const STParams &p, int blocks, size_t smem, cudaStream_t st);
+cudaError_t launch_st_search(const STParams &p, int blocks, size_t smem, cudaStream_t st, int cluster);
 cudaError_t launch_st_column(const STParams &p, int32_t n, int64_t g, unsigned long long *out,
                              cudaStream_t st);
 

@@ -723,3 +723,27 @@ def test_pinned_host_model_out_written_by_the_kernel(frontier):
         assert lp.lp_least_model(prog, None, pageable, frontier=frontier) == oit
         assert (pageable == oracle.pack_bits(om)).all()
         prog.close()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_one_cluster_launches_of_grid_kernels(seed, monkeypatch):
+    """The frontier and stable kernels launched as ONE 16-CTA cluster with cluster barriers
+    (pass_barrier<true>; default for small frontier programs, A/B-only for the stable
+    kernel): same results as the oracle."""
+    monkeypatch.setenv("LP_CLUSTER_FR_SLOTS", str(1 << 30))
+    monkeypatch.setenv("LP_CLUSTER_ST_SLOTS", str(1 << 30))
+    rng = np.random.default_rng([seed, 5150])
+    n = int(rng.integers(500, 20000))
+    P = lpgen.random_program(rng, n, 5 * n, max_len=5, n_facts=n // 20)
+    prog = lp.Program(P)
+    assert prog.info["frontier_cluster_ctas"] >= 1
+    check_lm(P, prog=prog, variants=(True,))
+    N = lpgen.random_normal_program(rng, 80, 300, max_len=3, k_max=7)
+    sp = lp.Program(N)
+    assert sp.info["stable_cluster_ctas"] >= 1
+    check_stable(N, prog=sp)
+    from oracle import search
+    S = lpgen.gen_c5(seed=seed, n=3000, R=15000, k=24)
+    o = search.stable_search(S, h=128, seed=seed, max_rounds=6)
+    g = lp.Program(S).stable_search(128, seed, 6)
+    assert g["rounds"] == o["rounds"] and g["passes"] == o["passes"] and g["accepted"].tolist() == o["accepted"]

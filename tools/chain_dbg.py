@@ -1,5 +1,5 @@
 import sys, time, os
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, lpgen, oracle
 from paper_2009_10247_b200 import lp
 L = int(sys.argv[1])
