@@ -1264,12 +1264,26 @@ __device__ __noinline__ bool lead_start_too_dense(const LMParams &p, const uint3
     if (tid < 32) bc[tid] = 0u;
     if (tid == 0) est = 0ull;
     __syncthreads();
-    for (int32_t w0 = tid & ~31; w0 < p.ksm_words; w0 += blockDim.x) {   // a warp's 32 words: one bucket
+    // each warp counts a contiguous range of summary words (registers), flushing its sum
+    // once per bucket (2048 words) it crosses: a few shared atomics per warp, not per word
+    const int nwarps = blockDim.x >> 5, warp = tid >> 5;
+    const int32_t per = ((p.ksm_words + nwarps - 1) / nwarps + 31) & ~31;   // (32-aligned: no chunk
+                                                                          //  straddles a bucket)
+    const int32_t w_lo = warp * per, w_hi = min(p.ksm_words, w_lo + per);
+    uint32_t c = 0;
+    int32_t cur_b = w_lo >> 11;
+    for (int32_t w0 = w_lo; w0 < w_hi; w0 += 32) {
         const int32_t w = w0 + lane;
-        uint32_t c = w < p.ksm_words ? (uint32_t)__popc(sm[w]) : 0u;
-        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-        if (lane == 0 && c) atomicAdd(&bc[(w0 >> 11) & 31], c);
+        if ((w0 >> 11) != cur_b) {   // (warp-uniform: w0 is)
+            for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+            if (lane == 0 && c) atomicAdd(&bc[cur_b & 31], c);
+            c = 0;
+            cur_b = w0 >> 11;
+        }
+        c += w < w_hi ? (uint32_t)__popc(sm[w]) : 0u;
     }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if (lane == 0 && c) atomicAdd(&bc[cur_b & 31], c);
     __syncthreads();
     for (int32_t r = tid; r < p.nruns; r += blockDim.x) {
         const int4 ru = runs_sm[r];
@@ -1384,7 +1398,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     // queue are estimated from the live runs and the density of set bits in their buckets;
     // more than n_slots / dense_div -> start with STREAM passes instead of verifying them
     // (a v0 with many atoms outside D2 lights the coarse buckets: DESIGN.md "Schedule")
-    if (!EXACT && keys && p.pass_mode == 0 && p.key_bits == 16 && p.nruns > 0 && p.predict &&
+    // (v0 = NULL: the facts light only D2 buckets, never a dense start -- no estimate)
+    if (!EXACT && keys && p.v0 && p.pass_mode == 0 && p.key_bits == 16 && p.nruns > 0 && p.predict &&
         lead_start_too_dense(p, sm, runs_sm)) {
         lead_pass = false;
         keys = false;
@@ -1828,7 +1843,7 @@ __device__ __forceinline__ void cl_verify(const LMParams &p, const Segment *segs
 template <int U>
 __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_constant__ LMParams p) {
     extern __shared__ __align__(16) uint32_t cbuf[];
-    __shared__ int32_t s_cnt, s_qn;
+    __shared__ int32_t s_cnt[2], s_qn[2];   // per pass parity: reset one pass ahead (fewer barriers)
     __shared__ int32_t cl_q[kClQueue];     // this pass's candidate rows
     __shared__ Segment ssegs[kMaxSmemSegs];
     __shared__ long long clk0;
@@ -1876,14 +1891,18 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
         colg = reinterpret_cast<const int32_t *>(sc);
     }
     // block-wide sum of one value per thread (the count of new atoms); two barriers
-    auto block_sum = [&](int32_t x) {
+    // block-wide sum of one value per thread into s_cnt[par] (zeroed a pass ahead); one barrier
+    auto block_sum = [&](int32_t x, int par) {
         for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
-        if (tid == 0) s_cnt = 0;
+        if (lane == 0 && x) atomicAdd(&s_cnt[par], x);
         __syncthreads();
-        if (lane == 0 && x) atomicAdd(&s_cnt, x);
-        __syncthreads();
-        return s_cnt;
+        return s_cnt[par];
     };
+    if (tid == 0) {
+        s_cnt[0] = s_cnt[1] = 0;
+        s_qn[0] = s_qn[1] = 0;
+    }
+    __syncthreads();
     // v_0 = (v0 restricted to the original atoms) | facts | ⊤ in both buffers (Def. 4), its
     // size, and the stages of the original atoms (this CTA's words)
     int32_t pc = 0;
@@ -1905,7 +1924,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
         if (p.stage && (w % S) == cr)
             for (int b = 0; b < 32 && lo + b < p.n_out; ++b) p.stage[lo + b] = ((orig >> b) & 1u) ? 0 : -1;
     }
-    int32_t total = block_sum(pc);
+    int32_t total = block_sum(pc, 1);   // (slot 1: pass 0 counts into slot 0)
     cluster.sync();   // (every CTA's buffers initialised before any remote OR)
     if (lead && p.pops && p.pop_cap > 0) p.pops[0] = total;
     const int32_t step = S * (int32_t)blockDim.x;
@@ -1920,8 +1939,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
                 const uint32_t x = rd[w] & ~wr[w];
                 if (x) atomicOr(wr + w, x);
             }
-        if (tid == 0) s_qn = 0;
-        __syncthreads();
+        // (the merge's ORs commute with this pass's; s_qn[k & 1] and s_cnt[k & 1] were zeroed
+        // during pass k-1, after its stream barrier -- past every reader of pass k-2)
         if (p.dbg && tid == 0 && k < 16) CDBG(k, 1) = globaltimer();
         // LEAD pass over this CTA's quads of the flat planes: a row whose lead atom is in v_k
         // and whose head is not is queued (one reservation per warp and quad step); the
@@ -1953,7 +1972,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
                     if (lane >= o) incl += y;
                 }
                 int base = 0;
-                if (lane == 31) base = atomicAdd(&s_qn, incl);
+                if (lane == 31) base = atomicAdd(&s_qn[k & 1], incl);
                 base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - c;
                 for (unsigned f = cand; f; f &= f - 1, ++base) {
                     const int32_t slot = q * 4 + __ffs(f) - 1;
@@ -1963,8 +1982,12 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
             }
         }
         __syncthreads();
+        if (tid == 0) {   // the next pass's slots (their last readers, in pass k-1, are past this barrier)
+            s_qn[(k + 1) & 1] = 0;
+            s_cnt[(k + 1) & 1] = 0;
+        }
         {
-            const int32_t nc = min(s_qn, kClQueue);
+            const int32_t nc = min(s_qn[k & 1], kClQueue);
             for (int32_t i = tid; i < nc; i += blockDim.x)
                 cl_verify(p, segs, colg, reinterpret_cast<const int32_t *>(hb), rd, wr, cl_q[i]);
         }
@@ -1998,7 +2021,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
                     if (a < p.n_out) p.stage[a] = k + 1;
                 }
         }
-        const int32_t sum = block_sum(nn);
+        const int32_t sum = block_sum(nn, k & 1);
         if (p.dbg && tid == 0 && k < 16) CDBG(k, 5) = globaltimer();
         if (lead && p.stats)
             atomicAdd(p.stats + 0, (p.stage_planes ? 0ull : 8ull * (unsigned long long)p.n_slots) +
@@ -2274,6 +2297,7 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
     int32_t n1 = 0, n2 = 0;
     constexpr int kStSpec = 2;
     int32_t s1[kStSpec] = {-1, -1}, s2[kStSpec] = {-1, -1};   // this thread's first entries of both lists
+    uint32_t fwc[kStSpec] = {0u, 0u};                          // gfull words of s2 (loaded early)
     for (int k = 0;; ++k) {
         const unsigned long long *rd = (k & 1) ? p.T1 : p.T0;
         unsigned long long *wr = (k & 1) ? p.T0 : p.T1;
@@ -2292,10 +2316,9 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
                 atomicOr(sm + (g >> 5), 1u << (g & 31));
             }
             if (use_full) {   // the full marks made during pass k-1 (rows changed in pass k-2)
-                uint32_t fw[kStSpec];
-                for (int u = 0; u < kStSpec; ++u) fw[u] = s2[u] >= 0 ? __ldcg(p.gfull + (s2[u] >> 5)) : 0u;
+                // (their gfull words were loaded right after the barrier, beside the list)
                 for (int u = 0; u < kStSpec; ++u)
-                    if (s2[u] >= 0 && ((fw[u] >> (s2[u] & 31)) & 1u)) atomicOr(full + (s2[u] >> 5), 1u << (s2[u] & 31));
+                    if (s2[u] >= 0 && ((fwc[u] >> (s2[u] & 31)) & 1u)) atomicOr(full + (s2[u] >> 5), 1u << (s2[u] & 31));
                 for (int64_t i = tid + kStSpec * blockDim.x; i < n2; i += blockDim.x) {
                     const uint32_t h = (uint32_t)__ldcg(l2 + i);
                     if ((__ldcg(p.gfull + (h >> 5)) >> (h & 31)) & 1u) atomicOr(full + (h >> 5), 1u << (h & 31));
@@ -2453,9 +2476,11 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
         // thread's first entries of the list are loaded together with it (slots past the
         // count hold stale entries of an earlier pass and are dropped)
         int32_t nx[kStSpec];
+        uint32_t fwn[kStSpec];   // the gfull words of the rows changed in pass k-1 (marked during pass k)
         for (int u = 0; u < kStSpec; ++u) {
             const int64_t i = tid + (int64_t)u * blockDim.x;
             nx[u] = i < p.ring_cap ? __ldcg(p.order + (int64_t)(k % 3) * p.ring_cap + i) : -1;
+            fwn[u] = (use_full && s1[u] >= 0) ? __ldcg(p.gfull + (s1[u] >> 5)) : 0u;
         }
         const int32_t cnt = cta_pass_counts(p.pcnt + k % 3, nullptr, nullptr).appended;
         const bool lead = blockIdx.x == 0 && tid == 0;
@@ -2472,6 +2497,7 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
         n1 = cnt;
         for (int u = 0; u < kStSpec; ++u) {
             s2[u] = s1[u];
+            fwc[u] = fwn[u];
             s1[u] = tid + u * (int)blockDim.x < cnt ? nx[u] : -1;
         }
     }
