@@ -624,8 +624,6 @@ __device__ __forceinline__ void build_live(const LMParams &p, const uint32_t *bm
             pre[0] = 0;
             pre[1] = (int32_t)(p.n_slots >> 3);
             *total = (int32_t)(p.n_slots >> 3);
-            if (blockIdx.x == 0 && p.stats)
-                atomicAdd(p.stats + 0, (unsigned long long)(p.n_slots >> 3) * (p.key_bits == 8 ? 10ull : 17ull));
         }
         return;
     }
@@ -657,8 +655,6 @@ __device__ __forceinline__ void build_live(const LMParams &p, const uint32_t *bm
     if (lane == 0) {
         pre[m] = tot;   // sentinel: the cursor never passes the last live run
         *total = tot;
-        if (blockIdx.x == 0 && p.stats)   // the pass's streamed bytes: codes + tag per octet
-            atomicAdd(p.stats + 0, (unsigned long long)tot * (p.key_bits == 8 ? 10ull : 17ull));
     }
 }
 
@@ -1039,6 +1035,8 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         int loaded = 0;
         if (!verifier) {
             const LiveList lv{ls.beg, ls.pre, *ls.total};   // (built before the call)
+            if (blockIdx.x == 0 && tid == 0 && p.stats)
+                atomicAdd(p.stats + 0, (unsigned long long)lv.total * (p.key_bits == 8 ? 10ull : 17ull));
             pipe_stream(p, sm, bmask, lv, sq[0], gq[0], &qcnt[0], &abandon, (int64_t)blockIdx.x * vbase + tid,
                         (int64_t)gridDim.x * vbase);
             __syncwarp();
@@ -1132,6 +1130,8 @@ __device__ __noinline__ PipeExit lm_pipe(const LMParams &p, uint32_t *sm, uint32
         build_live(p, bmask, ls.runs, ls.beg, ls.pre, ls.total);
         __syncthreads();
         const LiveList lv{ls.beg, ls.pre, *ls.total};
+        if (lead && p.stats)   // (this phase's stream: pass k+2's candidates)
+            atomicAdd(p.stats + 0, (unsigned long long)lv.total * (p.key_bits == 8 ? 10ull : 17ull));
         ds = de;
         de = t;
         // ---- phase j = k + 1
@@ -1487,6 +1487,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             if (p.dbg && tid == 0 && k >= 3 && k < 16) DBG_STAMP(7) = globaltimer();
         }
         const LiveList lv{live_beg, live_pre, live_tot};
+        if (lead && p.stats && keys && lead_pass)   // the pass's streamed bytes: codes + tag per live octet
+            atomicAdd(p.stats + 0, (unsigned long long)lv.total * (p.key_bits == 8 ? 10ull : 17ull));
         // rows queued in pass k are counted in cand[k % 3]; the slot of pass k+1 was last
         // read before the previous barrier and is first written after the next one
         if (lead) {
