@@ -747,3 +747,24 @@ def test_one_cluster_launches_of_grid_kernels(seed, monkeypatch):
     o = search.stable_search(S, h=128, seed=seed, max_rounds=6)
     g = lp.Program(S).stable_search(128, seed, 6)
     assert g["rounds"] == o["rounds"] and g["passes"] == o["passes"] and g["accepted"].tolist() == o["accepted"]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_frontier_counters_across_calls(seed):
+    """Back-to-back frontier calls on one program reuse its row counters, queues and list
+    (re-initialised by every call's prologue): small and large models, random start sets,
+    a capped call in between -- all equal the oracle."""
+    rng = np.random.default_rng([seed, 6060])
+    n = int(rng.integers(2000, 30000))
+    P = lpgen.random_program(rng, n, 4 * n, max_len=5, n_facts=max(1, n // 200))
+    prog = lp.Program(P)
+    starts = [None, rng.choice(n, size=n // 3, replace=False).tolist(), None,
+              rng.choice(n, size=5, replace=False).tolist(), None]
+    for i, v0 in enumerate(starts):
+        om, ostage, oit, opops = _oracle_lm(P, v0)
+        if i == 2:   # a capped call in between (its counters are re-initialised next time)
+            m, it, ex = prog.least_model(v0, frontier=True, max_passes=max(1, oit // 2))
+            assert it == max(1, min(oit, oit // 2))
+        model, iters, ex = prog.least_model(v0, frontier=True, popcounts=True, stages=True)
+        assert iters == oit and (model == om).all() and ex["popcounts"] == opops
+        assert (ex["stage"] == ostage).all()
