@@ -202,8 +202,9 @@ class _GpuShard:
         self.run = None      # lp_run of this rank's pass (set on the first pass: needs the payload)
         self.c_int = ctypes
 
-    def reset(self):
-        self.pops.zero_()
+    def reset(self, popcounts=True):
+        if popcounts:   # (the combine adds |v_{k+1}| into pops[k + 1]; unused otherwise)
+            self.pops.zero_()
 
     def _prepare(self, rank, payload):
         lp = self.lp
@@ -281,27 +282,38 @@ class ShardedLeastModel:
         start = np.zeros(self.W * 64, dtype=np.uint8)        # I_0 = facts of every rank's rules
         start[np.asarray(rules.head)[ptr[1:] == ptr[:-1]]] = 1
         self.start = start
+        self.start_pop = int(np.count_nonzero(start))   # |I_0| (host work once, not per run)
         self.facts_words = torch.from_numpy(np.packbits(start, bitorder="little").view(np.int64).copy()).to(device)
         self.v = [torch.zeros(self.W, dtype=torch.int64, device=device) for _ in range(2)]
         self.payload = torch.zeros(self.stride, dtype=torch.int64, device=device)
         self.gathered = torch.zeros(self.world * self.stride, dtype=torch.int64, device=device)
         self.max_passes = self.n + 3
 
-    def run(self, v0=None, popcounts: bool = True):
-        """Returns (model words uint64[ceil(n/64)], iters, popcount trace or [])."""
+    def run(self, v0=None, popcounts: bool = True, v0_words=None):
+        """Returns (model words uint64[ceil(n/64)], iters, popcount trace or []).  The start
+        set: v0 (bool mask or None = facts only) or v0_words (packed LSB-first uint64 words
+        of the atoms, as lp_least_model takes them; the facts are added on the device)."""
         import torch
         import torch.distributed as dist
 
-        if v0 is None:
+        if v0_words is not None:
+            w = torch.from_numpy(np.ascontiguousarray(v0_words, dtype=np.uint64).view(np.int64))
+            self.v[0].zero_()
+            self.v[0][:w.numel()].copy_(w, non_blocking=True)
+            self.v[0].bitwise_or_(self.facts_words)
+            if self.n % 64 and (self.n + 63) // 64 == self.W:   # (padding bits past atom n-1 off)
+                self.v[0][self.W - 1:].bitwise_and_((1 << (self.n % 64)) - 1)
+            pop0 = int(np.unpackbits(self.v[0].cpu().numpy().view(np.uint8)).sum()) if popcounts else 0
+        elif v0 is None:
             self.v[0].copy_(self.facts_words)
-            pop0 = int(self.start.sum())
+            pop0 = self.start_pop
         else:
             st = self.start.copy()
             st[:self.n] |= np.asarray(v0, dtype=bool).astype(np.uint8)
             self.v[0].copy_(torch.from_numpy(np.packbits(st, bitorder="little").view(np.int64).copy()))
-            pop0 = int(st.sum())
+            pop0 = int(np.count_nonzero(st)) if popcounts else 0
         b = self.backend
-        b.reset()
+        b.reset(popcounts)
         k = 0
         while True:
             if k >= self.max_passes:

@@ -130,7 +130,7 @@ class _OracleShard:
         self.n = P.n_atoms
         self.flags, self.pops = {}, {}
 
-    def reset(self):
+    def reset(self, popcounts=True):
         self.flags, self.pops = {}, {}
 
     def one_pass(self, rank, v, payload):

@@ -63,4 +63,27 @@ for i, (t, e) in enumerate(zip(rows, evs)):
           f"combine {1e6 * (t[3] - t[2]):6.1f}  wait {1e6 * (t[4] - t[3]):7.1f} us | device pass "
           f"{1e3 * e[0].elapsed_time(e[1]):7.1f}  gather {1e3 * e[1].elapsed_time(e[2]):6.1f}  "
           f"combine {1e3 * e[2].elapsed_time(e[3]):6.1f} us")
+
+# the bench's step shape: L2 flush on a side stream, barrier, events around run()
+side = torch.cuda.Stream()
+flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+for label, do_flush, do_barrier in (("plain", False, False), ("flush", True, False), ("barrier", False, True),
+                                    ("flush+barrier", True, True)):
+    ts = []
+    for i in range(6):
+        if do_flush:
+            with torch.cuda.stream(side):
+                flush.fill_(i)
+            side.synchronize()
+        if do_barrier:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sh.run(popcounts=False)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 1:
+            ts.append(e0.elapsed_time(e1))
+    print(f"run() {label:14s}: {np.mean(ts):.3f} ms (min {np.min(ts):.3f})")
 dist.destroy_process_group()
