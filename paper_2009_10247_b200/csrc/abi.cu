@@ -43,7 +43,7 @@ struct lp_program {
     int32_t *d_occ_slot = nullptr;
     int32_t *d_fq = nullptr;   // frontier level queues [2][n_ext + 1] x (atom, occ range, -)
     uint32_t *d_cnt = nullptr;
-    int cnt_bytes = 1;
+    int cnt_bits = 8;
     uint32_t *d_buf0 = nullptr, *d_buf1 = nullptr;
     int32_t nwords = 0;
     uint32_t *d_summary = nullptr;
@@ -453,8 +453,14 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
             TRY(dalloc(p, &p->d_fq, (size_t)8 * ((size_t)L.n_ext + 1)));
             CK(cudaMemset(p->d_fq, 0xFF, (size_t)8 * ((size_t)L.n_ext + 1) * sizeof(int32_t)));
         }
-        p->cnt_bytes = L.max_body <= 255 ? 1 : 4;
-        const size_t cw = p->cnt_bytes == 1 ? ((size_t)L.n_slots + 3) / 4 : (size_t)L.n_slots;
+        // the narrowest counter that holds every body length: nibbles (8 rows per word) when
+        // bodies are <= 15 atoms and the segments are 8-aligned (key / 16-bit layouts), bytes
+        // when <= 255, else uint32 -- the frontier's prologue re-initialises them every call
+        bool al8 = true;
+        for (const Segment &sg : L.segs) al8 = al8 && (sg.slot_off % 8 == 0) && (sg.count_pad % 8 == 0);
+        p->cnt_bits = (L.max_body <= 15 && al8 && !std::getenv("LP_NO_NIBBLES")) ? 4 : L.max_body <= 255 ? 8 : 32;
+        const size_t cw = p->cnt_bits == 4 ? ((size_t)L.n_slots + 7) / 8
+                        : p->cnt_bits == 8 ? ((size_t)L.n_slots + 3) / 4 : (size_t)L.n_slots;
         TRY(dalloc(p, &p->d_cnt, std::max<size_t>(cw, 1)));
     }
 
@@ -789,7 +795,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.occ_slot = p->d_occ_slot;
     q.fq = p->d_fq;
     q.cnt = p->d_cnt;
-    q.cnt_bytes = p->cnt_bytes;
+    q.cnt_bits = p->cnt_bits;
     q.dbg = debug_timing();
     q.qbuf = p->d_qbuf;
     q.qcap = p->qcap;

@@ -1681,9 +1681,11 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
     lm_prologue(p, false, gtid, gthreads);
     for (int32_t s = 0; s < p.nseg; ++s) {   // counters <- L (4 rows per word in byte mode)
         const Segment sg = p.segs[s];
-        const uint32_t v = p.cnt_bytes == 1 ? (uint32_t)sg.L * 0x01010101u : (uint32_t)sg.L;
-        const int64_t w0 = p.cnt_bytes == 1 ? sg.slot_off >> 2 : sg.slot_off;
-        const int64_t nw = p.cnt_bytes == 1 ? sg.count_pad >> 2 : sg.count_pad;
+        // (nibbles: 8 rows per word -- segments are 8-aligned then, see abi.cu; bytes: 4)
+        const uint32_t v = p.cnt_bits == 4 ? (uint32_t)sg.L * 0x11111111u
+                         : p.cnt_bits == 8 ? (uint32_t)sg.L * 0x01010101u : (uint32_t)sg.L;
+        const int64_t w0 = p.cnt_bits == 4 ? sg.slot_off >> 3 : p.cnt_bits == 8 ? sg.slot_off >> 2 : sg.slot_off;
+        const int64_t nw = p.cnt_bits == 4 ? sg.count_pad >> 3 : p.cnt_bits == 8 ? sg.count_pad >> 2 : sg.count_pad;
         for (int64_t w = gtid; w < nw; w += gthreads) p.cnt[w0 + w] = v;
     }
     pass_barrier<CL>();
@@ -1701,7 +1703,10 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
             const int4 e = __ldg(occ + o);
             const int32_t slot = e.x;
             bool fired;
-            if (p.cnt_bytes == 1) {   // a byte never underflows: <= L decrements
+            if (p.cnt_bits == 4) {    // a nibble never underflows: <= L <= 15 decrements
+                const uint32_t sh = (uint32_t)(slot & 7) << 2;
+                fired = ((atomicSub(p.cnt + (slot >> 3), 1u << sh) >> sh) & 0xFu) == 1u;
+            } else if (p.cnt_bits == 8) {   // a byte never underflows: <= L decrements
                 const uint32_t sh = (uint32_t)(slot & 3) << 3;
                 fired = ((atomicSub(p.cnt + (slot >> 2), 1u << sh) >> sh) & 0xFFu) == 1u;
             } else {

@@ -83,7 +83,7 @@ struct LMParams {
     const int32_t *occ_slot;   // [4 * nnz]: (slot, head(slot), occ range of that head) per occurrence
     int32_t *fq;               // [2][n_order_cap][4] frontier level queues (atom, occ range), -1 = empty
     uint32_t *cnt;             // per-slot remaining-body counters
-    int32_t cnt_bytes;         // 1: uint8 packed 4 per word; 4: uint32
+    int32_t cnt_bits;          // 4: nibbles, 8 per word; 8: bytes, 4 per word; 32: uint32
     unsigned long long *dbg;   // optional profiling timestamps (lpdbg_set_timing)
     // FILTER mode: per-CTA candidate queues (rows that passed the summary test)
     int32_t *qbuf;             // [grid][qcap]
