@@ -581,6 +581,20 @@ def main():
                                "gpu_speedup_full": med * 1e3 / ms_max}
         if "frontier" in out:
             out["cpu_baseline"]["gpu_speedup_frontier"] = med * 1e3 / out["frontier"]["ms_per_step"]
+        # the oracle's plain definition (Jacobi T_P over every rule each pass) as a
+        # separately labelled extra: one whole fixpoint, the same pinned core
+        old_aff = os.sched_getaffinity(0)
+        try:
+            os.sched_setaffinity(0, {core})
+            t0 = time.perf_counter()
+            _, jit, _, jconv = oracle.lm_jacobi(P)
+            tj = time.perf_counter() - t0
+        finally:
+            os.sched_setaffinity(0, old_aff)
+        assert jconv and jit == iters
+        out["cpu_jacobi"] = {"value": nnz * iters / tj, "unit": "nnz*iter/s", "cores": 1, "ms": tj * 1e3,
+                             "kind": "oracle O-LM Jacobi (oracle/lp_oracle.c orc_lm_jacobi: every rule, every pass)",
+                             "sample": f"one whole fixpoint of {args.workload}, core {core}"}
         out["model_check"] = "main-line model == oracle O-STAGE model (bit-exact), iters equal"
     if rank == 0:
         print(json.dumps(out), flush=True)

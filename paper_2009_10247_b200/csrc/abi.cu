@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -196,8 +198,19 @@ static uint64_t stream_plane_bytes(const lp_program *p) {
 // lp_load
 // ------------------------------------------------------------------------------------
 
+// LP_LOAD_TIMING=1: lp_load prints the host time of each phase to stderr (profiling aid)
+static void load_mark(const char *what) {
+    static thread_local std::chrono::steady_clock::time_point t0;
+    static const bool on = std::getenv("LP_LOAD_TIMING") != nullptr;
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    if (what) std::fprintf(stderr, "lp_load %-28s %8.3f s\n", what, std::chrono::duration<double>(t - t0).count());
+    t0 = t;
+}
+
 static lp_status load_device(lp_program *p, const lp_options *opt) {
     HostLayout &L = p->L;
+    load_mark(nullptr);
     CK(cudaSetDevice(p->device));
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
@@ -261,6 +274,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     }
     p->lm_smem = (size_t)p->sm_words * 4;
 
+    load_mark("small uploads");
     // key plane (summary mode, register-streaming kernel): every
     // extended atom gets a key -- atoms that can become true without v0 (D2: facts and the
     // heads of rules whose bodies are heads or facts; abar, ⊤) consecutive keys, every
@@ -361,6 +375,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
             p->d_lead_codes = c;
             p->d_octet_tag = t;
         }
+        load_mark("keys, buckets, codes");
         {   // lead-occurrence lists (pipelined LEAD passes): slots by body position 0
             std::vector<int32_t> lp((size_t)L.n_ext + 1, 0), ls;
             for (const Segment &sg : L.segs)
@@ -396,6 +411,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         p->lm_smem = std::max(p->lm_smem, (size_t)kw * 4);
     }
 
+    load_mark("lead-occurrence lists");
     // exact mode, ids < 2^21: rows bucketed by (lead >> 16, head >> 16) so a LEAD pass
     // streams 16-bit lead and head planes + a 16-bit tag per 8-row octet (lead bucket |
     // head bucket << 5 | trailing padding << 10): 4.25 bytes per row instead of 8
@@ -421,8 +437,10 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(upload(p, &p->d_xtag, tag));
     }
 
+    load_mark("exact 16-bit planes");
     // the program planes in their final row order
     if (L.has_occ) build_occ_lists(&L);
+    load_mark("occurrence lists (host)");
     if (p->exact) {   // flat lead plane for exact-mode LEAD passes (one loop, no segments)
         std::vector<int32_t> l32((size_t)std::max<int64_t>(L.n_slots, 4), L.bot);
         for (const Segment &sg : L.segs)
@@ -464,6 +482,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(dalloc(p, &p->d_cnt, std::max<size_t>(cw, 1)));
     }
 
+    load_mark("planes + frontier uploads");
     // stable path filter: one bit per extended atom (or per 2^any_shift atoms)
     {
         int sh = 0;
@@ -482,6 +501,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(dalloc(p, &p->d_st_ring, 3 * ((size_t)L.n_ext + 1)));
     }
 
+    load_mark("stable buffers");
     CK(prepare_kernels(p->lm_smem, p->st_smem));
     const int bl = lm_full_blocks_per_sm(p->exact, p->lm_smem);
     const int bf = lm_frontier_blocks_per_sm();
@@ -534,6 +554,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         }
     }
     p->st_blocks = cap_grid(sms * bs);
+    load_mark("queues, occupancy");
     // one-cluster launches: the frontier and stable kernels of
     // programs small enough that 16 SMs carry a pass, with cluster barriers (~0.5 us) in
     // place of the 148-CTA grid barrier; the grid_blocks test hook keeps the grid
@@ -597,6 +618,7 @@ extern "C" lp_status lp_load(const lp_rules *rules, const lp_options *opt, lp_pr
     std::string err;
     lp_status s;
     try {
+        load_mark(nullptr);
         s = encode(rules, occ && p->device >= 0, &p->L, &err,
                    opt && (opt->flags & LP_LOAD_PAPER_LAYOUT));
     } catch (const std::bad_alloc &) {
@@ -607,6 +629,7 @@ extern "C" lp_status lp_load(const lp_rules *rules, const lp_options *opt, lp_pr
         delete p;
         return set_err(s, err);
     }
+    load_mark("encode (host)");
     if (p->device >= 0) {
         s = load_device(p, opt);
         if (s != LP_OK) {
