@@ -1969,12 +1969,6 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
                     cand |= (q < nq && sm_bit(rd, (uint32_t)av[e]) && !sm_bit(rd, (uint32_t)hv[e])) ? (1u << e) : 0u;
-                if (p.stage_planes) {   // every plane in shared memory: verify at once (no
-                                        // long-latency load to batch behind a queue)
-                    for (unsigned f = cand; f; f &= f - 1)
-                        cl_verify(p, segs, colg, reinterpret_cast<const int32_t *>(hb), rd, wr, q * 4 + __ffs(f) - 1);
-                    continue;
-                }
                 const unsigned any = __ballot_sync(0xFFFFFFFFu, cand != 0);
                 if (!any) continue;
                 const int c = __popc(cand);
