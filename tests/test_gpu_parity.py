@@ -768,3 +768,41 @@ def test_frontier_counters_across_calls(seed):
         model, iters, ex = prog.least_model(v0, frontier=True, popcounts=True, stages=True)
         assert iters == oit and (model == om).all() and ex["popcounts"] == opops
         assert (ex["stage"] == ostage).all()
+
+
+def _hub_chain(N, hubs=3, fan2=True):
+    """a0 (fact) -> {x_1..x_N} -> b -> {y_1..y_N} -> c -> ...: every other level one hub
+    atom's warp fires N rows in ONE CTA (its per-CTA frontier queue spills), and with fan2
+    the level after a fan-out also claims N atoms spread over all CTAs (w_i <- x_i)."""
+    rules, nxt = [(0, [])], 1
+    hub = 0
+    for _ in range(hubs):
+        fan = list(range(nxt, nxt + N))
+        nxt += N
+        rules += [(a, [hub]) for a in fan]
+        if fan2:
+            rules += [(nxt + i, [a]) for i, a in enumerate(fan)]
+            nxt += N
+        rules.append((nxt, fan[:3]))   # the next hub needs three of the fan-out atoms
+        hub = nxt
+        nxt += 1
+    return lpgen.from_lists(nxt, rules)
+
+
+@pytest.mark.parametrize("N,fan2", [(1500, False), (60000, True), (300000, True)])
+def test_frontier_spill_queues(N, fan2):
+    """Levels at which one CTA (a hub atom's fan-out) or every CTA (the next level) claims
+    more heads than its shared-memory frontier queue holds: the spill queue and the spill
+    field of the level barrier word (set and cleared on the same word two levels apart)."""
+    P = _hub_chain(N, hubs=3, fan2=fan2)
+    prog = check_lm(P, variants=(True,))
+    check_lm(P, variants=(True,), grid_blocks=7)
+    # capped runs: the model after c passes (the full θ-pass is the reference of the cap,
+    # pinned on chains by test_max_passes_cap) -- a spilled candidate of level c + 1 must
+    # not leak into it
+    oit = oracle.lm_stage(P)[2]
+    for c in range(1, oit + 2):
+        fm, fit, fex = prog.least_model(frontier=True, max_passes=c, popcounts=True)
+        gm, git, gex = prog.least_model(frontier=False, max_passes=c, popcounts=True)
+        assert fit == git == min(c, oit) and fex["converged"] == gex["converged"] == (c >= oit)
+        assert (fm == gm).all() and fex["popcounts"] == gex["popcounts"], c
