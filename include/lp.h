@@ -205,6 +205,10 @@ typedef struct {
     int32_t frontier_cluster_ctas; /* > 0: the frontier variant runs as ONE cluster of
                                  this many CTAs (cluster barriers); 0: the grid         */
     int32_t stable_cluster_ctas;   /* the same for lp_stable_models / lp_stable_search */
+    int32_t armed_list_cap;   /* > 0: LEAD passes of the full θ-pass are armed (rows whose
+                                 lead atom is true and head is not, kept per CTA in lists
+                                 of this many entries);
+                                 0: they stream the lead / head (or key) planes        */
 } lp_info_t;
 
 /* Validate, standardize and encode a program, upload it (PAPER.md:62, 82-95,

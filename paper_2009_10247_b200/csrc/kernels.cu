@@ -425,6 +425,53 @@ __device__ __forceinline__ int verify_slot(const LMParams &p, const PassCtx &c, 
     return loaded;
 }
 
+// Armed LEAD pass (exact mode): test one armed row -- its lead atom is in v_k -- against
+// v_k in shared memory from its 32-byte record (head, L, body positions 1..5, slot; longer
+// bodies read positions 6.. from the column planes).  A firing row's head is emitted.
+// Returns true if the row stays armed (head not in v_{k+1}: some body atom is still false).
+template <bool EXACT>
+__device__ __forceinline__ bool armed_verify(const LMParams &p, const PassCtx &c, int32_t o, int &loaded) {
+    const int4 r0 = __ldg(p.arec + 2 * (int64_t)o);
+    const int4 r1 = __ldg(p.arec + 2 * (int64_t)o + 1);
+    const int32_t h = r0.x, L = r0.y;
+    LP_CHECK(h >= 0 && h < p.n_ext_atoms && L >= 1);
+    const int32_t b[5] = {r0.z, r0.w, r1.x, r1.y, r1.z};
+    bool ok = true;
+    uint32_t hw;
+    if (EXACT) {   // v_k in shared memory
+        hw = c.sm[h >> 5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) ok = ok && (j + 1 >= L || sm_bit(c.sm, (uint32_t)b[j]));
+    } else {       // v_k in L2: the head's and the body atoms' words in one round trip
+        uint32_t w[5];
+        hw = __ldcg(c.rd + (h >> 5));
+#pragma unroll
+        for (int j = 0; j < 5; ++j) w[j] = j + 1 < L ? __ldcg(c.rd + (b[j] >> 5)) : ~0u;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) ok = ok && ((w[j] >> (b[j] & 31)) & 1u);
+    }
+    if ((hw >> (h & 31)) & 1u) return false;   // head in v_k: the row adds nothing, now or later
+    loaded += min(L, 6) - 1;
+    if (ok && L > 6) {   // positions 6.. of the row's segment
+        const int32_t slot = r1.w;
+        int lo = 0, hi = p.nseg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (c.segs[mid].slot_off <= slot) lo = mid; else hi = mid - 1;
+        }
+        const int64_t cp = c.segs[lo].count_pad;
+        const int32_t *colp = p.col + c.segs[lo].col_off + (slot - c.segs[lo].slot_off);
+        for (int32_t j = 6; j < L && ok; ++j) {
+            const uint32_t x = (uint32_t)__ldg(colp + (int64_t)j * cp);
+            ok = EXACT ? sm_bit(c.sm, x) : ((__ldcg(c.rd + (x >> 5)) >> (x & 31)) & 1u);
+        }
+        loaded += L - 6;
+    }
+    if (!ok) return true;
+    emit_head(p, c, h, hw);
+    return false;
+}
+
 // FILTER mode: rows that passed the summary test are queued and verified in the
 // pass epilogue with many independent L2 requests in flight, so the streaming loop
 // never waits on a dependent L2 round trip.
@@ -1316,6 +1363,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     __shared__ int32_t live_beg[kMaxRuns];          //   and this pass's live list
     __shared__ int32_t live_pre[kMaxRuns + 1];
     __shared__ int32_t live_tot;
+    __shared__ int32_t a_n[2];                      // armed LEAD passes: entries of the two lists
+    __shared__ int32_t a_over;                      //   and the pass's overflow flag
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
@@ -1347,7 +1396,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                            bytes - o < kChunk ? bytes - o : kChunk, &fill_bar);
         bulk_g2s_plain(bmask, p.init_ksum + p.ksm_words, bb, &fill_bar);
     }
-    lm_prologue(p, !EXACT, gtid, gthreads);            // v_0 (row a3), in-kernel
+    // (armed LEAD passes in summary mode keep no copy of v_k in shared memory: no summary)
+    lm_prologue(p, !EXACT && !(p.arec && starts_lead(p)), gtid, gthreads);   // v_0 (row a3), in-kernel
     if (gtid == 0) {
         p.cand[0] = 0;
         p.cand[1] = 0;
@@ -1375,14 +1425,22 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             __syncthreads();
             add_to_shared<EXACT>(p, sm, bmask, 0, n0, true);
         } else {
-            smem_fill(sm, EXACT ? p.buf0 : p.summary, p.sm_words);
+            if (EXACT || !(p.arec && lead_pass)) smem_fill(sm, EXACT ? p.buf0 : p.summary, p.sm_words);
         }
     }
     if (lead && p.pops && p.pop_cap > 0) p.pops[0] = n0;
     if (tid == 0) {
         qcount = 0;
         loaded_cta = 0;
+        a_n[0] = a_n[1] = 0;
+        a_over = 0;
     }
+    // armed LEAD passes (exact mode): every CTA keeps the rows
+    // it armed -- lead atom in v_k, head not in v_k -- in a shared-memory list after the
+    // truth words (two lists: the one verified and the one the survivors move to)
+    bool armed = p.arec != nullptr && lead_pass;   // (summary mode: the host passes no key plane then)
+    int acur = 0;
+    int32_t *const alist = reinterpret_cast<int32_t *>(sm + (EXACT ? p.sm_words : 0));
     if (keys) {   // the live runs of summary(v_0)
         __syncthreads();
         build_live(p, bmask, runs_sm, live_beg, live_pre, &live_tot);
@@ -1392,6 +1450,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8 + 7] = globaltimer();
 
     int32_t ds = n0, de = n0;  // atoms that became true in the previous pass
+    int32_t dprev = n0;        // (the ds before that: the Δ size the arming loads were sized by)
     int k_start = 0;
     bool rebuild = false;                                // key space -> atom-id summary
     // Predictive start (auto schedule, 16-bit key plane): the rows a first LEAD pass would
@@ -1425,6 +1484,9 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     }
     constexpr int kSpec = 4;
     uint32_t spec[kSpec];      // the next delta's first list entries, loaded with its count
+    // (armed LEAD passes) this thread's Δ entry to arm, i = de + block + G * tid, and its arm
+    // range: loaded right after the barrier beside the count (entries past it are ignored)
+    int32_t arm_a = -1, arm_lo = 0, arm_hi = 0;
     for (int k = k_start;; ++k) {
         const uint32_t *rd = (k & 1) ? p.buf1 : p.buf0;
         uint32_t *wr = (k & 1) ? p.buf0 : p.buf1;
@@ -1459,6 +1521,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                         }
                     }
                 }
+            } else if (!EXACT && armed && lead_pass) {
+                // (armed summary mode: no shared copy of v_k to bring up to date)
             } else if (EXACT || keys) {
                 // the first kSpec x blockDim entries were loaded right after the barrier
 #pragma unroll
@@ -1540,6 +1604,60 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             }
         }
         else if (!EXACT && keys) octets_lead(p, c, lv, gtid, gthreads);
+        else if (lead_pass && armed) {
+            // arm the rows led by the atoms that became true in the previous pass (pass 0: the
+            // atoms of v_0); Δ entry i is armed by CTA (i - a0) mod G.  A full list verifies a
+            // row at once and marks the pass: its survivors cannot be kept, so the next LEAD
+            // passes stream the planes instead (the count of rows queued carries the mark)
+            int32_t *const L0 = alist + (int64_t)acur * p.arm_cap;
+            int32_t *const L1 = alist + (int64_t)(acur ^ 1) * p.arm_cap;
+            auto arm = [&](int32_t lo, int32_t hi) {
+                if (hi <= lo) return;
+                int32_t pos = atomicAdd(&a_n[acur], hi - lo);
+                for (int32_t o = lo; o < hi; ++o, ++pos) {
+                    if (pos < p.arm_cap) {
+                        L0[pos] = o;
+                    } else {
+                        a_over = 1;
+                        armed_verify<EXACT>(p, c, o, loaded);
+                    }
+                }
+            };
+            // (measured: arming from the list entries already loaded for the fold, instead of
+            // loading them again here, was slower -- C3 7.81 vs 7.60 ms)
+            // Δ entry i is armed by thread (i - a0) / G of CTA (i - a0) mod G, which also ORs the
+            // atom into wr (the buffer that still holds v_{k-1}: see below)
+            {
+                const int32_t a0 = k == 0 ? 0 : ds, a1 = k == 0 ? n0 : de;
+                int64_t i = a0 + blockIdx.x + (int64_t)gridDim.x * tid;
+                if (k > 0 && tid <= 2 * ((ds - dprev) / (int32_t)gridDim.x) + 1) {   // the first entry
+                    if (i < a1) {                                                     // came with the barrier
+                        arm(arm_lo, arm_hi);
+                        atomicOr(wr + (arm_a >> 5), 1u << (arm_a & 31));
+                    }
+                    i += gthreads;
+                }
+                for (; i < a1; i += gthreads) {
+                    const int32_t a = __ldcg(p.order + i);
+                    arm(__ldg(p.arm_ptr + a), __ldg(p.arm_ptr + a + 1));
+                    if (k > 0) atomicOr(wr + (a >> 5), 1u << (a & 31));
+                }
+            }
+            __syncthreads();
+            const int32_t na = min(a_n[acur], p.arm_cap);
+            for (int32_t i = tid; i < na; i += blockDim.x) {
+                const int32_t o = L0[i];
+                if (armed_verify<EXACT>(p, c, o, loaded)) L1[atomicAdd(&a_n[acur ^ 1], 1)] = o;   // (< na)
+            }
+            __syncthreads();
+            if (tid == 0) {   // (the overflow mark: 2^40 on the pass's verified-entry count)
+                if (na) atomicAdd(p.cand + k % 3, na);
+                if (a_over) atomicAdd(p.vent + k % 3, 1ull << 40);
+                a_n[acur] = 0;
+                a_over = 0;
+            }
+            acur ^= 1;
+        }
         else if (EXACT && lead_pass && p.xlead16) octets_exact16<4>(p, c, gtid, gthreads);
         else if (EXACT && lead_pass && p.lead32) flat_lead_exact<4>(p, c, gtid, gthreads);
         else if (lead_pass) all_segments<EXACT, true>(p, c, gtid, gthreads);
@@ -1555,10 +1673,11 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         // of v_k before the barrier (nobody reads wr during pass k -- emit_head tests the
         // head against v_k first -- so this is off the critical path at the pass top);
         // spread over all CTAs
-        for (int64_t i = ds + (int64_t)tid * gridDim.x + blockIdx.x; i < de; i += gthreads) {
-            const int32_t a = __ldcg(p.order + i);
-            atomicOr(wr + (a >> 5), 1u << (a & 31));
-        }
+        if (!(lead_pass && armed))   // (an armed pass did it while arming)
+            for (int64_t i = ds + (int64_t)tid * gridDim.x + blockIdx.x; i < de; i += gthreads) {
+                const int32_t a = __ldcg(p.order + i);
+                atomicOr(wr + (a >> 5), 1u << (a & 31));
+            }
         if (!EXACT || lead_pass) {  // epilogue: verify this CTA's queued rows
             __syncthreads();
             const int32_t nc = min(qcount, p.qcap + kSmemQueue);
@@ -1599,6 +1718,22 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                 spec[u] = i < p.n_order_cap ? (uint32_t)__ldcg(lst + i) : 0u;
             }
         }
+        if (armed && lead_pass) {
+            {
+                // (only as many threads as twice the last Δ needs: the loads past the count
+                // are wasted L2 requests)
+                const int64_t i = de + blockIdx.x + (int64_t)gridDim.x * tid;
+                const bool want = tid <= 2 * ((de - ds) / (int32_t)gridDim.x) + 1;
+                arm_a = (want && i < p.n_order_cap) ? __ldcg(p.order + i) : -1;
+                if (arm_a >= 0 && arm_a < p.n_ext_atoms) {
+                    arm_lo = __ldg(p.arm_ptr + arm_a);
+                    arm_hi = __ldg(p.arm_ptr + arm_a + 1);
+                } else {
+                    arm_a = 0;   // (past the count: never used)
+                    arm_lo = arm_hi = 0;
+                }
+            }
+        }
         const PassCounts pcs = cta_pass_counts(p.pcnt + k % 3, p.cand + k % 3, p.vent + k % 3);
         const int32_t t = de + pcs.appended;
         const int32_t queued = pcs.queued;
@@ -1607,7 +1742,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             // and head the verification loaded, the delta list read twice and the truth
             // words it ORs
             // (STREAM passes added the int4 loads they issued themselves, atomically)
-            atomicAdd(p.stats + 0, (unsigned long long)(lead_pass && !keys ? p.lead_bytes : 0) +
+            atomicAdd(p.stats + 0, (unsigned long long)(lead_pass && !keys ? (armed ? 32ull * (unsigned long long)queued + 12ull * (unsigned long long)(k == 0 ? n0 : de - ds) : p.lead_bytes) : 0) +
                                        4ull * (unsigned long long)queued + 12ull * (unsigned long long)(t - de));
             if (lead_pass) atomicAdd(p.stats + 1, 1ull);   // (reductions: no load on the
             atomicAdd(p.stats + 2, (unsigned long long)queued);   //  lead thread's critical path)
@@ -1637,12 +1772,17 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         // the rows or whose verification loaded more than 1/8 of the entries a STREAM pass
         // reads (a verified entry costs a 32-byte sector, a streamed one 4 bytes)
         const unsigned long long vq = pcs.vent;
+        if (armed && vq >= (1ull << 40)) {   // a list overflowed: stream from now on (summary
+            armed = false;                   // mode: over the atom-id summary, built first)
+            if (!EXACT) rebuild = true;
+        }
         if (lead_pass && p.pass_mode == 0 &&
             ((int64_t)queued * p.dense_div > p.n_slots || (long long)vq * 8 > p.stream_entries)) {
             lead_pass = false;
-            rebuild = keys;
+            rebuild = keys || (!EXACT && armed) || rebuild;
             keys = false;
         }
+        dprev = ds;
         ds = de;
         de = t;
     }

@@ -125,6 +125,12 @@ struct LMParams {
                                //   16-bit codes) or << 13 (uint16, 8-bit codes)
     int32_t key_bits;          // 16 (default) or 8 (LP_LOAD_KEY8)
     const int32_t *lead32;     // exact mode: [n_slots] body position 0 of every slot (flat)
+    // exact mode, armed LEAD passes: rows by lead atom (arm_ptr[a] .. arm_ptr[a+1]) as
+    // records [2 x int4: (head, L, body 1, body 2), (body 3, body 4, body 5, slot)], and the
+    // capacity of each of the two per-CTA lists (shared memory after the truth words)
+    const int32_t *arm_ptr;
+    const int4 *arec;          // NULL: LEAD passes stream the lead / head planes
+    int32_t arm_cap;
     const uint16_t *xlead16;   // exact mode, ids < 2^21: low 16 bits of lead / head, and per
     const uint16_t *xhead16;   //   octet lead bucket | head bucket << 5 | padding << 10
     const uint16_t *xtag;

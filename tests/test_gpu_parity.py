@@ -65,7 +65,8 @@ def check_lm(P, v0=None, prog=None, variants=(False, True), jacobi=False,
             assert 0 <= st["lead_passes"] <= iters, (tag, st)
             assert st["lead_passes"] == {"stream": 0, "lead": iters}.get(schedule, st["lead_passes"])
             # (key-mode LEAD passes stream only the live runs: at most the whole plane)
-            assert st["bytes"] > 0 or prog.info["lead_pass_bytes"] == 0 or st["lead_passes"] == 0
+            assert st["bytes"] > 0 or prog.info["lead_pass_bytes"] == 0 or st["lead_passes"] == 0 \
+                or st["rows_verified"] == 0   # (armed LEAD passes with nothing armed read nothing)
         assert iters == oit, (tag, iters, oit)
         assert (model == om).all(), tag
         assert ex["popcounts"] == opops, tag
@@ -806,3 +807,27 @@ def test_frontier_spill_queues(N, fan2):
         gm, git, gex = prog.least_model(frontier=False, max_passes=c, popcounts=True)
         assert fit == git == min(c, oit) and fex["converged"] == gex["converged"] == (c >= oit)
         assert (fm == gm).all() and fex["popcounts"] == gex["popcounts"], c
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("env", [dict(LP_NO_ARMED="1"), dict(LP_ARMED_ALWAYS="1", LP_ARM_CAP="32"),
+                                 dict(LP_ARMED_ALWAYS="1")])
+def test_armed_lead_passes(seed, env, monkeypatch):
+    """Exact-mode LEAD passes with armed row lists (default), without them (the lead / head
+    planes streamed every pass), and with lists so small that they overflow mid-fixpoint
+    (the overflowing pass verifies the rest at once, later LEAD passes stream): all equal
+    the oracle -- model, pass count, popcounts, stages -- on every schedule."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng([seed, 7117])
+    n = int(rng.integers(200, 40000))
+    P = lpgen.random_program(rng, n, int(rng.integers(1, 8)) * n, max_len=int(rng.integers(2, 10)),
+                             n_facts=max(1, n // int(rng.integers(20, 400))))
+    check_lm(P, variants=(False,), grid_blocks=int(rng.choice([0, 3, 37])))
+    # summary mode (v_k in L2 while armed; an overflow switches to the atom-id summary)
+    check_lm(P, variants=(False,), smem_bits_cap=128)
+    check_lm(P, v0=rng.choice(n, size=n // 50 + 1, replace=False).tolist(), variants=(False,),
+             smem_bits_cap=1024)
+    L = lpgen.layered(120, 64, 120 * 64 * 3, 3, seed=seed)
+    check_lm(L, variants=(False,))
+    check_lm(L, variants=(False,), smem_bits_cap=256)
