@@ -35,7 +35,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-KERNEL_REV = "lead16-live-runs"   # bump when the dominant kernel's traffic changes
+KERNEL_REV = "armed-lead"   # bump when the dominant kernel's traffic changes
 METRIC = ("least-model fixpoint time & nnz·iter/s (HBM GB/s vs peak); "
           "stable-model guesses/s")
 
@@ -302,8 +302,9 @@ def main():
     hbm_peak, peak_src = _peaks()
     # Roofline of the dominant kernel (lm_full_kernel<false>, one launch = the fixpoint):
     #   achieved = SURVEY §8(d)'s algorithmic bytes (B_pass x passes) / kernel time, as the
-    #   contract defines it.  The LEAD schedule reads only the live runs' key codes (not
-    #   every CSR entry), so this exceeds the HBM peak: frac > 1 means the work skipped,
+    #   contract defines it.  Armed LEAD passes read only the records of the rows whose
+    #   lead atom is true (not every CSR entry), so this exceeds the HBM peak: frac > 1
+    #   means the work skipped,
     #   not a bandwidth.  Beside it: the bytes the kernel itself counted and the ncu DRAM
     #   bytes of one launch, each as a fraction of the peak.
     b_pass = _model_bytes_per_pass(info, n)
@@ -313,8 +314,8 @@ def main():
     traffic = _ncu_traffic(args.workload, iters)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic,
-                "binding": "latency: grid barriers and dependent L2 round trips per pass (the "
-                           "live-run LEAD stream is a small, L2-resident part of the key plane)",
+                "binding": "latency: grid barriers and dependent L2 round trips per pass (armed "
+                           "LEAD passes verify a few thousand rows per pass from their records)",
                 "model": "SURVEY §8(d) B_pass = 4 nnz + 4 (R+1) + 4 (H+1) + 2 ceil((n+1)/8), "
                          "x passes per launch",
                 "model_bytes_per_pass": b_pass, "model_bytes_per_launch": model_bytes,
@@ -455,16 +456,22 @@ def main():
               "v0": "facts ∪ 1% uniform random atoms (numpy seed 20251020)"}
         out["random_v0"] = rb
         del v0r, rmodel
-        # ---- the 8-bit key plane (LP_LOAD_KEY8) on the same workload -----------------------
-        prog8 = lp.Program(P, device=local, frontier=False, key8=True)
+        # ---- the same workload without armed LEAD passes (LP_NO_ARMED, read by lp_load):
+        # the LEAD passes stream the live runs of the 16-bit key plane -------------------
+        os.environ["LP_NO_ARMED"] = "1"
+        try:
+            prog8 = lp.Program(P, device=local, frontier=False)
+        finally:
+            del os.environ["LP_NO_ARMED"]
+        assert prog8.info["armed_list_cap"] == 0
         k8ms, k8k, k8it, k8b, _ = timed_least_model(prog8, args.steps, args.warmup)
         assert k8it == iters and (model.cpu().numpy().view(np.uint64) == main_model).all()
-        out["key8"] = {"ms_per_step": allmax(k8ms), "kernel_ms": allmax(k8k),
-                       "value": ws * nnz * iters / (allmax(k8ms) / 1e3), "unit": "nnz*iter/s",
-                       "kernel_bytes_per_launch": k8b,
-                       "lead_pass_bytes": int(prog8.info["lead_pass_bytes"]),
-                       "note": "8-bit key codes: too many bucket runs for the live-run table, "
-                               "so every LEAD pass streams the whole (L2-resident) plane"}
+        out["unarmed"] = {"ms_per_step": allmax(k8ms), "kernel_ms": allmax(k8k),
+                          "value": ws * nnz * iters / (allmax(k8ms) / 1e3), "unit": "nnz*iter/s",
+                          "kernel_bytes_per_launch": k8b,
+                          "lead_pass_bytes": int(prog8.info["lead_pass_bytes"]),
+                          "note": "LP_NO_ARMED: LEAD passes stream the live runs of the 16-bit key "
+                                  "plane (the round-2 path before armed passes)"}
         prog8.close()
 
         # ---- frontier variant on the same workload --------------------------------------
