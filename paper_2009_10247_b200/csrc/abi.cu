@@ -70,6 +70,9 @@ struct lp_program {
     // [12..14] rows queued per full θ-pass (slot k % 3); [16..18] least-model and
     // [20..22] stable per-pass append counters (slot k % 3)
     int32_t *d_scal = nullptr;
+    // host-pointer calls: iters and the status word written by the kernel's epilogue into
+    // page-locked mapped memory (no scalar copies after the launch); NULL if unavailable
+    int32_t *h_scal = nullptr, *h_scal_dev = nullptr;
     unsigned long long *d_stats = nullptr;  // full θ-pass work statistics (lp_run.stats_out)
     unsigned long long *d_vent = nullptr;   // [3] entries verified per pass (schedule)
     void *d_lead_codes = nullptr;   // summary-mode key plane (low key_bits bits of the lead group)
@@ -241,6 +244,19 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     TRY(dalloc(p, &p->d_buf1, p->nwords));
     TRY(dalloc(p, &p->d_order, (size_t)L.n_ext + 1));
     TRY(dalloc(p, &p->d_scal, 32));
+    {   // (best effort: without it host-pointer calls copy the scalars back)
+        void *h = nullptr;
+        if (cudaHostAlloc(&h, 64, cudaHostAllocMapped) == cudaSuccess) {
+            void *hd = nullptr;
+            if (cudaHostGetDevicePointer(&hd, h, 0) == cudaSuccess) {
+                p->h_scal = static_cast<int32_t *>(h);
+                p->h_scal_dev = static_cast<int32_t *>(hd);
+            } else {
+                cudaFreeHost(h);
+            }
+        }
+        cudaGetLastError();
+    }
     CK(cudaMemset(p->d_scal, 0, 32 * sizeof(int32_t)));
     TRY(dalloc(p, &p->d_stats, 6));
     TRY(dalloc(p, &p->d_vent, 3));
@@ -631,6 +647,8 @@ static void free_all(lp_program *p) {
         else cudaFree(a.first);
     }
     p->allocs.clear();
+    if (p->h_scal) cudaFreeHost(p->h_scal);
+    p->h_scal = p->h_scal_dev = nullptr;
 }
 
 extern "C" lp_status lp_load(const lp_rules *rules, const lp_options *opt, lp_program **out) {
@@ -835,7 +853,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.tail = p->d_scal + 8 + par;
     q.tail_next = p->d_scal + 8 + (par ^ 1);
     q.status_out = p->d_scal + 10 + par;
-    q.status_user = (dev && run) ? run->status_out : nullptr;
+    q.status_user = (dev && run) ? run->status_out : (!dev && p->h_scal_dev) ? p->h_scal_dev + 1 : nullptr;
     q.status_next = p->d_scal + 10 + (par ^ 1);
     q.v0 = v0d;
     q.v0_words = (int32_t)(mw * 2);
@@ -850,12 +868,13 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     unsigned long long *mout = dev ? reinterpret_cast<unsigned long long *>(model_out)
                                : mout_mapped ? reinterpret_cast<unsigned long long *>(mout_mapped) : p->d_model;
     q.model_out = mout;
+    q.model_split = (mout_mapped && !frontier) ? 1 : 0;
     q.out_w0 = w0;
     q.out_wn = ow;
     q.stage = stage;
     q.pops = pops;
     q.pop_cap = pop_cap;
-    q.iters_out = dev ? iters_out : p->d_scal + 1;
+    q.iters_out = dev ? iters_out : p->h_scal_dev ? p->h_scal_dev : p->d_scal + 1;
     q.max_passes = L.n_ext + 2;
     q.user_cap = (run && run->max_passes > 0) ? run->max_passes : 0;
     q.occ_ptr = p->d_occ_ptr;
@@ -929,8 +948,10 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     if (dev) return LP_OK;
 
     int32_t scal[3] = {0, 0, 0};
-    CK(cudaMemcpyAsync(scal, p->d_scal, sizeof(scal), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(scal + 2, p->d_scal + 10 + par, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (!p->h_scal) {
+        CK(cudaMemcpyAsync(scal, p->d_scal, sizeof(scal), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(scal + 2, p->d_scal + 10 + par, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    }
     if (ow && !mout_mapped) CK(cudaMemcpyAsync(model_out, p->d_model, (size_t)ow * 8, cudaMemcpyDeviceToHost, st));
     if (stage) CK(cudaMemcpyAsync(run->stage_out, stage, sizeof(int32_t) * (size_t)L.n_out,
                                   cudaMemcpyDeviceToHost, st));
@@ -939,6 +960,10 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     if (stats_dev)
         CK(cudaMemcpyAsync(run->stats_out, stats_dev, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (p->h_scal) {   // (written by the kernel's epilogue; visible once the stream is done)
+        scal[1] = reinterpret_cast<volatile int32_t *>(p->h_scal)[0];
+        scal[2] = reinterpret_cast<volatile int32_t *>(p->h_scal)[1];
+    }
     *iters_out = scal[1];
     if (run && run->status_out) *run->status_out = scal[2];
     if (run && run->converged_out) *run->converged_out = scal[2] == 0 ? 1 : 0;

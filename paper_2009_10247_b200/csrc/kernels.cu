@@ -190,6 +190,18 @@ __device__ __forceinline__ int32_t block_reserve(int32_t *tail, int32_t cnt) {
     return r;
 }
 
+constexpr int kSplitFencePass = 2;   // (see model_split in lm_full_kernel)
+
+// Model word i (original atoms 64i .. 64i+63) from its two 32-bit truth words, into the
+// output window (lp_run.out_word_lo / out_word_count).
+__device__ __forceinline__ void model_word_out(const LMParams &p, int64_t i, uint32_t lo, uint32_t hi) {
+    if (i < p.out_w0 || i >= p.out_w0 + p.out_wn) return;
+    unsigned long long v = (unsigned long long)lo | ((unsigned long long)hi << 32);
+    const int64_t a0 = i * 64;
+    if (a0 + 64 > p.n_out) v &= a0 >= p.n_out ? 0ull : (1ull << (uint32_t)(p.n_out - a0)) - 1ull;
+    p.model_out[i - p.out_w0] = v;
+}
+
 // In-kernel prologue of every least-model kernel (no separate init launches):
 //   v_0 word w = (v0[w] restricted to original atoms) | facts[w] | ⊤,
 // written to both buffers.  Warps walk consecutive truth words (coalesced); each lane
@@ -219,7 +231,13 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
             const int4 v = __ldg(ib + w);
             b0[w] = v;
             b1[w] = v;
+            if (p.model_split) {   // model words 2w, 2w+1 (original atoms only)
+                model_word_out(p, 2 * w, (uint32_t)v.x, (uint32_t)v.y);
+                model_word_out(p, 2 * w + 1, (uint32_t)v.z, (uint32_t)v.w);
+            }
         }
+        // (split model output: the system fence that orders these stores before the
+        // epilogue's comes passes later, see lm_full_kernel -- by then they are done)
         for (int64_t i = gtid; i < p.n_init; i += gthreads) {
             p.order[i] = __ldg(p.init_list + i);
             if (keys) p.korder[i] = __ldg(p.init_klist + i);
@@ -247,6 +265,10 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
             if (w == (p.top >> 5)) bits |= 1u << (p.top & 31);
             p.buf0[w] = bits;
             p.buf1[w] = bits;
+        }
+        if (p.model_split) {   // model word w/2 from this lane's and the next lane's originals
+            const uint32_t hi = __shfl_down_sync(0xFFFFFFFFu, orig, 1);
+            if (!(w & 1) && w < p.nwords) model_word_out(p, w >> 1, orig, (w + 1) < p.nwords ? hi : 0u);
         }
         int32_t pos = block_reserve(p.tail, __popc(orig));
         for (uint32_t b = orig; b;) {
@@ -295,7 +317,19 @@ __device__ __forceinline__ void lm_zero_summaries(const LMParams &p, bool summar
 // `v` = the buffer the last pass wrote (v_{k+1}: complete after its barrier; at a
 // fixpoint both buffers hold the model, after a capped pass only this one does).
 __device__ __noinline__ void lm_extract(const LMParams &p, int64_t gtid, int64_t gthreads,
-                                        const uint32_t *v_last) {
+                                        const uint32_t *v_last, int32_t d0 = 0, int32_t d1 = -1) {
+    // split mode (p.model_split, derivation list [d0, d1) given): the prologue wrote v_0's
+    // words; only the words holding atoms derived since are written (a word written several
+    // times gets the same final value each time)
+    if (p.model_split && d1 >= d0) {
+        for (int64_t i = d0 + gtid; i < d1; i += gthreads) {
+            const int32_t a = __ldcg(p.order + i);
+            if (a >= p.n_out) continue;
+            const int64_t w = a >> 6;
+            model_word_out(p, w, __ldcg(v_last + 2 * w), __ldcg(v_last + 2 * w + 1));
+        }
+        return;
+    }
     // (lp_run.out_word_lo / out_word_count: only model words [w0, w0 + nw) are written,
     // to model_out[0 .. nw) -- a head-range shard's owned words)
     const int64_t nw = p.out_wn;
@@ -1409,6 +1443,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     grid.sync();
     if (p.dbg && tid == 0) p.dbg[(2 * gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
     const int32_t n0 = cta_pass_counts(p.tail, nullptr, nullptr).appended;
+    __shared__ int32_t s_n0;   // (read again in the pass loop: not held in a register)
+    if (tid == 0) s_n0 = n0;
     {
         if (!ksum_image)
             for (int32_t w = tid; w < kBucketWords; w += blockDim.x) bmask[w] = 0u;
@@ -1628,7 +1664,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             // Δ entry i is armed by thread (i - a0) / G of CTA (i - a0) mod G, which also ORs the
             // atom into wr (the buffer that still holds v_{k-1}: see below)
             {
-                const int32_t a0 = k == 0 ? 0 : ds, a1 = k == 0 ? n0 : de;
+                const int32_t a0 = k == 0 ? 0 : ds, a1 = k == 0 ? s_n0 : de;
                 int64_t i = a0 + blockIdx.x + (int64_t)gridDim.x * tid;
                 if (k > 0 && tid <= 2 * ((ds - dprev) / (int32_t)gridDim.x) + 1) {   // the first entry
                     if (i < a1) {                                                     // came with the barrier
@@ -1702,6 +1738,11 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             if (p.stats) atomicAdd(p.stats + 3, loaded_cta);
             loaded_cta = 0;
         }
+        // split model output: the prologue's PCIe stores of v_0's words are ordered before
+        // the epilogue's stores of the same words by one system fence per CTA (cumulative
+        // over the CTA's stores after the block barrier above) at the end of pass 2 --
+        // by then they have long completed, so it costs nothing; shorter runs fence below
+        if (p.model_split && k == kSplitFencePass && tid == 0) __threadfence_system();
         grid.sync();
         if (p.dbg && tid == 0 && k < 16) DBG_STAMP(5) = globaltimer();
 #undef DBG_STAMP
@@ -1742,7 +1783,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             // and head the verification loaded, the delta list read twice and the truth
             // words it ORs
             // (STREAM passes added the int4 loads they issued themselves, atomically)
-            atomicAdd(p.stats + 0, (unsigned long long)(lead_pass && !keys ? (armed ? 32ull * (unsigned long long)queued + 12ull * (unsigned long long)(k == 0 ? n0 : de - ds) : p.lead_bytes) : 0) +
+            atomicAdd(p.stats + 0, (unsigned long long)(lead_pass && !keys ? (armed ? 32ull * (unsigned long long)queued + 12ull * (unsigned long long)(k == 0 ? s_n0 : de - ds) : p.lead_bytes) : 0) +
                                        4ull * (unsigned long long)queued + 12ull * (unsigned long long)(t - de));
             if (lead_pass) atomicAdd(p.stats + 1, 1ull);   // (reductions: no load on the
             atomicAdd(p.stats + 2, (unsigned long long)queued);   //  lead thread's critical path)
@@ -1760,7 +1801,11 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             }
             if (p.dbg && tid == 0) p.dbg[(gridDim.x + blockIdx.x) * 8 + 6] = globaltimer();
             lm_zero_summaries(p, !EXACT, gtid, gthreads);
-            lm_extract(p, gtid, gthreads, wr);
+            if (p.model_split && k < kSplitFencePass) {   // (the fence above did not run yet)
+                if (tid == 0) __threadfence_system();
+                grid.sync();
+            }
+            lm_extract(p, gtid, gthreads, wr, s_n0, t);
             if (p.dbg) {
                 __syncthreads();
                 if (tid == 0) p.dbg[(gridDim.x + blockIdx.x) * 8 + 7] = globaltimer();

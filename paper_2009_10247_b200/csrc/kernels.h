@@ -57,6 +57,9 @@ struct LMParams {
     int32_t n_init;
     int32_t top;               // ⊤
     unsigned long long *model_out;  // [out_wn] written by the epilogue: model words out_w0..
+    int32_t model_split;       // 1 (page-locked host model buffer): the prologue writes v_0's words
+                               //   (over PCIe, in the background of the passes), the epilogue
+                               //   only the words that hold derived atoms
     int64_t out_w0, out_wn;
     int32_t *tail_next;        // the other-parity run counters, zeroed for the next call
     int32_t *status_next;

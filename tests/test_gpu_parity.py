@@ -831,3 +831,44 @@ def test_armed_lead_passes(seed, env, monkeypatch):
     L = lpgen.layered(120, 64, 120 * 64 * 3, 3, seed=seed)
     check_lm(L, variants=(False,))
     check_lm(L, variants=(False,), smem_bits_cap=256)
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("armed", [False, True])
+def test_pinned_model_split_writes(seed, armed, monkeypatch):
+    """Page-locked host model buffer (bench.py's e2e path): the prologue writes v_0's words
+    over PCIe and the epilogue only the words holding derived atoms.  A buffer full of
+    garbage must come back as exactly the model -- with a start set (generic prologue),
+    an output window, a pass cap, exact and summary mode, armed and unarmed LEAD passes."""
+    import torch
+    if armed:
+        monkeypatch.setenv("LP_ARMED_ALWAYS", "1")
+    else:
+        monkeypatch.setenv("LP_NO_ARMED", "1")
+    rng = np.random.default_rng([seed, 4242])
+    n = int(rng.integers(300, 9000))
+    P = lpgen.random_program(rng, n, 4 * n, max_len=5, n_facts=max(1, n // 40))
+    W = lp.bits_words(n)
+    for kw in (dict(grid_blocks=5), dict(smem_bits_cap=128)):
+        prog = lp.Program(P, **kw)
+        for v0l in (None, rng.choice(n, size=n // 30 + 1, replace=False).tolist()):
+            om, _, oit = oracle.lm_stage(P, v0=v0l)
+            v0 = None
+            if v0l is not None:
+                mask = np.zeros(n, dtype=bool)
+                mask[v0l] = True
+                v0 = lp.pack_mask(mask)
+            want = oracle.pack_bits(om)
+            pinned = torch.full((W,), -1, dtype=torch.int64).pin_memory()
+            assert lp.lp_least_model(prog, v0, pinned) == oit
+            assert (pinned.numpy().view(np.uint64)[:W] == want).all()
+            lo, cnt = W // 3, max(1, W // 2)
+            win = torch.full((cnt,), -1, dtype=torch.int64).pin_memory()
+            assert lp.lp_least_model(prog, v0, win, out_words=(lo, cnt)) == oit
+            assert (win.numpy().view(np.uint64) == want[lo:lo + cnt]).all()
+            cap = max(1, oit // 2)
+            capped = torch.full((W,), -1, dtype=torch.int64).pin_memory()
+            ref = np.zeros(W, dtype=np.uint64)
+            assert lp.lp_least_model(prog, v0, capped, max_passes=cap) == lp.lp_least_model(prog, v0, ref, max_passes=cap)
+            assert (capped.numpy().view(np.uint64) == ref).all()
+        prog.close()
