@@ -1383,7 +1383,11 @@ __device__ __noinline__ bool lead_start_too_dense(const LMParams &p, const uint3
 // or a STREAM pass (every body position streamed; the test is complete in EXACT mode,
 // summary survivors are queued).  Both compute exactly θ(M v_k); the schedule only
 // decides which bytes are read (p.pass_mode).
-template <bool EXACT>
+// ARMED: the instantiation for calls whose LEAD passes are armed (LMParams.arec set, no key
+// plane): the key-space LEAD machinery (key summary, live runs, pipelined / overlapped
+// passes) compiles out, and with it its register pressure; the other instantiation keeps it
+// and drops the armed code.  Both run STREAM passes and plane-streaming LEAD passes.
+template <bool EXACT, bool ARMED>
 __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_constant__ LMParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t qcount;
@@ -1414,7 +1418,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     }
 
     bool lead_pass = starts_lead(p);
-    bool keys = !EXACT && p.lead_codes && lead_pass;         // shared copy is in key space
+    bool keys = !ARMED && !EXACT && p.lead_codes && lead_pass;   // shared copy is in key space
     // v_0 = facts: the key summary and bucket mask images built at load are bulk-copied in
     // while the prologue runs (waited for after its barrier)
     const bool ksum_image = keys && !p.v0 && p.init_ksum;
@@ -1431,7 +1435,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         bulk_g2s_plain(bmask, p.init_ksum + p.ksm_words, bb, &fill_bar);
     }
     // (armed LEAD passes in summary mode keep no copy of v_k in shared memory: no summary)
-    lm_prologue(p, !EXACT && !(p.arec && starts_lead(p)), gtid, gthreads);   // v_0 (row a3), in-kernel
+    lm_prologue(p, !EXACT && !(ARMED && p.arec && starts_lead(p)), gtid, gthreads);   // v_0 (row a3), in-kernel
     if (gtid == 0) {
         p.cand[0] = 0;
         p.cand[1] = 0;
@@ -1461,7 +1465,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             __syncthreads();
             add_to_shared<EXACT>(p, sm, bmask, 0, n0, true);
         } else {
-            if (EXACT || !(p.arec && lead_pass)) smem_fill(sm, EXACT ? p.buf0 : p.summary, p.sm_words);
+            if (EXACT || !(ARMED && p.arec && lead_pass)) smem_fill(sm, EXACT ? p.buf0 : p.summary, p.sm_words);
         }
     }
     if (lead && p.pops && p.pop_cap > 0) p.pops[0] = n0;
@@ -1474,7 +1478,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     // armed LEAD passes (exact mode): every CTA keeps the rows
     // it armed -- lead atom in v_k, head not in v_k -- in a shared-memory list after the
     // truth words (two lists: the one verified and the one the survivors move to)
-    bool armed = p.arec != nullptr && lead_pass;   // (summary mode: the host passes no key plane then)
+    bool armed = ARMED && p.arec != nullptr && lead_pass;   // (summary mode: the host passes no key plane then)
     int acur = 0;
     int32_t *const alist = reinterpret_cast<int32_t *>(sm + (EXACT ? p.sm_words : 0));
     if (keys) {   // the live runs of summary(v_0)
@@ -1836,11 +1840,10 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
 cudaError_t launch_lm_full(const LMParams &p, bool exact, int blocks, size_t smem, cudaStream_t st) {
     LMParams q = p;
     void *args[] = {(void *)&q};
-    if (exact)
-        return cudaLaunchCooperativeKernel((const void *)lm_full_kernel<true>, dim3(blocks),
-                                           dim3(kFullThreads), args, smem, st);
-    return cudaLaunchCooperativeKernel((const void *)lm_full_kernel<false>, dim3(blocks),
-                                       dim3(kFullThreads), args, smem, st);
+    const bool armed = p.arec != nullptr;
+    const void *k = exact ? (armed ? (const void *)lm_full_kernel<true, true> : (const void *)lm_full_kernel<true, false>)
+                          : (armed ? (const void *)lm_full_kernel<false, true> : (const void *)lm_full_kernel<false, false>);
+    return cudaLaunchCooperativeKernel(k, dim3(blocks), dim3(kFullThreads), args, smem, st);
 }
 
 // ------------------------------------------------------------------------------------
@@ -2906,12 +2909,10 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
     const int cap = std::max(kMaxSmemBytes, kKeySmemBytes);   // + static smem <= 227 KB
     (void)lm_smem;
     (void)st_smem;
-    if ((e = cudaFuncSetAttribute((const void *)lm_full_kernel<true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, cap)))
-        return e;
-    if ((e = cudaFuncSetAttribute((const void *)lm_full_kernel<false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, cap)))
-        return e;
+    const void *full[4] = {(const void *)lm_full_kernel<true, false>, (const void *)lm_full_kernel<false, false>,
+                           (const void *)lm_full_kernel<true, true>, (const void *)lm_full_kernel<false, true>};
+    for (const void *k : full)
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, cap))) return e;
     if ((e = cudaFuncSetAttribute((const void *)st_fixpoint_kernel<false>,   // (+ its static candidate queue)
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
         return e;
@@ -2929,11 +2930,14 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
 }
 
 int lm_full_blocks_per_sm(bool exact, size_t smem) {
-    int nb = 0;
+    int nb = 0, na = 0;   // (both instantiations run on the same grid)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, exact ? (const void *)lm_full_kernel<true> : (const void *)lm_full_kernel<false>,
+        &nb, exact ? (const void *)lm_full_kernel<true, false> : (const void *)lm_full_kernel<false, false>,
         kFullThreads, smem);
-    return nb;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &na, exact ? (const void *)lm_full_kernel<true, true> : (const void *)lm_full_kernel<false, true>,
+        kFullThreads, smem);
+    return std::min(nb, na);
 }
 
 int lm_frontier_blocks_per_sm() {
