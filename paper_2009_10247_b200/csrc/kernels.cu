@@ -1718,7 +1718,10 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                 const int32_t a = __ldcg(p.order + i);
                 atomicOr(wr + (a >> 5), 1u << (a & 31));
             }
-        if (!EXACT || lead_pass) {  // epilogue: verify this CTA's queued rows
+        if (lead_pass && armed) {   // (an armed pass queues nothing: only its verified entries)
+            for (int o = 16; o; o >>= 1) loaded += __shfl_xor_sync(0xFFFFFFFFu, loaded, o);
+            if ((tid & 31) == 0 && loaded) atomicAdd(&loaded_cta, (unsigned long long)loaded);
+        } else if (!EXACT || lead_pass) {  // epilogue: verify this CTA's queued rows
             __syncthreads();
             const int32_t nc = min(qcount, p.qcap + kSmemQueue);
             __syncthreads();
