@@ -75,6 +75,9 @@ struct lp_program {
     int32_t *h_scal = nullptr, *h_scal_dev = nullptr;
     unsigned long long *d_stats = nullptr;  // full θ-pass work statistics (lp_run.stats_out)
     unsigned long long *d_vent = nullptr;   // [3] entries verified per pass (schedule)
+    int32_t *d_cand = nullptr;   // [3] rows queued per full θ-pass (slot k % 3), on a line of
+                                 // its own: the pass's append counters (d_scal) are the line
+                                 // every CTA reads right after each barrier
     void *d_lead_codes = nullptr;   // summary-mode key plane (low key_bits bits of the lead group)
     void *d_octet_tag = nullptr;    // per-octet bucket | padding tags
     int key_bits = 16;
@@ -260,6 +263,8 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     CK(cudaMemset(p->d_scal, 0, 32 * sizeof(int32_t)));
     TRY(dalloc(p, &p->d_stats, 6));
     TRY(dalloc(p, &p->d_vent, 3));
+    TRY(dalloc(p, &p->d_cand, 32));
+    CK(cudaMemset(p->d_cand, 0, 32 * sizeof(int32_t)));
     {
         std::vector<uint32_t> fb((size_t)p->nwords, 0u);   // facts of P (Def. 4)
         for (int32_t a : L.facts) fb[(size_t)a >> 5] |= 1u << (a & 31);
@@ -883,13 +888,14 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.cnt = p->d_cnt;
     q.cnt_bits = p->cnt_bits;
     q.dbg = debug_timing();
+    q.dbg_clock = debug_clock();
     q.qbuf = p->d_qbuf;
     q.qcap = p->qcap;
     q.pass_mode = (flags & LP_FULL_STREAM) ? 2 : (flags & LP_FULL_LEAD) ? 1 : 0;
     q.dense_div = p->dense_div;
     q.predict = p->env_no_predict ? 0 : 1;
     q.n_slots = L.n_slots;
-    q.cand = p->d_scal + 12;
+    q.cand = p->d_cand;
     q.vent = p->d_vent;
     q.overlap = p->env_no_overlap ? 0 : 1;
     q.stage_planes = p->cluster_stage ? 1 : 0;
@@ -898,6 +904,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.locc_ptr = pipe ? p->d_locc_ptr : nullptr;
     q.locc_slot = p->d_locc_slot;
     q.pbar = reinterpret_cast<uint32_t *>(p->d_scal + 24);
+    q.lbar = reinterpret_cast<unsigned long long *>(p->d_scal + 28);   // (ints 28..31: 8-aligned)
     {
         long long ent = 0;
         for (const Segment &sg : L.segs) ent += (long long)sg.L * sg.count_pad;
@@ -1304,3 +1311,4 @@ extern "C" const char *lp_last_error(void) { return g_err.c_str(); }
 // CTA done, barrier exit) written by the next full
 // θ-pass launch; NULL disables.
 extern "C" void lpdbg_set_timing(void *buf) { set_debug_timing((unsigned long long *)buf); }
+extern "C" void lpdbg_set_clock(int on) { set_debug_clock(on); }

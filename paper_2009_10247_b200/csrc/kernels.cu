@@ -64,8 +64,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 static unsigned long long *g_dbg = nullptr;
+static int g_dbg_clock = 0;
 void set_debug_timing(unsigned long long *buf) { g_dbg = buf; }
 unsigned long long *debug_timing() { return g_dbg; }
+void set_debug_clock(int on) { g_dbg_clock = on; }
+int debug_clock() { return g_dbg_clock; }
 
 // The barrier between passes: the whole cooperative grid, or -- for kernels launched as ONE
 // thread-block cluster (small programs: DESIGN.md "Cluster launches") -- the cluster
@@ -218,6 +221,7 @@ __device__ __noinline__ void lm_prologue(const LMParams &p, bool summary_mode, i
         *p.status_next = 0;
         p.pcnt[0] = p.pcnt[1] = p.pcnt[2] = 0;
         if (p.pbar) *p.pbar = 0u;
+        if (p.lbar) p.lbar[0] = p.lbar[1] = 0ull;   // (read after the prologue's grid barrier)
     }
     const bool keys = summary_mode && p.lead_codes;
     const bool osum = summary_mode && !(keys && starts_lead(p));
@@ -359,6 +363,8 @@ struct PassCtx {
     int32_t *sq;            // the first kSmemQueue queue entries (shared memory), or NULL
     int32_t *pc;            // this pass's append counter (p.pcnt[k % 3])
     int32_t base;           // derivation-list index of this pass's first append
+    int32_t *sapp = nullptr;  // (armed kernel) this CTA's appends in the pass (shared memory):
+                              // the level barrier carries their sum, so no count is read back
 };
 
 // Queue entry i of this CTA: shared memory for the first kSmemQueue entries (no global
@@ -398,7 +404,10 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
     const unsigned m = __activemask();
     const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
     int32_t base = 0;
-    if (lane == leader) base = atomicAdd(c.pc, __popc(m));
+    if (lane == leader) {
+        base = atomicAdd(c.pc, __popc(m));
+        if (c.sapp) atomicAdd(c.sapp, __popc(m));
+    }
     base = __shfl_sync(m, base, leader);
     const int32_t pos = c.base + base + __popc(m & ((1u << lane) - 1u));
     LP_CHECK(pos >= 0 && pos <= p.n_order_cap && h >= 0 && h < p.n_ext_atoms);
@@ -1403,6 +1412,11 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     __shared__ int32_t live_tot;
     __shared__ int32_t a_n[2];                      // armed LEAD passes: entries of the two lists
     __shared__ int32_t a_over;                      //   and the pass's overflow flag
+    // (armed kernel) the pass barrier: this CTA's appends and overflow, what the barrier
+    // word returned (the pass's appends, overflowing CTAs) and the previous pass's
+    // schedule counts (loaded during this pass, one pass behind)
+    __shared__ int32_t s_app, s_overflowed, s_bar_app, s_bar_over, s_q;
+    __shared__ unsigned long long s_v;
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
@@ -1474,6 +1488,8 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         loaded_cta = 0;
         a_n[0] = a_n[1] = 0;
         a_over = 0;
+        s_app = s_overflowed = s_bar_app = s_bar_over = s_q = 0;
+        s_v = 0ull;
     }
     // armed LEAD passes (exact mode): every CTA keeps the rows
     // it armed -- lead atom in v_k, head not in v_k -- in a shared-memory list after the
@@ -1527,11 +1543,16 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
     // (armed LEAD passes) this thread's Δ entry to arm, i = de + block + G * tid, and its arm
     // range: loaded right after the barrier beside the count (entries past it are ignored)
     int32_t arm_a = -1, arm_lo = 0, arm_hi = 0;
+    __shared__ unsigned long long s_bprev[2];           // (armed kernel, thread 0) barrier words
+    if (tid == 0) s_bprev[0] = s_bprev[1] = 0ull;      //   (first read after several syncs)
+    int32_t lag_q = 0;                                  // (thread 0) the pass counts one pass behind
+    unsigned long long lag_v = 0ull;
     for (int k = k_start;; ++k) {
         const uint32_t *rd = (k & 1) ? p.buf1 : p.buf0;
         uint32_t *wr = (k & 1) ? p.buf0 : p.buf1;
 #define DBG_STAMP(i) p.dbg[(k * gridDim.x + blockIdx.x) * 8 + (i)]
-        if (p.dbg && tid == 0 && k < 16) DBG_STAMP(0) = globaltimer();
+#define DBG_NOW() (p.dbg_clock ? (unsigned long long)clock64() : globaltimer())
+        if (p.dbg && tid == 0 && k < 16) DBG_STAMP(0) = DBG_NOW();
         if (p.overlap && !EXACT) {   // empty shared queue for this pass (last reader: before the barrier)
             for (int32_t i = tid; i < kSmemQueue; i += blockDim.x) squeue[i] = -1;
             if (tid == 0) streamers_done = 0;
@@ -1569,7 +1590,9 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                 for (int u = 0; u < kSpec; ++u) {
                     const int32_t i = ds + tid + u * (int32_t)blockDim.x;
                     if (i < de) {
-                        const uint32_t g = EXACT ? spec[u] : (spec[u] >> p.kshift);
+                        // (an entry past the speculative bound was not loaded: load it now)
+                        const uint32_t e = spec[u] != 0xFFFFFFFFu ? spec[u] : (uint32_t)__ldcg((EXACT ? p.order : p.korder) + i);
+                        const uint32_t g = EXACT ? e : (e >> p.kshift);
                         atomicOr(sm + (g >> 5), 1u << (g & 31));
                         if (!EXACT && keys) {
                             const uint32_t bk = g >> p.key_bits;
@@ -1581,14 +1604,14 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             } else {
                 add_to_shared<EXACT>(p, sm, bmask, ds, de, keys);
             }
-            if (p.dbg && tid == 0 && k >= 3 && k < 16) DBG_STAMP(6) = globaltimer();
+            if (p.dbg && !armed && tid == 0 && k >= 3 && k < 16) DBG_STAMP(6) = globaltimer();
             __syncthreads();
             if (keys && lead_pass && s_bmask_changed) {   // the live runs of summary(v_k)
                 build_live(p, bmask, runs_sm, live_beg, live_pre, &live_tot);
                 __syncthreads();
                 if (tid == 0) s_bmask_changed = 0;   // (read again only after the next fold)
             }
-            if (p.dbg && tid == 0 && k >= 3 && k < 16) DBG_STAMP(7) = globaltimer();
+            if (p.dbg && !armed && tid == 0 && k >= 3 && k < 16) DBG_STAMP(7) = globaltimer();
         }
         const LiveList lv{live_beg, live_pre, live_tot};
         if (lead && p.stats && keys && lead_pass)   // the pass's streamed bytes: codes + tag per live octet
@@ -1601,8 +1624,9 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             p.pcnt[(k + 1) % 3] = 0;
         }
         const PassCtx c{rd, wr, sm, p.qbuf + (int64_t)blockIdx.x * p.qcap, &qcount, k, bmask,
-                        p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, p.pcnt + k % 3, de};
-        if (p.dbg && tid == 0 && k < 16) DBG_STAMP(1) = globaltimer();
+                        p.nseg <= kMaxSmemSegs ? ssegs : p.segs, squeue, p.pcnt + k % 3, de,
+                        ARMED ? &s_app : nullptr};
+        if (p.dbg && tid == 0 && k < 16) DBG_STAMP(1) = DBG_NOW();
         const int j0 = (EXACT && lead_pass) ? 1 : 0;
         int loaded = 0;
         // Overlapped LEAD pass: kStreamWarps warps stream, the others verify the shared
@@ -1683,16 +1707,22 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                     if (k > 0) atomicOr(wr + (a >> 5), 1u << (a & 31));
                 }
             }
+            if (p.dbg && k < 16 && (tid & 31) == 0) atomicMax(&DBG_STAMP(6), DBG_NOW());   // arming done
             __syncthreads();
+            if (p.dbg && tid == 0 && k < 16) DBG_STAMP(7) = DBG_NOW();   // verification starts
             const int32_t na = min(a_n[acur], p.arm_cap);
             for (int32_t i = tid; i < na; i += blockDim.x) {
                 const int32_t o = L0[i];
                 if (armed_verify<EXACT>(p, c, o, loaded)) L1[atomicAdd(&a_n[acur ^ 1], 1)] = o;   // (< na)
             }
             __syncthreads();
-            if (tid == 0) {   // (the overflow mark: 2^40 on the pass's verified-entry count)
+            if (tid == 0) {   // (the overflow mark: carried by the pass barrier)
                 if (na) atomicAdd(p.cand + k % 3, na);
-                if (a_over) atomicAdd(p.vent + k % 3, 1ull << 40);
+                if (a_over) s_overflowed = 1;
+                if (p.stats && na) {   // (this CTA's share: the counts reach the lead a pass late)
+                    atomicAdd(p.stats + 0, 36ull * (unsigned long long)na);   // record + its list entry
+                    atomicAdd(p.stats + 2, (unsigned long long)na);
+                }
                 a_n[acur] = 0;
                 a_over = 0;
             }
@@ -1708,7 +1738,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
                 if ((tid & 31) == 0 && sl) atomicAdd(p.stats + 0, 16ull * (unsigned long long)sl);
             }
         }
-        if (p.dbg && k < 16 && (tid & 31) == 0) atomicMax(&DBG_STAMP(2), globaltimer());
+        if (p.dbg && k < 16 && (tid & 31) == 0) atomicMax(&DBG_STAMP(2), DBG_NOW());
         // wr still holds v_{k-1}: add the atoms derived in pass k-1 so that it is a superset
         // of v_k before the barrier (nobody reads wr during pass k -- emit_head tests the
         // head against v_k first -- so this is off the critical path at the pass top);
@@ -1735,9 +1765,9 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             if ((tid & 31) == 0 && loaded) atomicAdd(&loaded_cta, (unsigned long long)loaded);
         }
         if (p.dbg && k < 16) {
-            if ((tid & 31) == 0) atomicMax(&DBG_STAMP(3), globaltimer());
+            if ((tid & 31) == 0) atomicMax(&DBG_STAMP(3), DBG_NOW());
             __syncthreads();
-            if (tid == 0) DBG_STAMP(4) = globaltimer();
+            if (tid == 0) DBG_STAMP(4) = DBG_NOW();
         }
         __syncthreads();
         if (tid == 0 && loaded_cta) {   // body entries the verification loaded (schedule + stats)
@@ -1750,9 +1780,39 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         // over the CTA's stores after the block barrier above) at the end of pass 2 --
         // by then they have long completed, so it costs nothing; shorter runs fence below
         if (p.model_split && k == kSplitFencePass && tid == 0) __threadfence_system();
-        grid.sync();
-        if (p.dbg && tid == 0 && k < 16) DBG_STAMP(5) = globaltimer();
+        if constexpr (ARMED) {
+            // The pass barrier of the armed kernel: one 64-bit reduction per CTA on the word
+            // of this pass's parity, [arrivals:24 | overflowing CTAs:8 | appends:32] (both
+            // fields only grow within a call, per word: differences to the word's last value
+            // are this pass's), released after the block barrier above (cumulative over the
+            // CTA's writes) and polled with acquire -- the pass's append count arrives with
+            // the barrier instead of being read back from the hot counter line after it.
+            if (tid == 0) {
+                unsigned long long add = (1ull << 40) | (unsigned long long)(uint32_t)s_app;
+                if (s_overflowed) add += 1ull << 32;
+                asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p.lbar + (k & 1)), "l"(add) : "memory");
+                const uint32_t target = (uint32_t)((((unsigned long long)(k / 2) + 1ull) * gridDim.x) & 0xFFFFFFull);
+                unsigned long long v;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p.lbar + (k & 1)) : "memory");
+                    if ((((uint32_t)(v >> 40) - target) & 0xFFFFFFu) < 0x800000u) break;
+                }
+                const unsigned long long pv = s_bprev[k & 1];
+                s_bar_app = (int32_t)((uint32_t)v - (uint32_t)pv);
+                s_bar_over = (int32_t)((((v >> 32) & 0xFFull) - ((pv >> 32) & 0xFFull)) & 0xFFull);
+                s_bprev[k & 1] = v;
+                s_app = 0;
+                s_overflowed = 0;
+                s_q = lag_q;    // the previous pass's counts, loaded during this one
+                s_v = lag_v;
+            }
+            __syncthreads();
+        } else {
+            grid.sync();
+        }
+        if (p.dbg && tid == 0 && k < 16) DBG_STAMP(5) = DBG_NOW();
 #undef DBG_STAMP
+#undef DBG_NOW
         // after the barrier: this pass's appends (a slot nobody touches again before the
         // next barrier -- the shared tail would race with the next pass's appends)
         if (EXACT || keys) {
@@ -1760,29 +1820,47 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             // instead of after it (one L2 round trip less before the next stream); slots at
             // or past the count are not used (the next pass may be appending there already)
             const int32_t *lst = EXACT ? p.order : p.korder;
+            // (speculative: only up to about twice the last delta -- every CTA loads the same
+            // entries, so loads past the count queue on the same L2 lines for nothing;
+            // 0xFFFFFFFF = not loaded)
+            const int32_t spec_n = 2 * (de - ds) + 256;
 #pragma unroll
             for (int u = 0; u < kSpec; ++u) {
-                const int32_t i = de + tid + u * (int32_t)blockDim.x;
-                spec[u] = i < p.n_order_cap ? (uint32_t)__ldcg(lst + i) : 0u;
+                const int32_t d = tid + u * (int32_t)blockDim.x;
+                const int32_t i = de + d;
+                spec[u] = (d < spec_n && i < p.n_order_cap) ? (uint32_t)__ldcg(lst + i) : 0xFFFFFFFFu;
             }
         }
         if (armed && lead_pass) {
-            {
-                // (only as many threads as twice the last Δ needs: the loads past the count
-                // are wasted L2 requests)
-                const int64_t i = de + blockIdx.x + (int64_t)gridDim.x * tid;
-                const bool want = tid <= 2 * ((de - ds) / (int32_t)gridDim.x) + 1;
-                arm_a = (want && i < p.n_order_cap) ? __ldcg(p.order + i) : -1;
-                if (arm_a >= 0 && arm_a < p.n_ext_atoms) {
-                    arm_lo = __ldg(p.arm_ptr + arm_a);
-                    arm_hi = __ldg(p.arm_ptr + arm_a + 1);
-                } else {
-                    arm_a = 0;   // (past the count: never used)
-                    arm_lo = arm_hi = 0;
-                }
+            // (only as many threads as twice the last Δ needs: the loads past the count are
+            // wasted L2 requests)
+            const int64_t i = de + blockIdx.x + (int64_t)gridDim.x * tid;
+            const bool want = tid <= 2 * ((de - ds) / (int32_t)gridDim.x) + 1;
+            arm_a = (want && i < p.n_order_cap) ? __ldcg(p.order + i) : -1;
+        }
+        // (the pass's counts are requested before anything waits on the entry above: both
+        // round trips overlap; the arm ranges below then overlap the Δ fold)
+        PassCounts pcs;
+        if constexpr (ARMED) {   // (the appends came with the barrier; the schedule counts lag)
+            pcs.appended = s_bar_app;
+            pcs.queued = s_q;
+            pcs.vent = s_v;
+            if (tid == 0) {
+                lag_q = __ldcg(p.cand + k % 3);
+                lag_v = __ldcg(p.vent + k % 3);
+            }
+        } else {
+            pcs = cta_pass_counts(p.pcnt + k % 3, p.cand + k % 3, p.vent + k % 3);
+        }
+        if (armed && lead_pass) {
+            if (arm_a >= 0 && arm_a < p.n_ext_atoms) {
+                arm_lo = __ldg(p.arm_ptr + arm_a);
+                arm_hi = __ldg(p.arm_ptr + arm_a + 1);
+            } else {
+                arm_a = 0;   // (past the count: never used)
+                arm_lo = arm_hi = 0;
             }
         }
-        const PassCounts pcs = cta_pass_counts(p.pcnt + k % 3, p.cand + k % 3, p.vent + k % 3);
         const int32_t t = de + pcs.appended;
         const int32_t queued = pcs.queued;
         if (lead && p.stats) {
@@ -1790,10 +1868,12 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             // and head the verification loaded, the delta list read twice and the truth
             // words it ORs
             // (STREAM passes added the int4 loads they issued themselves, atomically)
-            atomicAdd(p.stats + 0, (unsigned long long)(lead_pass && !keys ? (armed ? 32ull * (unsigned long long)queued + 12ull * (unsigned long long)(k == 0 ? s_n0 : de - ds) : p.lead_bytes) : 0) +
-                                       4ull * (unsigned long long)queued + 12ull * (unsigned long long)(t - de));
+            // (armed kernel: the verified rows were added by each CTA itself, see above)
+            const unsigned long long qd = ARMED ? 0ull : (unsigned long long)queued;
+            atomicAdd(p.stats + 0, (unsigned long long)(lead_pass && !keys ? (armed ? 12ull * (unsigned long long)(k == 0 ? s_n0 : de - ds) : p.lead_bytes) : 0) +
+                                       4ull * qd + 12ull * (unsigned long long)(t - de));
             if (lead_pass) atomicAdd(p.stats + 1, 1ull);   // (reductions: no load on the
-            atomicAdd(p.stats + 2, (unsigned long long)queued);   //  lead thread's critical path)
+            atomicAdd(p.stats + 2, qd);                     //  lead thread's critical path)
         }
         if (t == de || k + 1 >= p.max_passes || k + 1 == p.user_cap) {  // u = v: fixpoint (or a cap)
             if (lead) {
@@ -1824,7 +1904,7 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
         // the rows or whose verification loaded more than 1/8 of the entries a STREAM pass
         // reads (a verified entry costs a 32-byte sector, a streamed one 4 bytes)
         const unsigned long long vq = pcs.vent;
-        if (armed && vq >= (1ull << 40)) {   // a list overflowed: stream from now on (summary
+        if (armed && s_bar_over > 0) {   // a list overflowed: stream from now on (summary
             armed = false;                   // mode: over the atom-id summary, built first)
             if (!EXACT) rebuild = true;
         }

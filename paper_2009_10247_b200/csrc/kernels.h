@@ -88,6 +88,7 @@ struct LMParams {
     uint32_t *cnt;             // per-slot remaining-body counters
     int32_t cnt_bits;          // 4: nibbles, 8 per word; 8: bytes, 4 per word; 32: uint32
     unsigned long long *dbg;   // optional profiling timestamps (lpdbg_set_timing)
+    int32_t dbg_clock;         // ... as SM clock64 values instead of %globaltimer (lpdbg_set_clock)
     // FILTER mode: per-CTA candidate queues (rows that passed the summary test)
     int32_t *qbuf;             // [grid][qcap]
     int32_t qcap;
@@ -111,6 +112,7 @@ struct LMParams {
     const int32_t *locc_ptr;   // [n_ext + 1]
     const int32_t *locc_slot;  // [rows]: the slots whose body position 0 is atom a
     uint32_t *pbar;
+    unsigned long long *lbar;  // [2] (armed kernel) the pass barrier words, by pass parity
     int32_t *pcnt;             // [3] atoms appended to the derivation list per pass (slot
                                //     k % 3): read by every CTA after the pass's barrier,
                                //     never written again before the next one
@@ -151,6 +153,8 @@ struct LMParams {
 // profiling hook (not part of the ABI): per-CTA %globaltimer stamps
 void set_debug_timing(unsigned long long *buf);
 unsigned long long *debug_timing();
+void set_debug_clock(int on);
+int debug_clock();
 
 // Batched (bit-sliced) stable-model fixpoint.
 struct STParams {

@@ -134,6 +134,17 @@ __global__ void __launch_bounds__(1024, 1) bench(Args a) {
                 }
                 __syncthreads();
                 break;
+            case 10:   // cg grid.sync + every CTA's thread 0 reads one hot counter line after it
+            case 11:   // ... after each CTA's warps added to that line during the round
+                if (a.variant == 11 && (tid & 31) == 0) atomicAdd(a.ctr + 256, 1u);
+                grid.sync();
+                {
+                    __shared__ uint32_t sv;
+                    if (tid == 0) sv = __ldcg(a.ctr + 256) + __ldcg(a.ctr + 257) + __ldcg(a.ctr + 258);
+                    __syncthreads();
+                    acc += sv;
+                }
+                break;
             case 9:   // two-level: 4 sub-counters (by blockIdx % 4), last arriver of each adds to top
                 __syncthreads();
                 if (tid == 0) {
@@ -180,9 +191,9 @@ int main(int argc, char **argv) {
     for (int i = 0; i < chain_n; ++i) nxt[h[i]] = h[(i + 1) % chain_n];
     cudaMemcpy(chain, nxt.data(), chain_n * 4, cudaMemcpyHostToDevice);
     const char *names[] = {"cg grid.sync", "counter fence+atomicAdd", "counter red.release/ld.acquire",
-                           "flag array", "cluster8 + counter", "syncthreads only", "counter + nanosleep poll", "last arriver flag", "counter relaxed poll + fence", "two-level 4 counters"};
+                           "flag array", "cluster8 + counter", "syncthreads only", "counter + nanosleep poll", "last arriver flag", "counter relaxed poll + fence", "two-level 4 counters", "grid.sync + hot-line read", "grid.sync + atomics + hot-line read"};
     for (int links : {0, 1, 3}) {
-        for (int v = 0; v < 10; ++v) {
+        for (int v = 0; v < 12; ++v) {
             cudaMemset(ctr, 0, 512 * 4);
             cudaMemset(flags, 0, G * 32 * 4);
             Args a{ctr, flags, chain, chain_n, links, rounds, v, out, sink};
