@@ -97,6 +97,8 @@ struct lp_program {
     int32_t *d_arm_ptr = nullptr;
     int4 *d_arec = nullptr;
     int32_t arm_cap = 0;
+    int64_t n_records = 0;
+    int32_t st_arm_cap = 0;   // stable: records owned per CTA (0: the scan)
     int32_t n_init = 0;
     uint64_t lm_runs = 0;
     int32_t *d_facts = nullptr;
@@ -481,7 +483,9 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
     // (programs of >= 1 M rows, like the 16-bit planes: below that the plane stream is a few
     // microseconds per pass and measured no slower -- C2 0.095 vs 0.100 ms armed)
     // (summary mode: the lists take the shared memory a key summary would; v_k stays in L2)
-    if (!std::getenv("LP_NO_ARMED") && (L.n_slots >= (1 << 20) || std::getenv("LP_ARMED_ALWAYS"))) {
+    // (normal programs: for the stable kernel's armed passes)
+    if (!std::getenv("LP_NO_ARMED") &&
+        (L.n_slots >= (1 << 20) || std::getenv("LP_ARMED_ALWAYS") || !L.definite)) {
         int64_t lim = (int64_t)kKeySmemBytes - (p->exact ? 4 * (int64_t)p->sm_words : 0);
         int64_t cap = std::min<int64_t>(lim / 8, p->exact ? 8192 : 16384) / 32 * 32;
         if (const char *e = std::getenv("LP_ARM_CAP")) cap = std::min<int64_t>(cap, std::atoll(e));
@@ -508,8 +512,11 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
                 }
             TRY(upload(p, &p->d_arm_ptr, ap));
             TRY(upload(p, &p->d_arec, rec));
-            p->arm_cap = (int32_t)cap;
-            p->lm_smem = std::max(p->lm_smem, (p->exact ? (size_t)p->sm_words * 4 : 0) + 8 * (size_t)cap);
+            p->n_records = ap[(size_t)L.n_ext];
+            if (L.definite) {   // (least-model calls only run on definite programs)
+                p->arm_cap = (int32_t)cap;
+                p->lm_smem = std::max(p->lm_smem, (p->exact ? (size_t)p->sm_words * 4 : 0) + 8 * (size_t)cap);
+            }
         }
     }
     TRY(upload(p, &p->d_segs, L.segs));
@@ -559,6 +566,17 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         // + the "true in every guess" bits when the filter is exact and they fit
         p->st_full = sh == 0 && 2 * (int64_t)p->any_words * 4 <= cap;
         p->st_smem = (size_t)p->any_words * 4 * (p->st_full ? 2 : 1);
+        // armed stable passes: CTA b owns records [b * cap, (b + 1) * cap) -- two lists of
+        // cap (record, lead) pairs each after the filter bits (exact filter only)
+        if (p->d_arec && !L.definite && sh == 0) {
+            int64_t blocks = sms;
+            if (opt && opt->grid_blocks > 0) blocks = std::min<int64_t>(blocks, opt->grid_blocks);
+            const int64_t cap_st = ((p->n_records + blocks - 1) / blocks + 31) / 32 * 32;
+            if (p->st_smem + 16 * (size_t)cap_st <= (size_t)kMaxSmemBytes && !std::getenv("LP_NO_ARMED_STABLE")) {
+                p->st_arm_cap = (int32_t)std::max<int64_t>(cap_st, 32);
+                p->st_smem += 16 * (size_t)p->st_arm_cap;
+            }
+        }
         TRY(dalloc(p, &p->d_any, p->any_words));
         TRY(dalloc(p, &p->d_gfull, p->any_words));
         TRY(dalloc(p, &p->d_mark, (size_t)L.n_ext));
@@ -1035,6 +1053,12 @@ static STParams st_params(lp_program *p) {
     s.dbg = debug_timing();
     // the flat lead plane holds extended-atom ids: usable when the any-filter is exact
     s.lead32 = (p->any_shift == 0) ? p->d_lead32 : nullptr;
+    s.arm_ptr = p->d_arm_ptr;
+    s.arm_cap = p->st_arm_cap;
+    {   // (the ownership covers every record only if the launch has enough CTAs)
+        const int64_t blocks = p->st_cluster > 0 ? p->st_cluster : p->st_blocks;
+        s.arec = (p->st_arm_cap > 0 && blocks * (int64_t)p->st_arm_cap >= p->n_records) ? p->d_arec : nullptr;
+    }
     s.n_slots = L.n_slots;
     s.cta_queue = (L.n_slots < (1LL << 27) && L.segs.size() <= 32) ? 1 : 0;
     s.W = p->W;

@@ -2546,6 +2546,54 @@ __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int
     }
 }
 
+// st_row for an armed row given by its record o (head, L, body positions 1..5, slot) and
+// its lead atom a (body position 0): the same work without the head / body-id loads.
+// Bodies longer than 6 go through st_row (the slot's segment).
+__device__ __forceinline__ void st_row_rec(const STParams &p, int32_t o, int32_t a,
+                                           const unsigned long long *rd, unsigned long long *wr,
+                                           int k, int lane, int32_t *pc, int32_t base) {
+    const int4 r0 = __ldg(p.arec + 2 * (int64_t)o);
+    const int4 r1 = __ldg(p.arec + 2 * (int64_t)o + 1);
+    const int32_t h = r0.x, L = r0.y;
+    if (L > 6) {
+        const int32_t slot = r1.w;
+        int lo = 0, hi = p.nseg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(&p.segs[mid].slot_off) <= slot) lo = mid; else hi = mid - 1;
+        }
+        const Segment sg = p.segs[lo];
+        st_row(p, sg, slot - sg.slot_off, rd, wr, k, lane, pc, base);
+        return;
+    }
+    const int32_t b[6] = {a, L > 1 ? r0.z : -1, L > 2 ? r0.w : -1, L > 3 ? r1.x : -1,
+                          L > 4 ? r1.y : -1, L > 5 ? r1.z : -1};
+    bool changed = false;
+    for (int32_t w = 2 * lane; w < p.Wp; w += 64) {
+        const ulonglong2 hv = __ldcg(reinterpret_cast<const ulonglong2 *>(rd + (int64_t)h * p.Wp + w));
+        ulonglong2 r[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+            r[j] = b[j] >= 0 ? __ldcg(reinterpret_cast<const ulonglong2 *>(rd + (int64_t)b[j] * p.Wp + w))
+                             : make_ulonglong2(~0ull, ~0ull);
+        ulonglong2 acc = make_ulonglong2(~hv.x, ~hv.y);
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            acc.x &= r[j].x;
+            acc.y &= r[j].y;
+        }
+        if (acc.x) { atomicOr(wr + (int64_t)h * p.Wp + w, acc.x); changed = true; }
+        if (acc.y) { atomicOr(wr + (int64_t)h * p.Wp + w + 1, acc.y); changed = true; }
+    }
+    if (__any_sync(0xFFFFFFFFu, changed) && lane == 0) {
+        if (atomicExch(p.mark + h, k + 1) != k + 1) {
+            const int32_t pos = atomicAdd(pc, 1);
+            LP_CHECK(pos < p.ring_cap);
+            p.order[base + pos] = h;
+        }
+    }
+}
+
 // Algorithm 2: M_{k+1} = θ(M_P M_k) over all guess columns at
 // once, until no word changes.  Shared memory holds one "any guess" bit per extended
 // atom; a row whose body has an atom false in every guess is skipped after the bit
@@ -2560,6 +2608,31 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
     const int64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
     __shared__ uint32_t st_q[kStQueue];  // candidate rows of this CTA's scan: slot | segment << 27
     __shared__ int32_t st_qn, st_qover;
+    // armed passes (exact any-filter, records available):
+    // the rows whose lead atom is true in some guess and whose head is not true in every
+    // guess, as (record, lead) pairs in two shared-memory lists after the filter bits, and
+    // this pass's candidates among them
+    __shared__ int2 st_qa[kStQueueA];
+    __shared__ int32_t sa_n[2], sa_over, sa_qn;
+    bool armed = p.arec != nullptr && p.any_shift == 0;
+    int acur = 0;
+    int2 *const alist = reinterpret_cast<int2 *>(sm + p.any_words * (p.use_full ? 2 : 1));
+    if (threadIdx.x == 0) {
+        sa_n[0] = sa_n[1] = 0;
+        sa_over = 0;
+        sa_qn = 0;
+    }
+    // CTA b owns the records [b * arm_cap, (b + 1) * arm_cap) (the host sizes arm_cap so the
+    // grid covers all of them): an atom that became true in some guess arms the part of its
+    // record range this CTA owns, so a list never holds more than arm_cap entries
+    const int32_t own_lo = (int32_t)blockIdx.x * p.arm_cap, own_hi = own_lo + p.arm_cap;
+    auto st_arm = [&](int32_t a) {
+        const int32_t lo = max(__ldg(p.arm_ptr + a), own_lo), hi = min(__ldg(p.arm_ptr + a + 1), own_hi);
+        if (hi <= lo) return;
+        int32_t pos = atomicAdd(&sa_n[acur], hi - lo);
+        LP_CHECK(pos + (hi - lo) <= p.arm_cap);
+        for (int32_t o = lo; o < hi; ++o) alist[(int64_t)acur * p.arm_cap + pos++] = make_int2(o, a);
+    };
     // the call's set-up, in the same launch: the previous call's rows and this call's
     // counters cleared, then T_0 (Def. 8) and its "any" bits
     st_clear_phase(p, clear_rows, gtid, gthreads);
@@ -2575,6 +2648,14 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
         if (use_full) full[w] = 0u;
     }
     __syncthreads();
+    if (armed) {   // pass 0: the atoms true in some guess of T_0 (⊤, the facts, the guessed abar_j)
+        const int32_t rows = 1 + p.nfacts + p.k;
+        for (int32_t r = tid; r < rows; r += blockDim.x) {
+            const int32_t a = r == 0 ? p.top : r <= p.nfacts ? p.facts[r - 1] : p.negated_ext[r - 1 - p.nfacts];
+            if (sm_bit(sm, (uint32_t)a)) st_arm(a);
+        }
+        __syncthreads();
+    }
     // rows changed in pass k-1 and in pass k-2: counts, their lists in ring segments
     // (k-1) % 3 and (k-2) % 3 of p.order (pass k appends to segment k % 3)
     int32_t n1 = 0, n2 = 0;
@@ -2589,14 +2670,19 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
             const int32_t *l2 = p.order + (int64_t)((k + 1) % 3) * p.ring_cap;
             // (the first kStSpec x blockDim entries of both lists are in registers: loaded
             // with the count after the barrier)
+            // (armed: an atom whose bit was not set yet became true in some guess in pass
+            // k-1 -- every CTA sees the same, each arms the records of it that it owns)
             for (int u = 0; u < kStSpec; ++u)
                 if (s1[u] >= 0) {
                     const uint32_t g = (uint32_t)s1[u] >> p.any_shift;
-                    atomicOr(sm + (g >> 5), 1u << (g & 31));
+                    const uint32_t old = atomicOr(sm + (g >> 5), 1u << (g & 31));
+                    if (armed && !((old >> (g & 31)) & 1u)) st_arm(s1[u]);
                 }
             for (int64_t i = tid + kStSpec * blockDim.x; i < n1; i += blockDim.x) {
-                const uint32_t g = (uint32_t)__ldcg(l1 + i) >> p.any_shift;
-                atomicOr(sm + (g >> 5), 1u << (g & 31));
+                const int32_t a = __ldcg(l1 + i);
+                const uint32_t g = (uint32_t)a >> p.any_shift;
+                const uint32_t old = atomicOr(sm + (g >> 5), 1u << (g & 31));
+                if (armed && !((old >> (g & 31)) & 1u)) st_arm(a);
             }
             if (use_full) {   // the full marks made during pass k-1 (rows changed in pass k-2)
                 // (their gfull words were loaded right after the barrier, beside the list)
@@ -2616,11 +2702,75 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
         __syncthreads();
         if (p.dbg && tid == 0 && k < 64) atomicMax(p.dbg + 4 * k + 2, globaltimer());   // pass top done
         if (blockIdx.x == 0 && tid == 0) p.pcnt[(k + 1) % 3] = 0;   // next pass's counter
+        if (armed) {
+            // armed pass: every listed row is tested from its record -- its head not true in
+            // every guess (else dropped for good), its other body atoms true in some guess
+            // (then it is a candidate this pass) -- and kept; candidates are processed by
+            // every warp of the CTA like the scan's
+            const int32_t na = sa_n[acur];
+            const int2 *L0 = alist + (int64_t)acur * p.arm_cap;
+            int2 *L1 = alist + (int64_t)(acur ^ 1) * p.arm_cap;
+            for (int32_t i0 = tid - lane; i0 < na; i0 += blockDim.x) {   // (warp-uniform)
+                const int32_t i = i0 + lane;
+                int2 e = make_int2(-1, -1);
+                bool cand = false;
+                if (i < na) {
+                    e = L0[i];
+                    const int4 r0 = __ldg(p.arec + 2 * (int64_t)e.x);
+                    const int4 r1 = __ldg(p.arec + 2 * (int64_t)e.x + 1);
+                    const int32_t h = r0.x, L = r0.y;
+                    if (!(use_full && sm_bit(full, (uint32_t)h))) {
+                        L1[atomicAdd(&sa_n[acur ^ 1], 1)] = e;   // (kept: < na entries)
+                        const int32_t b[5] = {r0.z, r0.w, r1.x, r1.y, r1.z};
+                        cand = true;
+#pragma unroll
+                        for (int j = 0; j < 5; ++j) cand = cand && (j + 1 >= L || sm_bit(sm, (uint32_t)b[j]));
+                        if (cand && L > 6) {   // positions 6.. from the column planes
+                            const int32_t slot = r1.w;
+                            int lo = 0, hi = p.nseg - 1;
+                            while (lo < hi) {
+                                const int mid = (lo + hi + 1) >> 1;
+                                if (__ldg(&p.segs[mid].slot_off) <= slot) lo = mid; else hi = mid - 1;
+                            }
+                            const Segment sg = p.segs[lo];
+                            for (int32_t j = 6; j < L && cand; ++j)
+                                cand = sm_bit(sm, (uint32_t)__ldg(p.col + sg.col_off + (int64_t)j * sg.count_pad + (slot - sg.slot_off)));
+                        }
+                    }
+                }
+                if (p.dbg && cand) atomicAdd(p.dbg + 4 * (k & 63) + 1, 1ull);
+                bool over = false;
+                if (cand) {
+                    const int32_t pos = atomicAdd(&sa_qn, 1);
+                    if (pos < kStQueueA) st_qa[pos] = e;
+                    else over = true;
+                }
+                unsigned m = __ballot_sync(0xFFFFFFFFu, over);   // (rare) a full queue: this warp
+                while (m) {                                      // processes them itself
+                    const int l = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int32_t o = __shfl_sync(0xFFFFFFFFu, e.x, l), a = __shfl_sync(0xFFFFFFFFu, e.y, l);
+                    st_row_rec(p, o, a, rd, wr, k, lane, p.pcnt + k % 3, (k % 3) * p.ring_cap);
+                }
+            }
+            __syncthreads();
+            const int32_t nq_c = min(sa_qn, kStQueueA);
+            for (int32_t i = tid >> 5; i < nq_c; i += blockDim.x >> 5) {
+                const int2 e = st_qa[i];
+                st_row_rec(p, e.x, e.y, rd, wr, k, lane, p.pcnt + k % 3, (k % 3) * p.ring_cap);
+            }
+            __syncthreads();   // (the list counters: reset for the next pass)
+            if (tid == 0) {
+                sa_n[acur] = 0;
+                sa_qn = 0;
+            }
+            acur ^= 1;
+        }
         // candidate scan: a lane tests 4 rows (one 16-byte load per body position, lead
         // position first -- usually an atom that is true in no guess -- and the heads
         // against the "full" bits); the warp then processes the candidates one by one.
         // With the flat lead plane (exact mode) one loop covers every segment.
-        if (p.lead32) {
+        if (!armed && p.lead32) {
             const int64_t nq = p.n_slots >> 2;
             const int4 *lb = reinterpret_cast<const int4 *>(p.lead32);
             const int4 *hb = reinterpret_cast<const int4 *>(p.head);
@@ -2690,7 +2840,7 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
             }
         }
         int64_t off = 0;  // rotate each segment's first warp (see all_segments)
-        for (int32_t s = 0; s < (p.lead32 ? 0 : p.nseg); ++s) {
+        for (int32_t s = 0; s < ((armed || p.lead32) ? 0 : p.nseg); ++s) {
             const Segment sg = p.segs[s];
             const int64_t nq = sg.count_pad >> 2;
             const int64_t gw = gwarp >= off ? gwarp - off : gwarp - off + nwarps;

@@ -31,6 +31,7 @@ constexpr int kSmemQueue = 768;        // candidate queue entries kept in shared
 constexpr int kStreamWarps = LP_STREAM_WARPS;
 constexpr int kBucketWords = 256;
 constexpr int kStQueue = 2048;         // stable search: candidate rows queued per CTA and pass
+constexpr int kStQueueA = 1024;        // ... (record, lead) pairs in armed passes
 
 // Least-model fixpoint (full θ-pass and frontier variants).
 struct LMParams {
@@ -178,6 +179,11 @@ struct STParams {
     unsigned long long *dbg;   // optional [64][4]: barrier exit, candidate rows, last CTA's
                                //   pass-top done, last CTA's scan done (per pass)
     const int32_t *lead32;     // exact mode: flat lead plane (one scan loop), else NULL
+    // armed passes: rows by lead atom (arm_ptr) as 32-byte records (as LMParams); CTA b owns
+    // records [b * arm_cap, (b + 1) * arm_cap) (arec NULL: the scan)
+    const int32_t *arm_ptr;
+    const int4 *arec;
+    int32_t arm_cap;
     int32_t cta_queue;         // candidates shared by the CTA's warps (slots < 2^27, <= 32 segments)
     int64_t n_slots;
     int32_t W;                 // guess words in use (the rest of Wp is padding)
