@@ -1054,6 +1054,7 @@ static STParams st_params(lp_program *p) {
     // the flat lead plane holds extended-atom ids: usable when the any-filter is exact
     s.lead32 = (p->any_shift == 0) ? p->d_lead32 : nullptr;
     s.arm_ptr = p->d_arm_ptr;
+    s.lbar = reinterpret_cast<unsigned long long *>(p->d_scal + 28);
     s.arm_cap = p->st_arm_cap;
     {   // (the ownership covers every record only if the launch has enough CTAs)
         const int64_t blocks = p->st_cluster > 0 ? p->st_cluster : p->st_blocks;

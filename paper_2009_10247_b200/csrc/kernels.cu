@@ -2474,6 +2474,7 @@ __device__ void st_clear_phase(const STParams &p, int32_t clear_rows, int64_t gt
     if (gtid == 0) {
         *p.tail = 0;
         p.pcnt[0] = p.pcnt[1] = p.pcnt[2] = 0;
+        if (p.lbar) p.lbar[0] = p.lbar[1] = 0ull;   // (the pass barrier words; read after a grid barrier)
         *p.status_out = 0;
         *p.n_accepted = 0;
     }
@@ -2495,7 +2496,7 @@ __device__ void st_check_phase(const STParams &p, int64_t gtid, int64_t gthreads
 // two words (one 16-byte load per body atom).
 __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int64_t i,
                                        const unsigned long long *rd, unsigned long long *wr,
-                                       int k, int lane, int32_t *pc, int32_t base) {
+                                       int k, int lane, int32_t *pc, int32_t base, int32_t *sapp = nullptr) {
     // the head and the first kB body ids in one round trip, then the head row and those body
     // rows in a second one (independent loads in flight), then the new bits of the guesses
     // whose head is still false; positions past kB (long bodies) 4 at a time with the
@@ -2540,6 +2541,7 @@ __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int
         if (atomicExch(p.mark + h, k + 1) != k + 1) {
             // this pass's list (ring segment k % 3, its own counter)
             const int32_t pos = atomicAdd(pc, 1);
+            if (sapp) atomicAdd(sapp, 1);   // (the CTA's appends: carried by the pass barrier)
             LP_CHECK(pos < p.ring_cap);
             p.order[base + pos] = h;   // (mark[h] != 0 afterwards: the next call clears row h)
         }
@@ -2551,7 +2553,7 @@ __device__ __forceinline__ void st_row(const STParams &p, const Segment &sg, int
 // Bodies longer than 6 go through st_row (the slot's segment).
 __device__ __forceinline__ void st_row_rec(const STParams &p, int32_t o, int32_t a,
                                            const unsigned long long *rd, unsigned long long *wr,
-                                           int k, int lane, int32_t *pc, int32_t base) {
+                                           int k, int lane, int32_t *pc, int32_t base, int32_t *sapp) {
     const int4 r0 = __ldg(p.arec + 2 * (int64_t)o);
     const int4 r1 = __ldg(p.arec + 2 * (int64_t)o + 1);
     const int32_t h = r0.x, L = r0.y;
@@ -2563,7 +2565,7 @@ __device__ __forceinline__ void st_row_rec(const STParams &p, int32_t o, int32_t
             if (__ldg(&p.segs[mid].slot_off) <= slot) lo = mid; else hi = mid - 1;
         }
         const Segment sg = p.segs[lo];
-        st_row(p, sg, slot - sg.slot_off, rd, wr, k, lane, pc, base);
+        st_row(p, sg, slot - sg.slot_off, rd, wr, k, lane, pc, base, sapp);
         return;
     }
     const int32_t b[6] = {a, L > 1 ? r0.z : -1, L > 2 ? r0.w : -1, L > 3 ? r1.x : -1,
@@ -2588,6 +2590,7 @@ __device__ __forceinline__ void st_row_rec(const STParams &p, int32_t o, int32_t
     if (__any_sync(0xFFFFFFFFu, changed) && lane == 0) {
         if (atomicExch(p.mark + h, k + 1) != k + 1) {
             const int32_t pos = atomicAdd(pc, 1);
+            if (sapp) atomicAdd(sapp, 1);
             LP_CHECK(pos < p.ring_cap);
             p.order[base + pos] = h;
         }
@@ -2614,6 +2617,10 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
     // this pass's candidates among them
     __shared__ int2 st_qa[kStQueueA];
     __shared__ int32_t sa_n[2], sa_over, sa_qn;
+    // (grid launches) the pass barrier carries this CTA's appends: no count read back
+    __shared__ int32_t s_st_app, s_st_cnt;
+    __shared__ unsigned long long s_st_prev[2];
+    int32_t *const sapp = CL ? nullptr : &s_st_app;
     bool armed = p.arec != nullptr && p.any_shift == 0;
     int acur = 0;
     int2 *const alist = reinterpret_cast<int2 *>(sm + p.any_words * (p.use_full ? 2 : 1));
@@ -2621,6 +2628,8 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
         sa_n[0] = sa_n[1] = 0;
         sa_over = 0;
         sa_qn = 0;
+        s_st_app = 0;
+        s_st_prev[0] = s_st_prev[1] = 0ull;
     }
     // CTA b owns the records [b * arm_cap, (b + 1) * arm_cap) (the host sizes arm_cap so the
     // grid covers all of them): an atom that became true in some guess arms the part of its
@@ -2750,14 +2759,14 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
                     const int l = __ffs(m) - 1;
                     m &= m - 1;
                     const int32_t o = __shfl_sync(0xFFFFFFFFu, e.x, l), a = __shfl_sync(0xFFFFFFFFu, e.y, l);
-                    st_row_rec(p, o, a, rd, wr, k, lane, p.pcnt + k % 3, (k % 3) * p.ring_cap);
+                    st_row_rec(p, o, a, rd, wr, k, lane, p.pcnt + k % 3, (k % 3) * p.ring_cap, sapp);
                 }
             }
             __syncthreads();
             const int32_t nq_c = min(sa_qn, kStQueueA);
             for (int32_t i = tid >> 5; i < nq_c; i += blockDim.x >> 5) {
                 const int2 e = st_qa[i];
-                st_row_rec(p, e.x, e.y, rd, wr, k, lane, p.pcnt + k % 3, (k % 3) * p.ring_cap);
+                st_row_rec(p, e.x, e.y, rd, wr, k, lane, p.pcnt + k % 3, (k % 3) * p.ring_cap, sapp);
             }
             __syncthreads();   // (the list counters: reset for the next pass)
             if (tid == 0) {
@@ -2824,7 +2833,7 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
                             const int s = __shfl_sync(0xFFFFFFFFu, sgi, l);
                             const Segment sg = p.segs[s];
                             st_row(p, sg, (q0 + l) * 4 + e - sg.slot_off, rd, wr, k, lane, p.pcnt + k % 3,
-                                   (k % 3) * p.ring_cap);
+                                   (k % 3) * p.ring_cap, sapp);
                         }
                     }
                 }
@@ -2836,7 +2845,7 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
                 const uint32_t ent = st_q[i];
                 const Segment sg = p.segs[ent >> 27];
                 st_row(p, sg, (int64_t)(ent & 0x7FFFFFFu) - sg.slot_off, rd, wr, k, lane, p.pcnt + k % 3,
-                       (k % 3) * p.ring_cap);
+                       (k % 3) * p.ring_cap, sapp);
             }
         }
         int64_t off = 0;  // rotate each segment's first warp (see all_segments)
@@ -2875,7 +2884,7 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
                     while (m) {
                         const int l = __ffs(m) - 1;
                         m &= m - 1;
-                        st_row(p, sg, (q0 + l) * 4 + e, rd, wr, k, lane, p.pcnt + k % 3, (k % 3) * p.ring_cap);
+                        st_row(p, sg, (q0 + l) * 4 + e, rd, wr, k, lane, p.pcnt + k % 3, (k % 3) * p.ring_cap, sapp);
                     }
                 }
             }
@@ -2903,7 +2912,28 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
             __syncthreads();
             if (tid == 0) atomicMax(p.dbg + 4 * k + 3, globaltimer());     // CTA's scan done
         }
-        pass_barrier<CL>();
+        if constexpr (CL) {
+            pass_barrier<CL>();
+        } else {
+            // one 64-bit release-reduction per CTA on the word of this pass's parity:
+            // [arrivals:24 | - | appends:32], both growing within a call (differences to the
+            // word's last value are this pass's); polled with acquire
+            __syncthreads();
+            if (tid == 0) {
+                const unsigned long long add = (1ull << 40) | (unsigned long long)(uint32_t)s_st_app;
+                asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p.lbar + (k & 1)), "l"(add) : "memory");
+                const uint32_t target = (uint32_t)((((unsigned long long)(k / 2) + 1ull) * gridDim.x) & 0xFFFFFFull);
+                unsigned long long v;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p.lbar + (k & 1)) : "memory");
+                    if ((((uint32_t)(v >> 40) - target) & 0xFFFFFFu) < 0x800000u) break;
+                }
+                s_st_cnt = (int32_t)((uint32_t)v - (uint32_t)s_st_prev[k & 1]);
+                s_st_prev[k & 1] = v;
+                s_st_app = 0;
+            }
+            __syncthreads();
+        }
         // rows changed in this pass: its own counter slot (the next pass appends to
         // another one, so every CTA reads the same value after the barrier); this
         // thread's first entries of the list are loaded together with it (slots past the
@@ -2915,7 +2945,7 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
             nx[u] = i < p.ring_cap ? __ldcg(p.order + (int64_t)(k % 3) * p.ring_cap + i) : -1;
             fwn[u] = (use_full && s1[u] >= 0) ? __ldcg(p.gfull + (s1[u] >> 5)) : 0u;
         }
-        const int32_t cnt = cta_pass_counts(p.pcnt + k % 3, nullptr, nullptr).appended;
+        const int32_t cnt = CL ? cta_pass_counts(p.pcnt + k % 3, nullptr, nullptr).appended : s_st_cnt;
         const bool lead = blockIdx.x == 0 && tid == 0;
         if (p.dbg && lead && k < 64) p.dbg[4 * k] = globaltimer();   // profiling hook
         if (cnt == 0) {

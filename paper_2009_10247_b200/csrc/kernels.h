@@ -184,6 +184,7 @@ struct STParams {
     const int32_t *arm_ptr;
     const int4 *arec;
     int32_t arm_cap;
+    unsigned long long *lbar;  // [2] the pass barrier words (grid launches), by pass parity
     int32_t cta_queue;         // candidates shared by the CTA's warps (slots < 2^27, <= 32 segments)
     int64_t n_slots;
     int32_t W;                 // guess words in use (the rest of Wp is padding)
