@@ -2644,10 +2644,14 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
     };
     // the call's set-up, in the same launch: the previous call's rows and this call's
     // counters cleared, then T_0 (Def. 8) and its "any" bits
+    const bool dlead = p.dbg && blockIdx.x == 0 && threadIdx.x == 0;   // (phase stamps: dbg[252..255])
+    if (dlead) p.dbg[252] = globaltimer();
     st_clear_phase(p, clear_rows, gtid, gthreads);
     pass_barrier<CL>();
+    if (dlead) p.dbg[253] = globaltimer();
     st_init_phase(p, gtid, gthreads);
     pass_barrier<CL>();
+    if (dlead) p.dbg[254] = globaltimer();
     // shared memory: "true in some guess" bits, then (exact filter only) "true in every
     // guess" bits -- a row whose head is full can change nothing
     uint32_t *full = sm + p.any_words;
@@ -2965,6 +2969,7 @@ __device__ __forceinline__ void st_run(const STParams &p, int32_t clear_rows) {
         }
     }
     // both buffers hold the fixpoint (rows changed in the last pass were copied during it)
+    if (dlead) p.dbg[255] = globaltimer();
     st_check_phase(p, gtid, gthreads);
 }
 

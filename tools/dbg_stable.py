@@ -21,6 +21,9 @@ lib.lpdbg_set_timing(buf.data_ptr())
 ids, passes, _ = prog.stable_models()
 lib.lpdbg_set_timing(None)
 t = buf.cpu().numpy().reshape(64, 4).astype(np.float64)
+ph = t[63]
+print(f"phases: clear {(ph[1] - ph[0]) / 1e3:.1f} us, init {(ph[2] - ph[1]) / 1e3:.1f} us, "
+      f"fixpoint {(ph[3] - ph[2]) / 1e3:.1f} us (passes {passes}) -- stamps of CTA 0")
 # pass k runs from barrier exit of k-1 to barrier exit of k
 for k in range(1, passes):
     b0 = t[k - 1, 0]
