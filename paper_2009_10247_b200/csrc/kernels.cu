@@ -2050,14 +2050,15 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
 // Launch a kernel either cooperatively over `blocks` CTAs or as ONE cluster of `cluster` CTAs.
 template <class K>
 static cudaError_t launch_grid_or_cluster(K kernel_grid, K kernel_cluster, const void *param, size_t psize,
-                                          int blocks, int cluster, size_t smem, cudaStream_t st) {
+                                          int blocks, int cluster, size_t smem, cudaStream_t st,
+                                          int cl_threads = 0) {
     (void)psize;
     void *args[] = {const_cast<void *>(param)};
     if (cluster <= 0)
         return cudaLaunchCooperativeKernel((const void *)kernel_grid, dim3(blocks), dim3(kThreads), args, smem, st);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)cluster);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3((unsigned)(cl_threads > 0 ? cl_threads : kThreads));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -2073,7 +2074,7 @@ static cudaError_t launch_grid_or_cluster(K kernel_grid, K kernel_cluster, const
 cudaError_t launch_lm_frontier(const LMParams &p, int blocks, cudaStream_t st, int cluster) {
     LMParams q = p;
     return launch_grid_or_cluster(lm_frontier_kernel<false>, lm_frontier_kernel<true>, &q, sizeof(q), blocks,
-                                  cluster, 0, st);
+                                  cluster, 0, st, p.fr_cl_threads);
 }
 
 // ------------------------------------------------------------------------------------
@@ -2342,8 +2343,9 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
 
 cudaError_t launch_lm_cluster(const LMParams &p, int cluster, size_t smem, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
+    const int threads = p.cl_threads > 0 ? p.cl_threads : kThreads;
     cfg.gridDim = dim3((unsigned)cluster);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3((unsigned)threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -2353,7 +2355,7 @@ cudaError_t launch_lm_cluster(const LMParams &p, int cluster, size_t smem, cudaS
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if ((p.n_slots >> 2) <= 2LL * cluster * kThreads) return cudaLaunchKernelEx(&cfg, lm_cluster_kernel<1>, p);
+    if ((p.n_slots >> 2) <= 2LL * cluster * threads) return cudaLaunchKernelEx(&cfg, lm_cluster_kernel<1>, p);
     return cudaLaunchKernelEx(&cfg, lm_cluster_kernel<4>, p);
 }
 

@@ -106,6 +106,8 @@ struct LMParams {
     long long stream_entries;  // body entries (incl. padding) one STREAM pass reads
     int32_t auto_stream_first; // auto schedule starts with STREAM passes (long bodies)
     int32_t stage_planes;      // cluster kernel: lead / head / col planes copied to shared memory
+    int32_t cl_threads;        // cluster kernel: threads per CTA (0: kThreads)
+    int32_t fr_cl_threads;     // one-cluster frontier launches: threads per CTA (0: kThreads)
     int32_t overlap;           // LEAD passes verify while they stream (warp-specialised)
     long long overlap_min_bytes;  // ... when the pass streams at least this many bytes
     // pipelined key-mode LEAD passes (lm_pipe): rows by lead atom, and the counter of the
