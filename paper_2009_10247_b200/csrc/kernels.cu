@@ -2441,7 +2441,12 @@ __device__ void st_init_phase(const STParams &p, int64_t gtid, int64_t gthreads)
         }
         p.T0[(int64_t)row * p.Wp + w] = v;
         p.T1[(int64_t)row * p.Wp + w] = v;
-        if (v) {
+        // the row's "true in some guess" bit: one atomic per group of lanes on the same row
+        // (a row's Wp words are consecutive x: up to 32 lanes would hit one word)
+        const unsigned am = __activemask();
+        const unsigned same = __match_any_sync(am, row);
+        const bool any = __any_sync(same, v != 0ull);
+        if (any && (threadIdx.x & 31) == __ffs(same) - 1) {
             const uint32_t g = (uint32_t)row >> p.any_shift;
             atomicOr(p.any_rw + (g >> 5), 1u << (g & 31));
         }
