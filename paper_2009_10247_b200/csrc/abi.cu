@@ -62,6 +62,7 @@ struct lp_program {
     bool env_no_overlap = false;  // LP_NO_OVERLAP
     bool env_no_ksum_image = false;  // LP_NO_KSUM_IMAGE
     bool env_no_zerocopy = false;    // LP_NO_ZEROCOPY
+    bool env_no_prefetch = false;    // LP_NO_PREFETCH
     long long overlap_min_bytes = 16ll << 20;   // LP_OVERLAP_MIN_MB: overlapped / pipelined
                                                 // LEAD passes from this live stream size on
     // [0] tail, [2] status (stable path); [1] iters; [3] passes; [4,5] n_accepted;
@@ -705,6 +706,7 @@ extern "C" lp_status lp_load(const lp_rules *rules, const lp_options *opt, lp_pr
     p->env_no_overlap = std::getenv("LP_NO_OVERLAP") != nullptr;
     p->env_no_ksum_image = std::getenv("LP_NO_KSUM_IMAGE") != nullptr;
     p->env_no_zerocopy = std::getenv("LP_NO_ZEROCOPY") != nullptr;
+    p->env_no_prefetch = std::getenv("LP_NO_PREFETCH") != nullptr;
     if (const char *e = std::getenv("LP_OVERLAP_MIN_MB")) p->overlap_min_bytes = (long long)std::atoll(e) << 20;
     if (opt && opt->derivable && !(opt->flags & LP_LOAD_PAPER_LAYOUT)) p->L.deriv_hint = opt->derivable;
     const bool occ = !(opt && (opt->flags & LP_LOAD_NO_FRONTIER));
@@ -921,6 +923,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.pass_mode = (flags & LP_FULL_STREAM) ? 2 : (flags & LP_FULL_LEAD) ? 1 : 0;
     q.dense_div = p->dense_div;
     q.predict = p->env_no_predict ? 0 : 1;
+    q.prefetch = p->env_no_prefetch ? 0 : 1;
     q.n_slots = L.n_slots;
     q.cand = p->d_cand;
     q.vent = p->d_vent;

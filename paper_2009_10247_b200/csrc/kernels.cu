@@ -63,6 +63,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+// L2 prefetch (fire and forget): pulls a line that a later pass / level will load out of
+// HBM while the grid waits at its barrier.
+__device__ __forceinline__ void prefetch_l2(const void *ptr) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+}
+
 static unsigned long long *g_dbg = nullptr;
 static int g_dbg_clock = 0;
 void set_debug_timing(unsigned long long *buf) { g_dbg = buf; }
@@ -412,6 +418,8 @@ __device__ __forceinline__ void emit_head(const LMParams &p, const PassCtx &c, i
     const int32_t pos = c.base + base + __popc(m & ((1u << lane) - 1u));
     LP_CHECK(pos >= 0 && pos <= p.n_order_cap && h >= 0 && h < p.n_ext_atoms);
     p.order[pos] = h;
+    // (armed passes look up h's arm range next pass: its arm_ptr line toward L2 now)
+    if (p.prefetch && p.arec) prefetch_l2(p.arm_ptr + h);
     if (p.lead_codes) p.korder[pos] = hkey >= 0 ? hkey : __ldg(p.key_of + h);   // once per atom
     if (p.stage && h < p.n_out) p.stage[h] = c.k + 1;
 }
@@ -1677,6 +1685,10 @@ __global__ void __launch_bounds__(kFullThreads, 1) lm_full_kernel(const __grid_c
             int32_t *const L1 = alist + (int64_t)(acur ^ 1) * p.arm_cap;
             auto arm = [&](int32_t lo, int32_t hi) {
                 if (hi <= lo) return;
+                // (the records are verified after the block barrier below, by other threads:
+                // start their cold lines toward L2 now, 4 records per line, up to 8 lines)
+                if (p.prefetch)
+                    for (int32_t o = lo & ~3, n = 0; o < hi && n < 8; o += 4, ++n) prefetch_l2(p.arec + 2 * (int64_t)o);
                 int32_t pos = atomicAdd(&a_n[acur], hi - lo);
                 for (int32_t o = lo; o < hi; ++o, ++pos) {
                     if (pos < p.arm_cap) {
@@ -1997,6 +2009,10 @@ __global__ void __launch_bounds__(kThreads, 1) lm_frontier_kernel(const __grid_c
                     LP_CHECK(pos < p.n_order_cap && slot >= 0 && slot < p.n_slots);
                     fq0[(int64_t)((kk + 1) & 1) * p.n_order_cap + pos] = make_int4(h, e.z, e.w, 0);
                     if (p.stage && h < p.n_out) p.stage[h] = kk + 1;
+                    // h's occurrences are read at the next level, after the barrier: start
+                    // their (cold) lines toward L2 now (up to 8 lines = 64 occurrences)
+                    if (p.prefetch)
+                        for (int32_t o = e.z & ~7, n = 0; o < e.w && n < 8; o += 8, ++n) prefetch_l2(occ + o);
                 }
             }
         }

@@ -151,6 +151,7 @@ struct LMParams {
     int32_t *korder;           // [n_ext + 1] key of order[i] (written with it)
     int32_t ksm_words;         // words of the key-space summary (shared memory)
     int32_t kshift;
+    int32_t prefetch;          // L2 prefetch of what the next pass / level loads (LP_NO_PREFETCH: off)
 };
 
 // profiling hook (not part of the ABI): per-CTA %globaltimer stamps
