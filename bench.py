@@ -179,6 +179,24 @@ def _model_bytes_per_pass(info, n):
             + 2 * ((n + 1 + 7) // 8))
 
 
+def _model_bytes_per_pass_stable(info, n, W):
+    """SURVEY.md §8(d)'s batched form: B_pass = 4·nnz + 4·(R+1) + 4·(H+1) + 2·(n+1+k)·W·8
+    (the program, then the bit-sliced truth matrix read and written, W guess words per row)."""
+    return (4 * int(info["nnz"]) + 4 * (int(info["n_rules"]) + 1) + 4 * (int(info["n_heads"]) + 1)
+            + 2 * (n + 1 + int(info["n_negated"])) * W * 8)
+
+
+def _l2_peak():
+    """Measured L2 read bandwidth (tools/l2bw.cu, profiles/l2_peak.json): the denominator of
+    the L2-resident stable pass's roofline."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "l2_peak.json")) as f:
+            d = json.load(f)
+        return float(d["gbs"]), d.get("source", "profiles/l2_peak.json")
+    except Exception:  # noqa: BLE001
+        return None, None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -220,7 +238,11 @@ def main():
         return float(t.item())
 
     stream = torch.cuda.Stream()
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+    # L2 flush before every timed call: a 1 GiB write (8x the L2).  Its ~0.15 ms on the device
+    # also covers the host's launch path (ctypes marshalling + lp_least_model), which is
+    # issued while the fill runs: with a 256 MiB fill (~37 us) a slow host left the device
+    # idle between the step's start event and the kernel (0.134 vs 0.088 ms on one box)
+    flush = torch.empty(1024 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
 
     def flush_l2():
         with torch.cuda.stream(stream):
@@ -338,7 +360,7 @@ def main():
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": args.workload, "n_atoms": n, "n_rules": int(info["n_rules"]),
                    "nnz": nnz, "iters": iters, "variant": "full fused θ-pass (Algorithm 1)",
-                   "v0": "facts only", "l2": "flushed between steps (256 MiB write)",
+                   "v0": "facts only", "l2": "flushed between steps (1 GiB write)",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "truth_mode": "summary-in-smem" if info["truth_mode"] else "exact-in-smem",
                    "grid": [int(info["grid_blocks"]), int(info["block_threads"])]},
@@ -532,6 +554,20 @@ def main():
                   "accepted": int(nacc.item()), "n_negated": sprog.info["n_negated"],
                   "l2": "flushed between steps", "launches_per_call": 1,
                   "sharding": f"guesses over {ws} rank(s), slice time max over ranks"}
+        # roofline (SURVEY §8(d) batched form): C5's program and truth matrix (~112 MB)
+        # stay in the 126 MB L2 across the passes, so the bound is L2, against the measured
+        # L2 read bandwidth; ncu DRAM bytes of one call beside it
+        Wall = max((G_all + 63) // 64, 1)
+        sb = _model_bytes_per_pass_stable(sprog.info, S.n_atoms, Wall)
+        spasses = int(stable["passes"])
+        l2_gbs, l2_src = _l2_peak()
+        ach = sb * spasses / (stable["kernel_ms"] / 1e3) / 1e9
+        stable["roofline"] = {"bound": "l2", "unit": "GB/s", "model_bytes_per_pass": sb,
+                              "passes_per_launch": spasses, "achieved": ach, "peak": l2_gbs,
+                              "frac": (ach / l2_gbs) if l2_gbs else None, "peak_source": l2_src,
+                              "traffic": _ncu_traffic("C5_stable", spasses),
+                              "binding": "latency: grid barriers and dependent L2 round trips per pass "
+                                         "(armed passes touch only the candidate rows' guess words)"}
         if dist:
             ids, ps = stable_models_sharded(sprog, sprog.info["n_free_negated"])
             stable["accepted"], stable["passes"] = int(ids.size), ps
