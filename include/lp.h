@@ -209,6 +209,12 @@ typedef struct {
                                  lead atom is true and head is not, kept per CTA in lists
                                  of this many entries);
                                  0: they stream the lead / head (or key) planes        */
+    int32_t stable_compact_atoms; /* > 0: lp_stable_models runs the compact kernel: |A*|, the
+                                 atoms that can be true in some guess (the least model of P+
+                                 with every abar_j true, computed by lp_load), held with
+                                 the live rows in shared memory, a CTA per guess word
+                                 (DESIGN.md "Compact stable kernel"); 0: the batched kernel */
+    int32_t stable_compact_rows;  /* live rows (body within A*, head not a fact)        */
 } lp_info_t;
 
 /* Validate, standardize and encode a program, upload it (PAPER.md:62, 82-95,

@@ -69,7 +69,8 @@ struct lp_program {
     // [6] search rounds, [7] search passes (sum over rounds);
     // [8,9] least-model tails and [10,11] statuses, alternating by call parity;
     // [12..14] rows queued per full θ-pass (slot k % 3); [16..18] least-model and
-    // [20..22] stable per-pass append counters (slot k % 3)
+    // [20..22] stable per-pass append counters (slot k % 3); [26] compact stable kernel:
+    // CTAs finished (self-resetting)
     int32_t *d_scal = nullptr;
     // host-pointer calls: iters and the status word written by the kernel's epilogue into
     // page-locked mapped memory (no scalar copies after the launch); NULL if unavailable
@@ -125,6 +126,18 @@ struct lp_program {
     size_t acc_words_alloc = 0, guess_words_alloc = 0;
     unsigned long long *d_sguess = nullptr;   // lp_stable_search: the round's columns [k][W]
     size_t sguess_words_alloc = 0;
+    // compact stable kernel: the live sub-program
+    bool cp_ok = false;
+    int32_t cp_na = 0, cp_nr = 0, cp_nnz = 0, cp_n0 = 0, cp_blob16 = 0;
+    size_t cp_smem = 0;
+    uint4 *d_cp_blob = nullptr;
+    int32_t *d_cp_atom = nullptr, *d_cp_neg = nullptr, *d_cp_abar = nullptr;
+    int32_t *d_cp_pw = nullptr;
+    size_t cp_pw_alloc = 0;
+    unsigned long long *d_cp_C = nullptr;   // [W][na] the last compact call's fixpoint matrix over A*
+    size_t cp_C_alloc = 0;
+    bool st_last_compact = false;   // the last stable call ran the compact kernel (result in C) ...
+    bool cp_expanded = false;       // ... and C was scattered into T0 for a readback
 
     int cluster = 0;            // > 0: exact-mode program run by ONE cluster of this many CTAs
     int cl_threads = 0;         // ... with this many threads per CTA (0: kThreads; LP_CLUSTER_THREADS)
@@ -222,6 +235,133 @@ static void load_mark(const char *what) {
     const auto t = std::chrono::steady_clock::now();
     if (what) std::fprintf(stderr, "lp_load %-28s %8.3f s\n", what, std::chrono::duration<double>(t - t0).count());
     t0 = t;
+}
+
+// The live sub-program of a normal program for the compact stable kernel: A* = the least
+// model of P+ (Eq. 4) from the facts, ⊤ and EVERY abar_j -- P+ is definite, so A* contains
+// the least model of every guess (Def. 8 only takes abar_j away) -- by counter forward
+// chaining over the encoded rows; a row can fire in some guess only if its body lies in A*.
+// Kept (compact ids, ascending extended atom id; rows in slot order) when it fits the
+// kernel's shared memory next to the two column buffers; rows whose head is a fact or ⊤
+// (all ones from T_0 on) are dropped.
+static lp_status build_compact_stable(lp_program *p) {
+    const HostLayout &L = p->L;
+    const int32_t ne = L.n_ext;
+    std::vector<uint8_t> tr((size_t)ne, 0), ones((size_t)ne, 0);
+    std::vector<int32_t> queue;
+    auto set_true = [&](int32_t a) {
+        if (!tr[a]) { tr[a] = 1; queue.push_back(a); }
+    };
+    set_true(L.top);
+    ones[L.top] = 1;
+    for (int32_t a : L.facts) { set_true(a); ones[a] = 1; }
+    for (int32_t a : L.st_facts) { set_true(a); ones[a] = 1; }
+    for (int32_t j = 0; j < L.k; ++j) set_true(L.n + j);
+    // occurrence lists over the real slots (every body position)
+    std::vector<int64_t> optr((size_t)ne + 1, 0);
+    for (const Segment &sg : L.segs)
+        for (int32_t j = 0; j < sg.L; ++j)
+            for (int64_t i = 0; i < sg.count; ++i) ++optr[(size_t)L.col[sg.col_off + (int64_t)j * sg.count_pad + i] + 1];
+    for (int32_t a = 0; a < ne; ++a) optr[a + 1] += optr[a];
+    if (optr[ne] > INT32_MAX || L.n_slots > INT32_MAX) return LP_OK;   // (no compact kernel)
+    std::vector<int32_t> oslot((size_t)optr[ne]), cnt((size_t)L.n_slots, 0);
+    {
+        std::vector<int64_t> fill(optr.begin(), optr.end() - 1);
+        for (const Segment &sg : L.segs)
+            for (int64_t i = 0; i < sg.count; ++i) {
+                cnt[sg.slot_off + i] = sg.L;
+                for (int32_t j = 0; j < sg.L; ++j)
+                    oslot[(size_t)fill[L.col[sg.col_off + (int64_t)j * sg.count_pad + i]]++] = (int32_t)(sg.slot_off + i);
+            }
+    }
+    std::vector<uint8_t> live((size_t)L.n_slots, 0);
+    for (size_t qi = 0; qi < queue.size(); ++qi) {
+        const int32_t a = queue[qi];
+        for (int64_t o = optr[a]; o < optr[a + 1]; ++o) {
+            const int32_t s = oslot[(size_t)o];
+            if (--cnt[s] == 0) {
+                live[s] = 1;
+                set_true(L.head[s]);
+            }
+        }
+    }
+    std::vector<int32_t> cid((size_t)ne, -1), atom, init;
+    for (int32_t a = 0; a < ne; ++a)
+        if (tr[a]) {
+            cid[a] = (int32_t)atom.size();
+            atom.push_back(a);
+            init.push_back(ones[a] ? -2 : (a >= L.n && a < L.n + L.k) ? a - L.n : -1);
+        }
+    if (atom.size() > 65535 || L.k > 32767) return LP_OK;
+    const size_t na = atom.size();
+    std::vector<uint16_t> rptr(1, (uint16_t)0), rhead, rbody;
+    for (const Segment &sg : L.segs)
+        for (int64_t i = 0; i < sg.count; ++i) {
+            const int64_t s = sg.slot_off + i;
+            if (!live[s] || ones[L.head[s]]) continue;
+            if (rhead.size() >= 65535 || rbody.size() + (size_t)sg.L > 65535) return LP_OK;
+            rhead.push_back((uint16_t)cid[L.head[s]]);
+            for (int32_t j = 0; j < sg.L; ++j) {
+                const int32_t b = L.col[sg.col_off + (int64_t)j * sg.count_pad + i];
+                if (!ones[b]) rbody.push_back((uint16_t)cid[b]);   // (all-ones rows never mask a bit)
+            }
+            rptr.push_back((uint16_t)rbody.size());
+        }
+    const size_t nr = rhead.size(), nz = rbody.size();
+    // the transpose: the live rows in which compact atom c occurs
+    std::vector<uint16_t> cptr(na + 1, 0), crow(nz);
+    {
+        std::vector<uint32_t> c32(na + 1, 0u);
+        for (uint16_t b : rbody) ++c32[(size_t)b + 1];
+        for (size_t c = 0; c < na; ++c) c32[c + 1] += c32[c];
+        for (size_t c = 0; c <= na; ++c) cptr[c] = (uint16_t)c32[c];
+        for (size_t r = 0; r < nr; ++r)
+            for (uint32_t i = rptr[r]; i < rptr[r + 1]; ++i) crow[c32[rbody[i]]++] = (uint16_t)r;
+    }
+    // pass 0 can fire only rows whose remaining body atoms are abar atoms (T_0 is zero elsewhere)
+    std::vector<uint16_t> row0;
+    for (size_t r = 0; r < nr; ++r) {
+        bool ok = true;
+        for (uint32_t i = rptr[r]; i < rptr[r + 1] && ok; ++i) ok = init[rbody[i]] >= 0;
+        if (ok) row0.push_back((uint16_t)r);
+    }
+    const size_t n0 = row0.size();
+    const size_t blob_bytes = (2 * ((nr + 1) + nr + nz + (na + 1) + nz + na + n0) + 15) / 16 * 16;
+    const size_t smem = blob_bytes + 16 * na + 2 * (na + (na & 1)) + 4 * (nz + (nz & 1)) + 4 * ((na + 31) / 32);
+    if (smem > (size_t)kMaxSmemBytes) return LP_OK;
+    std::vector<uint4> blob(blob_bytes / 16, make_uint4(0, 0, 0, 0));
+    {
+        uint16_t *b = reinterpret_cast<uint16_t *>(blob.data());
+        auto put = [&](const void *src, size_t n16) {
+            if (n16) std::memcpy(b, src, 2 * n16);
+            b += n16;
+        };
+        put(rptr.data(), nr + 1);
+        put(rhead.data(), nr);
+        put(rbody.data(), nz);
+        put(cptr.data(), na + 1);
+        put(crow.data(), nz);
+        std::vector<int16_t> i16(init.begin(), init.end());
+        put(i16.data(), na);
+        put(row0.data(), n0);
+    }
+    std::vector<int32_t> cneg(L.k), cabar(L.k);
+    for (int32_t j = 0; j < L.k; ++j) {
+        cneg[j] = cid[L.negated[j]];
+        cabar[j] = cid[L.n + j];
+    }
+    TRY(upload(p, &p->d_cp_blob, blob));
+    TRY(upload(p, &p->d_cp_atom, atom));
+    TRY(upload(p, &p->d_cp_neg, cneg));
+    TRY(upload(p, &p->d_cp_abar, cabar));
+    p->cp_na = (int32_t)na;
+    p->cp_nr = (int32_t)nr;
+    p->cp_nnz = (int32_t)nz;
+    p->cp_n0 = (int32_t)n0;
+    p->cp_blob16 = (int32_t)(blob_bytes / 16);
+    p->cp_smem = smem;
+    p->cp_ok = true;
+    return LP_OK;
 }
 
 static lp_status load_device(lp_program *p, const lp_options *opt) {
@@ -586,6 +726,8 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         TRY(dalloc(p, &p->d_st_ring, 3 * ((size_t)L.n_ext + 1)));
     }
 
+    if (!L.definite && L.k > 0 && !std::getenv("LP_NO_COMPACT_STABLE")) TRY(build_compact_stable(p));
+
     load_mark("stable buffers");
     CK(prepare_kernels(p->lm_smem, p->st_smem));
     const int bl = lm_full_blocks_per_sm(p->exact, p->lm_smem);
@@ -775,6 +917,8 @@ extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
     o->frontier_cluster_ctas = p->fr_cluster;
     o->stable_cluster_ctas = p->st_cluster;
     o->armed_list_cap = p->arm_cap;
+    o->stable_compact_atoms = p->cp_ok ? p->cp_na : 0;
+    o->stable_compact_rows = p->cp_ok ? p->cp_nr : 0;
     return LP_OK;
 }
 
@@ -1039,6 +1183,8 @@ static lp_status st_matrix(lp_program *p, int64_t G) {
 // layout is unchanged (only the rows it changed), else both buffers zeroed here.
 static lp_status st_clear_plan(lp_program *p, cudaStream_t st, STParams *s) {
     const bool full_clear = !(p->st_dirty_ok && p->st_last_Wp == p->Wp);
+    p->st_last_compact = false;   // (a compact call leaves T alone; its expansion into T0 for
+                                  //  a readback resets st_dirty_ok)
     if (full_clear) {   // first call, or a new matrix layout: both buffers from zero
         const size_t tbytes = (size_t)p->L.n_ext * p->Wp * sizeof(unsigned long long);
         CK(cudaMemsetAsync(p->d_T0, 0, tbytes, st));
@@ -1090,6 +1236,34 @@ static STParams st_params(lp_program *p) {
     s.status_user = nullptr;
     s.max_passes = L.n_ext + 2;
     return s;
+}
+
+static void st_compact_params(lp_program *p, STParams *s) {
+    s->cp_blob = p->d_cp_blob;
+    s->cp_blob16 = p->cp_blob16;
+    s->cp_na = p->cp_na;
+    s->cp_nr = p->cp_nr;
+    s->cp_nnz = p->cp_nnz;
+    s->cp_n0 = p->cp_n0;
+    s->cp_atom = p->d_cp_atom;
+    s->cp_neg = p->d_cp_neg;
+    s->cp_abar = p->d_cp_abar;
+    s->cp_C = p->d_cp_C;
+    s->cp_pw = p->d_cp_pw;
+    s->cp_done = p->d_scal + 26;
+}
+
+// A compact call's result is the compact matrix C; the matrix / column readbacks read T0:
+// zero it and scatter C into it once (T then no longer holds a batched call's dirty rows).
+static lp_status st_expand_compact(lp_program *p, cudaStream_t st) {
+    if (!p->st_last_compact || p->cp_expanded) return LP_OK;
+    STParams s = st_params(p);
+    st_compact_params(p, &s);
+    CK(cudaMemsetAsync(p->d_T0, 0, (size_t)p->L.n_ext * p->Wp * sizeof(unsigned long long), st));
+    CK(launch_st_expand(s, st));
+    p->cp_expanded = true;
+    p->st_dirty_ok = false;
+    return LP_OK;
 }
 
 extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, int64_t n_guesses,
@@ -1150,7 +1324,6 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
     STParams s = st_params(p);
     if (dev) s.passes_out = passes_out;
     if (dev && run) s.status_user = run->status_out;
-    TRY(st_clear_plan(p, st, &s));
     s.n_atoms = L.n;
     s.k = L.k;
     s.negated = p->d_negated;
@@ -1164,9 +1337,31 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
     s.any_rw = p->d_any;
     s.accepted = acc;
     s.n_accepted = nacc;
+    if (p->cp_ok) {
+        // compact kernel: the live sub-program in shared memory, a CTA per guess word, one
+        // ordinary launch; the fixpoint matrix stays compact (C[w][A*]) until a readback
+        if ((size_t)W > p->cp_pw_alloc) {
+            if (p->d_cp_pw) dev_release(p, p->d_cp_pw);
+            TRY(dalloc(p, &p->d_cp_pw, (size_t)W));
+            p->cp_pw_alloc = W;
+        }
+        const size_t cw = (size_t)W * p->cp_na;
+        if (cw > p->cp_C_alloc) {
+            if (p->d_cp_C) dev_release(p, p->d_cp_C);
+            TRY(dalloc(p, &p->d_cp_C, cw));
+            p->cp_C_alloc = cw;
+        }
+        st_compact_params(p, &s);
+        p->st_last_compact = true;
+        p->cp_expanded = false;
+        if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
+        CK(launch_st_compact(s, std::max(1, std::min(W, p->sms)), p->cp_smem, st));
+    } else {
+    TRY(st_clear_plan(p, st, &s));
     // ONE cooperative launch: clear, T_0, the fixpoint loop, the stability check
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
     CK(launch_st_fused(s, p->st_blocks, p->st_smem, st, p->st_cluster));
+    }
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
     p->stable_valid = true;
     if (dev) return LP_OK;
@@ -1269,6 +1464,7 @@ extern "C" lp_status lp_stable_matrix(lp_program *p, uint64_t *out, const lp_run
     cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
     CK(cudaSetDevice(p->device));
     if (p->L.n_out == 0) return LP_OK;
+    TRY(st_expand_compact(p, st));
     CK(cudaMemcpy2DAsync(out, (size_t)p->W * 8, p->d_T0, (size_t)p->Wp * 8, (size_t)p->W * 8,
                          (size_t)p->L.n_out, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
     if (!dev) CK(cudaStreamSynchronize(st));
@@ -1284,6 +1480,7 @@ extern "C" lp_status lp_guess_model(lp_program *p, int64_t guess, uint64_t *mode
     const bool dev = run && (run->flags & LP_PTR_DEVICE);
     cudaStream_t st = run ? (cudaStream_t)run->stream : nullptr;
     CK(cudaSetDevice(p->device));
+    TRY(st_expand_compact(p, st));
     STParams s = st_params(p);
     unsigned long long *o = dev ? reinterpret_cast<unsigned long long *>(model_out) : p->d_model;
     CK(launch_st_column(s, p->L.n_out, guess, o, st));

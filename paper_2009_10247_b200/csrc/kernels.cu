@@ -3004,6 +3004,212 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
 }
 
 // ------------------------------------------------------------------------------------
+// stable models: compact kernel (the live sub-program in shared memory, a CTA per guess word)
+// ------------------------------------------------------------------------------------
+//
+// The guess columns of Algorithm 2 never interact: M_{k+1} = θ(M_P M_k)
+// acts on every column by itself.  A row of M_P can fire in SOME guess only if its whole body
+// lies in A*, the least model of P+ with every abar_j true (P+ is definite, so A* contains
+// every guess's model); lp_load computes A* once per program and keeps the live rows (body
+// ⊆ A*, head not a fact) in compact ids, with their transpose.  When that fits shared
+// memory, CTA w runs the whole Jacobi fixpoint of guess word w (64 columns) out of shared
+// memory -- block barriers only: no grid barrier, no global traffic inside the loop.  Pass 0
+// evaluates every live row; pass k > 0 only the rows with a body atom whose word changed in
+// pass k-1 (any other row computes the bits it computed before, already in its head).  The
+// CTA then stores its column of the fixpoint matrix over A* (rows outside A* are zero) into
+// the compact matrix C[w][A*] (lp_stable_matrix / lp_guess_model expand it), tests Algorithm
+// 3's condition and records the word's pass count; the last CTA to
+// finish reduces the accepted count and the pass count (max over words = the batched loop's
+// passes: a pass changes the matrix iff it changes some column).  Same T_k at every k as
+// the batched kernel: same matrix, accepted ids and passes (DESIGN.md "Compact stable
+// kernel").
+__global__ void __launch_bounds__(kThreads, 1) st_compact_kernel(const __grid_constant__ STParams p) {
+    extern __shared__ __align__(16) unsigned long long cpb[];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int32_t na = p.cp_na, nr = p.cp_nr, nnz = p.cp_nnz;
+    // blob (uint16 units): row_ptr[nr+1] | row head[nr] | body[nnz] | occ_ptr[na+1] |
+    // occ row[nnz] | init[na]; then the two column buffers, the change lists and their bitmap
+    uint4 *blob = reinterpret_cast<uint4 *>(cpb);
+    const uint16_t *rptr = reinterpret_cast<const uint16_t *>(blob);
+    const uint16_t *rhead = rptr + nr + 1;
+    const uint16_t *rbody = rhead + nr;
+    const uint16_t *optr = rbody + nnz;
+    const uint16_t *orow = optr + na + 1;
+    const int16_t *ainit = reinterpret_cast<const int16_t *>(orow + nnz);
+    const uint16_t *row0 = reinterpret_cast<const uint16_t *>(ainit + na);   // [n0] rows that can fire in pass 0
+    unsigned long long *cur = cpb + 2 * (int64_t)p.cp_blob16;
+    unsigned long long *nxt = cur + na;
+    uint16_t *la = reinterpret_cast<uint16_t *>(nxt + na);    // [na] rows of T changed in this pass
+    uint16_t *lr0 = la + na + (na & 1);                       // [nnz] x 2: the AND-rows to evaluate in
+    uint16_t *lr1 = lr0 + nnz + (nnz & 1);                    //   this pass / in the next one
+    uint32_t *inl = reinterpret_cast<uint32_t *>(lr1 + nnz + (nnz & 1));   // bit a: a is on la
+    __shared__ int32_t s_na[2], s_nr[2], s_last, s_mp;
+    __shared__ unsigned long long s_n;
+    const bool dl = p.dbg && blockIdx.x == 0 && tid == 0;   // (phase stamps: tools/dbg_compact.py)
+    if (dl) p.dbg[0] = globaltimer();
+    for (int32_t i = tid; i < p.cp_blob16; i += blockDim.x) blob[i] = __ldg(p.cp_blob + i);
+    // (Algorithm 3's pairs, compact ids: requested now, used after the fixpoint)
+    int32_t cneg = -1, cabar = -1;
+    if (tid < 32 && lane < p.k) {
+        cneg = __ldg(p.cp_neg + lane);
+        cabar = __ldg(p.cp_abar + lane);
+    }
+    if (tid == 0) s_na[0] = s_na[1] = s_nr[0] = s_nr[1] = 0;
+    for (int32_t i = tid; i < ((na + 31) >> 5); i += blockDim.x) inl[i] = 0u;
+    __syncthreads();
+    for (int32_t w = blockIdx.x; w < p.W; w += gridDim.x) {
+        const unsigned long long valid = valid_word(w, p.W, p.G);
+        // T_0 (Def. 8) on A*: ⊤ and the facts all ones, abar_j from the guesses
+        for (int32_t a = tid; a < na; a += blockDim.x) {
+            const int32_t ini = ainit[a];
+            unsigned long long v = 0ull;
+            if (ini == -2) v = valid;
+            else if (ini >= 0) {
+                if (p.guesses) v = __ldg(p.guesses + (int64_t)ini * p.W + w) & valid;
+                else {
+                    const int32_t rank = __ldg(p.free_rank + ini);
+                    v = rank < 0 ? 0ull : (count_pattern(rank, w + p.woff) & valid);
+                }
+            }
+            cur[a] = v;
+            nxt[a] = v;
+        }
+        __syncthreads();
+        if (dl) p.dbg[1] = globaltimer();
+        // one AND-row against T_k (cur): its new bits are ORed into T_{k+1} (nxt); at its
+        // head's first change in this pass the head goes onto the pass's change list (one
+        // counter atomic per group of converged lanes) and the rows it occurs in onto the
+        // next pass's row list (a row listed twice is evaluated twice: ORs are idempotent)
+        auto eval_row = [&](int32_t r, int k) {
+            const uint32_t h = rhead[r];
+            unsigned long long acc = valid & ~cur[h];
+            if (!acc) return;
+            const uint32_t e = rptr[r + 1];
+            for (uint32_t i = rptr[r]; i < e && acc; ++i) acc &= cur[rbody[i]];
+            if (!acc) return;
+            uint32_t *n32 = reinterpret_cast<uint32_t *>(nxt + h);
+            if ((uint32_t)acc) atomicOr(n32, (uint32_t)acc);
+            if ((uint32_t)(acc >> 32)) atomicOr(n32 + 1, (uint32_t)(acc >> 32));
+            const uint32_t bit = 1u << (h & 31);
+            if (atomicOr(inl + (h >> 5), bit) & bit) return;
+            const uint32_t o0 = optr[h], o1 = optr[h + 1];
+            cg::coalesced_group g = cg::coalesced_threads();
+            int32_t base = 0;
+            if (g.thread_rank() == 0) base = atomicAdd(&s_na[k & 1], (int32_t)g.size());
+            la[g.shfl(base, 0) + (int32_t)g.thread_rank()] = (uint16_t)h;
+            if (o1 > o0) {
+                uint16_t *dst = ((k & 1) ? lr0 : lr1) + atomicAdd(&s_nr[(k + 1) & 1], (int32_t)(o1 - o0));
+                for (uint32_t o = o0; o < o1; ++o) *dst++ = orow[o];
+            }
+        };
+        int32_t passes = 0;
+        for (int k = 0;; ++k) {
+            // pass 0: the rows whose body lies in T_0's possible atoms (the others hold an atom
+            // that is zero in every column of T_0); pass k: the rows with a body atom that
+            // changed in pass k-1 (any other row computes the bits it computed before,
+            // already in its head)
+            const uint16_t *rows = k == 0 ? row0 : ((k & 1) ? lr1 : lr0);
+            const int32_t nrow = k == 0 ? p.cp_n0 : s_nr[k & 1];
+            for (int32_t i = tid; i < nrow; i += blockDim.x) eval_row(rows[i], k);
+            __syncthreads();
+            ++passes;
+            const int32_t nn = s_na[k & 1];
+            if (dl && k < 60) {
+                p.dbg[8 + 2 * k] = globaltimer();
+                p.dbg[9 + 2 * k] = (unsigned long long)nrow;
+            }
+            if (nn == 0) break;   // u = v in every column of the word
+            // T_{k+1} for the changed rows; the bitmap and the counters of the pass after next
+            for (int32_t i = tid; i < nn; i += blockDim.x) {
+                const uint32_t h = la[i];
+                cur[h] = nxt[h];
+                inl[h >> 5] = 0u;   // (same-value stores race benignly)
+            }
+            if (tid == 0) {
+                s_na[(k + 1) & 1] = 0;
+                s_nr[k & 1] = 0;
+            }
+            __syncthreads();
+        }
+        if (dl) p.dbg[2] = globaltimer();
+        // the word's column of the fixpoint matrix over A* (cur = nxt at the fixpoint)
+        for (int32_t a = tid; a < na; a += blockDim.x) p.cp_C[(int64_t)w * na + a] = cur[a];
+        if (tid < 32) {   // Algorithm 3: a_j ∈ M ⟺ abar_j ∉ M for every j
+            unsigned long long ok = valid;
+            for (int32_t j = lane; j < p.k; j += 32) {
+                const int32_t ca = j < 32 ? cneg : __ldg(p.cp_neg + j), cb = j < 32 ? cabar : __ldg(p.cp_abar + j);
+                ok &= (ca >= 0 ? cur[ca] : 0ull) ^ (cb >= 0 ? cur[cb] : 0ull);
+            }
+            for (int o = 16; o; o >>= 1) ok &= __shfl_xor_sync(0xFFFFFFFFu, ok, o);
+            if (lane == 0) {
+                p.accepted[w] = ok;
+                p.cp_pw[w] = passes;
+            }
+        }
+        if (tid == 0) s_na[0] = s_na[1] = s_nr[0] = s_nr[1] = 0;
+        __syncthreads();   // (cur and the counters are rebuilt for the CTA's next word)
+        if (dl) p.dbg[3] = globaltimer();
+    }
+    // the last CTA to finish reduces the per-word results (fence + ticket)
+    if (tid == 0) {
+        s_mp = 0;
+        s_n = 0ull;
+        __threadfence();
+        s_last = atomicAdd(p.cp_done, 1) == (int32_t)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    long long n = 0;
+    int32_t mp = 0;
+    for (int32_t w = tid; w < p.W; w += blockDim.x) {
+        n += __popcll(__ldcg(p.accepted + w));
+        mp = max(mp, __ldcg(p.cp_pw + w));
+    }
+    for (int o = 16; o; o >>= 1) {
+        n += __shfl_xor_sync(0xFFFFFFFFu, n, o);
+        mp = max(mp, __shfl_xor_sync(0xFFFFFFFFu, mp, o));
+    }
+    if (lane == 0) {
+        if (n) atomicAdd(&s_n, (unsigned long long)n);
+        atomicMax(&s_mp, mp);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        *p.n_accepted = (long long)s_n;
+        *p.passes_out = s_mp;
+        *p.status_out = 0;
+        if (p.status_user) *p.status_user = 0;
+        *p.cp_done = 0;
+        if (p.dbg) p.dbg[4] = globaltimer();
+    }
+}
+
+cudaError_t launch_st_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
+    st_compact_kernel<<<blocks, kThreads, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+// The compact matrix C[w][A*] scattered into the (zeroed) matrix T0[n_ext][Wp] that
+// lp_stable_matrix / lp_guess_model read (a thread per (atom, word), words fastest).
+__global__ void st_expand_kernel(const unsigned long long *C, const int32_t *atom, int32_t na, int32_t W,
+                                 int32_t Wp, unsigned long long *T0) {
+    const int64_t total = (int64_t)na * W;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = x / W, w = x % W;
+        T0[(int64_t)__ldg(atom + a) * Wp + w] = C[w * na + a];
+    }
+}
+
+cudaError_t launch_st_expand(const STParams &p, cudaStream_t st) {
+    const int64_t total = (int64_t)p.cp_na * p.W;
+    if (total == 0) return cudaSuccess;
+    const int b = (int)std::min<int64_t>((total + 255) / 256, 8192);
+    st_expand_kernel<<<b, 256, 0, st>>>(p.cp_C, p.cp_atom, p.cp_na, p.W, p.Wp, p.T0);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
 // guess-space reduction: sampling + local search (reading R23)
 // ------------------------------------------------------------------------------------
 //
@@ -3213,6 +3419,9 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
         return e;
     if ((e = cudaFuncSetAttribute((const void *)st_search_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
+        return e;
+    if ((e = cudaFuncSetAttribute((const void *)st_compact_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
         return e;
     // the one-cluster launches of the same kernels (16 CTAs: a non-portable cluster size)

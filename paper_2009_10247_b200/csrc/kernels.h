@@ -220,6 +220,21 @@ struct STParams {
     int32_t max_rounds;
     int32_t *rounds_out;
     int32_t *passes_sum_out;            // whole-matrix passes summed over the rounds
+    // compact kernel (st_compact_kernel): the live
+    // sub-program -- the rows that can fire in some guess, over the atoms A* that can be true
+    // in some guess (the closure of the facts with every abar_j true, computed by lp_load)
+    // -- as one blob of uint16: row_ptr (nr+1) | row head (nr) | body (nnz) | occ_ptr
+    // (na+1) | occ row (nnz) | init (na: -1 zero in T_0, -2 all ones, j >= 0 abar_j) | the
+    // rows whose (compact) body holds abar atoms only: all that can fire in pass 0 (n0)
+    const uint4 *cp_blob;
+    int32_t cp_blob16;                  // its size in 16-byte units
+    int32_t cp_na, cp_nr, cp_nnz, cp_n0;  // atoms of A*, live rows, their body entries, pass-0 rows
+    const int32_t *cp_atom;             // [na] extended atom id of compact atom c
+    const int32_t *cp_neg;              // [k] compact id of a_j (-1: not in A*, never true)
+    const int32_t *cp_abar;             // [k] compact id of abar_j
+    unsigned long long *cp_C;           // [W][na] the fixpoint matrix over A*, word-major
+    int32_t *cp_pw;                     // [W] passes of each guess word
+    int32_t *cp_done;                   // CTAs finished (self-resetting; the last one reduces)
 };
 
 // Multi-GPU exchange step (lp_shard_combine).
@@ -254,6 +269,11 @@ int lm_cluster_max(int want, size_t smem);
 // One cooperative launch per stable call: clear the previous call's rows, build T_0, the
 // fixpoint loop, the stability check.
 cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st, int cluster);
+// The same call on the live sub-program held in shared memory, a CTA per guess word (no
+// grid barrier: an ordinary launch).
+cudaError_t launch_st_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st);
+// ... and its compact matrix C scattered into the zeroed T0 (for the matrix / column readback)
+cudaError_t launch_st_expand(const STParams &p, cudaStream_t st);
 // Guess-space reduction: all rounds of sampling + local search in one cooperative launch.
 cudaError_t launch_st_search(const STParams &p, int blocks, size_t smem, cudaStream_t st, int cluster);
 cudaError_t launch_st_column(const STParams &p, int32_t n, int64_t g, unsigned long long *out,

@@ -23,3 +23,13 @@ def _build_oracle():
 def _build_library():
     from paper_2009_10247_b200 import build
     build.build()
+
+
+@pytest.fixture(params=["compact", "batched"])
+def stable_kernel(request, monkeypatch):
+    """lp_stable_models on both device paths: the compact kernel (live sub-program in shared
+    memory, the default when it fits) and the batched persistent kernel
+    (LP_NO_COMPACT_STABLE, read by lp_load)."""
+    if request.param == "batched":
+        monkeypatch.setenv("LP_NO_COMPACT_STABLE", "1")
+    return request.param

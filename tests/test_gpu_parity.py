@@ -322,7 +322,7 @@ def check_stable(P, guesses_u8=None, prog=None, chunk=8192, **kw):
     return prog, o
 
 
-def test_stable_examples():
+def test_stable_examples(stable_kernel):
     ex2 = lpgen.from_lists(6, [(0, [1, 2]), (1, [0, 3]), (2, [], [3]), (3, []), (4, [5])])
     check_stable(ex2)
     check_stable(ex2, guesses_u8=[[0], [1]])
@@ -334,7 +334,7 @@ def test_stable_examples():
 
 
 @pytest.mark.parametrize("seed", range(60))
-def test_random_normal_programs(seed):
+def test_random_normal_programs(seed, stable_kernel):
     rng = np.random.default_rng([seed, 4242])
     n = int(rng.integers(1, 200))
     P = lpgen.random_normal_program(rng, n, 3 * n, max_len=4, k_max=9)
@@ -346,7 +346,8 @@ def test_random_normal_programs(seed):
         check_stable(P, guesses_u8=g, prog=prog)
 
 
-def test_stable_summary_filter_mode():
+def test_stable_summary_filter_mode(monkeypatch):
+    monkeypatch.setenv("LP_NO_COMPACT_STABLE", "1")   # (a mode of the batched kernel)
     rng = np.random.default_rng(8)
     P = lpgen.random_normal_program(rng, 3000, 9000, max_len=4, k_max=7, n_facts=100)
     check_stable(P, smem_bits_cap=256, grid_blocks=5)
@@ -361,14 +362,15 @@ def test_guess_cap():
     assert e.value.status == lp.LP_E_CAP
 
 
-def test_config_c5_parity():
+def test_config_c5_parity(stable_kernel):
     P = lpgen.config("C5")
     prog, o = check_stable(P)
     assert prog.info["n_negated"] == 12
+    assert (prog.info["stable_compact_atoms"] > 0) == (stable_kernel == "compact")
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_guess_offset_slices(seed):
+def test_guess_offset_slices(seed, stable_kernel):
     """lp_run.guess_offset: rank slices of the 2^f guesses, solved one after another on
     this GPU (no slice waits on another), concatenate to the whole search."""
     from paper_2009_10247_b200.shard import guess_slices
@@ -394,7 +396,7 @@ def test_guess_offset_slices(seed):
             prog.stable_models(guess_offset=32, n_guesses=8)
 
 
-def test_guess_offset_c5_slices():
+def test_guess_offset_c5_slices(stable_kernel):
     P = lpgen.config("C5")
     o = oracle.stable(P)
     prog = lp.Program(P)
@@ -447,7 +449,7 @@ def test_paper_layout_matches_algorithm1(seed):
 
 
 @pytest.mark.parametrize("seed", range(12))
-def test_paper_layout_matches_algorithm2_3(seed):
+def test_paper_layout_matches_algorithm2_3(seed, stable_kernel):
     from oracle import paper
     rng = np.random.default_rng([seed, 909])
     P = lpgen.random_normal_program(rng, int(rng.integers(3, 14)), int(rng.integers(3, 30)),
@@ -687,7 +689,7 @@ def test_exact16_planes_large_program():
     assert prog.info["lead_pass_bytes"] < 5 * prog.info["n_rules"]
 
 
-def test_repeated_stable_calls_reuse_the_matrix():
+def test_repeated_stable_calls_reuse_the_matrix(stable_kernel):
     """Consecutive stable searches with the same matrix width clear only the rows the
     previous call changed; different guess sets, widths and offsets in any order must
     each give the oracle's accepted guesses and whole fixpoint matrix."""
@@ -701,6 +703,13 @@ def test_repeated_stable_calls_reuse_the_matrix():
         check_stable(P, guesses_u8=g, prog=prog)
         if trial == 2:
             check_stable(P, prog=prog)                  # all 2^f guesses in between
+        if trial == 3 and k:   # the search runs the batched kernel on the same matrix in between
+            from oracle import search
+            o = search.stable_search(P, h=70, seed=3, max_rounds=4)
+            got = prog.stable_search(70, 3, 4)
+            assert got["rounds"] == o["rounds"] and got["accepted"].tolist() == o["accepted"]
+    if k:
+        assert (prog.info["stable_compact_atoms"] > 0) == (stable_kernel == "compact")
 
 
 @pytest.mark.parametrize("frontier", [False, True])
@@ -733,6 +742,7 @@ def test_one_cluster_launches_of_grid_kernels(seed, monkeypatch):
     kernel): same results as the oracle."""
     monkeypatch.setenv("LP_CLUSTER_FR_SLOTS", str(1 << 30))
     monkeypatch.setenv("LP_CLUSTER_ST_SLOTS", str(1 << 30))
+    monkeypatch.setenv("LP_NO_COMPACT_STABLE", "1")   # (a launch shape of the batched kernel)
     rng = np.random.default_rng([seed, 5150])
     n = int(rng.integers(500, 20000))
     P = lpgen.random_program(rng, n, 5 * n, max_len=5, n_facts=n // 20)
