@@ -186,6 +186,10 @@ def _model_bytes_per_pass_stable(info, n, W):
             + 2 * (n + 1 + int(info["n_negated"])) * W * 8)
 
 
+def sprog_info_compact(stable):
+    return int(stable.get("compact_atoms", 0)) > 0
+
+
 def _l2_peak():
     """Measured L2 read bandwidth (tools/l2bw.cu, profiles/l2_peak.json): the denominator of
     the L2-resident stable pass's roofline."""
@@ -553,7 +557,13 @@ def main():
                   "kernel_ms": allmax(float(np.mean(st_k))), "passes": int(allmax(int(passes.item()))),
                   "accepted": int(nacc.item()), "n_negated": sprog.info["n_negated"],
                   "l2": "flushed between steps", "launches_per_call": 1,
-                  "sharding": f"guesses over {ws} rank(s), slice time max over ranks"}
+                  "sharding": f"guesses over {ws} rank(s), slice time max over ranks",
+                  "kernel": ("st_compact_kernel (live sub-program over A* in shared memory, a CTA "
+                             "per guess word; DESIGN.md 'Compact stable kernel')"
+                             if sprog.info["stable_compact_atoms"] > 0 else
+                             "st_fixpoint_kernel (batched persistent grid)"),
+                  "compact_atoms": sprog.info["stable_compact_atoms"],
+                  "compact_rows": sprog.info["stable_compact_rows"]}
         # roofline (SURVEY §8(d) batched form): C5's program and truth matrix (~112 MB)
         # stay in the 126 MB L2 across the passes, so the bound is L2, against the measured
         # L2 read bandwidth; ncu DRAM bytes of one call beside it
@@ -565,14 +575,49 @@ def main():
         stable["roofline"] = {"bound": "l2", "unit": "GB/s", "model_bytes_per_pass": sb,
                               "passes_per_launch": spasses, "achieved": ach, "peak": l2_gbs,
                               "frac": (ach / l2_gbs) if l2_gbs else None, "peak_source": l2_src,
-                              "traffic": _ncu_traffic("C5_stable", spasses),
-                              "binding": "latency: grid barriers and dependent L2 round trips per pass "
-                                         "(armed passes touch only the candidate rows' guess words)"}
+                              "traffic": _ncu_traffic("C5_stable_compact" if sprog.info["stable_compact_atoms"] > 0
+                                                      else "C5_stable", spasses),
+                              "binding": ("latency: dependent shared-memory loads and two block barriers "
+                                          "per pass inside one CTA per guess word (the model's bytes are "
+                                          "never moved: rows outside A* cannot fire, DESIGN.md R25)"
+                                          if sprog.info["stable_compact_atoms"] > 0 else
+                                          "latency: grid barriers and dependent L2 round trips per pass "
+                                          "(armed passes touch only the candidate rows' guess words)")}
         if dist:
             ids, ps = stable_models_sharded(sprog, sprog.info["n_free_negated"])
             stable["accepted"], stable["passes"] = int(ids.size), ps
         out["stable"] = stable
         sprog.close()
+        if not dist and sprog_info_compact(stable):
+            # A/B: the batched persistent-grid kernel on the same call (LP_NO_COMPACT_STABLE
+            # is read by lp_load)
+            os.environ["LP_NO_COMPACT_STABLE"] = "1"
+            bprog = lp.Program(S, device=local)
+            del os.environ["LP_NO_COMPACT_STABLE"]
+            bt, bk = [], []
+            for i in range(args.warmup + args.steps):
+                flush_l2()
+                e0, e1, k0, k1 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                e0.record(stream)
+                lp.lp_stable_models(bprog, None, G, acc, stream=stream, device_ptrs=True,
+                                    n_accepted_out=nacc, passes_out=passes, ev_begin=k0,
+                                    ev_end=k1, guess_offset=goff, status_out=status_d)
+                e1.record(stream)
+                stream.synchronize()
+                assert int(status_d.item()) == 0
+                if i >= args.warmup:
+                    bt.append(e0.elapsed_time(e1))
+                    bk.append(k0.elapsed_time(k1))
+            assert int(nacc.item()) == stable["accepted"] and int(passes.item()) == stable["passes"]
+            sb_ach = sb * spasses / (float(np.mean(bk)) / 1e3) / 1e9
+            out["stable_batched"] = {
+                "ms_per_step": float(np.mean(bt)), "kernel_ms": float(np.mean(bk)),
+                "guesses_per_s": G_all / (float(np.mean(bt)) / 1e3),
+                "kernel": "st_fixpoint_kernel (batched persistent grid, armed passes; LP_NO_COMPACT_STABLE)",
+                "roofline": {"bound": "l2", "unit": "GB/s", "achieved": sb_ach, "peak": l2_gbs,
+                             "frac": (sb_ach / l2_gbs) if l2_gbs else None,
+                             "traffic": _ncu_traffic("C5_stable", spasses)}}
+            bprog.close()
         # ---- guess-space reduction (lp_stable_search, reading R23): C5's
         # recipe with k = 32 negated atoms -- 2^32 guesses, enumeration refused (LP_E_CAP);
         # 128 sampled columns per round + local search, all rounds in one launch ----------

@@ -132,7 +132,7 @@ struct lp_program {
     size_t cp_smem = 0;
     uint4 *d_cp_blob = nullptr;
     int32_t *d_cp_atom = nullptr, *d_cp_neg = nullptr, *d_cp_abar = nullptr;
-    int32_t *d_cp_pw = nullptr;
+    int32_t *d_cp_pw = nullptr, *d_cp_rp = nullptr;
     size_t cp_pw_alloc = 0;
     unsigned long long *d_cp_C = nullptr;   // [W][na] the last compact call's fixpoint matrix over A*
     size_t cp_C_alloc = 0;
@@ -326,7 +326,7 @@ static lp_status build_compact_stable(lp_program *p) {
         if (ok) row0.push_back((uint16_t)r);
     }
     const size_t n0 = row0.size();
-    const size_t blob_bytes = (2 * ((nr + 1) + nr + nz + (na + 1) + nz + na + n0) + 15) / 16 * 16;
+    const size_t blob_bytes = (2 * (4 * nr + nz + (na + 1) + nz + na + n0) + 15) / 16 * 16;
     const size_t smem = blob_bytes + 16 * na + 2 * (na + (na & 1)) + 4 * (nz + (nz & 1)) + 4 * ((na + 31) / 32);
     if (smem > (size_t)kMaxSmemBytes) return LP_OK;
     std::vector<uint4> blob(blob_bytes / 16, make_uint4(0, 0, 0, 0));
@@ -336,8 +336,14 @@ static lp_status build_compact_stable(lp_program *p) {
             if (n16) std::memcpy(b, src, 2 * n16);
             b += n16;
         };
-        put(rptr.data(), nr + 1);
-        put(rhead.data(), nr);
+        std::vector<uint16_t> rrec(4 * nr);
+        for (size_t r = 0; r < nr; ++r) {
+            rrec[4 * r] = rhead[r];
+            rrec[4 * r + 1] = rptr[r];
+            rrec[4 * r + 2] = rptr[r + 1];
+            rrec[4 * r + 3] = rptr[r + 1] > rptr[r] ? rbody[rptr[r]] : (uint16_t)cid[L.top];
+        }
+        put(rrec.data(), 4 * nr);
         put(rbody.data(), nz);
         put(cptr.data(), na + 1);
         put(crow.data(), nz);
@@ -354,6 +360,7 @@ static lp_status build_compact_stable(lp_program *p) {
     TRY(upload(p, &p->d_cp_atom, atom));
     TRY(upload(p, &p->d_cp_neg, cneg));
     TRY(upload(p, &p->d_cp_abar, cabar));
+    TRY(upload(p, &p->d_cp_rp, std::vector<int32_t>(4, 0)));
     p->cp_na = (int32_t)na;
     p->cp_nr = (int32_t)nr;
     p->cp_nnz = (int32_t)nz;
@@ -1251,6 +1258,20 @@ static void st_compact_params(lp_program *p, STParams *s) {
     s->cp_C = p->d_cp_C;
     s->cp_pw = p->d_cp_pw;
     s->cp_done = p->d_scal + 26;
+    s->cp_rp = p->d_cp_rp;
+}
+
+// the compact matrix C[W][na] of the coming compact call
+static lp_status st_compact_matrix(lp_program *p) {
+    const size_t cw = (size_t)p->W * p->cp_na;
+    if (cw > p->cp_C_alloc) {
+        if (p->d_cp_C) dev_release(p, p->d_cp_C);
+        p->d_cp_C = nullptr;
+        p->cp_C_alloc = 0;
+        TRY(dalloc(p, &p->d_cp_C, cw));
+        p->cp_C_alloc = cw;
+    }
+    return LP_OK;
 }
 
 // A compact call's result is the compact matrix C; the matrix / column readbacks read T0:
@@ -1345,12 +1366,7 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
             TRY(dalloc(p, &p->d_cp_pw, (size_t)W));
             p->cp_pw_alloc = W;
         }
-        const size_t cw = (size_t)W * p->cp_na;
-        if (cw > p->cp_C_alloc) {
-            if (p->d_cp_C) dev_release(p, p->d_cp_C);
-            TRY(dalloc(p, &p->d_cp_C, cw));
-            p->cp_C_alloc = cw;
-        }
+        TRY(st_compact_matrix(p));
         st_compact_params(p, &s);
         p->st_last_compact = true;
         p->cp_expanded = false;
@@ -1396,7 +1412,7 @@ extern "C" lp_status lp_stable_search(lp_program *p, int64_t h, uint64_t seed, i
     CK(cudaSetDevice(p->device));
     TRY(st_matrix(p, h));
     const int32_t W = p->W;
-    const size_t gw = std::max<size_t>((size_t)L.k * W, 1);
+    const size_t gw = std::max<size_t>((size_t)L.k * W, 1) * (p->cp_ok ? 2 : 1);   // (compact: two column buffers)
     if (gw > p->sguess_words_alloc) {
         if (p->d_sguess) dev_release(p, p->d_sguess);
         TRY(dalloc(p, &p->d_sguess, gw));
@@ -1413,7 +1429,8 @@ extern "C" lp_status lp_stable_search(lp_program *p, int64_t h, uint64_t seed, i
         acc = p->d_acc;
     }
     STParams s = st_params(p);
-    TRY(st_clear_plan(p, st, &s));
+    if (p->cp_ok) TRY(st_compact_matrix(p));
+    else TRY(st_clear_plan(p, st, &s));
     s.n_atoms = L.n;
     s.k = L.k;
     s.negated = p->d_negated;
@@ -1436,7 +1453,14 @@ extern "C" lp_status lp_stable_search(lp_program *p, int64_t h, uint64_t seed, i
     s.passes_sum_out = dev ? passes_out : p->d_scal + 7;
     s.status_user = (dev && run) ? run->status_out : nullptr;
     if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
-    CK(launch_st_search(s, p->st_blocks, p->st_smem, st, p->st_cluster));
+    if (p->cp_ok) {   // the compact kernel's search: a CTA per guess word, a grid barrier per round
+        st_compact_params(p, &s);
+        p->st_last_compact = true;
+        p->cp_expanded = false;
+        CK(launch_st_search_compact(s, std::max(1, std::min(W, p->sms)), p->cp_smem, st));
+    } else {
+        CK(launch_st_search(s, p->st_blocks, p->st_smem, st, p->st_cluster));
+    }
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
     p->stable_valid = true;
     if (guesses_out && L.k > 0)

@@ -3023,130 +3023,181 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
 // passes: a pass changes the matrix iff it changes some column).  Same T_k at every k as
 // the batched kernel: same matrix, accepted ids and passes (DESIGN.md "Compact stable
 // kernel").
+// The CTA's shared memory: the blob (uint16 units: row records[nr][4] (head, body begin, body
+// end, first body atom or ⊤ for an empty body) | body[nnz] | occ_ptr[na+1] | occ row[nnz] |
+// init[na] | pass-0 rows[n0]), then the two column buffers, the change lists and their bitmap.
+struct CpView {
+    int32_t na, nr, nnz;
+    uint4 *blob;
+    const uint2 *rrec;       // (head | begin << 16, end | first body atom << 16)
+    const uint16_t *rbody, *optr, *orow, *row0;
+    const int16_t *ainit;
+    unsigned long long *cur, *nxt;
+    uint16_t *la;            // [na] rows of T changed in this pass
+    uint16_t *lr0, *lr1;     // [nnz] x 2: the AND-rows to evaluate in this pass / in the next one
+    uint32_t *inl;           // bit a: a is on la
+    int32_t *s_na, *s_nr;    // [2] each: list counters by pass parity
+};
+
+__device__ __forceinline__ CpView cp_view(const STParams &p, unsigned long long *cpb, int32_t *s_cnt) {
+    CpView v;
+    v.na = p.cp_na;
+    v.nr = p.cp_nr;
+    v.nnz = p.cp_nnz;
+    v.blob = reinterpret_cast<uint4 *>(cpb);
+    v.rrec = reinterpret_cast<const uint2 *>(cpb);
+    v.rbody = reinterpret_cast<const uint16_t *>(v.rrec + v.nr);
+    v.optr = v.rbody + v.nnz;
+    v.orow = v.optr + v.na + 1;
+    v.ainit = reinterpret_cast<const int16_t *>(v.orow + v.nnz);
+    v.row0 = reinterpret_cast<const uint16_t *>(v.ainit + v.na);
+    v.cur = cpb + 2 * (int64_t)p.cp_blob16;
+    v.nxt = v.cur + v.na;
+    v.la = reinterpret_cast<uint16_t *>(v.nxt + v.na);
+    v.lr0 = v.la + v.na + (v.na & 1);
+    v.lr1 = v.lr0 + v.nnz + (v.nnz & 1);
+    v.inl = reinterpret_cast<uint32_t *>(v.lr1 + v.nnz + (v.nnz & 1));
+    v.s_na = s_cnt;
+    v.s_nr = s_cnt + 2;
+    return v;
+}
+
+// the blob into shared memory, the list state cleared (ends with a block barrier)
+__device__ __forceinline__ void cp_stage(const STParams &p, const CpView &v) {
+    const int tid = threadIdx.x;
+    for (int32_t i = tid; i < p.cp_blob16; i += blockDim.x) v.blob[i] = __ldg(p.cp_blob + i);
+    if (tid == 0) v.s_na[0] = v.s_na[1] = v.s_nr[0] = v.s_nr[1] = 0;
+    for (int32_t i = tid; i < ((v.na + 31) >> 5); i += blockDim.x) v.inl[i] = 0u;
+    __syncthreads();
+}
+
+// The whole Jacobi fixpoint of guess word w in shared memory; returns the word's pass count
+// and leaves the fixpoint column over A* in v.cur.  cols: the caller's guesses [k][W] (NULL:
+// binary counting); SEARCH: they were written by this kernel (no read-only loads).
+template <bool SEARCH>
+__device__ __forceinline__ int32_t cp_word(const STParams &p, const CpView &v, int32_t w,
+                                           const unsigned long long *cols, bool dl) {
+    const int tid = threadIdx.x;
+    const int32_t na = v.na;
+    unsigned long long *cur = v.cur, *nxt = v.nxt;
+    const unsigned long long valid = valid_word(w, p.W, p.G);
+    // T_0 (Def. 8) on A*: ⊤ and the facts all ones, abar_j from the guesses
+    for (int32_t a = tid; a < na; a += blockDim.x) {
+        const int32_t ini = v.ainit[a];
+        unsigned long long x = 0ull;
+        if (ini == -2) x = valid;
+        else if (ini >= 0) {
+            if (cols) x = (SEARCH ? __ldcg(cols + (int64_t)ini * p.W + w) : __ldg(cols + (int64_t)ini * p.W + w)) & valid;
+            else {
+                const int32_t rank = __ldg(p.free_rank + ini);
+                x = rank < 0 ? 0ull : (count_pattern(rank, w + p.woff) & valid);
+            }
+        }
+        cur[a] = x;
+        nxt[a] = x;
+    }
+    __syncthreads();
+    if (dl) p.dbg[1] = globaltimer();
+    // one AND-row against T_k (cur): its new bits are ORed into T_{k+1} (nxt); at its
+    // head's first change in this pass the head goes onto the pass's change list (one
+    // counter atomic per group of converged lanes) and the rows it occurs in onto the
+    // next pass's row list (a row listed twice is evaluated twice: ORs are idempotent)
+    auto eval_row = [&](int32_t r, int k) {
+        const uint2 rc = v.rrec[r];
+        const uint32_t h = rc.x & 0xFFFFu, e = rc.y & 0xFFFFu;
+        unsigned long long acc = valid & ~cur[h] & cur[rc.y >> 16];
+        for (uint32_t i = (rc.x >> 16) + 1; i < e && acc; ++i) acc &= cur[v.rbody[i]];
+        if (!acc) return;
+        uint32_t *n32 = reinterpret_cast<uint32_t *>(nxt + h);
+        if ((uint32_t)acc) atomicOr(n32, (uint32_t)acc);
+        if ((uint32_t)(acc >> 32)) atomicOr(n32 + 1, (uint32_t)(acc >> 32));
+        const uint32_t bit = 1u << (h & 31);
+        if (atomicOr(v.inl + (h >> 5), bit) & bit) return;
+        const uint32_t o0 = v.optr[h], o1 = v.optr[h + 1];
+        cg::coalesced_group g = cg::coalesced_threads();
+        int32_t base = 0;
+        if (g.thread_rank() == 0) base = atomicAdd(&v.s_na[k & 1], (int32_t)g.size());
+        v.la[g.shfl(base, 0) + (int32_t)g.thread_rank()] = (uint16_t)h;
+        if (o1 > o0) {
+            uint16_t *dst = ((k & 1) ? v.lr0 : v.lr1) + atomicAdd(&v.s_nr[(k + 1) & 1], (int32_t)(o1 - o0));
+            for (uint32_t o = o0; o < o1; ++o) *dst++ = v.orow[o];
+        }
+    };
+    int32_t passes = 0;
+    for (int k = 0;; ++k) {
+        // pass 0: the rows whose body lies in T_0's possible atoms (the others hold an atom
+        // that is zero in every column of T_0); pass k: the rows with a body atom that
+        // changed in pass k-1 (any other row computes the bits it computed before,
+        // already in its head)
+        const uint16_t *rows = k == 0 ? v.row0 : ((k & 1) ? v.lr1 : v.lr0);
+        const int32_t nrow = k == 0 ? p.cp_n0 : v.s_nr[k & 1];
+        for (int32_t i = tid; i < nrow; i += blockDim.x) eval_row(rows[i], k);
+        __syncthreads();
+        ++passes;
+        const int32_t nn = v.s_na[k & 1];
+        if (dl && k < 60) {
+            p.dbg[8 + 2 * k] = globaltimer();
+            p.dbg[9 + 2 * k] = (unsigned long long)nrow;
+        }
+        if (nn == 0) break;   // u = v in every column of the word
+        // T_{k+1} for the changed rows; the bitmap and the counters of the pass after next
+        for (int32_t i = tid; i < nn; i += blockDim.x) {
+            const uint32_t h = v.la[i];
+            cur[h] = nxt[h];
+            v.inl[h >> 5] = 0u;   // (same-value stores race benignly)
+        }
+        if (tid == 0) {
+            v.s_na[(k + 1) & 1] = 0;
+            v.s_nr[k & 1] = 0;
+        }
+        __syncthreads();
+    }
+    if (dl) p.dbg[2] = globaltimer();
+    return passes;
+}
+
+// Algorithm 3 on the word's fixpoint column (warp 0; every lane returns
+// the accepted mask): a_j ∈ M ⟺ abar_j ∉ M for every j
+__device__ __forceinline__ unsigned long long cp_check(const STParams &p, const CpView &v, int32_t w,
+                                                       int32_t cneg, int32_t cabar) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long ok = valid_word(w, p.W, p.G);
+    for (int32_t j = lane; j < p.k; j += 32) {
+        const int32_t ca = j < 32 ? cneg : __ldg(p.cp_neg + j), cb = j < 32 ? cabar : __ldg(p.cp_abar + j);
+        ok &= (ca >= 0 ? v.cur[ca] : 0ull) ^ (cb >= 0 ? v.cur[cb] : 0ull);
+    }
+    for (int o = 16; o; o >>= 1) ok &= __shfl_xor_sync(0xFFFFFFFFu, ok, o);
+    return ok;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) st_compact_kernel(const __grid_constant__ STParams p) {
     extern __shared__ __align__(16) unsigned long long cpb[];
     const int tid = threadIdx.x, lane = tid & 31;
-    const int32_t na = p.cp_na, nr = p.cp_nr, nnz = p.cp_nnz;
-    // blob (uint16 units): row_ptr[nr+1] | row head[nr] | body[nnz] | occ_ptr[na+1] |
-    // occ row[nnz] | init[na]; then the two column buffers, the change lists and their bitmap
-    uint4 *blob = reinterpret_cast<uint4 *>(cpb);
-    const uint16_t *rptr = reinterpret_cast<const uint16_t *>(blob);
-    const uint16_t *rhead = rptr + nr + 1;
-    const uint16_t *rbody = rhead + nr;
-    const uint16_t *optr = rbody + nnz;
-    const uint16_t *orow = optr + na + 1;
-    const int16_t *ainit = reinterpret_cast<const int16_t *>(orow + nnz);
-    const uint16_t *row0 = reinterpret_cast<const uint16_t *>(ainit + na);   // [n0] rows that can fire in pass 0
-    unsigned long long *cur = cpb + 2 * (int64_t)p.cp_blob16;
-    unsigned long long *nxt = cur + na;
-    uint16_t *la = reinterpret_cast<uint16_t *>(nxt + na);    // [na] rows of T changed in this pass
-    uint16_t *lr0 = la + na + (na & 1);                       // [nnz] x 2: the AND-rows to evaluate in
-    uint16_t *lr1 = lr0 + nnz + (nnz & 1);                    //   this pass / in the next one
-    uint32_t *inl = reinterpret_cast<uint32_t *>(lr1 + nnz + (nnz & 1));   // bit a: a is on la
-    __shared__ int32_t s_na[2], s_nr[2], s_last, s_mp;
+    __shared__ int32_t s_cnt[4], s_last, s_mp;
     __shared__ unsigned long long s_n;
+    const CpView v = cp_view(p, cpb, s_cnt);
+    const int32_t na = v.na;
     const bool dl = p.dbg && blockIdx.x == 0 && tid == 0;   // (phase stamps: tools/dbg_compact.py)
     if (dl) p.dbg[0] = globaltimer();
-    for (int32_t i = tid; i < p.cp_blob16; i += blockDim.x) blob[i] = __ldg(p.cp_blob + i);
     // (Algorithm 3's pairs, compact ids: requested now, used after the fixpoint)
     int32_t cneg = -1, cabar = -1;
     if (tid < 32 && lane < p.k) {
         cneg = __ldg(p.cp_neg + lane);
         cabar = __ldg(p.cp_abar + lane);
     }
-    if (tid == 0) s_na[0] = s_na[1] = s_nr[0] = s_nr[1] = 0;
-    for (int32_t i = tid; i < ((na + 31) >> 5); i += blockDim.x) inl[i] = 0u;
-    __syncthreads();
+    cp_stage(p, v);
     for (int32_t w = blockIdx.x; w < p.W; w += gridDim.x) {
-        const unsigned long long valid = valid_word(w, p.W, p.G);
-        // T_0 (Def. 8) on A*: ⊤ and the facts all ones, abar_j from the guesses
-        for (int32_t a = tid; a < na; a += blockDim.x) {
-            const int32_t ini = ainit[a];
-            unsigned long long v = 0ull;
-            if (ini == -2) v = valid;
-            else if (ini >= 0) {
-                if (p.guesses) v = __ldg(p.guesses + (int64_t)ini * p.W + w) & valid;
-                else {
-                    const int32_t rank = __ldg(p.free_rank + ini);
-                    v = rank < 0 ? 0ull : (count_pattern(rank, w + p.woff) & valid);
-                }
-            }
-            cur[a] = v;
-            nxt[a] = v;
-        }
-        __syncthreads();
-        if (dl) p.dbg[1] = globaltimer();
-        // one AND-row against T_k (cur): its new bits are ORed into T_{k+1} (nxt); at its
-        // head's first change in this pass the head goes onto the pass's change list (one
-        // counter atomic per group of converged lanes) and the rows it occurs in onto the
-        // next pass's row list (a row listed twice is evaluated twice: ORs are idempotent)
-        auto eval_row = [&](int32_t r, int k) {
-            const uint32_t h = rhead[r];
-            unsigned long long acc = valid & ~cur[h];
-            if (!acc) return;
-            const uint32_t e = rptr[r + 1];
-            for (uint32_t i = rptr[r]; i < e && acc; ++i) acc &= cur[rbody[i]];
-            if (!acc) return;
-            uint32_t *n32 = reinterpret_cast<uint32_t *>(nxt + h);
-            if ((uint32_t)acc) atomicOr(n32, (uint32_t)acc);
-            if ((uint32_t)(acc >> 32)) atomicOr(n32 + 1, (uint32_t)(acc >> 32));
-            const uint32_t bit = 1u << (h & 31);
-            if (atomicOr(inl + (h >> 5), bit) & bit) return;
-            const uint32_t o0 = optr[h], o1 = optr[h + 1];
-            cg::coalesced_group g = cg::coalesced_threads();
-            int32_t base = 0;
-            if (g.thread_rank() == 0) base = atomicAdd(&s_na[k & 1], (int32_t)g.size());
-            la[g.shfl(base, 0) + (int32_t)g.thread_rank()] = (uint16_t)h;
-            if (o1 > o0) {
-                uint16_t *dst = ((k & 1) ? lr0 : lr1) + atomicAdd(&s_nr[(k + 1) & 1], (int32_t)(o1 - o0));
-                for (uint32_t o = o0; o < o1; ++o) *dst++ = orow[o];
-            }
-        };
-        int32_t passes = 0;
-        for (int k = 0;; ++k) {
-            // pass 0: the rows whose body lies in T_0's possible atoms (the others hold an atom
-            // that is zero in every column of T_0); pass k: the rows with a body atom that
-            // changed in pass k-1 (any other row computes the bits it computed before,
-            // already in its head)
-            const uint16_t *rows = k == 0 ? row0 : ((k & 1) ? lr1 : lr0);
-            const int32_t nrow = k == 0 ? p.cp_n0 : s_nr[k & 1];
-            for (int32_t i = tid; i < nrow; i += blockDim.x) eval_row(rows[i], k);
-            __syncthreads();
-            ++passes;
-            const int32_t nn = s_na[k & 1];
-            if (dl && k < 60) {
-                p.dbg[8 + 2 * k] = globaltimer();
-                p.dbg[9 + 2 * k] = (unsigned long long)nrow;
-            }
-            if (nn == 0) break;   // u = v in every column of the word
-            // T_{k+1} for the changed rows; the bitmap and the counters of the pass after next
-            for (int32_t i = tid; i < nn; i += blockDim.x) {
-                const uint32_t h = la[i];
-                cur[h] = nxt[h];
-                inl[h >> 5] = 0u;   // (same-value stores race benignly)
-            }
-            if (tid == 0) {
-                s_na[(k + 1) & 1] = 0;
-                s_nr[k & 1] = 0;
-            }
-            __syncthreads();
-        }
-        if (dl) p.dbg[2] = globaltimer();
+        const int32_t passes = cp_word<false>(p, v, w, p.guesses, dl);
         // the word's column of the fixpoint matrix over A* (cur = nxt at the fixpoint)
-        for (int32_t a = tid; a < na; a += blockDim.x) p.cp_C[(int64_t)w * na + a] = cur[a];
-        if (tid < 32) {   // Algorithm 3: a_j ∈ M ⟺ abar_j ∉ M for every j
-            unsigned long long ok = valid;
-            for (int32_t j = lane; j < p.k; j += 32) {
-                const int32_t ca = j < 32 ? cneg : __ldg(p.cp_neg + j), cb = j < 32 ? cabar : __ldg(p.cp_abar + j);
-                ok &= (ca >= 0 ? cur[ca] : 0ull) ^ (cb >= 0 ? cur[cb] : 0ull);
-            }
-            for (int o = 16; o; o >>= 1) ok &= __shfl_xor_sync(0xFFFFFFFFu, ok, o);
+        for (int32_t a = tid; a < na; a += blockDim.x) p.cp_C[(int64_t)w * na + a] = v.cur[a];
+        if (tid < 32) {
+            const unsigned long long ok = cp_check(p, v, w, cneg, cabar);
             if (lane == 0) {
                 p.accepted[w] = ok;
                 p.cp_pw[w] = passes;
             }
         }
-        if (tid == 0) s_na[0] = s_na[1] = s_nr[0] = s_nr[1] = 0;
+        if (tid == 0) s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0;
         __syncthreads();   // (cur and the counters are rebuilt for the CTA's next word)
         if (dl) p.dbg[3] = globaltimer();
     }
@@ -3324,6 +3375,141 @@ cudaError_t launch_st_search(const STParams &p, int blocks, size_t smem, cudaStr
                                   smem, st);
 }
 
+// The same search on the compact kernel's terms: CTA w
+// owns guess word w in every round -- it samples its 64 columns, runs their fixpoint in
+// shared memory, tests them and, from the fixpoint column still in shared memory, writes the
+// NEXT round's columns (the local-search move) into the other column buffer; one grid
+// barrier per round decides whether some column was accepted.  Same counter-based draws, so
+// the same columns, rounds, passes and accepted ids as st_search_kernel and the oracle.
+__global__ void __launch_bounds__(kThreads, 1) st_search_compact_kernel(const __grid_constant__ STParams p) {
+    extern __shared__ __align__(16) unsigned long long cpb[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ int32_t s_cnt[4], s_rp;
+    __shared__ long long s_nacc;
+    cg::grid_group grid = cg::this_grid();
+    const CpView v = cp_view(p, cpb, s_cnt);
+    const int32_t na = v.na;
+    const bool lead = blockIdx.x == 0 && tid == 0;
+    const int64_t hw_n = 2 * (int64_t)p.W;
+    unsigned long long *gb[2] = {p.gbuf, p.gbuf + (int64_t)p.k * p.W};
+    int32_t cneg = -1, cabar = -1;
+    if (tid < 32 && lane < p.k) {
+        cneg = __ldg(p.cp_neg + lane);
+        cabar = __ldg(p.cp_abar + lane);
+    }
+    if (lead) {
+        *p.n_accepted = 0;
+        p.cp_rp[0] = p.cp_rp[1] = p.cp_rp[2] = 0;
+        *p.status_out = 0;
+    }
+    cp_stage(p, v);
+    {   // round 0: the sampled columns of this CTA's words (a warp per (row j, 32 columns))
+        uint32_t *g32 = reinterpret_cast<uint32_t *>(gb[0]);
+        const unsigned long long m1 = sm64_mix(sm64_mix(p.seed) ^ 0ull);
+        for (int32_t w = blockIdx.x; w < p.W; w += gridDim.x)
+            for (int32_t t = warp; t < 2 * p.k; t += (int32_t)(blockDim.x >> 5)) {
+                const int32_t j = t >> 1;
+                const int64_t hw = 2 * (int64_t)w + (t & 1);
+                const int64_t g = hw * 32 + lane;
+                bool b = false;
+                if (g < p.G && p.free_rank[j] >= 0)
+                    b = (sm64_mix(sm64_mix(m1 ^ (unsigned long long)g) ^ (unsigned long long)j) >> 63) != 0;
+                const unsigned wd = __ballot_sync(0xFFFFFFFFu, b);
+                if (lane == 0) g32[(int64_t)j * hw_n + hw] = wd;
+            }
+    }
+    grid.sync();   // (the counters are zero before any CTA adds to them)
+    int32_t passes_sum = 0;
+    for (int32_t r = 0;; ++r) {
+        const unsigned long long *cols = gb[r & 1];
+        uint32_t *nx32 = reinterpret_cast<uint32_t *>(gb[(r + 1) & 1]);
+        const uint32_t *c32 = reinterpret_cast<const uint32_t *>(cols);
+        if (lead) p.cp_rp[(r + 1) % 3] = 0;   // (last read two barriers ago)
+        const unsigned long long m2 = sm64_mix(sm64_mix(p.seed) ^ (unsigned long long)(r + 1));
+        for (int32_t w = blockIdx.x; w < p.W; w += gridDim.x) {
+            const int32_t passes = cp_word<true>(p, v, w, cols, false);
+            for (int32_t a = tid; a < na; a += blockDim.x) p.cp_C[(int64_t)w * na + a] = v.cur[a];
+            if (tid < 32) {
+                const unsigned long long ok = cp_check(p, v, w, cneg, cabar);
+                if (lane == 0) {
+                    p.accepted[w] = ok;
+                    if (ok) atomicAdd((unsigned long long *)p.n_accepted, (unsigned long long)__popcll(ok));
+                    atomicMax(p.cp_rp + r % 3, passes);
+                }
+            }
+            // the local-search move of the word's columns (used only if no column of the
+            // round is accepted): warps 0 / 1 take its two 32-column halves, a_j ∈ LM_g read
+            // from the fixpoint column in shared memory
+            if (warp < 2) {
+                const int64_t hw = 2 * (int64_t)w + warp;
+                const int64_t g = hw * 32 + lane;
+                const bool valid = g < p.G;
+                const uint32_t *cur32 = reinterpret_cast<const uint32_t *>(v.cur);
+                const unsigned long long m3 = sm64_mix(m2 ^ (unsigned long long)g);
+                int32_t nviol = 0, nflip = 0;
+                for (int32_t j = 0; j < p.k; ++j) {
+                    const int32_t ca = __ldg(p.cp_neg + j);
+                    const uint32_t bar = (__ldcg(c32 + (int64_t)j * hw_n + hw) >> lane) & 1u;
+                    const uint32_t inlm = ca >= 0 ? (cur32[2 * ca + warp] >> lane) & 1u : 0u;
+                    const bool viol = bar + inlm != 1u;
+                    nviol += viol;
+                    nflip += viol && (sm64_mix(m3 ^ (unsigned long long)j) >> 63);
+                }
+                const int32_t sel = (nflip == 0 && nviol > 0)
+                                        ? (int32_t)(sm64_mix(m3 ^ (unsigned long long)p.k) % (unsigned long long)nviol)
+                                        : -1;
+                int32_t cnt = 0;
+                for (int32_t j = 0; j < p.k; ++j) {
+                    const int32_t ca = __ldg(p.cp_neg + j);
+                    const uint32_t bar = (__ldcg(c32 + (int64_t)j * hw_n + hw) >> lane) & 1u;
+                    const uint32_t inlm = ca >= 0 ? (cur32[2 * ca + warp] >> lane) & 1u : 0u;
+                    const bool viol = bar + inlm != 1u;
+                    bool flip;
+                    if (sel >= 0) {
+                        flip = viol && cnt == sel;
+                        cnt += viol;
+                    } else {
+                        flip = viol && (sm64_mix(m3 ^ (unsigned long long)j) >> 63);
+                    }
+                    const unsigned wd = __ballot_sync(0xFFFFFFFFu, valid && ((bar ^ (flip ? 1u : 0u)) != 0u));
+                    if (lane == 0) nx32[(int64_t)j * hw_n + hw] = wd;
+                }
+            }
+            if (tid == 0) s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0;
+            __syncthreads();
+        }
+        grid.sync();
+        if (tid == 0) {
+            s_nacc = __ldcg(reinterpret_cast<const long long *>(p.n_accepted));
+            s_rp = __ldcg(p.cp_rp + r % 3);
+        }
+        __syncthreads();
+        const long long nacc = s_nacc;
+        passes_sum += s_rp;
+        if (nacc > 0 || r + 1 >= p.max_rounds) {
+            if (r & 1)   // the round's columns into the buffer the host reads
+                for (int32_t w = blockIdx.x; w < p.W; w += gridDim.x)
+                    for (int32_t j = tid; j < p.k; j += blockDim.x)
+                        gb[0][(int64_t)j * p.W + w] = __ldcg(gb[1] + (int64_t)j * p.W + w);
+            if (lead) {
+                *p.rounds_out = r + 1;
+                *p.passes_sum_out = passes_sum;
+                *p.passes_out = s_rp;
+                if (p.status_user) *p.status_user = 0;
+            }
+            return;
+        }
+        __syncthreads();   // (s_nacc / s_rp are rewritten after the next barrier)
+    }
+}
+
+cudaError_t launch_st_search_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
+    STParams q = p;
+    void *args[] = {(void *)&q};
+    return cudaLaunchCooperativeKernel((const void *)st_search_compact_kernel, dim3(blocks), dim3(kThreads), args,
+                                       smem, st);
+}
+
 cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st, int cluster) {
     STParams q = p;
     return launch_grid_or_cluster(st_fixpoint_kernel<false>, st_fixpoint_kernel<true>, &q, sizeof(q), blocks,
@@ -3422,6 +3608,9 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
         return e;
     if ((e = cudaFuncSetAttribute((const void *)st_compact_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
+        return e;
+    if ((e = cudaFuncSetAttribute((const void *)st_search_compact_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
         return e;
     // the one-cluster launches of the same kernels (16 CTAs: a non-portable cluster size)

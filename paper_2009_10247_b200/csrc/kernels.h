@@ -223,7 +223,8 @@ struct STParams {
     // compact kernel (st_compact_kernel): the live
     // sub-program -- the rows that can fire in some guess, over the atoms A* that can be true
     // in some guess (the closure of the facts with every abar_j true, computed by lp_load)
-    // -- as one blob of uint16: row_ptr (nr+1) | row head (nr) | body (nnz) | occ_ptr
+    // -- as one blob of uint16: row records (nr x 4: head, body begin, body end, first body
+    // atom -- ⊤ when the body is empty) | body (nnz) | occ_ptr
     // (na+1) | occ row (nnz) | init (na: -1 zero in T_0, -2 all ones, j >= 0 abar_j) | the
     // rows whose (compact) body holds abar atoms only: all that can fire in pass 0 (n0)
     const uint4 *cp_blob;
@@ -235,6 +236,7 @@ struct STParams {
     unsigned long long *cp_C;           // [W][na] the fixpoint matrix over A*, word-major
     int32_t *cp_pw;                     // [W] passes of each guess word
     int32_t *cp_done;                   // CTAs finished (self-resetting; the last one reduces)
+    int32_t *cp_rp;                     // [3] search: a round's passes (max over words), slot r % 3
 };
 
 // Multi-GPU exchange step (lp_shard_combine).
@@ -272,6 +274,9 @@ cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStre
 // The same call on the live sub-program held in shared memory, a CTA per guess word (no
 // grid barrier: an ordinary launch).
 cudaError_t launch_st_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st);
+// ... the guess-space search on it (cooperative: one grid barrier per round; gbuf holds two
+// column buffers [2][k][W])
+cudaError_t launch_st_search_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st);
 // ... and its compact matrix C scattered into the zeroed T0 (for the matrix / column readback)
 cudaError_t launch_st_expand(const STParams &p, cudaStream_t st);
 // Guess-space reduction: all rounds of sampling + local search in one cooperative launch.

@@ -47,11 +47,11 @@ def _small_normal(seed):
 
 
 @pytest.mark.parametrize("seed", range(40))
-def test_small_programs(seed):
+def test_small_programs(seed, stable_kernel):
     check_search(_small_normal(seed), h=8 + seed % 3 * 61, seed=seed, max_rounds=24)
 
 
-def test_edges():
+def test_edges(stable_kernel):
     P = lpgen.from_lists(1, [(0, [], [0])])                 # no stable model
     prog, o = check_search(P, 64, 3, 5)
     assert not o["found"] and o["rounds"] == 5
@@ -70,7 +70,7 @@ def test_edges():
 
 
 @pytest.mark.parametrize("k", [24, 32, 40])
-def test_many_negations_where_enumeration_is_refused(k):
+def test_many_negations_where_enumeration_is_refused(k, stable_kernel):
     P = lpgen.gen_c5(seed=k, n=4000, R=20000, k=k)
     prog = lp.Program(P)
     with pytest.raises(lp.LPError) as e:
@@ -79,7 +79,7 @@ def test_many_negations_where_enumeration_is_refused(k):
     check_search(P, 256, 100 + k, 12, prog=prog)
 
 
-def test_c5_size_k32():
+def test_c5_size_k32(stable_kernel):
     """C5's recipe (100k atoms, 500k rules) with 32 negated atoms: 2^32 guesses cannot be
     enumerated; 128 sampled columns + local search find the stable model."""
     P = lpgen.gen_c5(seed=3, n=100_000, R=500_000, k=32)
@@ -87,7 +87,7 @@ def test_c5_size_k32():
     assert o["found"]
 
 
-def test_device_pointer_mode():
+def test_device_pointer_mode(stable_kernel):
     import torch
     P = lpgen.gen_c5(seed=3, n=100_000, R=500_000, k=32)
     o = search.stable_search(P, h=128, seed=5, max_rounds=40)
