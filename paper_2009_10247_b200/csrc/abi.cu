@@ -285,14 +285,20 @@ static lp_status build_compact_stable(lp_program *p) {
             }
         }
     }
+    // compact ids for A* minus the all-ones atoms (⊤, the facts: they never mask a bit and
+    // never change; -2 stands for them where a compact id is expected)
     std::vector<int32_t> cid((size_t)ne, -1), atom, init;
     for (int32_t a = 0; a < ne; ++a)
         if (tr[a]) {
+            if (ones[a]) {
+                cid[a] = -2;
+                continue;
+            }
             cid[a] = (int32_t)atom.size();
             atom.push_back(a);
-            init.push_back(ones[a] ? -2 : (a >= L.n && a < L.n + L.k) ? a - L.n : -1);
+            init.push_back((a >= L.n && a < L.n + L.k) ? a - L.n : -1);
         }
-    if (atom.size() > 65535 || L.k > 32767) return LP_OK;
+    if (atom.size() > 65534 || L.k > 32767) return LP_OK;
     const size_t na = atom.size();
     std::vector<uint16_t> rptr(1, (uint16_t)0), rhead, rbody;
     for (const Segment &sg : L.segs)
@@ -327,8 +333,8 @@ static lp_status build_compact_stable(lp_program *p) {
     }
     const size_t n0 = row0.size();
     const size_t blob_bytes = (2 * (4 * nr + nz + (na + 1) + nz + na + n0) + 15) / 16 * 16;
-    const size_t smem = blob_bytes + 16 * na + 2 * (na + (na & 1)) + 4 * (nz + (nz & 1)) + 4 * ((na + 31) / 32);
-    if (smem > (size_t)kMaxSmemBytes) return LP_OK;
+    const size_t smem = blob_bytes + 8 * na + 2 * (na + (na & 1)) + 4 * (nz + (nz & 1)) + 4 * ((na + 31) / 32);
+    if (smem > (size_t)kCpSmemBytes) return LP_OK;
     std::vector<uint4> blob(blob_bytes / 16, make_uint4(0, 0, 0, 0));
     {
         uint16_t *b = reinterpret_cast<uint16_t *>(blob.data());
@@ -341,7 +347,7 @@ static lp_status build_compact_stable(lp_program *p) {
             rrec[4 * r] = rhead[r];
             rrec[4 * r + 1] = rptr[r];
             rrec[4 * r + 2] = rptr[r + 1];
-            rrec[4 * r + 3] = rptr[r + 1] > rptr[r] ? rbody[rptr[r]] : (uint16_t)cid[L.top];
+            rrec[4 * r + 3] = rptr[r + 1] > rptr[r] ? rbody[rptr[r]] : (uint16_t)0xFFFF;   // (kCpNone)
         }
         put(rrec.data(), 4 * nr);
         put(rbody.data(), nz);
@@ -1280,6 +1286,9 @@ static lp_status st_expand_compact(lp_program *p, cudaStream_t st) {
     if (!p->st_last_compact || p->cp_expanded) return LP_OK;
     STParams s = st_params(p);
     st_compact_params(p, &s);
+    s.facts = p->d_facts;   // (the all-ones rows are not in C)
+    s.nfacts = p->nfacts;
+    s.top = p->L.top;
     CK(cudaMemsetAsync(p->d_T0, 0, (size_t)p->L.n_ext * p->Wp * sizeof(unsigned long long), st));
     CK(launch_st_expand(s, st));
     p->cp_expanded = true;
@@ -1361,17 +1370,17 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
     if (p->cp_ok) {
         // compact kernel: the live sub-program in shared memory, a CTA per guess word, one
         // ordinary launch; the fixpoint matrix stays compact (C[w][A*]) until a readback
-        if ((size_t)W > p->cp_pw_alloc) {
+        if ((size_t)2 * W > p->cp_pw_alloc) {   // (a pass count per 32-column half-word)
             if (p->d_cp_pw) dev_release(p, p->d_cp_pw);
-            TRY(dalloc(p, &p->d_cp_pw, (size_t)W));
-            p->cp_pw_alloc = W;
+            TRY(dalloc(p, &p->d_cp_pw, (size_t)2 * W));
+            p->cp_pw_alloc = (size_t)2 * W;
         }
         TRY(st_compact_matrix(p));
         st_compact_params(p, &s);
         p->st_last_compact = true;
         p->cp_expanded = false;
         if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
-        CK(launch_st_compact(s, std::max(1, std::min(W, p->sms)), p->cp_smem, st));
+        CK(launch_st_compact(s, std::max(1, std::min(2 * W, p->sms)), p->cp_smem, st));
     } else {
     TRY(st_clear_plan(p, st, &s));
     // ONE cooperative launch: clear, T_0, the fixpoint loop, the stability check
@@ -1457,7 +1466,7 @@ extern "C" lp_status lp_stable_search(lp_program *p, int64_t h, uint64_t seed, i
         st_compact_params(p, &s);
         p->st_last_compact = true;
         p->cp_expanded = false;
-        CK(launch_st_search_compact(s, std::max(1, std::min(W, p->sms)), p->cp_smem, st));
+        CK(launch_st_search_compact(s, std::max(1, std::min(2 * W, p->sms)), p->cp_smem, st));
     } else {
         CK(launch_st_search(s, p->st_blocks, p->st_smem, st, p->st_cluster));
     }

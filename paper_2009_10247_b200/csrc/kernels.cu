@@ -3024,15 +3024,19 @@ __global__ void __launch_bounds__(kThreads, 1) st_fixpoint_kernel(const __grid_c
 // the batched kernel: same matrix, accepted ids and passes (DESIGN.md "Compact stable
 // kernel").
 // The CTA's shared memory: the blob (uint16 units: row records[nr][4] (head, body begin, body
-// end, first body atom or ⊤ for an empty body) | body[nnz] | occ_ptr[na+1] | occ row[nnz] |
-// init[na] | pass-0 rows[n0]), then the two column buffers, the change lists and their bitmap.
+// end, first body atom or 0xFFFF for an empty body) | body[nnz] | occ_ptr[na+1] | occ
+// row[nnz] | init[na] | pass-0 rows[n0]), then the two column buffers, the change lists and
+// their bitmap.  A CTA works on HALF a guess word (32 columns, uint32 columns): twice the
+// CTAs and half the column bytes of a whole word.  The atoms that are all ones from T_0 on
+// (⊤, the facts) are not among the compact atoms: they never mask a bit and never change.
+constexpr uint32_t kCpNone = 0xFFFFu;
 struct CpView {
     int32_t na, nr, nnz;
     uint4 *blob;
     const uint2 *rrec;       // (head | begin << 16, end | first body atom << 16)
     const uint16_t *rbody, *optr, *orow, *row0;
-    const int16_t *ainit;
-    unsigned long long *cur, *nxt;
+    const int16_t *ainit;    // -1: zero in T_0, j >= 0: abar_j
+    uint32_t *cur, *nxt;
     uint16_t *la;            // [na] rows of T changed in this pass
     uint16_t *lr0, *lr1;     // [nnz] x 2: the AND-rows to evaluate in this pass / in the next one
     uint32_t *inl;           // bit a: a is on la
@@ -3051,7 +3055,7 @@ __device__ __forceinline__ CpView cp_view(const STParams &p, unsigned long long 
     v.orow = v.optr + v.na + 1;
     v.ainit = reinterpret_cast<const int16_t *>(v.orow + v.nnz);
     v.row0 = reinterpret_cast<const uint16_t *>(v.ainit + v.na);
-    v.cur = cpb + 2 * (int64_t)p.cp_blob16;
+    v.cur = reinterpret_cast<uint32_t *>(cpb + 2 * (int64_t)p.cp_blob16);
     v.nxt = v.cur + v.na;
     v.la = reinterpret_cast<uint16_t *>(v.nxt + v.na);
     v.lr0 = v.la + v.na + (v.na & 1);
@@ -3071,26 +3075,31 @@ __device__ __forceinline__ void cp_stage(const STParams &p, const CpView &v) {
     __syncthreads();
 }
 
-// The whole Jacobi fixpoint of guess word w in shared memory; returns the word's pass count
-// and leaves the fixpoint column over A* in v.cur.  cols: the caller's guesses [k][W] (NULL:
+// the valid columns of half-word hw (columns 32 hw .. 32 hw + 31)
+__device__ __forceinline__ uint32_t valid_half(const STParams &p, int32_t hw) {
+    return (uint32_t)(valid_word(hw >> 1, p.W, p.G) >> (32 * (hw & 1)));
+}
+
+// The whole Jacobi fixpoint of half-word hw in shared memory; returns its pass count and
+// leaves the fixpoint column over A* in v.cur.  cols: the caller's guesses [k][W] (NULL:
 // binary counting); SEARCH: they were written by this kernel (no read-only loads).
 template <bool SEARCH>
-__device__ __forceinline__ int32_t cp_word(const STParams &p, const CpView &v, int32_t w,
+__device__ __forceinline__ int32_t cp_word(const STParams &p, const CpView &v, int32_t hw,
                                            const unsigned long long *cols, bool dl) {
     const int tid = threadIdx.x;
     const int32_t na = v.na;
-    unsigned long long *cur = v.cur, *nxt = v.nxt;
-    const unsigned long long valid = valid_word(w, p.W, p.G);
-    // T_0 (Def. 8) on A*: ⊤ and the facts all ones, abar_j from the guesses
+    uint32_t *cur = v.cur, *nxt = v.nxt;
+    const uint32_t valid = valid_half(p, hw);
+    const uint32_t *c32 = reinterpret_cast<const uint32_t *>(cols);
+    // T_0 (Def. 8) on A* minus the all-ones rows: abar_j from the guesses
     for (int32_t a = tid; a < na; a += blockDim.x) {
         const int32_t ini = v.ainit[a];
-        unsigned long long x = 0ull;
-        if (ini == -2) x = valid;
-        else if (ini >= 0) {
-            if (cols) x = (SEARCH ? __ldcg(cols + (int64_t)ini * p.W + w) : __ldg(cols + (int64_t)ini * p.W + w)) & valid;
+        uint32_t x = 0u;
+        if (ini >= 0) {
+            if (cols) x = (SEARCH ? __ldcg(c32 + (int64_t)ini * 2 * p.W + hw) : __ldg(c32 + (int64_t)ini * 2 * p.W + hw)) & valid;
             else {
                 const int32_t rank = __ldg(p.free_rank + ini);
-                x = rank < 0 ? 0ull : (count_pattern(rank, w + p.woff) & valid);
+                x = rank < 0 ? 0u : ((uint32_t)(count_pattern(rank, (hw >> 1) + p.woff) >> (32 * (hw & 1))) & valid);
             }
         }
         cur[a] = x;
@@ -3104,13 +3113,12 @@ __device__ __forceinline__ int32_t cp_word(const STParams &p, const CpView &v, i
     // next pass's row list (a row listed twice is evaluated twice: ORs are idempotent)
     auto eval_row = [&](int32_t r, int k) {
         const uint2 rc = v.rrec[r];
-        const uint32_t h = rc.x & 0xFFFFu, e = rc.y & 0xFFFFu;
-        unsigned long long acc = valid & ~cur[h] & cur[rc.y >> 16];
+        const uint32_t h = rc.x & 0xFFFFu, e = rc.y & 0xFFFFu, b0 = rc.y >> 16;
+        uint32_t acc = valid & ~cur[h];
+        if (b0 != kCpNone) acc &= cur[b0];
         for (uint32_t i = (rc.x >> 16) + 1; i < e && acc; ++i) acc &= cur[v.rbody[i]];
         if (!acc) return;
-        uint32_t *n32 = reinterpret_cast<uint32_t *>(nxt + h);
-        if ((uint32_t)acc) atomicOr(n32, (uint32_t)acc);
-        if ((uint32_t)(acc >> 32)) atomicOr(n32 + 1, (uint32_t)(acc >> 32));
+        atomicOr(nxt + h, acc);
         const uint32_t bit = 1u << (h & 31);
         if (atomicOr(v.inl + (h >> 5), bit) & bit) return;
         const uint32_t o0 = v.optr[h], o1 = v.optr[h + 1];
@@ -3139,7 +3147,7 @@ __device__ __forceinline__ int32_t cp_word(const STParams &p, const CpView &v, i
             p.dbg[8 + 2 * k] = globaltimer();
             p.dbg[9 + 2 * k] = (unsigned long long)nrow;
         }
-        if (nn == 0) break;   // u = v in every column of the word
+        if (nn == 0) break;   // u = v in every column of the half-word
         // T_{k+1} for the changed rows; the bitmap and the counters of the pass after next
         for (int32_t i = tid; i < nn; i += blockDim.x) {
             const uint32_t h = v.la[i];
@@ -3156,15 +3164,21 @@ __device__ __forceinline__ int32_t cp_word(const STParams &p, const CpView &v, i
     return passes;
 }
 
-// Algorithm 3 on the word's fixpoint column (warp 0; every lane returns
-// the accepted mask): a_j ∈ M ⟺ abar_j ∉ M for every j
-__device__ __forceinline__ unsigned long long cp_check(const STParams &p, const CpView &v, int32_t w,
-                                                       int32_t cneg, int32_t cabar) {
+// a compact id's column bits: -1 = not in A* (never true), -2 = a fact (all ones)
+__device__ __forceinline__ uint32_t cp_bits(const CpView &v, int32_t c, uint32_t valid) {
+    return c >= 0 ? v.cur[c] : c == -2 ? valid : 0u;
+}
+
+// Algorithm 3 on the half-word's fixpoint column (warp 0; every lane
+// returns the accepted mask): a_j ∈ M ⟺ abar_j ∉ M for every j
+__device__ __forceinline__ uint32_t cp_check(const STParams &p, const CpView &v, int32_t hw,
+                                             int32_t cneg, int32_t cabar) {
     const int lane = threadIdx.x & 31;
-    unsigned long long ok = valid_word(w, p.W, p.G);
+    const uint32_t valid = valid_half(p, hw);
+    uint32_t ok = valid;
     for (int32_t j = lane; j < p.k; j += 32) {
         const int32_t ca = j < 32 ? cneg : __ldg(p.cp_neg + j), cb = j < 32 ? cabar : __ldg(p.cp_abar + j);
-        ok &= (ca >= 0 ? v.cur[ca] : 0ull) ^ (cb >= 0 ? v.cur[cb] : 0ull);
+        ok &= cp_bits(v, ca, valid) ^ cp_bits(v, cb, valid);
     }
     for (int o = 16; o; o >>= 1) ok &= __shfl_xor_sync(0xFFFFFFFFu, ok, o);
     return ok;
@@ -3186,22 +3200,24 @@ __global__ void __launch_bounds__(kThreads, 1) st_compact_kernel(const __grid_co
         cabar = __ldg(p.cp_abar + lane);
     }
     cp_stage(p, v);
-    for (int32_t w = blockIdx.x; w < p.W; w += gridDim.x) {
-        const int32_t passes = cp_word<false>(p, v, w, p.guesses, dl);
-        // the word's column of the fixpoint matrix over A* (cur = nxt at the fixpoint)
-        for (int32_t a = tid; a < na; a += blockDim.x) p.cp_C[(int64_t)w * na + a] = v.cur[a];
+    uint32_t *C32 = reinterpret_cast<uint32_t *>(p.cp_C);
+    uint32_t *acc32 = reinterpret_cast<uint32_t *>(p.accepted);
+    for (int32_t hw = blockIdx.x; hw < 2 * p.W; hw += gridDim.x) {
+        const int32_t passes = cp_word<false>(p, v, hw, p.guesses, dl);
+        // the half-word's column of the fixpoint matrix over A* (cur = nxt at the fixpoint)
+        for (int32_t a = tid; a < na; a += blockDim.x) C32[(int64_t)hw * na + a] = v.cur[a];
         if (tid < 32) {
-            const unsigned long long ok = cp_check(p, v, w, cneg, cabar);
+            const uint32_t ok = cp_check(p, v, hw, cneg, cabar);
             if (lane == 0) {
-                p.accepted[w] = ok;
-                p.cp_pw[w] = passes;
+                acc32[hw] = ok;
+                p.cp_pw[hw] = passes;
             }
         }
         if (tid == 0) s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0;
-        __syncthreads();   // (cur and the counters are rebuilt for the CTA's next word)
+        __syncthreads();   // (cur and the counters are rebuilt for the CTA's next half-word)
         if (dl) p.dbg[3] = globaltimer();
     }
-    // the last CTA to finish reduces the per-word results (fence + ticket)
+    // the last CTA to finish reduces the per-half-word results (fence + ticket)
     if (tid == 0) {
         s_mp = 0;
         s_n = 0ull;
@@ -3213,9 +3229,9 @@ __global__ void __launch_bounds__(kThreads, 1) st_compact_kernel(const __grid_co
     __threadfence();
     long long n = 0;
     int32_t mp = 0;
-    for (int32_t w = tid; w < p.W; w += blockDim.x) {
-        n += __popcll(__ldcg(p.accepted + w));
-        mp = max(mp, __ldcg(p.cp_pw + w));
+    for (int32_t hw = tid; hw < 2 * p.W; hw += blockDim.x) {
+        n += __popc(__ldcg(acc32 + hw));
+        mp = max(mp, __ldcg(p.cp_pw + hw));
     }
     for (int o = 16; o; o >>= 1) {
         n += __shfl_xor_sync(0xFFFFFFFFu, n, o);
@@ -3241,22 +3257,32 @@ cudaError_t launch_st_compact(const STParams &p, int blocks, size_t smem, cudaSt
     return cudaGetLastError();
 }
 
-// The compact matrix C[w][A*] scattered into the (zeroed) matrix T0[n_ext][Wp] that
-// lp_stable_matrix / lp_guess_model read (a thread per (atom, word), words fastest).
-__global__ void st_expand_kernel(const unsigned long long *C, const int32_t *atom, int32_t na, int32_t W,
-                                 int32_t Wp, unsigned long long *T0) {
-    const int64_t total = (int64_t)na * W;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t a = x / W, w = x % W;
-        T0[(int64_t)__ldg(atom + a) * Wp + w] = C[w * na + a];
+// The compact matrix C[hw][A*] (uint32 columns) scattered into the (zeroed) matrix
+// T0[n_ext][Wp] that lp_stable_matrix / lp_guess_model read (a thread per (atom, half-word),
+// half-words fastest), and the all-ones rows (⊤, the facts) written over the valid guesses.
+__global__ void st_expand_kernel(const uint32_t *C, const int32_t *atom, int32_t na, int32_t W, int64_t G,
+                                 int32_t Wp, unsigned long long *T0, const int32_t *facts, int32_t nfacts,
+                                 int32_t top) {
+    const int64_t H = 2 * (int64_t)W;
+    const int64_t total = (int64_t)na * H;
+    uint32_t *T32 = reinterpret_cast<uint32_t *>(T0);
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gn = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = gt; x < total; x += gn) {
+        const int64_t a = x / H, hw = x % H;
+        T32[(int64_t)__ldg(atom + a) * 2 * Wp + hw] = C[hw * na + a];
+    }
+    for (int64_t x = gt; x < (int64_t)(nfacts + 1) * W; x += gn) {
+        const int64_t r = x / W, w = x % W;
+        T0[(int64_t)(r == 0 ? top : __ldg(facts + r - 1)) * Wp + w] = valid_word(w, W, G);
     }
 }
 
 cudaError_t launch_st_expand(const STParams &p, cudaStream_t st) {
-    const int64_t total = (int64_t)p.cp_na * p.W;
+    const int64_t total = std::max<int64_t>((int64_t)p.cp_na * 2 * p.W, (int64_t)(p.nfacts + 1) * p.W);
     if (total == 0) return cudaSuccess;
     const int b = (int)std::min<int64_t>((total + 255) / 256, 8192);
-    st_expand_kernel<<<b, 256, 0, st>>>(p.cp_C, p.cp_atom, p.cp_na, p.W, p.Wp, p.T0);
+    st_expand_kernel<<<b, 256, 0, st>>>(reinterpret_cast<const uint32_t *>(p.cp_C), p.cp_atom, p.cp_na, p.W, p.G,
+                                        p.Wp, p.T0, p.facts, p.nfacts, p.top);
     return cudaGetLastError();
 }
 
@@ -3390,8 +3416,10 @@ __global__ void __launch_bounds__(kThreads, 1) st_search_compact_kernel(const __
     const CpView v = cp_view(p, cpb, s_cnt);
     const int32_t na = v.na;
     const bool lead = blockIdx.x == 0 && tid == 0;
-    const int64_t hw_n = 2 * (int64_t)p.W;
+    const int32_t hw_n = 2 * p.W;
     unsigned long long *gb[2] = {p.gbuf, p.gbuf + (int64_t)p.k * p.W};
+    uint32_t *C32 = reinterpret_cast<uint32_t *>(p.cp_C);
+    uint32_t *acc32 = reinterpret_cast<uint32_t *>(p.accepted);
     int32_t cneg = -1, cabar = -1;
     if (tid < 32 && lane < p.k) {
         cneg = __ldg(p.cp_neg + lane);
@@ -3403,14 +3431,12 @@ __global__ void __launch_bounds__(kThreads, 1) st_search_compact_kernel(const __
         *p.status_out = 0;
     }
     cp_stage(p, v);
-    {   // round 0: the sampled columns of this CTA's words (a warp per (row j, 32 columns))
+    {   // round 0: the sampled columns of this CTA's half-words (a warp per row j)
         uint32_t *g32 = reinterpret_cast<uint32_t *>(gb[0]);
         const unsigned long long m1 = sm64_mix(sm64_mix(p.seed) ^ 0ull);
-        for (int32_t w = blockIdx.x; w < p.W; w += gridDim.x)
-            for (int32_t t = warp; t < 2 * p.k; t += (int32_t)(blockDim.x >> 5)) {
-                const int32_t j = t >> 1;
-                const int64_t hw = 2 * (int64_t)w + (t & 1);
-                const int64_t g = hw * 32 + lane;
+        for (int32_t hw = blockIdx.x; hw < hw_n; hw += gridDim.x)
+            for (int32_t j = warp; j < p.k; j += (int32_t)(blockDim.x >> 5)) {
+                const int64_t g = (int64_t)hw * 32 + lane;
                 bool b = false;
                 if (g < p.G && p.free_rank[j] >= 0)
                     b = (sm64_mix(sm64_mix(m1 ^ (unsigned long long)g) ^ (unsigned long long)j) >> 63) != 0;
@@ -3426,31 +3452,29 @@ __global__ void __launch_bounds__(kThreads, 1) st_search_compact_kernel(const __
         const uint32_t *c32 = reinterpret_cast<const uint32_t *>(cols);
         if (lead) p.cp_rp[(r + 1) % 3] = 0;   // (last read two barriers ago)
         const unsigned long long m2 = sm64_mix(sm64_mix(p.seed) ^ (unsigned long long)(r + 1));
-        for (int32_t w = blockIdx.x; w < p.W; w += gridDim.x) {
-            const int32_t passes = cp_word<true>(p, v, w, cols, false);
-            for (int32_t a = tid; a < na; a += blockDim.x) p.cp_C[(int64_t)w * na + a] = v.cur[a];
+        for (int32_t hw = blockIdx.x; hw < hw_n; hw += gridDim.x) {
+            const int32_t passes = cp_word<true>(p, v, hw, cols, false);
+            for (int32_t a = tid; a < na; a += blockDim.x) C32[(int64_t)hw * na + a] = v.cur[a];
             if (tid < 32) {
-                const unsigned long long ok = cp_check(p, v, w, cneg, cabar);
+                const uint32_t ok = cp_check(p, v, hw, cneg, cabar);
                 if (lane == 0) {
-                    p.accepted[w] = ok;
-                    if (ok) atomicAdd((unsigned long long *)p.n_accepted, (unsigned long long)__popcll(ok));
+                    acc32[hw] = ok;
+                    if (ok) atomicAdd((unsigned long long *)p.n_accepted, (unsigned long long)__popc(ok));
                     atomicMax(p.cp_rp + r % 3, passes);
                 }
             }
-            // the local-search move of the word's columns (used only if no column of the
-            // round is accepted): warps 0 / 1 take its two 32-column halves, a_j ∈ LM_g read
-            // from the fixpoint column in shared memory
-            if (warp < 2) {
-                const int64_t hw = 2 * (int64_t)w + warp;
-                const int64_t g = hw * 32 + lane;
+            // the local-search move of the half-word's columns (used only if no column of
+            // the round is accepted): warp 1, a_j ∈ LM_g read from the fixpoint column in
+            // shared memory
+            if (warp == 1) {
+                const int64_t g = (int64_t)hw * 32 + lane;
                 const bool valid = g < p.G;
-                const uint32_t *cur32 = reinterpret_cast<const uint32_t *>(v.cur);
+                const uint32_t vh = valid_half(p, hw);
                 const unsigned long long m3 = sm64_mix(m2 ^ (unsigned long long)g);
                 int32_t nviol = 0, nflip = 0;
                 for (int32_t j = 0; j < p.k; ++j) {
-                    const int32_t ca = __ldg(p.cp_neg + j);
                     const uint32_t bar = (__ldcg(c32 + (int64_t)j * hw_n + hw) >> lane) & 1u;
-                    const uint32_t inlm = ca >= 0 ? (cur32[2 * ca + warp] >> lane) & 1u : 0u;
+                    const uint32_t inlm = (cp_bits(v, __ldg(p.cp_neg + j), vh) >> lane) & 1u;
                     const bool viol = bar + inlm != 1u;
                     nviol += viol;
                     nflip += viol && (sm64_mix(m3 ^ (unsigned long long)j) >> 63);
@@ -3460,9 +3484,8 @@ __global__ void __launch_bounds__(kThreads, 1) st_search_compact_kernel(const __
                                         : -1;
                 int32_t cnt = 0;
                 for (int32_t j = 0; j < p.k; ++j) {
-                    const int32_t ca = __ldg(p.cp_neg + j);
                     const uint32_t bar = (__ldcg(c32 + (int64_t)j * hw_n + hw) >> lane) & 1u;
-                    const uint32_t inlm = ca >= 0 ? (cur32[2 * ca + warp] >> lane) & 1u : 0u;
+                    const uint32_t inlm = (cp_bits(v, __ldg(p.cp_neg + j), vh) >> lane) & 1u;
                     const bool viol = bar + inlm != 1u;
                     bool flip;
                     if (sel >= 0) {
@@ -3487,10 +3510,13 @@ __global__ void __launch_bounds__(kThreads, 1) st_search_compact_kernel(const __
         const long long nacc = s_nacc;
         passes_sum += s_rp;
         if (nacc > 0 || r + 1 >= p.max_rounds) {
-            if (r & 1)   // the round's columns into the buffer the host reads
-                for (int32_t w = blockIdx.x; w < p.W; w += gridDim.x)
+            if (r & 1) {   // the round's columns into the buffer the host reads
+                const uint32_t *src = reinterpret_cast<const uint32_t *>(gb[1]);
+                uint32_t *dst = reinterpret_cast<uint32_t *>(gb[0]);
+                for (int32_t hw = blockIdx.x; hw < hw_n; hw += gridDim.x)
                     for (int32_t j = tid; j < p.k; j += blockDim.x)
-                        gb[0][(int64_t)j * p.W + w] = __ldcg(gb[1] + (int64_t)j * p.W + w);
+                        dst[(int64_t)j * hw_n + hw] = __ldcg(src + (int64_t)j * hw_n + hw);
+            }
             if (lead) {
                 *p.rounds_out = r + 1;
                 *p.passes_sum_out = passes_sum;
@@ -3608,10 +3634,10 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
         return e;
     if ((e = cudaFuncSetAttribute((const void *)st_compact_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kCpSmemBytes)))
         return e;
     if ((e = cudaFuncSetAttribute((const void *)st_search_compact_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kCpSmemBytes)))
         return e;
     // the one-cluster launches of the same kernels (16 CTAs: a non-portable cluster size)
     const void *cl[3] = {(const void *)st_fixpoint_kernel<true>, (const void *)st_search_kernel<true>,

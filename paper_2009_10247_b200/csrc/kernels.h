@@ -13,6 +13,7 @@ constexpr int kThreads = 1024;          // persistent kernels: 32 warps per CTA
 // per thread measured no faster on C4 and slower on C3.)
 constexpr int kFullThreads = 1024;
 constexpr int kMaxSmemBytes = 200 * 1024;
+constexpr int kCpSmemBytes = 226 * 1024;    // compact stable kernels (+ ~50 B static <= 227 KB)
 constexpr int kKeySmemBytes = 208 * 1024;   // key-space summary (register-streaming kernel only)
 constexpr int kMaxRuns = 256;          // key mode: bucket runs of the row order kept in shared
                                        // memory (more: LEAD passes stream every octet)
@@ -224,17 +225,19 @@ struct STParams {
     // sub-program -- the rows that can fire in some guess, over the atoms A* that can be true
     // in some guess (the closure of the facts with every abar_j true, computed by lp_load)
     // -- as one blob of uint16: row records (nr x 4: head, body begin, body end, first body
-    // atom -- ⊤ when the body is empty) | body (nnz) | occ_ptr
-    // (na+1) | occ row (nnz) | init (na: -1 zero in T_0, -2 all ones, j >= 0 abar_j) | the
-    // rows whose (compact) body holds abar atoms only: all that can fire in pass 0 (n0)
+    // atom -- 0xFFFF when the body is empty) | body (nnz) | occ_ptr
+    // (na+1) | occ row (nnz) | init (na: -1 zero in T_0, j >= 0 abar_j) | the rows whose
+    // (compact) body holds abar atoms only: all that can fire in pass 0 (n0).  Compact atoms
+    // are A* minus the all-ones rows (⊤, the facts), whose compact id reads -2.
     const uint4 *cp_blob;
     int32_t cp_blob16;                  // its size in 16-byte units
     int32_t cp_na, cp_nr, cp_nnz, cp_n0;  // atoms of A*, live rows, their body entries, pass-0 rows
     const int32_t *cp_atom;             // [na] extended atom id of compact atom c
-    const int32_t *cp_neg;              // [k] compact id of a_j (-1: not in A*, never true)
+    const int32_t *cp_neg;              // [k] compact id of a_j (-1: not in A*, never true; -2: a fact)
     const int32_t *cp_abar;             // [k] compact id of abar_j
-    unsigned long long *cp_C;           // [W][na] the fixpoint matrix over A*, word-major
-    int32_t *cp_pw;                     // [W] passes of each guess word
+    unsigned long long *cp_C;           // uint32 [2W][na]: the fixpoint matrix over the compact atoms,
+                                        //   one row per 32-column half-word
+    int32_t *cp_pw;                     // [2W] passes of each half-word
     int32_t *cp_done;                   // CTAs finished (self-resetting; the last one reduces)
     int32_t *cp_rp;                     // [3] search: a round's passes (max over words), slot r % 3
 };
