@@ -215,6 +215,10 @@ typedef struct {
                                  the live rows in shared memory, a CTA per guess word
                                  (DESIGN.md "Compact stable kernel"); 0: the batched kernel */
     int32_t stable_compact_rows;  /* live rows (body within A*, head not a fact)        */
+    int32_t small_rows;       /* > 0: the full θ-pass (auto schedule) runs the small-program
+                                 kernel: ONE CTA, the rows (this many, at least 1) in shared
+                                 memory, semi-naive row lists (DESIGN.md "Small-program
+                                 kernel"); 0: the cluster / persistent grid kernels      */
 } lp_info_t;
 
 /* Validate, standardize and encode a program, upload it (PAPER.md:62, 82-95,

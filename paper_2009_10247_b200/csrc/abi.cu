@@ -144,6 +144,11 @@ struct lp_program {
     int fr_cl_threads = 0;      // one-cluster frontier launches: threads per CTA (LP_FR_CLUSTER_THREADS)
     size_t cluster_smem = 0;
     bool cluster_stage = false; // ... with the program planes staged in shared memory
+    // small-program kernel: the rows in shared memory
+    bool small_ok = false;
+    uint4 *d_sm_blob = nullptr;
+    int32_t sm_blob16 = 0, sm_nr = 0, sm_nnz = 0;
+    size_t small_smem = 0;
     int sms = 0, threads = kThreads;
     int lm_blocks = 0, fr_blocks = 0, st_blocks = 0, grid_cap = 0;
     int fr_cluster = 0, st_cluster = 0;   // > 0: one-cluster launch of the frontier / stable kernels
@@ -374,6 +379,70 @@ static lp_status build_compact_stable(lp_program *p) {
     p->cp_blob16 = (int32_t)(blob_bytes / 16);
     p->cp_smem = smem;
     p->cp_ok = true;
+    return LP_OK;
+}
+
+// The rows of a small program for lm_small_kernel: 16-bit extended atom ids, rows in slot
+// order; a row whose head is a fact is dropped (v_0 holds its head), and so are the body
+// atoms that are facts or ⊤ (true in every v_k).
+static lp_status build_small(lp_program *p) {
+    const HostLayout &L = p->L;
+    const size_t ne = (size_t)L.n_ext;
+    if (ne > 65534 || L.n_slots > 65535) return LP_OK;
+    std::vector<uint8_t> ones(ne, 0);
+    ones[L.top] = 1;
+    for (int32_t a : L.facts) ones[a] = 1;
+    std::vector<uint16_t> rptr(1, (uint16_t)0), rhead, rbody;
+    for (const Segment &sg : L.segs)
+        for (int64_t i = 0; i < sg.count; ++i) {
+            const int32_t h = L.head[sg.slot_off + i];
+            if (ones[h]) continue;
+            if (rbody.size() + (size_t)sg.L > 65535) return LP_OK;
+            rhead.push_back((uint16_t)h);
+            for (int32_t j = 0; j < sg.L; ++j) {
+                const int32_t b = L.col[sg.col_off + (int64_t)j * sg.count_pad + i];
+                if (!ones[b]) rbody.push_back((uint16_t)b);
+            }
+            rptr.push_back((uint16_t)rbody.size());
+        }
+    const size_t nr = rhead.size(), nz = rbody.size();
+    std::vector<uint16_t> cptr(ne + 1, 0), crow(nz);
+    {
+        std::vector<uint32_t> c32(ne + 1, 0u);
+        for (uint16_t b : rbody) ++c32[(size_t)b + 1];
+        for (size_t c = 0; c < ne; ++c) c32[c + 1] += c32[c];
+        for (size_t c = 0; c <= ne; ++c) cptr[c] = (uint16_t)c32[c];
+        for (size_t r = 0; r < nr; ++r)
+            for (uint32_t i = rptr[r]; i < rptr[r + 1]; ++i) crow[c32[rbody[i]]++] = (uint16_t)r;
+    }
+    const size_t blob_bytes = (2 * (4 * nr + nz + (ne + 1) + nz) + 15) / 16 * 16;
+    const size_t smem = blob_bytes + 8 * (size_t)p->nwords + 2 * (ne + (ne & 1)) + 4 * (nz + (nz & 1));
+    if (smem > (size_t)kMaxSmemBytes) return LP_OK;
+    std::vector<uint4> blob(blob_bytes / 16, make_uint4(0, 0, 0, 0));
+    {
+        uint16_t *b = reinterpret_cast<uint16_t *>(blob.data());
+        auto put = [&](const void *src, size_t n16) {
+            if (n16) std::memcpy(b, src, 2 * n16);
+            b += n16;
+        };
+        std::vector<uint16_t> rrec(4 * nr);
+        for (size_t r = 0; r < nr; ++r) {
+            rrec[4 * r] = rhead[r];
+            rrec[4 * r + 1] = rptr[r];
+            rrec[4 * r + 2] = rptr[r + 1];
+            rrec[4 * r + 3] = rptr[r + 1] > rptr[r] ? rbody[rptr[r]] : (uint16_t)0xFFFF;
+        }
+        put(rrec.data(), 4 * nr);
+        put(rbody.data(), nz);
+        put(cptr.data(), ne + 1);
+        put(crow.data(), nz);
+    }
+    TRY(upload(p, &p->d_sm_blob, blob));
+    p->sm_blob16 = (int32_t)(blob_bytes / 16);
+    p->sm_nr = (int32_t)nr;
+    p->sm_nnz = (int32_t)nz;
+    p->small_smem = smem;
+    p->small_ok = true;
     return LP_OK;
 }
 
@@ -796,6 +865,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
             if (p->cluster == 1 && p->cl_threads == 0) p->cl_threads = 512;
         }
     }
+    if (p->cluster == 1 && !std::getenv("LP_NO_SMALL")) TRY(build_small(p));
     p->st_blocks = cap_grid(sms * bs);
     load_mark("queues, occupancy");
     // one-cluster launches: the frontier and stable kernels of
@@ -930,6 +1000,7 @@ extern "C" lp_status lp_info(const lp_program *p, lp_info_t *o) {
     o->frontier_cluster_ctas = p->fr_cluster;
     o->stable_cluster_ctas = p->st_cluster;
     o->armed_list_cap = p->arm_cap;
+    o->small_rows = p->small_ok ? std::max(p->sm_nr, 1) : 0;
     o->stable_compact_atoms = p->cp_ok ? p->cp_na : 0;
     o->stable_compact_rows = p->cp_ok ? p->cp_nr : 0;
     return LP_OK;
@@ -1086,6 +1157,10 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     q.vent = p->d_vent;
     q.overlap = p->env_no_overlap ? 0 : 1;
     q.stage_planes = p->cluster_stage ? 1 : 0;
+    q.sm_blob = p->d_sm_blob;
+    q.sm_blob16 = p->sm_blob16;
+    q.sm_nr = p->sm_nr;
+    q.sm_nnz = p->sm_nnz;
     q.cl_threads = p->cl_threads;
     q.fr_cl_threads = p->fr_cl_threads;
     q.overlap_min_bytes = p->overlap_min_bytes;
@@ -1137,6 +1212,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     const bool use_cluster = !frontier && p->cluster > 0 &&
                              !(flags & (LP_FULL_STREAM | LP_FULL_LEAD | LP_FULL_NO_PIPE));
     if (frontier) CK(launch_lm_frontier(q, p->fr_blocks, st, p->fr_cluster));
+    else if (use_cluster && p->small_ok) CK(launch_lm_small(q, p->small_smem, st));
     else if (use_cluster) CK(launch_lm_cluster(q, p->cluster, p->cluster_smem, st));
     else CK(launch_lm_full(q, p->exact, p->lm_blocks, p->lm_smem, st));
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));

@@ -2357,6 +2357,144 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
 #undef CDBG
 }
 
+// ------------------------------------------------------------------------------------
+// least model: ONE CTA, the whole program in shared memory, semi-naive row lists
+// ------------------------------------------------------------------------------------
+//
+// Programs whose rows fit shared memory in 16-bit ids (C1; DESIGN.md "Small-program
+// kernel").  lp_load packs the rows (fact heads and always-true body atoms dropped) as
+// 8-byte records (head, body range, first body atom), the body ids and the transpose (rows
+// by body atom).  Pass 0 evaluates every row against v_0; pass k > 0 only the rows that
+// hold an atom derived in pass k-1 (any other row fired before or still misses an atom):
+// the same θ(M v_k) per pass as the other kernels -- same model, iters, popcounts, stages.
+// A firing row ORs its head into v_{k+1} (the atomic's old value tells the first deriver,
+// which lists the head and the rows it occurs in for the next pass); after a block barrier
+// the listed heads are ORed into v_k.  Two block barriers per pass, no global traffic in
+// the loop apart from the stage stores.
+constexpr int kSmallThreads = 512;
+__global__ void __launch_bounds__(kSmallThreads, 1) lm_small_kernel(const __grid_constant__ LMParams p) {
+    extern __shared__ __align__(16) unsigned long long smb[];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int32_t nr = p.sm_nr, nnz = p.sm_nnz, ne = p.n_ext_atoms, nw = p.nwords;
+    uint4 *blob = reinterpret_cast<uint4 *>(smb);
+    const uint2 *rrec = reinterpret_cast<const uint2 *>(smb);   // (head | begin << 16, end | first body atom << 16)
+    const uint16_t *rbody = reinterpret_cast<const uint16_t *>(rrec + nr);
+    const uint16_t *optr = rbody + nnz;
+    const uint16_t *orow = optr + ne + 1;
+    uint32_t *cur = reinterpret_cast<uint32_t *>(smb + 2 * (int64_t)p.sm_blob16);   // v_k
+    uint32_t *nxt = cur + nw;                                                       // v_{k+1}
+    uint16_t *la = reinterpret_cast<uint16_t *>(nxt + nw);    // [ne] atoms derived in this pass
+    uint16_t *lr0 = la + ne + (ne & 1);                       // [nnz] x 2: the rows to evaluate in
+    uint16_t *lr1 = lr0 + nnz + (nnz & 1);                    //   this pass / in the next one
+    __shared__ int32_t s_na[2], s_nr[2], s_tot;
+    __shared__ long long clk0;
+    __shared__ unsigned long long ns0;
+    if (tid == 0) {
+        clk0 = clock64();
+        ns0 = globaltimer();
+        *p.tail_next = 0;
+        *p.status_next = 0;
+        if (p.stats)
+            for (int i = 0; i < 6; ++i) p.stats[i] = 0;
+        s_na[0] = s_na[1] = s_nr[0] = s_nr[1] = 0;
+        s_tot = 0;
+    }
+    for (int32_t i = tid; i < p.sm_blob16; i += blockDim.x) blob[i] = __ldg(p.sm_blob + i);
+    __syncthreads();
+    // v_0 = (v0 restricted to the original atoms) | facts | ⊤ in both buffers (Def. 4), its
+    // size, and the stages of the original atoms
+    int32_t pc = 0;
+    for (int32_t w = tid; w < nw; w += blockDim.x) {
+        const int64_t lo = (int64_t)w * 32;
+        uint32_t orig = __ldg(p.factbits + w);
+        if (p.v0 && w < p.v0_words) {
+            uint32_t x = __ldg(p.v0 + w);
+            if (lo + 32 > p.n_out) x &= lo >= p.n_out ? 0u : ((1u << (uint32_t)(p.n_out - lo)) - 1u);
+            orig |= x;
+        }
+        if (lo + 32 > p.n) orig &= lo >= p.n ? 0u : ((1u << (uint32_t)(p.n - lo)) - 1u);
+        uint32_t bits = orig;
+        if (w == (p.top >> 5)) bits |= 1u << (p.top & 31);
+        cur[w] = bits;
+        nxt[w] = bits;
+        pc += __popc(orig);
+        if (p.stage)
+            for (int b = 0; b < 32 && lo + b < p.n_out; ++b) p.stage[lo + b] = ((orig >> b) & 1u) ? 0 : -1;
+    }
+    for (int o = 16; o; o >>= 1) pc += __shfl_xor_sync(0xFFFFFFFFu, pc, o);
+    if (lane == 0 && pc) atomicAdd(&s_tot, pc);
+    __syncthreads();
+    int32_t total = s_tot;
+    if (tid == 0 && p.pops && p.pop_cap > 0) p.pops[0] = total;
+    for (int k = 0;; ++k) {
+        const uint16_t *rows = (k & 1) ? lr1 : lr0;
+        uint16_t *lrn = (k & 1) ? lr0 : lr1;
+        const int32_t nrow = k == 0 ? nr : s_nr[k & 1];
+        for (int32_t i = tid; i < nrow; i += blockDim.x) {
+            const uint2 rc = rrec[k == 0 ? i : (int32_t)rows[i]];
+            const uint32_t h = rc.x & 0xFFFFu, e = rc.y & 0xFFFFu, b0 = rc.y >> 16;
+            bool ok = !sm_bit(cur, h) && (b0 == 0xFFFFu || sm_bit(cur, b0));
+            for (uint32_t j = (rc.x >> 16) + 1; j < e && ok; ++j) ok = sm_bit(cur, rbody[j]);
+            if (!ok) continue;
+            const uint32_t bit = 1u << (h & 31);
+            if (atomicOr(nxt + (h >> 5), bit) & bit) continue;   // (another row derived h in this pass)
+            if (p.stage && (int32_t)h < p.n_out) p.stage[h] = k + 1;
+            const uint32_t o0 = optr[h], o1 = optr[h + 1];
+            cg::coalesced_group g = cg::coalesced_threads();
+            int32_t base = 0;
+            if (g.thread_rank() == 0) base = atomicAdd(&s_na[k & 1], (int32_t)g.size());
+            la[g.shfl(base, 0) + (int32_t)g.thread_rank()] = (uint16_t)h;
+            if (o1 > o0) {
+                uint16_t *dst = lrn + atomicAdd(&s_nr[(k + 1) & 1], (int32_t)(o1 - o0));
+                for (uint32_t o = o0; o < o1; ++o) *dst++ = orow[o];
+            }
+        }
+        __syncthreads();
+        const int32_t sum = s_na[k & 1];   // the atoms derived in pass k (⊤ is never a head)
+        if (tid == 0 && p.stats)
+            atomicAdd(p.stats + 0, 8ull * (unsigned long long)nrow + 4ull * (unsigned long long)sum);
+        if (sum == 0 || k + 1 >= p.max_passes || k + 1 == p.user_cap) {
+            if (tid == 0) {
+                *p.iters_out = k + 1;
+                if (sum != 0) atomicOr(p.status_out, k + 1 == p.user_cap ? kStCapped : kStGuard);
+                if (p.status_user) *p.status_user = atomicOr(p.status_out, 0);
+                if (p.stats) {
+                    atomicAdd(p.stats + 0, 16ull * (unsigned long long)p.sm_blob16);   // (the blob, read once)
+                    p.stats[1] = (unsigned long long)(k + 1);
+                    p.stats[4] = (unsigned long long)(clock64() - clk0);
+                    p.stats[5] = globaltimer() - ns0;
+                }
+            }
+            // the model (v_{k+1}) over the original atoms
+            for (int64_t i = tid; i < p.out_wn; i += blockDim.x) {
+                const int64_t w = p.out_w0 + i;
+                unsigned long long x = (unsigned long long)nxt[2 * w] | ((unsigned long long)nxt[2 * w + 1] << 32);
+                const int64_t lo = w * 64;
+                if (lo + 64 > p.n_out) x &= (1ull << (uint32_t)(p.n_out - lo)) - 1ull;
+                p.model_out[i] = x;
+            }
+            return;
+        }
+        total += sum;
+        if (tid == 0 && p.pops && k + 1 < p.pop_cap) p.pops[k + 1] = total;
+        // v_{k+1} into v_k for the derived atoms; the counters of the pass after next
+        for (int32_t i = tid; i < sum; i += blockDim.x) {
+            const uint32_t h = la[i];
+            atomicOr(cur + (h >> 5), 1u << (h & 31));
+        }
+        if (tid == 0) {
+            s_na[(k + 1) & 1] = 0;
+            s_nr[k & 1] = 0;
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_lm_small(const LMParams &p, size_t smem, cudaStream_t st) {
+    lm_small_kernel<<<1, kSmallThreads, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_lm_cluster(const LMParams &p, int cluster, size_t smem, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     const int threads = p.cl_threads > 0 ? p.cl_threads : kThreads;
@@ -3632,6 +3770,9 @@ cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem) {
         return e;
     if ((e = cudaFuncSetAttribute((const void *)st_search_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)))
+        return e;
+    if ((e = cudaFuncSetAttribute((const void *)lm_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kMaxSmemBytes)))
         return e;
     if ((e = cudaFuncSetAttribute((const void *)st_compact_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kCpSmemBytes)))

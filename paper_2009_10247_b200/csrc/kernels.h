@@ -106,6 +106,11 @@ struct LMParams {
     unsigned long long *vent;  // [3] body entries the verification loaded per pass (k % 3)
     long long stream_entries;  // body entries (incl. padding) one STREAM pass reads
     int32_t auto_stream_first; // auto schedule starts with STREAM passes (long bodies)
+    // small-program kernel (lm_small_kernel): rows as a blob of uint16 -- row records (nr x 4:
+    // head, body begin, body end, first body atom or 0xFFFF) | body (nnz) | occ_ptr
+    // (n_ext + 1) | occ row (nnz), fact heads and always-true body atoms dropped
+    const uint4 *sm_blob;
+    int32_t sm_blob16, sm_nr, sm_nnz;
     int32_t stage_planes;      // cluster kernel: lead / head / col planes copied to shared memory
     int32_t cl_threads;        // cluster kernel: threads per CTA (0: kThreads)
     int32_t fr_cl_threads;     // one-cluster frontier launches: threads per CTA (0: kThreads)
@@ -269,6 +274,8 @@ int cluster_size_for(int which, int want, size_t smem);
 // Exact-mode programs small enough for one thread-block cluster (truth in shared memory,
 // DSMEM exchange, cluster barriers): the whole fixpoint in one cluster launch.
 cudaError_t launch_lm_cluster(const LMParams &p, int cluster, size_t smem, cudaStream_t st);
+// Programs whose rows fit shared memory in 16-bit ids: ONE CTA, semi-naive row lists.
+cudaError_t launch_lm_small(const LMParams &p, size_t smem, cudaStream_t st);
 int lm_cluster_max(int want, size_t smem);
 
 // One cooperative launch per stable call: clear the previous call's rows, build T_0, the

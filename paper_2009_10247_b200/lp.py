@@ -68,7 +68,7 @@ class lp_info_t(ctypes.Structure):
                 ("n_aux", ctypes.c_int32), ("cluster_ctas", ctypes.c_int32),
                 ("frontier_cluster_ctas", ctypes.c_int32), ("stable_cluster_ctas", ctypes.c_int32),
                 ("armed_list_cap", ctypes.c_int32), ("stable_compact_atoms", ctypes.c_int32),
-                ("stable_compact_rows", ctypes.c_int32)]
+                ("stable_compact_rows", ctypes.c_int32), ("small_rows", ctypes.c_int32)]
 
 
 SYMBOLS = ("lp_load", "lp_info", "lp_negated_atoms", "lp_least_model", "lp_stable_models",

@@ -178,17 +178,26 @@ def test_auto_schedule_switches_mid_fixpoint(seed, cfg, monkeypatch):
     check_lm(P, v0=v0, prog=q, schedules=("auto",))
 
 
+@pytest.mark.parametrize("small", [True, False])
 @pytest.mark.parametrize("seed", range(24))
-def test_cluster_kernel(seed, monkeypatch):
+def test_cluster_kernel(seed, small, monkeypatch):
     """Exact-mode programs on ONE thread-block cluster (lm_cluster_kernel): one or two CTAs,
     the planes staged in shared memory or read from L2, random start sets; and the same
-    program forced onto the persistent grid (LP_NO_CLUSTER) for comparison."""
+    program forced onto the persistent grid (LP_NO_CLUSTER) for comparison.  small: programs
+    whose rows fit shared memory in 16-bit ids run lm_small_kernel instead (one CTA,
+    semi-naive row lists); LP_NO_SMALL keeps them on the cluster kernel."""
+    if not small:
+        monkeypatch.setenv("LP_NO_SMALL", "1")
     rng = np.random.default_rng([seed, 777])
     n = int(rng.integers(50, 8000))
     R = int(rng.integers(n, 8 * n))
     P = lpgen.random_program(rng, n, R, max_len=int(rng.integers(1, 9)), n_facts=max(1, n // 40))
     prog = lp.Program(P)
     assert prog.info["cluster_ctas"] >= 1, prog.info
+    if not small:
+        assert prog.info["small_rows"] == 0
+    elif prog.info["nnz"] < 15000:   # (rows, body ids and their transpose well under 200 KB)
+        assert prog.info["small_rows"] > 0, prog.info
     check_lm(P, prog=prog, schedules=("auto",), variants=(False,))
     v0 = rng.choice(n, size=max(1, n // 20), replace=False).tolist()
     check_lm(P, v0=v0, prog=prog, schedules=("auto",), variants=(False,))
@@ -275,7 +284,14 @@ def test_device_pointer_mode_matches_host_mode():
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
 def test_config_parity(cfg):
     P = lpgen.config(cfg)
-    check_lm(P, jacobi=(cfg != "C3"))
+    prog = check_lm(P, jacobi=(cfg != "C3"))
+    assert (prog.info["small_rows"] > 0) == (cfg == "C1")
+
+
+def test_config_c1_cluster_kernel(monkeypatch):
+    monkeypatch.setenv("LP_NO_SMALL", "1")
+    prog = check_lm(lpgen.config("C1"), jacobi=True)
+    assert prog.info["small_rows"] == 0 and prog.info["cluster_ctas"] == 1
 
 
 # (full-size C4: tests/test_gpu_c4.py)
