@@ -518,7 +518,11 @@ def main():
             cfgs[cname] = {"iters": a_it, "full_ms": allmax(a_ms), "full_kernel_ms": allmax(a_k),
                            "frontier_ms": allmax(f_ms), "frontier_kernel_ms": allmax(f_k),
                            "us_per_pass_full": 1e3 * allmax(a_k) / a_it,
-                           "nnz": int(qp.info["nnz"])}
+                           "nnz": int(qp.info["nnz"]),
+                           "kernel": ("lm_small_kernel (one CTA, rows in shared memory, semi-naive row "
+                                      "lists; full and frontier calls)" if qp.info["small_rows"] > 0 else
+                                      "lm_cluster_kernel / one-cluster frontier" if qp.info["cluster_ctas"] > 0
+                                      else "lm_full_kernel / lm_frontier_kernel (persistent grid)")}
             qp.close()
         out["configs"] = cfgs
         # ---- stable models ---------------------------------------------------------------

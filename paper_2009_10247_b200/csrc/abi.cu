@@ -1211,8 +1211,10 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     // persistent grid kernel (A/B and tests)
     const bool use_cluster = !frontier && p->cluster > 0 &&
                              !(flags & (LP_FULL_STREAM | LP_FULL_LEAD | LP_FULL_NO_PIPE));
-    if (frontier) CK(launch_lm_frontier(q, p->fr_blocks, st, p->fr_cluster));
-    else if (use_cluster && p->small_ok) CK(launch_lm_small(q, p->small_smem, st));
+    // (a small program's frontier call runs the small-program kernel too: it IS semi-naive,
+    // by row lists instead of counters -- same model, iters, popcounts, stages)
+    if (frontier && !p->small_ok) CK(launch_lm_frontier(q, p->fr_blocks, st, p->fr_cluster));
+    else if (p->small_ok && (frontier || use_cluster)) CK(launch_lm_small(q, p->small_smem, st));
     else if (use_cluster) CK(launch_lm_cluster(q, p->cluster, p->cluster_smem, st));
     else CK(launch_lm_full(q, p->exact, p->lm_blocks, p->lm_smem, st));
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));
