@@ -898,3 +898,17 @@ def test_pinned_model_split_writes(seed, armed, monkeypatch):
             assert lp.lp_least_model(prog, v0, capped, max_passes=cap) == lp.lp_least_model(prog, v0, ref, max_passes=cap)
             assert (capped.numpy().view(np.uint64) == ref).all()
         prog.close()
+
+
+def test_compact_kernel_more_half_words_than_ctas(stable_kernel):
+    """2^14 guesses = 512 half-words of 32 columns: every CTA of the compact kernel runs
+    several of them one after another (and the batched kernel 256 words per row)."""
+    P = lpgen.gen_c5(seed=5, n=2000, R=8000, k=14, occ=6)
+    prog, o = check_stable(P)
+    assert o["f"] == 14
+    assert (prog.info["stable_compact_atoms"] > 0) == (stable_kernel == "compact")
+    k = o["k"]
+    rng = np.random.default_rng(99)
+    g = rng.integers(0, 2, size=(6000, k)).astype(np.uint8)   # 188 half-words, the last one ragged
+    check_stable(P, guesses_u8=g, prog=prog)
+    check_stable(P, guesses_u8=g[:33], prog=prog)             # one word, its second half 1 column

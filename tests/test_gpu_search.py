@@ -111,3 +111,11 @@ def test_device_pointer_mode(stable_kernel):
     g = gs.cpu().numpy().view(np.uint64)
     cols = np.stack([np.unpackbits(g[j].view(np.uint8), bitorder="little")[:128] for j in range(k)], 1)
     assert (cols == o["guesses"]).all()
+
+
+def test_more_columns_than_ctas(stable_kernel):
+    """6,000 columns per round = 188 half-words: the compact search kernel's CTAs each own
+    several half-words through every round."""
+    P = lpgen.gen_c5(seed=7, n=2000, R=8000, k=26, occ=6)
+    check_search(P, 6000, 11, 5)
+    check_search(P, 33, 11, 9)
