@@ -860,9 +860,11 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
             p->cluster_stage = want == 1 && cs + planes <= (size_t)kMaxSmemBytes;
             p->cluster_smem = cs + (p->cluster_stage ? planes : 0);
             p->cluster = lm_cluster_max(want, p->cluster_smem);
-            // one CTA: 512 threads (C1: 23.3 vs 25.5 us with 1024, 28.3 with 256 -- cheaper
-            // block barriers, still enough threads to stage the planes and stream)
-            if (p->cluster == 1 && p->cl_threads == 0) p->cl_threads = 512;
+            // one CTA, few rows: 512 threads (C1: 23.3 vs 25.5 us with 1024, 28.3 with 256 --
+            // cheaper block barriers, still enough threads to stage the planes and stream);
+            // a CTA with tens of thousands of rows keeps 1024 (paper Table 2 rows 2-4, 10-30 k
+            // rules: 0.083-0.145 ms with 512 threads vs 0.064-0.104 with 1024)
+            if (p->cluster == 1 && p->cl_threads == 0 && L.n_slots <= 4096) p->cl_threads = 512;
         }
     }
     if (p->cluster == 1 && !std::getenv("LP_NO_SMALL")) TRY(build_small(p));
