@@ -1250,21 +1250,11 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
 // lp_stable_models
 // ------------------------------------------------------------------------------------
 
-// The bit-sliced matrix T (two buffers of n_ext rows x Wp words) for G guess columns.
+// The shape of the bit-sliced matrix T (n_ext rows x Wp words) for G guess columns.
 static lp_status st_matrix(lp_program *p, int64_t G) {
     const int64_t W64 = (G + 63) / 64;
     if (W64 > (1 << 26)) return set_err(LP_E_INVALID, "too many guesses");
     const int32_t W = (int32_t)W64, Wp = (W + 1) / 2 * 2;
-    const size_t need = (size_t)p->L.n_ext * Wp;
-    if (need > p->T_words_alloc) {
-        if (p->d_T0) dev_release(p, p->d_T0);
-        if (p->d_T1) dev_release(p, p->d_T1);
-        p->d_T0 = p->d_T1 = nullptr;
-        TRY(dalloc(p, &p->d_T0, need));
-        TRY(dalloc(p, &p->d_T1, need));
-        p->T_words_alloc = need;
-        p->st_dirty_ok = false;
-    }
     p->W = W;
     p->Wp = Wp;
     p->G = G;
@@ -1272,9 +1262,30 @@ static lp_status st_matrix(lp_program *p, int64_t G) {
     return LP_OK;
 }
 
+// Its two buffers, allocated when something needs them: the batched kernels, or the
+// expansion of a compact call's result for a readback.  (The compact kernels themselves keep
+// the result as C[2W][|A*|]: C5 2.4 MB instead of 2 x 51 MB.)
+static lp_status st_alloc_T(lp_program *p) {
+    const size_t need = (size_t)p->L.n_ext * p->Wp;
+    if (need > p->T_words_alloc) {
+        if (p->d_T0) dev_release(p, p->d_T0);
+        if (p->d_T1) dev_release(p, p->d_T1);
+        p->d_T0 = p->d_T1 = nullptr;
+        p->T_words_alloc = 0;
+        TRY(dalloc(p, &p->d_T0, need));
+        TRY(dalloc(p, &p->d_T1, need));
+        p->T_words_alloc = need;
+        p->st_dirty_ok = false;
+    }
+    return LP_OK;
+}
+
 // Rows of T left by the previous call: cleared by the kernel's first phase when the
 // layout is unchanged (only the rows it changed), else both buffers zeroed here.
 static lp_status st_clear_plan(lp_program *p, cudaStream_t st, STParams *s) {
+    TRY(st_alloc_T(p));
+    s->T0 = p->d_T0;
+    s->T1 = p->d_T1;
     const bool full_clear = !(p->st_dirty_ok && p->st_last_Wp == p->Wp);
     p->st_last_compact = false;   // (a compact call leaves T alone; its expansion into T0 for
                                   //  a readback resets st_dirty_ok)
@@ -1364,6 +1375,7 @@ static lp_status st_compact_matrix(lp_program *p) {
 // zero it and scatter C into it once (T then no longer holds a batched call's dirty rows).
 static lp_status st_expand_compact(lp_program *p, cudaStream_t st) {
     if (!p->st_last_compact || p->cp_expanded) return LP_OK;
+    TRY(st_alloc_T(p));
     STParams s = st_params(p);
     st_compact_params(p, &s);
     s.facts = p->d_facts;   // (the all-ones rows are not in C)
