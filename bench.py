@@ -622,6 +622,33 @@ def main():
                              "frac": (sb_ach / l2_gbs) if l2_gbs else None,
                              "traffic": _ncu_traffic("C5_stable", spasses)}}
             bprog.close()
+        # ---- the same recipe with 16 negated atoms: 65,536 guesses = 2,048 half-words of 32
+        # columns, 14 per CTA of the compact kernel (its throughput past the single wave the
+        # k = 12 workload fills; sampled columns oracle-checked in tests/test_gpu_parity.py) --
+        if not dist:
+            S16 = lpgen.gen_c5(seed=1, n=100_000, R=500_000, k=16)
+            p16 = lp.Program(S16, device=local)
+            G16 = 1 << p16.info["n_free_negated"]
+            acc16 = torch.zeros((G16 + 63) // 64, dtype=torch.int64, device="cuda")
+            t16 = []
+            for i in range(args.warmup + args.steps):
+                flush_l2()
+                k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                lp.lp_stable_models(p16, None, G16, acc16, stream=stream, device_ptrs=True,
+                                    n_accepted_out=nacc, passes_out=passes, ev_begin=k0, ev_end=k1,
+                                    status_out=status_d)
+                stream.synchronize()
+                assert int(status_d.item()) == 0
+                if i >= args.warmup:
+                    t16.append(k0.elapsed_time(k1))
+            out["stable_k16"] = {"workload": "C5 recipe, k = 16 (lpgen.gen_c5(seed=1, k=16))", "guesses": G16,
+                                 "kernel_ms": float(np.mean(t16)),
+                                 "guesses_per_s": G16 / (float(np.mean(t16)) / 1e3),
+                                 "passes": int(passes.item()), "accepted": int(nacc.item()),
+                                 "compact_atoms": p16.info["stable_compact_atoms"],
+                                 "kernel": "st_compact_kernel" if p16.info["stable_compact_atoms"] > 0
+                                           else "st_fixpoint_kernel"}
+            p16.close()
         # ---- guess-space reduction (lp_stable_search, reading R23): C5's
         # recipe with k = 32 negated atoms -- 2^32 guesses, enumeration refused (LP_E_CAP);
         # 128 sampled columns per round + local search, all rounds in one launch ----------

@@ -912,3 +912,26 @@ def test_compact_kernel_more_half_words_than_ctas(stable_kernel):
     g = rng.integers(0, 2, size=(6000, k)).astype(np.uint8)   # 188 half-words, the last one ragged
     check_stable(P, guesses_u8=g, prog=prog)
     check_stable(P, guesses_u8=g[:33], prog=prog)             # one word, its second half 1 column
+
+
+def test_c5_recipe_k16_sampled_columns(monkeypatch):
+    """C5's recipe with 16 negated atoms: 65,536 guesses = 2,048 half-words, 14 per CTA of
+    the compact kernel.  The oracle solves sampled columns one by one (model and accepted
+    bit); accepted ids and pass count must also equal the batched kernel's."""
+    P = lpgen.gen_c5(seed=1, n=100_000, R=500_000, k=16)
+    prog = lp.Program(P)
+    assert prog.info["stable_compact_atoms"] > 0 and prog.info["n_free_negated"] == 16
+    ids, passes, _ = prog.stable_models()
+    k = prog.info["n_negated"]
+    rng = np.random.default_rng(16)
+    sample = sorted(set(rng.integers(0, 1 << 16, size=40).tolist()) | {0, 65535} | set(ids.tolist()[:4]))
+    g = np.array([[(c >> j) & 1 for j in range(k)] for c in sample], dtype=np.uint8)
+    o = oracle.stable(P, guesses=g, want_models=True)
+    for i, c in enumerate(sample):
+        assert (prog.guess_model(int(c)) == o["models"][i]).all(), c
+        assert bool(o["accepted"][i]) == (c in set(ids.tolist())), c
+    assert passes >= int(o["passes"])
+    monkeypatch.setenv("LP_NO_COMPACT_STABLE", "1")
+    bprog = lp.Program(P)
+    bids, bpasses, _ = bprog.stable_models()
+    assert bids.tolist() == ids.tolist() and bpasses == passes
