@@ -130,6 +130,7 @@ struct lp_program {
     bool cp_ok = false;
     int32_t cp_na = 0, cp_nr = 0, cp_nnz = 0, cp_n0 = 0, cp_blob16 = 0;
     size_t cp_smem = 0;
+    int cp_occ = 1, cp_occ_search = 1;   // co-resident CTAs per SM of the compact kernels
     uint4 *d_cp_blob = nullptr;
     int32_t *d_cp_atom = nullptr, *d_cp_neg = nullptr, *d_cp_abar = nullptr;
     int32_t *d_cp_pw = nullptr, *d_cp_rp = nullptr;
@@ -812,6 +813,10 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
 
     load_mark("stable buffers");
     CK(prepare_kernels(p->lm_smem, p->st_smem));
+    if (p->cp_ok) {   // (small live parts: two CTAs per SM, each on its own half-words)
+        p->cp_occ = std::max(1, st_compact_blocks_per_sm(0, p->cp_smem));
+        p->cp_occ_search = std::max(1, st_compact_blocks_per_sm(1, p->cp_smem));
+    }
     const int bl = lm_full_blocks_per_sm(p->exact, p->lm_smem);
     const int bf = lm_frontier_blocks_per_sm();
     const int bs = st_blocks_per_sm(p->st_smem);
@@ -1472,7 +1477,7 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
         p->st_last_compact = true;
         p->cp_expanded = false;
         if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
-        CK(launch_st_compact(s, std::max(1, std::min(2 * W, p->sms)), p->cp_smem, st));
+        CK(launch_st_compact(s, std::max(1, std::min(2 * W, p->sms * p->cp_occ)), p->cp_smem, st));
     } else {
     TRY(st_clear_plan(p, st, &s));
     // ONE cooperative launch: clear, T_0, the fixpoint loop, the stability check
@@ -1558,7 +1563,7 @@ extern "C" lp_status lp_stable_search(lp_program *p, int64_t h, uint64_t seed, i
         st_compact_params(p, &s);
         p->st_last_compact = true;
         p->cp_expanded = false;
-        CK(launch_st_search_compact(s, std::max(1, std::min(2 * W, p->sms)), p->cp_smem, st));
+        CK(launch_st_search_compact(s, std::max(1, std::min(2 * W, p->sms * p->cp_occ_search)), p->cp_smem, st));
     } else {
         CK(launch_st_search(s, p->st_blocks, p->st_smem, st, p->st_cluster));
     }

@@ -3667,6 +3667,14 @@ __global__ void __launch_bounds__(kThreads, 1) st_search_compact_kernel(const __
     }
 }
 
+// co-resident CTAs per SM of the compact kernels with `smem` bytes (which: 0 stable, 1 search)
+int st_compact_blocks_per_sm(int which, size_t smem) {
+    int a = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &a, which ? (const void *)st_search_compact_kernel : (const void *)st_compact_kernel, kThreads, smem);
+    return a;
+}
+
 cudaError_t launch_st_search_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
     STParams q = p;
     void *args[] = {(void *)&q};

@@ -298,6 +298,7 @@ cudaError_t launch_st_column(const STParams &p, int32_t n, int64_t g, unsigned l
 int lm_full_blocks_per_sm(bool exact, size_t smem);
 int lm_frontier_blocks_per_sm();
 int st_blocks_per_sm(size_t smem);
+int st_compact_blocks_per_sm(int which, size_t smem);
 cudaError_t prepare_kernels(size_t lm_smem, size_t st_smem);
 
 }  // namespace lpb
