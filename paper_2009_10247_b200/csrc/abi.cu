@@ -131,6 +131,7 @@ struct lp_program {
     int32_t cp_na = 0, cp_nr = 0, cp_nnz = 0, cp_n0 = 0, cp_blob16 = 0;
     size_t cp_smem = 0;
     int cp_occ = 1, cp_occ_search = 1;   // co-resident CTAs per SM of the compact kernels
+    int cp_threads = 0;                  // LP_CP_THREADS: threads per CTA of st_compact_kernel (0: kThreads)
     uint4 *d_cp_blob = nullptr;
     int32_t *d_cp_atom = nullptr, *d_cp_neg = nullptr, *d_cp_abar = nullptr;
     int32_t *d_cp_pw = nullptr, *d_cp_rp = nullptr;
@@ -813,6 +814,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
 
     load_mark("stable buffers");
     CK(prepare_kernels(p->lm_smem, p->st_smem));
+    if (const char *e = std::getenv("LP_CP_THREADS")) p->cp_threads = std::max(64, std::min(kThreads, std::atoi(e) / 32 * 32));
     if (p->cp_ok) {   // (small live parts: two CTAs per SM, each on its own half-words)
         p->cp_occ = std::max(1, st_compact_blocks_per_sm(0, p->cp_smem));
         p->cp_occ_search = std::max(1, st_compact_blocks_per_sm(1, p->cp_smem));
@@ -1477,7 +1479,7 @@ extern "C" lp_status lp_stable_models(lp_program *p, const uint64_t *guesses, in
         p->st_last_compact = true;
         p->cp_expanded = false;
         if (run && run->ev_begin) CK(cudaEventRecord((cudaEvent_t)run->ev_begin, st));
-        CK(launch_st_compact(s, std::max(1, std::min(2 * W, p->sms * p->cp_occ)), p->cp_smem, st));
+        CK(launch_st_compact(s, std::max(1, std::min(2 * W, p->sms * p->cp_occ)), p->cp_smem, st, p->cp_threads));
     } else {
     TRY(st_clear_plan(p, st, &s));
     // ONE cooperative launch: clear, T_0, the fixpoint loop, the stability check

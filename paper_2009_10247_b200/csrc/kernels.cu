@@ -3390,8 +3390,8 @@ __global__ void __launch_bounds__(kThreads, 1) st_compact_kernel(const __grid_co
     }
 }
 
-cudaError_t launch_st_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st) {
-    st_compact_kernel<<<blocks, kThreads, smem, st>>>(p);
+cudaError_t launch_st_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st, int threads) {
+    st_compact_kernel<<<blocks, threads > 0 ? threads : kThreads, smem, st>>>(p);
     return cudaGetLastError();
 }
 

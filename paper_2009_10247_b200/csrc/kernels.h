@@ -283,7 +283,7 @@ int lm_cluster_max(int want, size_t smem);
 cudaError_t launch_st_fused(const STParams &p, int blocks, size_t smem, cudaStream_t st, int cluster);
 // The same call on the live sub-program held in shared memory, a CTA per guess word (no
 // grid barrier: an ordinary launch).
-cudaError_t launch_st_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st);
+cudaError_t launch_st_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st, int threads = 0);
 // ... the guess-space search on it (cooperative: one grid barrier per round; gbuf holds two
 // column buffers [2][k][W])
 cudaError_t launch_st_search_compact(const STParams &p, int blocks, size_t smem, cudaStream_t st);
