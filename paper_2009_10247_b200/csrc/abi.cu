@@ -340,7 +340,7 @@ static lp_status build_compact_stable(lp_program *p) {
     }
     const size_t n0 = row0.size();
     const size_t blob_bytes = (2 * (4 * nr + nz + (na + 1) + nz + na + n0) + 15) / 16 * 16;
-    const size_t smem = blob_bytes + 8 * na + 2 * (na + (na & 1)) + 4 * (nz + (nz & 1)) + 4 * ((na + 31) / 32);
+    const size_t smem = blob_bytes + 8 * na + 2 * (na + (na & 1)) + 4 * (nz + (nz & 1));
     if (smem > (size_t)kCpSmemBytes) return LP_OK;
     std::vector<uint4> blob(blob_bytes / 16, make_uint4(0, 0, 0, 0));
     {

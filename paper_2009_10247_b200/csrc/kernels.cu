@@ -3177,7 +3177,6 @@ struct CpView {
     uint32_t *cur, *nxt;
     uint16_t *la;            // [na] rows of T changed in this pass
     uint16_t *lr0, *lr1;     // [nnz] x 2: the AND-rows to evaluate in this pass / in the next one
-    uint32_t *inl;           // bit a: a is on la
     int32_t *s_na, *s_nr;    // [2] each: list counters by pass parity
 };
 
@@ -3198,7 +3197,6 @@ __device__ __forceinline__ CpView cp_view(const STParams &p, unsigned long long 
     v.la = reinterpret_cast<uint16_t *>(v.nxt + v.na);
     v.lr0 = v.la + v.na + (v.na & 1);
     v.lr1 = v.lr0 + v.nnz + (v.nnz & 1);
-    v.inl = reinterpret_cast<uint32_t *>(v.lr1 + v.nnz + (v.nnz & 1));
     v.s_na = s_cnt;
     v.s_nr = s_cnt + 2;
     return v;
@@ -3209,7 +3207,6 @@ __device__ __forceinline__ void cp_stage(const STParams &p, const CpView &v) {
     const int tid = threadIdx.x;
     for (int32_t i = tid; i < p.cp_blob16; i += blockDim.x) v.blob[i] = __ldg(p.cp_blob + i);
     if (tid == 0) v.s_na[0] = v.s_na[1] = v.s_nr[0] = v.s_nr[1] = 0;
-    for (int32_t i = tid; i < ((v.na + 31) >> 5); i += blockDim.x) v.inl[i] = 0u;
     __syncthreads();
 }
 
@@ -3252,13 +3249,14 @@ __device__ __forceinline__ int32_t cp_word(const STParams &p, const CpView &v, i
     auto eval_row = [&](int32_t r, int k) {
         const uint2 rc = v.rrec[r];
         const uint32_t h = rc.x & 0xFFFFu, e = rc.y & 0xFFFFu, b0 = rc.y >> 16;
-        uint32_t acc = valid & ~cur[h];
+        const uint32_t ch = cur[h];
+        uint32_t acc = valid & ~ch;
         if (b0 != kCpNone) acc &= cur[b0];
         for (uint32_t i = (rc.x >> 16) + 1; i < e && acc; ++i) acc &= cur[v.rbody[i]];
         if (!acc) return;
-        atomicOr(nxt + h, acc);
-        const uint32_t bit = 1u << (h & 31);
-        if (atomicOr(v.inl + (h >> 5), bit) & bit) return;
+        // (T_{k+1}[h] = T_k[h] until the pass's first OR, which adds bits T_k[h] lacks: the old
+        // value names the first row to change h in this pass)
+        if (atomicOr(nxt + h, acc) != ch) return;
         const uint32_t o0 = v.optr[h], o1 = v.optr[h + 1];
         cg::coalesced_group g = cg::coalesced_threads();
         int32_t base = 0;
@@ -3290,7 +3288,6 @@ __device__ __forceinline__ int32_t cp_word(const STParams &p, const CpView &v, i
         for (int32_t i = tid; i < nn; i += blockDim.x) {
             const uint32_t h = v.la[i];
             cur[h] = nxt[h];
-            v.inl[h >> 5] = 0u;   // (same-value stores race benignly)
         }
         if (tid == 0) {
             v.s_na[(k + 1) & 1] = 0;
