@@ -2443,9 +2443,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) lm_small_kernel(const __grid
             cg::coalesced_group g = cg::coalesced_threads();
             int32_t base = 0;
             if (g.thread_rank() == 0) base = atomicAdd(&s_na[k & 1], (int32_t)g.size());
-            la[g.shfl(base, 0) + (int32_t)g.thread_rank()] = (uint16_t)h;
+            base = g.shfl(base, 0) + (int32_t)g.thread_rank();
+            LP_CHECK(h < (uint32_t)ne && base < ne && o1 <= (uint32_t)nnz);
+            la[base] = (uint16_t)h;
             if (o1 > o0) {
-                uint16_t *dst = lrn + atomicAdd(&s_nr[(k + 1) & 1], (int32_t)(o1 - o0));
+                const int32_t rpos = atomicAdd(&s_nr[(k + 1) & 1], (int32_t)(o1 - o0));
+                LP_CHECK(rpos + (int32_t)(o1 - o0) <= nnz);
+                uint16_t *dst = lrn + rpos;
                 for (uint32_t o = o0; o < o1; ++o) *dst++ = orow[o];
             }
         }
@@ -3261,9 +3265,13 @@ __device__ __forceinline__ int32_t cp_word(const STParams &p, const CpView &v, i
         cg::coalesced_group g = cg::coalesced_threads();
         int32_t base = 0;
         if (g.thread_rank() == 0) base = atomicAdd(&v.s_na[k & 1], (int32_t)g.size());
-        v.la[g.shfl(base, 0) + (int32_t)g.thread_rank()] = (uint16_t)h;
+        base = g.shfl(base, 0) + (int32_t)g.thread_rank();
+        LP_CHECK(h < (uint32_t)v.na && base < v.na && o1 <= (uint32_t)v.nnz);
+        v.la[base] = (uint16_t)h;
         if (o1 > o0) {
-            uint16_t *dst = ((k & 1) ? v.lr0 : v.lr1) + atomicAdd(&v.s_nr[(k + 1) & 1], (int32_t)(o1 - o0));
+            const int32_t rpos = atomicAdd(&v.s_nr[(k + 1) & 1], (int32_t)(o1 - o0));
+            LP_CHECK(rpos + (int32_t)(o1 - o0) <= v.nnz);
+            uint16_t *dst = ((k & 1) ? v.lr0 : v.lr1) + rpos;
             for (uint32_t o = o0; o < o1; ++o) *dst++ = v.orow[o];
         }
     };
