@@ -151,6 +151,7 @@ struct lp_program {
     uint4 *d_sm_blob = nullptr;
     int32_t sm_blob16 = 0, sm_nr = 0, sm_nnz = 0;
     size_t small_smem = 0;
+    int small_threads = 0;   // LP_SMALL_THREADS: threads of lm_small_kernel's CTA (0: 512)
     int sms = 0, threads = kThreads;
     int lm_blocks = 0, fr_blocks = 0, st_blocks = 0, grid_cap = 0;
     int fr_cluster = 0, st_cluster = 0;   // > 0: one-cluster launch of the frontier / stable kernels
@@ -875,6 +876,7 @@ static lp_status load_device(lp_program *p, const lp_options *opt) {
         }
     }
     if (p->cluster == 1 && !std::getenv("LP_NO_SMALL")) TRY(build_small(p));
+    if (const char *e = std::getenv("LP_SMALL_THREADS")) p->small_threads = std::max(64, std::min(1024, std::atoi(e) / 32 * 32));
     p->st_blocks = cap_grid(sms * bs);
     load_mark("queues, occupancy");
     // one-cluster launches: the frontier and stable kernels of
@@ -1223,7 +1225,7 @@ extern "C" lp_status lp_least_model(lp_program *p, const uint64_t *v0, uint64_t 
     // (a small program's frontier call runs the small-program kernel too: it IS semi-naive,
     // by row lists instead of counters -- same model, iters, popcounts, stages)
     if (frontier && !p->small_ok) CK(launch_lm_frontier(q, p->fr_blocks, st, p->fr_cluster));
-    else if (p->small_ok && (frontier || use_cluster)) CK(launch_lm_small(q, p->small_smem, st));
+    else if (p->small_ok && (frontier || use_cluster)) CK(launch_lm_small(q, p->small_smem, st, p->small_threads));
     else if (use_cluster) CK(launch_lm_cluster(q, p->cluster, p->cluster_smem, st));
     else CK(launch_lm_full(q, p->exact, p->lm_blocks, p->lm_smem, st));
     if (run && run->ev_end) CK(cudaEventRecord((cudaEvent_t)run->ev_end, st));

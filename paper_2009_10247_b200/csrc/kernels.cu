@@ -2371,8 +2371,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_cluster_kernel(const __grid_co
 // which lists the head and the rows it occurs in for the next pass); after a block barrier
 // the listed heads are ORed into v_k.  Two block barriers per pass, no global traffic in
 // the loop apart from the stage stores.
-constexpr int kSmallThreads = 512;
-__global__ void __launch_bounds__(kSmallThreads, 1) lm_small_kernel(const __grid_constant__ LMParams p) {
+constexpr int kSmallThreads = 768;   // (C1, L2 flushed: 768 0.0171 ms, 1024 0.0190, 512 0.0192, 256 0.0212; LP_SMALL_THREADS)
+__global__ void __launch_bounds__(1024, 1) lm_small_kernel(const __grid_constant__ LMParams p) {
     extern __shared__ __align__(16) unsigned long long smb[];
     const int tid = threadIdx.x, lane = tid & 31;
     const int32_t nr = p.sm_nr, nnz = p.sm_nnz, ne = p.n_ext_atoms, nw = p.nwords;
@@ -2494,8 +2494,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) lm_small_kernel(const __grid
     }
 }
 
-cudaError_t launch_lm_small(const LMParams &p, size_t smem, cudaStream_t st) {
-    lm_small_kernel<<<1, kSmallThreads, smem, st>>>(p);
+cudaError_t launch_lm_small(const LMParams &p, size_t smem, cudaStream_t st, int threads) {
+    lm_small_kernel<<<1, threads > 0 ? threads : kSmallThreads, smem, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -275,7 +275,7 @@ int cluster_size_for(int which, int want, size_t smem);
 // DSMEM exchange, cluster barriers): the whole fixpoint in one cluster launch.
 cudaError_t launch_lm_cluster(const LMParams &p, int cluster, size_t smem, cudaStream_t st);
 // Programs whose rows fit shared memory in 16-bit ids: ONE CTA, semi-naive row lists.
-cudaError_t launch_lm_small(const LMParams &p, size_t smem, cudaStream_t st);
+cudaError_t launch_lm_small(const LMParams &p, size_t smem, cudaStream_t st, int threads = 0);
 int lm_cluster_max(int want, size_t smem);
 
 // One cooperative launch per stable call: clear the previous call's rows, build T_0, the
